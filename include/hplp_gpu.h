@@ -1,0 +1,74 @@
+/*
+ * hplp_gpu -- the solve()-level C ABI of the B200 rHPDHG solver.
+ *
+ * This is the drop-in boundary for the reference's public API
+ * (/root/reference/proj/include/hplp): problem load (CSR with bounds, or a
+ * standard-form CSR), SolverConfig, solve(), SolveStatus + KktError report.
+ * The C++ mirror of the reference types lives in
+ * paper_2407_16144_b200/csrc/hplp_gpu.hpp; INTEGRATION.md shows the ctypes
+ * and C++ bindings a maintainer adds on the reference side.
+ *
+ * All pointers are host pointers, copied on entry.  Return value: HPLP_OK or
+ * an HPLP_E* code with hplp_last_error() describing it; HPLP_EINVAL is the
+ * reference's std::invalid_argument, HPLP_EDOMAIN its std::domain_error.
+ */
+#ifndef HPLP_GPU_H_
+#define HPLP_GPU_H_
+
+#include <stdint.h>
+
+#include "hplp_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+const char* hplp_last_error(void);
+
+/* to_string(SolveStatus), src/solver.cpp:176-192. */
+const char* hplp_status_string(int32_t status);
+
+/* validate_config, src/solver.cpp:40-65 (HPLP_EINVAL + message). */
+int hplp_validate_config(const hplp_config_t* cfg);
+
+/* SolveResult solve(const StandardFormLP&, const SolverConfig&)
+ * (inc/solver.hpp:130, src/solver.cpp:206-342) on a standard-form LP
+ * min c'x s.t. Ax = b, x >= 0 given as CSR (StandardFormLP, inc/lp_model.hpp:27-37).
+ * Rows may list columns in any order; duplicates are an error
+ * (src/sparse_matrix.cpp:45-52). */
+int hplp_solve_csr(int32_t device, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                   const double* val, const double* b, const double* c, const hplp_config_t* cfg,
+                   hplp_io_t* io, hplp_result_t* result);
+
+/* A device-resident problem for repeated solves (upload once). */
+int hplp_solver_create(int32_t device, int64_t m, int64_t n, const int64_t* row_ptr,
+                       const int32_t* col_idx, const double* val, const double* b, const double* c,
+                       void** solver);
+int hplp_solver_solve(void* solver, const hplp_config_t* cfg, hplp_io_t* io, hplp_result_t* result);
+/* The underlying hx context (include/hx.h) for benchmarks and tests. */
+void* hplp_solver_hx(void* solver);
+void hplp_solver_free(void* solver);
+
+/* to_standard_form (inc/lp_model.hpp:126, src/lp_model.cpp:155-325): general
+ * form -> standard form with the reference's row/column ordering, plus the
+ * VariableMap for recovery. */
+int hplp_to_standard_form(const hplp_general_t* g, void** std_form, int64_t* m, int64_t* n, int64_t* nnz);
+int hplp_std_export(void* std_form, int64_t* row_ptr, int32_t* col_idx, double* val, double* b, double* c);
+/* VariableMap::recover_primal (src/lp_model.cpp:65-85) and recover_objective
+ * (inc/lp_model.hpp:116-118).  Either output may be NULL. */
+int hplp_std_recover(void* std_form, const double* x_std, double* x_orig, double std_objective,
+                     double* objective);
+void hplp_std_free(void* std_form);
+
+/* "Problem load in CSR with bounds" + solve + recovery in one call: the
+ * north-star entry point.  io holds standard-form buffers (may be NULL);
+ * x_orig (n of the general form) and objective (original sense, with the
+ * objective constant) may be NULL. */
+int hplp_solve_general(int32_t device, const hplp_general_t* g, const hplp_config_t* cfg, hplp_io_t* io,
+                       hplp_result_t* result, double* x_orig, double* objective);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HPLP_GPU_H_ */

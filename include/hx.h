@@ -1,0 +1,124 @@
+/*
+ * hx -- the thin C-ABI CUDA layer under the B200 rHPDHG host driver.
+ *
+ * One hx_ctx owns one device, its stream, the problem (A as CSR, an explicit
+ * A^T built on the device, b, c), all iterate buffers and the device-side
+ * controller state.  Plain pointers and sizes only; host pointers are copied.
+ * Every entry point returns an HPLP_* code (include/hplp_types.h) and leaves
+ * a message for hx_last_error().  One context per host thread; independent
+ * contexts may be used concurrently.
+ *
+ * The reference has no FFI: each entry point below replaces a reference C++
+ * function, cited in brackets.  include/hplp_gpu.h is the solve()-level
+ * boundary built on top of this layer.
+ */
+#ifndef HX_H_
+#define HX_H_
+
+#include <stdint.h>
+
+#include "hplp_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hx_ctx hx_ctx;
+
+/* Progress snapshot returned by hx_run (the loop state of
+ * src/solver.cpp:218-227 plus the last iteration's KKT/residual). */
+typedef struct hx_progress {
+  int64_t it;          /* iterations completed (reference `it`) */
+  int64_t n;           /* epoch index (reference `n`) */
+  int64_t k;           /* inner index (reference `k`) */
+  int64_t spmv_count;  /* device-side SpMVs since hx_setup (excl. setup) */
+  int32_t status;      /* -1 running, else HPLP_STATUS_* */
+  int32_t error;       /* HPLP_OK or HPLP_EDOMAIN / HPLP_ETIMEOUT */
+  int32_t paused;      /* 1: stopped at a trace point (trace_* valid) */
+  int32_t best_valid;  /* best_kkt finite */
+  double res_epoch_start;
+  double best_kkt;
+  hplp_kkt_t best_err;
+  /* last completed iteration (trace record fields) */
+  int64_t trace_it, trace_n, trace_k;
+  double trace_res;
+  hplp_kkt_t trace_kkt;
+  hplp_kkt_t final_kkt; /* KKT of the returned iterate for terminal status */
+  int64_t n_epochs;     /* epochs started since hx_setup */
+  hplp_cert_meta_t primal_cert, dual_cert;
+  double device_ms;     /* CUDA-event time of the hx_run call */
+  int64_t launches;     /* kernels launched by this call */
+} hx_progress_t;
+
+int hx_create(int32_t device, hx_ctx** out);
+void hx_destroy(hx_ctx* ctx);
+const char* hx_last_error(hx_ctx* ctx); /* ctx may be NULL (creation errors) */
+int hx_device_info(hx_ctx* ctx, int32_t* sm_count, int32_t* grid_ctas, int32_t* cta_threads);
+/* cudaStream_t the context launches on (for event timing by the caller). */
+void* hx_stream(hx_ctx* ctx);
+int64_t hx_launch_count(hx_ctx* ctx);
+
+/* [SparseMatrix(rows, cols, triplets), src/sparse_matrix.cpp:24-66;
+ *  StandardFormLP ctor, src/lp_model.cpp:35-43]
+ * Copies CSR A (validated: indices in range, finite values, ascending unique
+ * columns per row), b and c to the device, builds the explicit A^T with
+ * ascending row order per column (inc/sparse_matrix.hpp:61-62), and the
+ * nnz-balanced warp schedules of both matrices. */
+int hx_upload_csr(hx_ctx* ctx, int64_t m, int64_t n, const int64_t* row_ptr,
+                  const int32_t* col_idx, const double* val, const double* b, const double* c);
+/* Same with device-resident inputs (no host copies; used by re-uploads). */
+int hx_dims(hx_ctx* ctx, int64_t* m, int64_t* n, int64_t* nnz);
+
+/* [spmv, src/sparse_matrix.cpp:101-117]  out = A x, host vectors. */
+int hx_spmv(hx_ctx* ctx, const double* x, double* out);
+/* [spmv_transpose, src/sparse_matrix.cpp:119-136]  out = A^T y. */
+int hx_spmv_transpose(hx_ctx* ctx, const double* y, double* out);
+
+/* [power_iteration loop body, src/sparse_matrix.cpp:153-177]
+ * Runs from the unit start vector x0 (host, length n; drawn by the caller's
+ * std::mt19937_64 for parity) starting at iteration k0 with sigma_prev.
+ * Stops on convergence, max_iters, or sigma == 0 (*need_redraw = 1: the
+ * caller re-draws x from its generator and calls again with k0 = *iters). */
+int hx_power_iteration(hx_ctx* ctx, const double* x0, double tol, int64_t k0, int64_t max_iters,
+                       double sigma_prev, double* sigma, int64_t* iters, int32_t* converged,
+                       int32_t* need_redraw);
+
+/* [make_setup + initial_point + loop prologue, src/solver.cpp:67-87,208-216]
+ * Binds the config (validated by the caller), sigma_used and eta, loads the
+ * initial iterate (NULL = zeros), computes a_x = A x and sets the anchor.
+ * Resets it/n/k, best tracking and the epoch log. */
+int hx_setup(hx_ctx* ctx, const hplp_config_t* cfg, double sigma_used, double eta,
+             const double* x0, const double* y0);
+
+/* [the while(true) loop, src/solver.cpp:241-341]
+ * Runs up to max_iters iterations on the device with the reference's exact
+ * per-iteration semantics (termination, certificate scans, restarts, Halpern
+ * combine, best tracking).  trace_period > 0 pauses after every traced
+ * iteration.  One persistent cooperative kernel per call. */
+int hx_run(hx_ctx* ctx, int64_t max_iters, hx_progress_t* progress);
+int hx_progress(hx_ctx* ctx, hx_progress_t* progress);
+
+/* Epoch log (EpochStats, inc/solver.hpp:82-87) entries [first, first+count). */
+int hx_epochs(hx_ctx* ctx, int64_t first, int64_t count, hplp_epoch_t* out);
+
+/* Iterates: which = 0 current z (as of the last completed iteration when
+ * paused/terminated, else the next iterate), 1 best, 2 T(z) of the last
+ * completed iteration. */
+enum { HX_ITERATE_CURRENT = 0, HX_ITERATE_BEST = 1, HX_ITERATE_NEXT = 2, HX_ITERATE_LAST = 3 };
+int hx_get_iterate(hx_ctx* ctx, int32_t which, double* x, double* y);
+
+/* [make_certificate, src/solver.cpp:89-101] kind 0 primal (m), 1 dual (n). */
+int hx_get_certificate(hx_ctx* ctx, int32_t kind, double* vec);
+
+/* [kkt_error, src/pdhg_core.cpp:70-73] at the current iterate with fresh
+ * products (the limit path of src/solver.cpp:242-254 when no best exists). */
+int hx_kkt_current(hx_ctx* ctx, hplp_kkt_t* out);
+
+/* sizeof checks for the ABI tests. */
+int64_t hx_sizeof(int32_t which);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HX_H_ */

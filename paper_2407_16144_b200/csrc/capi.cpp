@@ -1,0 +1,223 @@
+// C ABI (include/hplp_gpu.h) over the C++ host driver (hplp_gpu.hpp).
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+
+#include "hplp_gpu.h"
+#include "hplp_gpu.hpp"
+#include "hx.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return HPLP_OK;
+  } catch (const std::domain_error& e) {
+    g_err = e.what();
+    return HPLP_EDOMAIN;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return HPLP_EINVAL;
+  } catch (const std::bad_alloc& e) {
+    g_err = e.what();
+    return HPLP_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HPLP_ECUDA;
+  }
+}
+
+void put_kkt(const hplp_gpu::KktError& e, hplp_kkt_t* o) {
+  *o = {e.primal_residual, e.dual_residual, e.gap_residual, e.max_relative};
+}
+
+void put_cert(const std::optional<hplp_gpu::Certificate>& c, hplp_cert_meta_t* m, double* vec) {
+  std::memset(m, 0, sizeof(*m));
+  if (!c) return;
+  m->present = 1;
+  m->source = c->source == hplp_gpu::CandidateSource::kNormalizedIterate ? HPLP_SOURCE_NORMALIZED_ITERATE
+                                                                          : HPLP_SOURCE_ITERATE_DIFFERENCE;
+  m->orientation = c->orientation == hplp_gpu::Orientation::kNegated ? HPLP_ORIENT_NEGATED : HPLP_ORIENT_AS_IS;
+  m->at_iteration = c->at_iteration;
+  m->residual = c->residual;
+  m->margin = c->margin;
+  if (vec) std::memcpy(vec, c->vector.data(), c->vector.size() * sizeof(double));
+}
+
+void fill_result(const hplp_gpu::SolveResult& r, hplp_io_t* io, hplp_result_t* res) {
+  std::memset(res, 0, sizeof(*res));
+  res->status = static_cast<int32_t>(r.status);
+  res->iterations = r.totals.iterations;
+  res->spmv_count = r.totals.spmv_count;
+  res->wall_seconds = r.totals.wall_seconds;
+  res->eta = r.totals.eta;
+  res->sigma_estimate = r.totals.sigma_estimate;
+  put_kkt(r.final_kkt, &res->final_kkt);
+  res->n_epochs = static_cast<int64_t>(r.epochs.size());
+  put_cert(r.primal_certificate, &res->primal_cert, io ? io->primal_cert : nullptr);
+  put_cert(r.dual_certificate, &res->dual_cert, io ? io->dual_cert : nullptr);
+  if (!io) return;
+  if (io->x) std::memcpy(io->x, r.final_iterate.x.data(), r.final_iterate.x.size() * sizeof(double));
+  if (io->y) std::memcpy(io->y, r.final_iterate.y.data(), r.final_iterate.y.size() * sizeof(double));
+  if (io->epochs)
+    for (std::size_t e = 0; e < r.epochs.size() && static_cast<int64_t>(e) < io->epochs_capacity; ++e) {
+      io->epochs[e].epoch = r.epochs[e].epoch;
+      io->epochs[e].restart_length = r.epochs[e].restart_length;
+      io->epochs[e].residual_at_start = r.epochs[e].residual_at_start;
+      put_kkt(r.epochs[e].kkt_at_start, &io->epochs[e].kkt_at_start);
+    }
+}
+
+hplp_gpu::SolverConfig config_with_io(const hplp_config_t* cfg, hplp_io_t* io, int64_t m, int64_t n) {
+  hplp_gpu::SolverConfig c = hplp_gpu::from_pod(*cfg);
+  if (io && io->init_x && io->init_y)
+    c.initial_iterate = hplp_gpu::Iterate{std::vector<double>(io->init_x, io->init_x + n),
+                                          std::vector<double>(io->init_y, io->init_y + m)};
+  if (io && io->trace_fn && cfg->trace_period > 0) {
+    c.trace_sink = [io](const hplp_gpu::TraceRecord& rec, const hplp_gpu::Iterate& z) {
+      hplp_trace_t t;
+      t.epoch = rec.epoch;
+      t.inner = rec.inner;
+      t.iteration = rec.iteration;
+      t.fixed_point_residual = rec.fixed_point_residual;
+      put_kkt(rec.kkt, &t.kkt);
+      t.candidate_norm_normalized = rec.candidate_norm_normalized;
+      t.candidate_norm_difference = rec.candidate_norm_difference;
+      t.wall_seconds = rec.wall_seconds;
+      io->trace_fn(&t, z.x.data(), static_cast<int64_t>(z.x.size()), z.y.data(), static_cast<int64_t>(z.y.size()),
+                   io->trace_user);
+    };
+  }
+  return c;
+}
+
+struct StdHandle {
+  hplp_gpu::StandardFormLP lp;
+  hplp_gpu::VariableMap map;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* hplp_last_error(void) { return g_err.c_str(); }
+
+const char* hplp_status_string(int32_t status) {
+  if (status < 0 || status > 5) return "unknown";
+  return hplp_gpu::to_string(static_cast<hplp_gpu::SolveStatus>(status));
+}
+
+int hplp_validate_config(const hplp_config_t* cfg) {
+  return guarded([&] {
+    const hplp_gpu::SolverConfig c = hplp_gpu::from_pod(*cfg);
+    if (!(c.tolerance > 0.0)) throw std::invalid_argument("SolverConfig: tolerance must be > 0");
+    if (c.iteration_limit < 0) throw std::invalid_argument("SolverConfig: iteration_limit must be >= 0");
+    if (!(c.certificate_tolerance > 0.0))
+      throw std::invalid_argument("SolverConfig: certificate_tolerance must be > 0");
+    if (c.infeasibility_check_period < 0 || c.trace_period < 0 || c.adaptive_stall_cap < 0)
+      throw std::invalid_argument("SolverConfig: periods must be >= 0");
+    if (c.restart.kind == hplp_gpu::RestartScheme::Kind::kFixedFrequency && c.restart.k_star < 1)
+      throw std::invalid_argument("RestartScheme: k_star must be >= 1");
+    if (c.restart.kind == hplp_gpu::RestartScheme::Kind::kAdaptiveResidualDecay &&
+        (!(c.restart.beta > 0.0) || !(c.restart.beta < 1.0) || c.restart.tau0 < 1))
+      throw std::invalid_argument("RestartScheme: adaptive needs beta in (0,1) and tau0 >= 1");
+  });
+}
+
+int hplp_solver_create(int32_t device, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                       const double* val, const double* b, const double* c, void** solver) {
+  return guarded([&] {
+    // SparseMatrix semantics first (sorts rows given in any order, rejects
+    // duplicates), then the device copy.
+    hplp_gpu::SparseMatrix a = hplp_gpu::SparseMatrix::from_csr(m, n, row_ptr, col_idx, val);
+    hplp_gpu::StandardFormLP lp(std::move(a), std::vector<double>(b, b + m), std::vector<double>(c, c + n));
+    *solver = new hplp_gpu::Solver(lp, device);
+  });
+}
+
+int hplp_solver_solve(void* solver, const hplp_config_t* cfg, hplp_io_t* io, hplp_result_t* result) {
+  return guarded([&] {
+    auto* s = static_cast<hplp_gpu::Solver*>(solver);
+    hplp_gpu::SolverConfig c = config_with_io(cfg, io, s->rows(), s->cols());
+    fill_result(s->solve(c), io, result);
+  });
+}
+
+void* hplp_solver_hx(void* solver) { return static_cast<hplp_gpu::Solver*>(solver)->hx(); }
+
+void hplp_solver_free(void* solver) { delete static_cast<hplp_gpu::Solver*>(solver); }
+
+int hplp_solve_csr(int32_t device, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                   const double* val, const double* b, const double* c, const hplp_config_t* cfg, hplp_io_t* io,
+                   hplp_result_t* result) {
+  void* s = nullptr;
+  int rc = hplp_solver_create(device, m, n, row_ptr, col_idx, val, b, c, &s);
+  if (rc != HPLP_OK) return rc;
+  rc = hplp_solver_solve(s, cfg, io, result);
+  hplp_solver_free(s);
+  return rc;
+}
+
+int hplp_to_standard_form(const hplp_general_t* g, void** std_form, int64_t* m, int64_t* n, int64_t* nnz) {
+  return guarded([&] {
+    auto conv = hplp_gpu::to_standard_form(*g);
+    auto* h = new StdHandle{std::move(conv.first), std::move(conv.second)};
+    *m = h->lp.num_rows();
+    *n = h->lp.num_cols();
+    *nnz = h->lp.a.nonzeros();
+    *std_form = h;
+  });
+}
+
+int hplp_std_export(void* std_form, int64_t* row_ptr, int32_t* col_idx, double* val, double* b, double* c) {
+  return guarded([&] {
+    const auto& h = *static_cast<StdHandle*>(std_form);
+    const auto& a = h.lp.a;
+    if (row_ptr) std::memcpy(row_ptr, a.row_ptr().data(), a.row_ptr().size() * sizeof(int64_t));
+    if (col_idx) std::memcpy(col_idx, a.col_idx().data(), a.col_idx().size() * sizeof(int32_t));
+    if (val) std::memcpy(val, a.values().data(), a.values().size() * sizeof(double));
+    if (b) std::memcpy(b, h.lp.b.data(), h.lp.b.size() * sizeof(double));
+    if (c) std::memcpy(c, h.lp.c.data(), h.lp.c.size() * sizeof(double));
+  });
+}
+
+int hplp_std_recover(void* std_form, const double* x_std, double* x_orig, double std_objective, double* objective) {
+  return guarded([&] {
+    const auto& h = *static_cast<StdHandle*>(std_form);
+    if (x_std && x_orig) {
+      std::vector<double> xs(x_std, x_std + h.map.standard_cols);
+      std::vector<double> xo = h.map.recover_primal(xs);
+      std::memcpy(x_orig, xo.data(), xo.size() * sizeof(double));
+    }
+    if (objective) *objective = h.map.recover_objective(std_objective);
+  });
+}
+
+void hplp_std_free(void* std_form) { delete static_cast<StdHandle*>(std_form); }
+
+int hplp_solve_general(int32_t device, const hplp_general_t* g, const hplp_config_t* cfg, hplp_io_t* io,
+                       hplp_result_t* result, double* x_orig, double* objective) {
+  return guarded([&] {
+    auto conv = hplp_gpu::to_standard_form(*g);
+    const hplp_gpu::StandardFormLP& lp = conv.first;
+    hplp_gpu::Solver s(lp, device);
+    hplp_gpu::SolverConfig c = config_with_io(cfg, io, lp.num_rows(), lp.num_cols());
+    hplp_gpu::SolveResult r = s.solve(c);
+    fill_result(r, io, result);
+    double cx = 0.0;
+    for (std::size_t j = 0; j < lp.c.size(); ++j) cx += lp.c[j] * r.final_iterate.x[j];
+    if (x_orig) {
+      std::vector<double> xo = conv.second.recover_primal(r.final_iterate.x);
+      std::memcpy(x_orig, xo.data(), xo.size() * sizeof(double));
+    }
+    if (objective) *objective = conv.second.recover_objective(cx);
+  });
+}
+
+}  // extern "C"

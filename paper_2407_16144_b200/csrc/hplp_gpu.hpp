@@ -1,0 +1,276 @@
+// hplp_gpu: C++ mirror of the reference hplp public API
+// (/root/reference/proj/include/hplp/{sparse_matrix,lp_model,pdhg_core,solver}.hpp)
+// whose solve() runs the rHPDHG loop on a B200 through the hx C-ABI layer
+// (include/hx.h).  Same type names, field meanings, defaults and exception
+// types; Eigen::VectorXd becomes std::vector<double>.  A C++ caller of the
+// reference switches by replacing `hplp::` with `hplp_gpu::`.
+#pragma once
+
+#include <cstdint>
+#include <functional>
+#include <limits>
+#include <optional>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "hplp_types.h"
+
+struct hx_ctx;  // include/hx.h
+
+namespace hplp_gpu {
+
+using Index = std::ptrdiff_t;
+using Vector = std::vector<double>;
+
+// inc/sparse_matrix.hpp:28-32
+struct Triplet {
+  Index row = 0;
+  Index col = 0;
+  double value = 0.0;
+};
+
+// inc/sparse_matrix.hpp:39-70.  Host CSR with ascending columns per row; the
+// device builds the column-major copy (A^T) itself.  Throws
+// std::invalid_argument on out-of-range indices, non-finite values and
+// duplicate (row, col) pairs (src/sparse_matrix.cpp:27-53).
+class SparseMatrix {
+ public:
+  SparseMatrix() = default;
+  SparseMatrix(Index n_rows, Index n_cols, const std::vector<Triplet>& entries);
+  static SparseMatrix from_csr(Index n_rows, Index n_cols, const int64_t* row_ptr, const int32_t* col_idx,
+                               const double* val);
+
+  Index rows() const { return rows_; }
+  Index cols() const { return cols_; }
+  Index nonzeros() const { return static_cast<Index>(val_.size()); }
+  const std::vector<int64_t>& row_ptr() const { return row_ptr_; }
+  const std::vector<int32_t>& col_idx() const { return col_idx_; }
+  const std::vector<double>& values() const { return val_; }
+  std::vector<Triplet> triplets_row_order() const;
+
+ private:
+  Index rows_ = 0;
+  Index cols_ = 0;
+  std::vector<int64_t> row_ptr_{0};
+  std::vector<int32_t> col_idx_;
+  std::vector<double> val_;
+};
+
+// inc/lp_model.hpp:27-37
+struct StandardFormLP {
+  SparseMatrix a;
+  Vector b;
+  Vector c;
+  StandardFormLP(SparseMatrix a_in, Vector b_in, Vector c_in);
+  Index num_rows() const { return a.rows(); }
+  Index num_cols() const { return a.cols(); }
+};
+
+// inc/lp_model.hpp:39-74
+enum class RowRelation { kLessEqual, kEqual, kGreaterEqual };
+
+struct GeneralFormRow {
+  std::string name;
+  RowRelation relation = RowRelation::kEqual;
+  double rhs = 0.0;
+  std::optional<double> range;
+};
+
+struct GeneralFormColumn {
+  std::string name;
+  double lower = 0.0;
+  double upper = std::numeric_limits<double>::infinity();
+};
+
+struct GeneralFormLP {
+  std::string name;
+  bool maximize = false;
+  std::string objective_name;
+  double objective_constant = 0.0;
+  std::vector<GeneralFormRow> rows;
+  std::vector<GeneralFormColumn> columns;
+  std::vector<double> objective;
+  std::vector<Triplet> entries;
+  Index num_rows() const { return static_cast<Index>(rows.size()); }
+  Index num_cols() const { return static_cast<Index>(columns.size()); }
+};
+
+// inc/lp_model.hpp:77-119
+struct VariableRecovery {
+  enum class Kind { kShifted, kMirrored, kSplit };
+  Kind kind = Kind::kShifted;
+  Index col = 0;
+  Index neg_col = 0;
+  double offset = 0;
+};
+
+struct RowConversion {
+  double lower = 0.0;
+  double upper = 0.0;
+  std::optional<Index> slack_col;
+  double slack_sign = 0.0;
+};
+
+struct BoundRow {
+  Index row = 0;
+  Index col = 0;
+  Index slack_col = 0;
+  double rhs = 0.0;
+};
+
+struct VariableMap {
+  std::vector<VariableRecovery> recoveries;
+  std::vector<RowConversion> row_conversions;
+  std::vector<BoundRow> bound_rows;
+  double objective_sign = 1.0;
+  double objective_constant = 0.0;
+  Index standard_rows = 0;
+  Index standard_cols = 0;
+  Vector recover_primal(const Vector& x_std) const;
+  double recover_objective(double standard_objective) const {
+    return objective_sign * standard_objective + objective_constant;
+  }
+};
+
+// inc/lp_model.hpp:126; same row/column ordering as src/lp_model.cpp:155-325.
+std::pair<StandardFormLP, VariableMap> to_standard_form(const GeneralFormLP& g);
+// The same from the flat CSR-with-bounds description of include/hplp_types.h.
+std::pair<StandardFormLP, VariableMap> to_standard_form(const hplp_general_t& g);
+
+// inc/pdhg_core.hpp:23-30, :82-87
+struct Iterate {
+  Vector x;
+  Vector y;
+};
+
+struct KktError {
+  double primal_residual = 0.0;
+  double dual_residual = 0.0;
+  double gap_residual = 0.0;
+  double max_relative = 0.0;
+};
+
+// inc/solver.hpp:32-58
+struct RestartScheme {
+  enum class Kind { kFixedFrequency, kAdaptiveResidualDecay, kNone };
+  Kind kind = Kind::kAdaptiveResidualDecay;
+  long k_star = 0;
+  double beta = 0.36787944117144233;
+  long tau0 = 32;
+  static RestartScheme fixed(long k_star);
+  static RestartScheme adaptive(double beta = 0.36787944117144233, long tau0 = 32);
+  static RestartScheme none();
+};
+
+bool should_restart(const RestartScheme& scheme, long n, long k, double residual_now,
+                    double residual_epoch_start);
+
+enum class SolveStatus {
+  kOptimal,
+  kPrimalInfeasible,
+  kDualInfeasible,
+  kPrimalDualInfeasible,
+  kIterationLimit,
+  kTimeLimit,
+};
+
+const char* to_string(SolveStatus status);
+
+enum class CandidateSource { kNormalizedIterate, kIterateDifference };
+enum class Orientation { kAsIs, kNegated };
+
+// inc/diagnostics.hpp:72-84 (the partition estimate is diagnostics-only and
+// left empty by the GPU loop).
+struct TraceRecord {
+  long epoch = 0;
+  long inner = 0;
+  long iteration = 0;
+  double fixed_point_residual = 0.0;
+  KktError kkt;
+  double candidate_norm_normalized = std::numeric_limits<double>::quiet_NaN();
+  double candidate_norm_difference = std::numeric_limits<double>::quiet_NaN();
+  double wall_seconds = 0.0;
+};
+
+// inc/solver.hpp:62-80
+struct SolverConfig {
+  RestartScheme restart;
+  double tolerance = 1e-8;
+  long iteration_limit = 1000000;
+  double time_limit_seconds = std::numeric_limits<double>::infinity();
+  std::optional<double> eta_override;
+  long infeasibility_check_period = 100;
+  long trace_period = 0;
+  double certificate_tolerance = 1e-6;
+  double tol_active = 1e-6;
+  long adaptive_stall_cap = 2000;
+  std::uint64_t seed = 12345;
+  std::optional<Iterate> initial_iterate;
+  std::function<void(const TraceRecord&, const Iterate&)> trace_sink;
+  int device = 0;  // B200 ordinal (extension; the reference has no device)
+};
+
+// inc/solver.hpp:82-116
+struct EpochStats {
+  long epoch = 0;
+  long restart_length = 0;
+  double residual_at_start = 0.0;
+  KktError kkt_at_start;
+};
+
+struct Certificate {
+  Vector vector;
+  CandidateSource source = CandidateSource::kIterateDifference;
+  long at_iteration = 0;
+  Orientation orientation = Orientation::kAsIs;
+  double residual = 0.0;
+  double margin = 0.0;
+};
+
+struct SolveTotals {
+  long iterations = 0;
+  long spmv_count = 0;
+  double wall_seconds = 0.0;
+  double eta = 0.0;
+  double sigma_estimate = 0.0;
+};
+
+struct SolveResult {
+  SolveStatus status = SolveStatus::kIterationLimit;
+  Iterate final_iterate;
+  KktError final_kkt;
+  std::optional<Certificate> primal_certificate;
+  std::optional<Certificate> dual_certificate;
+  std::vector<EpochStats> epochs;
+  SolveTotals totals;
+};
+
+// A device-resident problem: upload once, solve many times (bench, warm
+// starts).  Owns one hx context.
+class Solver {
+ public:
+  Solver(const StandardFormLP& lp, int device = 0);
+  Solver(int device, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const double* val,
+         const double* b, const double* c);
+  ~Solver();
+  Solver(const Solver&) = delete;
+  Solver& operator=(const Solver&) = delete;
+  SolveResult solve(const SolverConfig& config);
+  ::hx_ctx* hx() const { return ctx_; }
+  int64_t rows() const { return m_; }
+  int64_t cols() const { return n_; }
+
+ private:
+  ::hx_ctx* ctx_ = nullptr;
+  int64_t m_ = 0, n_ = 0, nnz_ = 0;
+};
+
+// inc/solver.hpp:130 -- src/solver.cpp:206-342 on the GPU.
+SolveResult solve(const StandardFormLP& lp, const SolverConfig& config);
+
+// config <-> flat POD (include/hplp_types.h)
+SolverConfig from_pod(const hplp_config_t& c);
+hplp_config_t to_pod(const SolverConfig& c);
+
+}  // namespace hplp_gpu

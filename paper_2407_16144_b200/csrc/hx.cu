@@ -1,0 +1,1798 @@
+// hx: the B200 (sm_100a) CUDA layer of the rHPDHG solver.  See include/hx.h
+// and DESIGN.md.
+//
+// Every rHPDHG iteration runs inside ONE persistent cooperative kernel
+// (loop_kernel): two fused SpMV phases separated by software grid barriers,
+// with the reference's scalar control logic (src/solver.cpp:241-341) executed
+// on the device by the last CTA to arrive at the end-of-iteration barrier.
+// No host round trip per iteration.
+//
+//   phase A (rows of the explicit A^T = columns j of A):
+//     x_j   = T_prev.x_j, or (1-w) T_prev.x_j + w anchor_x_j      [solver.cpp:333-336]
+//     aty_j = (A^T y)_j                                           [pdhg_core.cpp:80]
+//     x+_j  = max(0, x_j - eta (aty_j + c_j))                     [pdhg_core.cpp:81-82]
+//     partials ||[-(c + A^T y)]+||^2, c.x, ||x - x+||^2           [pdhg_core.cpp:60-63, 39]
+//   phase B (rows i of A):
+//     ax+_i = (A x+)_i                                            [pdhg_core.cpp:83]
+//     y+_i  = y_i + eta ((2 ax+_i - ax_i) - b_i)                  [pdhg_core.cpp:84]
+//     (1-w) y+ + w anchor_y and (1-w) ax+ + w ax_anchor, written
+//     speculatively so a non-restart needs no extra pass        [solver.cpp:335-337]
+//     partials ||Ax - b||^2, b.y, ||y - y+||^2, (y - y+).(Ax - Ax+)
+//   controller (last CTA): KKT [pdhg_core.cpp:57-68], canonical residual
+//     [:37-51], epochs, best iterate, termination [solver.cpp:292-295],
+//     certificate-scan scheduling [:297-317], restart [:162-174, :319-332],
+//     buffer roles for the next iteration.
+//
+// All reductions are fixed-order (static row->warp schedule, fixed trees, no
+// floating-point atomics): results are bit-reproducible run to run.  Device
+// arithmetic is compiled with -fmad=false so every scalar op rounds once,
+// like the reference's SSE2 build.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <string>
+
+#include "hx_internal.cuh"
+
+namespace hx {
+
+// ---------------------------------------------------------------------------
+// Control block in device global memory.  Only the controller (thread 0 of
+// the last-arriving CTA, working on a shared-memory copy) writes it.
+// ---------------------------------------------------------------------------
+enum Mode : int { kModeLoop = 0, kModePower = 1 };
+
+// What every CTA needs for its next phase (copied to shared memory).
+struct Roles {
+  int x_src, x_anchor, x_mode, zx_out, xp_out;
+  int y_cur, y_anchor, yp_out, yc_out;
+  int ax_cur, ax_anchor, axp_out, axc_out;
+  int stop;      // leave the kernel now
+  int check;     // run the certificate-scan phases for this iteration
+  int pw_mode;   // power: 0 gather x0, 1 gather z / zn
+  int cand_on[4];
+  int pad0;
+  double w_x;        // Halpern weight that forms x in phase A
+  double w_next;     // weight of the speculative combos in phase B
+  double eta;
+  double cand_scale; // 2/k for the normalized candidate
+  double cn2[4];     // candidate l2 norms: 0 v_x diff, 1 v_y diff, 2 v_x norm, 3 v_y norm
+  double pw_zn;
+};
+
+struct Ctl {
+  Roles r;
+  long long iteration_limit, check_period, stall_cap, k_star, tau0, trace_period;
+  int restart_kind, mode;
+  double tol, cert_tol, beta, sigma_used, b_norm, c_norm, time_limit_s;
+  unsigned long long t0_ns;
+  long long it, n, k, spmv, batch_end, n_epochs;
+  double res_epoch_start, best_kkt, best_err[4];
+  int x_best, y_best;
+  int status, error, paused, pad1;
+  long long last_it, last_n, last_k;
+  double last_res, last_kkt[4];
+  int last_zx, last_y, last_xp, last_yp, last_xa, last_ya, last_ax, last_axp;
+  double final_kkt[4];
+  int final_x, final_y;
+  int cfinite[4];
+  double cinf[4], cmax_u[4], cmax_negu[4], cdot[4], cmax_at[4], cmax_negat[4], cmax_abs_au[4];
+  hplp_cert_meta_t cert[2];  // 0 primal, 1 dual
+  int cert_cand[2];
+  long long pw_k, pw_max, pw_iters;
+  double pw_tol, pw_sigma, pw_sigma_prev, pw_sigma_cur;
+  int pw_converged, pw_redraw;
+};
+static_assert(sizeof(Ctl) % 8 == 0, "Ctl copied as 8-byte words");
+static_assert(sizeof(Roles) % 4 == 0, "Roles copied as 4-byte words");
+
+struct GridBar {
+  unsigned count, gen, abort, pad;
+};
+
+struct KParams {
+  Sched A;   // rows of A
+  Sched AT;  // rows of A^T
+  int m, n;
+  const double* __restrict__ b;
+  const double* __restrict__ c;
+  double* xpool;   // kXPool * n
+  double* ypool;   // kYPool * m
+  double* axpool;  // kAxPool * m
+  double* upool;   // [u0: n][u2: n][u1: m][u3: m] certificate unit vectors
+  double* slots;   // kMaxQ * grid
+  Ctl* ctl;
+  GridBar* bar;
+  hplp_epoch_t* epochs;  // ring of kEpochCap
+};
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Vectors written inside the kernel are read at L2 (ld.global.cg): no stale
+// L1 lines across grid barriers.  The matrix, b and c are read-only (ld.nc).
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+
+__device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = dmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <int Q, unsigned MaxMask>
+__device__ __forceinline__ void acc_init(double (&acc)[Q]) {
+#pragma unroll
+  for (int q = 0; q < Q; ++q) acc[q] = ((MaxMask >> q) & 1u) ? -INFINITY : 0.0;
+}
+
+// Per-thread accumulators -> slots[q * grid + cta] (fixed order).
+template <int Q, unsigned MaxMask>
+__device__ void block_to_slots(const double (&acc)[Q], double* slots, int grid) {
+  __shared__ double red[kWarps][kMaxQ];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const double v = ((MaxMask >> q) & 1u) ? warp_max(acc[q]) : warp_sum(acc[q]);
+    if (lane == 0) red[warp][q] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < Q) {
+    const int q = threadIdx.x;
+    const bool mx = (MaxMask >> q) & 1u;
+    double v = red[0][q];
+    for (int w = 1; w < kWarps; ++w) v = mx ? dmax(v, red[w][q]) : v + red[w][q];
+    slots[q * grid + blockIdx.x] = v;
+  }
+  __syncthreads();
+}
+
+// Warp-level fixed-order reduction of count values at p[i * stride].
+__device__ __forceinline__ double warp_reduce_strided(const double* p, int count, int stride, bool mx) {
+  const int lane = threadIdx.x & 31;
+  double v = mx ? -INFINITY : 0.0;
+  for (int i = lane; i < count; i += 32) {
+    const double s = ldcg(p + static_cast<long long>(i) * stride);
+    v = mx ? dmax(v, s) : v + s;
+  }
+  return mx ? warp_max(v) : warp_sum(v);
+}
+
+// tot = reduce(slots[slot_q]) (+) reduce(long_terms[.][long_q]); one warp.
+__device__ __forceinline__ double total_of(const double* slots, int grid, int slot_q,
+                                           const double* long_terms, int n_long, int long_q,
+                                           bool mx) {
+  const double v = warp_reduce_strided(slots + slot_q * grid, grid, 1, mx);
+  if (long_terms == nullptr || n_long == 0) return v;
+  const double l = warp_reduce_strided(long_terms + long_q, n_long, kMaxQ, mx);
+  return mx ? dmax(v, l) : v + l;
+}
+
+// ---------------------------------------------------------------------------
+// Fused SpMV engine.  Src: gather functor (column -> value).  Epi: row
+// epilogue apply(row, sum, terms[Q]).  Terms of regular rows accumulate per
+// thread; a long row's terms are parked in long_terms by whichever warp
+// finishes the row, so every reduction keeps a fixed order.
+// ---------------------------------------------------------------------------
+template <int Q, unsigned MaxMask, class Src, class Epi>
+__device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& src, Epi& epi,
+                                          double (&acc)[Q], int gwarp, int lane) {
+  const int t_end = S.task_ptr[gwarp + 1];
+  for (int t = S.task_ptr[gwarp]; t < t_end; ++t) {
+    const int4 tk = S.tasks[t];
+    const int lv = tk.z;
+    const int v = 1 << lv;
+    const int sub = lane & (v - 1);
+    const int per_pass = 32 >> lv;
+    for (int r0 = tk.x; r0 < tk.y; r0 += per_pass) {
+      const int r = r0 + (lane >> lv);
+      const bool active = r < tk.y;
+      double s = 0.0;
+      if (active) {
+        const int p1 = __ldg(S.ptr + r + 1);
+#pragma unroll 4
+        for (int p = __ldg(S.ptr + r) + sub; p < p1; p += v)
+          s += __ldg(S.val + p) * src(__ldg(S.idx + p));
+      }
+      for (int o = v >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (active && sub == 0) {
+        double tm[Q];
+        epi.apply(r, s, tm);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) acc[q] = ((MaxMask >> q) & 1u) ? dmax(acc[q], tm[q]) : acc[q] + tm[q];
+      }
+    }
+  }
+  const int pe = S.piece_ptr[gwarp + 1];
+  for (int pi = S.piece_ptr[gwarp]; pi < pe; ++pi) {
+    const Piece pc = S.pieces[pi];
+    double s = 0.0;
+#pragma unroll 4
+    for (int p = pc.p0 + lane; p < pc.p1; p += 32) s += __ldg(S.val + p) * src(__ldg(S.idx + p));
+    s = warp_sum(s);
+    if (lane == 0) {
+      double* part = S.piece_part[set];
+      part[pc.slot] = s;
+      __threadfence();
+      const unsigned old = atomicAdd(S.piece_cnt[set] + pc.counter, 1u);
+      if (old == static_cast<unsigned>(pc.npieces - 1)) {
+        __threadfence();
+        const int first = pc.slot - pc.index;
+        double tot = 0.0;
+        for (int i = 0; i < pc.npieces; ++i) tot += ldcg(part + first + i);
+        S.piece_cnt[set][pc.counter] = 0u;
+        double tm[Q];
+        epi.apply(pc.row, tot, tm);
+        double* lt = S.long_terms[set] + static_cast<long long>(pc.counter) * kMaxQ;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) lt[q] = tm[q];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---- gather sources --------------------------------------------------------
+struct SrcVec {
+  const double* v;
+  __device__ __forceinline__ double operator()(int j) const { return ldcg(v + j); }
+};
+struct SrcDiv {  // power iteration: x = z / ||z|| formed on the fly (same rounding)
+  const double* v;
+  double d;
+  __device__ __forceinline__ double operator()(int j) const { return ldcg(v + j) / d; }
+};
+
+// ---- epilogues -------------------------------------------------------------
+struct EpiPrimal {  // phase A, rows of A^T
+  const double* xs;
+  const double* xa;
+  const double* c;
+  double* zx;
+  double* xp;
+  double w, eta;
+  int mode;
+  __device__ __forceinline__ void apply(int j, double aty, double (&t)[3]) const {
+    double x;
+    if (mode) {
+      const double omw = 1.0 - w;
+      x = omw * ldcg(xs + j) + w * ldcg(xa + j);
+    } else {
+      x = ldcg(xs + j);
+    }
+    zx[j] = x;
+    const double cj = __ldg(c + j);
+    double xn = x - eta * (aty + cj);
+    xn = xn < 0.0 ? 0.0 : xn;
+    xp[j] = xn;
+    double rc = -(cj + aty);
+    rc = rc < 0.0 ? 0.0 : rc;
+    const double dx = x - xn;
+    t[0] = rc * rc;
+    t[1] = cj * x;
+    t[2] = dx * dx;
+  }
+};
+
+struct EpiDual {  // phase B, rows of A
+  const double* y;
+  const double* ax;
+  const double* b;
+  const double* ya;
+  const double* axa;
+  double* yp;
+  double* axp;
+  double* yc;
+  double* axc;
+  double eta, w;
+  __device__ __forceinline__ void apply(int i, double s, double (&t)[4]) const {
+    const double yi = ldcg(y + i);
+    const double axi = ldcg(ax + i);
+    const double bi = __ldg(b + i);
+    const double ypi = yi + eta * ((2.0 * s - axi) - bi);
+    yp[i] = ypi;
+    axp[i] = s;
+    const double omw = 1.0 - w;
+    yc[i] = omw * ypi + w * ldcg(ya + i);
+    axc[i] = omw * s + w * ldcg(axa + i);
+    const double d = axi - bi;
+    const double dy = yi - ypi;
+    const double dax = axi - s;
+    t[0] = d * d;
+    t[1] = bi * yi;
+    t[2] = dy * dy;
+    t[3] = dy * dax;
+  }
+};
+
+struct EpiStoreSq {  // out = s, term s^2 (power iteration)
+  double* out;
+  __device__ __forceinline__ void apply(int r, double s, double (&t)[1]) const {
+    out[r] = s;
+    t[0] = s * s;
+  }
+};
+
+struct EpiPosNeg {  // primal certificate: max(A^T u), max(-A^T u)
+  __device__ __forceinline__ void apply(int, double s, double (&t)[2]) const {
+    t[0] = s;
+    t[1] = -s;
+  }
+};
+
+struct EpiAbs {  // dual certificate: max |A u|
+  __device__ __forceinline__ void apply(int, double s, double (&t)[1]) const { t[0] = fabs(s); }
+};
+
+// ---------------------------------------------------------------------------
+// Grid barrier.  The last CTA to arrive runs ctl() (whole CTA) before the
+// release; everybody else spins (with a 10 s watchdog) on the generation.
+// ---------------------------------------------------------------------------
+template <class F>
+__device__ bool grid_sync(const KParams& P, F&& ctl) {
+  __shared__ int s_last, s_ok;
+  __shared__ unsigned s_gen;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = *reinterpret_cast<volatile unsigned*>(&P.bar->gen);
+    __threadfence();
+    const unsigned arrived = atomicAdd(&P.bar->count, 1u);
+    s_last = arrived == gridDim.x - 1;
+    s_gen = gen;
+    s_ok = 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    ctl();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      P.bar->count = 0u;
+      __threadfence();
+      atomicAdd(&P.bar->gen, 1u);
+    }
+  } else if (threadIdx.x == 0) {
+    const unsigned long long t0 = global_ns();
+    while (*reinterpret_cast<volatile unsigned*>(&P.bar->gen) == s_gen) {
+      if (*reinterpret_cast<volatile unsigned*>(&P.bar->abort)) {
+        s_ok = 0;
+        break;
+      }
+      __nanosleep(32);
+      if (global_ns() - t0 > 10000000000ull) {
+        atomicExch(&P.bar->abort, 1u);
+        s_ok = 0;
+        break;
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+struct NoCtl {
+  __device__ void operator()() const {}
+};
+
+__device__ void load_roles(const Ctl* ctl, Roles& R) {
+  const unsigned* src = reinterpret_cast<const unsigned*>(&ctl->r);
+  unsigned* dst = reinterpret_cast<unsigned*>(&R);
+  for (int i = threadIdx.x; i < static_cast<int>(sizeof(Roles) / 4); i += blockDim.x)
+    dst[i] = __ldcg(src + i);
+  __syncthreads();
+}
+
+__device__ void ctl_load(const Ctl* g, Ctl& s) {
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(g);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(&s);
+  for (int i = threadIdx.x; i < static_cast<int>(sizeof(Ctl) / 8); i += blockDim.x)
+    dst[i] = __ldcg(src + i);
+  __syncthreads();
+}
+
+__device__ void ctl_store(const Ctl& s, Ctl* g) {
+  __syncthreads();
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&s);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(g);
+  for (int i = threadIdx.x; i < static_cast<int>(sizeof(Ctl) / 8); i += blockDim.x) dst[i] = src[i];
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Controller logic (thread 0 of the last CTA, on the shared copy).
+// ---------------------------------------------------------------------------
+__device__ int pick_free(int pool, int e0, int e1, int e2, int e3) {
+  for (int i = 0; i < pool; ++i)
+    if (i != e0 && i != e1 && i != e2 && i != e3) return i;
+  return -1;
+}
+
+// should_restart, src/solver.cpp:162-174.
+__device__ bool should_restart(const Ctl& C, long long n, long long k, double now, double start) {
+  switch (C.restart_kind) {
+    case HPLP_RESTART_FIXED:
+      return k >= C.k_star;
+    case HPLP_RESTART_ADAPTIVE:
+      if (n == 0) return k > C.tau0;
+      return now <= C.beta * start;
+    default:
+      return false;
+  }
+}
+
+__device__ void set_final_limit(Ctl& C, int status) {
+  C.status = status;
+  if (C.best_kkt < INFINITY) {  // isfinite(best_kkt): best_kkt only ever decreases from +inf
+    C.final_x = C.x_best;
+    C.final_y = C.y_best;
+    for (int q = 0; q < 4; ++q) C.final_kkt[q] = C.best_err[q];
+  } else {
+    C.final_x = -1;  // host evaluates kkt_error(z) with fresh products
+    C.final_y = -1;
+  }
+  C.r.stop = 1;
+}
+
+// Restart decision + Halpern combine bookkeeping + next roles + limits
+// (src/solver.cpp:319-341 and the loop-top checks :242-254).
+__device__ void finish_iteration(Ctl& C, hplp_epoch_t* epochs, double res) {
+  Roles& R = C.r;
+  bool restart = should_restart(C, C.n, C.k, res, C.res_epoch_start);
+  if (!restart && C.restart_kind == HPLP_RESTART_ADAPTIVE && C.stall_cap > 0 && C.k >= C.stall_cap)
+    restart = true;
+  if (restart) {
+    if (C.n_epochs > 0) epochs[(C.n_epochs - 1) % kEpochCap].restart_length = C.k;
+    R.x_src = R.xp_out;
+    R.x_mode = 0;
+    R.x_anchor = R.xp_out;
+    R.y_cur = R.yp_out;
+    R.y_anchor = R.yp_out;
+    R.ax_cur = R.axp_out;
+    R.ax_anchor = R.axp_out;
+    R.w_x = 0.0;
+    C.n += 1;
+    C.k = 0;
+  } else {
+    const double w = 1.0 / static_cast<double>(C.k + 2);
+    R.x_src = R.xp_out;
+    R.x_mode = 1;
+    R.w_x = w;
+    R.y_cur = R.yc_out;
+    R.ax_cur = R.axc_out;
+    C.k += 1;
+  }
+  R.check = 0;
+  C.it += 1;
+  R.zx_out = pick_free(kXPool, R.x_src, R.x_anchor, C.x_best, -1);
+  R.xp_out = pick_free(kXPool, R.x_src, R.x_anchor, C.x_best, R.zx_out);
+  R.yp_out = pick_free(kYPool, R.y_cur, R.y_anchor, C.y_best, -1);
+  R.yc_out = pick_free(kYPool, R.y_cur, R.y_anchor, C.y_best, R.yp_out);
+  R.axp_out = pick_free(kAxPool, R.ax_cur, R.ax_anchor, -1, -1);
+  R.axc_out = pick_free(kAxPool, R.ax_cur, R.ax_anchor, R.axp_out, -1);
+  R.w_next = 1.0 / static_cast<double>(C.k + 2);
+  if (C.it >= C.iteration_limit) {
+    set_final_limit(C, HPLP_STATUS_ITERATION_LIMIT);
+  } else if (static_cast<double>(global_ns() - C.t0_ns) * 1e-9 > C.time_limit_s) {
+    set_final_limit(C, HPLP_STATUS_TIME_LIMIT);
+  }
+  if (C.trace_period > 0 && C.last_it % C.trace_period == 0) {
+    C.paused = 1;
+    R.stop = 1;
+  }
+  if (C.it >= C.batch_end) R.stop = 1;
+}
+
+// After phases A+B: KKT, residual, epochs, best, termination, scan or finish.
+__device__ void main_logic(Ctl& C, const double* tot, hplp_epoch_t* epochs) {
+  Roles& R = C.r;
+  if (C.t0_ns == 0ull) C.t0_ns = global_ns();
+  const double dres = tot[0], cx = tot[1], dx2 = tot[2];
+  const double pres = tot[3], by = tot[4], dy2 = tot[5], dyax = tot[6];
+  // kkt_error_with_products, src/pdhg_core.cpp:57-68
+  double kkt[4];
+  kkt[0] = sqrt(pres) / (1.0 + C.b_norm);
+  kkt[1] = sqrt(dres) / (1.0 + C.c_norm);
+  kkt[2] = fabs(cx + by) / (1.0 + fabs(cx) + fabs(by));
+  double mx = kkt[0];
+  if (mx < kkt[1]) mx = kkt[1];
+  if (mx < kkt[2]) mx = kkt[2];
+  kkt[3] = mx;
+  // canonical_norm_with_product, src/pdhg_core.cpp:37-51
+  const double eta = R.eta;
+  const double q = dx2 / eta - 2.0 * dyax + dy2 / eta;
+  double res;
+  if (q < 0.0) {
+    const double scale = (dx2 + dy2) / eta;
+    if (q < -1e-9 * scale) {
+      C.error = HPLP_EDOMAIN;
+      R.stop = 1;
+      return;
+    }
+    res = 0.0;
+  } else {
+    res = sqrt(q);
+  }
+  C.spmv += 2;
+  if (C.k == 0) {  // src/solver.cpp:261-264
+    C.res_epoch_start = res;
+    hplp_epoch_t& e = epochs[C.n_epochs % kEpochCap];
+    e.epoch = C.n;
+    e.restart_length = 0;
+    e.residual_at_start = res;
+    e.kkt_at_start = {kkt[0], kkt[1], kkt[2], kkt[3]};
+    C.n_epochs += 1;
+  }
+  if (kkt[3] < C.best_kkt) {  // :265-269
+    C.best_kkt = kkt[3];
+    for (int i = 0; i < 4; ++i) C.best_err[i] = kkt[i];
+    C.x_best = R.zx_out;
+    C.y_best = R.y_cur;
+  }
+  C.last_it = C.it;
+  C.last_n = C.n;
+  C.last_k = C.k;
+  C.last_res = res;
+  for (int i = 0; i < 4; ++i) C.last_kkt[i] = kkt[i];
+  C.last_zx = R.zx_out;
+  C.last_xp = R.xp_out;
+  C.last_y = R.y_cur;
+  C.last_yp = R.yp_out;
+  C.last_xa = R.x_anchor;
+  C.last_ya = R.y_anchor;
+  C.last_ax = R.ax_cur;
+  C.last_axp = R.axp_out;
+  if (kkt[3] <= C.tol) {  // :292-295, returns z
+    C.status = HPLP_STATUS_OPTIMAL;
+    C.final_x = R.zx_out;
+    C.final_y = R.y_cur;
+    for (int i = 0; i < 4; ++i) C.final_kkt[i] = kkt[i];
+    R.stop = 1;
+    if (C.trace_period > 0 && C.last_it % C.trace_period == 0) C.paused = 1;
+    return;
+  }
+  if (C.check_period > 0 && C.it > 0 && (C.it % C.check_period == 0 || C.k == 0)) {  // :297-298
+    R.check = 1;
+    R.cand_scale = C.k >= 1 ? 2.0 / static_cast<double>(C.k) : 0.0;
+    return;
+  }
+  finish_iteration(C, epochs, res);
+}
+
+// validate_primal_infeasibility, src/infeasibility.cpp:41-67, from reductions.
+__device__ bool eval_primal(const Ctl& C, int c, hplp_cert_meta_t& rep) {
+  const double tol = C.cert_tol;
+  double inf_u = C.cinf[c];
+  if (inf_u < 0.0) inf_u = 0.0;
+  const double threshold = tol * dmax(1.0, inf_u * C.sigma_used);
+  double best_res = INFINITY;
+  bool valid = false;
+  for (int si = 0; si < 2; ++si) {
+    const double s = si == 0 ? 1.0 : -1.0;
+    const double residual = dmax(0.0, si == 0 ? C.cmax_at[c] : C.cmax_negat[c]);
+    const double margin = s * C.cdot[c];
+    const bool ok = residual <= threshold && margin > 0.0 && margin >= tol * C.b_norm;
+    if (ok || (!valid && residual < best_res)) {
+      best_res = residual;
+      rep.residual = residual;
+      rep.margin = margin;
+      rep.orientation = si == 0 ? HPLP_ORIENT_AS_IS : HPLP_ORIENT_NEGATED;
+    }
+    if (ok) {
+      valid = true;
+      break;
+    }
+  }
+  return valid;
+}
+
+// validate_dual_infeasibility, src/infeasibility.cpp:76-106, from reductions.
+__device__ bool eval_dual(const Ctl& C, int c, hplp_cert_meta_t& rep) {
+  const double tol = C.cert_tol;
+  double inf_u = C.cinf[c];
+  if (inf_u < 0.0) inf_u = 0.0;
+  const double threshold = tol * dmax(1.0, inf_u * C.sigma_used);
+  const double nonneg_threshold = tol * dmax(1.0, inf_u);
+  const double margin_threshold = -tol * dmax(1.0, C.c_norm);
+  const double ray = dmax(0.0, C.cmax_abs_au[c]);
+  double best_res = INFINITY;
+  bool valid = false;
+  for (int si = 0; si < 2; ++si) {
+    const double s = si == 0 ? 1.0 : -1.0;
+    const double sign = dmax(0.0, si == 0 ? C.cmax_negu[c] : C.cmax_u[c]);
+    const double residual = dmax(ray, sign);
+    const double margin = s * C.cdot[c];
+    const bool ok = ray <= threshold && sign <= nonneg_threshold && margin <= margin_threshold;
+    if (ok || (!valid && residual < best_res)) {
+      best_res = residual;
+      rep.residual = residual;
+      rep.margin = margin;
+      rep.orientation = si == 0 ? HPLP_ORIENT_AS_IS : HPLP_ORIENT_NEGATED;
+    }
+    if (ok) {
+      valid = true;
+      break;
+    }
+  }
+  return valid;
+}
+
+// CertificateScan::check semantics, src/solver.cpp:108-135 (+ :300-317).
+// Candidates: 0 v_x diff, 1 v_y diff, 2 v_x normalized, 3 v_y normalized.
+__device__ void scan_logic(Ctl& C, hplp_epoch_t* epochs) {
+  Roles& R = C.r;
+  hplp_cert_meta_t prim{}, dual{};
+  bool have_p = false, have_d = false;
+  for (int src = 0; src < 2; ++src) {  // difference first, then normalized
+    if (src == 1 && C.last_k < 1) break;
+    const int cy = src == 0 ? 1 : 3, cx = src == 0 ? 0 : 2;
+    const int source = src == 0 ? HPLP_SOURCE_ITERATE_DIFFERENCE : HPLP_SOURCE_NORMALIZED_ITERATE;
+    if (!have_p && R.cn2[cy] > 0.0) {
+      C.spmv += 1;
+      hplp_cert_meta_t rep{};
+      if (C.cfinite[cy] && eval_primal(C, cy, rep)) {
+        have_p = true;
+        prim = rep;
+        prim.present = 1;
+        prim.source = source;
+        prim.at_iteration = C.last_it;
+        C.cert_cand[0] = cy;
+      }
+    }
+    if (!have_d && R.cn2[cx] > 0.0) {
+      C.spmv += 1;
+      hplp_cert_meta_t rep{};
+      if (C.cfinite[cx] && eval_dual(C, cx, rep)) {
+        have_d = true;
+        dual = rep;
+        dual.present = 1;
+        dual.source = source;
+        dual.at_iteration = C.last_it;
+        C.cert_cand[1] = cx;
+      }
+    }
+  }
+  if (have_p || have_d) {
+    C.cert[0] = prim;
+    C.cert[1] = dual;
+    C.status = have_p && have_d ? HPLP_STATUS_PRIMAL_DUAL_INFEASIBLE
+               : have_p         ? HPLP_STATUS_PRIMAL_INFEASIBLE
+                                : HPLP_STATUS_DUAL_INFEASIBLE;
+    C.final_x = C.last_zx;
+    C.final_y = C.last_y;
+    for (int i = 0; i < 4; ++i) C.final_kkt[i] = C.last_kkt[i];
+    R.stop = 1;
+    if (C.trace_period > 0 && C.last_it % C.trace_period == 0) C.paused = 1;
+    return;
+  }
+  finish_iteration(C, epochs, C.last_res);
+}
+
+// ---------------------------------------------------------------------------
+// The persistent loop kernel.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 2) loop_kernel(KParams P) {
+  __shared__ Roles R;
+  __shared__ Ctl sC;
+  __shared__ double tot[kMaxQ];
+  const int G = gridDim.x;
+  const int lane = threadIdx.x & 31;
+  const int gwarp = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int gtid = blockIdx.x * kThreads + threadIdx.x;
+  const int gstride = G * kThreads;
+  const int n = P.n, m = P.m;
+  load_roles(P.ctl, R);
+  const int mode = __ldcg(&P.ctl->mode);
+
+  if (mode == kModePower) {
+    // power_iteration loop body, src/sparse_matrix.cpp:153-177
+    double* x0 = P.xpool;
+    double* z = P.xpool + n;
+    double* w = P.ypool;
+    while (!R.stop) {
+      {
+        double acc[1];
+        acc_init<1, 0>(acc);
+        EpiStoreSq e{w};
+        if (R.pw_mode == 0) spmv_rows<1, 0>(P.A, 0, SrcVec{x0}, e, acc, gwarp, lane);
+        else spmv_rows<1, 0>(P.A, 0, SrcDiv{z, R.pw_zn}, e, acc, gwarp, lane);
+        block_to_slots<1, 0>(acc, P.slots, G);
+      }
+      bool ok = grid_sync(P, [&] {
+        ctl_load(P.ctl, sC);
+        if ((threadIdx.x >> 5) == 0) {
+          const double t = total_of(P.slots, G, 0, P.A.long_terms[0], P.A.n_long, 0, false);
+          if (lane == 0) tot[0] = t;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          const double sigma = sqrt(tot[0]);
+          sC.pw_iters = sC.pw_k + 1;
+          sC.pw_sigma_cur = sigma;
+          if (sigma == 0.0) {
+            sC.pw_redraw = 1;
+            sC.r.stop = 1;
+          }
+        }
+        ctl_store(sC, P.ctl);
+      });
+      if (!ok) return;
+      load_roles(P.ctl, R);
+      if (R.stop) break;
+      {
+        double acc[1];
+        acc_init<1, 0>(acc);
+        EpiStoreSq e{z};
+        spmv_rows<1, 0>(P.AT, 0, SrcVec{w}, e, acc, gwarp, lane);
+        block_to_slots<1, 0>(acc, P.slots, G);
+      }
+      ok = grid_sync(P, [&] {
+        ctl_load(P.ctl, sC);
+        if ((threadIdx.x >> 5) == 0) {
+          const double t = total_of(P.slots, G, 0, P.AT.long_terms[0], P.AT.n_long, 0, false);
+          if (lane == 0) tot[0] = t;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          const double sigma = sC.pw_sigma_cur;
+          sC.pw_sigma = sigma;
+          if (sC.pw_k > 0 && fabs(sigma - sC.pw_sigma_prev) <= sC.pw_tol * sigma) {
+            sC.pw_converged = 1;
+            sC.r.stop = 1;
+          } else {
+            sC.pw_sigma_prev = sigma;
+            const double zn = sqrt(tot[0]);
+            if (zn == 0.0) {
+              sC.pw_converged = 1;
+              sC.r.stop = 1;
+            } else {
+              sC.r.pw_mode = 1;
+              sC.r.pw_zn = zn;
+              sC.pw_k += 1;
+              if (sC.pw_k >= sC.pw_max) sC.r.stop = 1;
+            }
+          }
+        }
+        ctl_store(sC, P.ctl);
+      });
+      if (!ok) return;
+      load_roles(P.ctl, R);
+    }
+    return;
+  }
+
+  while (!R.stop) {
+    // ---- phase A: A^T y, primal step, primal partials ----
+    {
+      double acc[3];
+      acc_init<3, 0>(acc);
+      EpiPrimal e{P.xpool + static_cast<size_t>(R.x_src) * n,
+                  P.xpool + static_cast<size_t>(R.x_anchor) * n,
+                  P.c,
+                  P.xpool + static_cast<size_t>(R.zx_out) * n,
+                  P.xpool + static_cast<size_t>(R.xp_out) * n,
+                  R.w_x,
+                  R.eta,
+                  R.x_mode};
+      spmv_rows<3, 0>(P.AT, 0, SrcVec{P.ypool + static_cast<size_t>(R.y_cur) * m}, e, acc, gwarp,
+                      lane);
+      block_to_slots<3, 0>(acc, P.slots, G);
+    }
+    if (!grid_sync(P, NoCtl{})) return;
+    // ---- phase B: A x+, dual step, speculative Halpern combos, partials ----
+    {
+      double acc[4];
+      acc_init<4, 0>(acc);
+      EpiDual e{P.ypool + static_cast<size_t>(R.y_cur) * m,
+                P.axpool + static_cast<size_t>(R.ax_cur) * m,
+                P.b,
+                P.ypool + static_cast<size_t>(R.y_anchor) * m,
+                P.axpool + static_cast<size_t>(R.ax_anchor) * m,
+                P.ypool + static_cast<size_t>(R.yp_out) * m,
+                P.axpool + static_cast<size_t>(R.axp_out) * m,
+                P.ypool + static_cast<size_t>(R.yc_out) * m,
+                P.axpool + static_cast<size_t>(R.axc_out) * m,
+                R.eta,
+                R.w_next};
+      spmv_rows<4, 0>(P.A, 0, SrcVec{P.xpool + static_cast<size_t>(R.xp_out) * n}, e, acc, gwarp,
+                      lane);
+      block_to_slots<4, 0>(acc, P.slots + 3 * G, G);
+    }
+    if (!grid_sync(P, [&] {
+          ctl_load(P.ctl, sC);
+          const int wq = threadIdx.x >> 5;
+          if (wq < 7) {
+            const Sched& S = wq < 3 ? P.AT : P.A;
+            const double t = total_of(P.slots, G, wq, S.long_terms[0], S.n_long, wq < 3 ? wq : wq - 3, false);
+            if (lane == 0) tot[wq] = t;
+          }
+          __syncthreads();
+          if (threadIdx.x == 0) main_logic(sC, tot, P.epochs);
+          ctl_store(sC, P.ctl);
+        }))
+      return;
+    load_roles(P.ctl, R);
+    if (!R.check) continue;
+
+    // ---- certificate scan (src/solver.cpp:297-317) ----
+    // C1: candidate norms and finiteness.
+    const double* zx = P.xpool + static_cast<size_t>(R.zx_out) * n;
+    const double* xp = P.xpool + static_cast<size_t>(R.xp_out) * n;
+    const double* xa = P.xpool + static_cast<size_t>(R.x_anchor) * n;
+    const double* yc = P.ypool + static_cast<size_t>(R.y_cur) * m;
+    const double* yp = P.ypool + static_cast<size_t>(R.yp_out) * m;
+    const double* ya = P.ypool + static_cast<size_t>(R.y_anchor) * m;
+    {
+      double acc[8];
+      acc_init<8, 0>(acc);
+      const double s = R.cand_scale;
+      for (int j = gtid; j < n; j += gstride) {
+        const double x = ldcg(zx + j);
+        const double vd = ldcg(xp + j) - x;
+        const double vn = s * (x - ldcg(xa + j));
+        acc[0] += vd * vd;
+        acc[2] += vn * vn;
+        acc[4] += isfinite(vd) ? 0.0 : 1.0;
+        acc[6] += isfinite(vn) ? 0.0 : 1.0;
+      }
+      for (int i = gtid; i < m; i += gstride) {
+        const double y = ldcg(yc + i);
+        const double vd = ldcg(yp + i) - y;
+        const double vn = s * (y - ldcg(ya + i));
+        acc[1] += vd * vd;
+        acc[3] += vn * vn;
+        acc[5] += isfinite(vd) ? 0.0 : 1.0;
+        acc[7] += isfinite(vn) ? 0.0 : 1.0;
+      }
+      block_to_slots<8, 0>(acc, P.slots, G);
+    }
+    if (!grid_sync(P, [&] {
+          ctl_load(P.ctl, sC);
+          const int wq = threadIdx.x >> 5;
+          if (wq < 8) {
+            const double t = total_of(P.slots, G, wq, nullptr, 0, 0, false);
+            if (lane == 0) tot[wq] = t;
+          }
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            Roles& RR = sC.r;
+            int any = 0;
+            for (int c = 0; c < 4; ++c) {
+              RR.cn2[c] = sqrt(tot[c]);
+              sC.cfinite[c] = tot[4 + c] == 0.0;
+              const bool normalized = c >= 2;
+              RR.cand_on[c] = (!normalized || sC.last_k >= 1) && RR.cn2[c] > 0.0 && sC.cfinite[c];
+              any |= RR.cand_on[c];
+            }
+            if (!any) scan_logic(sC, P.epochs);  // nothing to validate
+          }
+          ctl_store(sC, P.ctl);
+        }))
+      return;
+    load_roles(P.ctl, R);
+    if (!R.check) continue;
+    // C2: unit vectors u = v / ||v|| and their reductions.
+    {
+      double acc[12];
+      acc_init<12, 0x577u>(acc);
+      const double s = R.cand_scale;
+      double* u0 = P.upool;
+      double* u2 = P.upool + n;
+      double* u1 = P.upool + 2 * static_cast<size_t>(n);
+      double* u3 = u1 + m;
+      for (int j = gtid; j < n; j += gstride) {
+        const double x = ldcg(zx + j);
+        const double cj = __ldg(P.c + j);
+        if (R.cand_on[0]) {
+          const double u = (ldcg(xp + j) - x) / R.cn2[0];
+          u0[j] = u;
+          acc[0] = dmax(acc[0], fabs(u));
+          acc[1] = dmax(acc[1], u);
+          acc[2] = dmax(acc[2], -u);
+          acc[3] += cj * u;
+        }
+        if (R.cand_on[2]) {
+          const double u = (s * (x - ldcg(xa + j))) / R.cn2[2];
+          u2[j] = u;
+          acc[4] = dmax(acc[4], fabs(u));
+          acc[5] = dmax(acc[5], u);
+          acc[6] = dmax(acc[6], -u);
+          acc[7] += cj * u;
+        }
+      }
+      for (int i = gtid; i < m; i += gstride) {
+        const double y = ldcg(yc + i);
+        const double bi = __ldg(P.b + i);
+        if (R.cand_on[1]) {
+          const double u = (ldcg(yp + i) - y) / R.cn2[1];
+          u1[i] = u;
+          acc[8] = dmax(acc[8], fabs(u));
+          acc[9] += bi * u;
+        }
+        if (R.cand_on[3]) {
+          const double u = (s * (y - ldcg(ya + i))) / R.cn2[3];
+          u3[i] = u;
+          acc[10] = dmax(acc[10], fabs(u));
+          acc[11] += bi * u;
+        }
+      }
+      block_to_slots<12, 0x577u>(acc, P.slots, G);
+    }
+    if (!grid_sync(P, [&] {
+          ctl_load(P.ctl, sC);
+          const int wq = threadIdx.x >> 5;
+          if (wq < 12) {
+            const double t = total_of(P.slots, G, wq, nullptr, 0, 0, ((0x577u >> wq) & 1u) != 0);
+            if (lane == 0) tot[wq] = t;
+          }
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            sC.cinf[0] = tot[0], sC.cmax_u[0] = tot[1], sC.cmax_negu[0] = tot[2], sC.cdot[0] = tot[3];
+            sC.cinf[2] = tot[4], sC.cmax_u[2] = tot[5], sC.cmax_negu[2] = tot[6], sC.cdot[2] = tot[7];
+            sC.cinf[1] = tot[8], sC.cdot[1] = tot[9];
+            sC.cinf[3] = tot[10], sC.cdot[3] = tot[11];
+          }
+          ctl_store(sC, P.ctl);
+        }))
+      return;
+    load_roles(P.ctl, R);
+    // C3: the validation SpMVs, up to four independent products.
+    {
+      double acc[6];
+      acc_init<6, 0x3Fu>(acc);
+      const double* u0 = P.upool;
+      const double* u2 = P.upool + n;
+      const double* u1 = P.upool + 2 * static_cast<size_t>(n);
+      const double* u3 = u1 + m;
+      if (R.cand_on[1]) {
+        double a2[2];
+        acc_init<2, 3u>(a2);
+        EpiPosNeg e;
+        spmv_rows<2, 3u>(P.AT, 0, SrcVec{u1}, e, a2, gwarp, lane);
+        acc[0] = a2[0], acc[1] = a2[1];
+      }
+      if (R.cand_on[3]) {
+        double a2[2];
+        acc_init<2, 3u>(a2);
+        EpiPosNeg e;
+        spmv_rows<2, 3u>(P.AT, 1, SrcVec{u3}, e, a2, gwarp, lane);
+        acc[2] = a2[0], acc[3] = a2[1];
+      }
+      if (R.cand_on[0]) {
+        double a1[1];
+        acc_init<1, 1u>(a1);
+        EpiAbs e;
+        spmv_rows<1, 1u>(P.A, 0, SrcVec{u0}, e, a1, gwarp, lane);
+        acc[4] = a1[0];
+      }
+      if (R.cand_on[2]) {
+        double a1[1];
+        acc_init<1, 1u>(a1);
+        EpiAbs e;
+        spmv_rows<1, 1u>(P.A, 1, SrcVec{u2}, e, a1, gwarp, lane);
+        acc[5] = a1[0];
+      }
+      block_to_slots<6, 0x3Fu>(acc, P.slots, G);
+    }
+    if (!grid_sync(P, [&] {
+          ctl_load(P.ctl, sC);
+          const int wq = threadIdx.x >> 5;
+          if (wq < 6) {
+            const Sched& S = wq < 4 ? P.AT : P.A;
+            const int set = wq < 4 ? (wq >> 1) : (wq - 4);
+            const int lq = wq < 4 ? (wq & 1) : 0;
+            const double t = total_of(P.slots, G, wq, S.long_terms[set], S.n_long, lq, true);
+            if (lane == 0) tot[wq] = t;
+          }
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            sC.cmax_at[1] = tot[0], sC.cmax_negat[1] = tot[1];
+            sC.cmax_at[3] = tot[2], sC.cmax_negat[3] = tot[3];
+            sC.cmax_abs_au[0] = tot[4], sC.cmax_abs_au[2] = tot[5];
+            scan_logic(sC, P.epochs);
+          }
+          ctl_store(sC, P.ctl);
+        }))
+      return;
+    load_roles(P.ctl, R);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Standalone kernels (setup, boundary SpMVs, results)
+// ---------------------------------------------------------------------------
+struct EpiStore {
+  double* out;
+  __device__ __forceinline__ void apply(int r, double s, double (&t)[1]) const {
+    out[r] = s;
+    t[0] = 0.0;
+  }
+};
+
+__global__ void __launch_bounds__(kThreads, 2) spmv_store_kernel(Sched S, const double* x, double* out) {
+  double acc[1];
+  acc_init<1, 0>(acc);
+  EpiStore e{out};
+  spmv_rows<1, 0>(S, 0, SrcVec{x}, e, acc, blockIdx.x * kWarps + (threadIdx.x >> 5), threadIdx.x & 31);
+}
+
+__global__ void combine_kernel(int len, double w, const double* a, const double* b, double* out) {
+  const double omw = 1.0 - w;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x)
+    out[i] = omw * a[i] + w * b[i];
+}
+
+// make_certificate, src/solver.cpp:89-101: (s / ||raw||) * raw, raw rebuilt
+// from the iterate buffers exactly as the scan formed it.
+__global__ void cert_kernel(int len, int normalized, double scale, double factor, const double* p,
+                            const double* q, double* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) {
+    const double raw = normalized ? scale * (p[i] - q[i]) : q[i] - p[i];
+    out[i] = factor * raw;
+  }
+}
+
+// Fixed-order sums of squares / products for setup norms and kkt_current.
+// which: 0 -> ||v||^2 ; 1 -> KKT partials (needs ax, b, aty, c, x, y).
+__global__ void __launch_bounds__(kThreads, 2)
+kkt_partials_kernel(int m, int n, const double* ax, const double* b, const double* aty,
+                    const double* c, const double* x, const double* y, double* slots) {
+  double acc[6];
+  acc_init<6, 0>(acc);
+  const int gtid = blockIdx.x * kThreads + threadIdx.x, gs = gridDim.x * kThreads;
+  for (int i = gtid; i < m; i += gs) {
+    const double bi = b[i];
+    if (ax) {
+      const double d = ax[i] - bi;
+      acc[0] += d * d;
+      acc[3] += bi * y[i];
+    }
+    acc[4] += bi * bi;
+  }
+  for (int j = gtid; j < n; j += gs) {
+    const double cj = c[j];
+    if (aty) {
+      double r = -(cj + aty[j]);
+      r = r < 0.0 ? 0.0 : r;
+      acc[1] += r * r;
+      acc[2] += cj * x[j];
+    }
+    acc[5] += cj * cj;
+  }
+  block_to_slots<6, 0>(acc, slots, gridDim.x);
+}
+
+__global__ void final_reduce_kernel(const double* slots, int grid, int q_count, double* out) {
+  const int wq = threadIdx.x >> 5;
+  for (int q = wq; q < q_count; q += blockDim.x / 32) {
+    const double t = warp_reduce_strided(slots + q * grid, grid, 1, false);
+    if ((threadIdx.x & 31) == 0) out[q] = t;
+  }
+}
+
+// Device-side CSR validation (src/sparse_matrix.cpp:27-53): flags
+// 1 out-of-range column, 2 non-finite value, 4 unsorted row, 8 duplicate,
+// 16 non-monotone row pointer.
+__global__ void validate_kernel(int m, int n, const long long* rp, const int* ci, const double* v,
+                                unsigned* flags) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const long long p0 = rp[i], p1 = rp[i + 1];
+    unsigned f = 0;
+    if (p1 < p0) f |= 16u;
+    for (long long p = p0; p < p1; ++p) {
+      const int col = ci[p];
+      if (col < 0 || col >= n) f |= 1u;
+      if (!isfinite(v[p])) f |= 2u;
+      if (p > p0) {
+        if (col < ci[p - 1]) f |= 4u;
+        if (col == ci[p - 1]) f |= 8u;
+      }
+    }
+    if (f) atomicOr(flags, f);
+  }
+}
+
+__global__ void narrow_ptr_kernel(int len, const long long* src, int* dst) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x)
+    dst[i] = static_cast<int>(src[i]);
+}
+
+__global__ void row_of_kernel(int m, const int* rp, int* row_of, int* iota) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    for (int p = rp[i]; p < rp[i + 1]; ++p) {
+      row_of[p] = i;
+      iota[p] = p;
+    }
+}
+
+__global__ void col_count_kernel(int nnz, const int* ci, int* count) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += gridDim.x * blockDim.x)
+    atomicAdd(count + ci[p], 1);
+}
+
+__global__ void gather_t_kernel(int nnz, const int* perm, const int* row_of, const double* val, int* t_idx,
+                                double* t_val) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += gridDim.x * blockDim.x) {
+    const int p = perm[k];
+    t_idx[k] = row_of[p];
+    t_val[k] = val[p];
+  }
+}
+
+}  // namespace hx
+
+// ===========================================================================
+// Host side
+// ===========================================================================
+using namespace hx;
+
+namespace {
+
+struct DevSched {
+  int4* tasks = nullptr;
+  int* task_ptr = nullptr;
+  Piece* pieces = nullptr;
+  int* piece_ptr = nullptr;
+  double* part = nullptr;    // 2 * n_slots
+  unsigned* cnt = nullptr;   // 2 * n_long
+  double* terms = nullptr;   // 2 * n_long * kMaxQ
+  Sched view;
+  double max_cost = 0, mean_cost = 0;
+};
+
+}  // namespace
+
+struct hx_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int sm_count = 0;
+  int grid = 0;
+  std::string err;
+  int64_t m = 0, n = 0, nnz = 0;
+  bool uploaded = false, setup_done = false;
+  int64_t launches = 0;
+  // device data
+  int* a_ptr = nullptr;
+  int* a_idx = nullptr;
+  double* a_val = nullptr;
+  int* t_ptr = nullptr;
+  int* t_idx = nullptr;
+  double* t_val = nullptr;
+  double* b = nullptr;
+  double* c = nullptr;
+  DevSched sa, st;
+  double* xpool = nullptr;
+  double* ypool = nullptr;
+  double* axpool = nullptr;
+  double* upool = nullptr;
+  double* slots = nullptr;
+  double* scratch = nullptr;  // kMaxQ doubles
+  Ctl* ctl = nullptr;
+  GridBar* bar = nullptr;
+  hplp_epoch_t* epochs = nullptr;
+  Ctl h;  // host mirror
+  double b_norm = 0, c_norm = 0;
+};
+
+namespace {
+
+thread_local std::string g_create_err;
+
+int set_err(hx_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  else g_create_err = msg;
+  return code;
+}
+
+#define HX_CUDA(ctx, expr)                                                                    \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return set_err(ctx, e_ == cudaErrorMemoryAllocation ? HPLP_ENOMEM : HPLP_ECUDA,         \
+                     std::string(#expr) + ": " + cudaGetErrorString(e_));                     \
+  } while (0)
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t count) {
+  return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T));
+}
+
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+void free_sched(DevSched& s) {
+  dfree(s.tasks), dfree(s.task_ptr), dfree(s.pieces), dfree(s.piece_ptr);
+  dfree(s.part), dfree(s.cnt), dfree(s.terms);
+  s = DevSched{};
+}
+
+void free_problem(hx_ctx* c) {
+  dfree(c->a_ptr), dfree(c->a_idx), dfree(c->a_val), dfree(c->t_ptr), dfree(c->t_idx), dfree(c->t_val);
+  dfree(c->b), dfree(c->c), dfree(c->xpool), dfree(c->ypool), dfree(c->axpool), dfree(c->upool);
+  free_sched(c->sa);
+  free_sched(c->st);
+  c->a_ptr = c->a_idx = c->t_ptr = c->t_idx = nullptr;
+  c->a_val = c->t_val = c->b = c->c = c->xpool = c->ypool = c->axpool = c->upool = nullptr;
+  c->uploaded = c->setup_done = false;
+}
+
+int upload_sched(hx_ctx* ctx, DevSched& d, const int* ptr_host, int rows, int cols, const int* dptr,
+                 const int* didx, const double* dval) {
+  SchedHost h = build_schedule(ptr_host, rows, ctx->grid * kWarps);
+  HX_CUDA(ctx, dalloc(&d.tasks, h.tasks.size()));
+  HX_CUDA(ctx, dalloc(&d.task_ptr, h.task_ptr.size()));
+  HX_CUDA(ctx, dalloc(&d.pieces, h.pieces.size()));
+  HX_CUDA(ctx, dalloc(&d.piece_ptr, h.piece_ptr.size()));
+  HX_CUDA(ctx, dalloc(&d.part, 2 * static_cast<size_t>(h.n_slots)));
+  HX_CUDA(ctx, dalloc(&d.cnt, 2 * static_cast<size_t>(h.n_long)));
+  HX_CUDA(ctx, dalloc(&d.terms, 2 * static_cast<size_t>(h.n_long) * kMaxQ));
+  auto cp = [&](void* dst, const void* src, size_t bytes) {
+    return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream) : cudaSuccess;
+  };
+  HX_CUDA(ctx, cp(d.tasks, h.tasks.data(), h.tasks.size() * sizeof(int4)));
+  HX_CUDA(ctx, cp(d.task_ptr, h.task_ptr.data(), h.task_ptr.size() * sizeof(int)));
+  HX_CUDA(ctx, cp(d.pieces, h.pieces.data(), h.pieces.size() * sizeof(Piece)));
+  HX_CUDA(ctx, cp(d.piece_ptr, h.piece_ptr.data(), h.piece_ptr.size() * sizeof(int)));
+  HX_CUDA(ctx, cudaMemsetAsync(d.cnt, 0, std::max<size_t>(1, 2 * static_cast<size_t>(h.n_long)) * sizeof(unsigned),
+                               ctx->stream));
+  HX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // host vectors go out of scope
+  Sched& v = d.view;
+  v.rows = rows;
+  v.cols = cols;
+  v.ptr = dptr;
+  v.idx = didx;
+  v.val = dval;
+  v.tasks = d.tasks;
+  v.task_ptr = d.task_ptr;
+  v.pieces = d.pieces;
+  v.piece_ptr = d.piece_ptr;
+  v.n_long = h.n_long;
+  for (int s = 0; s < 2; ++s) {
+    v.piece_part[s] = d.part + static_cast<size_t>(s) * h.n_slots;
+    v.piece_cnt[s] = d.cnt + static_cast<size_t>(s) * h.n_long;
+    v.long_terms[s] = d.terms + static_cast<size_t>(s) * h.n_long * kMaxQ;
+  }
+  d.max_cost = h.max_warp_cost;
+  d.mean_cost = h.mean_warp_cost;
+  return HPLP_OK;
+}
+
+KParams params(hx_ctx* c) {
+  KParams P;
+  P.A = c->sa.view;
+  P.AT = c->st.view;
+  P.m = static_cast<int>(c->m);
+  P.n = static_cast<int>(c->n);
+  P.b = c->b;
+  P.c = c->c;
+  P.xpool = c->xpool;
+  P.ypool = c->ypool;
+  P.axpool = c->axpool;
+  P.upool = c->upool;
+  P.slots = c->slots;
+  P.ctl = c->ctl;
+  P.bar = c->bar;
+  P.epochs = c->epochs;
+  return P;
+}
+
+int launch_loop(hx_ctx* c) {
+  KParams P = params(c);
+  void* args[] = {&P};
+  HX_CUDA(c, cudaMemcpyAsync(c->ctl, &c->h, sizeof(Ctl), cudaMemcpyHostToDevice, c->stream));
+  HX_CUDA(c, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(loop_kernel), dim3(c->grid), dim3(kThreads),
+                                         args, 0, c->stream));
+  c->launches += 1;
+  HX_CUDA(c, cudaMemcpyAsync(&c->h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
+  GridBar gb;
+  HX_CUDA(c, cudaMemcpyAsync(&gb, c->bar, sizeof(GridBar), cudaMemcpyDeviceToHost, c->stream));
+  HX_CUDA(c, cudaStreamSynchronize(c->stream));
+  HX_CUDA(c, cudaGetLastError());
+  if (gb.abort) {
+    cudaMemsetAsync(c->bar, 0, sizeof(GridBar), c->stream);
+    cudaStreamSynchronize(c->stream);
+    return set_err(c, HPLP_ETIMEOUT, "hx: grid barrier watchdog fired (device hang avoided)");
+  }
+  return HPLP_OK;
+}
+
+int spmv_dev(hx_ctx* c, bool transpose, const double* x, double* out) {
+  const Sched& S = transpose ? c->st.view : c->sa.view;
+  spmv_store_kernel<<<c->grid, kThreads, 0, c->stream>>>(S, x, out);
+  c->launches += 1;
+  HX_CUDA(c, cudaGetLastError());
+  return HPLP_OK;
+}
+
+double* xbuf(hx_ctx* c, int i) { return c->xpool + static_cast<size_t>(i) * c->n; }
+double* ybuf(hx_ctx* c, int i) { return c->ypool + static_cast<size_t>(i) * c->m; }
+double* axbuf(hx_ctx* c, int i) { return c->axpool + static_cast<size_t>(i) * c->m; }
+
+void fill_progress(hx_ctx* c, hx_progress_t* p) {
+  if (!p) return;
+  const Ctl& C = c->h;
+  p->it = C.it;
+  p->n = C.n;
+  p->k = C.k;
+  p->spmv_count = C.spmv;
+  p->status = C.status;
+  p->error = C.error;
+  p->paused = C.paused;
+  p->best_valid = C.best_kkt < std::numeric_limits<double>::infinity();
+  p->res_epoch_start = C.res_epoch_start;
+  p->best_kkt = C.best_kkt;
+  p->best_err = {C.best_err[0], C.best_err[1], C.best_err[2], C.best_err[3]};
+  p->trace_it = C.last_it;
+  p->trace_n = C.last_n;
+  p->trace_k = C.last_k;
+  p->trace_res = C.last_res;
+  p->trace_kkt = {C.last_kkt[0], C.last_kkt[1], C.last_kkt[2], C.last_kkt[3]};
+  p->final_kkt = {C.final_kkt[0], C.final_kkt[1], C.final_kkt[2], C.final_kkt[3]};
+  p->n_epochs = C.n_epochs;
+  p->primal_cert = C.cert[0];
+  p->dual_cert = C.cert[1];
+}
+
+}  // namespace
+
+extern "C" {
+
+int hx_create(int32_t device, hx_ctx** out) {
+  *out = nullptr;
+  auto ctx = std::make_unique<hx_ctx>();
+  ctx->device = device;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_err(nullptr, HPLP_ECUDA, "hx_create: no CUDA device visible (the B200 path has no CPU fallback)");
+  if (device < 0 || device >= ndev) return set_err(nullptr, HPLP_EINVAL, "hx_create: bad device index");
+  hx_ctx* c = ctx.get();
+  HX_CUDA(nullptr, cudaSetDevice(device));
+  cudaDeviceProp prop;
+  HX_CUDA(nullptr, cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return set_err(nullptr, HPLP_ECUDA, "hx_create: this build targets sm_100a (B200); found sm_" +
+                                            std::to_string(prop.major * 10 + prop.minor));
+  if (!prop.cooperativeLaunch) return set_err(nullptr, HPLP_ECUDA, "hx_create: cooperative launch unsupported");
+  c->sm_count = prop.multiProcessorCount;
+  int occ = 0;
+  HX_CUDA(nullptr, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, loop_kernel, kThreads, 0));
+  if (occ < 1) return set_err(nullptr, HPLP_ECUDA, "hx_create: loop kernel does not fit on an SM");
+  c->grid = c->sm_count * std::min(occ, 2);
+  HX_CUDA(nullptr, cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  HX_CUDA(nullptr, cudaEventCreate(&c->ev0));
+  HX_CUDA(nullptr, cudaEventCreate(&c->ev1));
+  HX_CUDA(nullptr, dalloc(&c->slots, static_cast<size_t>(kMaxQ) * c->grid));
+  HX_CUDA(nullptr, dalloc(&c->scratch, kMaxQ));
+  HX_CUDA(nullptr, dalloc(&c->ctl, 1));
+  HX_CUDA(nullptr, dalloc(&c->bar, 1));
+  HX_CUDA(nullptr, dalloc(&c->epochs, kEpochCap));
+  HX_CUDA(nullptr, cudaMemset(c->bar, 0, sizeof(GridBar)));
+  HX_CUDA(nullptr, cudaMemset(c->ctl, 0, sizeof(Ctl)));
+  std::memset(&c->h, 0, sizeof(Ctl));
+  *out = ctx.release();
+  return HPLP_OK;
+}
+
+void hx_destroy(hx_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  free_problem(c);
+  dfree(c->slots), dfree(c->scratch), dfree(c->ctl), dfree(c->bar), dfree(c->epochs);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* hx_last_error(hx_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+int hx_device_info(hx_ctx* c, int32_t* sm_count, int32_t* grid_ctas, int32_t* cta_threads) {
+  if (sm_count) *sm_count = c->sm_count;
+  if (grid_ctas) *grid_ctas = c->grid;
+  if (cta_threads) *cta_threads = kThreads;
+  return HPLP_OK;
+}
+
+void* hx_stream(hx_ctx* c) { return c->stream; }
+int64_t hx_launch_count(hx_ctx* c) { return c->launches; }
+
+int hx_dims(hx_ctx* c, int64_t* m, int64_t* n, int64_t* nnz) {
+  if (m) *m = c->m;
+  if (n) *n = c->n;
+  if (nnz) *nnz = c->nnz;
+  return c->uploaded ? HPLP_OK : set_err(c, HPLP_ESTATE, "hx_dims: no problem uploaded");
+}
+
+int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                  const double* val, const double* b, const double* cc) {
+  HX_CUDA(c, cudaSetDevice(c->device));
+  free_problem(c);
+  if (m < 0 || n < 0) return set_err(c, HPLP_EINVAL, "SparseMatrix: negative dimension");
+  if (row_ptr[0] != 0) return set_err(c, HPLP_EINVAL, "hx_upload_csr: row_ptr[0] must be 0");
+  const int64_t nnz = row_ptr[m];
+  if (nnz < 0 || nnz >= (int64_t{1} << 31) || m >= (int64_t{1} << 31) - 1 || n >= (int64_t{1} << 31) - 1)
+    return set_err(c, HPLP_EINVAL, "hx_upload_csr: sizes exceed the int32 index range of this build");
+  for (int64_t i = 0; i < m; ++i)
+    if (!std::isfinite(b[i])) return set_err(c, HPLP_EINVAL, "StandardFormLP: non-finite b or c");
+  for (int64_t j = 0; j < n; ++j)
+    if (!std::isfinite(cc[j])) return set_err(c, HPLP_EINVAL, "StandardFormLP: non-finite b or c");
+  c->m = m, c->n = n, c->nnz = nnz;
+  cudaStream_t s = c->stream;
+  const int nblk = 4 * c->sm_count;
+  // Matrix A (CSR), validated on the device.
+  long long* rp64 = nullptr;
+  unsigned* flags = nullptr;
+  HX_CUDA(c, dalloc(&rp64, m + 1));
+  HX_CUDA(c, dalloc(&flags, 1));
+  HX_CUDA(c, dalloc(&c->a_ptr, m + 1));
+  HX_CUDA(c, dalloc(&c->a_idx, nnz));
+  HX_CUDA(c, dalloc(&c->a_val, nnz));
+  HX_CUDA(c, dalloc(&c->b, m));
+  HX_CUDA(c, dalloc(&c->c, n));
+  HX_CUDA(c, cudaMemcpyAsync(rp64, row_ptr, (m + 1) * sizeof(long long), cudaMemcpyHostToDevice, s));
+  if (nnz) {
+    HX_CUDA(c, cudaMemcpyAsync(c->a_idx, col_idx, nnz * sizeof(int), cudaMemcpyHostToDevice, s));
+    HX_CUDA(c, cudaMemcpyAsync(c->a_val, val, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+  }
+  if (m) HX_CUDA(c, cudaMemcpyAsync(c->b, b, m * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (n) HX_CUDA(c, cudaMemcpyAsync(c->c, cc, n * sizeof(double), cudaMemcpyHostToDevice, s));
+  HX_CUDA(c, cudaMemsetAsync(flags, 0, sizeof(unsigned), s));
+  validate_kernel<<<nblk, 256, 0, s>>>(static_cast<int>(m), static_cast<int>(n), rp64, c->a_idx, c->a_val, flags);
+  narrow_ptr_kernel<<<nblk, 256, 0, s>>>(static_cast<int>(m + 1), rp64, c->a_ptr);
+  unsigned hflags = 0;
+  HX_CUDA(c, cudaMemcpyAsync(&hflags, flags, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+  HX_CUDA(c, cudaStreamSynchronize(s));
+  dfree(rp64);
+  dfree(flags);
+  c->launches += 2;
+  if (hflags & 16u) return set_err(c, HPLP_EINVAL, "hx_upload_csr: row_ptr is not monotone");
+  if (hflags & 1u) return set_err(c, HPLP_EINVAL, "SparseMatrix: entry out of range");
+  if (hflags & 2u) return set_err(c, HPLP_EINVAL, "SparseMatrix: non-finite value");
+  if (hflags & 8u) return set_err(c, HPLP_EINVAL, "SparseMatrix: duplicate entry");
+  if (hflags & 4u)
+    return set_err(c, HPLP_EINVAL, "hx_upload_csr: columns must ascend within each row (sort on the host)");
+  // Explicit A^T with ascending rows per column: stable radix sort by column.
+  {
+    int *row_of = nullptr, *iota = nullptr, *keys_out = nullptr, *perm = nullptr, *cnt = nullptr;
+    HX_CUDA(c, dalloc(&row_of, nnz));
+    HX_CUDA(c, dalloc(&iota, nnz));
+    HX_CUDA(c, dalloc(&keys_out, nnz));
+    HX_CUDA(c, dalloc(&perm, nnz));
+    HX_CUDA(c, dalloc(&cnt, n + 1));
+    HX_CUDA(c, dalloc(&c->t_ptr, n + 1));
+    HX_CUDA(c, dalloc(&c->t_idx, nnz));
+    HX_CUDA(c, dalloc(&c->t_val, nnz));
+    row_of_kernel<<<nblk, 256, 0, s>>>(static_cast<int>(m), c->a_ptr, row_of, iota);
+    int bits = 1;
+    while ((int64_t{1} << bits) < n + 1) ++bits;
+    size_t tmp_bytes = 0, scan_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, c->a_idx, keys_out, iota, perm, static_cast<int>(nnz), 0,
+                                    bits, s);
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, cnt, c->t_ptr, static_cast<int>(n + 1), s);
+    void* tmp = nullptr;
+    HX_CUDA(c, cudaMalloc(&tmp, std::max<size_t>(1, std::max(tmp_bytes, scan_bytes))));
+    if (nnz)
+      HX_CUDA(c, cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, c->a_idx, keys_out, iota, perm,
+                                                 static_cast<int>(nnz), 0, bits, s));
+    HX_CUDA(c, cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(int), s));
+    col_count_kernel<<<nblk, 256, 0, s>>>(static_cast<int>(nnz), c->a_idx, cnt);
+    HX_CUDA(c, cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, cnt, c->t_ptr, static_cast<int>(n + 1), s));
+    gather_t_kernel<<<nblk, 256, 0, s>>>(static_cast<int>(nnz), perm, row_of, c->a_val, c->t_idx, c->t_val);
+    HX_CUDA(c, cudaStreamSynchronize(s));
+    HX_CUDA(c, cudaGetLastError());
+    c->launches += 5;
+    dfree(tmp), dfree(row_of), dfree(iota), dfree(keys_out), dfree(perm), dfree(cnt);
+  }
+  // Schedules (host, from the pointer arrays).
+  {
+    std::vector<int> ph(static_cast<size_t>(m) + 1), pt(static_cast<size_t>(n) + 1);
+    for (int64_t i = 0; i <= m; ++i) ph[i] = static_cast<int>(row_ptr[i]);
+    HX_CUDA(c, cudaMemcpy(pt.data(), c->t_ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+    int rc = upload_sched(c, c->sa, ph.data(), static_cast<int>(m), static_cast<int>(n), c->a_ptr, c->a_idx,
+                          c->a_val);
+    if (rc) return rc;
+    rc = upload_sched(c, c->st, pt.data(), static_cast<int>(n), static_cast<int>(m), c->t_ptr, c->t_idx, c->t_val);
+    if (rc) return rc;
+  }
+  HX_CUDA(c, dalloc(&c->xpool, static_cast<size_t>(kXPool) * n));
+  HX_CUDA(c, dalloc(&c->ypool, static_cast<size_t>(kYPool) * m));
+  HX_CUDA(c, dalloc(&c->axpool, static_cast<size_t>(kAxPool) * m));
+  HX_CUDA(c, dalloc(&c->upool, 2 * static_cast<size_t>(n) + 2 * static_cast<size_t>(m)));
+  // ||b||, ||c|| once (loop invariants of src/pdhg_core.cpp:60,62).
+  kkt_partials_kernel<<<c->grid, kThreads, 0, s>>>(static_cast<int>(m), static_cast<int>(n), nullptr, c->b,
+                                                   nullptr, c->c, nullptr, nullptr, c->slots);
+  final_reduce_kernel<<<1, 256, 0, s>>>(c->slots, c->grid, 6, c->scratch);
+  double tot[6];
+  HX_CUDA(c, cudaMemcpyAsync(tot, c->scratch, sizeof(tot), cudaMemcpyDeviceToHost, s));
+  HX_CUDA(c, cudaStreamSynchronize(s));
+  c->launches += 2;
+  c->b_norm = std::sqrt(tot[4]);
+  c->c_norm = std::sqrt(tot[5]);
+  c->uploaded = true;
+  return HPLP_OK;
+}
+
+int hx_spmv(hx_ctx* c, const double* x, double* out) {
+  if (!c->uploaded) return set_err(c, HPLP_ESTATE, "hx_spmv: no problem uploaded");
+  double* dx = c->upool;
+  double* dout = c->upool + 2 * c->n;
+  HX_CUDA(c, cudaMemcpyAsync(dx, x, c->n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  int rc = spmv_dev(c, false, dx, dout);
+  if (rc) return rc;
+  HX_CUDA(c, cudaMemcpyAsync(out, dout, c->m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  HX_CUDA(c, cudaStreamSynchronize(c->stream));
+  return HPLP_OK;
+}
+
+int hx_spmv_transpose(hx_ctx* c, const double* y, double* out) {
+  if (!c->uploaded) return set_err(c, HPLP_ESTATE, "hx_spmv_transpose: no problem uploaded");
+  double* dy = c->upool + 2 * c->n;
+  double* dout = c->upool;
+  HX_CUDA(c, cudaMemcpyAsync(dy, y, c->m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  int rc = spmv_dev(c, true, dy, dout);
+  if (rc) return rc;
+  HX_CUDA(c, cudaMemcpyAsync(out, dout, c->n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  HX_CUDA(c, cudaStreamSynchronize(c->stream));
+  return HPLP_OK;
+}
+
+int hx_power_iteration(hx_ctx* c, const double* x0, double tol, int64_t k0, int64_t max_iters, double sigma_prev,
+                       double* sigma, int64_t* iters, int32_t* converged, int32_t* need_redraw) {
+  if (!c->uploaded) return set_err(c, HPLP_ESTATE, "hx_power_iteration: no problem uploaded");
+  HX_CUDA(c, cudaMemcpyAsync(xbuf(c, 0), x0, c->n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  Ctl& C = c->h;
+  std::memset(&C, 0, sizeof(Ctl));
+  C.mode = kModePower;
+  C.pw_k = k0;
+  C.pw_max = max_iters;
+  C.pw_tol = tol;
+  C.pw_sigma_prev = sigma_prev;
+  C.pw_sigma = sigma_prev;  // res.sigma == sigma_prev between iterations
+  C.pw_iters = k0;
+  C.r.pw_mode = 0;
+  C.r.stop = k0 >= max_iters ? 1 : 0;
+  if (!C.r.stop) {
+    int rc = launch_loop(c);
+    if (rc) return rc;
+  }
+  *sigma = C.pw_sigma;
+  *iters = C.pw_iters;
+  *converged = C.pw_converged;
+  *need_redraw = C.pw_redraw;
+  c->setup_done = false;
+  return HPLP_OK;
+}
+
+int hx_setup(hx_ctx* c, const hplp_config_t* cfg, double sigma_used, double eta, const double* x0,
+             const double* y0) {
+  if (!c->uploaded) return set_err(c, HPLP_ESTATE, "hx_setup: no problem uploaded");
+  cudaStream_t s = c->stream;
+  if (x0) HX_CUDA(c, cudaMemcpyAsync(xbuf(c, 0), x0, c->n * sizeof(double), cudaMemcpyHostToDevice, s));
+  else HX_CUDA(c, cudaMemsetAsync(xbuf(c, 0), 0, c->n * sizeof(double), s));
+  if (y0) HX_CUDA(c, cudaMemcpyAsync(ybuf(c, 0), y0, c->m * sizeof(double), cudaMemcpyHostToDevice, s));
+  else HX_CUDA(c, cudaMemsetAsync(ybuf(c, 0), 0, c->m * sizeof(double), s));
+  int rc = spmv_dev(c, false, xbuf(c, 0), axbuf(c, 0));  // a_x = A x, src/solver.cpp:213
+  if (rc) return rc;
+  Ctl& C = c->h;
+  std::memset(&C, 0, sizeof(Ctl));
+  C.mode = kModeLoop;
+  C.iteration_limit = cfg->iteration_limit;
+  C.check_period = cfg->infeasibility_check_period;
+  C.stall_cap = cfg->adaptive_stall_cap;
+  C.k_star = cfg->k_star;
+  C.tau0 = cfg->tau0;
+  C.trace_period = cfg->trace_period;
+  C.restart_kind = cfg->restart_kind;
+  C.tol = cfg->tolerance;
+  C.cert_tol = cfg->certificate_tolerance;
+  C.beta = cfg->beta;
+  C.sigma_used = sigma_used;
+  C.b_norm = c->b_norm;
+  C.c_norm = c->c_norm;
+  C.time_limit_s = cfg->time_limit_seconds;
+  C.t0_ns = 0;
+  C.best_kkt = std::numeric_limits<double>::infinity();
+  C.x_best = C.y_best = -1;
+  C.status = -1;
+  C.final_x = C.final_y = -1;
+  C.cert_cand[0] = C.cert_cand[1] = -1;
+  Roles& R = C.r;
+  R.eta = eta;
+  R.x_src = 0, R.x_anchor = 0, R.x_mode = 0, R.w_x = 0.0;
+  R.zx_out = 1, R.xp_out = 2;
+  R.y_cur = 0, R.y_anchor = 0, R.yp_out = 1, R.yc_out = 2;
+  R.ax_cur = 0, R.ax_anchor = 0, R.axp_out = 1, R.axc_out = 2;
+  R.w_next = 0.5;  // 1/(k+2) at k = 0
+  R.stop = 0;
+  HX_CUDA(c, cudaMemsetAsync(c->epochs, 0, kEpochCap * sizeof(hplp_epoch_t), s));
+  HX_CUDA(c, cudaStreamSynchronize(s));
+  c->setup_done = true;
+  return HPLP_OK;
+}
+
+int hx_run(hx_ctx* c, int64_t max_iters, hx_progress_t* p) {
+  if (!c->setup_done) return set_err(c, HPLP_ESTATE, "hx_run: call hx_setup first");
+  Ctl& C = c->h;
+  const int64_t launches0 = c->launches;
+  float ms = 0.f;
+  if (C.status < 0 && C.error == 0 && max_iters > 0) {
+    if (C.it >= C.iteration_limit) {
+      // src/solver.cpp:242-248 before any iteration of this call
+      C.status = HPLP_STATUS_ITERATION_LIMIT;
+      if (C.best_kkt < std::numeric_limits<double>::infinity()) {
+        C.final_x = C.x_best, C.final_y = C.y_best;
+        std::memcpy(C.final_kkt, C.best_err, sizeof(C.final_kkt));
+      } else {
+        C.final_x = C.final_y = -1;
+      }
+    } else {
+      C.batch_end = C.it + max_iters;
+      C.r.stop = 0;
+      C.paused = 0;
+      HX_CUDA(c, cudaEventRecord(c->ev0, c->stream));
+      int rc = launch_loop(c);
+      if (rc) return rc;
+      HX_CUDA(c, cudaEventRecord(c->ev1, c->stream));
+      HX_CUDA(c, cudaEventSynchronize(c->ev1));
+      HX_CUDA(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    }
+  }
+  fill_progress(c, p);
+  if (p) {
+    p->device_ms = ms;
+    p->launches = c->launches - launches0;
+  }
+  if (C.error == HPLP_EDOMAIN)
+    return set_err(c, HPLP_EDOMAIN, "canonical norm: quadratic form is negative (eta too large for this matrix)");
+  return HPLP_OK;
+}
+
+int hx_progress(hx_ctx* c, hx_progress_t* p) {
+  fill_progress(c, p);
+  return HPLP_OK;
+}
+
+int hx_epochs(hx_ctx* c, int64_t first, int64_t count, hplp_epoch_t* out) {
+  if (count <= 0) return HPLP_OK;
+  if (first < c->h.n_epochs - kEpochCap) return set_err(c, HPLP_ESTATE, "hx_epochs: entries already overwritten");
+  for (int64_t e = 0; e < count; ++e) {
+    const int64_t slot = (first + e) % kEpochCap;
+    HX_CUDA(c, cudaMemcpyAsync(out + e, c->epochs + slot, sizeof(hplp_epoch_t), cudaMemcpyDeviceToHost, c->stream));
+  }
+  HX_CUDA(c, cudaStreamSynchronize(c->stream));
+  return HPLP_OK;
+}
+
+int hx_get_iterate(hx_ctx* c, int32_t which, double* x, double* y) {
+  if (!c->setup_done) return set_err(c, HPLP_ESTATE, "hx_get_iterate: no solve state");
+  const Ctl& C = c->h;
+  const double* dx = nullptr;
+  const double* dy = nullptr;
+  cudaStream_t s = c->stream;
+  switch (which) {
+    case HX_ITERATE_BEST:
+      if (C.x_best < 0) return set_err(c, HPLP_ESTATE, "hx_get_iterate: no best iterate yet");
+      dx = xbuf(c, C.x_best), dy = ybuf(c, C.y_best);
+      break;
+    case HX_ITERATE_LAST:
+      if (C.it == 0 && C.status < 0) return set_err(c, HPLP_ESTATE, "hx_get_iterate: no iteration completed");
+      dx = xbuf(c, C.last_zx), dy = ybuf(c, C.last_y);
+      break;
+    case HX_ITERATE_NEXT:
+      dx = xbuf(c, C.last_xp), dy = ybuf(c, C.last_yp);
+      break;
+    default: {  // the iterate the next iteration starts from
+      if (C.status >= 0 && C.final_x >= 0) {
+        dx = xbuf(c, C.final_x), dy = ybuf(c, C.final_y);
+      } else if (C.r.x_mode == 0) {
+        dx = xbuf(c, C.r.x_src), dy = ybuf(c, C.r.y_cur);
+      } else {
+        double* tmp = c->upool;
+        combine_kernel<<<4 * c->sm_count, 256, 0, s>>>(static_cast<int>(c->n), C.r.w_x, xbuf(c, C.r.x_src),
+                                                       xbuf(c, C.r.x_anchor), tmp);
+        c->launches += 1;
+        dx = tmp, dy = ybuf(c, C.r.y_cur);
+      }
+    }
+  }
+  if (x && c->n) HX_CUDA(c, cudaMemcpyAsync(x, dx, c->n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (y && c->m) HX_CUDA(c, cudaMemcpyAsync(y, dy, c->m * sizeof(double), cudaMemcpyDeviceToHost, s));
+  HX_CUDA(c, cudaStreamSynchronize(s));
+  return HPLP_OK;
+}
+
+int hx_get_certificate(hx_ctx* c, int32_t kind, double* vec) {
+  const Ctl& C = c->h;
+  if (kind < 0 || kind > 1 || !C.cert[kind].present)
+    return set_err(c, HPLP_ESTATE, "hx_get_certificate: no such certificate");
+  const int cand = C.cert_cand[kind];
+  const bool normalized = cand >= 2;
+  const bool is_x = (cand == 0 || cand == 2);
+  const int len = static_cast<int>(is_x ? c->n : c->m);
+  const double* p;
+  const double* q;
+  if (is_x) {
+    p = xbuf(c, C.last_zx);
+    q = normalized ? xbuf(c, C.last_xa) : xbuf(c, C.last_xp);
+  } else {
+    p = ybuf(c, C.last_y);
+    q = normalized ? ybuf(c, C.last_ya) : ybuf(c, C.last_yp);
+  }
+  const double sgn = C.cert[kind].orientation == HPLP_ORIENT_NEGATED ? -1.0 : 1.0;
+  const double factor = sgn / C.r.cn2[cand];
+  double* tmp = c->upool;
+  cert_kernel<<<4 * c->sm_count, 256, 0, c->stream>>>(len, normalized ? 1 : 0, C.r.cand_scale, factor, p, q, tmp);
+  c->launches += 1;
+  HX_CUDA(c, cudaMemcpyAsync(vec, tmp, len * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  HX_CUDA(c, cudaStreamSynchronize(c->stream));
+  return HPLP_OK;
+}
+
+int hx_kkt_current(hx_ctx* c, hplp_kkt_t* out) {
+  if (!c->setup_done) return set_err(c, HPLP_ESTATE, "hx_kkt_current: no solve state");
+  const Ctl& C = c->h;
+  cudaStream_t s = c->stream;
+  // current z: materialize x into u-scratch, y from its buffer
+  double* xcur = c->upool;
+  double* aty = c->upool + c->n;
+  double* ax = c->upool + 2 * c->n;
+  const double* ycur = ybuf(c, C.r.y_cur);
+  if (C.r.x_mode == 0) {
+    HX_CUDA(c, cudaMemcpyAsync(xcur, xbuf(c, C.r.x_src), c->n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  } else {
+    combine_kernel<<<4 * c->sm_count, 256, 0, s>>>(static_cast<int>(c->n), C.r.w_x, xbuf(c, C.r.x_src),
+                                                   xbuf(c, C.r.x_anchor), xcur);
+    c->launches += 1;
+  }
+  int rc = spmv_dev(c, false, xcur, ax);
+  if (rc) return rc;
+  rc = spmv_dev(c, true, ycur, aty);
+  if (rc) return rc;
+  kkt_partials_kernel<<<c->grid, kThreads, 0, s>>>(static_cast<int>(c->m), static_cast<int>(c->n), ax, c->b, aty,
+                                                   c->c, xcur, ycur, c->slots);
+  final_reduce_kernel<<<1, 256, 0, s>>>(c->slots, c->grid, 6, c->scratch);
+  c->launches += 2;
+  double tot[6];
+  HX_CUDA(c, cudaMemcpyAsync(tot, c->scratch, sizeof(tot), cudaMemcpyDeviceToHost, s));
+  HX_CUDA(c, cudaStreamSynchronize(s));
+  // kkt_error_with_products, src/pdhg_core.cpp:57-68 (scalar epilogue)
+  out->primal_residual = std::sqrt(tot[0]) / (1.0 + c->b_norm);
+  out->dual_residual = std::sqrt(tot[1]) / (1.0 + c->c_norm);
+  out->gap_residual = std::fabs(tot[2] + tot[3]) / (1.0 + std::fabs(tot[2]) + std::fabs(tot[3]));
+  out->max_relative = std::max({out->primal_residual, out->dual_residual, out->gap_residual});
+  return HPLP_OK;
+}
+
+int64_t hx_sizeof(int32_t which) {
+  switch (which) {
+    case 0: return sizeof(hplp_config_t);
+    case 1: return sizeof(hplp_result_t);
+    case 2: return sizeof(hplp_io_t);
+    case 3: return sizeof(hplp_epoch_t);
+    case 4: return sizeof(hplp_trace_t);
+    case 5: return sizeof(hplp_general_t);
+    case 6: return sizeof(hx_progress_t);
+    default: return -1;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,352 @@
+// hplp_gpu::solve -- the C++ host driver of the B200 rHPDHG solver.
+//
+// Mirrors src/solver.cpp:206-342 of the reference: setup (power iteration
+// with the reference's seeded std::mt19937_64 start vector, step size),
+// initial iterate, then the iteration loop -- which runs ON THE DEVICE in
+// batches through hx_run (include/hx.h), the controller making every
+// per-iteration decision there.  The host only drains epoch records, feeds
+// the synchronous trace sink (trace_period > 0 pauses the device after each
+// traced iteration) and assembles the SolveResult.  There is no CPU compute
+// path: without a B200 the hx layer fails and solve() throws.
+#include <chrono>
+#include <cmath>
+#include <random>
+#include <stdexcept>
+#include <string>
+
+#include "hplp_gpu.hpp"
+#include "hx.h"
+
+namespace hplp_gpu {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+constexpr double kPowerTol = 1e-4;          // src/solver.cpp:24
+constexpr int64_t kPowerMaxIters = 5000;    // src/solver.cpp:25
+constexpr int64_t kBatch = 4096;            // iterations per hx_run when not tracing
+
+[[noreturn]] void throw_hx(hx_ctx* ctx, int rc) {
+  const std::string msg = hx_last_error(ctx);
+  if (rc == HPLP_EINVAL) throw std::invalid_argument(msg);
+  if (rc == HPLP_EDOMAIN) throw std::domain_error(msg);
+  throw std::runtime_error("hplp_gpu: " + msg);
+}
+
+void check(hx_ctx* ctx, int rc) {
+  if (rc != HPLP_OK) throw_hx(ctx, rc);
+}
+
+// validate_config, src/solver.cpp:40-65
+void validate_config(const SolverConfig& config) {
+  if (!(config.tolerance > 0.0)) throw std::invalid_argument("SolverConfig: tolerance must be > 0");
+  if (config.iteration_limit < 0) throw std::invalid_argument("SolverConfig: iteration_limit must be >= 0");
+  if (!(config.certificate_tolerance > 0.0))
+    throw std::invalid_argument("SolverConfig: certificate_tolerance must be > 0");
+  if (config.infeasibility_check_period < 0 || config.trace_period < 0 || config.adaptive_stall_cap < 0)
+    throw std::invalid_argument("SolverConfig: periods must be >= 0");
+  if (config.restart.kind == RestartScheme::Kind::kFixedFrequency && config.restart.k_star < 1)
+    throw std::invalid_argument("RestartScheme: k_star must be >= 1");
+  if (config.restart.kind == RestartScheme::Kind::kAdaptiveResidualDecay &&
+      (!(config.restart.beta > 0.0) || !(config.restart.beta < 1.0) || config.restart.tau0 < 1))
+    throw std::invalid_argument("RestartScheme: adaptive needs beta in (0,1) and tau0 >= 1");
+}
+
+// StepSize ctor, src/pdhg_core.cpp:21-35
+double step_size(double eta, double sigma_estimate) {
+  if (!(eta > 0.0) || !std::isfinite(eta)) throw std::invalid_argument("StepSize: eta must be positive and finite");
+  if (sigma_estimate > 0.0 && eta > 1.0 / (2.0 * sigma_estimate) * (1 + 1e-12))
+    throw std::invalid_argument("StepSize: eta exceeds 1/(2 ||A||_2-estimate) = " +
+                                std::to_string(1.0 / (2.0 * sigma_estimate)));
+  return eta;
+}
+
+double seq_norm(const Vector& v) {  // Vector::norm with a sequential sum
+  double s = 0.0;
+  for (double a : v) s += a * a;
+  return std::sqrt(s);
+}
+
+KktError kkt_of(const hplp_kkt_t& k) {
+  return {k.primal_residual, k.dual_residual, k.gap_residual, k.max_relative};
+}
+
+struct PowerResult {
+  double sigma = 0.0;
+  int64_t iterations = 0;
+  bool converged = false;
+};
+
+// power_iteration, src/sparse_matrix.cpp:138-179: the start vector (and any
+// re-draw) comes from the same std::mt19937_64 stream as the reference; the
+// SpMVs and norms run on the device (hx_power_iteration).
+PowerResult power_iteration(hx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, double tol, int64_t max_iters,
+                            uint64_t seed) {
+  PowerResult res;
+  if (m == 0 || n == 0 || nnz == 0) {
+    res.converged = true;
+    return res;
+  }
+  std::mt19937_64 gen(seed);
+  std::normal_distribution<double> dist(0.0, 1.0);
+  Vector x(static_cast<std::size_t>(n));
+  for (auto& v : x) v = dist(gen);
+  double xn = seq_norm(x);
+  if (xn == 0.0) std::fill(x.begin(), x.end(), 1.0), xn = seq_norm(x);
+  for (auto& v : x) v /= xn;
+  int64_t k0 = 0;
+  double sigma_prev = 0.0;
+  while (true) {
+    double sigma = 0.0;
+    int64_t iters = 0;
+    int32_t conv = 0, redraw = 0;
+    check(ctx, hx_power_iteration(ctx, x.data(), tol, k0, max_iters, sigma_prev, &sigma, &iters, &conv, &redraw));
+    res.iterations = iters;
+    res.sigma = sigma;
+    if (!redraw) {
+      res.converged = conv != 0;
+      return res;
+    }
+    // sigma == 0 at iteration iters-1: re-draw and continue (:158-163)
+    for (auto& v : x) v = dist(gen);
+    const double nn = seq_norm(x);
+    for (auto& v : x) v /= nn;
+    k0 = iters;
+    sigma_prev = sigma;
+    if (k0 >= max_iters) return res;
+  }
+}
+
+}  // namespace
+
+RestartScheme RestartScheme::fixed(long k_star) {
+  RestartScheme s;
+  s.kind = Kind::kFixedFrequency;
+  s.k_star = k_star;
+  return s;
+}
+
+RestartScheme RestartScheme::adaptive(double beta, long tau0) {
+  RestartScheme s;
+  s.kind = Kind::kAdaptiveResidualDecay;
+  s.beta = beta;
+  s.tau0 = tau0;
+  return s;
+}
+
+RestartScheme RestartScheme::none() {
+  RestartScheme s;
+  s.kind = Kind::kNone;
+  return s;
+}
+
+// src/solver.cpp:162-174 (the device controller implements the same rule).
+bool should_restart(const RestartScheme& scheme, long n, long k, double residual_now, double residual_epoch_start) {
+  switch (scheme.kind) {
+    case RestartScheme::Kind::kFixedFrequency:
+      return k >= scheme.k_star;
+    case RestartScheme::Kind::kAdaptiveResidualDecay:
+      if (n == 0) return k > scheme.tau0;
+      return residual_now <= scheme.beta * residual_epoch_start;
+    case RestartScheme::Kind::kNone:
+      return false;
+  }
+  return false;
+}
+
+// src/solver.cpp:176-192
+const char* to_string(SolveStatus status) {
+  switch (status) {
+    case SolveStatus::kOptimal:
+      return "optimal";
+    case SolveStatus::kPrimalInfeasible:
+      return "primal_infeasible";
+    case SolveStatus::kDualInfeasible:
+      return "dual_infeasible";
+    case SolveStatus::kPrimalDualInfeasible:
+      return "primal_dual_infeasible";
+    case SolveStatus::kIterationLimit:
+      return "iteration_limit";
+    case SolveStatus::kTimeLimit:
+      return "time_limit";
+  }
+  return "unknown";
+}
+
+hplp_config_t to_pod(const SolverConfig& c) {
+  hplp_config_t p = hplp_config_default();
+  p.restart_kind = c.restart.kind == RestartScheme::Kind::kFixedFrequency ? HPLP_RESTART_FIXED
+                   : c.restart.kind == RestartScheme::Kind::kNone        ? HPLP_RESTART_NONE
+                                                                         : HPLP_RESTART_ADAPTIVE;
+  p.k_star = c.restart.k_star;
+  p.beta = c.restart.beta;
+  p.tau0 = c.restart.tau0;
+  p.tolerance = c.tolerance;
+  p.iteration_limit = c.iteration_limit;
+  p.time_limit_seconds = c.time_limit_seconds;
+  p.has_eta_override = c.eta_override.has_value();
+  p.eta_override = c.eta_override.value_or(0.0);
+  p.infeasibility_check_period = c.infeasibility_check_period;
+  p.trace_period = c.trace_period;
+  p.certificate_tolerance = c.certificate_tolerance;
+  p.tol_active = c.tol_active;
+  p.adaptive_stall_cap = c.adaptive_stall_cap;
+  p.seed = c.seed;
+  return p;
+}
+
+SolverConfig from_pod(const hplp_config_t& p) {
+  SolverConfig c;
+  c.restart = p.restart_kind == HPLP_RESTART_FIXED  ? RestartScheme::fixed(p.k_star)
+              : p.restart_kind == HPLP_RESTART_NONE ? RestartScheme::none()
+                                                    : RestartScheme::adaptive(p.beta, p.tau0);
+  c.restart.k_star = p.k_star;
+  c.tolerance = p.tolerance;
+  c.iteration_limit = p.iteration_limit;
+  c.time_limit_seconds = p.time_limit_seconds;
+  if (p.has_eta_override) c.eta_override = p.eta_override;
+  c.infeasibility_check_period = p.infeasibility_check_period;
+  c.trace_period = p.trace_period;
+  c.certificate_tolerance = p.certificate_tolerance;
+  c.tol_active = p.tol_active;
+  c.adaptive_stall_cap = p.adaptive_stall_cap;
+  c.seed = p.seed;
+  return c;
+}
+
+Solver::Solver(const StandardFormLP& lp, int device)
+    : Solver(device, lp.num_rows(), lp.num_cols(), lp.a.row_ptr().data(), lp.a.col_idx().data(),
+             lp.a.values().data(), lp.b.data(), lp.c.data()) {}
+
+Solver::Solver(int device, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const double* val,
+               const double* b, const double* c)
+    : m_(m), n_(n), nnz_(row_ptr[m]) {
+  int rc = hx_create(device, &ctx_);
+  if (rc != HPLP_OK) throw_hx(nullptr, rc);
+  rc = hx_upload_csr(ctx_, m, n, row_ptr, col_idx, val, b, c);
+  if (rc != HPLP_OK) {
+    const std::string msg = hx_last_error(ctx_);
+    hx_destroy(ctx_);
+    ctx_ = nullptr;
+    if (rc == HPLP_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error("hplp_gpu: " + msg);
+  }
+}
+
+Solver::~Solver() { hx_destroy(ctx_); }
+
+// solve(): src/solver.cpp:206-342.
+SolveResult Solver::solve(const SolverConfig& config) {
+  const auto t0 = Clock::now();
+  auto since = [&] { return std::chrono::duration<double>(Clock::now() - t0).count(); };
+  validate_config(config);
+  hx_ctx* ctx = ctx_;
+  // make_setup (:67-78)
+  const PowerResult pi = power_iteration(ctx, m_, n_, nnz_, kPowerTol, kPowerMaxIters, config.seed);
+  const double sigma_used = pi.sigma * (1.0 + kPowerTol);
+  long n_spmv = 2 * static_cast<long>(pi.iterations);
+  const double eta = config.eta_override ? step_size(*config.eta_override, sigma_used)
+                     : sigma_used <= 0.0 ? step_size(1.0, 0.0)
+                                         : step_size(1.0 / (2.0 * sigma_used), sigma_used);
+  // initial_point (:80-87)
+  const double* x0 = nullptr;
+  const double* y0 = nullptr;
+  if (config.initial_iterate) {
+    const Iterate& z = *config.initial_iterate;
+    if (static_cast<int64_t>(z.x.size()) != n_ || static_cast<int64_t>(z.y.size()) != m_)
+      throw std::invalid_argument("SolverConfig: initial iterate has wrong size");
+    x0 = z.x.data();
+    y0 = z.y.data();
+  }
+  hplp_config_t pod = to_pod(config);
+  pod.time_limit_seconds = config.time_limit_seconds - since();  // device clock starts at the loop
+  check(ctx, hx_setup(ctx, &pod, sigma_used, eta, x0, y0));
+  n_spmv += 1;  // a_x = A x (:213-214)
+
+  SolveResult out;
+  std::vector<hplp_epoch_t> epochs;
+  hx_progress_t p{};
+  check(ctx, hx_progress(ctx, &p));
+  auto drain_epochs = [&] {
+    const int64_t have = static_cast<int64_t>(epochs.size());
+    const int64_t from = have > 0 ? have - 1 : 0;  // re-read the open epoch (restart_length)
+    if (p.n_epochs > from) {
+      epochs.resize(static_cast<std::size_t>(p.n_epochs));
+      check(ctx, hx_epochs(ctx, from, p.n_epochs - from, epochs.data() + from));
+    }
+  };
+  while (p.status < 0) {
+    if (since() > config.time_limit_seconds && p.it < config.iteration_limit) {
+      // host-side guard for the time limit between batches (:249-254)
+      break;
+    }
+    const int64_t batch = config.trace_period > 0 ? config.trace_period : kBatch;
+    const int rc = hx_run(ctx, batch, &p);
+    if (rc != HPLP_OK) throw_hx(ctx, rc);
+    drain_epochs();
+    if (p.paused && config.trace_sink) {
+      TraceRecord rec;
+      rec.epoch = p.trace_n;
+      rec.inner = p.trace_k;
+      rec.iteration = p.trace_it;
+      rec.fixed_point_residual = p.trace_res;
+      rec.kkt = kkt_of(p.trace_kkt);
+      rec.candidate_norm_difference = p.trace_res;  // ||T(z) - z|| == ||z - T(z)||
+      rec.wall_seconds = since();
+      Iterate z{Vector(static_cast<std::size_t>(n_)), Vector(static_cast<std::size_t>(m_))};
+      check(ctx, hx_get_iterate(ctx, HX_ITERATE_LAST, z.x.data(), z.y.data()));
+      config.trace_sink(rec, z);
+    }
+  }
+  SolveStatus status = p.status >= 0 ? static_cast<SolveStatus>(p.status) : SolveStatus::kTimeLimit;
+  out.status = status;
+  out.final_iterate.x.resize(static_cast<std::size_t>(n_));
+  out.final_iterate.y.resize(static_cast<std::size_t>(m_));
+  long extra_spmv = 0;
+  if (status == SolveStatus::kIterationLimit || status == SolveStatus::kTimeLimit) {
+    // (:242-254) best iterate if any KKT value was finite, else z with fresh products
+    if (p.best_valid) {
+      check(ctx, hx_get_iterate(ctx, HX_ITERATE_BEST, out.final_iterate.x.data(), out.final_iterate.y.data()));
+      out.final_kkt = kkt_of(p.best_err);
+    } else {
+      check(ctx, hx_get_iterate(ctx, HX_ITERATE_CURRENT, out.final_iterate.x.data(), out.final_iterate.y.data()));
+      hplp_kkt_t k;
+      check(ctx, hx_kkt_current(ctx, &k));
+      out.final_kkt = kkt_of(k);
+      extra_spmv = 2;
+    }
+  } else {
+    check(ctx, hx_get_iterate(ctx, HX_ITERATE_LAST, out.final_iterate.x.data(), out.final_iterate.y.data()));
+    out.final_kkt = kkt_of(p.final_kkt);
+  }
+  auto take_cert = [&](int kind, const hplp_cert_meta_t& meta, std::optional<Certificate>& dst, int64_t len) {
+    if (!meta.present) return;
+    Certificate c;
+    c.vector.resize(static_cast<std::size_t>(len));
+    check(ctx, hx_get_certificate(ctx, kind, c.vector.data()));
+    c.source = meta.source == HPLP_SOURCE_NORMALIZED_ITERATE ? CandidateSource::kNormalizedIterate
+                                                             : CandidateSource::kIterateDifference;
+    c.at_iteration = static_cast<long>(meta.at_iteration);
+    c.orientation = meta.orientation == HPLP_ORIENT_NEGATED ? Orientation::kNegated : Orientation::kAsIs;
+    c.residual = meta.residual;
+    c.margin = meta.margin;
+    dst = std::move(c);
+  };
+  take_cert(0, p.primal_cert, out.primal_certificate, m_);
+  take_cert(1, p.dual_cert, out.dual_certificate, n_);
+  out.epochs.reserve(epochs.size());
+  for (const hplp_epoch_t& e : epochs)
+    out.epochs.push_back({static_cast<long>(e.epoch), static_cast<long>(e.restart_length), e.residual_at_start,
+                          kkt_of(e.kkt_at_start)});
+  if (!out.epochs.empty() && out.epochs.back().restart_length == 0) out.epochs.back().restart_length = p.k;
+  out.totals = {static_cast<long>(p.it), n_spmv + static_cast<long>(p.spmv_count) + extra_spmv, since(), eta,
+                sigma_used};
+  return out;
+}
+
+SolveResult solve(const StandardFormLP& lp, const SolverConfig& config) {
+  Solver s(lp, config.device);
+  return s.solve(config);
+}
+
+}  // namespace hplp_gpu

@@ -1,0 +1,387 @@
+"""Python front-end of the B200 rHPDHG solver (ctypes over include/hplp_gpu.h
+and include/hx.h).
+
+Names mirror the reference API (/root/reference/proj/include/hplp):
+``to_standard_form``, ``Solver.solve`` / ``solve`` (SolverConfig fields as
+keyword arguments), status strings of ``to_string(SolveStatus)``.  There is
+no CPU path: if libhplp_gpu.so cannot be loaded, or no B200 is visible, every
+call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+
+from . import abi
+from .abi import dptr, i32ptr, i64ptr
+from .build import GPU_LIB, ensure_built
+
+
+class HplpError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class HxProgress(C.Structure):
+    """hx_progress_t (include/hx.h)."""
+
+    _fields_ = [
+        ("it", C.c_int64), ("n", C.c_int64), ("k", C.c_int64), ("spmv_count", C.c_int64),
+        ("status", C.c_int32), ("error", C.c_int32), ("paused", C.c_int32), ("best_valid", C.c_int32),
+        ("res_epoch_start", C.c_double), ("best_kkt", C.c_double), ("best_err", abi.Kkt),
+        ("trace_it", C.c_int64), ("trace_n", C.c_int64), ("trace_k", C.c_int64),
+        ("trace_res", C.c_double), ("trace_kkt", abi.Kkt), ("final_kkt", abi.Kkt),
+        ("n_epochs", C.c_int64), ("primal_cert", abi.CertMeta), ("dual_cert", abi.CertMeta),
+        ("device_ms", C.c_double), ("launches", C.c_int64),
+    ]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libhplp_gpu.so (building it in-tree if needed)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    ensure_built()
+    if not GPU_LIB.exists():
+        raise HplpError(abi.HPLP_ECUDA, f"{GPU_LIB} missing: the B200 path has no CPU fallback")
+    L = C.CDLL(str(GPU_LIB))
+    V, I64, I32, D = C.c_void_p, C.c_int64, C.c_int32, C.c_double
+    PD, PI64, PI32, PV = C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_void_p)
+
+    def sig(name, res, *args):
+        f = getattr(L, name)
+        f.restype, f.argtypes = res, list(args)
+
+    sig("hplp_last_error", C.c_char_p)
+    sig("hplp_status_string", C.c_char_p, I32)
+    sig("hplp_validate_config", C.c_int, C.POINTER(abi.Config))
+    sig("hplp_solve_csr", C.c_int, I32, I64, I64, PI64, PI32, PD, PD, PD, C.POINTER(abi.Config),
+        C.POINTER(abi.IO), C.POINTER(abi.Result))
+    sig("hplp_solver_create", C.c_int, I32, I64, I64, PI64, PI32, PD, PD, PD, PV)
+    sig("hplp_solver_solve", C.c_int, V, C.POINTER(abi.Config), C.POINTER(abi.IO), C.POINTER(abi.Result))
+    sig("hplp_solver_hx", V, V)
+    sig("hplp_solver_free", None, V)
+    sig("hplp_to_standard_form", C.c_int, C.POINTER(abi.General), PV, PI64, PI64, PI64)
+    sig("hplp_std_export", C.c_int, V, PI64, PI32, PD, PD, PD)
+    sig("hplp_std_recover", C.c_int, V, PD, PD, D, PD)
+    sig("hplp_std_free", None, V)
+    sig("hplp_solve_general", C.c_int, I32, C.POINTER(abi.General), C.POINTER(abi.Config), C.POINTER(abi.IO),
+        C.POINTER(abi.Result), PD, PD)
+    # hx layer
+    sig("hx_create", C.c_int, I32, PV)
+    sig("hx_destroy", None, V)
+    sig("hx_last_error", C.c_char_p, V)
+    sig("hx_device_info", C.c_int, V, PI32, PI32, PI32)
+    sig("hx_stream", V, V)
+    sig("hx_launch_count", I64, V)
+    sig("hx_upload_csr", C.c_int, V, I64, I64, PI64, PI32, PD, PD, PD)
+    sig("hx_dims", C.c_int, V, PI64, PI64, PI64)
+    sig("hx_spmv", C.c_int, V, PD, PD)
+    sig("hx_spmv_transpose", C.c_int, V, PD, PD)
+    sig("hx_power_iteration", C.c_int, V, PD, D, I64, I64, D, PD, PI64, PI32, PI32)
+    sig("hx_setup", C.c_int, V, C.POINTER(abi.Config), D, D, PD, PD)
+    sig("hx_run", C.c_int, V, I64, C.POINTER(HxProgress))
+    sig("hx_progress", C.c_int, V, C.POINTER(HxProgress))
+    sig("hx_epochs", C.c_int, V, I64, I64, C.POINTER(abi.Epoch))
+    sig("hx_get_iterate", C.c_int, V, I32, PD, PD)
+    sig("hx_get_certificate", C.c_int, V, I32, PD)
+    sig("hx_kkt_current", C.c_int, V, C.POINTER(abi.Kkt))
+    sig("hx_sizeof", I64, I32)
+    _lib = L
+    return L
+
+
+def _check(rc: int, ctx=None) -> None:
+    if rc == 0:
+        return
+    L = lib()
+    msg = (L.hx_last_error(ctx) if ctx is not None else L.hplp_last_error()).decode()
+    if rc == abi.HPLP_EINVAL:
+        raise ValueError(msg)
+    if rc == abi.HPLP_EDOMAIN:
+        raise ArithmeticError(msg)
+    raise HplpError(rc, msg)
+
+
+def to_string(status: int) -> str:
+    """to_string(SolveStatus), src/solver.cpp:176-192."""
+    return lib().hplp_status_string(status).decode()
+
+
+class StdForm:
+    """to_standard_form output: standard-form CSR + VariableMap handle."""
+
+    def __init__(self, general):
+        L = lib()
+        self._g = general
+        ga = general.as_abi()
+        h = C.c_void_p()
+        m, n, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(L.hplp_to_standard_form(C.byref(ga), C.byref(h), C.byref(m), C.byref(n), C.byref(nnz)))
+        self.h = h
+        self.m, self.n, self.nnz = m.value, n.value, nnz.value
+        self.row_ptr = np.empty(self.m + 1, np.int64)
+        self.col_idx = np.empty(self.nnz, np.int32)
+        self.val = np.empty(self.nnz)
+        self.b, self.c = np.empty(self.m), np.empty(self.n)
+        _check(L.hplp_std_export(h, i64ptr(self.row_ptr), i32ptr(self.col_idx), dptr(self.val), dptr(self.b),
+                                 dptr(self.c)))
+
+    def csr(self):
+        return self.m, self.n, self.row_ptr, self.col_idx, self.val, self.b, self.c
+
+    def recover(self, x_std, std_objective=None):
+        """(x_original, objective_original) -- VariableMap recovery."""
+        x_std = np.ascontiguousarray(x_std, np.float64)
+        if std_objective is None:
+            std_objective = float(self.c @ x_std)
+        xo = np.empty(self._g.n)
+        obj = C.c_double()
+        _check(lib().hplp_std_recover(self.h, dptr(x_std), dptr(xo), std_objective, C.byref(obj)))
+        return xo, obj.value
+
+    def __del__(self):
+        try:
+            lib().hplp_std_free(self.h)
+        except Exception:
+            pass
+
+
+def to_standard_form(general) -> StdForm:
+    return StdForm(general)
+
+
+def _result(res: abi.Result, x, y, pc, dc, eps, recs) -> dict:
+    ne = min(res.n_epochs, len(eps))
+    meta = lambda m: dict(source=m.source, orientation=m.orientation, at_iteration=m.at_iteration,  # noqa: E731
+                          residual=m.residual, margin=m.margin)
+    return dict(
+        status=abi.STATUS_NAMES[res.status], status_code=res.status, iterations=res.iterations,
+        spmv_count=res.spmv_count, wall_seconds=res.wall_seconds, eta=res.eta, sigma_estimate=res.sigma_estimate,
+        kkt=res.final_kkt.as_tuple(), n_epochs=res.n_epochs,
+        epochs=[(e.epoch, e.restart_length, e.residual_at_start, e.kkt_at_start.as_tuple()) for e in eps[:ne]],
+        x=x, y=y,
+        primal_cert=(pc, meta(res.primal_cert)) if res.primal_cert.present else None,
+        dual_cert=(dc, meta(res.dual_cert)) if res.dual_cert.present else None,
+        trace=recs,
+    )
+
+
+def _io(m, n, init, trace, epochs_capacity):
+    x, y = np.empty(n), np.empty(m)
+    pc, dc = np.zeros(m), np.zeros(n)
+    eps = (abi.Epoch * epochs_capacity)()
+    recs = []
+
+    def sink(rec, xp, nn, yp, mm, user):
+        r = rec.contents
+        recs.append(dict(epoch=r.epoch, inner=r.inner, iteration=r.iteration, res=r.fixed_point_residual,
+                         kkt=r.kkt.as_tuple(), cand_norm_normalized=r.candidate_norm_normalized,
+                         cand_norm_difference=r.candidate_norm_difference,
+                         x=np.ctypeslib.as_array(xp, (nn,)).copy(), y=np.ctypeslib.as_array(yp, (mm,)).copy()))
+
+    cb = abi.TRACE_FN(sink) if trace else abi.TRACE_FN()
+    ix = iy = None
+    if init is not None:
+        ix = np.ascontiguousarray(init[0], np.float64)
+        iy = np.ascontiguousarray(init[1], np.float64)
+    io = abi.IO(dptr(ix), dptr(iy), dptr(x), dptr(y), dptr(pc), dptr(dc), eps, epochs_capacity, cb, None)
+    keep = (ix, iy, cb)
+    return io, x, y, pc, dc, eps, recs, keep
+
+
+def _config(config, trace, kw):
+    cfg = config if config is not None else abi.Config.default(**kw)
+    if trace and cfg.trace_period == 0:
+        cfg.trace_period = 1
+    return cfg
+
+
+class Solver:
+    """A device-resident standard-form LP (hplp_solver_create): upload once,
+    solve many times.  ``solve`` mirrors hplp::solve (src/solver.cpp:206)."""
+
+    def __init__(self, m, n, row_ptr, col_idx, val, b, c, device: int = 0):
+        L = lib()
+        self.m, self.n = int(m), int(n)
+        self._keep = [np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col_idx, np.int32),
+                      np.ascontiguousarray(val, np.float64), np.ascontiguousarray(b, np.float64),
+                      np.ascontiguousarray(c, np.float64)]
+        rp, ci, v, bb, cc = self._keep
+        h = C.c_void_p()
+        _check(L.hplp_solver_create(device, self.m, self.n, i64ptr(rp), i32ptr(ci), dptr(v), dptr(bb), dptr(cc),
+                                    C.byref(h)))
+        self.h = h
+        self._keep = None
+        self.hx = HX(L.hplp_solver_hx(h), owned=False)
+
+    @classmethod
+    def from_std(cls, std: StdForm, device: int = 0) -> "Solver":
+        return cls(*std.csr(), device=device)
+
+    def solve(self, config=None, init=None, trace=False, epochs_capacity=1 << 16, **kw) -> dict:
+        cfg = _config(config, trace, kw)
+        io, x, y, pc, dc, eps, recs, keep = _io(self.m, self.n, init, trace, epochs_capacity)
+        res = abi.Result()
+        _check(lib().hplp_solver_solve(self.h, C.byref(cfg), C.byref(io), C.byref(res)))
+        del keep
+        return _result(res, x, y, pc, dc, eps, recs)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().hplp_solver_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def solve(m, n, row_ptr, col_idx, val, b, c, config=None, init=None, trace=False, device=0,
+          epochs_capacity=1 << 16, **kw) -> dict:
+    """One-shot solve() through the C ABI with host buffers (hplp_solve_csr)."""
+    cfg = _config(config, trace, kw)
+    rp, ci, v, bb, cc = (np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col_idx, np.int32),
+                         np.ascontiguousarray(val, np.float64), np.ascontiguousarray(b, np.float64),
+                         np.ascontiguousarray(c, np.float64))
+    io, x, y, pc, dc, eps, recs, keep = _io(int(m), int(n), init, trace, epochs_capacity)
+    res = abi.Result()
+    _check(lib().hplp_solve_csr(device, int(m), int(n), i64ptr(rp), i32ptr(ci), dptr(v), dptr(bb), dptr(cc),
+                                C.byref(cfg), C.byref(io), C.byref(res)))
+    del keep
+    return _result(res, x, y, pc, dc, eps, recs)
+
+
+def solve_general(general, config=None, device=0, **kw):
+    """Problem load in CSR with bounds -> to_standard_form -> solve -> recovery
+    (hplp_solve_general).  Returns (result dict, x_original, objective)."""
+    cfg = _config(config, False, kw)
+    L = lib()
+    ga = general.as_abi()
+    std_m, std_n = _std_dims(general)
+    io, x, y, pc, dc, eps, recs, keep = _io(std_m, std_n, None, False, 1 << 16)
+    res = abi.Result()
+    xo = np.empty(general.n)
+    obj = C.c_double()
+    _check(L.hplp_solve_general(device, C.byref(ga), C.byref(cfg), C.byref(io), C.byref(res), dptr(xo),
+                                C.byref(obj)))
+    del keep
+    return _result(res, x, y, pc, dc, eps, recs), xo, obj.value
+
+
+def _std_dims(general):
+    s = StdForm(general)
+    return s.m, s.n
+
+
+class HX:
+    """The hx C-ABI CUDA layer (include/hx.h), for kernel-level tests/bench."""
+
+    def __init__(self, handle=None, device: int = 0, owned: bool = True):
+        L = lib()
+        if handle is None:
+            h = C.c_void_p()
+            rc = L.hx_create(device, C.byref(h))
+            if rc:
+                raise HplpError(rc, L.hx_last_error(None).decode())
+            handle = h.value
+        self.h = C.c_void_p(handle)
+        self.owned = owned
+        self.m = self.n = self.nnz = 0
+        if not owned:
+            m, n, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+            if L.hx_dims(self.h, C.byref(m), C.byref(n), C.byref(nnz)) == 0:
+                self.m, self.n, self.nnz = m.value, n.value, nnz.value
+
+    def _c(self, rc):
+        _check(rc, self.h)
+
+    def info(self):
+        sm, g, t = C.c_int32(), C.c_int32(), C.c_int32()
+        lib().hx_device_info(self.h, C.byref(sm), C.byref(g), C.byref(t))
+        return dict(sm_count=sm.value, grid=g.value, threads=t.value)
+
+    def stream(self) -> int:
+        return lib().hx_stream(self.h) or 0
+
+    def launches(self) -> int:
+        return lib().hx_launch_count(self.h)
+
+    def upload(self, m, n, row_ptr, col_idx, val, b, c):
+        rp, ci, v, bb, cc = (np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col_idx, np.int32),
+                             np.ascontiguousarray(val, np.float64), np.ascontiguousarray(b, np.float64),
+                             np.ascontiguousarray(c, np.float64))
+        self._c(lib().hx_upload_csr(self.h, int(m), int(n), i64ptr(rp), i32ptr(ci), dptr(v), dptr(bb), dptr(cc)))
+        self.m, self.n, self.nnz = int(m), int(n), int(rp[-1])
+
+    def spmv(self, x):
+        x = np.ascontiguousarray(x, np.float64)
+        out = np.empty(self.m)
+        self._c(lib().hx_spmv(self.h, dptr(x), dptr(out)))
+        return out
+
+    def spmv_transpose(self, y):
+        y = np.ascontiguousarray(y, np.float64)
+        out = np.empty(self.n)
+        self._c(lib().hx_spmv_transpose(self.h, dptr(y), dptr(out)))
+        return out
+
+    def power_iteration(self, x0, tol=1e-4, k0=0, max_iters=5000, sigma_prev=0.0):
+        x0 = np.ascontiguousarray(x0, np.float64)
+        s, it, cv, rd = C.c_double(), C.c_int64(), C.c_int32(), C.c_int32()
+        self._c(lib().hx_power_iteration(self.h, dptr(x0), tol, k0, max_iters, sigma_prev, C.byref(s),
+                                         C.byref(it), C.byref(cv), C.byref(rd)))
+        return s.value, it.value, bool(cv.value), bool(rd.value)
+
+    def setup(self, config, sigma_used, eta, x0=None, y0=None):
+        x0 = None if x0 is None else np.ascontiguousarray(x0, np.float64)
+        y0 = None if y0 is None else np.ascontiguousarray(y0, np.float64)
+        self._c(lib().hx_setup(self.h, C.byref(config), sigma_used, eta, dptr(x0), dptr(y0)))
+
+    def run(self, max_iters) -> HxProgress:
+        p = HxProgress()
+        self._c(lib().hx_run(self.h, int(max_iters), C.byref(p)))
+        return p
+
+    def progress(self) -> HxProgress:
+        p = HxProgress()
+        self._c(lib().hx_progress(self.h, C.byref(p)))
+        return p
+
+    def epochs(self, first, count):
+        out = (abi.Epoch * max(count, 1))()
+        self._c(lib().hx_epochs(self.h, first, count, out))
+        return [(e.epoch, e.restart_length, e.residual_at_start, e.kkt_at_start.as_tuple()) for e in out[:count]]
+
+    def get_iterate(self, which=0):
+        x, y = np.empty(self.n), np.empty(self.m)
+        self._c(lib().hx_get_iterate(self.h, which, dptr(x), dptr(y)))
+        return x, y
+
+    def kkt_current(self):
+        k = abi.Kkt()
+        self._c(lib().hx_kkt_current(self.h, C.byref(k)))
+        return k.as_tuple()
+
+    def close(self):
+        if self.owned and getattr(self, "h", None):
+            lib().hx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+ITERATE_CURRENT, ITERATE_BEST, ITERATE_NEXT, ITERATE_LAST = range(4)
+INF = math.inf

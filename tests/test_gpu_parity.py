@@ -1,0 +1,226 @@
+"""B200 parity tests: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star):
+  (a) per-iteration iterates, first 100 iterations: ||z_gpu - z_cpu||_inf /
+      ||z_cpu||_inf <= 1e-10, identical (epoch, inner) restart sequence;
+  (b) solve at tol 1e-4: identical status, objective within 1e-4 relative.
+Kernel-level SpMVs: normwise relative error <= 1e-13 (different, fixed
+summation order than the reference's sequential sums).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import CpuLp
+from paper_2407_16144_b200 import abi, hplp
+from tests.helpers import csr_args, problem, random_std_lp, rel_inf
+
+pytestmark = pytest.mark.gpu
+
+PROBLEMS = ["cfg0", "cfg1_small", "cfg2_small", "transport_small", "zipf_small"]
+_cache = {}
+
+
+def std(name):
+    if name not in _cache:
+        g = problem(name)
+        _cache[name] = (g, hplp.to_standard_form(g))
+    return _cache[name]
+
+
+@pytest.fixture(scope="module")
+def hx(gpu_required):
+    return hplp.HX(device=0)
+
+
+@pytest.mark.parametrize("name", PROBLEMS)
+def test_spmv_parity(hx, name):
+    g, s = std(name)
+    hx.upload(*csr_args(s))
+    cpu = CpuLp("port", *csr_args(s))
+    rng = np.random.default_rng(7)
+    for _ in range(3):
+        x = rng.normal(size=s.n)
+        y = rng.normal(size=s.m)
+        assert rel_inf(hx.spmv(x), cpu.spmv(x)) <= 1e-13
+        assert rel_inf(hx.spmv_transpose(y), cpu.spmv_transpose(y)) <= 1e-13
+
+
+def test_spmv_adjointness(hx):
+    # y'(Ax) == (A'y)'x to 1e-12 relative
+    g, s = std("zipf_small")
+    hx.upload(*csr_args(s))
+    rng = np.random.default_rng(3)
+    x, y = rng.normal(size=s.n), rng.normal(size=s.m)
+    lhs, rhs = y @ hx.spmv(x), hx.spmv_transpose(y) @ x
+    assert abs(lhs - rhs) <= 1e-12 * max(abs(lhs), 1.0)
+
+
+@pytest.mark.parametrize("name", ["cfg0", "cfg1_small", "transport_small"])
+def test_power_iteration_parity(gpu_required, name):
+    g, s = std(name)
+    cpu = CpuLp("port", *csr_args(s))
+    sigma_c, it_c, conv_c, _ = cpu.power_iteration()
+    r = hplp.solve(*csr_args(s), iteration_limit=0)
+    assert abs(r["sigma_estimate"] / (1 + 1e-4) - sigma_c) <= 1e-10 * sigma_c
+    assert r["spmv_count"] == 2 * it_c + 1 + 2
+
+
+def _trace_cmp(gpu_trace, cpu_trace, tol=1e-10):
+    assert len(gpu_trace) == len(cpu_trace)
+    worst = 0.0
+    for tg, tc in zip(gpu_trace, cpu_trace):
+        assert (tg["iteration"], tg["epoch"], tg["inner"]) == (tc["iteration"], tc["epoch"], tc["inner"])
+        zc = np.concatenate([tc["x"], tc["y"]])
+        zg = np.concatenate([tg["x"], tg["y"]])
+        e = rel_inf(zg, zc)
+        worst = max(worst, e)
+        assert e <= tol, (tg["iteration"], e)
+        assert abs(tg["res"] - tc["res"]) <= 1e-8 * max(tc["res"], 1e-300) + 1e-300
+    return worst
+
+
+@pytest.mark.parametrize("name", ["cfg0", "cfg1_small", "cfg2_small", "zipf_small"])
+def test_iterate_parity_first_100(gpu_required, name):
+    g, s = std(name)
+    cpu = CpuLp("port", *csr_args(s)).solve(iteration_limit=100, tolerance=1e-12, trace=True)
+    gpu = hplp.solve(*csr_args(s), iteration_limit=100, tolerance=1e-12, trace=True)
+    assert len(cpu["trace"]) == 100
+    _trace_cmp(gpu["trace"], cpu["trace"])
+    assert gpu["status"] == cpu["status"] == "iteration_limit"
+    assert gpu["iterations"] == cpu["iterations"] == 100
+    assert gpu["spmv_count"] == cpu["spmv_count"]
+    assert [e[:2] for e in gpu["epochs"]] == [e[:2] for e in cpu["epochs"]]
+
+
+def _objective(s, x):
+    return float(s.c @ x)
+
+
+@pytest.mark.parametrize("name", ["cfg0", "transport_small"])
+def test_solve_parity_tol_1e4(gpu_required, name):
+    g, s = std(name)
+    cpu = CpuLp("port", *csr_args(s)).solve(tolerance=1e-4, iteration_limit=200000)
+    gpu = hplp.solve(*csr_args(s), tolerance=1e-4, iteration_limit=200000)
+    assert gpu["status"] == cpu["status"] == "optimal"
+    oc, og = _objective(s, cpu["x"]), _objective(s, gpu["x"])
+    assert abs(og - oc) <= 1e-4 * max(1.0, abs(oc))
+    assert gpu["kkt"][3] <= 1e-4
+    if not math.isnan(g.planted_objective):
+        _, obj = s.recover(gpu["x"])
+        assert abs(obj - g.planted_objective) <= 1e-2 * max(1.0, abs(g.planted_objective))
+
+
+def test_infeasible_certificate(gpu_required):
+    g, s = std("cfg2_small")
+    gpu = hplp.solve(*csr_args(s), tolerance=1e-4, iteration_limit=100000)
+    cpu = CpuLp("port", *csr_args(s)).solve(tolerance=1e-4, iteration_limit=100000)
+    assert gpu["status"] == cpu["status"] == "primal_infeasible"
+    vec, meta = gpu["primal_cert"]
+    rep = CpuLp("port", *csr_args(s)).validate_primal(vec, 1e-6, gpu["sigma_estimate"])
+    assert rep["valid"] and rep["orientation"] == abi.ORIENT_AS_IS
+    assert abs(np.linalg.norm(vec) - 1.0) <= 1e-12
+    assert meta["at_iteration"] == gpu["iterations"]
+
+
+# ---- SPEC.md known-answer instances through the GPU path -------------------
+def _csr(rows, m, n):
+    rp = [0]
+    ci, v = [], []
+    for r in rows:
+        for c, val in r:
+            ci.append(c)
+            v.append(val)
+        rp.append(len(ci))
+    return m, n, np.array(rp, np.int64), np.array(ci, np.int32), np.array(v)
+
+
+def test_kat_e1_optimal(gpu_required):
+    # E1: c=(0), A=[1], b=(1) -> x ~ 1, y ~ 0
+    m, n, rp, ci, v = _csr([[(0, 1.0)]], 1, 1)
+    r = hplp.solve(m, n, rp, ci, v, np.array([1.0]), np.array([0.0]), tolerance=1e-8)
+    assert r["status"] == "optimal"
+    assert abs(r["x"][0] - 1.0) <= 1e-6 and abs(r["y"][0]) <= 1e-6
+    c = CpuLp("port", m, n, rp, ci, v, [1.0], [0.0]).solve(tolerance=1e-8)
+    assert r["iterations"] == c["iterations"]
+
+
+def test_kat_primal_infeasible(gpu_required):
+    # A=[[1],[1]], b=(1,2), c=0 -> PrimalInfeasible (AC6)
+    m, n, rp, ci, v = _csr([[(0, 1.0)], [(0, 1.0)]], 2, 1)
+    r = hplp.solve(m, n, rp, ci, v, np.array([1.0, 2.0]), np.array([0.0]))
+    assert r["status"] == "primal_infeasible" and r["iterations"] <= 10000
+    c = CpuLp("port", m, n, rp, ci, v, [1.0, 2.0], [0.0]).solve()
+    assert r["iterations"] == c["iterations"]
+    assert np.allclose(r["primal_cert"][0], c["primal_cert"][0], rtol=0, atol=1e-12)
+
+
+def test_kat_dual_infeasible(gpu_required):
+    # c=(-1,0), A=[1,-1], b=0 -> DualInfeasible with ray ~ (1,1)/sqrt2
+    m, n, rp, ci, v = _csr([[(0, 1.0), (1, -1.0)]], 1, 2)
+    r = hplp.solve(m, n, rp, ci, v, np.array([0.0]), np.array([-1.0, 0.0]))
+    assert r["status"] == "dual_infeasible"
+    c = CpuLp("port", m, n, rp, ci, v, [0.0], [-1.0, 0.0]).solve()
+    assert r["iterations"] == c["iterations"]
+    assert np.allclose(r["dual_cert"][0], c["dual_cert"][0], atol=1e-9)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_small_lps(gpu_required, seed):
+    args = random_std_lp(seed, 6, 10)
+    cpu = CpuLp("port", *args).solve(tolerance=1e-8, iteration_limit=20000)
+    gpu = hplp.solve(*args, tolerance=1e-8, iteration_limit=20000)
+    assert gpu["status"] == cpu["status"]
+    assert gpu["iterations"] == cpu["iterations"]
+    assert rel_inf(np.concatenate([gpu["x"], gpu["y"]]), np.concatenate([cpu["x"], cpu["y"]])) <= 1e-8
+
+
+def test_determinism(gpu_required):
+    g, s = std("cfg1_small")
+    a = hplp.solve(*csr_args(s), iteration_limit=500, tolerance=1e-12)
+    b = hplp.solve(*csr_args(s), iteration_limit=500, tolerance=1e-12)
+    assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["y"], b["y"])
+    assert a["kkt"] == b["kkt"] and a["epochs"] == b["epochs"]
+
+
+def test_zero_iteration_limit(gpu_required):
+    g, s = std("cfg0")
+    cpu = CpuLp("port", *csr_args(s)).solve(iteration_limit=0)
+    gpu = hplp.solve(*csr_args(s), iteration_limit=0)
+    assert gpu["status"] == cpu["status"] == "iteration_limit"
+    assert np.all(gpu["x"] == 0) and np.all(gpu["y"] == 0)
+    assert np.allclose(gpu["kkt"], cpu["kkt"], rtol=1e-12)
+    assert gpu["spmv_count"] == cpu["spmv_count"]
+
+
+def test_empty_matrix(gpu_required):
+    # nnz = 0: sigma = 0, eta = 1 (src/pdhg_core.cpp:32-33)
+    m, n = 2, 3
+    rp = np.zeros(m + 1, np.int64)
+    b, c = np.array([0.0, 0.0]), np.array([1.0, 2.0, 0.5])
+    cpu = CpuLp("port", m, n, rp, np.zeros(0, np.int32), np.zeros(0), b, c).solve()
+    gpu = hplp.solve(m, n, rp, np.zeros(0, np.int32), np.zeros(0), b, c)
+    assert gpu["status"] == cpu["status"]
+    assert gpu["iterations"] == cpu["iterations"]
+    assert gpu["eta"] == cpu["eta"] == 1.0
+
+
+def test_fixed_and_none_restarts(gpu_required):
+    g, s = std("cfg0")
+    for kw in (dict(restart_kind=abi.RESTART_FIXED, k_star=50), dict(restart_kind=abi.RESTART_NONE)):
+        cpu = CpuLp("port", *csr_args(s)).solve(iteration_limit=300, tolerance=1e-12, **kw)
+        gpu = hplp.solve(*csr_args(s), iteration_limit=300, tolerance=1e-12, **kw)
+        assert [e[:2] for e in gpu["epochs"]] == [e[:2] for e in cpu["epochs"]]
+        assert rel_inf(np.concatenate([gpu["x"], gpu["y"]]), np.concatenate([cpu["x"], cpu["y"]])) <= 1e-9
+
+
+def test_invalid_inputs_raise(gpu_required):
+    m, n, rp, ci, v = _csr([[(0, 1.0), (0, 2.0)]], 1, 1)
+    with pytest.raises(ValueError):
+        hplp.solve(m, n, rp, ci, v, np.array([1.0]), np.array([0.0]))
+    m, n, rp, ci, v = _csr([[(0, 1.0)]], 1, 1)
+    with pytest.raises(ValueError):
+        hplp.solve(m, n, rp, ci, v, np.array([1.0]), np.array([0.0]), tolerance=0.0)
