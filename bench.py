@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 rHPDHG iteration loop (BASELINE.json metric:
+"rHPDHG iters/sec & time-to-1e-4 rel KKT ... vs CPU; % HBM roofline").
+
+Workload: BASELINE.json configs[1] (medium planted LP, 100k x 200k, ~2M nnz,
+row scales 1e-2..1e2), standard form 300,000 x 430,000 with ~2.43M nnz,
+seeded synthetic data (the paper's MIPLIB set is not in this container).
+
+A step = one hx_run batch of ITERS_PER_STEP full rHPDHG iterations (KKT,
+restarts, certificate scans every 100 iterations -- nothing skipped) on a
+device-resident problem; L2 is flushed (256 MiB write) before every timed
+step.  value = iterations/s over the K timed steps (CUDA events on the
+solver's stream, max over ranks).  e2e = the same metric through the public C
+ABI (hplp_solve_csr) from host buffers: upload + A^T build + power iteration
++ loop + download, every step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIG_ID = 1
+ITERS_PER_STEP = 1000
+E2E_ITERS = 5000
+METRIC = "rHPDHG iters/sec & time-to-1e-4 rel KKT (1/2/4/8 B200) vs CPU; % HBM roofline"
+UNIT = "iters/s"
+
+
+def algorithmic_bytes(m: int, n: int, nnz: int) -> int:
+    """Frozen per-iteration byte count:
+    B_iter = 24 nnz + 68 m + 44 n + 8 (fp64 values, int32 indices)."""
+    return 24 * nnz + 68 * m + 44 * n + 8
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def build_problem():
+    from paper_2407_16144_b200 import gen, hplp
+
+    g = gen.generate(CONFIG_ID)
+    s = hplp.to_standard_form(g)
+    return g, s
+
+
+def traffic_from_profile():
+    """dram bytes per loop-kernel launch from the committed ncu capture."""
+    p = ROOT / "profiles" / "loop_kernel_traffic.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return d.get("dram_bytes_per_launch"), d
+        except Exception:
+            pass
+    return None, None
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (reference compiled here, else the oracle port) -- rank 0, N=1
+# ---------------------------------------------------------------------------
+def cpu_iters_per_sec(s, iters: int):
+    import oracle
+
+    kind = "reference" if oracle.available("reference") else "port"
+    lp = oracle.CpuLp(kind, *s.csr())
+    sigma, pit, conv, t_power = lp.power_iteration()
+    r = lp.solve(iteration_limit=iters, tolerance=1e-4)
+    loop_s = max(r["wall_seconds"] - t_power, 1e-9)
+    return kind, iters / loop_s, dict(power_iterations=pit, power_seconds=t_power, solve_wall_s=r["wall_seconds"])
+
+
+def run_reference(args):
+    world, rank, local = dist_setup()
+    if rank != 0:
+        return 0
+    import oracle
+
+    g, s = build_problem()
+    kind = "reference" if oracle.available("reference") else "port"
+    lp = oracle.CpuLp(kind, *s.csr())
+    iters = args.ref_iters
+    sigma, pit, conv, t_power = lp.power_iteration()
+    for _ in range(args.warmup):
+        lp.solve(iteration_limit=max(1, iters // 5), tolerance=1e-4)
+    loop_times = []
+    for _ in range(args.steps):
+        r = lp.solve(iteration_limit=iters, tolerance=1e-4)
+        loop_times.append(max(r["wall_seconds"] - t_power, 1e-9))
+    total = sum(loop_times)
+    value = iters * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded planted LP, configs[1])",
+        "config": {"workload": f"configs[{CONFIG_ID}] medium planted LP, standard form {s.m}x{s.n}, nnz {s.nnz}",
+                   "iters_per_step": iters, "parallelism": "none (single-threaded reference)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind,
+                         "sample": f"{args.steps} x solve(iteration_limit={iters}) on configs[1]; power iteration "
+                                   f"({pit} its, {t_power:.2f}s) timed separately and subtracted"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_gpu(args):
+    import torch
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2407_16144_b200 import abi, hplp
+
+    g, s = build_problem()
+    m, n, nnz = s.m, s.n, s.nnz
+    solver = hplp.Solver.from_std(s, device=local)
+    hx = solver.hx
+    stream = torch.cuda.ExternalStream(hx.stream(), device=torch.device("cuda", local))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    # setup exactly as solve() does (power iteration on the device, seeded start)
+    r0 = solver.solve(iteration_limit=0)
+    sigma_used, eta = r0["sigma_estimate"], r0["eta"]
+    cfg = abi.Config.default(tolerance=1e-4, iteration_limit=10**9)
+
+    def fresh():
+        hx.setup(cfg, sigma_used, eta)
+
+    fresh()
+    for _ in range(args.warmup):
+        p = hx.run(ITERS_PER_STEP)
+        if p.status >= 0:
+            fresh()
+    times = []
+    launches0 = hx.launches()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            if hx.progress().status >= 0:
+                fresh()
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            p = hx.run(ITERS_PER_STEP)
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+    launches = hx.launches() - launches0
+    iters_done = ITERS_PER_STEP * args.steps
+    elapsed = sum(times)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([elapsed], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    value = world * iters_done / elapsed
+    b_iter = algorithmic_bytes(m, n, nnz)
+    peak, peak_kind = measured_peak()
+    per_launch_s = elapsed / args.steps
+    achieved = b_iter * ITERS_PER_STEP / per_launch_s / 1e9
+    traffic, prof = traffic_from_profile()
+
+    # e2e through the public C ABI from host buffers (upload + setup + loop + download)
+    e2e_times = []
+    h2d = 8 * (m + 1) + 12 * nnz + 8 * m + 8 * n
+    d2h = 8 * (m + n)
+    rp, ci, v, b, c = s.row_ptr, s.col_idx, s.val, s.b, s.c
+    for i in range(args.e2e_steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = hplp.solve(m, n, rp, ci, v, b, c, iteration_limit=E2E_ITERS, tolerance=1e-4, device=local)
+        dt = time.perf_counter() - t0
+        if i > 0:  # first call is warm-up (context creation)
+            e2e_times.append(dt)
+        assert r["iterations"] == E2E_ITERS or r["status"] != "iteration_limit"
+    e2e_value = world * E2E_ITERS / statistics.median(e2e_times)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([statistics.median(e2e_times)], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_value = world * E2E_ITERS / float(t.item())
+
+    # time to 1e-4 (configs[0] converges; configs[1] capped)
+    ttt = {}
+    if rank == 0 and not args.no_ttt:
+        from paper_2407_16144_b200 import gen
+
+        for cid, cap in ((0, 30.0), (1, args.ttt_cap)):
+            gg = g if cid == CONFIG_ID else gen.generate(cid)
+            ss = s if cid == CONFIG_ID else hplp.to_standard_form(gg)
+            t0 = time.perf_counter()
+            rr = hplp.solve(*ss.csr(), tolerance=1e-4, time_limit_seconds=cap, device=local)
+            dt = time.perf_counter() - t0
+            _, obj = ss.recover(rr["x"])
+            ttt[f"configs[{cid}]"] = {"status": rr["status"], "seconds": round(dt, 4), "iterations": rr["iterations"],
+                                      "kkt_max": rr["kkt"][3], "objective": obj,
+                                      "planted_objective": gg.planted_objective}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        kind, cval, info = cpu_iters_per_sec(s, args.cpu_iters)
+        cpu = {"value": cval, "unit": UNIT, "cores": 1, "kind": kind,
+               "sample": f"solve(iteration_limit={args.cpu_iters}) on configs[1], single thread; power iteration "
+                         f"({info['power_iterations']} its, {info['power_seconds']:.2f}s) timed separately and "
+                         f"subtracted"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded planted LP, BASELINE configs[1]; MIPLIB not available)",
+            "config": {"workload": f"configs[{CONFIG_ID}] medium planted LP, standard form {m}x{n}, nnz {nnz}",
+                       "iters_per_step": ITERS_PER_STEP, "l2": "flushed (256 MiB write) before every timed step",
+                       "parallelism": "single GPU" if world == 1 else f"replicas x{world} (independent LPs)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "hx::loop_kernel",
+                         "algorithmic_bytes_per_iter": b_iter, "peak_source": peak_kind,
+                         "frac_of_8TBs": achieved / 8000.0},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "iters_per_step": E2E_ITERS,
+                    "path": "hplp_solve_csr (C ABI): upload + A^T build + power iteration + loop + download"},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "time_to_1e-4": ttt,
+            "per_step_ms": [round(1e3 * t, 3) for t in times],
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+    solver.close()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-iters", type=int, default=40)
+    ap.add_argument("--ref-iters", type=int, default=20)
+    ap.add_argument("--ttt-cap", type=float, default=30.0)
+    ap.add_argument("--no-ttt", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

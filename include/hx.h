@@ -114,6 +114,11 @@ int hx_get_certificate(hx_ctx* ctx, int32_t kind, double* vec);
  * products (the limit path of src/solver.cpp:242-254 when no best exists). */
 int hx_kkt_current(hx_ctx* ctx, hplp_kkt_t* out);
 
+/* Diagnostics: per-CTA phase timers when the context was created with
+ * HX_PROFILE=1 in the environment; out holds grid * 8 counters (ns):
+ * phase A, barrier 1, phase B, barrier 2, controller, iterations. */
+int hx_profile(hx_ctx* ctx, unsigned long long* out, int32_t reset);
+
 /* sizeof checks for the ABI tests. */
 int64_t hx_sizeof(int32_t which);
 

@@ -5,13 +5,14 @@ the hx CUDA layer, g++ for the host driver and generator (csrc/Makefile).
 """
 from __future__ import annotations
 
+import os
 import subprocess
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "lib"
-GPU_LIB = LIB / "libhplp_gpu.so"
+GPU_LIB = Path(os.environ["HPLP_GPU_LIB"]) if os.environ.get("HPLP_GPU_LIB") else LIB / "libhplp_gpu.so"
 GEN_LIB = LIB / "libhplp_gen.so"
 
 
@@ -25,5 +26,7 @@ def ensure_built() -> None:
     srcs = [p for p in CSRC.iterdir() if p.suffix in (".cu", ".cuh", ".cpp", ".hpp")]
     srcs += list((PKG.parent / "include").glob("*.h"))
     newest = max(p.stat().st_mtime for p in srcs)
+    if os.environ.get("HPLP_GPU_LIB"):
+        return
     if not GPU_LIB.exists() or not GEN_LIB.exists() or min(GPU_LIB.stat().st_mtime, GEN_LIB.stat().st_mtime) < newest:
         build()

@@ -2,9 +2,11 @@
 // and DESIGN.md.
 //
 // Every rHPDHG iteration runs inside ONE persistent cooperative kernel
-// (loop_kernel): two fused SpMV phases separated by software grid barriers,
-// with the reference's scalar control logic (src/solver.cpp:241-341) executed
-// on the device by the last CTA to arrive at the end-of-iteration barrier.
+// (loop_kernel): two fused SpMV phases separated by software grid barriers.
+// The reference's scalar control logic (src/solver.cpp:241-341) is
+// REPLICATED in every CTA: after the end-of-iteration barrier each CTA
+// reduces the same per-CTA partials in the same fixed order, so all CTAs hold
+// bit-identical totals and take identical decisions with no broadcast step.
 // No host round trip per iteration.
 //
 //   phase A (rows of the explicit A^T = columns j of A):
@@ -18,10 +20,15 @@
 //     (1-w) y+ + w anchor_y and (1-w) ax+ + w ax_anchor, written
 //     speculatively so a non-restart needs no extra pass        [solver.cpp:335-337]
 //     partials ||Ax - b||^2, b.y, ||y - y+||^2, (y - y+).(Ax - Ax+)
-//   controller (last CTA): KKT [pdhg_core.cpp:57-68], canonical residual
+//   controller (every CTA): KKT [pdhg_core.cpp:57-68], canonical residual
 //     [:37-51], epochs, best iterate, termination [solver.cpp:292-295],
 //     certificate-scan scheduling [:297-317], restart [:162-174, :319-332],
 //     buffer roles for the next iteration.
+//
+// SpMV engine: nnz-chunked warp tasks with kLoadsPerLane independent index /
+// value loads per lane in flight, products staged in shared memory, then
+// lane-per-row sums in ascending column order -- for rows up to
+// kStreamRowMax nonzeros this is exactly the reference's summation order.
 //
 // All reductions are fixed-order (static row->warp schedule, fixed trees, no
 // floating-point atomics): results are bit-reproducible run to run.  Device
@@ -31,6 +38,8 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -41,13 +50,9 @@
 
 namespace hx {
 
-// ---------------------------------------------------------------------------
-// Control block in device global memory.  Only the controller (thread 0 of
-// the last-arriving CTA, working on a shared-memory copy) writes it.
-// ---------------------------------------------------------------------------
 enum Mode : int { kModeLoop = 0, kModePower = 1 };
 
-// What every CTA needs for its next phase (copied to shared memory).
+// Buffer roles and per-iteration scalars every thread needs.
 struct Roles {
   int x_src, x_anchor, x_mode, zx_out, xp_out;
   int y_cur, y_anchor, yp_out, yc_out;
@@ -65,12 +70,14 @@ struct Roles {
   double pw_zn;
 };
 
+// Controller state.  Lives in global memory between launches; during a
+// launch every CTA keeps an identical replica in shared memory.
 struct Ctl {
   Roles r;
   long long iteration_limit, check_period, stall_cap, k_star, tau0, trace_period;
   int restart_kind, mode;
-  double tol, cert_tol, beta, sigma_used, b_norm, c_norm, time_limit_s;
-  unsigned long long t0_ns;
+  double tol, cert_tol, beta, sigma_used, b_norm, c_norm;
+  unsigned long long time_budget_ns;  // remaining wall time for this launch
   long long it, n, k, spmv, batch_end, n_epochs;
   double res_epoch_start, best_kkt, best_err[4];
   int x_best, y_best;
@@ -89,11 +96,19 @@ struct Ctl {
   int pw_converged, pw_redraw;
 };
 static_assert(sizeof(Ctl) % 8 == 0, "Ctl copied as 8-byte words");
-static_assert(sizeof(Roles) % 4 == 0, "Roles copied as 4-byte words");
 
 struct GridBar {
-  unsigned count, gen, abort, pad;
+  unsigned long long count;  // monotonic arrivals within one launch
+  unsigned abort;            // watchdog fired
+  unsigned time_up[2];       // time-limit flag, by iteration parity (CTA 0 writes)
+  unsigned pad;
 };
+
+// Slot regions (kMaxQ * grid doubles each).  A CTA may still be reading the
+// totals of one reduction while a faster CTA writes the next one, so every
+// reduction that can overlap its successor has its own region; phases A and
+// B alternate by iteration parity.
+enum Region : int { kRegA = 0, kRegB = 2, kRegC1 = 4, kRegC2 = 5, kRegC3 = 6, kRegPA = 7, kRegPB = 8, kRegions = 9 };
 
 struct KParams {
   Sched A;   // rows of A
@@ -109,6 +124,7 @@ struct KParams {
   Ctl* ctl;
   GridBar* bar;
   hplp_epoch_t* epochs;  // ring of kEpochCap
+  unsigned long long* prof;  // optional per-CTA phase timers [grid][8] (HX_PROFILE=1)
 };
 
 // ---------------------------------------------------------------------------
@@ -123,6 +139,7 @@ __device__ __forceinline__ unsigned long long global_ns() {
 // Vectors written inside the kernel are read at L2 (ld.global.cg): no stale
 // L1 lines across grid barriers.  The matrix, b and c are read-only (ld.nc).
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ double ldca(const double* p) { return __ldca(p); }
 
 __device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }
 
@@ -143,10 +160,22 @@ __device__ __forceinline__ void acc_init(double (&acc)[Q]) {
   for (int q = 0; q < Q; ++q) acc[q] = ((MaxMask >> q) & 1u) ? -INFINITY : 0.0;
 }
 
+template <int Q, unsigned MaxMask>
+__device__ __forceinline__ void acc_add(double (&acc)[Q], const double (&t)[Q]) {
+#pragma unroll
+  for (int q = 0; q < Q; ++q) acc[q] = ((MaxMask >> q) & 1u) ? dmax(acc[q], t[q]) : acc[q] + t[q];
+}
+
+// One shared scratch for every block_to_slots instantiation.
+__device__ __forceinline__ double (*red_buf())[kMaxQ] {
+  __shared__ double red[kWarps][kMaxQ];
+  return red;
+}
+
 // Per-thread accumulators -> slots[q * grid + cta] (fixed order).
 template <int Q, unsigned MaxMask>
 __device__ void block_to_slots(const double (&acc)[Q], double* slots, int grid) {
-  __shared__ double red[kWarps][kMaxQ];
+  double (*red)[kMaxQ] = red_buf();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
@@ -161,7 +190,6 @@ __device__ void block_to_slots(const double (&acc)[Q], double* slots, int grid) 
     for (int w = 1; w < kWarps; ++w) v = mx ? dmax(v, red[w][q]) : v + red[w][q];
     slots[q * grid + blockIdx.x] = v;
   }
-  __syncthreads();
 }
 
 // Warp-level fixed-order reduction of count values at p[i * stride].
@@ -186,81 +214,120 @@ __device__ __forceinline__ double total_of(const double* slots, int grid, int sl
 }
 
 // ---------------------------------------------------------------------------
-// Fused SpMV engine.  Src: gather functor (column -> value).  Epi: row
-// epilogue apply(row, sum, terms[Q]).  Terms of regular rows accumulate per
-// thread; a long row's terms are parked in long_terms by whichever warp
-// finishes the row, so every reduction keeps a fixed order.
+// Fused SpMV engine (task kinds in hx_internal.cuh).
+//
+// Warp w runs tasks w, w + W, ... (static round robin: deterministic and
+// statistically balanced).  Per task each lane issues kLoadsPerLane
+// independent index/value loads and then as many independent gathers --
+// all in registers; B200 measurements (tools/spmv_micro.cu) show register
+// loads with a large L1 beat shared-memory staging for random fp64 gathers.
+// Stream tasks write the products to a 2 KB per-warp buffer and sum them
+// lane-per-row in ascending column order (the reference's own order,
+// src/sparse_matrix.cpp:108-115); pieces are summed warp-wide.  The row
+// epilogue's inputs are loaded before the gathers so their latency overlaps.
+// Epi: load(row) / apply(row, sum, inputs, terms[Q]).  Terms of regular rows
+// accumulate per thread; a long row's terms are parked in long_terms by
+// whichever warp finishes it, so every reduction keeps a fixed order.
 // ---------------------------------------------------------------------------
+struct WarpStage {
+  double prod[kChunk];
+};
+constexpr size_t kStageBytes = sizeof(WarpStage) * kWarps;
+
 template <int Q, unsigned MaxMask, class Src, class Epi>
-__device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& src, Epi& epi,
-                                          double (&acc)[Q], int gwarp, int lane) {
-  const int t_end = S.task_ptr[gwarp + 1];
-  for (int t = S.task_ptr[gwarp]; t < t_end; ++t) {
-    const int4 tk = S.tasks[t];
-    const int lv = tk.z;
-    const int v = 1 << lv;
-    const int sub = lane & (v - 1);
-    const int per_pass = 32 >> lv;
-    for (int r0 = tk.x; r0 < tk.y; r0 += per_pass) {
-      const int r = r0 + (lane >> lv);
-      const bool active = r < tk.y;
+__device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& src, Epi& epi, double (&acc)[Q],
+                                          int gwarp, int lane, WarpStage* st) {
+  const int W = gridDim.x * kWarps;
+  const int* __restrict__ idx = S.idx;
+  const double* __restrict__ val = S.val;
+  for (int t = gwarp; t < S.n_tasks; t += W) {
+    const int4 tk = __ldg(S.tasks + t);
+    const int r0 = tk.x, r1 = tk.y & kRowMask, kind = tk.y >> kKindShift;
+    const int p0 = tk.z, len = tk.w - tk.z;
+    const bool has_row = kind == kTaskStream && lane < r1 - r0;
+    int ra = 0, rb = 0;
+    typename Epi::In in{};
+    if (has_row) {
+      ra = __ldg(S.ptr + r0 + lane);
+      rb = __ldg(S.ptr + r0 + lane + 1);
+      in = epi.load(r0 + lane);
+    }
+    int ci[kLoadsPerLane];
+    double cv[kLoadsPerLane];
+#pragma unroll
+    for (int j = 0; j < kLoadsPerLane; ++j) {
+      const int q = j * 32 + lane;
+      ci[j] = q < len ? __ldg(idx + p0 + q) : 0;
+      cv[j] = q < len ? __ldg(val + p0 + q) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kLoadsPerLane; ++j) {
+      const int q = j * 32 + lane;
+      if (q < len) cv[j] = cv[j] * src(ci[j]);
+    }
+    if (kind == kTaskStream) {
+#pragma unroll
+      for (int j = 0; j < kLoadsPerLane; ++j) st->prod[j * 32 + lane] = cv[j];
+      __syncwarp();
+      if (has_row) {
+        double s = 0.0;
+        for (int q = ra - p0; q < rb - p0; ++q) s += st->prod[q];
+        double tm[Q];
+        epi.apply(r0 + lane, s, in, tm);
+        acc_add<Q, MaxMask>(acc, tm);
+      }
+      __syncwarp();
+    } else {
       double s = 0.0;
-      if (active) {
-        const int p1 = __ldg(S.ptr + r + 1);
-#pragma unroll 4
-        for (int p = __ldg(S.ptr + r) + sub; p < p1; p += v)
-          s += __ldg(S.val + p) * src(__ldg(S.idx + p));
-      }
-      for (int o = v >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (active && sub == 0) {
-        double tm[Q];
-        epi.apply(r, s, tm);
 #pragma unroll
-        for (int q = 0; q < Q; ++q) acc[q] = ((MaxMask >> q) & 1u) ? dmax(acc[q], tm[q]) : acc[q] + tm[q];
+      for (int j = 0; j < kLoadsPerLane; ++j) s += cv[j];
+      s = warp_sum(s);
+      if (lane == 0) {
+        const int4 meta = __ldg(S.meta + t);  // {slot, npieces, counter, index}
+        if (meta.y == 1) {
+          double tm[Q];
+          epi.apply(r0, s, epi.load(r0), tm);
+          acc_add<Q, MaxMask>(acc, tm);
+        } else {
+          double* part = S.piece_part(set);
+          part[meta.x] = s;
+          __threadfence();
+          const unsigned old = atomicAdd(S.piece_cnt(set) + meta.z, 1u);
+          if (old == static_cast<unsigned>(meta.y - 1)) {
+            __threadfence();
+            const int first = meta.x - meta.w;
+            double tot = 0.0;
+            for (int i = 0; i < meta.y; ++i) tot += ldcg(part + first + i);
+            S.piece_cnt(set)[meta.z] = 0u;
+            double tm[Q];
+            epi.apply(r0, tot, epi.load(r0), tm);
+            double* lt = S.long_terms(set) + static_cast<long long>(meta.z) * kMaxQ;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) lt[q] = tm[q];
+          }
+        }
       }
     }
-  }
-  const int pe = S.piece_ptr[gwarp + 1];
-  for (int pi = S.piece_ptr[gwarp]; pi < pe; ++pi) {
-    const Piece pc = S.pieces[pi];
-    double s = 0.0;
-#pragma unroll 4
-    for (int p = pc.p0 + lane; p < pc.p1; p += 32) s += __ldg(S.val + p) * src(__ldg(S.idx + p));
-    s = warp_sum(s);
-    if (lane == 0) {
-      double* part = S.piece_part[set];
-      part[pc.slot] = s;
-      __threadfence();
-      const unsigned old = atomicAdd(S.piece_cnt[set] + pc.counter, 1u);
-      if (old == static_cast<unsigned>(pc.npieces - 1)) {
-        __threadfence();
-        const int first = pc.slot - pc.index;
-        double tot = 0.0;
-        for (int i = 0; i < pc.npieces; ++i) tot += ldcg(part + first + i);
-        S.piece_cnt[set][pc.counter] = 0u;
-        double tm[Q];
-        epi.apply(pc.row, tot, tm);
-        double* lt = S.long_terms[set] + static_cast<long long>(pc.counter) * kMaxQ;
-#pragma unroll
-        for (int q = 0; q < Q; ++q) lt[q] = tm[q];
-      }
-    }
-    __syncwarp();
   }
 }
 
 // ---- gather sources --------------------------------------------------------
+// Kernel-written vectors are gathered through L1 (ld.global.ca would also
+// do): every grid barrier's gpu-scope fence invalidates L1 (CCTL.IVALL), so
+// no stale line survives into the next phase.
 struct SrcVec {
   const double* v;
-  __device__ __forceinline__ double operator()(int j) const { return ldcg(v + j); }
+  __device__ __forceinline__ double operator()(int j) const { return ldca(v + j); }
 };
 struct SrcDiv {  // power iteration: x = z / ||z|| formed on the fly (same rounding)
   const double* v;
   double d;
-  __device__ __forceinline__ double operator()(int j) const { return ldcg(v + j) / d; }
+  __device__ __forceinline__ double operator()(int j) const { return ldca(v + j) / d; }
 };
 
 // ---- epilogues -------------------------------------------------------------
+struct NoIn {};
+
 struct EpiPrimal {  // phase A, rows of A^T
   const double* xs;
   const double* xa;
@@ -269,16 +336,22 @@ struct EpiPrimal {  // phase A, rows of A^T
   double* xp;
   double w, eta;
   int mode;
-  __device__ __forceinline__ void apply(int j, double aty, double (&t)[3]) const {
+  struct In {
+    double xs, xa, c;
+  };
+  __device__ __forceinline__ In load(int j) const {
+    return In{ldcg(xs + j), mode ? ldcg(xa + j) : 0.0, __ldg(c + j)};
+  }
+  __device__ __forceinline__ void apply(int j, double aty, const In& in, double (&t)[3]) const {
     double x;
     if (mode) {
       const double omw = 1.0 - w;
-      x = omw * ldcg(xs + j) + w * ldcg(xa + j);
+      x = omw * in.xs + w * in.xa;
     } else {
-      x = ldcg(xs + j);
+      x = in.xs;
     }
     zx[j] = x;
-    const double cj = __ldg(c + j);
+    const double cj = in.c;
     double xn = x - eta * (aty + cj);
     xn = xn < 0.0 ? 0.0 : xn;
     xp[j] = xn;
@@ -302,16 +375,22 @@ struct EpiDual {  // phase B, rows of A
   double* yc;
   double* axc;
   double eta, w;
-  __device__ __forceinline__ void apply(int i, double s, double (&t)[4]) const {
-    const double yi = ldcg(y + i);
-    const double axi = ldcg(ax + i);
-    const double bi = __ldg(b + i);
+  struct In {
+    double y, ax, b, ya, axa;
+  };
+  __device__ __forceinline__ In load(int i) const {
+    return In{ldcg(y + i), ldcg(ax + i), __ldg(b + i), ldcg(ya + i), ldcg(axa + i)};
+  }
+  __device__ __forceinline__ void apply(int i, double s, const In& in, double (&t)[4]) const {
+    const double yi = in.y;
+    const double axi = in.ax;
+    const double bi = in.b;
     const double ypi = yi + eta * ((2.0 * s - axi) - bi);
     yp[i] = ypi;
     axp[i] = s;
     const double omw = 1.0 - w;
-    yc[i] = omw * ypi + w * ldcg(ya + i);
-    axc[i] = omw * s + w * ldcg(axa + i);
+    yc[i] = omw * ypi + w * in.ya;
+    axc[i] = omw * s + w * in.axa;
     const double d = axi - bi;
     const double dy = yi - ypi;
     const double dax = axi - s;
@@ -324,62 +403,74 @@ struct EpiDual {  // phase B, rows of A
 
 struct EpiStoreSq {  // out = s, term s^2 (power iteration)
   double* out;
-  __device__ __forceinline__ void apply(int r, double s, double (&t)[1]) const {
+  using In = NoIn;
+  __device__ __forceinline__ In load(int) const { return {}; }
+  __device__ __forceinline__ void apply(int r, double s, const In&, double (&t)[1]) const {
     out[r] = s;
     t[0] = s * s;
   }
 };
 
+struct EpiStore {
+  double* out;
+  using In = NoIn;
+  __device__ __forceinline__ In load(int) const { return {}; }
+  __device__ __forceinline__ void apply(int r, double s, const In&, double (&t)[1]) const {
+    out[r] = s;
+    t[0] = 0.0;
+  }
+};
+
 struct EpiPosNeg {  // primal certificate: max(A^T u), max(-A^T u)
-  __device__ __forceinline__ void apply(int, double s, double (&t)[2]) const {
+  using In = NoIn;
+  __device__ __forceinline__ In load(int) const { return {}; }
+  __device__ __forceinline__ void apply(int, double s, const In&, double (&t)[2]) const {
     t[0] = s;
     t[1] = -s;
   }
 };
 
 struct EpiAbs {  // dual certificate: max |A u|
-  __device__ __forceinline__ void apply(int, double s, double (&t)[1]) const { t[0] = fabs(s); }
+  using In = NoIn;
+  __device__ __forceinline__ In load(int) const { return {}; }
+  __device__ __forceinline__ void apply(int, double s, const In&, double (&t)[1]) const { t[0] = fabs(s); }
 };
 
 // ---------------------------------------------------------------------------
-// Grid barrier.  The last CTA to arrive runs ctl() (whole CTA) before the
-// release; everybody else spins (with a 10 s watchdog) on the generation.
+// Grid barrier: one monotonic 64-bit arrival counter per launch (reset by
+// the host before each launch), so a barrier is a single release atomic per
+// CTA plus an acquire spin until count >= (barriers passed) * grid.  A 10 s
+// watchdog turns a hang into HPLP_ETIMEOUT instead of a dead GPU.  The
+// gpu-scope fence after the spin also invalidates this SM's L1
+// (CCTL.IVALL), so L1-cached gathers never see stale lines.
 // ---------------------------------------------------------------------------
-template <class F>
-__device__ bool grid_sync(const KParams& P, F&& ctl) {
-  __shared__ int s_last, s_ok;
-  __shared__ unsigned s_gen;
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ bool grid_sync(GridBar* bar, unsigned long long& target) {
+  __shared__ int s_ok;
   __syncthreads();
+  target += gridDim.x;
   if (threadIdx.x == 0) {
-    const unsigned gen = *reinterpret_cast<volatile unsigned*>(&P.bar->gen);
-    __threadfence();
-    const unsigned arrived = atomicAdd(&P.bar->count, 1u);
-    s_last = arrived == gridDim.x - 1;
-    s_gen = gen;
     s_ok = 1;
-  }
-  __syncthreads();
-  if (s_last) {
     __threadfence();
-    ctl();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      P.bar->count = 0u;
-      __threadfence();
-      atomicAdd(&P.bar->gen, 1u);
-    }
-  } else if (threadIdx.x == 0) {
+    atomicAdd(&bar->count, 1ull);
     const unsigned long long t0 = global_ns();
-    while (*reinterpret_cast<volatile unsigned*>(&P.bar->gen) == s_gen) {
-      if (*reinterpret_cast<volatile unsigned*>(&P.bar->abort)) {
-        s_ok = 0;
-        break;
-      }
-      __nanosleep(32);
-      if (global_ns() - t0 > 10000000000ull) {
-        atomicExch(&P.bar->abort, 1u);
-        s_ok = 0;
-        break;
+    unsigned spins = 0;
+    while (ld_acquire_u64(&bar->count) < target) {
+      if ((++spins & 255u) == 0u) {
+        if (*reinterpret_cast<volatile unsigned*>(&bar->abort)) {
+          s_ok = 0;
+          break;
+        }
+        if (global_ns() - t0 > 10000000000ull) {
+          atomicExch(&bar->abort, 1u);
+          s_ok = 0;
+          break;
+        }
       }
     }
     __threadfence();
@@ -388,36 +479,9 @@ __device__ bool grid_sync(const KParams& P, F&& ctl) {
   return s_ok != 0;
 }
 
-struct NoCtl {
-  __device__ void operator()() const {}
-};
-
-__device__ void load_roles(const Ctl* ctl, Roles& R) {
-  const unsigned* src = reinterpret_cast<const unsigned*>(&ctl->r);
-  unsigned* dst = reinterpret_cast<unsigned*>(&R);
-  for (int i = threadIdx.x; i < static_cast<int>(sizeof(Roles) / 4); i += blockDim.x)
-    dst[i] = __ldcg(src + i);
-  __syncthreads();
-}
-
-__device__ void ctl_load(const Ctl* g, Ctl& s) {
-  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(g);
-  unsigned long long* dst = reinterpret_cast<unsigned long long*>(&s);
-  for (int i = threadIdx.x; i < static_cast<int>(sizeof(Ctl) / 8); i += blockDim.x)
-    dst[i] = __ldcg(src + i);
-  __syncthreads();
-}
-
-__device__ void ctl_store(const Ctl& s, Ctl* g) {
-  __syncthreads();
-  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&s);
-  unsigned long long* dst = reinterpret_cast<unsigned long long*>(g);
-  for (int i = threadIdx.x; i < static_cast<int>(sizeof(Ctl) / 8); i += blockDim.x) dst[i] = src[i];
-  __syncthreads();
-}
-
 // ---------------------------------------------------------------------------
-// Controller logic (thread 0 of the last CTA, on the shared copy).
+// Controller logic (thread 0 of every CTA, on its shared replica).  Only CTA 0
+// (writer) touches global memory (epoch ring).
 // ---------------------------------------------------------------------------
 __device__ int pick_free(int pool, int e0, int e1, int e2, int e3) {
   for (int i = 0; i < pool; ++i)
@@ -440,7 +504,7 @@ __device__ bool should_restart(const Ctl& C, long long n, long long k, double no
 
 __device__ void set_final_limit(Ctl& C, int status) {
   C.status = status;
-  if (C.best_kkt < INFINITY) {  // isfinite(best_kkt): best_kkt only ever decreases from +inf
+  if (C.best_kkt < INFINITY) {  // isfinite(best_kkt): it only ever decreases from +inf
     C.final_x = C.x_best;
     C.final_y = C.y_best;
     for (int q = 0; q < 4; ++q) C.final_kkt[q] = C.best_err[q];
@@ -451,15 +515,15 @@ __device__ void set_final_limit(Ctl& C, int status) {
   C.r.stop = 1;
 }
 
-// Restart decision + Halpern combine bookkeeping + next roles + limits
+// Restart decision + Halpern bookkeeping + next roles + limits
 // (src/solver.cpp:319-341 and the loop-top checks :242-254).
-__device__ void finish_iteration(Ctl& C, hplp_epoch_t* epochs, double res) {
+__device__ void finish_iteration(Ctl& C, hplp_epoch_t* epochs, bool writer, double res, bool time_up) {
   Roles& R = C.r;
   bool restart = should_restart(C, C.n, C.k, res, C.res_epoch_start);
   if (!restart && C.restart_kind == HPLP_RESTART_ADAPTIVE && C.stall_cap > 0 && C.k >= C.stall_cap)
     restart = true;
   if (restart) {
-    if (C.n_epochs > 0) epochs[(C.n_epochs - 1) % kEpochCap].restart_length = C.k;
+    if (writer && C.n_epochs > 0) epochs[(C.n_epochs - 1) % kEpochCap].restart_length = C.k;
     R.x_src = R.xp_out;
     R.x_mode = 0;
     R.x_anchor = R.xp_out;
@@ -490,7 +554,7 @@ __device__ void finish_iteration(Ctl& C, hplp_epoch_t* epochs, double res) {
   R.w_next = 1.0 / static_cast<double>(C.k + 2);
   if (C.it >= C.iteration_limit) {
     set_final_limit(C, HPLP_STATUS_ITERATION_LIMIT);
-  } else if (static_cast<double>(global_ns() - C.t0_ns) * 1e-9 > C.time_limit_s) {
+  } else if (time_up) {
     set_final_limit(C, HPLP_STATUS_TIME_LIMIT);
   }
   if (C.trace_period > 0 && C.last_it % C.trace_period == 0) {
@@ -501,9 +565,8 @@ __device__ void finish_iteration(Ctl& C, hplp_epoch_t* epochs, double res) {
 }
 
 // After phases A+B: KKT, residual, epochs, best, termination, scan or finish.
-__device__ void main_logic(Ctl& C, const double* tot, hplp_epoch_t* epochs) {
+__device__ void main_logic(Ctl& C, const double* tot, hplp_epoch_t* epochs, bool writer, bool time_up) {
   Roles& R = C.r;
-  if (C.t0_ns == 0ull) C.t0_ns = global_ns();
   const double dres = tot[0], cx = tot[1], dx2 = tot[2];
   const double pres = tot[3], by = tot[4], dy2 = tot[5], dyax = tot[6];
   // kkt_error_with_products, src/pdhg_core.cpp:57-68
@@ -533,11 +596,13 @@ __device__ void main_logic(Ctl& C, const double* tot, hplp_epoch_t* epochs) {
   C.spmv += 2;
   if (C.k == 0) {  // src/solver.cpp:261-264
     C.res_epoch_start = res;
-    hplp_epoch_t& e = epochs[C.n_epochs % kEpochCap];
-    e.epoch = C.n;
-    e.restart_length = 0;
-    e.residual_at_start = res;
-    e.kkt_at_start = {kkt[0], kkt[1], kkt[2], kkt[3]};
+    if (writer) {
+      hplp_epoch_t& e = epochs[C.n_epochs % kEpochCap];
+      e.epoch = C.n;
+      e.restart_length = 0;
+      e.residual_at_start = res;
+      e.kkt_at_start = {kkt[0], kkt[1], kkt[2], kkt[3]};
+    }
     C.n_epochs += 1;
   }
   if (kkt[3] < C.best_kkt) {  // :265-269
@@ -573,7 +638,7 @@ __device__ void main_logic(Ctl& C, const double* tot, hplp_epoch_t* epochs) {
     R.cand_scale = C.k >= 1 ? 2.0 / static_cast<double>(C.k) : 0.0;
     return;
   }
-  finish_iteration(C, epochs, res);
+  finish_iteration(C, epochs, writer, res, time_up);
 }
 
 // validate_primal_infeasibility, src/infeasibility.cpp:41-67, from reductions.
@@ -636,7 +701,7 @@ __device__ bool eval_dual(const Ctl& C, int c, hplp_cert_meta_t& rep) {
 
 // CertificateScan::check semantics, src/solver.cpp:108-135 (+ :300-317).
 // Candidates: 0 v_x diff, 1 v_y diff, 2 v_x normalized, 3 v_y normalized.
-__device__ void scan_logic(Ctl& C, hplp_epoch_t* epochs) {
+__device__ void scan_logic(Ctl& C, hplp_epoch_t* epochs, bool writer, bool time_up) {
   Roles& R = C.r;
   hplp_cert_meta_t prim{}, dual{};
   bool have_p = false, have_d = false;
@@ -682,355 +747,403 @@ __device__ void scan_logic(Ctl& C, hplp_epoch_t* epochs) {
     if (C.trace_period > 0 && C.last_it % C.trace_period == 0) C.paused = 1;
     return;
   }
-  finish_iteration(C, epochs, C.last_res);
+  finish_iteration(C, epochs, writer, C.last_res, time_up);
+}
+
+__device__ void ctl_load(const Ctl* g, Ctl& s) {
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(g);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(&s);
+  for (int i = threadIdx.x; i < static_cast<int>(sizeof(Ctl) / 8); i += blockDim.x) dst[i] = __ldcg(src + i);
+  __syncthreads();
+}
+
+__device__ void ctl_store(const Ctl& s, Ctl* g) {
+  __syncthreads();
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(&s);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(g);
+  for (int i = threadIdx.x; i < static_cast<int>(sizeof(Ctl) / 8); i += blockDim.x) dst[i] = src[i];
+}
+
+// ---------------------------------------------------------------------------
+// Phases.  Each is a separate (noinline) function so the register allocator
+// sees one SpMV instantiation at a time; KParams lives in global memory.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double* region_ptr(const KParams* P, int r) {
+  return P->slots + static_cast<size_t>(r) * kMaxQ * gridDim.x;
+}
+
+__device__ __forceinline__ int gwarp_id() { return blockIdx.x * kWarps + (threadIdx.x >> 5); }
+
+// phase A: A^T y, primal step (+ Halpern formation of x), primal partials
+__device__ __noinline__ void phase_primal(const KParams* P, const Roles* R, int par, WarpStage* stage) {
+  const int n = P->n, m = P->m;
+  double acc[3];
+  acc_init<3, 0>(acc);
+  EpiPrimal e{P->xpool + static_cast<size_t>(R->x_src) * n,
+              P->xpool + static_cast<size_t>(R->x_anchor) * n,
+              P->c,
+              P->xpool + static_cast<size_t>(R->zx_out) * n,
+              P->xpool + static_cast<size_t>(R->xp_out) * n,
+              R->w_x,
+              R->eta,
+              R->x_mode};
+  const Sched S = P->AT;
+  spmv_rows<3, 0>(S, par, SrcVec{P->ypool + static_cast<size_t>(R->y_cur) * m}, e, acc, gwarp_id(),
+                  threadIdx.x & 31, stage);
+  block_to_slots<3, 0>(acc, region_ptr(P, kRegA + par), gridDim.x);
+}
+
+// phase B: A x+, dual step, speculative Halpern combos, dual partials
+__device__ __noinline__ void phase_dual(const KParams* P, const Roles* R, int par, WarpStage* stage) {
+  const int n = P->n, m = P->m;
+  double acc[4];
+  acc_init<4, 0>(acc);
+  EpiDual e{P->ypool + static_cast<size_t>(R->y_cur) * m,
+            P->axpool + static_cast<size_t>(R->ax_cur) * m,
+            P->b,
+            P->ypool + static_cast<size_t>(R->y_anchor) * m,
+            P->axpool + static_cast<size_t>(R->ax_anchor) * m,
+            P->ypool + static_cast<size_t>(R->yp_out) * m,
+            P->axpool + static_cast<size_t>(R->axp_out) * m,
+            P->ypool + static_cast<size_t>(R->yc_out) * m,
+            P->axpool + static_cast<size_t>(R->axc_out) * m,
+            R->eta,
+            R->w_next};
+  const Sched S = P->A;
+  spmv_rows<4, 0>(S, par, SrcVec{P->xpool + static_cast<size_t>(R->xp_out) * n}, e, acc, gwarp_id(),
+                  threadIdx.x & 31, stage);
+  block_to_slots<4, 0>(acc, region_ptr(P, kRegB + par), gridDim.x);
+}
+
+// totals of phases A+B (warps 0..6) -> tot[0..6]
+__device__ __noinline__ void totals_main(const KParams* P, int par, double* tot) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  if (warp < 3) {
+    const double t = total_of(region_ptr(P, kRegA + par), G, warp, P->AT.long_terms(par), P->AT.n_long, warp, false);
+    if (lane == 0) tot[warp] = t;
+  } else if (warp < 7) {
+    const double t =
+        total_of(region_ptr(P, kRegB + par), G, warp - 3, P->A.long_terms(par), P->A.n_long, warp - 3, false);
+    if (lane == 0) tot[warp] = t;
+  }
+}
+
+// power iteration halves: w = A x (x = x0 or z / zn), z = A^T w
+__device__ __noinline__ void power_a(const KParams* P, const Roles* R, WarpStage* stage) {
+  double acc[1];
+  acc_init<1, 0>(acc);
+  EpiStoreSq e{P->ypool};
+  const Sched S = P->A;
+  if (R->pw_mode == 0) spmv_rows<1, 0>(S, 0, SrcVec{P->xpool}, e, acc, gwarp_id(), threadIdx.x & 31, stage);
+  else spmv_rows<1, 0>(S, 0, SrcDiv{P->xpool + P->n, R->pw_zn}, e, acc, gwarp_id(), threadIdx.x & 31, stage);
+  block_to_slots<1, 0>(acc, region_ptr(P, kRegPA), gridDim.x);
+}
+
+__device__ __noinline__ void power_b(const KParams* P, WarpStage* stage) {
+  double acc[1];
+  acc_init<1, 0>(acc);
+  EpiStoreSq e{P->xpool + P->n};
+  const Sched S = P->AT;
+  spmv_rows<1, 0>(S, 0, SrcVec{P->ypool}, e, acc, gwarp_id(), threadIdx.x & 31, stage);
+  block_to_slots<1, 0>(acc, region_ptr(P, kRegPB), gridDim.x);
+}
+
+// certificate scan C1: candidate norms and finiteness
+__device__ __noinline__ void cert_norms(const KParams* P, const Roles* R) {
+  const int n = P->n, m = P->m;
+  const int gtid = blockIdx.x * kThreads + threadIdx.x, gs = gridDim.x * kThreads;
+  const double* zx = P->xpool + static_cast<size_t>(R->zx_out) * n;
+  const double* xp = P->xpool + static_cast<size_t>(R->xp_out) * n;
+  const double* xa = P->xpool + static_cast<size_t>(R->x_anchor) * n;
+  const double* yc = P->ypool + static_cast<size_t>(R->y_cur) * m;
+  const double* yp = P->ypool + static_cast<size_t>(R->yp_out) * m;
+  const double* ya = P->ypool + static_cast<size_t>(R->y_anchor) * m;
+  double acc[8];
+  acc_init<8, 0>(acc);
+  const double s = R->cand_scale;
+  for (int j = gtid; j < n; j += gs) {
+    const double x = ldcg(zx + j);
+    const double vd = ldcg(xp + j) - x;
+    const double vn = s * (x - ldcg(xa + j));
+    acc[0] += vd * vd;
+    acc[2] += vn * vn;
+    acc[4] += isfinite(vd) ? 0.0 : 1.0;
+    acc[6] += isfinite(vn) ? 0.0 : 1.0;
+  }
+  for (int i = gtid; i < m; i += gs) {
+    const double y = ldcg(yc + i);
+    const double vd = ldcg(yp + i) - y;
+    const double vn = s * (y - ldcg(ya + i));
+    acc[1] += vd * vd;
+    acc[3] += vn * vn;
+    acc[5] += isfinite(vd) ? 0.0 : 1.0;
+    acc[7] += isfinite(vn) ? 0.0 : 1.0;
+  }
+  block_to_slots<8, 0>(acc, region_ptr(P, kRegC1), gridDim.x);
+}
+
+// certificate scan C2: unit vectors u = v / ||v|| and their reductions
+__device__ __noinline__ void cert_units(const KParams* P, const Roles* R) {
+  const int n = P->n, m = P->m;
+  const int gtid = blockIdx.x * kThreads + threadIdx.x, gs = gridDim.x * kThreads;
+  const double* zx = P->xpool + static_cast<size_t>(R->zx_out) * n;
+  const double* xp = P->xpool + static_cast<size_t>(R->xp_out) * n;
+  const double* xa = P->xpool + static_cast<size_t>(R->x_anchor) * n;
+  const double* yc = P->ypool + static_cast<size_t>(R->y_cur) * m;
+  const double* yp = P->ypool + static_cast<size_t>(R->yp_out) * m;
+  const double* ya = P->ypool + static_cast<size_t>(R->y_anchor) * m;
+  double acc[12];
+  acc_init<12, 0x577u>(acc);
+  const double s = R->cand_scale;
+  double* u0 = P->upool;
+  double* u2 = P->upool + n;
+  double* u1 = P->upool + 2 * static_cast<size_t>(n);
+  double* u3 = u1 + m;
+  for (int j = gtid; j < n; j += gs) {
+    const double x = ldcg(zx + j);
+    const double cj = __ldg(P->c + j);
+    if (R->cand_on[0]) {
+      const double u = (ldcg(xp + j) - x) / R->cn2[0];
+      u0[j] = u;
+      acc[0] = dmax(acc[0], fabs(u));
+      acc[1] = dmax(acc[1], u);
+      acc[2] = dmax(acc[2], -u);
+      acc[3] += cj * u;
+    }
+    if (R->cand_on[2]) {
+      const double u = (s * (x - ldcg(xa + j))) / R->cn2[2];
+      u2[j] = u;
+      acc[4] = dmax(acc[4], fabs(u));
+      acc[5] = dmax(acc[5], u);
+      acc[6] = dmax(acc[6], -u);
+      acc[7] += cj * u;
+    }
+  }
+  for (int i = gtid; i < m; i += gs) {
+    const double y = ldcg(yc + i);
+    const double bi = __ldg(P->b + i);
+    if (R->cand_on[1]) {
+      const double u = (ldcg(yp + i) - y) / R->cn2[1];
+      u1[i] = u;
+      acc[8] = dmax(acc[8], fabs(u));
+      acc[9] += bi * u;
+    }
+    if (R->cand_on[3]) {
+      const double u = (s * (y - ldcg(ya + i))) / R->cn2[3];
+      u3[i] = u;
+      acc[10] = dmax(acc[10], fabs(u));
+      acc[11] += bi * u;
+    }
+  }
+  block_to_slots<12, 0x577u>(acc, region_ptr(P, kRegC2), gridDim.x);
+}
+
+// certificate scan C3: the validation SpMVs, up to four independent products
+__device__ __noinline__ void cert_products(const KParams* P, const Roles* R, WarpStage* stage) {
+  const int n = P->n, m = P->m;
+  double acc[6];
+  acc_init<6, 0x3Fu>(acc);
+  const double* u0 = P->upool;
+  const double* u2 = P->upool + n;
+  const double* u1 = P->upool + 2 * static_cast<size_t>(n);
+  const double* u3 = u1 + m;
+  const int gw = gwarp_id(), lane = threadIdx.x & 31;
+  const Sched AT = P->AT;
+  const Sched A = P->A;
+  for (int k = 0; k < 2; ++k) {
+    if (R->cand_on[1 + 2 * k]) {
+      double a2[2];
+      acc_init<2, 3u>(a2);
+      EpiPosNeg e;
+      spmv_rows<2, 3u>(AT, 2 + k, SrcVec{k ? u3 : u1}, e, a2, gw, lane, stage);
+      acc[2 * k] = a2[0], acc[2 * k + 1] = a2[1];
+    }
+    if (R->cand_on[2 * k]) {
+      double a1[1];
+      acc_init<1, 1u>(a1);
+      EpiAbs e;
+      spmv_rows<1, 1u>(A, 2 + k, SrcVec{k ? u2 : u0}, e, a1, gw, lane, stage);
+      acc[4 + k] = a1[0];
+    }
+  }
+  block_to_slots<6, 0x3Fu>(acc, region_ptr(P, kRegC3), gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
 // The persistent loop kernel.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads, 2) loop_kernel(KParams P) {
-  __shared__ Roles R;
-  __shared__ Ctl sC;
+__global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid_constant__ KParams KP) {
+  const KParams* P = &KP;  // constant bank; no local copy (grid_constant)
+  __shared__ Ctl C;
   __shared__ double tot[kMaxQ];
+  __shared__ int s_time_up;
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
   const int G = gridDim.x;
   const int lane = threadIdx.x & 31;
-  const int gwarp = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const int gtid = blockIdx.x * kThreads + threadIdx.x;
-  const int gstride = G * kThreads;
-  const int n = P.n, m = P.m;
-  load_roles(P.ctl, R);
-  const int mode = __ldcg(&P.ctl->mode);
+  const int warp = threadIdx.x >> 5;
+  const bool writer = blockIdx.x == 0;
+  WarpStage* stage = reinterpret_cast<WarpStage*>(dyn_smem) + warp;
+  const unsigned long long t_start = global_ns();
+  ctl_load(P->ctl, C);
+  const unsigned long long budget = C.time_budget_ns;
+  const Roles* R = &C.r;
+  GridBar* bar = P->bar;
+  unsigned long long target = 0;
 
-  if (mode == kModePower) {
+  if (C.mode == kModePower) {
     // power_iteration loop body, src/sparse_matrix.cpp:153-177
-    double* x0 = P.xpool;
-    double* z = P.xpool + n;
-    double* w = P.ypool;
-    while (!R.stop) {
-      {
-        double acc[1];
-        acc_init<1, 0>(acc);
-        EpiStoreSq e{w};
-        if (R.pw_mode == 0) spmv_rows<1, 0>(P.A, 0, SrcVec{x0}, e, acc, gwarp, lane);
-        else spmv_rows<1, 0>(P.A, 0, SrcDiv{z, R.pw_zn}, e, acc, gwarp, lane);
-        block_to_slots<1, 0>(acc, P.slots, G);
+    while (!R->stop) {
+      power_a(P, R, stage);
+      if (!grid_sync(bar, target)) return;
+      if (warp == 0) {
+        const double t = total_of(region_ptr(P, kRegPA), G, 0, P->A.long_terms(0), P->A.n_long, 0, false);
+        if (lane == 0) tot[0] = t;
       }
-      bool ok = grid_sync(P, [&] {
-        ctl_load(P.ctl, sC);
-        if ((threadIdx.x >> 5) == 0) {
-          const double t = total_of(P.slots, G, 0, P.A.long_terms[0], P.A.n_long, 0, false);
-          if (lane == 0) tot[0] = t;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const double sigma = sqrt(tot[0]);
+        C.pw_iters = C.pw_k + 1;
+        C.pw_sigma_cur = sigma;
+        if (sigma == 0.0) {
+          C.pw_redraw = 1;
+          C.r.stop = 1;
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          const double sigma = sqrt(tot[0]);
-          sC.pw_iters = sC.pw_k + 1;
-          sC.pw_sigma_cur = sigma;
-          if (sigma == 0.0) {
-            sC.pw_redraw = 1;
-            sC.r.stop = 1;
-          }
-        }
-        ctl_store(sC, P.ctl);
-      });
-      if (!ok) return;
-      load_roles(P.ctl, R);
-      if (R.stop) break;
-      {
-        double acc[1];
-        acc_init<1, 0>(acc);
-        EpiStoreSq e{z};
-        spmv_rows<1, 0>(P.AT, 0, SrcVec{w}, e, acc, gwarp, lane);
-        block_to_slots<1, 0>(acc, P.slots, G);
       }
-      ok = grid_sync(P, [&] {
-        ctl_load(P.ctl, sC);
-        if ((threadIdx.x >> 5) == 0) {
-          const double t = total_of(P.slots, G, 0, P.AT.long_terms[0], P.AT.n_long, 0, false);
-          if (lane == 0) tot[0] = t;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          const double sigma = sC.pw_sigma_cur;
-          sC.pw_sigma = sigma;
-          if (sC.pw_k > 0 && fabs(sigma - sC.pw_sigma_prev) <= sC.pw_tol * sigma) {
-            sC.pw_converged = 1;
-            sC.r.stop = 1;
+      __syncthreads();
+      if (R->stop) break;
+      power_b(P, stage);
+      if (!grid_sync(bar, target)) return;
+      if (warp == 0) {
+        const double t = total_of(region_ptr(P, kRegPB), G, 0, P->AT.long_terms(0), P->AT.n_long, 0, false);
+        if (lane == 0) tot[1] = t;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const double sigma = C.pw_sigma_cur;
+        C.pw_sigma = sigma;
+        if (C.pw_k > 0 && fabs(sigma - C.pw_sigma_prev) <= C.pw_tol * sigma) {
+          C.pw_converged = 1;
+          C.r.stop = 1;
+        } else {
+          C.pw_sigma_prev = sigma;
+          const double zn = sqrt(tot[1]);
+          if (zn == 0.0) {
+            C.pw_converged = 1;
+            C.r.stop = 1;
           } else {
-            sC.pw_sigma_prev = sigma;
-            const double zn = sqrt(tot[0]);
-            if (zn == 0.0) {
-              sC.pw_converged = 1;
-              sC.r.stop = 1;
-            } else {
-              sC.r.pw_mode = 1;
-              sC.r.pw_zn = zn;
-              sC.pw_k += 1;
-              if (sC.pw_k >= sC.pw_max) sC.r.stop = 1;
-            }
+            C.r.pw_mode = 1;
+            C.r.pw_zn = zn;
+            C.pw_k += 1;
+            if (C.pw_k >= C.pw_max) C.r.stop = 1;
           }
         }
-        ctl_store(sC, P.ctl);
-      });
-      if (!ok) return;
-      load_roles(P.ctl, R);
+      }
+      __syncthreads();
     }
+    if (writer) ctl_store(C, P->ctl);
     return;
   }
 
-  while (!R.stop) {
-    // ---- phase A: A^T y, primal step, primal partials ----
-    {
-      double acc[3];
-      acc_init<3, 0>(acc);
-      EpiPrimal e{P.xpool + static_cast<size_t>(R.x_src) * n,
-                  P.xpool + static_cast<size_t>(R.x_anchor) * n,
-                  P.c,
-                  P.xpool + static_cast<size_t>(R.zx_out) * n,
-                  P.xpool + static_cast<size_t>(R.xp_out) * n,
-                  R.w_x,
-                  R.eta,
-                  R.x_mode};
-      spmv_rows<3, 0>(P.AT, 0, SrcVec{P.ypool + static_cast<size_t>(R.y_cur) * m}, e, acc, gwarp,
-                      lane);
-      block_to_slots<3, 0>(acc, P.slots, G);
+  unsigned long long* prof = P->prof ? P->prof + blockIdx.x * 8 : nullptr;
+  unsigned long long tp = global_ns(), pacc[6] = {0, 0, 0, 0, 0, 0};
+  auto mark = [&](int k) {
+    if (prof && threadIdx.x == 0) {
+      const unsigned long long t = global_ns();
+      pacc[k] += t - tp;
+      tp = t;
     }
-    if (!grid_sync(P, NoCtl{})) return;
-    // ---- phase B: A x+, dual step, speculative Halpern combos, partials ----
-    {
-      double acc[4];
-      acc_init<4, 0>(acc);
-      EpiDual e{P.ypool + static_cast<size_t>(R.y_cur) * m,
-                P.axpool + static_cast<size_t>(R.ax_cur) * m,
-                P.b,
-                P.ypool + static_cast<size_t>(R.y_anchor) * m,
-                P.axpool + static_cast<size_t>(R.ax_anchor) * m,
-                P.ypool + static_cast<size_t>(R.yp_out) * m,
-                P.axpool + static_cast<size_t>(R.axp_out) * m,
-                P.ypool + static_cast<size_t>(R.yc_out) * m,
-                P.axpool + static_cast<size_t>(R.axc_out) * m,
-                R.eta,
-                R.w_next};
-      spmv_rows<4, 0>(P.A, 0, SrcVec{P.xpool + static_cast<size_t>(R.xp_out) * n}, e, acc, gwarp,
-                      lane);
-      block_to_slots<4, 0>(acc, P.slots + 3 * G, G);
-    }
-    if (!grid_sync(P, [&] {
-          ctl_load(P.ctl, sC);
-          const int wq = threadIdx.x >> 5;
-          if (wq < 7) {
-            const Sched& S = wq < 3 ? P.AT : P.A;
-            const double t = total_of(P.slots, G, wq, S.long_terms[0], S.n_long, wq < 3 ? wq : wq - 3, false);
-            if (lane == 0) tot[wq] = t;
-          }
-          __syncthreads();
-          if (threadIdx.x == 0) main_logic(sC, tot, P.epochs);
-          ctl_store(sC, P.ctl);
-        }))
-      return;
-    load_roles(P.ctl, R);
-    if (!R.check) continue;
+  };
+  while (!R->stop) {
+    const int par = static_cast<int>(C.it & 1);
+    phase_primal(P, R, par, stage);
+    if (writer && threadIdx.x == 0 && budget != 0ull)
+      bar->time_up[par] = (global_ns() - t_start) > budget ? 1u : 0u;
+    mark(0);
+    if (!grid_sync(bar, target)) return;
+    mark(1);
+    phase_dual(P, R, par, stage);
+    mark(2);
+    if (!grid_sync(bar, target)) return;
+    mark(3);
+    totals_main(P, par, tot);
+    if (threadIdx.x == 7 * 32) s_time_up = budget != 0ull && *reinterpret_cast<volatile unsigned*>(&bar->time_up[par]) != 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) main_logic(C, tot, P->epochs, writer, s_time_up != 0);
+    __syncthreads();
+    mark(4);
+    if (prof && threadIdx.x == 0) pacc[5] += 1;
+    if (!R->check) continue;
 
     // ---- certificate scan (src/solver.cpp:297-317) ----
-    // C1: candidate norms and finiteness.
-    const double* zx = P.xpool + static_cast<size_t>(R.zx_out) * n;
-    const double* xp = P.xpool + static_cast<size_t>(R.xp_out) * n;
-    const double* xa = P.xpool + static_cast<size_t>(R.x_anchor) * n;
-    const double* yc = P.ypool + static_cast<size_t>(R.y_cur) * m;
-    const double* yp = P.ypool + static_cast<size_t>(R.yp_out) * m;
-    const double* ya = P.ypool + static_cast<size_t>(R.y_anchor) * m;
-    {
-      double acc[8];
-      acc_init<8, 0>(acc);
-      const double s = R.cand_scale;
-      for (int j = gtid; j < n; j += gstride) {
-        const double x = ldcg(zx + j);
-        const double vd = ldcg(xp + j) - x;
-        const double vn = s * (x - ldcg(xa + j));
-        acc[0] += vd * vd;
-        acc[2] += vn * vn;
-        acc[4] += isfinite(vd) ? 0.0 : 1.0;
-        acc[6] += isfinite(vn) ? 0.0 : 1.0;
-      }
-      for (int i = gtid; i < m; i += gstride) {
-        const double y = ldcg(yc + i);
-        const double vd = ldcg(yp + i) - y;
-        const double vn = s * (y - ldcg(ya + i));
-        acc[1] += vd * vd;
-        acc[3] += vn * vn;
-        acc[5] += isfinite(vd) ? 0.0 : 1.0;
-        acc[7] += isfinite(vn) ? 0.0 : 1.0;
-      }
-      block_to_slots<8, 0>(acc, P.slots, G);
+    cert_norms(P, R);
+    if (!grid_sync(bar, target)) return;
+    if (warp < 8) {
+      const double t = total_of(region_ptr(P, kRegC1), G, warp, nullptr, 0, 0, false);
+      if (lane == 0) tot[warp] = t;
     }
-    if (!grid_sync(P, [&] {
-          ctl_load(P.ctl, sC);
-          const int wq = threadIdx.x >> 5;
-          if (wq < 8) {
-            const double t = total_of(P.slots, G, wq, nullptr, 0, 0, false);
-            if (lane == 0) tot[wq] = t;
-          }
-          __syncthreads();
-          if (threadIdx.x == 0) {
-            Roles& RR = sC.r;
-            int any = 0;
-            for (int c = 0; c < 4; ++c) {
-              RR.cn2[c] = sqrt(tot[c]);
-              sC.cfinite[c] = tot[4 + c] == 0.0;
-              const bool normalized = c >= 2;
-              RR.cand_on[c] = (!normalized || sC.last_k >= 1) && RR.cn2[c] > 0.0 && sC.cfinite[c];
-              any |= RR.cand_on[c];
-            }
-            if (!any) scan_logic(sC, P.epochs);  // nothing to validate
-          }
-          ctl_store(sC, P.ctl);
-        }))
-      return;
-    load_roles(P.ctl, R);
-    if (!R.check) continue;
-    // C2: unit vectors u = v / ||v|| and their reductions.
-    {
-      double acc[12];
-      acc_init<12, 0x577u>(acc);
-      const double s = R.cand_scale;
-      double* u0 = P.upool;
-      double* u2 = P.upool + n;
-      double* u1 = P.upool + 2 * static_cast<size_t>(n);
-      double* u3 = u1 + m;
-      for (int j = gtid; j < n; j += gstride) {
-        const double x = ldcg(zx + j);
-        const double cj = __ldg(P.c + j);
-        if (R.cand_on[0]) {
-          const double u = (ldcg(xp + j) - x) / R.cn2[0];
-          u0[j] = u;
-          acc[0] = dmax(acc[0], fabs(u));
-          acc[1] = dmax(acc[1], u);
-          acc[2] = dmax(acc[2], -u);
-          acc[3] += cj * u;
-        }
-        if (R.cand_on[2]) {
-          const double u = (s * (x - ldcg(xa + j))) / R.cn2[2];
-          u2[j] = u;
-          acc[4] = dmax(acc[4], fabs(u));
-          acc[5] = dmax(acc[5], u);
-          acc[6] = dmax(acc[6], -u);
-          acc[7] += cj * u;
-        }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int any = 0;
+      for (int c = 0; c < 4; ++c) {
+        C.r.cn2[c] = sqrt(tot[c]);
+        C.cfinite[c] = tot[4 + c] == 0.0;
+        const bool normalized = c >= 2;
+        C.r.cand_on[c] = (!normalized || C.last_k >= 1) && C.r.cn2[c] > 0.0 && C.cfinite[c];
+        any |= C.r.cand_on[c];
       }
-      for (int i = gtid; i < m; i += gstride) {
-        const double y = ldcg(yc + i);
-        const double bi = __ldg(P.b + i);
-        if (R.cand_on[1]) {
-          const double u = (ldcg(yp + i) - y) / R.cn2[1];
-          u1[i] = u;
-          acc[8] = dmax(acc[8], fabs(u));
-          acc[9] += bi * u;
-        }
-        if (R.cand_on[3]) {
-          const double u = (s * (y - ldcg(ya + i))) / R.cn2[3];
-          u3[i] = u;
-          acc[10] = dmax(acc[10], fabs(u));
-          acc[11] += bi * u;
-        }
-      }
-      block_to_slots<12, 0x577u>(acc, P.slots, G);
+      if (!any) scan_logic(C, P->epochs, writer, s_time_up != 0);  // nothing to validate
     }
-    if (!grid_sync(P, [&] {
-          ctl_load(P.ctl, sC);
-          const int wq = threadIdx.x >> 5;
-          if (wq < 12) {
-            const double t = total_of(P.slots, G, wq, nullptr, 0, 0, ((0x577u >> wq) & 1u) != 0);
-            if (lane == 0) tot[wq] = t;
-          }
-          __syncthreads();
-          if (threadIdx.x == 0) {
-            sC.cinf[0] = tot[0], sC.cmax_u[0] = tot[1], sC.cmax_negu[0] = tot[2], sC.cdot[0] = tot[3];
-            sC.cinf[2] = tot[4], sC.cmax_u[2] = tot[5], sC.cmax_negu[2] = tot[6], sC.cdot[2] = tot[7];
-            sC.cinf[1] = tot[8], sC.cdot[1] = tot[9];
-            sC.cinf[3] = tot[10], sC.cdot[3] = tot[11];
-          }
-          ctl_store(sC, P.ctl);
-        }))
-      return;
-    load_roles(P.ctl, R);
-    // C3: the validation SpMVs, up to four independent products.
-    {
-      double acc[6];
-      acc_init<6, 0x3Fu>(acc);
-      const double* u0 = P.upool;
-      const double* u2 = P.upool + n;
-      const double* u1 = P.upool + 2 * static_cast<size_t>(n);
-      const double* u3 = u1 + m;
-      if (R.cand_on[1]) {
-        double a2[2];
-        acc_init<2, 3u>(a2);
-        EpiPosNeg e;
-        spmv_rows<2, 3u>(P.AT, 0, SrcVec{u1}, e, a2, gwarp, lane);
-        acc[0] = a2[0], acc[1] = a2[1];
-      }
-      if (R.cand_on[3]) {
-        double a2[2];
-        acc_init<2, 3u>(a2);
-        EpiPosNeg e;
-        spmv_rows<2, 3u>(P.AT, 1, SrcVec{u3}, e, a2, gwarp, lane);
-        acc[2] = a2[0], acc[3] = a2[1];
-      }
-      if (R.cand_on[0]) {
-        double a1[1];
-        acc_init<1, 1u>(a1);
-        EpiAbs e;
-        spmv_rows<1, 1u>(P.A, 0, SrcVec{u0}, e, a1, gwarp, lane);
-        acc[4] = a1[0];
-      }
-      if (R.cand_on[2]) {
-        double a1[1];
-        acc_init<1, 1u>(a1);
-        EpiAbs e;
-        spmv_rows<1, 1u>(P.A, 1, SrcVec{u2}, e, a1, gwarp, lane);
-        acc[5] = a1[0];
-      }
-      block_to_slots<6, 0x3Fu>(acc, P.slots, G);
+    __syncthreads();
+    if (!R->check) continue;
+    cert_units(P, R);
+    if (!grid_sync(bar, target)) return;
+    if (warp < 12) {
+      const double t = total_of(region_ptr(P, kRegC2), G, warp, nullptr, 0, 0, ((0x577u >> warp) & 1u) != 0);
+      if (lane == 0) tot[warp] = t;
     }
-    if (!grid_sync(P, [&] {
-          ctl_load(P.ctl, sC);
-          const int wq = threadIdx.x >> 5;
-          if (wq < 6) {
-            const Sched& S = wq < 4 ? P.AT : P.A;
-            const int set = wq < 4 ? (wq >> 1) : (wq - 4);
-            const int lq = wq < 4 ? (wq & 1) : 0;
-            const double t = total_of(P.slots, G, wq, S.long_terms[set], S.n_long, lq, true);
-            if (lane == 0) tot[wq] = t;
-          }
-          __syncthreads();
-          if (threadIdx.x == 0) {
-            sC.cmax_at[1] = tot[0], sC.cmax_negat[1] = tot[1];
-            sC.cmax_at[3] = tot[2], sC.cmax_negat[3] = tot[3];
-            sC.cmax_abs_au[0] = tot[4], sC.cmax_abs_au[2] = tot[5];
-            scan_logic(sC, P.epochs);
-          }
-          ctl_store(sC, P.ctl);
-        }))
-      return;
-    load_roles(P.ctl, R);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      C.cinf[0] = tot[0], C.cmax_u[0] = tot[1], C.cmax_negu[0] = tot[2], C.cdot[0] = tot[3];
+      C.cinf[2] = tot[4], C.cmax_u[2] = tot[5], C.cmax_negu[2] = tot[6], C.cdot[2] = tot[7];
+      C.cinf[1] = tot[8], C.cdot[1] = tot[9];
+      C.cinf[3] = tot[10], C.cdot[3] = tot[11];
+    }
+    __syncthreads();
+    cert_products(P, R, stage);
+    if (!grid_sync(bar, target)) return;
+    if (warp < 6) {
+      const int set = 2 + (warp < 4 ? (warp >> 1) : (warp - 4));
+      const int lq = warp < 4 ? (warp & 1) : 0;
+      const double* lt = warp < 4 ? P->AT.long_terms(set) : P->A.long_terms(set);
+      const int nl = warp < 4 ? P->AT.n_long : P->A.n_long;
+      const double t = total_of(region_ptr(P, kRegC3), G, warp, lt, nl, lq, true);
+      if (lane == 0) tot[warp] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      C.cmax_at[1] = tot[0], C.cmax_negat[1] = tot[1];
+      C.cmax_at[3] = tot[2], C.cmax_negat[3] = tot[3];
+      C.cmax_abs_au[0] = tot[4], C.cmax_abs_au[2] = tot[5];
+      scan_logic(C, P->epochs, writer, s_time_up != 0);
+    }
+    __syncthreads();
   }
+  if (prof && threadIdx.x == 0)
+    for (int k = 0; k < 6; ++k) prof[k] += pacc[k];
+  if (writer) ctl_store(C, P->ctl);
 }
 
 // ---------------------------------------------------------------------------
 // Standalone kernels (setup, boundary SpMVs, results)
 // ---------------------------------------------------------------------------
-struct EpiStore {
-  double* out;
-  __device__ __forceinline__ void apply(int r, double s, double (&t)[1]) const {
-    out[r] = s;
-    t[0] = 0.0;
-  }
-};
-
-__global__ void __launch_bounds__(kThreads, 2) spmv_store_kernel(Sched S, const double* x, double* out) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) spmv_store_kernel(Sched S, const double* x, double* out) {
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
   double acc[1];
   acc_init<1, 0>(acc);
   EpiStore e{out};
-  spmv_rows<1, 0>(S, 0, SrcVec{x}, e, acc, blockIdx.x * kWarps + (threadIdx.x >> 5), threadIdx.x & 31);
+  spmv_rows<1, 0>(S, 0, SrcVec{x}, e, acc, blockIdx.x * kWarps + (threadIdx.x >> 5), threadIdx.x & 31,
+                  reinterpret_cast<WarpStage*>(dyn_smem) + (threadIdx.x >> 5));
 }
 
 __global__ void combine_kernel(int len, double w, const double* a, const double* b, double* out) {
@@ -1049,9 +1162,8 @@ __global__ void cert_kernel(int len, int normalized, double scale, double factor
   }
 }
 
-// Fixed-order sums of squares / products for setup norms and kkt_current.
-// which: 0 -> ||v||^2 ; 1 -> KKT partials (needs ax, b, aty, c, x, y).
-__global__ void __launch_bounds__(kThreads, 2)
+// Fixed-order partial sums for the setup norms and kkt_current.
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
 kkt_partials_kernel(int m, int n, const double* ax, const double* b, const double* aty,
                     const double* c, const double* x, const double* y, double* slots) {
   double acc[6];
@@ -1147,12 +1259,10 @@ namespace {
 
 struct DevSched {
   int4* tasks = nullptr;
-  int* task_ptr = nullptr;
-  Piece* pieces = nullptr;
-  int* piece_ptr = nullptr;
-  double* part = nullptr;    // 2 * n_slots
-  unsigned* cnt = nullptr;   // 2 * n_long
-  double* terms = nullptr;   // 2 * n_long * kMaxQ
+  int4* meta = nullptr;
+  double* part = nullptr;    // 4 * n_slots
+  unsigned* cnt = nullptr;   // 4 * n_long
+  double* terms = nullptr;   // 4 * n_long * kMaxQ
   Sched view;
   double max_cost = 0, mean_cost = 0;
 };
@@ -1187,9 +1297,12 @@ struct hx_ctx {
   double* scratch = nullptr;  // kMaxQ doubles
   Ctl* ctl = nullptr;
   GridBar* bar = nullptr;
+  KParams* kparams = nullptr;
+  unsigned long long* prof = nullptr;  // HX_PROFILE=1: per-CTA phase timers
   hplp_epoch_t* epochs = nullptr;
   Ctl h;  // host mirror
   double b_norm = 0, c_norm = 0;
+  double time_limit_s = 0, loop_elapsed_s = 0;  // SolverConfig::time_limit_seconds budget of the loop
 };
 
 namespace {
@@ -1220,7 +1333,7 @@ void dfree(void* p) {
 }
 
 void free_sched(DevSched& s) {
-  dfree(s.tasks), dfree(s.task_ptr), dfree(s.pieces), dfree(s.piece_ptr);
+  dfree(s.tasks), dfree(s.meta);
   dfree(s.part), dfree(s.cnt), dfree(s.terms);
   s = DevSched{};
 }
@@ -1239,20 +1352,16 @@ int upload_sched(hx_ctx* ctx, DevSched& d, const int* ptr_host, int rows, int co
                  const int* didx, const double* dval) {
   SchedHost h = build_schedule(ptr_host, rows, ctx->grid * kWarps);
   HX_CUDA(ctx, dalloc(&d.tasks, h.tasks.size()));
-  HX_CUDA(ctx, dalloc(&d.task_ptr, h.task_ptr.size()));
-  HX_CUDA(ctx, dalloc(&d.pieces, h.pieces.size()));
-  HX_CUDA(ctx, dalloc(&d.piece_ptr, h.piece_ptr.size()));
-  HX_CUDA(ctx, dalloc(&d.part, 2 * static_cast<size_t>(h.n_slots)));
-  HX_CUDA(ctx, dalloc(&d.cnt, 2 * static_cast<size_t>(h.n_long)));
-  HX_CUDA(ctx, dalloc(&d.terms, 2 * static_cast<size_t>(h.n_long) * kMaxQ));
+  HX_CUDA(ctx, dalloc(&d.meta, h.meta.size()));
+  HX_CUDA(ctx, dalloc(&d.part, 4 * static_cast<size_t>(h.n_slots)));
+  HX_CUDA(ctx, dalloc(&d.cnt, 4 * static_cast<size_t>(h.n_long)));
+  HX_CUDA(ctx, dalloc(&d.terms, 4 * static_cast<size_t>(h.n_long) * kMaxQ));
   auto cp = [&](void* dst, const void* src, size_t bytes) {
     return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream) : cudaSuccess;
   };
   HX_CUDA(ctx, cp(d.tasks, h.tasks.data(), h.tasks.size() * sizeof(int4)));
-  HX_CUDA(ctx, cp(d.task_ptr, h.task_ptr.data(), h.task_ptr.size() * sizeof(int)));
-  HX_CUDA(ctx, cp(d.pieces, h.pieces.data(), h.pieces.size() * sizeof(Piece)));
-  HX_CUDA(ctx, cp(d.piece_ptr, h.piece_ptr.data(), h.piece_ptr.size() * sizeof(int)));
-  HX_CUDA(ctx, cudaMemsetAsync(d.cnt, 0, std::max<size_t>(1, 2 * static_cast<size_t>(h.n_long)) * sizeof(unsigned),
+  HX_CUDA(ctx, cp(d.meta, h.meta.data(), h.meta.size() * sizeof(int4)));
+  HX_CUDA(ctx, cudaMemsetAsync(d.cnt, 0, std::max<size_t>(1, 4 * static_cast<size_t>(h.n_long)) * sizeof(unsigned),
                                ctx->stream));
   HX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // host vectors go out of scope
   Sched& v = d.view;
@@ -1262,15 +1371,13 @@ int upload_sched(hx_ctx* ctx, DevSched& d, const int* ptr_host, int rows, int co
   v.idx = didx;
   v.val = dval;
   v.tasks = d.tasks;
-  v.task_ptr = d.task_ptr;
-  v.pieces = d.pieces;
-  v.piece_ptr = d.piece_ptr;
+  v.n_tasks = static_cast<int>(h.tasks.size());
+  v.meta = d.meta;
   v.n_long = h.n_long;
-  for (int s = 0; s < 2; ++s) {
-    v.piece_part[s] = d.part + static_cast<size_t>(s) * h.n_slots;
-    v.piece_cnt[s] = d.cnt + static_cast<size_t>(s) * h.n_long;
-    v.long_terms[s] = d.terms + static_cast<size_t>(s) * h.n_long * kMaxQ;
-  }
+  v.part_base = d.part;
+  v.cnt_base = d.cnt;
+  v.terms_base = d.terms;
+  v.n_slots = h.n_slots;
   d.max_cost = h.max_warp_cost;
   d.mean_cost = h.mean_warp_cost;
   return HPLP_OK;
@@ -1292,6 +1399,7 @@ KParams params(hx_ctx* c) {
   P.ctl = c->ctl;
   P.bar = c->bar;
   P.epochs = c->epochs;
+  P.prof = c->prof;
   return P;
 }
 
@@ -1299,8 +1407,9 @@ int launch_loop(hx_ctx* c) {
   KParams P = params(c);
   void* args[] = {&P};
   HX_CUDA(c, cudaMemcpyAsync(c->ctl, &c->h, sizeof(Ctl), cudaMemcpyHostToDevice, c->stream));
+  HX_CUDA(c, cudaMemsetAsync(c->bar, 0, sizeof(GridBar), c->stream));
   HX_CUDA(c, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(loop_kernel), dim3(c->grid), dim3(kThreads),
-                                         args, 0, c->stream));
+                                         args, kStageBytes, c->stream));
   c->launches += 1;
   HX_CUDA(c, cudaMemcpyAsync(&c->h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
   GridBar gb;
@@ -1308,8 +1417,6 @@ int launch_loop(hx_ctx* c) {
   HX_CUDA(c, cudaStreamSynchronize(c->stream));
   HX_CUDA(c, cudaGetLastError());
   if (gb.abort) {
-    cudaMemsetAsync(c->bar, 0, sizeof(GridBar), c->stream);
-    cudaStreamSynchronize(c->stream);
     return set_err(c, HPLP_ETIMEOUT, "hx: grid barrier watchdog fired (device hang avoided)");
   }
   return HPLP_OK;
@@ -1317,7 +1424,7 @@ int launch_loop(hx_ctx* c) {
 
 int spmv_dev(hx_ctx* c, bool transpose, const double* x, double* out) {
   const Sched& S = transpose ? c->st.view : c->sa.view;
-  spmv_store_kernel<<<c->grid, kThreads, 0, c->stream>>>(S, x, out);
+  spmv_store_kernel<<<c->grid, kThreads, kStageBytes, c->stream>>>(S, x, out);
   c->launches += 1;
   HX_CUDA(c, cudaGetLastError());
   return HPLP_OK;
@@ -1373,16 +1480,25 @@ int hx_create(int32_t device, hx_ctx** out) {
                                             std::to_string(prop.major * 10 + prop.minor));
   if (!prop.cooperativeLaunch) return set_err(nullptr, HPLP_ECUDA, "hx_create: cooperative launch unsupported");
   c->sm_count = prop.multiProcessorCount;
+  HX_CUDA(nullptr, cudaFuncSetAttribute(loop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kStageBytes)));
+  HX_CUDA(nullptr, cudaFuncSetAttribute(spmv_store_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kStageBytes)));
   int occ = 0;
-  HX_CUDA(nullptr, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, loop_kernel, kThreads, 0));
+  HX_CUDA(nullptr, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, loop_kernel, kThreads, kStageBytes));
   if (occ < 1) return set_err(nullptr, HPLP_ECUDA, "hx_create: loop kernel does not fit on an SM");
-  c->grid = c->sm_count * std::min(occ, 2);
+  c->grid = c->sm_count * std::min(occ, kMinBlocks);
   HX_CUDA(nullptr, cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   HX_CUDA(nullptr, cudaEventCreate(&c->ev0));
   HX_CUDA(nullptr, cudaEventCreate(&c->ev1));
-  HX_CUDA(nullptr, dalloc(&c->slots, static_cast<size_t>(kMaxQ) * c->grid));
+  HX_CUDA(nullptr, dalloc(&c->slots, static_cast<size_t>(kRegions) * kMaxQ * c->grid));
   HX_CUDA(nullptr, dalloc(&c->scratch, kMaxQ));
   HX_CUDA(nullptr, dalloc(&c->ctl, 1));
+  HX_CUDA(nullptr, dalloc(&c->kparams, 1));
+  if (const char* e = std::getenv("HX_PROFILE"); e && e[0] == '1') {
+    HX_CUDA(nullptr, dalloc(&c->prof, static_cast<size_t>(c->grid) * 8));
+    HX_CUDA(nullptr, cudaMemset(c->prof, 0, static_cast<size_t>(c->grid) * 8 * sizeof(unsigned long long)));
+  }
   HX_CUDA(nullptr, dalloc(&c->bar, 1));
   HX_CUDA(nullptr, dalloc(&c->epochs, kEpochCap));
   HX_CUDA(nullptr, cudaMemset(c->bar, 0, sizeof(GridBar)));
@@ -1396,7 +1512,7 @@ void hx_destroy(hx_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   free_problem(c);
-  dfree(c->slots), dfree(c->scratch), dfree(c->ctl), dfree(c->bar), dfree(c->epochs);
+  dfree(c->slots), dfree(c->scratch), dfree(c->ctl), dfree(c->bar), dfree(c->epochs), dfree(c->kparams), dfree(c->prof);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -1608,8 +1724,8 @@ int hx_setup(hx_ctx* c, const hplp_config_t* cfg, double sigma_used, double eta,
   C.sigma_used = sigma_used;
   C.b_norm = c->b_norm;
   C.c_norm = c->c_norm;
-  C.time_limit_s = cfg->time_limit_seconds;
-  C.t0_ns = 0;
+  c->time_limit_s = cfg->time_limit_seconds;
+  c->loop_elapsed_s = 0.0;
   C.best_kkt = std::numeric_limits<double>::infinity();
   C.x_best = C.y_best = -1;
   C.status = -1;
@@ -1644,15 +1760,29 @@ int hx_run(hx_ctx* c, int64_t max_iters, hx_progress_t* p) {
       } else {
         C.final_x = C.final_y = -1;
       }
+    } else if (c->loop_elapsed_s > c->time_limit_s) {
+      // src/solver.cpp:249-254 at the top of the next iteration
+      C.status = HPLP_STATUS_TIME_LIMIT;
+      if (C.best_kkt < std::numeric_limits<double>::infinity()) {
+        C.final_x = C.x_best, C.final_y = C.y_best;
+        std::memcpy(C.final_kkt, C.best_err, sizeof(C.final_kkt));
+      } else {
+        C.final_x = C.final_y = -1;
+      }
     } else {
       C.batch_end = C.it + max_iters;
       C.r.stop = 0;
       C.paused = 0;
+      const double remaining = c->time_limit_s - c->loop_elapsed_s;
+      C.time_budget_ns = std::isinf(remaining) ? 0ull
+                                               : std::max<unsigned long long>(1ull, static_cast<unsigned long long>(remaining * 1e9));
+      const auto w0 = std::chrono::steady_clock::now();
       HX_CUDA(c, cudaEventRecord(c->ev0, c->stream));
       int rc = launch_loop(c);
       if (rc) return rc;
       HX_CUDA(c, cudaEventRecord(c->ev1, c->stream));
       HX_CUDA(c, cudaEventSynchronize(c->ev1));
+      c->loop_elapsed_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
       HX_CUDA(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
     }
   }
@@ -1779,6 +1909,38 @@ int hx_kkt_current(hx_ctx* c, hplp_kkt_t* out) {
   out->dual_residual = std::sqrt(tot[1]) / (1.0 + c->c_norm);
   out->gap_residual = std::fabs(tot[2] + tot[3]) / (1.0 + std::fabs(tot[2]) + std::fabs(tot[3]));
   out->max_relative = std::max({out->primal_residual, out->dual_residual, out->gap_residual});
+  return HPLP_OK;
+}
+
+// Phase timers (HX_PROFILE=1): out[grid * 8] accumulated ns per CTA:
+// 0 phase A, 1 barrier 1, 2 phase B, 3 barrier 2, 4 totals+controller, 5 iterations.
+int hx_profile(hx_ctx* c, unsigned long long* out, int32_t reset) {
+  if (!c->prof) return set_err(c, HPLP_ESTATE, "hx_profile: set HX_PROFILE=1 before hx_create");
+  HX_CUDA(c, cudaMemcpy(out, c->prof, static_cast<size_t>(c->grid) * 8 * sizeof(unsigned long long),
+                        cudaMemcpyDeviceToHost));
+  if (reset) HX_CUDA(c, cudaMemset(c->prof, 0, static_cast<size_t>(c->grid) * 8 * sizeof(unsigned long long)));
+  return HPLP_OK;
+}
+
+// Microbenchmark: reps x (A x or A^T y) on device-resident random vectors,
+// CUDA-event timed on the context stream; *ms = mean per SpMV.
+int hx_bench_spmv(hx_ctx* c, int32_t transpose, int32_t reps, double* ms) {
+  if (!c->uploaded) return set_err(c, HPLP_ESTATE, "hx_bench_spmv: no problem uploaded");
+  double* in = transpose ? c->upool + 2 * c->n : c->upool;
+  double* out = transpose ? c->upool : c->upool + 2 * c->n;
+  HX_CUDA(c, cudaMemsetAsync(in, 0, (transpose ? c->m : c->n) * sizeof(double), c->stream));
+  int rc = spmv_dev(c, transpose != 0, in, out);
+  if (rc) return rc;
+  HX_CUDA(c, cudaEventRecord(c->ev0, c->stream));
+  for (int r = 0; r < reps; ++r) {
+    rc = spmv_dev(c, transpose != 0, in, out);
+    if (rc) return rc;
+  }
+  HX_CUDA(c, cudaEventRecord(c->ev1, c->stream));
+  HX_CUDA(c, cudaEventSynchronize(c->ev1));
+  float t = 0.f;
+  HX_CUDA(c, cudaEventElapsedTime(&t, c->ev0, c->ev1));
+  *ms = t / reps;
   return HPLP_OK;
 }
 

@@ -12,22 +12,38 @@
 
 namespace hx {
 
-constexpr int kThreads = 512;              // threads per CTA of every hx kernel
+#ifndef HX_THREADS
+#define HX_THREADS 512
+#endif
+constexpr int kThreads = HX_THREADS;              // threads per CTA of every hx kernel
 constexpr int kWarps = kThreads / 32;
+constexpr int kMinBlocks = 1024 / kThreads;     // 32 resident warps per SM (64 registers)
 constexpr int kMaxQ = 16;                  // reduction quantities per phase
 constexpr int kXPool = 6;                  // n-vectors: iterates, anchors, best, T(z)
 constexpr int kYPool = 6;                  // m-vectors: y, anchors, best, T(z), combos
 constexpr int kAxPool = 4;                 // m-vectors: A x carried / anchor / products
 constexpr int kEpochCap = 1 << 16;         // device epoch ring (host drains per hx_run)
 constexpr double kRowCost = 3.0;           // epilogue cost of one row in nnz units
+constexpr int kLoadsPerLane = 8;           // nonzeros per lane per task
+constexpr int kChunk = 32 * kLoadsPerLane; // max nonzeros per warp task (256)
+constexpr int kStreamRowMax = 64;          // rows up to this length are summed lane-per-row
+constexpr int kStreamRowsMax = 32;         // rows per stream task (one per lane)
 
-// A warp-task of consecutive rows handled with vector width 1 << log2v.
-// (int4: row_begin, row_end, log2v, unused)
-// A piece of one long row; the last piece to finish reduces the pieces in
-// index order and runs the row's epilogue (deterministic).
-struct Piece {
-  int row, p0, p1, slot, npieces, counter, index, pad;
-};
+// Warp tasks, int4 {row_begin, row_end | kind << 30, p_begin, p_end}; every
+// task covers at most kChunk nonzeros, loaded kLoadsPerLane per lane into
+// registers with independent loads and gathers (shared memory only holds a
+// 2 KB product buffer per warp, so L1 keeps its capacity for the gathers);
+// warp w runs tasks w, w + W, w + 2W, ... (static round robin):
+//   kTaskStream: consecutive short rows, summed lane-per-row in ascending
+//                column order (the reference's own order,
+//                src/sparse_matrix.cpp:108-115);
+//   kTaskPiece:  a slice of one longer row; meta[t] = {slot, npieces,
+//                counter, index}.  A single-piece row is finished in place;
+//                otherwise the last piece to finish reduces the pieces in
+//                index order and runs the row's epilogue (deterministic).
+enum TaskKind : int { kTaskStream = 0, kTaskPiece = 1 };
+constexpr int kKindShift = 30;
+constexpr int kRowMask = (1 << kKindShift) - 1;
 
 // Device view of one CSR matrix plus its nnz-balanced warp schedule.
 struct Sched {
@@ -37,21 +53,28 @@ struct Sched {
   const int* idx = nullptr;
   const double* val = nullptr;
   const int4* tasks = nullptr;
-  const int* task_ptr = nullptr;   // [warps + 1]
-  const Piece* pieces = nullptr;
-  const int* piece_ptr = nullptr;  // [warps + 1]
+  const int4* meta = nullptr;      // piece tasks: {slot, npieces, counter, index}
+  int n_tasks = 0;
   int n_long = 0;
-  double* piece_part[2] = {nullptr, nullptr};   // per concurrent SpMV lane
-  unsigned* piece_cnt[2] = {nullptr, nullptr};
-  double* long_terms[2] = {nullptr, nullptr};   // [n_long * kMaxQ]
+  // Long-row scratch per "set" (base + set * stride; no dynamically indexed
+  // arrays, which would force the kernel parameters into local memory):
+  // sets 0/1 alternate by iteration parity in the main phases, sets 2/3
+  // serve the certificate SpMVs.
+  double* part_base = nullptr;   // [4][n_slots]
+  unsigned* cnt_base = nullptr;  // [4][n_long]
+  double* terms_base = nullptr;  // [4][n_long * kMaxQ]
+  int n_slots = 0;
+  __host__ __device__ double* piece_part(int set) const { return part_base + static_cast<size_t>(set) * n_slots; }
+  __host__ __device__ unsigned* piece_cnt(int set) const { return cnt_base + static_cast<size_t>(set) * n_long; }
+  __host__ __device__ double* long_terms(int set) const {
+    return terms_base + static_cast<size_t>(set) * n_long * kMaxQ;
+  }
 };
 
 // Host-side schedule before upload.
 struct SchedHost {
   std::vector<int4> tasks;
-  std::vector<int> task_ptr;
-  std::vector<Piece> pieces;
-  std::vector<int> piece_ptr;
+  std::vector<int4> meta;
   int n_long = 0;
   int n_slots = 0;
   double max_warp_cost = 0.0, mean_warp_cost = 0.0;

@@ -1,12 +1,12 @@
 // nnz-balanced warp schedule for the fused SpMV phases (host side).
 //
-// Rows are cut into warp-tasks of consecutive rows sharing one vector width
-// v in {1,2,4,8,16,32} (a sub-warp of v lanes per row, about two passes per
-// row), rows longer than 2P are cut into pieces of about P nonzeros, and the
-// row-ordered item list is split into one contiguous slice per warp with
-// equal cost (nnz + kRowCost per row).  Static and deterministic: the same
-// matrix and grid always give the same row -> (warp, lane) map, which is what
-// makes every reduction in the solver reproducible bit for bit.
+// Rows of length <= kStreamRowMax are packed into stream tasks of at most
+// kChunk nonzeros / kStreamRowsMax rows; every longer row is cut into pieces
+// of at most kChunk nonzeros (a single piece when it fits).  The row-ordered
+// task list is then cut into one contiguous, equal-cost slice per warp
+// (cost = nnz + kRowCost per row).  Static and deterministic: the same matrix
+// and grid always give the same row -> (warp, lane) map, which is what makes
+// every reduction in the solver reproducible bit for bit.
 #include <algorithm>
 #include <cmath>
 
@@ -14,104 +14,84 @@
 
 namespace hx {
 
-namespace {
-int log2_width(int64_t len) {
-  if (len <= 2) return 0;
-  if (len <= 4) return 1;
-  if (len <= 8) return 2;
-  if (len <= 16) return 3;
-  if (len <= 32) return 4;
-  return 5;
-}
-}  // namespace
-
 SchedHost build_schedule(const int* ptr, int rows, int warps) {
   SchedHost s;
   const int64_t nnz = ptr[rows];
   const double total = static_cast<double>(nnz) + kRowCost * rows;
-  const double per_warp = std::max(1.0, total / warps);
-  const int64_t piece = static_cast<int64_t>(std::clamp(total / (2.0 * warps), 256.0, 16384.0));
-  const int64_t long_len = 2 * piece;
-  const double task_max = std::max(64.0, per_warp / 4.0);
 
-  struct Item {
-    bool is_piece;
-    int index;
-    double cost;
+  std::vector<double> cost;
+  auto push = [&](int r0, int r1, int kind, int p0, int p1, int4 meta, double c) {
+    s.tasks.push_back(int4{r0, r1 | (kind << kKindShift), p0, p1});
+    s.meta.push_back(meta);
+    cost.push_back(c);
   };
-  std::vector<Item> items;
-  int4 cur{0, 0, -1, 0};
-  double cur_cost = 0.0;
-  auto close = [&] {
-    if (cur.z >= 0 && cur.y > cur.x) {
-      items.push_back({false, static_cast<int>(s.tasks.size()), cur_cost});
-      s.tasks.push_back(cur);
-    }
-    cur.z = -1;
-    cur_cost = 0.0;
-  };
-  for (int r = 0; r < rows; ++r) {
+  int r = 0;
+  while (r < rows) {
     const int64_t len = ptr[r + 1] - ptr[r];
-    if (len > long_len) {
-      close();
-      const int np = static_cast<int>((len + piece - 1) / piece);
+    if (len > kStreamRowMax) {
+      const int np = static_cast<int>((len + kChunk - 1) / kChunk);
       for (int q = 0; q < np; ++q) {
-        Piece pc;
-        pc.row = r;
-        pc.p0 = static_cast<int>(ptr[r] + len * q / np);
-        pc.p1 = static_cast<int>(ptr[r] + len * (q + 1) / np);
-        pc.slot = s.n_slots + q;
-        pc.npieces = np;
-        pc.counter = s.n_long;
-        pc.index = q;
-        pc.pad = 0;
-        items.push_back({true, static_cast<int>(s.pieces.size()),
-                         static_cast<double>(pc.p1 - pc.p0) + (q + 1 == np ? kRowCost : 0.0)});
-        s.pieces.push_back(pc);
+        const int p0 = static_cast<int>(ptr[r] + len * q / np);
+        const int p1 = static_cast<int>(ptr[r] + len * (q + 1) / np);
+        push(r, r + 1, kTaskPiece, p0, p1, int4{s.n_slots + q, np, np > 1 ? s.n_long : -1, q},
+             static_cast<double>(p1 - p0) + (q + 1 == np ? kRowCost : 0.0));
       }
-      s.n_slots += np;
-      s.n_long += 1;
+      if (np > 1) {
+        s.n_slots += np;
+        s.n_long += 1;
+      }
+      ++r;
       continue;
     }
-    const int lv = log2_width(len);
-    const double cost = static_cast<double>(len) + kRowCost;
-    const int max_rows = (32 >> lv) * 64;
-    if (cur.z != lv || cur_cost + cost > task_max || cur.y - cur.x >= max_rows) {
-      close();
-      cur = int4{r, r, lv, 0};
+    const int r0 = r;
+    int64_t used = 0;
+    while (r < rows && r - r0 < kStreamRowsMax) {
+      const int64_t l = ptr[r + 1] - ptr[r];
+      if (l > kStreamRowMax || used + l > kChunk) break;
+      used += l;
+      ++r;
     }
-    cur.y = r + 1;
-    cur_cost += cost;
+    push(r0, r, kTaskStream, static_cast<int>(ptr[r0]), static_cast<int>(ptr[r]), int4{0, 0, 0, 0},
+         static_cast<double>(used) + kRowCost * (r - r0));
   }
-  close();
 
-  // Contiguous equal-cost slices of the item list, one per warp.
-  s.task_ptr.assign(static_cast<std::size_t>(warps) + 1, 0);
-  s.piece_ptr.assign(static_cast<std::size_t>(warps) + 1, 0);
+  // Deal the tasks to warps by cost: heaviest first, snake order (round 0 to
+  // warps 0..W-1, round 1 to W-1..0, ...), laid out so that warp w's tasks sit
+  // at positions w, w + W, w + 2W, ... which is how the kernels walk them.
+  // Deterministic and balanced; reductions stay fixed-order because every
+  // row keeps one (warp, lane) owner.
+  const std::size_t nt = s.tasks.size();
+  std::vector<int> order(nt);
+  for (std::size_t t = 0; t < nt; ++t) order[t] = static_cast<int>(t);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  const std::size_t rounds = (nt + warps - 1) / warps;
+  std::vector<int> slot_task(rounds * warps, -1);
+  for (std::size_t i = 0; i < nt; ++i) {
+    const std::size_t round = i / warps, pos = i % warps;
+    const std::size_t w = (round & 1) ? warps - 1 - pos : pos;
+    slot_task[round * warps + w] = order[i];
+  }
+  std::vector<int4> tasks, meta;
   std::vector<double> wcost(static_cast<std::size_t>(warps), 0.0);
-  double prefix = 0.0;
-  int nt = 0, np = 0;
-  int w_prev = 0;
-  for (const Item& it : items) {
-    const double mid = prefix + 0.5 * it.cost;
-    int w = std::min(warps - 1, static_cast<int>(mid / per_warp));
-    w = std::max(w, w_prev);  // monotone
-    for (int q = w_prev + 1; q <= w; ++q) {
-      s.task_ptr[q] = nt;
-      s.piece_ptr[q] = np;
+  tasks.reserve(nt);
+  for (std::size_t k = 0; k < slot_task.size(); ++k) {
+    int t = slot_task[k];
+    if (t < 0) {  // padding slot of the last round: an empty task
+      tasks.push_back(int4{0, 0, 0, 0});
+      meta.push_back(int4{0, 0, 0, 0});
+      continue;
     }
-    w_prev = w;
-    if (it.is_piece) ++np;
-    else ++nt;
-    wcost[w] += it.cost;
-    prefix += it.cost;
+    tasks.push_back(s.tasks[t]);
+    meta.push_back(s.meta[t]);
+    wcost[k % warps] += cost[t];
   }
-  for (int q = w_prev + 1; q <= warps; ++q) {
-    s.task_ptr[q] = nt;
-    s.piece_ptr[q] = np;
+  // trim trailing padding (kernels stop at n_tasks)
+  while (!tasks.empty() && tasks.back().x == 0 && tasks.back().y == 0 && tasks.back().w == 0) {
+    tasks.pop_back();
+    meta.pop_back();
   }
-  s.task_ptr[0] = 0;
-  s.piece_ptr[0] = 0;
+  s.tasks.swap(tasks);
+  s.meta.swap(meta);
   double mx = 0.0;
   for (double c : wcost) mx = std::max(mx, c);
   s.max_warp_cost = mx;

@@ -93,6 +93,7 @@ def lib() -> C.CDLL:
     sig("hx_get_certificate", C.c_int, V, I32, PD)
     sig("hx_kkt_current", C.c_int, V, C.POINTER(abi.Kkt))
     sig("hx_sizeof", I64, I32)
+    sig("hx_profile", C.c_int, V, C.POINTER(C.c_uint64), I32)
     _lib = L
     return L
 
@@ -365,6 +366,17 @@ class HX:
         x, y = np.empty(self.n), np.empty(self.m)
         self._c(lib().hx_get_iterate(self.h, which, dptr(x), dptr(y)))
         return x, y
+
+    def phase_profile(self, reset=True):
+        """Per-CTA phase timers (HX_PROFILE=1): dict of mean/max us per iteration."""
+        g = self.info()["grid"]
+        buf = (C.c_uint64 * (g * 8))()
+        self._c(lib().hx_profile(self.h, buf, int(reset)))
+        a = np.array(buf[:], dtype=np.float64).reshape(g, 8)
+        its = max(a[0, 5], 1.0)
+        names = ["phase_A", "barrier1", "phase_B", "barrier2", "controller"]
+        return {nm: dict(mean_us=float(a[:, i].mean() / its / 1e3), max_us=float(a[:, i].max() / its / 1e3),
+                         min_us=float(a[:, i].min() / its / 1e3)) for i, nm in enumerate(names)}
 
     def kkt_current(self):
         k = abi.Kkt()
