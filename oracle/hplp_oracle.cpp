@@ -738,6 +738,8 @@ StdForm to_standard_form(const hplp_general_t* g) {
   }
   StdForm s;
   s.lp.a = make_csr(m_std, n_std, rp.data(), ci.data(), cv.data());
+  if (!all_finite(b_std) || !all_finite(c_std))  // StandardFormLP ctor, src/lp_model.cpp:40-42
+    throw std::invalid_argument("StandardFormLP: non-finite b or c");
   s.lp.b = std::move(b_std);
   s.lp.c = std::move(c_std);
   for (int64_t j = 0; j < n; ++j) {
