@@ -170,7 +170,7 @@ def run_reference(args):
     total = sum(loop_times)
     value = iters * args.steps / total
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "device": "cpu", "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded planted LP, configs[1])",
         "config": {"workload": f"configs[{CONFIG_ID}] medium planted LP, standard form {s.m}x{s.n}, nnz {s.nnz}",
