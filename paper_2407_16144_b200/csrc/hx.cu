@@ -172,9 +172,18 @@ __device__ __forceinline__ double (*red_buf())[kMaxQ] {
   return red;
 }
 
-// Per-thread accumulators -> slots[q * grid + cta] (fixed order).
+// Partial-sum records: each CTA publishes its kMaxQ partials of a reduction
+// round as one 128-byte record, written to kReplicas copies of the region so
+// the (redundant, every-CTA) readers spread over distinct L2 lines.
+constexpr int kReplicas = 4;
+
+__device__ __forceinline__ size_t region_stride(int grid) {
+  return static_cast<size_t>(kReplicas) * grid * kMaxQ;
+}
+
+// Per-thread accumulators -> this CTA's record in every replica (fixed order).
 template <int Q, unsigned MaxMask>
-__device__ void block_to_slots(const double (&acc)[Q], double* slots, int grid) {
+__device__ void block_to_slots(const double (&acc)[Q], double* region, int grid) {
   double (*red)[kMaxQ] = red_buf();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -183,16 +192,71 @@ __device__ void block_to_slots(const double (&acc)[Q], double* slots, int grid) 
     if (lane == 0) red[warp][q] = v;
   }
   __syncthreads();
-  if (threadIdx.x < Q) {
-    const int q = threadIdx.x;
+  if (threadIdx.x < Q * kReplicas) {
+    const int q = threadIdx.x % Q, k = threadIdx.x / Q;
     const bool mx = (MaxMask >> q) & 1u;
     double v = red[0][q];
     for (int w = 1; w < kWarps; ++w) v = mx ? dmax(v, red[w][q]) : v + red[w][q];
-    slots[q * grid + blockIdx.x] = v;
+    region[(static_cast<size_t>(k) * grid + blockIdx.x) * kMaxQ + q] = v;
   }
 }
 
-// Warp-level fixed-order reduction of count values at p[i * stride].
+// Source of one reduced quantity: records of a region (+ optional long-row
+// terms), column rq / lq of the 16-wide records.
+struct QSrc {
+  const double* region;
+  int rq;
+  const double* lt;
+  int n_long;
+  int lq;
+  bool mx;
+};
+
+// Totals of up to kMaxQ quantities, computed by the whole CTA in a fixed
+// order: thread t handles quantity t % kMaxQ over records t / kMaxQ + kJ k,
+// then thread q combines the kJ partials in index order.  Every CTA computes
+// bit-identical totals.  Desc: q -> QSrc.
+constexpr int kJ = kThreads / kMaxQ;
+// One shared scratch for every block_totals instantiation.
+__device__ __forceinline__ double (*part_buf())[kJ][kMaxQ] {
+  __shared__ double part[2][kJ][kMaxQ];
+  return part;
+}
+
+template <class Desc>
+__device__ void block_totals(int Q, const Desc& desc, double* tot) {
+  double (*part)[kJ][kMaxQ] = part_buf();
+  const int q = threadIdx.x % kMaxQ, j = threadIdx.x / kMaxQ;
+  const int G = gridDim.x;
+  if (q < Q) {
+    const QSrc d = desc(q);
+    const double* rec = d.region + static_cast<size_t>(blockIdx.x % kReplicas) * G * kMaxQ;
+    double v = d.mx ? -INFINITY : 0.0, l = v;
+    for (int c = j; c < G; c += kJ) {
+      const double x = ldcg(rec + static_cast<size_t>(c) * kMaxQ + d.rq);
+      v = d.mx ? dmax(v, x) : v + x;
+    }
+    if (d.lt)
+      for (int c = j; c < d.n_long; c += kJ) {
+        const double x = ldcg(d.lt + static_cast<size_t>(c) * kMaxQ + d.lq);
+        l = d.mx ? dmax(l, x) : l + x;
+      }
+    part[0][j][q] = v;
+    part[1][j][q] = l;
+  }
+  __syncthreads();
+  if (threadIdx.x < Q) {
+    const QSrc d = desc(threadIdx.x);
+    double v = part[0][0][threadIdx.x], l = part[1][0][threadIdx.x];
+    for (int jj = 1; jj < kJ; ++jj) {
+      v = d.mx ? dmax(v, part[0][jj][threadIdx.x]) : v + part[0][jj][threadIdx.x];
+      l = d.mx ? dmax(l, part[1][jj][threadIdx.x]) : l + part[1][jj][threadIdx.x];
+    }
+    tot[threadIdx.x] = d.lt ? (d.mx ? dmax(v, l) : v + l) : v;
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ double warp_reduce_strided(const double* p, int count, int stride, bool mx) {
   const int lane = threadIdx.x & 31;
   double v = mx ? -INFINITY : 0.0;
@@ -201,16 +265,6 @@ __device__ __forceinline__ double warp_reduce_strided(const double* p, int count
     v = mx ? dmax(v, s) : v + s;
   }
   return mx ? warp_max(v) : warp_sum(v);
-}
-
-// tot = reduce(slots[slot_q]) (+) reduce(long_terms[.][long_q]); one warp.
-__device__ __forceinline__ double total_of(const double* slots, int grid, int slot_q,
-                                           const double* long_terms, int n_long, int long_q,
-                                           bool mx) {
-  const double v = warp_reduce_strided(slots + slot_q * grid, grid, 1, mx);
-  if (long_terms == nullptr || n_long == 0) return v;
-  const double l = warp_reduce_strided(long_terms + long_q, n_long, kMaxQ, mx);
-  return mx ? dmax(v, l) : v + l;
 }
 
 // ---------------------------------------------------------------------------
@@ -234,14 +288,40 @@ struct WarpStage {
 };
 constexpr size_t kStageBytes = sizeof(WarpStage) * kWarps;
 
+// Index/value registers of one task (kLoadsPerLane per lane).
+struct TaskRegs {
+  int ci[kLoadsPerLane];
+  double cv[kLoadsPerLane];
+};
+
+__device__ __forceinline__ void load_task(const Sched& S, const int4& tk, int lane, TaskRegs& r) {
+  const int p0 = tk.z, len = tk.w - tk.z;
+#pragma unroll
+  for (int j = 0; j < kLoadsPerLane; ++j) {
+    const int q = j * 32 + lane;
+    r.ci[j] = q < len ? __ldg(S.idx + p0 + q) : 0;
+    r.cv[j] = q < len ? __ldg(S.val + p0 + q) : 0.0;
+  }
+}
+
 template <int Q, unsigned MaxMask, class Src, class Epi>
 __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& src, Epi& epi, double (&acc)[Q],
                                           int gwarp, int lane, WarpStage* st) {
   const int W = gridDim.x * kWarps;
-  const int* __restrict__ idx = S.idx;
-  const double* __restrict__ val = S.val;
-  for (int t = gwarp; t < S.n_tasks; t += W) {
-    const int4 tk = __ldg(S.tasks + t);
+  const int n = S.n_tasks;
+  const int4 kNone{0, 0, 0, 0};
+  int t = gwarp;
+  if (t >= n) return;
+  // software pipeline: descriptors two tasks ahead, index/value loads one
+  // task ahead of the gathers
+  int4 tk = __ldg(S.tasks + t);
+  int4 tk1 = t + W < n ? __ldg(S.tasks + t + W) : kNone;
+  TaskRegs cur;
+  load_task(S, tk, lane, cur);
+  for (; t < n; t += W) {
+    const int4 tk2 = t + 2 * W < n ? __ldg(S.tasks + t + 2 * W) : kNone;
+    TaskRegs nxt;
+    load_task(S, tk1, lane, nxt);
     const int r0 = tk.x, r1 = tk.y & kRowMask, kind = tk.y >> kKindShift;
     const int p0 = tk.z, len = tk.w - tk.z;
     const bool has_row = kind == kTaskStream && lane < r1 - r0;
@@ -252,22 +332,14 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
       rb = __ldg(S.ptr + r0 + lane + 1);
       in = epi.load(r0 + lane);
     }
-    int ci[kLoadsPerLane];
-    double cv[kLoadsPerLane];
 #pragma unroll
     for (int j = 0; j < kLoadsPerLane; ++j) {
       const int q = j * 32 + lane;
-      ci[j] = q < len ? __ldg(idx + p0 + q) : 0;
-      cv[j] = q < len ? __ldg(val + p0 + q) : 0.0;
-    }
-#pragma unroll
-    for (int j = 0; j < kLoadsPerLane; ++j) {
-      const int q = j * 32 + lane;
-      if (q < len) cv[j] = cv[j] * src(ci[j]);
+      if (q < len) cur.cv[j] = cur.cv[j] * src(cur.ci[j]);
     }
     if (kind == kTaskStream) {
 #pragma unroll
-      for (int j = 0; j < kLoadsPerLane; ++j) st->prod[j * 32 + lane] = cv[j];
+      for (int j = 0; j < kLoadsPerLane; ++j) st->prod[j * 32 + lane] = cur.cv[j];
       __syncwarp();
       if (has_row) {
         double s = 0.0;
@@ -280,7 +352,7 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
     } else {
       double s = 0.0;
 #pragma unroll
-      for (int j = 0; j < kLoadsPerLane; ++j) s += cv[j];
+      for (int j = 0; j < kLoadsPerLane; ++j) s += cur.cv[j];
       s = warp_sum(s);
       if (lane == 0) {
         const int4 meta = __ldg(S.meta + t);  // {slot, npieces, counter, index}
@@ -308,6 +380,9 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
         }
       }
     }
+    tk = tk1;
+    tk1 = tk2;
+    cur = nxt;
   }
 }
 
@@ -769,13 +844,13 @@ __device__ void ctl_store(const Ctl& s, Ctl* g) {
 // sees one SpMV instantiation at a time; KParams lives in global memory.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double* region_ptr(const KParams* P, int r) {
-  return P->slots + static_cast<size_t>(r) * kMaxQ * gridDim.x;
+  return P->slots + static_cast<size_t>(r) * region_stride(gridDim.x);
 }
 
 __device__ __forceinline__ int gwarp_id() { return blockIdx.x * kWarps + (threadIdx.x >> 5); }
 
 // phase A: A^T y, primal step (+ Halpern formation of x), primal partials
-__device__ __noinline__ void phase_primal(const KParams* P, const Roles* R, int par, WarpStage* stage) {
+__device__ HX_PHASE_INLINE void phase_primal(const KParams* P, const Roles* R, int par, WarpStage* stage) {
   const int n = P->n, m = P->m;
   double acc[3];
   acc_init<3, 0>(acc);
@@ -794,7 +869,7 @@ __device__ __noinline__ void phase_primal(const KParams* P, const Roles* R, int 
 }
 
 // phase B: A x+, dual step, speculative Halpern combos, dual partials
-__device__ __noinline__ void phase_dual(const KParams* P, const Roles* R, int par, WarpStage* stage) {
+__device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int par, WarpStage* stage) {
   const int n = P->n, m = P->m;
   double acc[4];
   acc_init<4, 0>(acc);
@@ -815,22 +890,20 @@ __device__ __noinline__ void phase_dual(const KParams* P, const Roles* R, int pa
   block_to_slots<4, 0>(acc, region_ptr(P, kRegB + par), gridDim.x);
 }
 
-// totals of phases A+B (warps 0..6) -> tot[0..6]
-__device__ __noinline__ void totals_main(const KParams* P, int par, double* tot) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = gridDim.x;
-  if (warp < 3) {
-    const double t = total_of(region_ptr(P, kRegA + par), G, warp, P->AT.long_terms(par), P->AT.n_long, warp, false);
-    if (lane == 0) tot[warp] = t;
-  } else if (warp < 7) {
-    const double t =
-        total_of(region_ptr(P, kRegB + par), G, warp - 3, P->A.long_terms(par), P->A.n_long, warp - 3, false);
-    if (lane == 0) tot[warp] = t;
-  }
+// totals of phases A+B -> tot[0..6]
+__device__ HX_PHASE_INLINE void totals_main(const KParams* P, int par, double* tot) {
+  const double* ra = region_ptr(P, kRegA + par);
+  const double* rb = region_ptr(P, kRegB + par);
+  const double* lta = P->AT.long_terms(par);
+  const double* ltb = P->A.long_terms(par);
+  const int na = P->AT.n_long, nb = P->A.n_long;
+  block_totals(7, [&](int q) {
+    return q < 3 ? QSrc{ra, q, na ? lta : nullptr, na, q, false} : QSrc{rb, q - 3, nb ? ltb : nullptr, nb, q - 3, false};
+  }, tot);
 }
 
 // power iteration halves: w = A x (x = x0 or z / zn), z = A^T w
-__device__ __noinline__ void power_a(const KParams* P, const Roles* R, WarpStage* stage) {
+__device__ HX_PHASE_INLINE void power_a(const KParams* P, const Roles* R, WarpStage* stage) {
   double acc[1];
   acc_init<1, 0>(acc);
   EpiStoreSq e{P->ypool};
@@ -840,7 +913,7 @@ __device__ __noinline__ void power_a(const KParams* P, const Roles* R, WarpStage
   block_to_slots<1, 0>(acc, region_ptr(P, kRegPA), gridDim.x);
 }
 
-__device__ __noinline__ void power_b(const KParams* P, WarpStage* stage) {
+__device__ HX_PHASE_INLINE void power_b(const KParams* P, WarpStage* stage) {
   double acc[1];
   acc_init<1, 0>(acc);
   EpiStoreSq e{P->xpool + P->n};
@@ -850,7 +923,7 @@ __device__ __noinline__ void power_b(const KParams* P, WarpStage* stage) {
 }
 
 // certificate scan C1: candidate norms and finiteness
-__device__ __noinline__ void cert_norms(const KParams* P, const Roles* R) {
+__device__ HX_PHASE_INLINE void cert_norms(const KParams* P, const Roles* R) {
   const int n = P->n, m = P->m;
   const int gtid = blockIdx.x * kThreads + threadIdx.x, gs = gridDim.x * kThreads;
   const double* zx = P->xpool + static_cast<size_t>(R->zx_out) * n;
@@ -884,7 +957,7 @@ __device__ __noinline__ void cert_norms(const KParams* P, const Roles* R) {
 }
 
 // certificate scan C2: unit vectors u = v / ||v|| and their reductions
-__device__ __noinline__ void cert_units(const KParams* P, const Roles* R) {
+__device__ HX_PHASE_INLINE void cert_units(const KParams* P, const Roles* R) {
   const int n = P->n, m = P->m;
   const int gtid = blockIdx.x * kThreads + threadIdx.x, gs = gridDim.x * kThreads;
   const double* zx = P->xpool + static_cast<size_t>(R->zx_out) * n;
@@ -940,7 +1013,7 @@ __device__ __noinline__ void cert_units(const KParams* P, const Roles* R) {
 }
 
 // certificate scan C3: the validation SpMVs, up to four independent products
-__device__ __noinline__ void cert_products(const KParams* P, const Roles* R, WarpStage* stage) {
+__device__ HX_PHASE_INLINE void cert_products(const KParams* P, const Roles* R, WarpStage* stage) {
   const int n = P->n, m = P->m;
   double acc[6];
   acc_init<6, 0x3Fu>(acc);
@@ -996,11 +1069,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
     while (!R->stop) {
       power_a(P, R, stage);
       if (!grid_sync(bar, target)) return;
-      if (warp == 0) {
-        const double t = total_of(region_ptr(P, kRegPA), G, 0, P->A.long_terms(0), P->A.n_long, 0, false);
-        if (lane == 0) tot[0] = t;
+      {
+        const double* rg = region_ptr(P, kRegPA);
+        const double* lt = P->A.n_long ? P->A.long_terms(0) : nullptr;
+        const int nl = P->A.n_long;
+        block_totals(1, [&](int) { return QSrc{rg, 0, lt, nl, 0, false}; }, tot);
       }
-      __syncthreads();
       if (threadIdx.x == 0) {
         const double sigma = sqrt(tot[0]);
         C.pw_iters = C.pw_k + 1;
@@ -1014,11 +1088,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
       if (R->stop) break;
       power_b(P, stage);
       if (!grid_sync(bar, target)) return;
-      if (warp == 0) {
-        const double t = total_of(region_ptr(P, kRegPB), G, 0, P->AT.long_terms(0), P->AT.n_long, 0, false);
-        if (lane == 0) tot[1] = t;
+      {
+        const double* rg = region_ptr(P, kRegPB);
+        const double* lt = P->AT.n_long ? P->AT.long_terms(0) : nullptr;
+        const int nl = P->AT.n_long;
+        block_totals(1, [&](int) { return QSrc{rg, 0, lt, nl, 0, false}; }, tot + 1);
       }
-      __syncthreads();
       if (threadIdx.x == 0) {
         const double sigma = C.pw_sigma_cur;
         C.pw_sigma = sigma;
@@ -1046,7 +1121,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
   }
 
   unsigned long long* prof = P->prof ? P->prof + blockIdx.x * 8 : nullptr;
-  unsigned long long tp = global_ns(), pacc[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long tp = global_ns(), pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   auto mark = [&](int k) {
     if (prof && threadIdx.x == 0) {
       const unsigned long long t = global_ns();
@@ -1069,20 +1144,20 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
     totals_main(P, par, tot);
     if (threadIdx.x == 7 * 32) s_time_up = budget != 0ull && *reinterpret_cast<volatile unsigned*>(&bar->time_up[par]) != 0u;
     __syncthreads();
+    mark(4);
     if (threadIdx.x == 0) main_logic(C, tot, P->epochs, writer, s_time_up != 0);
     __syncthreads();
-    mark(4);
+    mark(6);
     if (prof && threadIdx.x == 0) pacc[5] += 1;
     if (!R->check) continue;
 
     // ---- certificate scan (src/solver.cpp:297-317) ----
     cert_norms(P, R);
     if (!grid_sync(bar, target)) return;
-    if (warp < 8) {
-      const double t = total_of(region_ptr(P, kRegC1), G, warp, nullptr, 0, 0, false);
-      if (lane == 0) tot[warp] = t;
+    {
+      const double* rg = region_ptr(P, kRegC1);
+      block_totals(8, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, false}; }, tot);
     }
-    __syncthreads();
     if (threadIdx.x == 0) {
       int any = 0;
       for (int c = 0; c < 4; ++c) {
@@ -1098,11 +1173,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
     if (!R->check) continue;
     cert_units(P, R);
     if (!grid_sync(bar, target)) return;
-    if (warp < 12) {
-      const double t = total_of(region_ptr(P, kRegC2), G, warp, nullptr, 0, 0, ((0x577u >> warp) & 1u) != 0);
-      if (lane == 0) tot[warp] = t;
+    {
+      const double* rg = region_ptr(P, kRegC2);
+      block_totals(12, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, ((0x577u >> q) & 1u) != 0}; }, tot);
     }
-    __syncthreads();
     if (threadIdx.x == 0) {
       C.cinf[0] = tot[0], C.cmax_u[0] = tot[1], C.cmax_negu[0] = tot[2], C.cdot[0] = tot[3];
       C.cinf[2] = tot[4], C.cmax_u[2] = tot[5], C.cmax_negu[2] = tot[6], C.cdot[2] = tot[7];
@@ -1112,15 +1186,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
     __syncthreads();
     cert_products(P, R, stage);
     if (!grid_sync(bar, target)) return;
-    if (warp < 6) {
-      const int set = 2 + (warp < 4 ? (warp >> 1) : (warp - 4));
-      const int lq = warp < 4 ? (warp & 1) : 0;
-      const double* lt = warp < 4 ? P->AT.long_terms(set) : P->A.long_terms(set);
-      const int nl = warp < 4 ? P->AT.n_long : P->A.n_long;
-      const double t = total_of(region_ptr(P, kRegC3), G, warp, lt, nl, lq, true);
-      if (lane == 0) tot[warp] = t;
+    {
+      const double* rg = region_ptr(P, kRegC3);
+      block_totals(6, [&](int q) {
+        const int set = 2 + (q < 4 ? (q >> 1) : (q - 4));
+        const int lq = q < 4 ? (q & 1) : 0;
+        const int nl = q < 4 ? P->AT.n_long : P->A.n_long;
+        const double* lt = nl ? (q < 4 ? P->AT.long_terms(set) : P->A.long_terms(set)) : nullptr;
+        return QSrc{rg, q, lt, nl, lq, true};
+      }, tot);
     }
-    __syncthreads();
     if (threadIdx.x == 0) {
       C.cmax_at[1] = tot[0], C.cmax_negat[1] = tot[1];
       C.cmax_at[3] = tot[2], C.cmax_negat[3] = tot[3];
@@ -1129,8 +1204,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
     }
     __syncthreads();
   }
-  if (prof && threadIdx.x == 0)
+  if (prof && threadIdx.x == 0) {
     for (int k = 0; k < 6; ++k) prof[k] += pacc[k];
+    prof[7] += pacc[6];
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    prof[6] = smid;
+  }
   if (writer) ctl_store(C, P->ctl);
 }
 
@@ -1191,10 +1271,10 @@ kkt_partials_kernel(int m, int n, const double* ax, const double* b, const doubl
   block_to_slots<6, 0>(acc, slots, gridDim.x);
 }
 
-__global__ void final_reduce_kernel(const double* slots, int grid, int q_count, double* out) {
+__global__ void final_reduce_kernel(const double* region, int grid, int q_count, double* out) {
   const int wq = threadIdx.x >> 5;
   for (int q = wq; q < q_count; q += blockDim.x / 32) {
-    const double t = warp_reduce_strided(slots + q * grid, grid, 1, false);
+    const double t = warp_reduce_strided(region + q, grid, kMaxQ, false);  // replica 0
     if ((threadIdx.x & 31) == 0) out[q] = t;
   }
 }
@@ -1491,7 +1571,7 @@ int hx_create(int32_t device, hx_ctx** out) {
   HX_CUDA(nullptr, cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   HX_CUDA(nullptr, cudaEventCreate(&c->ev0));
   HX_CUDA(nullptr, cudaEventCreate(&c->ev1));
-  HX_CUDA(nullptr, dalloc(&c->slots, static_cast<size_t>(kRegions) * kMaxQ * c->grid));
+  HX_CUDA(nullptr, dalloc(&c->slots, static_cast<size_t>(kRegions) * kReplicas * kMaxQ * c->grid));
   HX_CUDA(nullptr, dalloc(&c->scratch, kMaxQ));
   HX_CUDA(nullptr, dalloc(&c->ctl, 1));
   HX_CUDA(nullptr, dalloc(&c->kparams, 1));

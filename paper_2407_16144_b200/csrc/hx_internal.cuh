@@ -17,14 +17,27 @@ namespace hx {
 #endif
 constexpr int kThreads = HX_THREADS;              // threads per CTA of every hx kernel
 constexpr int kWarps = kThreads / 32;
-constexpr int kMinBlocks = 1024 / kThreads;     // 32 resident warps per SM (64 registers)
+// One 512-thread CTA per SM with a 128-register budget and every phase
+// inlined: measured fastest on B200 (no spills -- spill reloads after each
+// grid barrier's L1 invalidation cost an L2 round trip).
+#ifndef HX_MIN_BLOCKS
+#define HX_MIN_BLOCKS 1
+#endif
+constexpr int kMinBlocks = HX_MIN_BLOCKS;         // resident CTAs per SM the register budget targets
+#ifndef HX_PHASE_INLINE
+#define HX_PHASE_INLINE __forceinline__
+#endif
 constexpr int kMaxQ = 16;                  // reduction quantities per phase
 constexpr int kXPool = 6;                  // n-vectors: iterates, anchors, best, T(z)
 constexpr int kYPool = 6;                  // m-vectors: y, anchors, best, T(z), combos
 constexpr int kAxPool = 4;                 // m-vectors: A x carried / anchor / products
 constexpr int kEpochCap = 1 << 16;         // device epoch ring (host drains per hx_run)
 constexpr double kRowCost = 3.0;           // epilogue cost of one row in nnz units
-constexpr int kLoadsPerLane = 8;           // nonzeros per lane per task
+constexpr double kTaskCost = 64.0;         // fixed latency cost of one warp task in nnz units
+#ifndef HX_LOADS
+#define HX_LOADS 8
+#endif
+constexpr int kLoadsPerLane = HX_LOADS;    // nonzeros per lane per task
 constexpr int kChunk = 32 * kLoadsPerLane; // max nonzeros per warp task (256)
 constexpr int kStreamRowMax = 64;          // rows up to this length are summed lane-per-row
 constexpr int kStreamRowsMax = 32;         // rows per stream task (one per lane)

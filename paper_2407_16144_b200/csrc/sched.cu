@@ -9,6 +9,8 @@
 // every reduction in the solver reproducible bit for bit.
 #include <algorithm>
 #include <cmath>
+#include <functional>
+#include <queue>
 
 #include "hx_internal.cuh"
 
@@ -23,7 +25,7 @@ SchedHost build_schedule(const int* ptr, int rows, int warps) {
   auto push = [&](int r0, int r1, int kind, int p0, int p1, int4 meta, double c) {
     s.tasks.push_back(int4{r0, r1 | (kind << kKindShift), p0, p1});
     s.meta.push_back(meta);
-    cost.push_back(c);
+    cost.push_back(c + kTaskCost);
   };
   int r = 0;
   while (r < rows) {
@@ -55,37 +57,35 @@ SchedHost build_schedule(const int* ptr, int rows, int warps) {
          static_cast<double>(used) + kRowCost * (r - r0));
   }
 
-  // Deal the tasks to warps by cost: heaviest first, snake order (round 0 to
-  // warps 0..W-1, round 1 to W-1..0, ...), laid out so that warp w's tasks sit
-  // at positions w, w + W, w + 2W, ... which is how the kernels walk them.
-  // Deterministic and balanced; reductions stay fixed-order because every
-  // row keeps one (warp, lane) owner.
+  // Longest-processing-time dealing: tasks heaviest first, each to the
+  // currently least-loaded warp (ties to the lower warp id).  Warp w's tasks are
+  // laid out at positions w, w + W, w + 2W, ... (padded with empty tasks),
+  // which is how the kernels walk them.  Deterministic and balanced;
+  // reductions stay fixed-order because every row keeps one (warp, lane) owner.
   const std::size_t nt = s.tasks.size();
   std::vector<int> order(nt);
   for (std::size_t t = 0; t < nt; ++t) order[t] = static_cast<int>(t);
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
-  const std::size_t rounds = (nt + warps - 1) / warps;
-  std::vector<int> slot_task(rounds * warps, -1);
-  for (std::size_t i = 0; i < nt; ++i) {
-    const std::size_t round = i / warps, pos = i % warps;
-    const std::size_t w = (round & 1) ? warps - 1 - pos : pos;
-    slot_task[round * warps + w] = order[i];
-  }
-  std::vector<int4> tasks, meta;
+  using Load = std::pair<double, int>;  // (load, warp)
+  std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+  for (int w = 0; w < warps; ++w) heap.push({0.0, w});
+  std::vector<std::vector<int>> per_warp(static_cast<std::size_t>(warps));
   std::vector<double> wcost(static_cast<std::size_t>(warps), 0.0);
-  tasks.reserve(nt);
-  for (std::size_t k = 0; k < slot_task.size(); ++k) {
-    int t = slot_task[k];
-    if (t < 0) {  // padding slot of the last round: an empty task
-      tasks.push_back(int4{0, 0, 0, 0});
-      meta.push_back(int4{0, 0, 0, 0});
-      continue;
-    }
-    tasks.push_back(s.tasks[t]);
-    meta.push_back(s.meta[t]);
-    wcost[k % warps] += cost[t];
+  for (int t : order) {
+    auto [load, w] = heap.top();
+    heap.pop();
+    per_warp[w].push_back(t);
+    wcost[w] = load + cost[t];
+    heap.push({wcost[w], w});
   }
-  // trim trailing padding (kernels stop at n_tasks)
+  std::size_t rounds = 0;
+  for (const auto& v : per_warp) rounds = std::max(rounds, v.size());
+  std::vector<int4> tasks(rounds * warps, int4{0, 0, 0, 0}), meta(rounds * warps, int4{0, 0, 0, 0});
+  for (int w = 0; w < warps; ++w)
+    for (std::size_t k = 0; k < per_warp[w].size(); ++k) {
+      tasks[k * warps + w] = s.tasks[per_warp[w][k]];
+      meta[k * warps + w] = s.meta[per_warp[w][k]];
+    }
   while (!tasks.empty() && tasks.back().x == 0 && tasks.back().y == 0 && tasks.back().w == 0) {
     tasks.pop_back();
     meta.pop_back();

@@ -374,9 +374,9 @@ class HX:
         self._c(lib().hx_profile(self.h, buf, int(reset)))
         a = np.array(buf[:], dtype=np.float64).reshape(g, 8)
         its = max(a[0, 5], 1.0)
-        names = ["phase_A", "barrier1", "phase_B", "barrier2", "controller"]
+        names = {"phase_A": 0, "barrier1": 1, "phase_B": 2, "barrier2": 3, "totals": 4, "controller_logic": 7}
         return {nm: dict(mean_us=float(a[:, i].mean() / its / 1e3), max_us=float(a[:, i].max() / its / 1e3),
-                         min_us=float(a[:, i].min() / its / 1e3)) for i, nm in enumerate(names)}
+                         min_us=float(a[:, i].min() / its / 1e3)) for nm, i in names.items()}
 
     def kkt_current(self):
         k = abi.Kkt()
