@@ -115,8 +115,9 @@ int hx_get_certificate(hx_ctx* ctx, int32_t kind, double* vec);
 int hx_kkt_current(hx_ctx* ctx, hplp_kkt_t* out);
 
 /* Diagnostics: per-CTA phase timers when the context was created with
- * HX_PROFILE=1 in the environment; out holds grid * 8 counters (ns):
- * phase A, barrier 1, phase B, barrier 2, controller, iterations. */
+ * HX_PROFILE=1 in the environment; out holds grid * 16 counters (SM cycles):
+ * phase A, barrier 1, phase B, barrier 2, totals, iterations, smid,
+ * controller, controller math / scalar / sync. */
 int hx_profile(hx_ctx* ctx, unsigned long long* out, int32_t reset);
 
 /* sizeof checks for the ABI tests. */

@@ -91,6 +91,7 @@ struct Ctl {
   double cinf[4], cmax_u[4], cmax_negu[4], cdot[4], cmax_at[4], cmax_negat[4], cmax_abs_au[4];
   hplp_cert_meta_t cert[2];  // 0 primal, 1 dual
   int cert_cand[2];
+  double w_k2, w_k3;  // 1/(k+2), 1/(k+3) of the current iteration
   long long pw_k, pw_max, pw_iters;
   double pw_tol, pw_sigma, pw_sigma_prev, pw_sigma_cur;
   int pw_converged, pw_redraw;
@@ -531,10 +532,13 @@ __device__ bool grid_sync(GridBar* bar, unsigned long long& target) {
   target += gridDim.x;
   if (threadIdx.x == 0) {
     s_ok = 1;
-    __threadfence();
-    atomicAdd(&bar->count, 1ull);
+    // release: this CTA's writes (ordered before by bar.sync) become visible
+    // before the arrival (SASS: MEMBAR.ALL.GPU + REDG, no return)
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(&bar->count), "l"(1ull) : "memory");
     const unsigned long long t0 = global_ns();
     unsigned spins = 0;
+    // acquire (SASS: LDG.STRONG.GPU + CCTL.IVALL): later reads, L1-cached
+    // ones included, see every CTA's released writes
     while (ld_acquire_u64(&bar->count) < target) {
       if ((++spins & 255u) == 0u) {
         if (*reinterpret_cast<volatile unsigned*>(&bar->abort)) {
@@ -548,7 +552,6 @@ __device__ bool grid_sync(GridBar* bar, unsigned long long& target) {
         }
       }
     }
-    __threadfence();
   }
   __syncthreads();
   return s_ok != 0;
@@ -593,6 +596,7 @@ __device__ void set_final_limit(Ctl& C, int status) {
 // Restart decision + Halpern bookkeeping + next roles + limits
 // (src/solver.cpp:319-341 and the loop-top checks :242-254).
 __device__ void finish_iteration(Ctl& C, hplp_epoch_t* epochs, bool writer, double res, bool time_up) {
+  // C.w_k2 = 1/(k+2), C.w_k3 = 1/(k+3) were computed in parallel (warp 0)
   Roles& R = C.r;
   bool restart = should_restart(C, C.n, C.k, res, C.res_epoch_start);
   if (!restart && C.restart_kind == HPLP_RESTART_ADAPTIVE && C.stall_cap > 0 && C.k >= C.stall_cap)
@@ -610,7 +614,7 @@ __device__ void finish_iteration(Ctl& C, hplp_epoch_t* epochs, bool writer, doub
     C.n += 1;
     C.k = 0;
   } else {
-    const double w = 1.0 / static_cast<double>(C.k + 2);
+    const double w = C.w_k2;  // 1.0 / (k + 2)
     R.x_src = R.xp_out;
     R.x_mode = 1;
     R.w_x = w;
@@ -626,7 +630,7 @@ __device__ void finish_iteration(Ctl& C, hplp_epoch_t* epochs, bool writer, doub
   R.yc_out = pick_free(kYPool, R.y_cur, R.y_anchor, C.y_best, R.yp_out);
   R.axp_out = pick_free(kAxPool, R.ax_cur, R.ax_anchor, -1, -1);
   R.axc_out = pick_free(kAxPool, R.ax_cur, R.ax_anchor, R.axp_out, -1);
-  R.w_next = 1.0 / static_cast<double>(C.k + 2);
+  R.w_next = restart ? 0.5 : C.w_k3;  // 1.0 / (k_new + 2)
   if (C.it >= C.iteration_limit) {
     set_final_limit(C, HPLP_STATUS_ITERATION_LIMIT);
   } else if (time_up) {
@@ -640,22 +644,23 @@ __device__ void finish_iteration(Ctl& C, hplp_epoch_t* epochs, bool writer, doub
 }
 
 // After phases A+B: KKT, residual, epochs, best, termination, scan or finish.
-__device__ void main_logic(Ctl& C, const double* tot, hplp_epoch_t* epochs, bool writer, bool time_up) {
+// pre[0..2]: KKT components (kkt_error_with_products, src/pdhg_core.cpp:57-68),
+// pre[3] = dx2/eta, pre[4] = dy2/eta, computed one per lane of warp 0.
+__device__ void main_logic(Ctl& C, const double* tot, const double* pre, hplp_epoch_t* epochs, bool writer,
+                           bool time_up) {
   Roles& R = C.r;
-  const double dres = tot[0], cx = tot[1], dx2 = tot[2];
-  const double pres = tot[3], by = tot[4], dy2 = tot[5], dyax = tot[6];
-  // kkt_error_with_products, src/pdhg_core.cpp:57-68
+  const double dx2 = tot[2], dy2 = tot[5], dyax = tot[6];
   double kkt[4];
-  kkt[0] = sqrt(pres) / (1.0 + C.b_norm);
-  kkt[1] = sqrt(dres) / (1.0 + C.c_norm);
-  kkt[2] = fabs(cx + by) / (1.0 + fabs(cx) + fabs(by));
+  kkt[0] = pre[0];
+  kkt[1] = pre[1];
+  kkt[2] = pre[2];
   double mx = kkt[0];
   if (mx < kkt[1]) mx = kkt[1];
   if (mx < kkt[2]) mx = kkt[2];
   kkt[3] = mx;
   // canonical_norm_with_product, src/pdhg_core.cpp:37-51
   const double eta = R.eta;
-  const double q = dx2 / eta - 2.0 * dyax + dy2 / eta;
+  const double q = pre[3] - 2.0 * dyax + pre[4];
   double res;
   if (q < 0.0) {
     const double scale = (dx2 + dy2) / eta;
@@ -1120,11 +1125,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
     return;
   }
 
-  unsigned long long* prof = P->prof ? P->prof + blockIdx.x * 8 : nullptr;
-  unsigned long long tp = global_ns(), pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  auto mark = [&](int k) {
+  unsigned long long* prof = P->prof ? P->prof + blockIdx.x * 16 : nullptr;
+  unsigned long long tp = clock64(), pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pacc2[3] = {0, 0, 0};
+  auto mark = [&](int k) {  // SM cycles (clock64); the host converts with the SM clock
     if (prof && threadIdx.x == 0) {
-      const unsigned long long t = global_ns();
+      const unsigned long long t = clock64();
       pacc[k] += t - tp;
       tp = t;
     }
@@ -1145,8 +1150,38 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
     if (threadIdx.x == 7 * 32) s_time_up = budget != 0ull && *reinterpret_cast<volatile unsigned*>(&bar->time_up[par]) != 0u;
     __syncthreads();
     mark(4);
-    if (threadIdx.x == 0) main_logic(C, tot, P->epochs, writer, s_time_up != 0);
+    unsigned long long cA = clock64(), cB = 0, cC = 0;
+    if (warp == 0) {
+      // the independent fp64 divides / square roots, one per lane, executed
+      // uniformly (operands selected per lane, one sqrt + one divide)
+      const double t0 = tot[0], t1 = tot[1], t2 = tot[2], t3 = tot[3], t4 = tot[4], t5 = tot[5];
+      double num = 1.0, den = 1.0;
+      if (lane == 0) num = t3, den = 1.0 + C.b_norm;
+      else if (lane == 1) num = t0, den = 1.0 + C.c_norm;
+      else if (lane == 2) num = fabs(t1 + t4), den = 1.0 + fabs(t1) + fabs(t4);
+      else if (lane == 3) num = t2, den = C.r.eta;
+      else if (lane == 4) num = t5, den = C.r.eta;
+      else if (lane == 5) den = static_cast<double>(C.k + 2);
+      else if (lane == 6) den = static_cast<double>(C.k + 3);
+      const double sq = sqrt(num);
+      const double v = (lane < 2 ? sq : num) / den;
+      double pre[7];
+#pragma unroll
+      for (int i = 0; i < 7; ++i) pre[i] = __shfl_sync(0xffffffffu, v, i);
+      cB = clock64();
+      if (lane == 0) {
+        C.w_k2 = pre[5];
+        C.w_k3 = pre[6];
+        main_logic(C, tot, pre, P->epochs, writer, s_time_up != 0);
+      }
+      cC = clock64();
+    }
     __syncthreads();
+    if (prof && threadIdx.x == 0) {
+      pacc2[0] += cB - cA;
+      pacc2[1] += cC - cB;
+      pacc2[2] += clock64() - cC;
+    }
     mark(6);
     if (prof && threadIdx.x == 0) pacc[5] += 1;
     if (!R->check) continue;
@@ -1207,6 +1242,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
   if (prof && threadIdx.x == 0) {
     for (int k = 0; k < 6; ++k) prof[k] += pacc[k];
     prof[7] += pacc[6];
+    for (int k = 0; k < 3; ++k) prof[8 + k] += pacc2[k];
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     prof[6] = smid;
@@ -1576,8 +1612,8 @@ int hx_create(int32_t device, hx_ctx** out) {
   HX_CUDA(nullptr, dalloc(&c->ctl, 1));
   HX_CUDA(nullptr, dalloc(&c->kparams, 1));
   if (const char* e = std::getenv("HX_PROFILE"); e && e[0] == '1') {
-    HX_CUDA(nullptr, dalloc(&c->prof, static_cast<size_t>(c->grid) * 8));
-    HX_CUDA(nullptr, cudaMemset(c->prof, 0, static_cast<size_t>(c->grid) * 8 * sizeof(unsigned long long)));
+    HX_CUDA(nullptr, dalloc(&c->prof, static_cast<size_t>(c->grid) * 16));
+    HX_CUDA(nullptr, cudaMemset(c->prof, 0, static_cast<size_t>(c->grid) * 16 * sizeof(unsigned long long)));
   }
   HX_CUDA(nullptr, dalloc(&c->bar, 1));
   HX_CUDA(nullptr, dalloc(&c->epochs, kEpochCap));
@@ -1996,9 +2032,9 @@ int hx_kkt_current(hx_ctx* c, hplp_kkt_t* out) {
 // 0 phase A, 1 barrier 1, 2 phase B, 3 barrier 2, 4 totals+controller, 5 iterations.
 int hx_profile(hx_ctx* c, unsigned long long* out, int32_t reset) {
   if (!c->prof) return set_err(c, HPLP_ESTATE, "hx_profile: set HX_PROFILE=1 before hx_create");
-  HX_CUDA(c, cudaMemcpy(out, c->prof, static_cast<size_t>(c->grid) * 8 * sizeof(unsigned long long),
+  HX_CUDA(c, cudaMemcpy(out, c->prof, static_cast<size_t>(c->grid) * 16 * sizeof(unsigned long long),
                         cudaMemcpyDeviceToHost));
-  if (reset) HX_CUDA(c, cudaMemset(c->prof, 0, static_cast<size_t>(c->grid) * 8 * sizeof(unsigned long long)));
+  if (reset) HX_CUDA(c, cudaMemset(c->prof, 0, static_cast<size_t>(c->grid) * 16 * sizeof(unsigned long long)));
   return HPLP_OK;
 }
 

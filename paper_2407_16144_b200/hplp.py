@@ -367,16 +367,18 @@ class HX:
         self._c(lib().hx_get_iterate(self.h, which, dptr(x), dptr(y)))
         return x, y
 
-    def phase_profile(self, reset=True):
-        """Per-CTA phase timers (HX_PROFILE=1): dict of mean/max us per iteration."""
+    def phase_profile(self, reset=True, sm_mhz=1965.0):
+        """Per-CTA phase timers (HX_PROFILE=1, SM cycles): mean/max/min us per iteration."""
         g = self.info()["grid"]
-        buf = (C.c_uint64 * (g * 8))()
+        buf = (C.c_uint64 * (g * 16))()
         self._c(lib().hx_profile(self.h, buf, int(reset)))
-        a = np.array(buf[:], dtype=np.float64).reshape(g, 8)
+        a = np.array(buf[:], dtype=np.float64).reshape(g, 16)
         its = max(a[0, 5], 1.0)
-        names = {"phase_A": 0, "barrier1": 1, "phase_B": 2, "barrier2": 3, "totals": 4, "controller_logic": 7}
-        return {nm: dict(mean_us=float(a[:, i].mean() / its / 1e3), max_us=float(a[:, i].max() / its / 1e3),
-                         min_us=float(a[:, i].min() / its / 1e3)) for nm, i in names.items()}
+        names = {"phase_A": 0, "barrier1": 1, "phase_B": 2, "barrier2": 3, "totals": 4, "controller_logic": 7,
+                 "ctl_math": 8, "ctl_scalar": 9, "ctl_sync": 10}
+        k = 1.0 / its / sm_mhz  # cycles -> us per iteration
+        return {nm: dict(mean_us=float(a[:, i].mean() * k), max_us=float(a[:, i].max() * k),
+                         min_us=float(a[:, i].min() * k)) for nm, i in names.items()}
 
     def kkt_current(self):
         k = abi.Kkt()

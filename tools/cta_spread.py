@@ -17,12 +17,12 @@ hx = solver.hx
 hx.setup(abi.Config.default(tolerance=1e-4, iteration_limit=10**9), r0["sigma_estimate"], r0["eta"])
 g = hx.info()["grid"]
 for rep in range(2):
-    buf = (C.c_uint64 * (g * 8))()
+    buf = (C.c_uint64 * (g * 16))()
     hplp.lib().hx_profile(hx.h, buf, 1)
     hx.run(500)
-    buf = (C.c_uint64 * (g * 8))()
+    buf = (C.c_uint64 * (g * 16))()
     hplp.lib().hx_profile(hx.h, buf, 1)
-    a = np.array(buf[:], dtype=np.float64).reshape(g, 8)
+    a = np.array(buf[:], dtype=np.float64).reshape(g, 16)
     its = a[0, 5]
     pa, pb = a[:, 0] / its / 1e3, a[:, 2] / its / 1e3
     sm = a[:, 6].astype(int)
