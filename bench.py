@@ -334,7 +334,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-iters", type=int, default=40)
     ap.add_argument("--ref-iters", type=int, default=20)
-    ap.add_argument("--ttt-cap", type=float, default=30.0)
+    ap.add_argument("--ttt-cap", type=float, default=60.0)
     ap.add_argument("--no-ttt", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
