@@ -64,6 +64,12 @@ typedef struct hplp_config {
   double tol_active;
   int64_t adaptive_stall_cap;
   uint64_t seed;
+  /* Extension (no reference counterpart): diagonal
+   * preconditioning applied to the instance before the loop.  0 / -1 = off,
+   * i.e. the reference's own semantics. */
+  int32_t precondition_ruiz_iters;
+  int32_t reserved0;
+  double precondition_pc_alpha;
 } hplp_config_t;
 
 /* KktError, inc/pdhg_core.hpp:82-87. */
@@ -179,6 +185,9 @@ static inline hplp_config_t hplp_config_default(void) {
   c.tol_active = 1e-6;
   c.adaptive_stall_cap = 2000;
   c.seed = 12345u;
+  c.precondition_ruiz_iters = 0;
+  c.reserved0 = 0;
+  c.precondition_pc_alpha = -1.0;
   return c;
 }
 

@@ -69,6 +69,17 @@ int hx_upload_csr(hx_ctx* ctx, int64_t m, int64_t n, const int64_t* row_ptr,
 /* Same with device-resident inputs (no host copies; used by re-uploads). */
 int hx_dims(hx_ctx* ctx, int64_t* m, int64_t* n, int64_t* nnz);
 
+/* Diagonal preconditioning of the uploaded problem in place (no reference
+ * counterpart; SPEC.md:101,259 name Ruiz / Pock-Chambolle as extension
+ * points): ruiz_iters rounds of Ruiz inf-norm equilibration, then one
+ * Pock-Chambolle step (pc_alpha >= 0).  A' = R A C, b' = R b, c' = C c on both
+ * stored copies; the accumulated scales R (m) and C (n) are returned when the
+ * pointers are non-NULL.  Iterates of the transformed LP map back as
+ * x = C x', y = R y'. */
+int hx_precondition(hx_ctx* ctx, int32_t ruiz_iters, double pc_alpha, double* row_scale, double* col_scale);
+/* The device problem (after any preconditioning): CSR A, b, c. */
+int hx_download_problem(hx_ctx* ctx, int64_t* row_ptr, int32_t* col_idx, double* val, double* b, double* c);
+
 /* [spmv, src/sparse_matrix.cpp:101-117]  out = A x, host vectors. */
 int hx_spmv(hx_ctx* ctx, const double* x, double* out);
 /* [spmv_transpose, src/sparse_matrix.cpp:119-136]  out = A^T y. */

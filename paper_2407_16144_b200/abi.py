@@ -49,6 +49,9 @@ class Config(C.Structure):
         ("tol_active", C.c_double),
         ("adaptive_stall_cap", C.c_int64),
         ("seed", C.c_uint64),
+        ("precondition_ruiz_iters", C.c_int32),
+        ("reserved0", C.c_int32),
+        ("precondition_pc_alpha", C.c_double),
     ]
 
     @classmethod
@@ -69,6 +72,9 @@ class Config(C.Structure):
             tol_active=1e-6,
             adaptive_stall_cap=2000,
             seed=12345,
+            precondition_ruiz_iters=0,
+            reserved0=0,
+            precondition_pc_alpha=-1.0,
         )
         for k, v in kw.items():
             if k == "eta_override" and v is not None:

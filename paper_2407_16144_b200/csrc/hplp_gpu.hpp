@@ -209,6 +209,13 @@ struct SolverConfig {
   std::optional<Iterate> initial_iterate;
   std::function<void(const TraceRecord&, const Iterate&)> trace_sink;
   int device = 0;  // B200 ordinal (extension; the reference has no device)
+  // Extension (no reference counterpart): Ruiz rounds and a
+  // Pock-Chambolle step applied on the device before the loop; the loop then
+  // runs the reference's exact semantics on the scaled instance and the
+  // result is mapped back (x = C x', y = R y', certificates re-normalised).
+  // final_kkt is the KKT error of the scaled instance the loop terminated on.
+  int precondition_ruiz_iters = 0;
+  double precondition_pc_alpha = -1.0;  // < 0: no Pock-Chambolle step
 };
 
 // inc/solver.hpp:82-116
@@ -264,6 +271,10 @@ class Solver {
  private:
   ::hx_ctx* ctx_ = nullptr;
   int64_t m_ = 0, n_ = 0, nnz_ = 0;
+  bool scaled_ = false;
+  int ruiz_ = 0;
+  double pc_alpha_ = -1.0;
+  Vector row_scale_, col_scale_;  // R (m), C (n) when scaled_
 };
 
 // inc/solver.hpp:130 -- src/solver.cpp:206-342 on the GPU.

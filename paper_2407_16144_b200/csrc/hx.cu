@@ -1364,6 +1364,49 @@ __global__ void gather_t_kernel(int nnz, const int* perm, const int* row_of, con
   }
 }
 
+// ---------------------------------------------------------------------------
+// Diagonal preconditioning (Ruiz equilibration + Pock-Chambolle), an instance
+// transform A' = R A C, b' = R b, c' = C c applied to both stored copies with
+// identical rounding ((a * r_i) * c_j).  Setup-time kernels, thread per row.
+// ---------------------------------------------------------------------------
+// kind 0: max |a_ij| over the row, kind 1: sum |a_ij|^p (p = 2 - alpha for
+// rows of A, alpha for rows of A^T, passed as `power`).
+__global__ void row_norm_kernel(int rows, const int* rp, const double* v, int kind, double power, double* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int p = rp[i]; p < rp[i + 1]; ++p) {
+      const double a = fabs(v[p]);
+      if (kind == 0) acc = a > acc ? a : acc;
+      else acc += power == 1.0 ? a : pow(a, power);
+    }
+    out[i] = acc;
+  }
+}
+
+// d = 1/sqrt(norm) (1 where the norm is 0); acc *= d.
+__global__ void inv_sqrt_kernel(int len, double* d, double* acc) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) {
+    const double nrm = d[i];
+    const double f = nrm > 0.0 ? 1.0 / sqrt(nrm) : 1.0;
+    d[i] = f;
+    acc[i] = acc[i] * f;
+  }
+}
+
+// val(row i, col j) = (val * dr[i]) * dc[j]; `transposed` swaps the roles.
+__global__ void scale_csr_kernel(int rows, const int* rp, const int* ci, double* v, const double* d_row,
+                                 const double* d_col, int transposed) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x)
+    for (int p = rp[i]; p < rp[i + 1]; ++p) {
+      const int j = ci[p];
+      v[p] = transposed ? (v[p] * d_row[j]) * d_col[i] : (v[p] * d_row[i]) * d_col[j];
+    }
+}
+
+__global__ void scale_vec_kernel(int len, double* v, const double* d) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) v[i] = v[i] * d[i];
+}
+
 }  // namespace hx
 
 // ===========================================================================
@@ -1760,6 +1803,83 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   c->b_norm = std::sqrt(tot[4]);
   c->c_norm = std::sqrt(tot[5]);
   c->uploaded = true;
+  return HPLP_OK;
+}
+
+// Diagonal preconditioning of the uploaded problem (no reference
+// counterpart: SPEC.md:101/259 name it an extension point).  ruiz_iters
+// rounds of Ruiz infinity-norm equilibration, then (pc_alpha >= 0) one
+// Pock-Chambolle step with exponent alpha.  Writes the accumulated row
+// scales R (m) and column scales C (n) when the pointers are non-NULL.
+int hx_precondition(hx_ctx* c, int32_t ruiz_iters, double pc_alpha, double* row_scale, double* col_scale) {
+  if (!c->uploaded) return set_err(c, HPLP_ESTATE, "hx_precondition: no problem uploaded");
+  if (ruiz_iters < 0) return set_err(c, HPLP_EINVAL, "hx_precondition: ruiz_iters must be >= 0");
+  cudaStream_t s = c->stream;
+  const int m = static_cast<int>(c->m), n = static_cast<int>(c->n);
+  const int nb = 4 * c->sm_count;
+  double *dr = nullptr, *dc = nullptr, *R = nullptr, *Cs = nullptr;
+  HX_CUDA(c, dalloc(&dr, m));
+  HX_CUDA(c, dalloc(&dc, n));
+  HX_CUDA(c, dalloc(&R, m));
+  HX_CUDA(c, dalloc(&Cs, n));
+  std::vector<double> ones(static_cast<size_t>(std::max(m, n)), 1.0);
+  if (m) HX_CUDA(c, cudaMemcpyAsync(R, ones.data(), m * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (n) HX_CUDA(c, cudaMemcpyAsync(Cs, ones.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
+  auto apply = [&]() -> int {
+    inv_sqrt_kernel<<<nb, 256, 0, s>>>(m, dr, R);
+    inv_sqrt_kernel<<<nb, 256, 0, s>>>(n, dc, Cs);
+    scale_csr_kernel<<<nb, 256, 0, s>>>(m, c->a_ptr, c->a_idx, c->a_val, dr, dc, 0);
+    scale_csr_kernel<<<nb, 256, 0, s>>>(n, c->t_ptr, c->t_idx, c->t_val, dr, dc, 1);
+    scale_vec_kernel<<<nb, 256, 0, s>>>(m, c->b, dr);
+    scale_vec_kernel<<<nb, 256, 0, s>>>(n, c->c, dc);
+    c->launches += 6;
+    HX_CUDA(c, cudaGetLastError());
+    return HPLP_OK;
+  };
+  for (int k = 0; k < ruiz_iters; ++k) {
+    row_norm_kernel<<<nb, 256, 0, s>>>(m, c->a_ptr, c->a_val, 0, 1.0, dr);
+    row_norm_kernel<<<nb, 256, 0, s>>>(n, c->t_ptr, c->t_val, 0, 1.0, dc);
+    c->launches += 2;
+    int rc = apply();
+    if (rc) return rc;
+  }
+  if (pc_alpha >= 0.0) {
+    row_norm_kernel<<<nb, 256, 0, s>>>(m, c->a_ptr, c->a_val, 1, 2.0 - pc_alpha, dr);
+    row_norm_kernel<<<nb, 256, 0, s>>>(n, c->t_ptr, c->t_val, 1, pc_alpha, dc);
+    c->launches += 2;
+    int rc = apply();
+    if (rc) return rc;
+  }
+  if (row_scale && m) HX_CUDA(c, cudaMemcpyAsync(row_scale, R, m * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (col_scale && n) HX_CUDA(c, cudaMemcpyAsync(col_scale, Cs, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  // ||b||, ||c|| of the transformed instance
+  kkt_partials_kernel<<<c->grid, kThreads, 0, s>>>(m, n, nullptr, c->b, nullptr, c->c, nullptr, nullptr, c->slots);
+  final_reduce_kernel<<<1, 256, 0, s>>>(c->slots, c->grid, 6, c->scratch);
+  double tot[6];
+  HX_CUDA(c, cudaMemcpyAsync(tot, c->scratch, sizeof(tot), cudaMemcpyDeviceToHost, s));
+  HX_CUDA(c, cudaStreamSynchronize(s));
+  c->launches += 2;
+  c->b_norm = std::sqrt(tot[4]);
+  c->c_norm = std::sqrt(tot[5]);
+  dfree(dr), dfree(dc), dfree(R), dfree(Cs);
+  c->setup_done = false;
+  return HPLP_OK;
+}
+
+// The device problem (after any preconditioning) as CSR + b + c.
+int hx_download_problem(hx_ctx* c, int64_t* row_ptr, int32_t* col_idx, double* val, double* b, double* cc) {
+  if (!c->uploaded) return set_err(c, HPLP_ESTATE, "hx_download_problem: no problem uploaded");
+  cudaStream_t s = c->stream;
+  if (row_ptr) {
+    std::vector<int> rp(static_cast<size_t>(c->m) + 1);
+    HX_CUDA(c, cudaMemcpy(rp.data(), c->a_ptr, (c->m + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i <= c->m; ++i) row_ptr[i] = rp[i];
+  }
+  if (col_idx && c->nnz) HX_CUDA(c, cudaMemcpyAsync(col_idx, c->a_idx, c->nnz * sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (val && c->nnz) HX_CUDA(c, cudaMemcpyAsync(val, c->a_val, c->nnz * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (b && c->m) HX_CUDA(c, cudaMemcpyAsync(b, c->b, c->m * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (cc && c->n) HX_CUDA(c, cudaMemcpyAsync(cc, c->c, c->n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  HX_CUDA(c, cudaStreamSynchronize(s));
   return HPLP_OK;
 }
 

@@ -192,6 +192,8 @@ hplp_config_t to_pod(const SolverConfig& c) {
   p.tol_active = c.tol_active;
   p.adaptive_stall_cap = c.adaptive_stall_cap;
   p.seed = c.seed;
+  p.precondition_ruiz_iters = c.precondition_ruiz_iters;
+  p.precondition_pc_alpha = c.precondition_pc_alpha;
   return p;
 }
 
@@ -211,6 +213,8 @@ SolverConfig from_pod(const hplp_config_t& p) {
   c.tol_active = p.tol_active;
   c.adaptive_stall_cap = p.adaptive_stall_cap;
   c.seed = p.seed;
+  c.precondition_ruiz_iters = p.precondition_ruiz_iters;
+  c.precondition_pc_alpha = p.precondition_pc_alpha;
   return c;
 }
 
@@ -241,6 +245,27 @@ SolveResult Solver::solve(const SolverConfig& config) {
   auto since = [&] { return std::chrono::duration<double>(Clock::now() - t0).count(); };
   validate_config(config);
   hx_ctx* ctx = ctx_;
+  // optional diagonal preconditioning (extension), applied once per Solver
+  const bool want_scale = config.precondition_ruiz_iters > 0 || config.precondition_pc_alpha >= 0.0;
+  if (want_scale || scaled_) {
+    if (config.precondition_ruiz_iters < 0) throw std::invalid_argument("SolverConfig: precondition_ruiz_iters < 0");
+    if (scaled_ && (config.precondition_ruiz_iters != ruiz_ || config.precondition_pc_alpha != pc_alpha_))
+      throw std::invalid_argument("Solver: preconditioning is applied once per Solver; settings cannot change");
+    if (!scaled_) {
+      row_scale_.assign(static_cast<std::size_t>(m_), 1.0);
+      col_scale_.assign(static_cast<std::size_t>(n_), 1.0);
+      check(ctx, hx_precondition(ctx, config.precondition_ruiz_iters, config.precondition_pc_alpha, row_scale_.data(),
+                                 col_scale_.data()));
+      scaled_ = true;
+      ruiz_ = config.precondition_ruiz_iters;
+      pc_alpha_ = config.precondition_pc_alpha;
+    }
+  }
+  auto unscale = [&](Vector& x, Vector& y) {  // x = C x', y = R y'
+    if (!scaled_) return;
+    for (std::size_t j = 0; j < x.size(); ++j) x[j] *= col_scale_[j];
+    for (std::size_t i = 0; i < y.size(); ++i) y[i] *= row_scale_[i];
+  };
   // make_setup (:67-78)
   const PowerResult pi = power_iteration(ctx, m_, n_, nnz_, kPowerTol, kPowerMaxIters, config.seed);
   const double sigma_used = pi.sigma * (1.0 + kPowerTol);
@@ -251,12 +276,21 @@ SolveResult Solver::solve(const SolverConfig& config) {
   // initial_point (:80-87)
   const double* x0 = nullptr;
   const double* y0 = nullptr;
+  Vector xs0, ys0;
   if (config.initial_iterate) {
     const Iterate& z = *config.initial_iterate;
     if (static_cast<int64_t>(z.x.size()) != n_ || static_cast<int64_t>(z.y.size()) != m_)
       throw std::invalid_argument("SolverConfig: initial iterate has wrong size");
     x0 = z.x.data();
     y0 = z.y.data();
+    if (scaled_) {  // x' = x / C, y' = y / R
+      xs0 = z.x;
+      ys0 = z.y;
+      for (std::size_t j = 0; j < xs0.size(); ++j) xs0[j] /= col_scale_[j];
+      for (std::size_t i = 0; i < ys0.size(); ++i) ys0[i] /= row_scale_[i];
+      x0 = xs0.data();
+      y0 = ys0.data();
+    }
   }
   hplp_config_t pod = to_pod(config);
   pod.time_limit_seconds = config.time_limit_seconds - since();  // device clock starts at the loop
@@ -295,6 +329,7 @@ SolveResult Solver::solve(const SolverConfig& config) {
       rec.wall_seconds = since();
       Iterate z{Vector(static_cast<std::size_t>(n_)), Vector(static_cast<std::size_t>(m_))};
       check(ctx, hx_get_iterate(ctx, HX_ITERATE_LAST, z.x.data(), z.y.data()));
+      unscale(z.x, z.y);
       config.trace_sink(rec, z);
     }
   }
@@ -319,11 +354,20 @@ SolveResult Solver::solve(const SolverConfig& config) {
     check(ctx, hx_get_iterate(ctx, HX_ITERATE_LAST, out.final_iterate.x.data(), out.final_iterate.y.data()));
     out.final_kkt = kkt_of(p.final_kkt);
   }
+  unscale(out.final_iterate.x, out.final_iterate.y);
   auto take_cert = [&](int kind, const hplp_cert_meta_t& meta, std::optional<Certificate>& dst, int64_t len) {
     if (!meta.present) return;
     Certificate c;
     c.vector.resize(static_cast<std::size_t>(len));
     check(ctx, hx_get_certificate(ctx, kind, c.vector.data()));
+    if (scaled_) {  // y = R y' (primal certificate), u = C u' (dual ray), unit norm again
+      const Vector& sc = kind == 0 ? row_scale_ : col_scale_;
+      double nn = 0.0;
+      for (std::size_t i = 0; i < c.vector.size(); ++i) nn += (c.vector[i] *= sc[i]) * c.vector[i];
+      nn = std::sqrt(nn);
+      if (nn > 0.0)
+        for (double& v2 : c.vector) v2 /= nn;
+    }
     c.source = meta.source == HPLP_SOURCE_NORMALIZED_ITERATE ? CandidateSource::kNormalizedIterate
                                                              : CandidateSource::kIterateDifference;
     c.at_iteration = static_cast<long>(meta.at_iteration);

@@ -94,6 +94,8 @@ def lib() -> C.CDLL:
     sig("hx_kkt_current", C.c_int, V, C.POINTER(abi.Kkt))
     sig("hx_sizeof", I64, I32)
     sig("hx_profile", C.c_int, V, C.POINTER(C.c_uint64), I32)
+    sig("hx_precondition", C.c_int, V, I32, D, PD, PD)
+    sig("hx_download_problem", C.c_int, V, PI64, PI32, PD, PD, PD)
     _lib = L
     return L
 
@@ -361,6 +363,21 @@ class HX:
         out = (abi.Epoch * max(count, 1))()
         self._c(lib().hx_epochs(self.h, first, count, out))
         return [(e.epoch, e.restart_length, e.residual_at_start, e.kkt_at_start.as_tuple()) for e in out[:count]]
+
+    def precondition(self, ruiz_iters=10, pc_alpha=1.0):
+        """Ruiz + Pock-Chambolle scaling of the uploaded problem in place;
+        returns the accumulated (row_scale R, col_scale C)."""
+        R, Cs = np.empty(self.m), np.empty(self.n)
+        self._c(lib().hx_precondition(self.h, int(ruiz_iters), float(pc_alpha), dptr(R), dptr(Cs)))
+        return R, Cs
+
+    def download_problem(self):
+        """(row_ptr, col_idx, val, b, c) of the device problem."""
+        rp = np.empty(self.m + 1, np.int64)
+        ci, v = np.empty(self.nnz, np.int32), np.empty(self.nnz)
+        b, c = np.empty(self.m), np.empty(self.n)
+        self._c(lib().hx_download_problem(self.h, i64ptr(rp), i32ptr(ci), dptr(v), dptr(b), dptr(c)))
+        return rp, ci, v, b, c
 
     def get_iterate(self, which=0):
         x, y = np.empty(self.n), np.empty(self.m)
