@@ -67,6 +67,13 @@ void hplp_std_free(void* std_form);
 int hplp_solve_general(int32_t device, const hplp_general_t* g, const hplp_config_t* cfg, hplp_io_t* io,
                        hplp_result_t* result, double* x_orig, double* objective);
 
+/* Multi-GPU row partition plan: rank p owns rows
+ * [row_bounds[p], row_bounds[p+1]) of A and columns [col_bounds[p],
+ * col_bounds[p+1]) (rows of A^T), each cut balanced by nnz + 3 per row.
+ * row_bounds and col_bounds hold parts + 1 entries. */
+int hplp_plan_partition(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx, int32_t parts,
+                        int64_t* row_bounds, int64_t* col_bounds);
+
 #ifdef __cplusplus
 }
 #endif
