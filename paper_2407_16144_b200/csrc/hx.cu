@@ -144,6 +144,14 @@ __device__ __forceinline__ double ldca(const double* p) { return __ldca(p); }
 
 __device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }
 
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -307,7 +315,7 @@ __device__ __forceinline__ void load_task(const Sched& S, const int4& tk, int la
 
 template <int Q, unsigned MaxMask, class Src, class Epi>
 __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& src, Epi& epi, double (&acc)[Q],
-                                          int gwarp, int lane, WarpStage* st) {
+                                          int gwarp, int lane, WarpStage* st, unsigned long long seq = 1) {
   const int W = gridDim.x * kWarps;
   const int n = S.n_tasks;
   const int4 kNone{0, 0, 0, 0};
@@ -325,13 +333,22 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
     load_task(S, tk1, lane, nxt);
     const int r0 = tk.x, r1 = tk.y & kRowMask, kind = tk.y >> kKindShift;
     const int p0 = tk.z, len = tk.w - tk.z;
-    const bool has_row = kind == kTaskStream && lane < r1 - r0;
-    int ra = 0, rb = 0;
-    typename Epi::In in{};
+    // stream tasks: up to two rows per lane (lane, lane + 32); their bounds and
+    // epilogue inputs are loaded before the gathers so the latencies overlap
+    const int nrows = r1 - r0;
+    const bool has_row = kind == kTaskStream && lane < nrows;
+    const bool has_row2 = kind == kTaskStream && lane + 32 < nrows;
+    int ra = 0, rb = 0, ra2 = 0, rb2 = 0;
+    typename Epi::In in{}, in2{};
     if (has_row) {
       ra = __ldg(S.ptr + r0 + lane);
       rb = __ldg(S.ptr + r0 + lane + 1);
       in = epi.load(r0 + lane);
+    }
+    if (has_row2) {
+      ra2 = __ldg(S.ptr + r0 + lane + 32);
+      rb2 = __ldg(S.ptr + r0 + lane + 33);
+      in2 = epi.load(r0 + lane + 32);
     }
 #pragma unroll
     for (int j = 0; j < kLoadsPerLane; ++j) {
@@ -342,11 +359,28 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
 #pragma unroll
       for (int j = 0; j < kLoadsPerLane; ++j) st->prod[j * 32 + lane] = cur.cv[j];
       __syncwarp();
-      if (has_row) {
+      // ascending-order sums (the reference's), loads issued 4 ahead
+      auto row_sum = [&](int qa, int qe) {
         double s = 0.0;
-        for (int q = ra - p0; q < rb - p0; ++q) s += st->prod[q];
+        int q = qa;
+        for (; q + 4 <= qe; q += 4) {
+          const double a0 = st->prod[q], a1 = st->prod[q + 1], a2 = st->prod[q + 2], a3 = st->prod[q + 3];
+          s += a0;
+          s += a1;
+          s += a2;
+          s += a3;
+        }
+        for (; q < qe; ++q) s += st->prod[q];
+        return s;
+      };
+      if (has_row) {
         double tm[Q];
-        epi.apply(r0 + lane, s, in, tm);
+        epi.apply(r0 + lane, row_sum(ra - p0, rb - p0), in, tm);
+        acc_add<Q, MaxMask>(acc, tm);
+      }
+      if (has_row2) {
+        double tm[Q];
+        epi.apply(r0 + lane + 32, row_sum(ra2 - p0, rb2 - p0), in2, tm);
         acc_add<Q, MaxMask>(acc, tm);
       }
       __syncwarp();
@@ -377,6 +411,8 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
             double* lt = S.long_terms(set) + static_cast<long long>(meta.z) * kMaxQ;
 #pragma unroll
             for (int q = 0; q < Q; ++q) lt[q] = tm[q];
+            // publish to the owner CTA (fold_long): terms before flag
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(S.long_flag(set) + meta.z), "l"(seq) : "memory");
           }
         }
       }
@@ -384,6 +420,36 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
     tk = tk1;
     tk1 = tk2;
     cur = nxt;
+  }
+}
+
+// Owner side of the long-row protocol: warp 0 waits for each owned long row
+// of this phase (flag == seq) and folds its terms, in list order, into
+// lane 0's accumulators -- a fixed order, so totals stay bit-reproducible.
+template <int Q, unsigned MaxMask>
+__device__ __forceinline__ void fold_long(const Sched& S, int set, unsigned long long seq, double (&acc)[Q]) {
+  if (S.n_long == 0 || threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const int b = __ldg(S.owned_ptr + blockIdx.x), e = __ldg(S.owned_ptr + blockIdx.x + 1);
+  double part[Q];
+  acc_init<Q, MaxMask>(part);
+  const unsigned long long* flags = S.long_flag(set);
+  for (int i = b + lane; i < e; i += 32) {
+    const int k = __ldg(S.owned_idx + i);
+    const unsigned long long t0 = global_ns();
+    while (ld_acquire_u64(flags + k) < seq) {
+      if (global_ns() - t0 > 10000000000ull) break;  // watchdog (the barrier reports it)
+    }
+    const double* lt = S.long_terms(set) + static_cast<long long>(k) * kMaxQ;
+    double t[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) t[q] = ldcg(lt + q);
+    acc_add<Q, MaxMask>(part, t);
+  }
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const double v = ((MaxMask >> q) & 1u) ? warp_max(part[q]) : warp_sum(part[q]);
+    if (lane == 0) acc[q] = ((MaxMask >> q) & 1u) ? dmax(acc[q], v) : acc[q] + v;
   }
 }
 
@@ -520,12 +586,6 @@ struct EpiAbs {  // dual certificate: max |A u|
 // gpu-scope fence after the spin also invalidates this SM's L1
 // (CCTL.IVALL), so L1-cached gathers never see stale lines.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
 __device__ bool grid_sync(GridBar* bar, unsigned long long& target) {
   __shared__ int s_ok;
   __syncthreads();
@@ -855,7 +915,8 @@ __device__ __forceinline__ double* region_ptr(const KParams* P, int r) {
 __device__ __forceinline__ int gwarp_id() { return blockIdx.x * kWarps + (threadIdx.x >> 5); }
 
 // phase A: A^T y, primal step (+ Halpern formation of x), primal partials
-__device__ HX_PHASE_INLINE void phase_primal(const KParams* P, const Roles* R, int par, WarpStage* stage) {
+__device__ HX_PHASE_INLINE void phase_primal(const KParams* P, const Roles* R, int par, WarpStage* stage,
+                                             unsigned long long seq) {
   const int n = P->n, m = P->m;
   double acc[3];
   acc_init<3, 0>(acc);
@@ -869,12 +930,14 @@ __device__ HX_PHASE_INLINE void phase_primal(const KParams* P, const Roles* R, i
               R->x_mode};
   const Sched S = P->AT;
   spmv_rows<3, 0>(S, par, SrcVec{P->ypool + static_cast<size_t>(R->y_cur) * m}, e, acc, gwarp_id(),
-                  threadIdx.x & 31, stage);
+                  threadIdx.x & 31, stage, seq);
+  fold_long<3, 0>(S, par, seq, acc);
   block_to_slots<3, 0>(acc, region_ptr(P, kRegA + par), gridDim.x);
 }
 
 // phase B: A x+, dual step, speculative Halpern combos, dual partials
-__device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int par, WarpStage* stage) {
+__device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int par, WarpStage* stage,
+                                           unsigned long long seq) {
   const int n = P->n, m = P->m;
   double acc[4];
   acc_init<4, 0>(acc);
@@ -891,7 +954,8 @@ __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int
             R->w_next};
   const Sched S = P->A;
   spmv_rows<4, 0>(S, par, SrcVec{P->xpool + static_cast<size_t>(R->xp_out) * n}, e, acc, gwarp_id(),
-                  threadIdx.x & 31, stage);
+                  threadIdx.x & 31, stage, seq);
+  fold_long<4, 0>(S, par, seq, acc);
   block_to_slots<4, 0>(acc, region_ptr(P, kRegB + par), gridDim.x);
 }
 
@@ -899,31 +963,29 @@ __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int
 __device__ HX_PHASE_INLINE void totals_main(const KParams* P, int par, double* tot) {
   const double* ra = region_ptr(P, kRegA + par);
   const double* rb = region_ptr(P, kRegB + par);
-  const double* lta = P->AT.long_terms(par);
-  const double* ltb = P->A.long_terms(par);
-  const int na = P->AT.n_long, nb = P->A.n_long;
-  block_totals(7, [&](int q) {
-    return q < 3 ? QSrc{ra, q, na ? lta : nullptr, na, q, false} : QSrc{rb, q - 3, nb ? ltb : nullptr, nb, q - 3, false};
-  }, tot);
+  block_totals(7, [&](int q) { return q < 3 ? QSrc{ra, q, nullptr, 0, 0, false} : QSrc{rb, q - 3, nullptr, 0, 0, false}; },
+               tot);
 }
 
 // power iteration halves: w = A x (x = x0 or z / zn), z = A^T w
-__device__ HX_PHASE_INLINE void power_a(const KParams* P, const Roles* R, WarpStage* stage) {
+__device__ HX_PHASE_INLINE void power_a(const KParams* P, const Roles* R, WarpStage* stage, unsigned long long seq) {
   double acc[1];
   acc_init<1, 0>(acc);
   EpiStoreSq e{P->ypool};
   const Sched S = P->A;
-  if (R->pw_mode == 0) spmv_rows<1, 0>(S, 0, SrcVec{P->xpool}, e, acc, gwarp_id(), threadIdx.x & 31, stage);
-  else spmv_rows<1, 0>(S, 0, SrcDiv{P->xpool + P->n, R->pw_zn}, e, acc, gwarp_id(), threadIdx.x & 31, stage);
+  if (R->pw_mode == 0) spmv_rows<1, 0>(S, 0, SrcVec{P->xpool}, e, acc, gwarp_id(), threadIdx.x & 31, stage, seq);
+  else spmv_rows<1, 0>(S, 0, SrcDiv{P->xpool + P->n, R->pw_zn}, e, acc, gwarp_id(), threadIdx.x & 31, stage, seq);
+  fold_long<1, 0>(S, 0, seq, acc);
   block_to_slots<1, 0>(acc, region_ptr(P, kRegPA), gridDim.x);
 }
 
-__device__ HX_PHASE_INLINE void power_b(const KParams* P, WarpStage* stage) {
+__device__ HX_PHASE_INLINE void power_b(const KParams* P, WarpStage* stage, unsigned long long seq) {
   double acc[1];
   acc_init<1, 0>(acc);
   EpiStoreSq e{P->xpool + P->n};
   const Sched S = P->AT;
-  spmv_rows<1, 0>(S, 0, SrcVec{P->ypool}, e, acc, gwarp_id(), threadIdx.x & 31, stage);
+  spmv_rows<1, 0>(S, 0, SrcVec{P->ypool}, e, acc, gwarp_id(), threadIdx.x & 31, stage, seq);
+  fold_long<1, 0>(S, 0, seq, acc);
   block_to_slots<1, 0>(acc, region_ptr(P, kRegPB), gridDim.x);
 }
 
@@ -1018,7 +1080,8 @@ __device__ HX_PHASE_INLINE void cert_units(const KParams* P, const Roles* R) {
 }
 
 // certificate scan C3: the validation SpMVs, up to four independent products
-__device__ HX_PHASE_INLINE void cert_products(const KParams* P, const Roles* R, WarpStage* stage) {
+__device__ HX_PHASE_INLINE void cert_products(const KParams* P, const Roles* R, WarpStage* stage,
+                                              unsigned long long seq) {
   const int n = P->n, m = P->m;
   double acc[6];
   acc_init<6, 0x3Fu>(acc);
@@ -1034,14 +1097,16 @@ __device__ HX_PHASE_INLINE void cert_products(const KParams* P, const Roles* R, 
       double a2[2];
       acc_init<2, 3u>(a2);
       EpiPosNeg e;
-      spmv_rows<2, 3u>(AT, 2 + k, SrcVec{k ? u3 : u1}, e, a2, gw, lane, stage);
+      spmv_rows<2, 3u>(AT, 2 + k, SrcVec{k ? u3 : u1}, e, a2, gw, lane, stage, seq);
+      fold_long<2, 3u>(AT, 2 + k, seq, a2);
       acc[2 * k] = a2[0], acc[2 * k + 1] = a2[1];
     }
     if (R->cand_on[2 * k]) {
       double a1[1];
       acc_init<1, 1u>(a1);
       EpiAbs e;
-      spmv_rows<1, 1u>(A, 2 + k, SrcVec{k ? u2 : u0}, e, a1, gw, lane, stage);
+      spmv_rows<1, 1u>(A, 2 + k, SrcVec{k ? u2 : u0}, e, a1, gw, lane, stage, seq);
+      fold_long<1, 1u>(A, 2 + k, seq, a1);
       acc[4 + k] = a1[0];
     }
   }
@@ -1068,17 +1133,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
   const Roles* R = &C.r;
   GridBar* bar = P->bar;
   unsigned long long target = 0;
+  unsigned long long seq = 1;  // phase sequence number (long-row flags; reset per launch)
 
   if (C.mode == kModePower) {
     // power_iteration loop body, src/sparse_matrix.cpp:153-177
     while (!R->stop) {
-      power_a(P, R, stage);
+      power_a(P, R, stage, ++seq);
       if (!grid_sync(bar, target)) return;
       {
         const double* rg = region_ptr(P, kRegPA);
-        const double* lt = P->A.n_long ? P->A.long_terms(0) : nullptr;
-        const int nl = P->A.n_long;
-        block_totals(1, [&](int) { return QSrc{rg, 0, lt, nl, 0, false}; }, tot);
+        block_totals(1, [&](int) { return QSrc{rg, 0, nullptr, 0, 0, false}; }, tot);
       }
       if (threadIdx.x == 0) {
         const double sigma = sqrt(tot[0]);
@@ -1091,13 +1155,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
       }
       __syncthreads();
       if (R->stop) break;
-      power_b(P, stage);
+      power_b(P, stage, ++seq);
       if (!grid_sync(bar, target)) return;
       {
         const double* rg = region_ptr(P, kRegPB);
-        const double* lt = P->AT.n_long ? P->AT.long_terms(0) : nullptr;
-        const int nl = P->AT.n_long;
-        block_totals(1, [&](int) { return QSrc{rg, 0, lt, nl, 0, false}; }, tot + 1);
+        block_totals(1, [&](int) { return QSrc{rg, 0, nullptr, 0, 0, false}; }, tot + 1);
       }
       if (threadIdx.x == 0) {
         const double sigma = C.pw_sigma_cur;
@@ -1136,13 +1198,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
   };
   while (!R->stop) {
     const int par = static_cast<int>(C.it & 1);
-    phase_primal(P, R, par, stage);
+    phase_primal(P, R, par, stage, ++seq);
     if (writer && threadIdx.x == 0 && budget != 0ull)
       bar->time_up[par] = (global_ns() - t_start) > budget ? 1u : 0u;
     mark(0);
     if (!grid_sync(bar, target)) return;
     mark(1);
-    phase_dual(P, R, par, stage);
+    phase_dual(P, R, par, stage, ++seq);
     mark(2);
     if (!grid_sync(bar, target)) return;
     mark(3);
@@ -1219,17 +1281,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
       C.cinf[3] = tot[10], C.cdot[3] = tot[11];
     }
     __syncthreads();
-    cert_products(P, R, stage);
+    cert_products(P, R, stage, ++seq);
     if (!grid_sync(bar, target)) return;
     {
       const double* rg = region_ptr(P, kRegC3);
-      block_totals(6, [&](int q) {
-        const int set = 2 + (q < 4 ? (q >> 1) : (q - 4));
-        const int lq = q < 4 ? (q & 1) : 0;
-        const int nl = q < 4 ? P->AT.n_long : P->A.n_long;
-        const double* lt = nl ? (q < 4 ? P->AT.long_terms(set) : P->A.long_terms(set)) : nullptr;
-        return QSrc{rg, q, lt, nl, lq, true};
-      }, tot);
+      block_totals(6, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, true}; }, tot);
     }
     if (threadIdx.x == 0) {
       C.cmax_at[1] = tot[0], C.cmax_negat[1] = tot[1];
@@ -1422,6 +1478,9 @@ struct DevSched {
   double* part = nullptr;    // 4 * n_slots
   unsigned* cnt = nullptr;   // 4 * n_long
   double* terms = nullptr;   // 4 * n_long * kMaxQ
+  int* owned_ptr = nullptr;
+  int* owned_idx = nullptr;
+  unsigned long long* flags = nullptr;  // 4 * n_long
   Sched view;
   double max_cost = 0, mean_cost = 0;
 };
@@ -1492,7 +1551,7 @@ void dfree(void* p) {
 }
 
 void free_sched(DevSched& s) {
-  dfree(s.tasks), dfree(s.meta);
+  dfree(s.tasks), dfree(s.meta), dfree(s.owned_ptr), dfree(s.owned_idx), dfree(s.flags);
   dfree(s.part), dfree(s.cnt), dfree(s.terms);
   s = DevSched{};
 }
@@ -1515,10 +1574,15 @@ int upload_sched(hx_ctx* ctx, DevSched& d, const int* ptr_host, int rows, int co
   HX_CUDA(ctx, dalloc(&d.part, 4 * static_cast<size_t>(h.n_slots)));
   HX_CUDA(ctx, dalloc(&d.cnt, 4 * static_cast<size_t>(h.n_long)));
   HX_CUDA(ctx, dalloc(&d.terms, 4 * static_cast<size_t>(h.n_long) * kMaxQ));
+  HX_CUDA(ctx, dalloc(&d.owned_ptr, h.owned_ptr.size()));
+  HX_CUDA(ctx, dalloc(&d.owned_idx, h.owned_idx.size()));
+  HX_CUDA(ctx, dalloc(&d.flags, 4 * static_cast<size_t>(h.n_long)));
   auto cp = [&](void* dst, const void* src, size_t bytes) {
     return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream) : cudaSuccess;
   };
   HX_CUDA(ctx, cp(d.tasks, h.tasks.data(), h.tasks.size() * sizeof(int4)));
+  HX_CUDA(ctx, cp(d.owned_ptr, h.owned_ptr.data(), h.owned_ptr.size() * sizeof(int)));
+  HX_CUDA(ctx, cp(d.owned_idx, h.owned_idx.data(), h.owned_idx.size() * sizeof(int)));
   HX_CUDA(ctx, cp(d.meta, h.meta.data(), h.meta.size() * sizeof(int4)));
   HX_CUDA(ctx, cudaMemsetAsync(d.cnt, 0, std::max<size_t>(1, 4 * static_cast<size_t>(h.n_long)) * sizeof(unsigned),
                                ctx->stream));
@@ -1537,6 +1601,9 @@ int upload_sched(hx_ctx* ctx, DevSched& d, const int* ptr_host, int rows, int co
   v.cnt_base = d.cnt;
   v.terms_base = d.terms;
   v.n_slots = h.n_slots;
+  v.owned_ptr = d.owned_ptr;
+  v.owned_idx = d.owned_idx;
+  v.flag_base = d.flags;
   d.max_cost = h.max_warp_cost;
   d.mean_cost = h.mean_warp_cost;
   return HPLP_OK;
@@ -1567,6 +1634,10 @@ int launch_loop(hx_ctx* c) {
   void* args[] = {&P};
   HX_CUDA(c, cudaMemcpyAsync(c->ctl, &c->h, sizeof(Ctl), cudaMemcpyHostToDevice, c->stream));
   HX_CUDA(c, cudaMemsetAsync(c->bar, 0, sizeof(GridBar), c->stream));
+  for (DevSched* d : {&c->sa, &c->st})  // long-row flags restart with the per-launch sequence
+    if (d->view.n_long)
+      HX_CUDA(c, cudaMemsetAsync(d->flags, 0, 4 * static_cast<size_t>(d->view.n_long) * sizeof(unsigned long long),
+                                 c->stream));
   HX_CUDA(c, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(loop_kernel), dim3(c->grid), dim3(kThreads),
                                          args, kStageBytes, c->stream));
   c->launches += 1;

@@ -40,7 +40,7 @@ constexpr double kTaskCost = 64.0;         // fixed latency cost of one warp tas
 constexpr int kLoadsPerLane = HX_LOADS;    // nonzeros per lane per task
 constexpr int kChunk = 32 * kLoadsPerLane; // max nonzeros per warp task (256)
 constexpr int kStreamRowMax = 64;          // rows up to this length are summed lane-per-row
-constexpr int kStreamRowsMax = 32;         // rows per stream task (one per lane)
+constexpr int kStreamRowsMax = 64;         // rows per stream task (two per lane)
 
 // Warp tasks, int4 {row_begin, row_end | kind << 30, p_begin, p_end}; every
 // task covers at most kChunk nonzeros, loaded kLoadsPerLane per lane into
@@ -77,6 +77,17 @@ struct Sched {
   unsigned* cnt_base = nullptr;  // [4][n_long]
   double* terms_base = nullptr;  // [4][n_long * kMaxQ]
   int n_slots = 0;
+  // Each multi-piece ("long") row has a static owner CTA (the one running its
+  // piece 0): the last piece to finish publishes the row's epilogue terms and
+  // a sequence flag; the owner folds its rows' terms into its own partial
+  // record in list order.  owned_idx[owned_ptr[c] .. owned_ptr[c+1]) are the
+  // long rows CTA c owns.
+  const int* owned_ptr = nullptr;             // [grid + 1]
+  const int* owned_idx = nullptr;
+  unsigned long long* flag_base = nullptr;    // [4][n_long] phase sequence flags
+  __host__ __device__ unsigned long long* long_flag(int set) const {
+    return flag_base + static_cast<size_t>(set) * n_long;
+  }
   __host__ __device__ double* piece_part(int set) const { return part_base + static_cast<size_t>(set) * n_slots; }
   __host__ __device__ unsigned* piece_cnt(int set) const { return cnt_base + static_cast<size_t>(set) * n_long; }
   __host__ __device__ double* long_terms(int set) const {
@@ -88,6 +99,8 @@ struct Sched {
 struct SchedHost {
   std::vector<int4> tasks;
   std::vector<int4> meta;
+  std::vector<int> owned_ptr;  // [grid + 1]
+  std::vector<int> owned_idx;
   int n_long = 0;
   int n_slots = 0;
   double max_warp_cost = 0.0, mean_warp_cost = 0.0;

@@ -92,6 +92,21 @@ SchedHost build_schedule(const int* ptr, int rows, int warps) {
   }
   s.tasks.swap(tasks);
   s.meta.swap(meta);
+  // owner CTA of every long row = the CTA whose warp runs its piece 0
+  const int grid = warps / kWarps;
+  std::vector<int> owner(static_cast<std::size_t>(s.n_long), 0);
+  for (std::size_t k = 0; k < s.tasks.size(); ++k) {
+    const int4& tk = s.tasks[k];
+    const int4& mt = s.meta[k];
+    if ((tk.y >> kKindShift) == kTaskPiece && mt.y > 1 && mt.w == 0)
+      owner[mt.z] = static_cast<int>(k % static_cast<std::size_t>(warps)) / kWarps;
+  }
+  s.owned_ptr.assign(static_cast<std::size_t>(grid) + 1, 0);
+  for (int l = 0; l < s.n_long; ++l) ++s.owned_ptr[owner[l] + 1];
+  for (int c = 0; c < grid; ++c) s.owned_ptr[c + 1] += s.owned_ptr[c];
+  s.owned_idx.assign(static_cast<std::size_t>(s.n_long), 0);
+  std::vector<int> fill(s.owned_ptr.begin(), s.owned_ptr.end() - 1);
+  for (int l = 0; l < s.n_long; ++l) s.owned_idx[fill[owner[l]]++] = l;
   double mx = 0.0;
   for (double c : wcost) mx = std::max(mx, c);
   s.max_warp_cost = mx;
