@@ -81,7 +81,7 @@ struct Ctl {
   long long it, n, k, spmv, batch_end, n_epochs;
   double res_epoch_start, best_kkt, best_err[4];
   int x_best, y_best;
-  int status, error, paused, pad1;
+  int status, error, paused, x_best_prev;  // x_best before this iteration's update
   long long last_it, last_n, last_k;
   double last_res, last_kkt[4];
   int last_zx, last_y, last_xp, last_yp, last_xa, last_ya, last_ax, last_axp;
@@ -313,9 +313,28 @@ __device__ __forceinline__ void load_task(const Sched& S, const int4& tk, int la
   }
 }
 
+// The pipeline's head: the first two task descriptors and the first task's
+// index/value registers.  They depend only on the (read-only) matrix, so a
+// phase's head is loaded before the grid barrier that precedes the phase and
+// its latency hides behind the barrier wait.
+struct SpmvHead {
+  int4 tk, tk1;
+  TaskRegs cur;
+};
+
+__device__ __forceinline__ void spmv_head(const Sched& S, int gwarp, int lane, SpmvHead& h) {
+  const int W = gridDim.x * kWarps;
+  const int n = S.n_tasks;
+  const int4 kNone{0, 0, 0, 0};
+  h.tk = gwarp < n ? __ldg(S.tasks + gwarp) : kNone;
+  h.tk1 = gwarp + W < n ? __ldg(S.tasks + gwarp + W) : kNone;
+  load_task(S, h.tk, lane, h.cur);
+}
+
 template <int Q, unsigned MaxMask, class Src, class Epi>
 __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& src, Epi& epi, double (&acc)[Q],
-                                          int gwarp, int lane, WarpStage* st, unsigned long long seq = 1) {
+                                          int gwarp, int lane, WarpStage* st, unsigned long long seq,
+                                          const SpmvHead& head) {
   const int W = gridDim.x * kWarps;
   const int n = S.n_tasks;
   const int4 kNone{0, 0, 0, 0};
@@ -323,10 +342,9 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
   if (t >= n) return;
   // software pipeline: descriptors two tasks ahead, index/value loads one
   // task ahead of the gathers
-  int4 tk = __ldg(S.tasks + t);
-  int4 tk1 = t + W < n ? __ldg(S.tasks + t + W) : kNone;
-  TaskRegs cur;
-  load_task(S, tk, lane, cur);
+  int4 tk = head.tk;
+  int4 tk1 = head.tk1;
+  TaskRegs cur = head.cur;
   for (; t < n; t += W) {
     const int4 tk2 = t + 2 * W < n ? __ldg(S.tasks + t + 2 * W) : kNone;
     TaskRegs nxt;
@@ -421,6 +439,14 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
     tk1 = tk2;
     cur = nxt;
   }
+}
+
+template <int Q, unsigned MaxMask, class Src, class Epi>
+__device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& src, Epi& epi, double (&acc)[Q],
+                                          int gwarp, int lane, WarpStage* st, unsigned long long seq = 1) {
+  SpmvHead head;
+  spmv_head(S, gwarp, lane, head);
+  spmv_rows<Q, MaxMask>(S, set, src, epi, acc, gwarp, lane, st, seq, head);
 }
 
 // Owner side of the long-row protocol: warp 0 waits for each owned long row
@@ -621,9 +647,9 @@ __device__ bool grid_sync(GridBar* bar, unsigned long long& target) {
 // Controller logic (thread 0 of every CTA, on its shared replica).  Only CTA 0
 // (writer) touches global memory (epoch ring).
 // ---------------------------------------------------------------------------
-__device__ int pick_free(int pool, int e0, int e1, int e2, int e3) {
+__device__ int pick_free(int pool, int e0, int e1, int e2, int e3, int e4 = -1, int e5 = -1) {
   for (int i = 0; i < pool; ++i)
-    if (i != e0 && i != e1 && i != e2 && i != e3) return i;
+    if (i != e0 && i != e1 && i != e2 && i != e3 && i != e4 && i != e5) return i;
   return -1;
 }
 
@@ -684,8 +710,11 @@ __device__ void finish_iteration(Ctl& C, hplp_epoch_t* epochs, bool writer, doub
   }
   R.check = 0;
   C.it += 1;
-  R.zx_out = pick_free(kXPool, R.x_src, R.x_anchor, C.x_best, -1);
-  R.xp_out = pick_free(kXPool, R.x_src, R.x_anchor, C.x_best, R.zx_out);
+  // x outputs avoid this iteration's T(z) and the best iterate before and
+  // after its update too, so that without a restart the picks equal the
+  // speculative ones (make_spec), which cannot know the update yet
+  R.zx_out = pick_free(kXPool, R.x_src, R.x_anchor, C.x_best, C.last_zx, C.x_best_prev);
+  R.xp_out = pick_free(kXPool, R.x_src, R.x_anchor, C.x_best, C.last_zx, C.x_best_prev, R.zx_out);
   R.yp_out = pick_free(kYPool, R.y_cur, R.y_anchor, C.y_best, -1);
   R.yc_out = pick_free(kYPool, R.y_cur, R.y_anchor, C.y_best, R.yp_out);
   R.axp_out = pick_free(kAxPool, R.ax_cur, R.ax_anchor, -1, -1);
@@ -745,6 +774,7 @@ __device__ void main_logic(Ctl& C, const double* tot, const double* pre, hplp_ep
     }
     C.n_epochs += 1;
   }
+  C.x_best_prev = C.x_best;
   if (kkt[3] < C.best_kkt) {  // :265-269
     C.best_kkt = kkt[3];
     for (int i = 0; i < 4; ++i) C.best_err[i] = kkt[i];
@@ -890,6 +920,28 @@ __device__ void scan_logic(Ctl& C, hplp_epoch_t* epochs, bool writer, bool time_
   finish_iteration(C, epochs, writer, C.last_res, time_up);
 }
 
+// Roles of phase A for iteration it+1 assuming no restart and no stop
+// (finish_iteration's no-restart branch), known before the controller runs.
+// The x outputs avoid T(z) of iteration it and the current best, the two
+// candidates for the best after the update, so they equal finish_iteration's
+// picks whenever no restart happens.
+__device__ void make_spec(const Ctl& C, Roles& S) {
+  const Roles& R = C.r;
+  S = R;
+  S.x_src = R.xp_out;
+  S.x_mode = 1;
+  S.w_x = 1.0 / static_cast<double>(C.k + 2);
+  S.y_cur = R.yc_out;
+  S.zx_out = pick_free(kXPool, S.x_src, S.x_anchor, C.x_best, R.zx_out);
+  S.xp_out = pick_free(kXPool, S.x_src, S.x_anchor, C.x_best, R.zx_out, S.zx_out);
+}
+
+// Did the speculative phase A compute exactly what phase A with roles R would?
+__device__ __forceinline__ bool same_phase_a(const Roles& R, const Roles& S) {
+  return R.x_mode == S.x_mode && R.x_src == S.x_src && R.x_anchor == S.x_anchor && R.zx_out == S.zx_out &&
+         R.xp_out == S.xp_out && R.y_cur == S.y_cur && R.w_x == S.w_x && R.eta == S.eta;
+}
+
 __device__ void ctl_load(const Ctl* g, Ctl& s) {
   const unsigned long long* src = reinterpret_cast<const unsigned long long*>(g);
   unsigned long long* dst = reinterpret_cast<unsigned long long*>(&s);
@@ -916,7 +968,7 @@ __device__ __forceinline__ int gwarp_id() { return blockIdx.x * kWarps + (thread
 
 // phase A: A^T y, primal step (+ Halpern formation of x), primal partials
 __device__ HX_PHASE_INLINE void phase_primal(const KParams* P, const Roles* R, int par, WarpStage* stage,
-                                             unsigned long long seq) {
+                                             unsigned long long seq, const SpmvHead& head) {
   const int n = P->n, m = P->m;
   double acc[3];
   acc_init<3, 0>(acc);
@@ -930,14 +982,14 @@ __device__ HX_PHASE_INLINE void phase_primal(const KParams* P, const Roles* R, i
               R->x_mode};
   const Sched S = P->AT;
   spmv_rows<3, 0>(S, par, SrcVec{P->ypool + static_cast<size_t>(R->y_cur) * m}, e, acc, gwarp_id(),
-                  threadIdx.x & 31, stage, seq);
+                  threadIdx.x & 31, stage, seq, head);
   fold_long<3, 0>(S, par, seq, acc);
   block_to_slots<3, 0>(acc, region_ptr(P, kRegA + par), gridDim.x);
 }
 
 // phase B: A x+, dual step, speculative Halpern combos, dual partials
 __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int par, WarpStage* stage,
-                                           unsigned long long seq) {
+                                           unsigned long long seq, const SpmvHead& head) {
   const int n = P->n, m = P->m;
   double acc[4];
   acc_init<4, 0>(acc);
@@ -954,17 +1006,43 @@ __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int
             R->w_next};
   const Sched S = P->A;
   spmv_rows<4, 0>(S, par, SrcVec{P->xpool + static_cast<size_t>(R->xp_out) * n}, e, acc, gwarp_id(),
-                  threadIdx.x & 31, stage, seq);
+                  threadIdx.x & 31, stage, seq, head);
   fold_long<4, 0>(S, par, seq, acc);
   block_to_slots<4, 0>(acc, region_ptr(P, kRegB + par), gridDim.x);
 }
 
-// totals of phases A+B -> tot[0..6]
-__device__ HX_PHASE_INLINE void totals_main(const KParams* P, int par, double* tot) {
-  const double* ra = region_ptr(P, kRegA + par);
-  const double* rb = region_ptr(P, kRegB + par);
-  block_totals(7, [&](int q) { return q < 3 ? QSrc{ra, q, nullptr, 0, 0, false} : QSrc{rb, q - 3, nullptr, 0, 0, false}; },
-               tot);
+// Totals of phases A+B -> t[0..6], computed by warp 0 alone (the other warps
+// are in the speculative phase A by then): lane l sums records l, l + 32, ...
+// and a xor butterfly finishes -- commutative pairwise adds, so every lane of
+// every CTA holds bit-identical totals.
+constexpr int kTotRounds = 5;  // 160 records in one round of loads
+__device__ __forceinline__ void warp_totals_main(const KParams* P, int par, double (&t)[7]) {
+  const int lane = threadIdx.x & 31, G = gridDim.x;
+  const size_t rep = static_cast<size_t>(blockIdx.x % kReplicas) * G * kMaxQ;
+  const double* ra = region_ptr(P, kRegA + par) + rep;
+  const double* rb = region_ptr(P, kRegB + par) + rep;
+#pragma unroll
+  for (int q = 0; q < 7; ++q) t[q] = 0.0;
+  for (int base = 0; base < G; base += 32 * kTotRounds) {
+    double v[kTotRounds][7];
+#pragma unroll
+    for (int i = 0; i < kTotRounds; ++i) {
+      const int c = base + 32 * i + lane;
+      const bool ok = c < G;
+      const double* a = ra + static_cast<size_t>(c) * kMaxQ;
+      const double* b = rb + static_cast<size_t>(c) * kMaxQ;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) v[i][q] = ok ? ldcg(a + q) : 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[i][3 + q] = ok ? ldcg(b + q) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < kTotRounds; ++i)
+#pragma unroll
+      for (int q = 0; q < 7; ++q) t[q] += v[i][q];
+  }
+#pragma unroll
+  for (int q = 0; q < 7; ++q) t[q] = warp_sum(t[q]);
 }
 
 // power iteration halves: w = A x (x = x0 or z / zn), z = A^T w
@@ -1196,33 +1274,47 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
       tp = t;
     }
   };
+  // Phase A of iteration it+1 runs speculatively (roles of "no restart,
+  // no stop": make_spec) in warps 1..15 while warp 0 reduces the partials
+  // and runs the controller of iteration it; warp 0 then runs its own,
+  // lighter, share of the tasks (the schedule's lead).  When the decision
+  // differs from the speculation (a restart, a stop), every CTA waits for
+  // the speculative phase to finish everywhere and phase A is redone with
+  // the real roles.  The speculative outputs go to buffers no live role
+  // uses, so a discarded speculation leaves no trace.
+  __shared__ Roles SR;
+  bool spec_done = false;
   while (!R->stop) {
     const int par = static_cast<int>(C.it & 1);
-    phase_primal(P, R, par, stage, ++seq);
-    if (writer && threadIdx.x == 0 && budget != 0ull)
-      bar->time_up[par] = (global_ns() - t_start) > budget ? 1u : 0u;
+    SpmvHead head;
+    if (!spec_done) {
+      spmv_head(P->AT, gwarp_id(), lane, head);
+      phase_primal(P, R, par, stage, ++seq, head);
+      if (writer && threadIdx.x == 0 && budget != 0ull)
+        bar->time_up[par] = (global_ns() - t_start) > budget ? 1u : 0u;
+    }
     mark(0);
+    spmv_head(P->A, gwarp_id(), lane, head);
     if (!grid_sync(bar, target)) return;
     mark(1);
-    phase_dual(P, R, par, stage, ++seq);
+    phase_dual(P, R, par, stage, ++seq, head);
+    if (threadIdx.x == 0) make_spec(C, SR);
     mark(2);
+    spmv_head(P->AT, gwarp_id(), lane, head);
     if (!grid_sync(bar, target)) return;
     mark(3);
-    totals_main(P, par, tot);
-    if (threadIdx.x == 7 * 32) s_time_up = budget != 0ull && *reinterpret_cast<volatile unsigned*>(&bar->time_up[par]) != 0u;
-    __syncthreads();
-    mark(4);
-    unsigned long long cA = clock64(), cB = 0, cC = 0;
     if (warp == 0) {
+      unsigned long long cA = clock64(), cB = 0, cC = 0;
+      double t[7];
+      warp_totals_main(P, par, t);
       // the independent fp64 divides / square roots, one per lane, executed
       // uniformly (operands selected per lane, one sqrt + one divide)
-      const double t0 = tot[0], t1 = tot[1], t2 = tot[2], t3 = tot[3], t4 = tot[4], t5 = tot[5];
       double num = 1.0, den = 1.0;
-      if (lane == 0) num = t3, den = 1.0 + C.b_norm;
-      else if (lane == 1) num = t0, den = 1.0 + C.c_norm;
-      else if (lane == 2) num = fabs(t1 + t4), den = 1.0 + fabs(t1) + fabs(t4);
-      else if (lane == 3) num = t2, den = C.r.eta;
-      else if (lane == 4) num = t5, den = C.r.eta;
+      if (lane == 0) num = t[3], den = 1.0 + C.b_norm;
+      else if (lane == 1) num = t[0], den = 1.0 + C.c_norm;
+      else if (lane == 2) num = fabs(t[1] + t[4]), den = 1.0 + fabs(t[1]) + fabs(t[4]);
+      else if (lane == 3) num = t[2], den = C.r.eta;
+      else if (lane == 4) num = t[5], den = C.r.eta;
       else if (lane == 5) den = static_cast<double>(C.k + 2);
       else if (lane == 6) den = static_cast<double>(C.k + 3);
       const double sq = sqrt(num);
@@ -1232,68 +1324,84 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
       for (int i = 0; i < 7; ++i) pre[i] = __shfl_sync(0xffffffffu, v, i);
       cB = clock64();
       if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < 7; ++i) tot[i] = t[i];
+        s_time_up = budget != 0ull && *reinterpret_cast<volatile unsigned*>(&bar->time_up[par]) != 0u;
         C.w_k2 = pre[5];
         C.w_k3 = pre[6];
         main_logic(C, tot, pre, P->epochs, writer, s_time_up != 0);
       }
       cC = clock64();
-    }
-    __syncthreads();
-    if (prof && threadIdx.x == 0) {
-      pacc2[0] += cB - cA;
-      pacc2[1] += cC - cB;
-      pacc2[2] += clock64() - cC;
-    }
-    mark(6);
-    if (prof && threadIdx.x == 0) pacc[5] += 1;
-    if (!R->check) continue;
-
-    // ---- certificate scan (src/solver.cpp:297-317) ----
-    cert_norms(P, R);
-    if (!grid_sync(bar, target)) return;
-    {
-      const double* rg = region_ptr(P, kRegC1);
-      block_totals(8, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, false}; }, tot);
-    }
-    if (threadIdx.x == 0) {
-      int any = 0;
-      for (int c = 0; c < 4; ++c) {
-        C.r.cn2[c] = sqrt(tot[c]);
-        C.cfinite[c] = tot[4 + c] == 0.0;
-        const bool normalized = c >= 2;
-        C.r.cand_on[c] = (!normalized || C.last_k >= 1) && C.r.cn2[c] > 0.0 && C.cfinite[c];
-        any |= C.r.cand_on[c];
+      __syncwarp();
+      if (prof && threadIdx.x == 0) {
+        pacc2[0] += cB - cA;
+        pacc2[1] += cC - cB;
       }
-      if (!any) scan_logic(C, P->epochs, writer, s_time_up != 0);  // nothing to validate
     }
+    mark(4);
+    // speculative phase A of iteration it+1
+    phase_primal(P, &SR, par ^ 1, stage, ++seq, head);
+    if (writer && threadIdx.x == 0 && budget != 0ull)
+      bar->time_up[par ^ 1] = (global_ns() - t_start) > budget ? 1u : 0u;
     __syncthreads();
-    if (!R->check) continue;
-    cert_units(P, R);
-    if (!grid_sync(bar, target)) return;
-    {
-      const double* rg = region_ptr(P, kRegC2);
-      block_totals(12, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, ((0x577u >> q) & 1u) != 0}; }, tot);
+    mark(0);
+    if (prof && threadIdx.x == 0) pacc[5] += 1;
+
+    if (R->check) {
+      // ---- certificate scan (src/solver.cpp:297-317) ----
+      cert_norms(P, R);
+      if (!grid_sync(bar, target)) return;
+      {
+        const double* rg = region_ptr(P, kRegC1);
+        block_totals(8, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, false}; }, tot);
+      }
+      if (threadIdx.x == 0) {
+        int any = 0;
+        for (int c = 0; c < 4; ++c) {
+          C.r.cn2[c] = sqrt(tot[c]);
+          C.cfinite[c] = tot[4 + c] == 0.0;
+          const bool normalized = c >= 2;
+          C.r.cand_on[c] = (!normalized || C.last_k >= 1) && C.r.cn2[c] > 0.0 && C.cfinite[c];
+          any |= C.r.cand_on[c];
+        }
+        if (!any) scan_logic(C, P->epochs, writer, s_time_up != 0);  // nothing to validate
+      }
+      __syncthreads();
+      if (R->check) {
+        cert_units(P, R);
+        if (!grid_sync(bar, target)) return;
+        {
+          const double* rg = region_ptr(P, kRegC2);
+          block_totals(12, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, ((0x577u >> q) & 1u) != 0}; }, tot);
+        }
+        if (threadIdx.x == 0) {
+          C.cinf[0] = tot[0], C.cmax_u[0] = tot[1], C.cmax_negu[0] = tot[2], C.cdot[0] = tot[3];
+          C.cinf[2] = tot[4], C.cmax_u[2] = tot[5], C.cmax_negu[2] = tot[6], C.cdot[2] = tot[7];
+          C.cinf[1] = tot[8], C.cdot[1] = tot[9];
+          C.cinf[3] = tot[10], C.cdot[3] = tot[11];
+        }
+        __syncthreads();
+        cert_products(P, R, stage, ++seq);
+        if (!grid_sync(bar, target)) return;
+        {
+          const double* rg = region_ptr(P, kRegC3);
+          block_totals(6, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, true}; }, tot);
+        }
+        if (threadIdx.x == 0) {
+          C.cmax_at[1] = tot[0], C.cmax_negat[1] = tot[1];
+          C.cmax_at[3] = tot[2], C.cmax_negat[3] = tot[3];
+          C.cmax_abs_au[0] = tot[4], C.cmax_abs_au[2] = tot[5];
+          scan_logic(C, P->epochs, writer, s_time_up != 0);
+        }
+        __syncthreads();
+      }
     }
-    if (threadIdx.x == 0) {
-      C.cinf[0] = tot[0], C.cmax_u[0] = tot[1], C.cmax_negu[0] = tot[2], C.cdot[0] = tot[3];
-      C.cinf[2] = tot[4], C.cmax_u[2] = tot[5], C.cmax_negu[2] = tot[6], C.cdot[2] = tot[7];
-      C.cinf[1] = tot[8], C.cdot[1] = tot[9];
-      C.cinf[3] = tot[10], C.cdot[3] = tot[11];
-    }
-    __syncthreads();
-    cert_products(P, R, stage, ++seq);
-    if (!grid_sync(bar, target)) return;
-    {
-      const double* rg = region_ptr(P, kRegC3);
-      block_totals(6, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, true}; }, tot);
-    }
-    if (threadIdx.x == 0) {
-      C.cmax_at[1] = tot[0], C.cmax_negat[1] = tot[1];
-      C.cmax_at[3] = tot[2], C.cmax_negat[3] = tot[3];
-      C.cmax_abs_au[0] = tot[4], C.cmax_abs_au[2] = tot[5];
-      scan_logic(C, P->epochs, writer, s_time_up != 0);
-    }
-    __syncthreads();
+    if (R->stop) break;
+    spec_done = same_phase_a(*R, SR);
+    // a redo reuses this parity's long-row counters: wait until every CTA's
+    // speculative phase A is complete
+    if (!spec_done && !grid_sync(bar, target)) return;
+    mark(6);
   }
   if (prof && threadIdx.x == 0) {
     for (int k = 0; k < 6; ++k) prof[k] += pacc[k];
@@ -1567,8 +1675,8 @@ void free_problem(hx_ctx* c) {
 }
 
 int upload_sched(hx_ctx* ctx, DevSched& d, const int* ptr_host, int rows, int cols, const int* dptr,
-                 const int* didx, const double* dval) {
-  SchedHost h = build_schedule(ptr_host, rows, ctx->grid * kWarps);
+                 const int* didx, const double* dval, double lead = 0.0) {
+  SchedHost h = build_schedule(ptr_host, rows, ctx->grid * kWarps, lead);
   HX_CUDA(ctx, dalloc(&d.tasks, h.tasks.size()));
   HX_CUDA(ctx, dalloc(&d.meta, h.meta.size()));
   HX_CUDA(ctx, dalloc(&d.part, 4 * static_cast<size_t>(h.n_slots)));
@@ -1856,7 +1964,13 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     int rc = upload_sched(c, c->sa, ph.data(), static_cast<int>(m), static_cast<int>(n), c->a_ptr, c->a_idx,
                           c->a_val);
     if (rc) return rc;
-    rc = upload_sched(c, c->st, pt.data(), static_cast<int>(n), static_cast<int>(m), c->t_ptr, c->t_idx, c->t_val);
+    // phase A (rows of A^T) runs speculatively while warp 0 of every CTA runs
+    // the controller: warp 0 starts with a lead of about the controller's
+    // latency, in schedule cost units (~100 per microsecond on B200)
+    double lead = 1200.0;
+    if (const char* e = std::getenv("HX_LEAD")) lead = std::atof(e);
+    rc = upload_sched(c, c->st, pt.data(), static_cast<int>(n), static_cast<int>(m), c->t_ptr, c->t_idx, c->t_val,
+                      lead);
     if (rc) return rc;
   }
   HX_CUDA(c, dalloc(&c->xpool, static_cast<size_t>(kXPool) * n));
@@ -2034,7 +2148,7 @@ int hx_setup(hx_ctx* c, const hplp_config_t* cfg, double sigma_used, double eta,
   c->time_limit_s = cfg->time_limit_seconds;
   c->loop_elapsed_s = 0.0;
   C.best_kkt = std::numeric_limits<double>::infinity();
-  C.x_best = C.y_best = -1;
+  C.x_best = C.y_best = C.x_best_prev = -1;
   C.status = -1;
   C.final_x = C.final_y = -1;
   C.cert_cand[0] = C.cert_cand[1] = -1;

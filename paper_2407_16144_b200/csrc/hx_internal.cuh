@@ -28,7 +28,7 @@ constexpr int kMinBlocks = HX_MIN_BLOCKS;         // resident CTAs per SM the re
 #define HX_PHASE_INLINE __forceinline__
 #endif
 constexpr int kMaxQ = 16;                  // reduction quantities per phase
-constexpr int kXPool = 6;                  // n-vectors: iterates, anchors, best, T(z)
+constexpr int kXPool = 7;                  // n-vectors: iterates, anchors, best, T(z), speculative outputs
 constexpr int kYPool = 6;                  // m-vectors: y, anchors, best, T(z), combos
 constexpr int kAxPool = 4;                 // m-vectors: A x carried / anchor / products
 constexpr int kEpochCap = 1 << 16;         // device epoch ring (host drains per hx_run)
@@ -106,6 +106,8 @@ struct SchedHost {
   double max_warp_cost = 0.0, mean_warp_cost = 0.0;
 };
 
-SchedHost build_schedule(const int* ptr_host, int rows, int warps);
+// lead: initial load (cost units) of warp 0 of every CTA, which runs the
+// controller before its own tasks in the speculative phase A.
+SchedHost build_schedule(const int* ptr_host, int rows, int warps, double lead = 0.0);
 
 }  // namespace hx

@@ -16,7 +16,7 @@
 
 namespace hx {
 
-SchedHost build_schedule(const int* ptr, int rows, int warps) {
+SchedHost build_schedule(const int* ptr, int rows, int warps, double lead) {
   SchedHost s;
   const int64_t nnz = ptr[rows];
   const double total = static_cast<double>(nnz) + kRowCost * rows;
@@ -68,9 +68,12 @@ SchedHost build_schedule(const int* ptr, int rows, int warps) {
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
   using Load = std::pair<double, int>;  // (load, warp)
   std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
-  for (int w = 0; w < warps; ++w) heap.push({0.0, w});
   std::vector<std::vector<int>> per_warp(static_cast<std::size_t>(warps));
   std::vector<double> wcost(static_cast<std::size_t>(warps), 0.0);
+  for (int w = 0; w < warps; ++w) {
+    wcost[w] = w % kWarps == 0 ? lead : 0.0;
+    heap.push({wcost[w], w});
+  }
   for (int t : order) {
     auto [load, w] = heap.top();
     heap.pop();
@@ -108,7 +111,7 @@ SchedHost build_schedule(const int* ptr, int rows, int warps) {
   std::vector<int> fill(s.owned_ptr.begin(), s.owned_ptr.end() - 1);
   for (int l = 0; l < s.n_long; ++l) s.owned_idx[fill[owner[l]]++] = l;
   double mx = 0.0;
-  for (double c : wcost) mx = std::max(mx, c);
+  for (int w = 0; w < warps; ++w) mx = std::max(mx, wcost[w] - (w % kWarps == 0 ? lead : 0.0));
   s.max_warp_cost = mx;
   s.mean_warp_cost = total / warps;
   return s;

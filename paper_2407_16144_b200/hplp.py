@@ -391,8 +391,11 @@ class HX:
         self._c(lib().hx_profile(self.h, buf, int(reset)))
         a = np.array(buf[:], dtype=np.float64).reshape(g, 16)
         its = max(a[0, 5], 1.0)
-        names = {"phase_A": 0, "barrier1": 1, "phase_B": 2, "barrier2": 3, "totals": 4, "controller_logic": 7,
-                 "ctl_math": 8, "ctl_scalar": 9, "ctl_sync": 10}
+        # phase_A: the (speculative) phase A after warp 0's controller; controller:
+        # warp 0's totals + logic (its split: ctl_totals / ctl_scalar);
+        # scan_or_redo: certificate scans and redone phases A
+        names = {"phase_A": 0, "barrier1": 1, "phase_B": 2, "barrier2": 3, "controller": 4, "scan_or_redo": 7,
+                 "ctl_totals": 8, "ctl_scalar": 9}
         k = 1.0 / its / sm_mhz  # cycles -> us per iteration
         return {nm: dict(mean_us=float(a[:, i].mean() * k), max_us=float(a[:, i].max() * k),
                          min_us=float(a[:, i].min() * k)) for nm, i in names.items()}
