@@ -125,10 +125,17 @@ int hx_get_certificate(hx_ctx* ctx, int32_t kind, double* vec);
  * products (the limit path of src/solver.cpp:242-254 when no best exists). */
 int hx_kkt_current(hx_ctx* ctx, hplp_kkt_t* out);
 
+/* The warp task list of the fused SpMV (which: 0 rows of A, 1 rows of A^T),
+ * 4 int32 per task {row_begin, row_end | kind << 30, nz_begin, nz_end}; warp w
+ * of the grid runs tasks w, w + W, w + 2W, ... (W = grid * warps per CTA).
+ * Diagnostics: the schedule's per-warp composition. */
+int hx_sched_tasks(hx_ctx* ctx, int32_t which, int32_t* out, int64_t capacity, int64_t* count);
+
 /* Diagnostics: per-CTA phase timers when the context was created with
- * HX_PROFILE=1 in the environment; out holds grid * 16 counters (SM cycles):
- * phase A, barrier 1, phase B, barrier 2, totals, iterations, smid,
- * controller, controller math / scalar / sync. */
+ * HX_PROFILE=1 in the environment; out holds grid * (16 + 2 * warps per CTA)
+ * counters (SM cycles): per CTA phase A, barrier 1, phase B, barrier 2,
+ * controller, iterations, smid, scan/redo, controller totals / scalar; then
+ * (builds with -DHX_WPROF only) per-warp SpMV cycles of phase A and B. */
 int hx_profile(hx_ctx* ctx, unsigned long long* out, int32_t reset);
 
 /* sizeof checks for the ABI tests. */

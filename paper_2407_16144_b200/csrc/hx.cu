@@ -981,8 +981,15 @@ __device__ HX_PHASE_INLINE void phase_primal(const KParams* P, const Roles* R, i
               R->eta,
               R->x_mode};
   const Sched S = P->AT;
+#ifdef HX_WPROF
+  const unsigned long long w0 = clock64();
+#endif
   spmv_rows<3, 0>(S, par, SrcVec{P->ypool + static_cast<size_t>(R->y_cur) * m}, e, acc, gwarp_id(),
                   threadIdx.x & 31, stage, seq, head);
+#ifdef HX_WPROF
+  if (P->prof && (threadIdx.x & 31) == 0)
+    P->prof[gridDim.x * 16 + gwarp_id()] += clock64() - w0;
+#endif
   fold_long<3, 0>(S, par, seq, acc);
   block_to_slots<3, 0>(acc, region_ptr(P, kRegA + par), gridDim.x);
 }
@@ -1005,8 +1012,15 @@ __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int
             R->eta,
             R->w_next};
   const Sched S = P->A;
+#ifdef HX_WPROF
+  const unsigned long long w0 = clock64();
+#endif
   spmv_rows<4, 0>(S, par, SrcVec{P->xpool + static_cast<size_t>(R->xp_out) * n}, e, acc, gwarp_id(),
                   threadIdx.x & 31, stage, seq, head);
+#ifdef HX_WPROF
+  if (P->prof && (threadIdx.x & 31) == 0)
+    P->prof[gridDim.x * (16 + kWarps) + gwarp_id()] += clock64() - w0;
+#endif
   fold_long<4, 0>(S, par, seq, acc);
   block_to_slots<4, 0>(acc, region_ptr(P, kRegB + par), gridDim.x);
 }
@@ -1580,6 +1594,8 @@ using namespace hx;
 
 namespace {
 
+constexpr int kProfWords = 16 + 2 * kWarps;  // per CTA: phase timers + per-warp SpMV timers
+
 struct DevSched {
   int4* tasks = nullptr;
   int4* meta = nullptr;
@@ -1834,8 +1850,8 @@ int hx_create(int32_t device, hx_ctx** out) {
   HX_CUDA(nullptr, dalloc(&c->ctl, 1));
   HX_CUDA(nullptr, dalloc(&c->kparams, 1));
   if (const char* e = std::getenv("HX_PROFILE"); e && e[0] == '1') {
-    HX_CUDA(nullptr, dalloc(&c->prof, static_cast<size_t>(c->grid) * 16));
-    HX_CUDA(nullptr, cudaMemset(c->prof, 0, static_cast<size_t>(c->grid) * 16 * sizeof(unsigned long long)));
+    HX_CUDA(nullptr, dalloc(&c->prof, static_cast<size_t>(c->grid) * kProfWords));
+    HX_CUDA(nullptr, cudaMemset(c->prof, 0, static_cast<size_t>(c->grid) * kProfWords * sizeof(unsigned long long)));
   }
   HX_CUDA(nullptr, dalloc(&c->bar, 1));
   HX_CUDA(nullptr, dalloc(&c->epochs, kEpochCap));
@@ -2333,13 +2349,25 @@ int hx_kkt_current(hx_ctx* c, hplp_kkt_t* out) {
   return HPLP_OK;
 }
 
-// Phase timers (HX_PROFILE=1): out[grid * 8] accumulated ns per CTA:
-// 0 phase A, 1 barrier 1, 2 phase B, 3 barrier 2, 4 totals+controller, 5 iterations.
+// Phase timers (HX_PROFILE=1): out[grid * 16] accumulated SM cycles per CTA
+// (slots listed in hplp.py HX.phase_profile), then -- in an HX_WPROF build
+// only -- per-warp SpMV cycles of phase A [grid * kWarps] and phase B.
+int hx_sched_tasks(hx_ctx* c, int32_t which, int32_t* out, int64_t capacity, int64_t* count) {
+  if (!c->uploaded) return set_err(c, HPLP_ESTATE, "hx_sched_tasks: no problem uploaded");
+  const DevSched& d = which == 0 ? c->sa : c->st;
+  const int64_t nt = d.view.n_tasks;
+  if (count) *count = nt;
+  if (out && capacity > 0)
+    HX_CUDA(c, cudaMemcpy(out, d.tasks, static_cast<size_t>(std::min(capacity, nt)) * sizeof(int4),
+                          cudaMemcpyDeviceToHost));
+  return HPLP_OK;
+}
+
 int hx_profile(hx_ctx* c, unsigned long long* out, int32_t reset) {
   if (!c->prof) return set_err(c, HPLP_ESTATE, "hx_profile: set HX_PROFILE=1 before hx_create");
-  HX_CUDA(c, cudaMemcpy(out, c->prof, static_cast<size_t>(c->grid) * 16 * sizeof(unsigned long long),
-                        cudaMemcpyDeviceToHost));
-  if (reset) HX_CUDA(c, cudaMemset(c->prof, 0, static_cast<size_t>(c->grid) * 16 * sizeof(unsigned long long)));
+  const size_t words = static_cast<size_t>(c->grid) * kProfWords;
+  HX_CUDA(c, cudaMemcpy(out, c->prof, words * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  if (reset) HX_CUDA(c, cudaMemset(c->prof, 0, words * sizeof(unsigned long long)));
   return HPLP_OK;
 }
 

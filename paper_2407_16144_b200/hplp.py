@@ -94,6 +94,7 @@ def lib() -> C.CDLL:
     sig("hx_kkt_current", C.c_int, V, C.POINTER(abi.Kkt))
     sig("hx_sizeof", I64, I32)
     sig("hx_profile", C.c_int, V, C.POINTER(C.c_uint64), I32)
+    sig("hx_sched_tasks", C.c_int, V, I32, C.POINTER(C.c_int32), I64, C.POINTER(C.c_int64))
     sig("hx_precondition", C.c_int, V, I32, D, PD, PD)
     sig("hx_download_problem", C.c_int, V, PI64, PI32, PD, PD, PD)
     _lib = L
@@ -387,9 +388,9 @@ class HX:
     def phase_profile(self, reset=True, sm_mhz=1965.0):
         """Per-CTA phase timers (HX_PROFILE=1, SM cycles): mean/max/min us per iteration."""
         g = self.info()["grid"]
-        buf = (C.c_uint64 * (g * 16))()
+        buf = (C.c_uint64 * (g * (16 + 2 * self.WARPS)))()
         self._c(lib().hx_profile(self.h, buf, int(reset)))
-        a = np.array(buf[:], dtype=np.float64).reshape(g, 16)
+        a = np.array(buf[: g * 16], dtype=np.float64).reshape(g, 16)
         its = max(a[0, 5], 1.0)
         # phase_A: the (speculative) phase A after warp 0's controller; controller:
         # warp 0's totals + logic (its split: ctl_totals / ctl_scalar);
@@ -399,6 +400,26 @@ class HX:
         k = 1.0 / its / sm_mhz  # cycles -> us per iteration
         return {nm: dict(mean_us=float(a[:, i].mean() * k), max_us=float(a[:, i].max() * k),
                          min_us=float(a[:, i].min() * k)) for nm, i in names.items()}
+
+    WARPS = 16  # warps per CTA (csrc/hx_internal.cuh kWarps)
+
+    def warp_profile(self, reset=True):
+        """Per-warp SpMV cycles of phases A and B (a -DHX_WPROF build with
+        HX_PROFILE=1), shape (2, grid * WARPS); plus the per-CTA counters."""
+        g = self.info()["grid"]
+        buf = (C.c_uint64 * (g * (16 + 2 * self.WARPS)))()
+        self._c(lib().hx_profile(self.h, buf, int(reset)))
+        a = np.array(buf[:], dtype=np.float64)
+        return a[g * 16:].reshape(2, g * self.WARPS), a[: g * 16].reshape(g, 16)
+
+    def sched_tasks(self, which):
+        """Warp task list (0: rows of A, 1: rows of A^T) as an (n_tasks, 4) int32 array."""
+        cnt = C.c_int64()
+        self._c(lib().hx_sched_tasks(self.h, which, None, 0, C.byref(cnt)))
+        out = np.empty((cnt.value, 4), np.int32)
+        self._c(lib().hx_sched_tasks(self.h, which, out.ctypes.data_as(C.POINTER(C.c_int32)), cnt.value,
+                                     C.byref(cnt)))
+        return out
 
     def kkt_current(self):
         k = abi.Kkt()
