@@ -44,9 +44,19 @@ int hplp_solve_csr(int32_t device, int64_t m, int64_t n, const int64_t* row_ptr,
 int hplp_solver_create(int32_t device, int64_t m, int64_t n, const int64_t* row_ptr,
                        const int32_t* col_idx, const double* val, const double* b, const double* c,
                        void** solver);
+/* The same LP row-partitioned across nranks contexts of this process (SURVEY.md
+ * §8e): rank r on devices[r % ndevices], nnz-balanced blocks from
+ * hplp_plan_partition, bound with hx_team_bind.  Ranks sharing a device are
+ * emulated as CTA groups of one launch (ctas_per_rank 0 = split evenly).
+ * hplp_solver_solve then runs the partitioned loop. */
+int hplp_solver_create_team(const int32_t* devices, int32_t ndevices, int32_t nranks, int32_t ctas_per_rank,
+                            int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const double* val,
+                            const double* b, const double* c, void** solver);
 int hplp_solver_solve(void* solver, const hplp_config_t* cfg, hplp_io_t* io, hplp_result_t* result);
 /* The underlying hx context (include/hx.h) for benchmarks and tests. */
 void* hplp_solver_hx(void* solver);
+/* hx context of rank `rank` of a team (rank 0 = hplp_solver_hx); NULL if none. */
+void* hplp_solver_rank_hx(void* solver, int32_t rank);
 void hplp_solver_free(void* solver);
 
 /* to_standard_form (inc/lp_model.hpp:126, src/lp_model.cpp:155-325): general

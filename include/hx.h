@@ -109,6 +109,44 @@ int hx_setup(hx_ctx* ctx, const hplp_config_t* cfg, double sigma_used, double et
 int hx_run(hx_ctx* ctx, int64_t max_iters, hx_progress_t* progress);
 int hx_progress(hx_ctx* ctx, hx_progress_t* progress);
 
+/* ---- Multi-GPU row partition (north star "A is
+ * row-partitioned across the 8 GPUs of a single box") ------------------------
+ * A team of nranks contexts solves ONE LP: rank r owns rows [row0,row1) of A
+ * (y, A x, b) and columns [col0,col1) (x, c) -- hplp_plan_partition gives
+ * nnz-balanced blocks.  Each rank's loop kernel runs its blocks and pushes
+ * every owned slice a peer gathers (x+, y+, the Halpern y combo, certificate
+ * vectors) and its partial-sum records straight into the peers' device
+ * memory (NVLink P2P stores), with a two-level cross-rank barrier; every rank
+ * reduces all records in one fixed order, so the replicated controllers take
+ * bit-identical decisions.  The reference has no counterpart (its solve() is
+ * single-threaded); results equal the single-GPU solve within
+ * reduction-order rounding.
+ *
+ * hx_set_partition  before hx_upload_csr (which still takes the FULL problem:
+ *                   setup, power iteration and the boundary SpMVs run whole on
+ *                   every rank, deterministically identical).  ctas = CTAs of
+ *                   this rank (0 = one per SM; emulation splits one device).
+ * hx_team_bind      ranks living in one process: on one device the team is
+ *                   emulated as CTA groups of one cooperative launch (the way
+ *                   to exercise the protocol with one GPU); on several devices
+ *                   peer access is enabled and each device runs its rank.
+ *                   Then hx_team_run drives all of them.
+ * hx_team_export /  one process per GPU: each rank exports CUDA IPC handles of
+ * hx_team_import    its shared buffers, the blobs are exchanged by the caller
+ *                   (torch.distributed all_gather_object in bench.py) and every
+ *                   rank imports all blobs; then each rank calls hx_run, all
+ *                   ranks concurrently (the barrier's 10 s watchdog turns a
+ *                   missing rank into HPLP_ETIMEOUT).
+ * Iterates and certificates read back from any rank are assembled from the
+ * peers' blocks. */
+int hx_set_partition(hx_ctx* ctx, int32_t nranks, int32_t rank, int64_t row0, int64_t row1, int64_t col0,
+                     int64_t col1, int32_t ctas);
+int hx_team_bind(hx_ctx** ctxs, int32_t count);
+int hx_team_export(hx_ctx* ctx, void* blob, int64_t capacity, int64_t* size);
+int hx_team_import(hx_ctx* ctx, const void* blob, int64_t size);
+/* progress: count entries (one per ctxs[i]) or NULL. */
+int hx_team_run(hx_ctx** ctxs, int32_t count, int64_t max_iters, hx_progress_t* progress);
+
 /* Epoch log (EpochStats, inc/solver.hpp:82-87) entries [first, first+count). */
 int hx_epochs(hx_ctx* ctx, int64_t first, int64_t count, hplp_epoch_t* out);
 

@@ -141,6 +141,18 @@ int hplp_solver_create(int32_t device, int64_t m, int64_t n, const int64_t* row_
   });
 }
 
+int hplp_solver_create_team(const int32_t* devices, int32_t ndevices, int32_t nranks, int32_t ctas_per_rank,
+                            int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const double* val,
+                            const double* b, const double* c, void** solver) {
+  return guarded([&] {
+    if (!devices || ndevices < 1) throw std::invalid_argument("hplp_solver_create_team: no devices");
+    hplp_gpu::SparseMatrix a = hplp_gpu::SparseMatrix::from_csr(m, n, row_ptr, col_idx, val);
+    std::vector<int> devs(devices, devices + ndevices);
+    *solver = new hplp_gpu::Solver(devs, nranks, m, n, a.row_ptr().data(), a.col_idx().data(), a.values().data(), b, c,
+                                   ctas_per_rank);
+  });
+}
+
 int hplp_solver_solve(void* solver, const hplp_config_t* cfg, hplp_io_t* io, hplp_result_t* result) {
   return guarded([&] {
     auto* s = static_cast<hplp_gpu::Solver*>(solver);
@@ -150,6 +162,8 @@ int hplp_solver_solve(void* solver, const hplp_config_t* cfg, hplp_io_t* io, hpl
 }
 
 void* hplp_solver_hx(void* solver) { return static_cast<hplp_gpu::Solver*>(solver)->hx(); }
+
+void* hplp_solver_rank_hx(void* solver, int32_t rank) { return static_cast<hplp_gpu::Solver*>(solver)->rank_hx(rank); }
 
 void hplp_solver_free(void* solver) { delete static_cast<hplp_gpu::Solver*>(solver); }
 

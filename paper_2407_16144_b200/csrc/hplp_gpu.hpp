@@ -260,16 +260,28 @@ class Solver {
   Solver(const StandardFormLP& lp, int device = 0);
   Solver(int device, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const double* val,
          const double* b, const double* c);
+  // Multi-GPU row partition: nranks contexts in this process,
+  // rank r on devices[r % devices.size()], blocks from hplp_plan_partition.
+  // Ranks sharing one device are emulated as CTA groups of one launch
+  // (ctas_per_rank = 0 splits the device evenly).
+  Solver(const std::vector<int>& devices, int nranks, int64_t m, int64_t n, const int64_t* row_ptr,
+         const int32_t* col_idx, const double* val, const double* b, const double* c, int ctas_per_rank = 0);
   ~Solver();
   Solver(const Solver&) = delete;
   Solver& operator=(const Solver&) = delete;
   SolveResult solve(const SolverConfig& config);
   ::hx_ctx* hx() const { return ctx_; }
+  ::hx_ctx* rank_hx(int r) const {
+    return ranks_.empty() ? (r == 0 ? ctx_ : nullptr)
+                          : (r >= 0 && r < static_cast<int>(ranks_.size()) ? ranks_[r] : nullptr);
+  }
+  int nranks() const { return ranks_.empty() ? 1 : static_cast<int>(ranks_.size()); }
   int64_t rows() const { return m_; }
   int64_t cols() const { return n_; }
 
  private:
-  ::hx_ctx* ctx_ = nullptr;
+  ::hx_ctx* ctx_ = nullptr;          // the context (a team: rank 0)
+  std::vector<::hx_ctx*> ranks_;      // team in rank order; empty for one context
   int64_t m_ = 0, n_ = 0, nnz_ = 0;
   bool scaled_ = false;
   int ruiz_ = 0;

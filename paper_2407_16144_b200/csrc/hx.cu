@@ -95,6 +95,7 @@ struct Ctl {
   long long pw_k, pw_max, pw_iters;
   double pw_tol, pw_sigma, pw_sigma_prev, pw_sigma_cur;
   int pw_converged, pw_redraw;
+  unsigned long long team_epochs;  // cross-rank barriers passed so far (identical on every rank)
 };
 static_assert(sizeof(Ctl) % 8 == 0, "Ctl copied as 8-byte words");
 
@@ -103,6 +104,38 @@ struct GridBar {
   unsigned abort;            // watchdog fired
   unsigned time_up[2];       // time-limit flag, by iteration parity (CTA 0 writes)
   unsigned pad;
+  unsigned long long go;     // team barrier: last cross-rank epoch released to this rank's CTAs
+};
+
+// Cross-rank barrier word of one rank of a row-partitioned team, on its own
+// 128-byte line.  `arrive` counts the arrivals of every rank's leader CTA and
+// is monotonic for the context's lifetime (never reset between launches, so a
+// fast peer can arrive before this rank's next launch starts); time_up is the
+// time-limit flag, written by rank 0 alone so every rank stops together.
+struct RankBar {
+  unsigned long long arrive;
+  unsigned time_up[2];
+  unsigned long long pad[14];
+};
+
+// Row partition of the team plus the peers' buffers.  Rank r
+// owns rows [row0, row1) of A (y, A x, b) and columns [col0, col1) (x, c);
+// iterate pools are full length on every rank and every owned slice that a
+// peer gathers from (x+, the two y candidates, certificate unit vectors) is
+// pushed into the peers' pools by the epilogue that produces it: P2P stores
+// over NVLink (CUDA IPC mappings) on a multi-GPU node, or plain stores when
+// the ranks are emulated as CTA groups of one launch on one device.
+// Per-CTA partial records go to every rank's slot regions the same way, so
+// each rank reduces all ranks' records locally in one fixed order and the
+// replicated controllers stay bit-identical across ranks.
+struct Team {
+  int rank, nranks, grp_ctas, pad;
+  int row0, row1, col0, col1;
+  double* px[kMaxRanks];    // xpool of every rank (px[rank] = own)
+  double* py[kMaxRanks];    // ypool
+  double* pu[kMaxRanks];    // upool
+  double* ps[kMaxRanks];    // slots
+  RankBar* pb[kMaxRanks];   // cross-rank barrier words
 };
 
 // Slot regions (kMaxQ * grid doubles each).  A CTA may still be reading the
@@ -126,6 +159,14 @@ struct KParams {
   GridBar* bar;
   hplp_epoch_t* epochs;  // ring of kEpochCap
   unsigned long long* prof;  // optional per-CTA phase timers [grid][8] (HX_PROFILE=1)
+  Team T;                    // row partition + peers (loop_kernel_team only)
+};
+
+// Where this CTA sits: its index among the CTAs of its rank (cta of nctas)
+// and its partial record among all ranks' records (rec of nrec).  Single GPU:
+// cta = rec = blockIdx.x, nctas = nrec = gridDim.x.
+struct Geo {
+  int cta, nctas, rec, nrec;
 };
 
 // ---------------------------------------------------------------------------
@@ -190,7 +231,8 @@ __device__ __forceinline__ size_t region_stride(int grid) {
   return static_cast<size_t>(kReplicas) * grid * kMaxQ;
 }
 
-// Per-thread accumulators -> this CTA's record in every replica (fixed order).
+// Per-thread accumulators -> this CTA's record in every replica (fixed order);
+// standalone kernels (record blockIdx.x of gridDim.x).
 template <int Q, unsigned MaxMask>
 __device__ void block_to_slots(const double (&acc)[Q], double* region, int grid) {
   double (*red)[kMaxQ] = red_buf();
@@ -207,6 +249,34 @@ __device__ void block_to_slots(const double (&acc)[Q], double* region, int grid)
     double v = red[0][q];
     for (int w = 1; w < kWarps; ++w) v = mx ? dmax(v, red[w][q]) : v + red[w][q];
     region[(static_cast<size_t>(k) * grid + blockIdx.x) * kMaxQ + q] = v;
+  }
+}
+
+// Loop-kernel version: record g.rec of g.nrec in slot region `region`; a
+// ranked CTA writes it into every rank's slots (own included), so all ranks
+// hold all records.
+template <int Q, unsigned MaxMask, bool RK, class KP>
+__device__ void block_to_slots(const double (&acc)[Q], const KP* P, int region, const Geo& g) {
+  double (*red)[kMaxQ] = red_buf();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const double v = ((MaxMask >> q) & 1u) ? warp_max(acc[q]) : warp_sum(acc[q]);
+    if (lane == 0) red[warp][q] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < Q * kReplicas) {
+    const int q = threadIdx.x % Q, k = threadIdx.x / Q;
+    const bool mx = (MaxMask >> q) & 1u;
+    double v = red[0][q];
+    for (int w = 1; w < kWarps; ++w) v = mx ? dmax(v, red[w][q]) : v + red[w][q];
+    const size_t off = static_cast<size_t>(region) * region_stride(g.nrec) +
+                       (static_cast<size_t>(k) * g.nrec + g.rec) * kMaxQ + q;
+    if constexpr (RK) {
+      for (int r = 0; r < P->T.nranks; ++r) P->T.ps[r][off] = v;
+    } else {
+      P->slots[off] = v;
+    }
   }
 }
 
@@ -233,13 +303,13 @@ __device__ __forceinline__ double (*part_buf())[kJ][kMaxQ] {
 }
 
 template <class Desc>
-__device__ void block_totals(int Q, const Desc& desc, double* tot) {
+__device__ void block_totals(int Q, const Desc& desc, double* tot, const Geo& g) {
   double (*part)[kJ][kMaxQ] = part_buf();
   const int q = threadIdx.x % kMaxQ, j = threadIdx.x / kMaxQ;
-  const int G = gridDim.x;
+  const int G = g.nrec;
   if (q < Q) {
     const QSrc d = desc(q);
-    const double* rec = d.region + static_cast<size_t>(blockIdx.x % kReplicas) * G * kMaxQ;
+    const double* rec = d.region + static_cast<size_t>(g.cta % kReplicas) * G * kMaxQ;
     double v = d.mx ? -INFINITY : 0.0, l = v;
     for (int c = j; c < G; c += kJ) {
       const double x = ldcg(rec + static_cast<size_t>(c) * kMaxQ + d.rq);
@@ -323,7 +393,7 @@ struct SpmvHead {
 };
 
 __device__ __forceinline__ void spmv_head(const Sched& S, int gwarp, int lane, SpmvHead& h) {
-  const int W = gridDim.x * kWarps;
+  const int W = S.W;
   const int n = S.n_tasks;
   const int4 kNone{0, 0, 0, 0};
   h.tk = gwarp < n ? __ldg(S.tasks + gwarp) : kNone;
@@ -335,7 +405,7 @@ template <int Q, unsigned MaxMask, class Src, class Epi>
 __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& src, Epi& epi, double (&acc)[Q],
                                           int gwarp, int lane, WarpStage* st, unsigned long long seq,
                                           const SpmvHead& head) {
-  const int W = gridDim.x * kWarps;
+  const int W = S.W;
   const int n = S.n_tasks;
   const int4 kNone{0, 0, 0, 0};
   int t = gwarp;
@@ -453,10 +523,11 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
 // of this phase (flag == seq) and folds its terms, in list order, into
 // lane 0's accumulators -- a fixed order, so totals stay bit-reproducible.
 template <int Q, unsigned MaxMask>
-__device__ __forceinline__ void fold_long(const Sched& S, int set, unsigned long long seq, double (&acc)[Q]) {
+__device__ __forceinline__ void fold_long(const Sched& S, int set, unsigned long long seq, double (&acc)[Q],
+                                          int cta) {
   if (S.n_long == 0 || threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
-  const int b = __ldg(S.owned_ptr + blockIdx.x), e = __ldg(S.owned_ptr + blockIdx.x + 1);
+  const int b = __ldg(S.owned_ptr + cta), e = __ldg(S.owned_ptr + cta + 1);
   double part[Q];
   acc_init<Q, MaxMask>(part);
   const unsigned long long* flags = S.long_flag(set);
@@ -496,6 +567,14 @@ struct SrcDiv {  // power iteration: x = z / ||z|| formed on the fly (same round
 // ---- epilogues -------------------------------------------------------------
 struct NoIn {};
 
+// Ranked epilogues push each owned element a peer gathers into every other
+// rank's pool at the same offset (P2P stores on a multi-GPU node).
+__device__ __forceinline__ void push_peers(const Team* T, double* const* base, size_t off, double v) {
+  for (int r = 0; r < T->nranks; ++r)
+    if (r != T->rank) base[r][off] = v;
+}
+
+template <bool RK>
 struct EpiPrimal {  // phase A, rows of A^T
   const double* xs;
   const double* xa;
@@ -504,6 +583,8 @@ struct EpiPrimal {  // phase A, rows of A^T
   double* xp;
   double w, eta;
   int mode;
+  const Team* T;   // RK: peers of the x+ push
+  size_t xp_off;   // offset of x+ in the x pools
   struct In {
     double xs, xa, c;
   };
@@ -523,6 +604,7 @@ struct EpiPrimal {  // phase A, rows of A^T
     double xn = x - eta * (aty + cj);
     xn = xn < 0.0 ? 0.0 : xn;
     xp[j] = xn;
+    if constexpr (RK) push_peers(T, T->px, xp_off + j, xn);
     double rc = -(cj + aty);
     rc = rc < 0.0 ? 0.0 : rc;
     const double dx = x - xn;
@@ -532,6 +614,7 @@ struct EpiPrimal {  // phase A, rows of A^T
   }
 };
 
+template <bool RK>
 struct EpiDual {  // phase B, rows of A
   const double* y;
   const double* ax;
@@ -543,6 +626,8 @@ struct EpiDual {  // phase B, rows of A
   double* yc;
   double* axc;
   double eta, w;
+  const Team* T;          // RK: peers of the y+ / combo push
+  size_t yp_off, yc_off;  // offsets of y+ and the combo in the y pools
   struct In {
     double y, ax, b, ya, axa;
   };
@@ -557,7 +642,12 @@ struct EpiDual {  // phase B, rows of A
     yp[i] = ypi;
     axp[i] = s;
     const double omw = 1.0 - w;
-    yc[i] = omw * ypi + w * in.ya;
+    const double yci = omw * ypi + w * in.ya;
+    yc[i] = yci;
+    if constexpr (RK) {
+      push_peers(T, T->py, yp_off + i, ypi);
+      push_peers(T, T->py, yc_off + i, yci);
+    }
     axc[i] = omw * s + w * in.axa;
     const double d = axi - bi;
     const double dy = yi - ypi;
@@ -637,6 +727,75 @@ __device__ bool grid_sync(GridBar* bar, unsigned long long& target) {
           break;
         }
       }
+    }
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Team barrier (row-partitioned ranks), two levels:
+//  1. every CTA of this rank arrives on the rank's local counter with a
+//     system-scope release, which orders its P2P stores into peers' memory
+//     (x+ / y slices, partial records) before the arrival;
+//  2. the rank's leader (CTA 0) waits for all local CTAs, then bumps the
+//     monotonic `arrive` word of every rank (system-scope release, one P2P
+//     atomic per peer), waits until its own word shows all ranks' leaders for
+//     this epoch, and releases its CTAs through `go`.
+// Causality is transitive along peer CTA -> peer leader -> this leader ->
+// this CTA, so after the barrier every slice a peer pushed is visible here,
+// and the acquire spins invalidate L1 as in grid_sync.  `repoch` (cross-rank
+// barriers passed) continues across launches and is identical on all ranks.
+// Each spin has the same 10 s watchdog; a rank whose peer died stops with
+// HPLP_ETIMEOUT instead of hanging the GPU.
+__device__ bool team_sync(GridBar* bar, const Team& T, const Geo& g, unsigned long long& target,
+                          unsigned long long& repoch) {
+  __shared__ int s_ok;
+  __syncthreads();
+  target += g.nctas;
+  repoch += 1;
+  if (threadIdx.x == 0) {
+    s_ok = 1;
+    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(&bar->count), "l"(1ull) : "memory");
+    const unsigned long long t0 = global_ns();
+    unsigned spins = 0;
+    auto alive = [&]() -> bool {
+      if ((++spins & 255u) != 0u) return true;
+      if (*reinterpret_cast<volatile unsigned*>(&bar->abort)) return false;
+      if (global_ns() - t0 > 10000000000ull) {
+        atomicExch(&bar->abort, 1u);
+        return false;
+      }
+      return true;
+    };
+    if (g.cta == 0) {
+      while (ld_acquire_sys_u64(&bar->count) < target)
+        if (!alive()) {
+          s_ok = 0;
+          break;
+        }
+      if (s_ok) {
+        for (int r = 0; r < T.nranks; ++r)
+          asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(&T.pb[r]->arrive), "l"(1ull) : "memory");
+        const unsigned long long want = repoch * static_cast<unsigned long long>(T.nranks);
+        while (ld_acquire_sys_u64(&T.pb[T.rank]->arrive) < want)
+          if (!alive()) {
+            s_ok = 0;
+            break;
+          }
+      }
+      if (s_ok) asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&bar->go), "l"(repoch) : "memory");
+    } else {
+      while (ld_acquire_u64(&bar->go) < repoch)
+        if (!alive()) {
+          s_ok = 0;
+          break;
+        }
     }
   }
   __syncthreads();
@@ -960,47 +1119,51 @@ __device__ void ctl_store(const Ctl& s, Ctl* g) {
 // Phases.  Each is a separate (noinline) function so the register allocator
 // sees one SpMV instantiation at a time; KParams lives in global memory.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double* region_ptr(const KParams* P, int r) {
-  return P->slots + static_cast<size_t>(r) * region_stride(gridDim.x);
+__device__ __forceinline__ double* region_ptr(const KParams* P, int r, int nrec) {
+  return P->slots + static_cast<size_t>(r) * region_stride(nrec);
 }
 
-__device__ __forceinline__ int gwarp_id() { return blockIdx.x * kWarps + (threadIdx.x >> 5); }
+__device__ __forceinline__ int gwarp_id(const Geo& g) { return g.cta * kWarps + (threadIdx.x >> 5); }
 
 // phase A: A^T y, primal step (+ Halpern formation of x), primal partials
+template <bool RK>
 __device__ HX_PHASE_INLINE void phase_primal(const KParams* P, const Roles* R, int par, WarpStage* stage,
-                                             unsigned long long seq, const SpmvHead& head) {
+                                             unsigned long long seq, const SpmvHead& head, const Geo& g) {
   const int n = P->n, m = P->m;
   double acc[3];
   acc_init<3, 0>(acc);
-  EpiPrimal e{P->xpool + static_cast<size_t>(R->x_src) * n,
+  EpiPrimal<RK> e{P->xpool + static_cast<size_t>(R->x_src) * n,
               P->xpool + static_cast<size_t>(R->x_anchor) * n,
               P->c,
               P->xpool + static_cast<size_t>(R->zx_out) * n,
               P->xpool + static_cast<size_t>(R->xp_out) * n,
               R->w_x,
               R->eta,
-              R->x_mode};
+              R->x_mode,
+              &P->T,
+              static_cast<size_t>(R->xp_out) * n};
   const Sched S = P->AT;
 #ifdef HX_WPROF
   const unsigned long long w0 = clock64();
 #endif
-  spmv_rows<3, 0>(S, par, SrcVec{P->ypool + static_cast<size_t>(R->y_cur) * m}, e, acc, gwarp_id(),
+  spmv_rows<3, 0>(S, par, SrcVec{P->ypool + static_cast<size_t>(R->y_cur) * m}, e, acc, gwarp_id(g),
                   threadIdx.x & 31, stage, seq, head);
 #ifdef HX_WPROF
-  if (P->prof && (threadIdx.x & 31) == 0)
-    P->prof[gridDim.x * 16 + gwarp_id()] += clock64() - w0;
+  if constexpr (!RK)
+    if (P->prof && (threadIdx.x & 31) == 0) P->prof[gridDim.x * 16 + gwarp_id(g)] += clock64() - w0;
 #endif
-  fold_long<3, 0>(S, par, seq, acc);
-  block_to_slots<3, 0>(acc, region_ptr(P, kRegA + par), gridDim.x);
+  fold_long<3, 0>(S, par, seq, acc, g.cta);
+  block_to_slots<3, 0, RK>(acc, P, kRegA + par, g);
 }
 
 // phase B: A x+, dual step, speculative Halpern combos, dual partials
+template <bool RK>
 __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int par, WarpStage* stage,
-                                           unsigned long long seq, const SpmvHead& head) {
+                                           unsigned long long seq, const SpmvHead& head, const Geo& g) {
   const int n = P->n, m = P->m;
   double acc[4];
   acc_init<4, 0>(acc);
-  EpiDual e{P->ypool + static_cast<size_t>(R->y_cur) * m,
+  EpiDual<RK> e{P->ypool + static_cast<size_t>(R->y_cur) * m,
             P->axpool + static_cast<size_t>(R->ax_cur) * m,
             P->b,
             P->ypool + static_cast<size_t>(R->y_anchor) * m,
@@ -1010,19 +1173,22 @@ __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int
             P->ypool + static_cast<size_t>(R->yc_out) * m,
             P->axpool + static_cast<size_t>(R->axc_out) * m,
             R->eta,
-            R->w_next};
+            R->w_next,
+            &P->T,
+            static_cast<size_t>(R->yp_out) * m,
+            static_cast<size_t>(R->yc_out) * m};
   const Sched S = P->A;
 #ifdef HX_WPROF
   const unsigned long long w0 = clock64();
 #endif
-  spmv_rows<4, 0>(S, par, SrcVec{P->xpool + static_cast<size_t>(R->xp_out) * n}, e, acc, gwarp_id(),
+  spmv_rows<4, 0>(S, par, SrcVec{P->xpool + static_cast<size_t>(R->xp_out) * n}, e, acc, gwarp_id(g),
                   threadIdx.x & 31, stage, seq, head);
 #ifdef HX_WPROF
-  if (P->prof && (threadIdx.x & 31) == 0)
-    P->prof[gridDim.x * (16 + kWarps) + gwarp_id()] += clock64() - w0;
+  if constexpr (!RK)
+    if (P->prof && (threadIdx.x & 31) == 0) P->prof[gridDim.x * (16 + kWarps) + gwarp_id(g)] += clock64() - w0;
 #endif
-  fold_long<4, 0>(S, par, seq, acc);
-  block_to_slots<4, 0>(acc, region_ptr(P, kRegB + par), gridDim.x);
+  fold_long<4, 0>(S, par, seq, acc, g.cta);
+  block_to_slots<4, 0, RK>(acc, P, kRegB + par, g);
 }
 
 // Totals of phases A+B -> t[0..6], computed by warp 0 alone (the other warps
@@ -1030,11 +1196,11 @@ __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int
 // and a xor butterfly finishes -- commutative pairwise adds, so every lane of
 // every CTA holds bit-identical totals.
 constexpr int kTotRounds = 5;  // 160 records in one round of loads
-__device__ __forceinline__ void warp_totals_main(const KParams* P, int par, double (&t)[7]) {
-  const int lane = threadIdx.x & 31, G = gridDim.x;
-  const size_t rep = static_cast<size_t>(blockIdx.x % kReplicas) * G * kMaxQ;
-  const double* ra = region_ptr(P, kRegA + par) + rep;
-  const double* rb = region_ptr(P, kRegB + par) + rep;
+__device__ __forceinline__ void warp_totals_main(const KParams* P, int par, double (&t)[7], const Geo& g) {
+  const int lane = threadIdx.x & 31, G = g.nrec;
+  const size_t rep = static_cast<size_t>(g.cta % kReplicas) * G * kMaxQ;
+  const double* ra = region_ptr(P, kRegA + par, G) + rep;
+  const double* rb = region_ptr(P, kRegB + par, G) + rep;
 #pragma unroll
   for (int q = 0; q < 7; ++q) t[q] = 0.0;
   for (int base = 0; base < G; base += 32 * kTotRounds) {
@@ -1060,31 +1226,47 @@ __device__ __forceinline__ void warp_totals_main(const KParams* P, int par, doub
 }
 
 // power iteration halves: w = A x (x = x0 or z / zn), z = A^T w
-__device__ HX_PHASE_INLINE void power_a(const KParams* P, const Roles* R, WarpStage* stage, unsigned long long seq) {
+// (single-rank only: a team computes sigma redundantly on every rank, each
+// with its full-matrix schedules -- deterministic and identical, no exchange)
+__device__ HX_PHASE_INLINE void power_a(const KParams* P, const Roles* R, WarpStage* stage, unsigned long long seq,
+                                        const Geo& g) {
   double acc[1];
   acc_init<1, 0>(acc);
   EpiStoreSq e{P->ypool};
   const Sched S = P->A;
-  if (R->pw_mode == 0) spmv_rows<1, 0>(S, 0, SrcVec{P->xpool}, e, acc, gwarp_id(), threadIdx.x & 31, stage, seq);
-  else spmv_rows<1, 0>(S, 0, SrcDiv{P->xpool + P->n, R->pw_zn}, e, acc, gwarp_id(), threadIdx.x & 31, stage, seq);
-  fold_long<1, 0>(S, 0, seq, acc);
-  block_to_slots<1, 0>(acc, region_ptr(P, kRegPA), gridDim.x);
+  if (R->pw_mode == 0) spmv_rows<1, 0>(S, 0, SrcVec{P->xpool}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
+  else spmv_rows<1, 0>(S, 0, SrcDiv{P->xpool + P->n, R->pw_zn}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
+  fold_long<1, 0>(S, 0, seq, acc, g.cta);
+  block_to_slots<1, 0, false>(acc, P, kRegPA, g);
 }
 
-__device__ HX_PHASE_INLINE void power_b(const KParams* P, WarpStage* stage, unsigned long long seq) {
+__device__ HX_PHASE_INLINE void power_b(const KParams* P, WarpStage* stage, unsigned long long seq, const Geo& g) {
   double acc[1];
   acc_init<1, 0>(acc);
   EpiStoreSq e{P->xpool + P->n};
   const Sched S = P->AT;
-  spmv_rows<1, 0>(S, 0, SrcVec{P->ypool}, e, acc, gwarp_id(), threadIdx.x & 31, stage, seq);
-  fold_long<1, 0>(S, 0, seq, acc);
-  block_to_slots<1, 0>(acc, region_ptr(P, kRegPB), gridDim.x);
+  spmv_rows<1, 0>(S, 0, SrcVec{P->ypool}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
+  fold_long<1, 0>(S, 0, seq, acc, g.cta);
+  block_to_slots<1, 0, false>(acc, P, kRegPB, g);
 }
 
 // certificate scan C1: candidate norms and finiteness
-__device__ HX_PHASE_INLINE void cert_norms(const KParams* P, const Roles* R) {
+// Element ranges a CTA sweeps: the owned column / row blocks of its rank.
+template <bool RK>
+__device__ __forceinline__ void owned_ranges(const KParams* P, int& c0, int& c1, int& r0, int& r1) {
+  if constexpr (RK) {
+    c0 = P->T.col0, c1 = P->T.col1, r0 = P->T.row0, r1 = P->T.row1;
+  } else {
+    c0 = 0, c1 = P->n, r0 = 0, r1 = P->m;
+  }
+}
+
+template <bool RK>
+__device__ HX_PHASE_INLINE void cert_norms(const KParams* P, const Roles* R, const Geo& g) {
   const int n = P->n, m = P->m;
-  const int gtid = blockIdx.x * kThreads + threadIdx.x, gs = gridDim.x * kThreads;
+  const int gtid = g.cta * kThreads + threadIdx.x, gs = g.nctas * kThreads;
+  int c0, c1, r0, r1;
+  owned_ranges<RK>(P, c0, c1, r0, r1);
   const double* zx = P->xpool + static_cast<size_t>(R->zx_out) * n;
   const double* xp = P->xpool + static_cast<size_t>(R->xp_out) * n;
   const double* xa = P->xpool + static_cast<size_t>(R->x_anchor) * n;
@@ -1094,7 +1276,7 @@ __device__ HX_PHASE_INLINE void cert_norms(const KParams* P, const Roles* R) {
   double acc[8];
   acc_init<8, 0>(acc);
   const double s = R->cand_scale;
-  for (int j = gtid; j < n; j += gs) {
+  for (int j = c0 + gtid; j < c1; j += gs) {
     const double x = ldcg(zx + j);
     const double vd = ldcg(xp + j) - x;
     const double vn = s * (x - ldcg(xa + j));
@@ -1103,7 +1285,7 @@ __device__ HX_PHASE_INLINE void cert_norms(const KParams* P, const Roles* R) {
     acc[4] += isfinite(vd) ? 0.0 : 1.0;
     acc[6] += isfinite(vn) ? 0.0 : 1.0;
   }
-  for (int i = gtid; i < m; i += gs) {
+  for (int i = r0 + gtid; i < r1; i += gs) {
     const double y = ldcg(yc + i);
     const double vd = ldcg(yp + i) - y;
     const double vn = s * (y - ldcg(ya + i));
@@ -1112,13 +1294,22 @@ __device__ HX_PHASE_INLINE void cert_norms(const KParams* P, const Roles* R) {
     acc[5] += isfinite(vd) ? 0.0 : 1.0;
     acc[7] += isfinite(vn) ? 0.0 : 1.0;
   }
-  block_to_slots<8, 0>(acc, region_ptr(P, kRegC1), gridDim.x);
+  block_to_slots<8, 0, RK>(acc, P, kRegC1, g);
 }
 
 // certificate scan C2: unit vectors u = v / ||v|| and their reductions
-__device__ HX_PHASE_INLINE void cert_units(const KParams* P, const Roles* R) {
+template <bool RK>
+__device__ HX_PHASE_INLINE void cert_units(const KParams* P, const Roles* R, const Geo& g) {
   const int n = P->n, m = P->m;
-  const int gtid = blockIdx.x * kThreads + threadIdx.x, gs = gridDim.x * kThreads;
+  const int gtid = g.cta * kThreads + threadIdx.x, gs = g.nctas * kThreads;
+  int c0, c1, r0, r1;
+  owned_ranges<RK>(P, c0, c1, r0, r1);
+  // u vectors are SpMV gather sources of the validation products: a ranked
+  // CTA pushes its owned slices to the peers (same upool offsets)
+  auto put = [&](double* base, size_t off, double v) {
+    base[off] = v;
+    if constexpr (RK) push_peers(&P->T, P->T.pu, off, v);
+  };
   const double* zx = P->xpool + static_cast<size_t>(R->zx_out) * n;
   const double* xp = P->xpool + static_cast<size_t>(R->xp_out) * n;
   const double* xa = P->xpool + static_cast<size_t>(R->x_anchor) * n;
@@ -1128,16 +1319,12 @@ __device__ HX_PHASE_INLINE void cert_units(const KParams* P, const Roles* R) {
   double acc[12];
   acc_init<12, 0x577u>(acc);
   const double s = R->cand_scale;
-  double* u0 = P->upool;
-  double* u2 = P->upool + n;
-  double* u1 = P->upool + 2 * static_cast<size_t>(n);
-  double* u3 = u1 + m;
-  for (int j = gtid; j < n; j += gs) {
+  for (int j = c0 + gtid; j < c1; j += gs) {
     const double x = ldcg(zx + j);
     const double cj = __ldg(P->c + j);
     if (R->cand_on[0]) {
       const double u = (ldcg(xp + j) - x) / R->cn2[0];
-      u0[j] = u;
+      put(P->upool, static_cast<size_t>(j), u);
       acc[0] = dmax(acc[0], fabs(u));
       acc[1] = dmax(acc[1], u);
       acc[2] = dmax(acc[2], -u);
@@ -1145,35 +1332,36 @@ __device__ HX_PHASE_INLINE void cert_units(const KParams* P, const Roles* R) {
     }
     if (R->cand_on[2]) {
       const double u = (s * (x - ldcg(xa + j))) / R->cn2[2];
-      u2[j] = u;
+      put(P->upool, static_cast<size_t>(n) + j, u);
       acc[4] = dmax(acc[4], fabs(u));
       acc[5] = dmax(acc[5], u);
       acc[6] = dmax(acc[6], -u);
       acc[7] += cj * u;
     }
   }
-  for (int i = gtid; i < m; i += gs) {
+  for (int i = r0 + gtid; i < r1; i += gs) {
     const double y = ldcg(yc + i);
     const double bi = __ldg(P->b + i);
     if (R->cand_on[1]) {
       const double u = (ldcg(yp + i) - y) / R->cn2[1];
-      u1[i] = u;
+      put(P->upool, 2 * static_cast<size_t>(n) + i, u);
       acc[8] = dmax(acc[8], fabs(u));
       acc[9] += bi * u;
     }
     if (R->cand_on[3]) {
       const double u = (s * (y - ldcg(ya + i))) / R->cn2[3];
-      u3[i] = u;
+      put(P->upool, 2 * static_cast<size_t>(n) + m + i, u);
       acc[10] = dmax(acc[10], fabs(u));
       acc[11] += bi * u;
     }
   }
-  block_to_slots<12, 0x577u>(acc, region_ptr(P, kRegC2), gridDim.x);
+  block_to_slots<12, 0x577u, RK>(acc, P, kRegC2, g);
 }
 
 // certificate scan C3: the validation SpMVs, up to four independent products
+template <bool RK>
 __device__ HX_PHASE_INLINE void cert_products(const KParams* P, const Roles* R, WarpStage* stage,
-                                              unsigned long long seq) {
+                                              unsigned long long seq, const Geo& g) {
   const int n = P->n, m = P->m;
   double acc[6];
   acc_init<6, 0x3Fu>(acc);
@@ -1181,7 +1369,7 @@ __device__ HX_PHASE_INLINE void cert_products(const KParams* P, const Roles* R, 
   const double* u2 = P->upool + n;
   const double* u1 = P->upool + 2 * static_cast<size_t>(n);
   const double* u3 = u1 + m;
-  const int gw = gwarp_id(), lane = threadIdx.x & 31;
+  const int gw = gwarp_id(g), lane = threadIdx.x & 31;
   const Sched AT = P->AT;
   const Sched A = P->A;
   for (int k = 0; k < 2; ++k) {
@@ -1190,7 +1378,7 @@ __device__ HX_PHASE_INLINE void cert_products(const KParams* P, const Roles* R, 
       acc_init<2, 3u>(a2);
       EpiPosNeg e;
       spmv_rows<2, 3u>(AT, 2 + k, SrcVec{k ? u3 : u1}, e, a2, gw, lane, stage, seq);
-      fold_long<2, 3u>(AT, 2 + k, seq, a2);
+      fold_long<2, 3u>(AT, 2 + k, seq, a2, g.cta);
       acc[2 * k] = a2[0], acc[2 * k + 1] = a2[1];
     }
     if (R->cand_on[2 * k]) {
@@ -1198,26 +1386,27 @@ __device__ HX_PHASE_INLINE void cert_products(const KParams* P, const Roles* R, 
       acc_init<1, 1u>(a1);
       EpiAbs e;
       spmv_rows<1, 1u>(A, 2 + k, SrcVec{k ? u2 : u0}, e, a1, gw, lane, stage, seq);
-      fold_long<1, 1u>(A, 2 + k, seq, a1);
+      fold_long<1, 1u>(A, 2 + k, seq, a1, g.cta);
       acc[4 + k] = a1[0];
     }
   }
-  block_to_slots<6, 0x3Fu>(acc, region_ptr(P, kRegC3), gridDim.x);
+  block_to_slots<6, 0x3Fu, RK>(acc, P, kRegC3, g);
 }
 
 // ---------------------------------------------------------------------------
 // The persistent loop kernel.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid_constant__ KParams KP) {
-  const KParams* P = &KP;  // constant bank; no local copy (grid_constant)
+// RK = false: one GPU, P in the constant bank (loop_kernel).  RK = true: one
+// rank of a row-partitioned team (loop_kernel_team), P in shared memory.
+template <bool RK>
+__device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
   __shared__ Ctl C;
   __shared__ double tot[kMaxQ];
   __shared__ int s_time_up;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
-  const int G = gridDim.x;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const bool writer = blockIdx.x == 0;
+  const bool writer = g.cta == 0;
   WarpStage* stage = reinterpret_cast<WarpStage*>(dyn_smem) + warp;
   const unsigned long long t_start = global_ns();
   ctl_load(P->ctl, C);
@@ -1226,15 +1415,33 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
   GridBar* bar = P->bar;
   unsigned long long target = 0;
   unsigned long long seq = 1;  // phase sequence number (long-row flags; reset per launch)
+  unsigned long long repoch = C.team_epochs;  // team barriers passed (continues across launches)
+  auto sync = [&]() -> bool {
+    if constexpr (RK) return team_sync(bar, P->T, g, target, repoch);
+    else return grid_sync(bar, target);
+  };
+  // time-limit flag: decided by rank 0 alone so every rank stops together
+  auto set_time_up = [&](int pr, unsigned v) {
+    if constexpr (RK) {
+      if (P->T.rank == 0)
+        for (int r = 0; r < P->T.nranks; ++r) *reinterpret_cast<volatile unsigned*>(&P->T.pb[r]->time_up[pr]) = v;
+    } else {
+      bar->time_up[pr] = v;
+    }
+  };
+  auto get_time_up = [&](int pr) -> unsigned {
+    if constexpr (RK) return *reinterpret_cast<volatile unsigned*>(&P->T.pb[P->T.rank]->time_up[pr]);
+    else return *reinterpret_cast<volatile unsigned*>(&bar->time_up[pr]);
+  };
 
-  if (C.mode == kModePower) {
+  if (!RK && C.mode == kModePower) {
     // power_iteration loop body, src/sparse_matrix.cpp:153-177
     while (!R->stop) {
-      power_a(P, R, stage, ++seq);
-      if (!grid_sync(bar, target)) return;
+      power_a(P, R, stage, ++seq, g);
+      if (!sync()) return;
       {
-        const double* rg = region_ptr(P, kRegPA);
-        block_totals(1, [&](int) { return QSrc{rg, 0, nullptr, 0, 0, false}; }, tot);
+        const double* rg = region_ptr(P, kRegPA, g.nrec);
+        block_totals(1, [&](int) { return QSrc{rg, 0, nullptr, 0, 0, false}; }, tot, g);
       }
       if (threadIdx.x == 0) {
         const double sigma = sqrt(tot[0]);
@@ -1247,11 +1454,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
       }
       __syncthreads();
       if (R->stop) break;
-      power_b(P, stage, ++seq);
-      if (!grid_sync(bar, target)) return;
+      power_b(P, stage, ++seq, g);
+      if (!sync()) return;
       {
-        const double* rg = region_ptr(P, kRegPB);
-        block_totals(1, [&](int) { return QSrc{rg, 0, nullptr, 0, 0, false}; }, tot + 1);
+        const double* rg = region_ptr(P, kRegPB, g.nrec);
+        block_totals(1, [&](int) { return QSrc{rg, 0, nullptr, 0, 0, false}; }, tot + 1, g);
       }
       if (threadIdx.x == 0) {
         const double sigma = C.pw_sigma_cur;
@@ -1279,7 +1486,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
     return;
   }
 
-  unsigned long long* prof = P->prof ? P->prof + blockIdx.x * 16 : nullptr;
+  unsigned long long* prof = (!RK && P->prof) ? P->prof + blockIdx.x * 16 : nullptr;
   unsigned long long tp = clock64(), pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pacc2[3] = {0, 0, 0};
   auto mark = [&](int k) {  // SM cycles (clock64); the host converts with the SM clock
     if (prof && threadIdx.x == 0) {
@@ -1302,25 +1509,24 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
     const int par = static_cast<int>(C.it & 1);
     SpmvHead head;
     if (!spec_done) {
-      spmv_head(P->AT, gwarp_id(), lane, head);
-      phase_primal(P, R, par, stage, ++seq, head);
-      if (writer && threadIdx.x == 0 && budget != 0ull)
-        bar->time_up[par] = (global_ns() - t_start) > budget ? 1u : 0u;
+      spmv_head(P->AT, gwarp_id(g), lane, head);
+      phase_primal<RK>(P, R, par, stage, ++seq, head, g);
+      if (writer && threadIdx.x == 0 && budget != 0ull) set_time_up(par, (global_ns() - t_start) > budget ? 1u : 0u);
     }
     mark(0);
-    spmv_head(P->A, gwarp_id(), lane, head);
-    if (!grid_sync(bar, target)) return;
+    spmv_head(P->A, gwarp_id(g), lane, head);
+    if (!sync()) return;
     mark(1);
-    phase_dual(P, R, par, stage, ++seq, head);
+    phase_dual<RK>(P, R, par, stage, ++seq, head, g);
     if (threadIdx.x == 0) make_spec(C, SR);
     mark(2);
-    spmv_head(P->AT, gwarp_id(), lane, head);
-    if (!grid_sync(bar, target)) return;
+    spmv_head(P->AT, gwarp_id(g), lane, head);
+    if (!sync()) return;
     mark(3);
     if (warp == 0) {
       unsigned long long cA = clock64(), cB = 0, cC = 0;
       double t[7];
-      warp_totals_main(P, par, t);
+      warp_totals_main(P, par, t, g);
       // the independent fp64 divides / square roots, one per lane, executed
       // uniformly (operands selected per lane, one sqrt + one divide)
       double num = 1.0, den = 1.0;
@@ -1340,7 +1546,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
       if (lane == 0) {
 #pragma unroll
         for (int i = 0; i < 7; ++i) tot[i] = t[i];
-        s_time_up = budget != 0ull && *reinterpret_cast<volatile unsigned*>(&bar->time_up[par]) != 0u;
+        s_time_up = budget != 0ull && get_time_up(par) != 0u;
         C.w_k2 = pre[5];
         C.w_k3 = pre[6];
         main_logic(C, tot, pre, P->epochs, writer, s_time_up != 0);
@@ -1354,20 +1560,20 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
     }
     mark(4);
     // speculative phase A of iteration it+1
-    phase_primal(P, &SR, par ^ 1, stage, ++seq, head);
+    phase_primal<RK>(P, &SR, par ^ 1, stage, ++seq, head, g);
     if (writer && threadIdx.x == 0 && budget != 0ull)
-      bar->time_up[par ^ 1] = (global_ns() - t_start) > budget ? 1u : 0u;
+      set_time_up(par ^ 1, (global_ns() - t_start) > budget ? 1u : 0u);
     __syncthreads();
     mark(0);
     if (prof && threadIdx.x == 0) pacc[5] += 1;
 
     if (R->check) {
       // ---- certificate scan (src/solver.cpp:297-317) ----
-      cert_norms(P, R);
-      if (!grid_sync(bar, target)) return;
+      cert_norms<RK>(P, R, g);
+      if (!sync()) return;
       {
-        const double* rg = region_ptr(P, kRegC1);
-        block_totals(8, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, false}; }, tot);
+        const double* rg = region_ptr(P, kRegC1, g.nrec);
+        block_totals(8, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, false}; }, tot, g);
       }
       if (threadIdx.x == 0) {
         int any = 0;
@@ -1382,11 +1588,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
       }
       __syncthreads();
       if (R->check) {
-        cert_units(P, R);
-        if (!grid_sync(bar, target)) return;
+        cert_units<RK>(P, R, g);
+        if (!sync()) return;
         {
-          const double* rg = region_ptr(P, kRegC2);
-          block_totals(12, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, ((0x577u >> q) & 1u) != 0}; }, tot);
+          const double* rg = region_ptr(P, kRegC2, g.nrec);
+          block_totals(12, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, ((0x577u >> q) & 1u) != 0}; }, tot, g);
         }
         if (threadIdx.x == 0) {
           C.cinf[0] = tot[0], C.cmax_u[0] = tot[1], C.cmax_negu[0] = tot[2], C.cdot[0] = tot[3];
@@ -1395,11 +1601,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
           C.cinf[3] = tot[10], C.cdot[3] = tot[11];
         }
         __syncthreads();
-        cert_products(P, R, stage, ++seq);
-        if (!grid_sync(bar, target)) return;
+        cert_products<RK>(P, R, stage, ++seq, g);
+        if (!sync()) return;
         {
-          const double* rg = region_ptr(P, kRegC3);
-          block_totals(6, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, true}; }, tot);
+          const double* rg = region_ptr(P, kRegC3, g.nrec);
+          block_totals(6, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, true}; }, tot, g);
         }
         if (threadIdx.x == 0) {
           C.cmax_at[1] = tot[0], C.cmax_negat[1] = tot[1];
@@ -1414,7 +1620,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
     spec_done = same_phase_a(*R, SR);
     // a redo reuses this parity's long-row counters: wait until every CTA's
     // speculative phase A is complete
-    if (!spec_done && !grid_sync(bar, target)) return;
+    if (!spec_done && !sync()) return;
     mark(6);
   }
   if (prof && threadIdx.x == 0) {
@@ -1425,7 +1631,38 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     prof[6] = smid;
   }
+  if (threadIdx.x == 0) C.team_epochs = repoch;
   if (writer) ctl_store(C, P->ctl);
+}
+
+__global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid_constant__ KParams KP) {
+  // constant bank; no local copy (grid_constant)
+  const Geo g{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x),
+              static_cast<int>(gridDim.x)};
+  loop_body<false>(&KP, g);
+}
+
+static_assert(sizeof(KParams) % 8 == 0, "KParams copied as 8-byte words");
+
+// One launch runs every rank of `team` that lives on this device: CTAs
+// [r * grp_ctas, (r + 1) * grp_ctas) are rank team[r].T.rank.  On a
+// multi-GPU node each device launches its own rank (one group); on one
+// device a whole team is emulated as groups of one cooperative launch (their
+// CTAs wait on one another, so they must be co-resident -- never separate
+// launches).
+__global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_team(const KParams* __restrict__ team,
+                                                                         int grp_ctas) {
+  __shared__ KParams sP;
+  const int group = blockIdx.x / grp_ctas;
+  {
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(team + group);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&sP);
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(KParams) / 8); i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  const int cta = blockIdx.x % grp_ctas;
+  const Geo g{cta, grp_ctas, sP.T.rank * grp_ctas + cta, sP.T.nranks * grp_ctas};
+  loop_body<true>(&sP, g);
 }
 
 // ---------------------------------------------------------------------------
@@ -1645,6 +1882,19 @@ struct hx_ctx {
   Ctl h;  // host mirror
   double b_norm = 0, c_norm = 0;
   double time_limit_s = 0, loop_elapsed_s = 0;  // SolverConfig::time_limit_seconds budget of the loop
+  // Row-partitioned team (hx_set_partition / hx_team_*).  The
+  // context keeps the full problem (setup kernels, power iteration and the
+  // boundary SpMVs run on it unchanged -- every rank computes the same
+  // values); the loop kernel runs the partition schedules pa / pt.
+  bool ranked = false;
+  Team team{};                       // own range + every rank's buffers
+  int pcol0[kMaxRanks] = {}, pcol1[kMaxRanks] = {};  // every rank's column block (result assembly)
+  DevSched pa, pt;                   // rows [row0,row1) of A, [col0,col1) of A^T
+  RankBar* rbar = nullptr;
+  KParams* team_dev = nullptr;       // kMaxRanks launch parameter blocks
+  unsigned long long team_epochs = 0;
+  std::vector<hx_ctx*> local_team;   // ranks launched together (same device), rank order
+  std::vector<void*> ipc_open;       // peer mappings to close
 };
 
 namespace {
@@ -1685,14 +1935,25 @@ void free_problem(hx_ctx* c) {
   dfree(c->b), dfree(c->c), dfree(c->xpool), dfree(c->ypool), dfree(c->axpool), dfree(c->upool);
   free_sched(c->sa);
   free_sched(c->st);
+  free_sched(c->pa);
+  free_sched(c->pt);
   c->a_ptr = c->a_idx = c->t_ptr = c->t_idx = nullptr;
   c->a_val = c->t_val = c->b = c->c = c->xpool = c->ypool = c->axpool = c->upool = nullptr;
   c->uploaded = c->setup_done = false;
 }
 
+// Schedule of rows [row0, row0 + rows) of a CSR matrix (the whole matrix by
+// default; a rank's block in a team).  Task rows stay global indices.
 int upload_sched(hx_ctx* ctx, DevSched& d, const int* ptr_host, int rows, int cols, const int* dptr,
-                 const int* didx, const double* dval, double lead = 0.0) {
-  SchedHost h = build_schedule(ptr_host, rows, ctx->grid * kWarps, lead);
+                 const int* didx, const double* dval, double lead = 0.0, int row0 = 0) {
+  SchedHost h = build_schedule(ptr_host + row0, rows, ctx->grid * kWarps, lead);
+  if (row0)
+    for (int4& t : h.tasks)
+      if (t.x != t.y || t.z != t.w) {
+        const int kind = t.y >> kKindShift;
+        t.x += row0;
+        t.y = ((t.y & kRowMask) + row0) | (kind << kKindShift);
+      }
   HX_CUDA(ctx, dalloc(&d.tasks, h.tasks.size()));
   HX_CUDA(ctx, dalloc(&d.meta, h.meta.size()));
   HX_CUDA(ctx, dalloc(&d.part, 4 * static_cast<size_t>(h.n_slots)));
@@ -1714,6 +1975,7 @@ int upload_sched(hx_ctx* ctx, DevSched& d, const int* ptr_host, int rows, int co
   Sched& v = d.view;
   v.rows = rows;
   v.cols = cols;
+  v.W = ctx->grid * kWarps;
   v.ptr = dptr;
   v.idx = didx;
   v.val = dval;
@@ -1734,7 +1996,7 @@ int upload_sched(hx_ctx* ctx, DevSched& d, const int* ptr_host, int rows, int co
 }
 
 KParams params(hx_ctx* c) {
-  KParams P;
+  KParams P{};
   P.A = c->sa.view;
   P.AT = c->st.view;
   P.m = static_cast<int>(c->m);
@@ -1772,6 +2034,110 @@ int launch_loop(hx_ctx* c) {
   HX_CUDA(c, cudaGetLastError());
   if (gb.abort) {
     return set_err(c, HPLP_ETIMEOUT, "hx: grid barrier watchdog fired (device hang avoided)");
+  }
+  return HPLP_OK;
+}
+
+// ---- row-partitioned team ---------------------------------------------------
+// Launch parameters of one rank: its partition schedules plus the team.
+KParams team_params(hx_ctx* c) {
+  KParams P = params(c);
+  P.A = c->pa.view;
+  P.AT = c->pt.view;
+  P.prof = nullptr;
+  P.T = c->team;
+  return P;
+}
+
+// Issue one loop launch for the ranks of `ranks` that share a device (rank
+// order): a single cooperative launch of ranks.size() * grid CTAs on the
+// first rank's stream.  No host wait here (device-to-pageable copies block,
+// so they wait for team_complete): a process driving several devices issues
+// every device's launch before any rank can stall on a peer.
+int team_issue(const std::vector<hx_ctx*>& ranks, std::vector<KParams>& hp) {
+  hx_ctx* lead = ranks.front();
+  cudaStream_t s = lead->stream;
+  HX_CUDA(lead, cudaSetDevice(lead->device));
+  hp.clear();
+  for (hx_ctx* c : ranks) {
+    hp.push_back(team_params(c));
+    c->h.team_epochs = c->team_epochs;
+    HX_CUDA(lead, cudaMemcpyAsync(c->ctl, &c->h, sizeof(Ctl), cudaMemcpyHostToDevice, s));
+    HX_CUDA(lead, cudaMemsetAsync(c->bar, 0, sizeof(GridBar), s));
+    for (DevSched* d : {&c->pa, &c->pt})
+      if (d->view.n_long)
+        HX_CUDA(lead, cudaMemsetAsync(d->flags, 0, 4 * static_cast<size_t>(d->view.n_long) * sizeof(unsigned long long),
+                                      s));
+  }
+  HX_CUDA(lead, cudaMemcpyAsync(lead->team_dev, hp.data(), hp.size() * sizeof(KParams), cudaMemcpyHostToDevice, s));
+  int grp = lead->grid;
+  KParams* dev = lead->team_dev;
+  void* args[] = {&dev, &grp};
+  HX_CUDA(lead, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(loop_kernel_team),
+                                            dim3(static_cast<unsigned>(lead->grid * ranks.size())), dim3(kThreads),
+                                            args, kStageBytes, s));
+  lead->launches += 1;
+  return HPLP_OK;
+}
+
+int team_complete(const std::vector<hx_ctx*>& ranks) {
+  hx_ctx* lead = ranks.front();
+  HX_CUDA(lead, cudaSetDevice(lead->device));
+  std::vector<GridBar> gb(ranks.size());
+  for (size_t i = 0; i < ranks.size(); ++i) {
+    HX_CUDA(lead, cudaMemcpyAsync(&ranks[i]->h, ranks[i]->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, lead->stream));
+    HX_CUDA(lead, cudaMemcpyAsync(&gb[i], ranks[i]->bar, sizeof(GridBar), cudaMemcpyDeviceToHost, lead->stream));
+  }
+  HX_CUDA(lead, cudaStreamSynchronize(lead->stream));
+  HX_CUDA(lead, cudaGetLastError());
+  bool aborted = false;
+  for (size_t i = 0; i < ranks.size(); ++i) {
+    ranks[i]->team_epochs = ranks[i]->h.team_epochs;
+    aborted |= gb[i].abort != 0;
+  }
+  if (aborted) {
+    for (hx_ctx* c : ranks) c->team.nranks = 0;  // barrier words out of step: the team is unusable
+    return set_err(lead, HPLP_ETIMEOUT, "hx: team barrier watchdog fired (a rank stalled; device hang avoided)");
+  }
+  return HPLP_OK;
+}
+
+// One loop launch of a whole team known to this process, grouped by device.
+int team_launch(const std::vector<hx_ctx*>& all) {
+  std::vector<std::vector<hx_ctx*>> groups;
+  for (hx_ctx* c : all) {
+    bool placed = false;
+    for (auto& g : groups)
+      if (g.front()->device == c->device) {
+        g.push_back(c);
+        placed = true;
+      }
+    if (!placed) groups.push_back({c});
+  }
+  std::vector<std::vector<KParams>> hp(groups.size());
+  int rc = HPLP_OK;
+  size_t issued = 0;
+  for (; issued < groups.size() && rc == HPLP_OK; ++issued) rc = team_issue(groups[issued], hp[issued]);
+  for (size_t k = 0; k < issued; ++k) {
+    const int r2 = team_complete(groups[k]);
+    if (rc == HPLP_OK) rc = r2;
+    if (r2 != HPLP_OK)
+      for (hx_ctx* c : all) c->err = groups[k].front()->err;
+  }
+  return rc;
+}
+
+// Result assembly: the x pool vector `role` holds valid values only on each
+// rank's own column block (x+ and everything formed from it are pushed to
+// every rank, the x formed in phase A is not); copy the peers' blocks in.
+int assemble_x(hx_ctx* c, int role) {
+  if (!c->ranked || role < 0) return HPLP_OK;
+  for (int r = 0; r < c->team.nranks; ++r) {
+    const int64_t len = c->pcol1[r] - c->pcol0[r];
+    if (r == c->team.rank || len <= 0) continue;
+    const size_t off = static_cast<size_t>(role) * c->n + c->pcol0[r];
+    HX_CUDA(c, cudaMemcpyAsync(c->xpool + off, c->team.px[r] + off, len * sizeof(double), cudaMemcpyDefault,
+                               c->stream));
   }
   return HPLP_OK;
 }
@@ -1838,6 +2204,8 @@ int hx_create(int32_t device, hx_ctx** out) {
                                         static_cast<int>(kStageBytes)));
   HX_CUDA(nullptr, cudaFuncSetAttribute(spmv_store_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(kStageBytes)));
+  HX_CUDA(nullptr, cudaFuncSetAttribute(loop_kernel_team, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kStageBytes)));
   int occ = 0;
   HX_CUDA(nullptr, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, loop_kernel, kThreads, kStageBytes));
   if (occ < 1) return set_err(nullptr, HPLP_ECUDA, "hx_create: loop kernel does not fit on an SM");
@@ -1865,6 +2233,8 @@ int hx_create(int32_t device, hx_ctx** out) {
 void hx_destroy(hx_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
+  dfree(c->rbar), dfree(c->team_dev);
   free_problem(c);
   dfree(c->slots), dfree(c->scratch), dfree(c->ctl), dfree(c->bar), dfree(c->epochs), dfree(c->kparams), dfree(c->prof);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -1988,11 +2358,30 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     rc = upload_sched(c, c->st, pt.data(), static_cast<int>(n), static_cast<int>(m), c->t_ptr, c->t_idx, c->t_val,
                       lead);
     if (rc) return rc;
+    if (c->ranked) {  // this rank's blocks: rows [row0,row1) of A, [col0,col1) of A^T
+      Team& T = c->team;
+      if (T.row1 > m || T.col1 > n)
+        return set_err(c, HPLP_EINVAL, "hx_upload_csr: partition range exceeds the problem (hx_set_partition)");
+      rc = upload_sched(c, c->pa, ph.data(), T.row1 - T.row0, static_cast<int>(n), c->a_ptr, c->a_idx, c->a_val, 0.0,
+                        T.row0);
+      if (rc) return rc;
+      rc = upload_sched(c, c->pt, pt.data(), T.col1 - T.col0, static_cast<int>(m), c->t_ptr, c->t_idx, c->t_val, lead,
+                        T.col0);
+      if (rc) return rc;
+    }
   }
   HX_CUDA(c, dalloc(&c->xpool, static_cast<size_t>(kXPool) * n));
   HX_CUDA(c, dalloc(&c->ypool, static_cast<size_t>(kYPool) * m));
   HX_CUDA(c, dalloc(&c->axpool, static_cast<size_t>(kAxPool) * m));
   HX_CUDA(c, dalloc(&c->upool, 2 * static_cast<size_t>(n) + 2 * static_cast<size_t>(m)));
+  if (c->ranked) {
+    Team& T = c->team;
+    for (int r = 0; r < kMaxRanks; ++r) T.px[r] = T.py[r] = T.pu[r] = T.ps[r] = nullptr, T.pb[r] = nullptr;
+    T.px[T.rank] = c->xpool, T.py[T.rank] = c->ypool, T.pu[T.rank] = c->upool, T.ps[T.rank] = c->slots;
+    T.pb[T.rank] = c->rbar;
+    c->pcol0[T.rank] = T.col0, c->pcol1[T.rank] = T.col1;
+    c->local_team.assign(1, c);
+  }
   // ||b||, ||c|| once (loop invariants of src/pdhg_core.cpp:60,62).
   kkt_partials_kernel<<<c->grid, kThreads, 0, s>>>(static_cast<int>(m), static_cast<int>(n), nullptr, c->b,
                                                    nullptr, c->c, nullptr, nullptr, c->slots);
@@ -2182,55 +2571,272 @@ int hx_setup(hx_ctx* c, const hplp_config_t* cfg, double sigma_used, double eta,
   return HPLP_OK;
 }
 
-int hx_run(hx_ctx* c, int64_t max_iters, hx_progress_t* p) {
-  if (!c->setup_done) return set_err(c, HPLP_ESTATE, "hx_run: call hx_setup first");
+}  // extern "C"
+
+namespace {
+
+// Loop-top checks of a batch (src/solver.cpp:242-254 before any iteration of
+// this call); true when the loop must launch.
+bool run_begin(hx_ctx* c, int64_t max_iters) {
   Ctl& C = c->h;
-  const int64_t launches0 = c->launches;
-  float ms = 0.f;
-  if (C.status < 0 && C.error == 0 && max_iters > 0) {
-    if (C.it >= C.iteration_limit) {
-      // src/solver.cpp:242-248 before any iteration of this call
-      C.status = HPLP_STATUS_ITERATION_LIMIT;
-      if (C.best_kkt < std::numeric_limits<double>::infinity()) {
-        C.final_x = C.x_best, C.final_y = C.y_best;
-        std::memcpy(C.final_kkt, C.best_err, sizeof(C.final_kkt));
-      } else {
-        C.final_x = C.final_y = -1;
-      }
-    } else if (c->loop_elapsed_s > c->time_limit_s) {
-      // src/solver.cpp:249-254 at the top of the next iteration
-      C.status = HPLP_STATUS_TIME_LIMIT;
-      if (C.best_kkt < std::numeric_limits<double>::infinity()) {
-        C.final_x = C.x_best, C.final_y = C.y_best;
-        std::memcpy(C.final_kkt, C.best_err, sizeof(C.final_kkt));
-      } else {
-        C.final_x = C.final_y = -1;
-      }
+  if (!(C.status < 0 && C.error == 0 && max_iters > 0)) return false;
+  auto limit = [&](int status) {
+    C.status = status;
+    if (C.best_kkt < std::numeric_limits<double>::infinity()) {
+      C.final_x = C.x_best, C.final_y = C.y_best;
+      std::memcpy(C.final_kkt, C.best_err, sizeof(C.final_kkt));
     } else {
-      C.batch_end = C.it + max_iters;
-      C.r.stop = 0;
-      C.paused = 0;
-      const double remaining = c->time_limit_s - c->loop_elapsed_s;
-      C.time_budget_ns = std::isinf(remaining) ? 0ull
-                                               : std::max<unsigned long long>(1ull, static_cast<unsigned long long>(remaining * 1e9));
-      const auto w0 = std::chrono::steady_clock::now();
-      HX_CUDA(c, cudaEventRecord(c->ev0, c->stream));
-      int rc = launch_loop(c);
-      if (rc) return rc;
-      HX_CUDA(c, cudaEventRecord(c->ev1, c->stream));
-      HX_CUDA(c, cudaEventSynchronize(c->ev1));
-      c->loop_elapsed_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
-      HX_CUDA(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+      C.final_x = C.final_y = -1;
     }
+  };
+  if (C.it >= C.iteration_limit) {  // :242-248
+    limit(HPLP_STATUS_ITERATION_LIMIT);
+    return false;
   }
+  if (c->loop_elapsed_s > c->time_limit_s) {  // :249-254 at the top of the next iteration
+    limit(HPLP_STATUS_TIME_LIMIT);
+    return false;
+  }
+  C.batch_end = C.it + max_iters;
+  C.r.stop = 0;
+  C.paused = 0;
+  const double remaining = c->time_limit_s - c->loop_elapsed_s;
+  C.time_budget_ns = std::isinf(remaining)
+                         ? 0ull
+                         : std::max<unsigned long long>(1ull, static_cast<unsigned long long>(remaining * 1e9));
+  return true;
+}
+
+int run_end(hx_ctx* c, hx_progress_t* p, float ms, int64_t launches0) {
   fill_progress(c, p);
   if (p) {
     p->device_ms = ms;
     p->launches = c->launches - launches0;
   }
-  if (C.error == HPLP_EDOMAIN)
+  if (c->h.error == HPLP_EDOMAIN)
     return set_err(c, HPLP_EDOMAIN, "canonical norm: quadratic form is negative (eta too large for this matrix)");
   return HPLP_OK;
+}
+
+// One batch of a team whose ranks all live in this process (emulated on one
+// device, or one rank per device); every rank's host mirror is identical.
+int team_run(const std::vector<hx_ctx*>& ranks, int64_t max_iters, hx_progress_t* progress) {
+  hx_ctx* lead = ranks.front();
+  std::vector<int64_t> l0;
+  bool go = false;
+  for (hx_ctx* c : ranks) {
+    if (!c->setup_done) return set_err(lead, HPLP_ESTATE, "hx_team_run: call hx_setup on every rank first");
+    if (!c->ranked || c->team.nranks == 0)
+      return set_err(lead, HPLP_ESTATE, "hx_team_run: rank is not part of a usable team");
+    for (int r = 0; r < c->team.nranks; ++r)
+      if (!c->team.px[r] || !c->team.py[r] || !c->team.pu[r] || !c->team.ps[r] || !c->team.pb[r])
+        return set_err(lead, HPLP_ESTATE, "hx_run: team incomplete (bind or import every rank first)");
+    l0.push_back(c->launches);
+    go = run_begin(c, max_iters);  // identical decision on every rank
+  }
+  float ms = 0.f;
+  if (go) {
+    const auto w0 = std::chrono::steady_clock::now();
+    HX_CUDA(lead, cudaSetDevice(lead->device));
+    HX_CUDA(lead, cudaEventRecord(lead->ev0, lead->stream));
+    int rc = team_launch(ranks);
+    if (rc) return rc;
+    HX_CUDA(lead, cudaSetDevice(lead->device));
+    HX_CUDA(lead, cudaEventRecord(lead->ev1, lead->stream));
+    HX_CUDA(lead, cudaEventSynchronize(lead->ev1));
+    HX_CUDA(lead, cudaEventElapsedTime(&ms, lead->ev0, lead->ev1));
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+    for (hx_ctx* c : ranks) c->loop_elapsed_s += el;
+  }
+  int rc = HPLP_OK;
+  for (size_t i = 0; i < ranks.size(); ++i) {
+    const int r2 = run_end(ranks[i], progress ? progress + i : nullptr, ms, l0[i]);
+    if (rc == HPLP_OK) rc = r2;
+  }
+  if (rc) lead->err = ranks.back()->err;
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hx_run(hx_ctx* c, int64_t max_iters, hx_progress_t* p) {
+  if (!c->setup_done) return set_err(c, HPLP_ESTATE, "hx_run: call hx_setup first");
+  if (c->ranked) {
+    if (c->local_team.size() > 1)
+      return set_err(c, HPLP_ESTATE, "hx_run: ranks bound in this process run together through hx_team_run");
+    return team_run({c}, max_iters, p);
+  }
+  const int64_t launches0 = c->launches;
+  float ms = 0.f;
+  if (run_begin(c, max_iters)) {
+    const auto w0 = std::chrono::steady_clock::now();
+    HX_CUDA(c, cudaEventRecord(c->ev0, c->stream));
+    int rc = launch_loop(c);
+    if (rc) return rc;
+    HX_CUDA(c, cudaEventRecord(c->ev1, c->stream));
+    HX_CUDA(c, cudaEventSynchronize(c->ev1));
+    c->loop_elapsed_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+    HX_CUDA(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  }
+  return run_end(c, p, ms, launches0);
+}
+
+// ---- row-partitioned team (include/hx.h) ---------------------------------
+int hx_set_partition(hx_ctx* c, int32_t nranks, int32_t rank, int64_t row0, int64_t row1, int64_t col0,
+                     int64_t col1, int32_t ctas) {
+  if (c->uploaded) return set_err(c, HPLP_ESTATE, "hx_set_partition: call before hx_upload_csr");
+  if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks)
+    return set_err(c, HPLP_EINVAL, "hx_set_partition: need 1 <= nranks <= 8 and 0 <= rank < nranks");
+  if (row0 < 0 || row1 < row0 || col0 < 0 || col1 < col0 || row1 >= (int64_t{1} << 31) || col1 >= (int64_t{1} << 31))
+    return set_err(c, HPLP_EINVAL, "hx_set_partition: bad row / column block");
+  int occ = 0;
+  HX_CUDA(c, cudaSetDevice(c->device));
+  HX_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, loop_kernel_team, kThreads, kStageBytes));
+  const int max_ctas = c->sm_count * std::min(std::max(occ, 1), kMinBlocks);
+  if (ctas < 0 || ctas > max_ctas) return set_err(c, HPLP_EINVAL, "hx_set_partition: ctas out of range");
+  if (ctas > 0) c->grid = ctas;
+  c->ranked = true;
+  c->team = Team{};
+  c->team.rank = rank, c->team.nranks = nranks, c->team.grp_ctas = c->grid;
+  c->team.row0 = static_cast<int>(row0), c->team.row1 = static_cast<int>(row1);
+  c->team.col0 = static_cast<int>(col0), c->team.col1 = static_cast<int>(col1);
+  for (int r = 0; r < kMaxRanks; ++r) c->pcol0[r] = c->pcol1[r] = 0;
+  c->local_team.clear();
+  c->team_epochs = 0;
+  // slot regions hold every rank's records
+  dfree(c->slots);
+  c->slots = nullptr;
+  HX_CUDA(c, dalloc(&c->slots, static_cast<size_t>(kRegions) * kReplicas * kMaxQ * c->grid * nranks));
+  if (!c->rbar) HX_CUDA(c, dalloc(&c->rbar, 1));
+  HX_CUDA(c, cudaMemset(c->rbar, 0, sizeof(RankBar)));
+  if (!c->team_dev) HX_CUDA(c, dalloc(&c->team_dev, kMaxRanks));
+  return HPLP_OK;
+}
+
+int hx_team_bind(hx_ctx** ctxs, int32_t count) {
+  if (count < 1 || count > kMaxRanks || !ctxs) return set_err(nullptr, HPLP_EINVAL, "hx_team_bind: bad team size");
+  std::vector<hx_ctx*> by(static_cast<size_t>(count), nullptr);
+  for (int i = 0; i < count; ++i) {
+    hx_ctx* c = ctxs[i];
+    if (!c || !c->ranked || !c->uploaded)
+      return set_err(c, HPLP_ESTATE, "hx_team_bind: every rank needs hx_set_partition + hx_upload_csr");
+    if (c->team.nranks != count || by[c->team.rank])
+      return set_err(c, HPLP_EINVAL, "hx_team_bind: ranks must be 0..count-1, each once");
+    if (c->m != ctxs[0]->m || c->n != ctxs[0]->n || c->nnz != ctxs[0]->nnz || c->grid != ctxs[0]->grid)
+      return set_err(c, HPLP_EINVAL, "hx_team_bind: ranks disagree on the problem or the CTA count");
+    by[c->team.rank] = c;
+  }
+  int64_t rows = 0, cols = 0;
+  for (hx_ctx* c : by) {
+    if (c->team.row0 != rows || c->team.col0 != cols)
+      return set_err(c, HPLP_EINVAL, "hx_team_bind: row / column blocks must tile the problem in rank order");
+    rows = c->team.row1, cols = c->team.col1;
+  }
+  if (rows != by[0]->m || cols != by[0]->n)
+    return set_err(by[0], HPLP_EINVAL, "hx_team_bind: row / column blocks must cover the problem");
+  bool one_device = true;
+  for (hx_ctx* c : by) one_device &= c->device == by[0]->device;
+  if (one_device) {
+    int occ = 0;
+    HX_CUDA(by[0], cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, loop_kernel_team, kThreads, kStageBytes));
+    if (static_cast<int64_t>(by[0]->grid) * count > static_cast<int64_t>(by[0]->sm_count) * occ)
+      return set_err(by[0], HPLP_EINVAL,
+                     "hx_team_bind: the emulated team does not fit on the device at once (ctas * ranks > resident CTAs)");
+  } else {
+    for (hx_ctx* a : by)
+      for (hx_ctx* b : by)
+        if (a->device != b->device) {
+          HX_CUDA(a, cudaSetDevice(a->device));
+          const cudaError_t e = cudaDeviceEnablePeerAccess(b->device, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+            return set_err(a, HPLP_ECUDA, std::string("hx_team_bind: peer access: ") + cudaGetErrorString(e));
+          cudaGetLastError();
+        }
+  }
+  for (hx_ctx* c : by) {
+    Team& T = c->team;
+    for (int r = 0; r < count; ++r) {
+      T.px[r] = by[r]->xpool, T.py[r] = by[r]->ypool, T.pu[r] = by[r]->upool, T.ps[r] = by[r]->slots;
+      T.pb[r] = by[r]->rbar;
+      c->pcol0[r] = by[r]->team.col0, c->pcol1[r] = by[r]->team.col1;
+    }
+    c->local_team = by;
+  }
+  return HPLP_OK;
+}
+
+namespace {
+struct TeamBlob {
+  int32_t magic, rank, nranks, grid;
+  int64_t m, n, nnz;
+  int32_t row0, row1, col0, col1;
+  cudaIpcMemHandle_t hx, hy, hu, hs, hb;
+};
+constexpr int32_t kBlobMagic = 0x48585442;  // "HXTB"
+}  // namespace
+
+int hx_team_export(hx_ctx* c, void* blob, int64_t capacity, int64_t* size) {
+  if (size) *size = static_cast<int64_t>(sizeof(TeamBlob));
+  if (!blob) return HPLP_OK;
+  if (!c->ranked || !c->uploaded) return set_err(c, HPLP_ESTATE, "hx_team_export: needs hx_set_partition + upload");
+  if (capacity < static_cast<int64_t>(sizeof(TeamBlob))) return set_err(c, HPLP_EINVAL, "hx_team_export: blob too small");
+  TeamBlob b{};
+  b.magic = kBlobMagic, b.rank = c->team.rank, b.nranks = c->team.nranks, b.grid = c->grid;
+  b.m = c->m, b.n = c->n, b.nnz = c->nnz;
+  b.row0 = c->team.row0, b.row1 = c->team.row1, b.col0 = c->team.col0, b.col1 = c->team.col1;
+  HX_CUDA(c, cudaSetDevice(c->device));
+  HX_CUDA(c, cudaIpcGetMemHandle(&b.hx, c->xpool));
+  HX_CUDA(c, cudaIpcGetMemHandle(&b.hy, c->ypool));
+  HX_CUDA(c, cudaIpcGetMemHandle(&b.hu, c->upool));
+  HX_CUDA(c, cudaIpcGetMemHandle(&b.hs, c->slots));
+  HX_CUDA(c, cudaIpcGetMemHandle(&b.hb, c->rbar));
+  std::memcpy(blob, &b, sizeof(b));
+  return HPLP_OK;
+}
+
+int hx_team_import(hx_ctx* c, const void* blob, int64_t size) {
+  if (!c->ranked || !c->uploaded) return set_err(c, HPLP_ESTATE, "hx_team_import: needs hx_set_partition + upload");
+  if (size < static_cast<int64_t>(sizeof(TeamBlob))) return set_err(c, HPLP_EINVAL, "hx_team_import: short blob");
+  TeamBlob b;
+  std::memcpy(&b, blob, sizeof(b));
+  if (b.magic != kBlobMagic || b.nranks != c->team.nranks || b.rank < 0 || b.rank >= b.nranks)
+    return set_err(c, HPLP_EINVAL, "hx_team_import: blob of another team");
+  if (b.m != c->m || b.n != c->n || b.nnz != c->nnz || b.grid != c->grid)
+    return set_err(c, HPLP_EINVAL, "hx_team_import: ranks disagree on the problem or the CTA count");
+  c->pcol0[b.rank] = b.col0, c->pcol1[b.rank] = b.col1;
+  if (b.rank == c->team.rank) return HPLP_OK;
+  HX_CUDA(c, cudaSetDevice(c->device));
+  void* p[5] = {};
+  const cudaIpcMemHandle_t* h[5] = {&b.hx, &b.hy, &b.hu, &b.hs, &b.hb};
+  for (int k = 0; k < 5; ++k) {
+    HX_CUDA(c, cudaIpcOpenMemHandle(&p[k], *h[k], cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_open.push_back(p[k]);
+  }
+  Team& T = c->team;
+  T.px[b.rank] = static_cast<double*>(p[0]);
+  T.py[b.rank] = static_cast<double*>(p[1]);
+  T.pu[b.rank] = static_cast<double*>(p[2]);
+  T.ps[b.rank] = static_cast<double*>(p[3]);
+  T.pb[b.rank] = static_cast<RankBar*>(p[4]);
+  return HPLP_OK;
+}
+
+int hx_team_run(hx_ctx** ctxs, int32_t count, int64_t max_iters, hx_progress_t* progress) {
+  if (count < 1 || !ctxs) return set_err(nullptr, HPLP_EINVAL, "hx_team_run: empty team");
+  std::vector<hx_ctx*> v(ctxs, ctxs + count);
+  for (hx_ctx* c : v)
+    if (!c->ranked || c->local_team.size() != static_cast<size_t>(count))
+      return set_err(c, HPLP_ESTATE, "hx_team_run: pass exactly the contexts bound by hx_team_bind");
+  std::sort(v.begin(), v.end(), [](hx_ctx* a, hx_ctx* b) { return a->team.rank < b->team.rank; });
+  std::vector<hx_progress_t> pr(v.size());
+  const int rc = team_run(v, max_iters, pr.data());
+  if (progress)
+    for (int i = 0; i < count; ++i)
+      for (size_t k = 0; k < v.size(); ++k)
+        if (v[k] == ctxs[i]) progress[i] = pr[k];
+  return rc;
 }
 
 int hx_progress(hx_ctx* c, hx_progress_t* p) {
@@ -2258,10 +2864,12 @@ int hx_get_iterate(hx_ctx* c, int32_t which, double* x, double* y) {
   switch (which) {
     case HX_ITERATE_BEST:
       if (C.x_best < 0) return set_err(c, HPLP_ESTATE, "hx_get_iterate: no best iterate yet");
+      if (int rc = assemble_x(c, C.x_best)) return rc;
       dx = xbuf(c, C.x_best), dy = ybuf(c, C.y_best);
       break;
     case HX_ITERATE_LAST:
       if (C.it == 0 && C.status < 0) return set_err(c, HPLP_ESTATE, "hx_get_iterate: no iteration completed");
+      if (int rc = assemble_x(c, C.last_zx)) return rc;
       dx = xbuf(c, C.last_zx), dy = ybuf(c, C.last_y);
       break;
     case HX_ITERATE_NEXT:
@@ -2269,6 +2877,7 @@ int hx_get_iterate(hx_ctx* c, int32_t which, double* x, double* y) {
       break;
     default: {  // the iterate the next iteration starts from
       if (C.status >= 0 && C.final_x >= 0) {
+        if (int rc = assemble_x(c, C.final_x)) return rc;
         dx = xbuf(c, C.final_x), dy = ybuf(c, C.final_y);
       } else if (C.r.x_mode == 0) {
         dx = xbuf(c, C.r.x_src), dy = ybuf(c, C.r.y_cur);
@@ -2298,6 +2907,7 @@ int hx_get_certificate(hx_ctx* c, int32_t kind, double* vec) {
   const double* p;
   const double* q;
   if (is_x) {
+    if (int rc = assemble_x(c, C.last_zx)) return rc;
     p = xbuf(c, C.last_zx);
     q = normalized ? xbuf(c, C.last_xa) : xbuf(c, C.last_xp);
   } else {

@@ -41,6 +41,7 @@ constexpr int kLoadsPerLane = HX_LOADS;    // nonzeros per lane per task
 constexpr int kChunk = 32 * kLoadsPerLane; // max nonzeros per warp task (256)
 constexpr int kStreamRowMax = 64;          // rows up to this length are summed lane-per-row
 constexpr int kStreamRowsMax = 64;         // rows per stream task (two per lane)
+constexpr int kMaxRanks = 8;               // ranks of a row-partitioned team (one node)
 
 // Warp tasks, int4 {row_begin, row_end | kind << 30, p_begin, p_end}; every
 // task covers at most kChunk nonzeros, loaded kLoadsPerLane per lane into
@@ -62,6 +63,7 @@ constexpr int kRowMask = (1 << kKindShift) - 1;
 struct Sched {
   int rows = 0;
   int cols = 0;
+  int W = 0;                       // warps the schedule was dealt to (CTAs * kWarps)
   const int* ptr = nullptr;
   const int* idx = nullptr;
   const double* val = nullptr;

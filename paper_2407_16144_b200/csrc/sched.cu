@@ -18,7 +18,7 @@ namespace hx {
 
 SchedHost build_schedule(const int* ptr, int rows, int warps, double lead) {
   SchedHost s;
-  const int64_t nnz = ptr[rows];
+  const int64_t nnz = ptr[rows] - ptr[0];  // ptr may point into a larger matrix (a rank's block)
   const double total = static_cast<double>(nnz) + kRowCost * rows;
 
   std::vector<double> cost;

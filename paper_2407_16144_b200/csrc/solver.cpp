@@ -8,13 +8,16 @@
 // the synchronous trace sink (trace_period > 0 pauses the device after each
 // traced iteration) and assembles the SolveResult.  There is no CPU compute
 // path: without a B200 the hx layer fails and solve() throws.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "hplp_gpu.hpp"
+#include "hplp_gpu.h"
 #include "hx.h"
 
 namespace hplp_gpu {
@@ -237,7 +240,49 @@ Solver::Solver(int device, int64_t m, int64_t n, const int64_t* row_ptr, const i
   }
 }
 
-Solver::~Solver() { hx_destroy(ctx_); }
+Solver::Solver(const std::vector<int>& devices, int nranks, int64_t m, int64_t n, const int64_t* row_ptr,
+               const int32_t* col_idx, const double* val, const double* b, const double* c, int ctas_per_rank)
+    : m_(m), n_(n), nnz_(row_ptr[m]) {
+  if (devices.empty() || nranks < 1) throw std::invalid_argument("Solver: a team needs devices and nranks >= 1");
+  std::vector<int64_t> rb(static_cast<std::size_t>(nranks) + 1), cb(static_cast<std::size_t>(nranks) + 1);
+  if (hplp_plan_partition(m, n, row_ptr, col_idx, nranks, rb.data(), cb.data()) != HPLP_OK)
+    throw std::invalid_argument("Solver: partition plan failed");
+  auto fail = [&](hx_ctx* ctx, int rc) {
+    const std::string msg = hx_last_error(ctx);
+    for (hx_ctx* x : ranks_) hx_destroy(x);
+    ranks_.clear();
+    ctx_ = nullptr;
+    if (rc == HPLP_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error("hplp_gpu: " + msg);
+  };
+  for (int r = 0; r < nranks; ++r) {
+    const int dev = devices[static_cast<std::size_t>(r) % devices.size()];
+    hx_ctx* ctx = nullptr;
+    int rc = hx_create(dev, &ctx);
+    if (rc != HPLP_OK) fail(nullptr, rc);
+    ranks_.push_back(ctx);
+    int ctas = ctas_per_rank;
+    if (ctas == 0) {  // ranks sharing this device split its SMs
+      int sharing = 0;
+      for (int q = 0; q < nranks; ++q) sharing += devices[static_cast<std::size_t>(q) % devices.size()] == dev;
+      int32_t grid = 0;
+      hx_device_info(ctx, nullptr, &grid, nullptr);
+      ctas = sharing > 1 ? std::max(1, grid / sharing) : 0;
+    }
+    rc = hx_set_partition(ctx, nranks, r, rb[r], rb[r + 1], cb[r], cb[r + 1], ctas);
+    if (rc != HPLP_OK) fail(ctx, rc);
+    rc = hx_upload_csr(ctx, m, n, row_ptr, col_idx, val, b, c);
+    if (rc != HPLP_OK) fail(ctx, rc);
+  }
+  const int rc = hx_team_bind(ranks_.data(), nranks);
+  if (rc != HPLP_OK) fail(ranks_[0], rc);
+  ctx_ = ranks_[0];
+}
+
+Solver::~Solver() {
+  if (ranks_.empty()) hx_destroy(ctx_);
+  for (hx_ctx* x : ranks_) hx_destroy(x);
+}
 
 // solve(): src/solver.cpp:206-342.
 SolveResult Solver::solve(const SolverConfig& config) {
@@ -256,6 +301,9 @@ SolveResult Solver::solve(const SolverConfig& config) {
       col_scale_.assign(static_cast<std::size_t>(n_), 1.0);
       check(ctx, hx_precondition(ctx, config.precondition_ruiz_iters, config.precondition_pc_alpha, row_scale_.data(),
                                  col_scale_.data()));
+      for (std::size_t r = 1; r < ranks_.size(); ++r)  // every rank holds the same transformed problem
+        check(ranks_[r], hx_precondition(ranks_[r], config.precondition_ruiz_iters, config.precondition_pc_alpha,
+                                         nullptr, nullptr));
       scaled_ = true;
       ruiz_ = config.precondition_ruiz_iters;
       pc_alpha_ = config.precondition_pc_alpha;
@@ -295,7 +343,16 @@ SolveResult Solver::solve(const SolverConfig& config) {
   hplp_config_t pod = to_pod(config);
   pod.time_limit_seconds = config.time_limit_seconds - since();  // device clock starts at the loop
   check(ctx, hx_setup(ctx, &pod, sigma_used, eta, x0, y0));
+  for (std::size_t r = 1; r < ranks_.size(); ++r) check(ranks_[r], hx_setup(ranks_[r], &pod, sigma_used, eta, x0, y0));
   n_spmv += 1;  // a_x = A x (:213-214)
+  // one batch of the loop: the context, or every rank of the team together
+  auto run_batch = [&](int64_t batch, hx_progress_t* prog) {
+    if (ranks_.empty()) return hx_run(ctx, batch, prog);
+    std::vector<hx_progress_t> all(ranks_.size());
+    const int rc = hx_team_run(ranks_.data(), static_cast<int32_t>(ranks_.size()), batch, all.data());
+    *prog = all[0];
+    return rc;
+  };
 
   SolveResult out;
   std::vector<hplp_epoch_t> epochs;
@@ -315,7 +372,7 @@ SolveResult Solver::solve(const SolverConfig& config) {
       break;
     }
     const int64_t batch = config.trace_period > 0 ? config.trace_period : kBatch;
-    const int rc = hx_run(ctx, batch, &p);
+    const int rc = run_batch(batch, &p);
     if (rc != HPLP_OK) throw_hx(ctx, rc);
     drain_epochs();
     if (p.paused && config.trace_sink) {

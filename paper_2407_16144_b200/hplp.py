@@ -65,6 +65,9 @@ def lib() -> C.CDLL:
         C.POINTER(abi.IO), C.POINTER(abi.Result))
     sig("hplp_solver_create", C.c_int, I32, I64, I64, PI64, PI32, PD, PD, PD, PV)
     sig("hplp_solver_solve", C.c_int, V, C.POINTER(abi.Config), C.POINTER(abi.IO), C.POINTER(abi.Result))
+    sig("hplp_solver_create_team", C.c_int, PI32, I32, I32, I32, I64, I64, PI64, PI32, PD, PD, PD, PV)
+    sig("hplp_solver_rank_hx", V, V, I32)
+    sig("hplp_plan_partition", C.c_int, I64, I64, PI64, PI32, I32, PI64, PI64)
     sig("hplp_solver_hx", V, V)
     sig("hplp_solver_free", None, V)
     sig("hplp_to_standard_form", C.c_int, C.POINTER(abi.General), PV, PI64, PI64, PI64)
@@ -97,6 +100,11 @@ def lib() -> C.CDLL:
     sig("hx_sched_tasks", C.c_int, V, I32, C.POINTER(C.c_int32), I64, C.POINTER(C.c_int64))
     sig("hx_precondition", C.c_int, V, I32, D, PD, PD)
     sig("hx_download_problem", C.c_int, V, PI64, PI32, PD, PD, PD)
+    sig("hx_set_partition", C.c_int, V, I32, I32, I64, I64, I64, I64, I32)
+    sig("hx_team_bind", C.c_int, PV, I32)
+    sig("hx_team_export", C.c_int, V, C.c_char_p, I64, PI64)
+    sig("hx_team_import", C.c_int, V, C.c_char_p, I64)
+    sig("hx_team_run", C.c_int, PV, I32, I64, C.POINTER(HxProgress))
     _lib = L
     return L
 
@@ -228,6 +236,31 @@ class Solver:
     @classmethod
     def from_std(cls, std: StdForm, device: int = 0) -> "Solver":
         return cls(*std.csr(), device=device)
+
+    @classmethod
+    def team(cls, m, n, row_ptr, col_idx, val, b, c, nranks: int, devices=(0,), ctas_per_rank: int = 0) -> "Solver":
+        """The LP row-partitioned across `nranks` contexts of this process
+        (hplp_solver_create_team): rank r on devices[r % len(devices)]; ranks
+        sharing a device are emulated as CTA groups of one launch."""
+        self = cls.__new__(cls)
+        L = lib()
+        self.m, self.n = int(m), int(n)
+        rp, ci, v, bb, cc = (np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col_idx, np.int32),
+                             np.ascontiguousarray(val, np.float64), np.ascontiguousarray(b, np.float64),
+                             np.ascontiguousarray(c, np.float64))
+        devs = np.ascontiguousarray(devices, np.int32)
+        h = C.c_void_p()
+        _check(L.hplp_solver_create_team(i32ptr(devs), len(devs), int(nranks), int(ctas_per_rank), self.m, self.n,
+                                         i64ptr(rp), i32ptr(ci), dptr(v), dptr(bb), dptr(cc), C.byref(h)))
+        self.h = h
+        self._keep = None
+        self.nranks = int(nranks)
+        self.hx = HX(L.hplp_solver_hx(h), owned=False)
+        return self
+
+    def rank_hx(self, r: int) -> "HX":
+        """hx context of rank r of a team (rank 0 = self.hx)."""
+        return HX(lib().hplp_solver_rank_hx(self.h, int(r)), owned=False)
 
     def solve(self, config=None, init=None, trace=False, epochs_capacity=1 << 16, **kw) -> dict:
         cfg = _config(config, trace, kw)
@@ -380,6 +413,21 @@ class HX:
         self._c(lib().hx_download_problem(self.h, i64ptr(rp), i32ptr(ci), dptr(v), dptr(b), dptr(c)))
         return rp, ci, v, b, c
 
+    # ---- row-partitioned team (include/hx.h) ----
+    def set_partition(self, nranks, rank, row0, row1, col0, col1, ctas=0):
+        self._c(lib().hx_set_partition(self.h, int(nranks), int(rank), int(row0), int(row1), int(col0), int(col1),
+                                       int(ctas)))
+
+    def team_export(self) -> bytes:
+        size = C.c_int64()
+        self._c(lib().hx_team_export(self.h, None, 0, C.byref(size)))
+        buf = C.create_string_buffer(size.value)
+        self._c(lib().hx_team_export(self.h, buf, size.value, C.byref(size)))
+        return buf.raw[: size.value]
+
+    def team_import(self, blob: bytes):
+        self._c(lib().hx_team_import(self.h, blob, len(blob)))
+
     def get_iterate(self, which=0):
         x, y = np.empty(self.n), np.empty(self.m)
         self._c(lib().hx_get_iterate(self.h, which, dptr(x), dptr(y)))
@@ -436,6 +484,28 @@ class HX:
             self.close()
         except Exception:
             pass
+
+
+def plan_partition(m, n, row_ptr, col_idx, parts):
+    """hplp_plan_partition: (row_bounds, col_bounds), parts + 1 entries each."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    ci = np.ascontiguousarray(col_idx, np.int32)
+    rb, cb = np.empty(parts + 1, np.int64), np.empty(parts + 1, np.int64)
+    _check(lib().hplp_plan_partition(int(m), int(n), i64ptr(rp), i32ptr(ci), int(parts), i64ptr(rb), i64ptr(cb)))
+    return rb, cb
+
+
+def team_run(hxs, max_iters):
+    """hx_team_run over contexts bound by hx_team_bind; one progress per context."""
+    arr = (C.c_void_p * len(hxs))(*[h.h.value for h in hxs])
+    prog = (HxProgress * len(hxs))()
+    _check(lib().hx_team_run(arr, len(hxs), int(max_iters), prog), hxs[0].h)
+    return list(prog)
+
+
+def team_bind(hxs):
+    arr = (C.c_void_p * len(hxs))(*[h.h.value for h in hxs])
+    _check(lib().hx_team_bind(arr, len(hxs)), hxs[0].h)
 
 
 ITERATE_CURRENT, ITERATE_BEST, ITERATE_NEXT, ITERATE_LAST = range(4)
