@@ -14,6 +14,11 @@ solver's stream, max over ranks).  e2e = the same metric through the public C
 ABI (hplp_solve_csr) from host buffers: upload + A^T build + power iteration
 + loop + download, every step.
 
+--gpus N > 1 (launched by torchrun, one process per GPU): the SAME LP is
+row-partitioned across the N GPUs (hplp_solver_create_rank +
+CUDA IPC peers exchanged over torch.distributed) -- strong scaling, value =
+iterations/s of that one LP, timed as the max over ranks.
+
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 """
 from __future__ import annotations
@@ -192,7 +197,7 @@ def run_gpu(args):
 
     world, rank, local = dist_setup()
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -200,7 +205,13 @@ def run_gpu(args):
 
     g, s = build_problem()
     m, n, nnz = s.m, s.n, s.nnz
-    solver = hplp.Solver.from_std(s, device=local)
+    sharded = world > 1 or args.sharded
+    if sharded:
+        from paper_2407_16144_b200 import team
+
+        solver = team.rank_solver(s, local)
+    else:
+        solver = hplp.Solver.from_std(s, device=local)
     hx = solver.hx
     stream = torch.cuda.ExternalStream(hx.stream(), device=torch.device("cuda", local))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -241,9 +252,10 @@ def run_gpu(args):
         t = torch.tensor([elapsed], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
-    value = world * iters_done / elapsed
+    value = iters_done / elapsed  # iterations of the one LP (all ranks work on it)
     b_iter = algorithmic_bytes(m, n, nnz)
     peak, peak_kind = measured_peak()
+    peak *= world  # sharded: the aggregate HBM of the N GPUs
     per_launch_s = elapsed / args.steps
     achieved = b_iter * ITERS_PER_STEP / per_launch_s / 1e9
     traffic, prof = traffic_from_profile()
@@ -256,29 +268,41 @@ def run_gpu(args):
     for i in range(args.e2e_steps + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        r = hplp.solve(m, n, rp, ci, v, b, c, iteration_limit=E2E_ITERS, tolerance=1e-4, device=local)
+        if sharded:  # create the rank solver from host buffers, join, solve, download
+            rs = team.rank_solver(s, local)
+            r = rs.solve(iteration_limit=E2E_ITERS, tolerance=1e-4)
+            rs.close()
+        else:
+            r = hplp.solve(m, n, rp, ci, v, b, c, iteration_limit=E2E_ITERS, tolerance=1e-4, device=local)
         dt = time.perf_counter() - t0
         if i > 0:  # first call is warm-up (context creation)
             e2e_times.append(dt)
         assert r["iterations"] == E2E_ITERS or r["status"] != "iteration_limit"
-    e2e_value = world * E2E_ITERS / statistics.median(e2e_times)
+    e2e_value = E2E_ITERS / statistics.median(e2e_times)
     if world > 1:
         import torch.distributed as dist
 
         t = torch.tensor([statistics.median(e2e_times)], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_value = world * E2E_ITERS / float(t.item())
+        e2e_value = E2E_ITERS / float(t.item())
 
     # time to 1e-4 (configs[0] converges; configs[1] capped)
     ttt = {}
-    if rank == 0 and not args.no_ttt:
+    if (rank == 0 or sharded) and not args.no_ttt:
         from paper_2407_16144_b200 import gen
 
         for cid, cap in ((0, 30.0), (1, args.ttt_cap)):
+            if sharded and cid != CONFIG_ID:
+                continue
             gg = g if cid == CONFIG_ID else gen.generate(cid)
             ss = s if cid == CONFIG_ID else hplp.to_standard_form(gg)
             t0 = time.perf_counter()
-            rr = hplp.solve(*ss.csr(), tolerance=1e-4, time_limit_seconds=cap, device=local)
+            if sharded:
+                rs = team.rank_solver(ss, local)
+                rr = rs.solve(tolerance=1e-4, time_limit_seconds=cap)
+                rs.close()
+            else:
+                rr = hplp.solve(*ss.csr(), tolerance=1e-4, time_limit_seconds=cap, device=local)
             dt = time.perf_counter() - t0
             _, obj = ss.recover(rr["x"])
             ttt[f"configs[{cid}]"] = {"status": rr["status"], "seconds": round(dt, 4), "iterations": rr["iterations"],
@@ -297,26 +321,29 @@ def run_gpu(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded planted LP, BASELINE configs[1]; MIPLIB not available)",
             "config": {"workload": f"configs[{CONFIG_ID}] medium planted LP, standard form {m}x{n}, nnz {nnz}",
                        "iters_per_step": ITERS_PER_STEP, "l2": "flushed (256 MiB write) before every timed step",
-                       "parallelism": "single GPU" if world == 1 else f"replicas x{world} (independent LPs)"},
+                       "parallelism": "single GPU" if world == 1 else
+                       f"row-partitioned x{world}: one LP, rows/columns split by nnz, slices pushed over NVLink P2P"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "hx::loop_kernel",
+                         "frac": achieved / peak, "traffic": traffic if world == 1 else None,
+                         "kernel": "hx::loop_kernel" if world == 1 else "hx::loop_kernel_team",
                          "algorithmic_bytes_per_iter": b_iter, "peak_source": peak_kind,
-                         "frac_of_8TBs": achieved / 8000.0},
+                         "frac_of_8TBs": achieved / (8000.0 * world)},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "iters_per_step": E2E_ITERS,
-                    "path": "hplp_solve_csr (C ABI): upload + A^T build + power iteration + loop + download"},
+                    "path": "hplp_solve_csr (C ABI): upload + A^T build + power iteration + loop + download"
+                    if world == 1 else "hplp_solver_create_rank + IPC join + hplp_solver_solve per rank"},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "time_to_1e-4": ttt,
             "per_step_ms": [round(1e3 * t, 3) for t in times],
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch.distributed as dist
 
         dist.barrier()
@@ -337,6 +364,8 @@ def main():
     ap.add_argument("--ttt-cap", type=float, default=60.0)
     ap.add_argument("--no-ttt", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the row-partitioned rank path even at N=1 (test of the N>1 code path)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

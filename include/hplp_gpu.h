@@ -52,6 +52,18 @@ int hplp_solver_create(int32_t device, int64_t m, int64_t n, const int64_t* row_
 int hplp_solver_create_team(const int32_t* devices, int32_t ndevices, int32_t nranks, int32_t ctas_per_rank,
                             int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const double* val,
                             const double* b, const double* c, void** solver);
+/* One rank of a team spread over processes (one process per GPU, e.g. under
+ * torchrun): the solver owns block `rank` of hplp_plan_partition(nranks).
+ * Every process exports its blob (CUDA IPC handles of the buffers peers write
+ * into), the caller exchanges the blobs (any transport; bench.py uses
+ * torch.distributed all_gather_object) and imports all of them; then all ranks
+ * call hplp_solver_solve with the same config, concurrently. */
+int hplp_solver_create_rank(int32_t device, int32_t nranks, int32_t rank, int64_t m, int64_t n,
+                            const int64_t* row_ptr, const int32_t* col_idx, const double* val, const double* b,
+                            const double* c, void** solver);
+/* blob = NULL: *size = bytes needed. */
+int hplp_solver_team_export(void* solver, void* blob, int64_t capacity, int64_t* size);
+int hplp_solver_team_import(void* solver, const void* blob, int64_t size);
 int hplp_solver_solve(void* solver, const hplp_config_t* cfg, hplp_io_t* io, hplp_result_t* result);
 /* The underlying hx context (include/hx.h) for benchmarks and tests. */
 void* hplp_solver_hx(void* solver);

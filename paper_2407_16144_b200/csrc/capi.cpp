@@ -153,6 +153,31 @@ int hplp_solver_create_team(const int32_t* devices, int32_t ndevices, int32_t nr
   });
 }
 
+int hplp_solver_create_rank(int32_t device, int32_t nranks, int32_t rank, int64_t m, int64_t n,
+                            const int64_t* row_ptr, const int32_t* col_idx, const double* val, const double* b,
+                            const double* c, void** solver) {
+  return guarded([&] {
+    hplp_gpu::SparseMatrix a = hplp_gpu::SparseMatrix::from_csr(m, n, row_ptr, col_idx, val);
+    *solver = new hplp_gpu::Solver(device, nranks, rank, m, n, a.row_ptr().data(), a.col_idx().data(),
+                                   a.values().data(), b, c);
+  });
+}
+
+int hplp_solver_team_export(void* solver, void* blob, int64_t capacity, int64_t* size) {
+  return guarded([&] {
+    const std::vector<unsigned char> v = static_cast<hplp_gpu::Solver*>(solver)->team_export();
+    if (size) *size = static_cast<int64_t>(v.size());
+    if (blob) {
+      if (capacity < static_cast<int64_t>(v.size())) throw std::invalid_argument("hplp_solver_team_export: blob too small");
+      std::memcpy(blob, v.data(), v.size());
+    }
+  });
+}
+
+int hplp_solver_team_import(void* solver, const void* blob, int64_t size) {
+  return guarded([&] { static_cast<hplp_gpu::Solver*>(solver)->team_import(blob, static_cast<std::size_t>(size)); });
+}
+
 int hplp_solver_solve(void* solver, const hplp_config_t* cfg, hplp_io_t* io, hplp_result_t* result) {
   return guarded([&] {
     auto* s = static_cast<hplp_gpu::Solver*>(solver);

@@ -266,6 +266,14 @@ class Solver {
   // (ctas_per_rank = 0 splits the device evenly).
   Solver(const std::vector<int>& devices, int nranks, int64_t m, int64_t n, const int64_t* row_ptr,
          const int32_t* col_idx, const double* val, const double* b, const double* c, int ctas_per_rank = 0);
+  // One rank of a team spread over processes (one process per GPU): the
+  // context owns block `rank` of hplp_plan_partition(nranks); the caller
+  // exchanges team_export() blobs between the processes and hands every
+  // rank's blob to team_import() before the first solve().
+  Solver(int device, int nranks, int rank, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+         const double* val, const double* b, const double* c);
+  std::vector<unsigned char> team_export() const;
+  void team_import(const void* blob, std::size_t size);
   ~Solver();
   Solver(const Solver&) = delete;
   Solver& operator=(const Solver&) = delete;

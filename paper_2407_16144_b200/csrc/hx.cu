@@ -45,6 +45,7 @@
 #include <limits>
 #include <memory>
 #include <string>
+#include <type_traits>
 
 #include "hx_internal.cuh"
 
@@ -129,7 +130,8 @@ struct RankBar {
 // each rank reduces all ranks' records locally in one fixed order and the
 // replicated controllers stay bit-identical across ranks.
 struct Team {
-  int rank, nranks, grp_ctas, pad;
+  int rank, nranks, grp_ctas;
+  int sys;                  // 1: some peer is another GPU -> system-scope release/acquire
   int row0, row1, col0, col1;
   double* px[kMaxRanks];    // xpool of every rank (px[rank] = own)
   double* py[kMaxRanks];    // ypool
@@ -761,7 +763,10 @@ __device__ bool team_sync(GridBar* bar, const Team& T, const Geo& g, unsigned lo
   repoch += 1;
   if (threadIdx.x == 0) {
     s_ok = 1;
-    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(&bar->count), "l"(1ull) : "memory");
+    // peers on other GPUs see this CTA's P2P stores only through a
+    // system-scope release; ranks sharing one device need gpu scope only
+    if (T.sys) asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(&bar->count), "l"(1ull) : "memory");
+    else asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(&bar->count), "l"(1ull) : "memory");
     const unsigned long long t0 = global_ns();
     unsigned spins = 0;
     auto alive = [&]() -> bool {
@@ -774,16 +779,20 @@ __device__ bool team_sync(GridBar* bar, const Team& T, const Geo& g, unsigned lo
       return true;
     };
     if (g.cta == 0) {
-      while (ld_acquire_sys_u64(&bar->count) < target)
+      while ((T.sys ? ld_acquire_sys_u64(&bar->count) : ld_acquire_u64(&bar->count)) < target)
         if (!alive()) {
           s_ok = 0;
           break;
         }
       if (s_ok) {
-        for (int r = 0; r < T.nranks; ++r)
-          asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(&T.pb[r]->arrive), "l"(1ull) : "memory");
+        for (int r = 0; r < T.nranks; ++r) {
+          if (T.sys)
+            asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(&T.pb[r]->arrive), "l"(1ull) : "memory");
+          else
+            asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(&T.pb[r]->arrive), "l"(1ull) : "memory");
+        }
         const unsigned long long want = repoch * static_cast<unsigned long long>(T.nranks);
-        while (ld_acquire_sys_u64(&T.pb[T.rank]->arrive) < want)
+        while ((T.sys ? ld_acquire_sys_u64(&T.pb[T.rank]->arrive) : ld_acquire_u64(&T.pb[T.rank]->arrive)) < want)
           if (!alive()) {
             s_ok = 0;
             break;
@@ -1650,19 +1659,19 @@ static_assert(sizeof(KParams) % 8 == 0, "KParams copied as 8-byte words");
 // device a whole team is emulated as groups of one cooperative launch (their
 // CTAs wait on one another, so they must be co-resident -- never separate
 // launches).
-__global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_team(const KParams* __restrict__ team,
-                                                                         int grp_ctas) {
-  __shared__ KParams sP;
-  const int group = blockIdx.x / grp_ctas;
-  {
-    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(team + group);
-    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&sP);
-    for (int i = threadIdx.x; i < static_cast<int>(sizeof(KParams) / 8); i += blockDim.x) dst[i] = __ldg(src + i);
-  }
-  __syncthreads();
-  const int cta = blockIdx.x % grp_ctas;
-  const Geo g{cta, grp_ctas, sP.T.rank * grp_ctas + cta, sP.T.nranks * grp_ctas};
-  loop_body<true>(&sP, g);
+struct TeamLaunch {
+  KParams p[kMaxRanks];  // the ranks of this launch (one on a multi-GPU node)
+  int ranks, grp_ctas;
+};
+static_assert(sizeof(TeamLaunch) < 32000, "TeamLaunch must fit the kernel parameter space");
+
+__global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_team(const __grid_constant__ TeamLaunch L) {
+  // parameters stay in the constant bank (like loop_kernel), indexed by group
+  const int group = blockIdx.x / L.grp_ctas;
+  const KParams* P = &L.p[group];
+  const int cta = blockIdx.x % L.grp_ctas;
+  const Geo g{cta, L.grp_ctas, P->T.rank * L.grp_ctas + cta, P->T.nranks * L.grp_ctas};
+  loop_body<true>(P, g);
 }
 
 // ---------------------------------------------------------------------------
@@ -1891,7 +1900,6 @@ struct hx_ctx {
   int pcol0[kMaxRanks] = {}, pcol1[kMaxRanks] = {};  // every rank's column block (result assembly)
   DevSched pa, pt;                   // rows [row0,row1) of A, [col0,col1) of A^T
   RankBar* rbar = nullptr;
-  KParams* team_dev = nullptr;       // kMaxRanks launch parameter blocks
   unsigned long long team_epochs = 0;
   std::vector<hx_ctx*> local_team;   // ranks launched together (same device), rank order
   std::vector<void*> ipc_open;       // peer mappings to close
@@ -2069,10 +2077,13 @@ int team_issue(const std::vector<hx_ctx*>& ranks, std::vector<KParams>& hp) {
         HX_CUDA(lead, cudaMemsetAsync(d->flags, 0, 4 * static_cast<size_t>(d->view.n_long) * sizeof(unsigned long long),
                                       s));
   }
-  HX_CUDA(lead, cudaMemcpyAsync(lead->team_dev, hp.data(), hp.size() * sizeof(KParams), cudaMemcpyHostToDevice, s));
-  int grp = lead->grid;
-  KParams* dev = lead->team_dev;
-  void* args[] = {&dev, &grp};
+  static_assert(std::is_trivially_copyable<TeamLaunch>::value, "TeamLaunch");
+  auto tl = std::make_unique<TeamLaunch>();
+  std::memset(tl.get(), 0, sizeof(TeamLaunch));
+  for (size_t i = 0; i < hp.size(); ++i) tl->p[i] = hp[i];
+  tl->ranks = static_cast<int>(hp.size());
+  tl->grp_ctas = lead->grid;
+  void* args[] = {tl.get()};
   HX_CUDA(lead, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(loop_kernel_team),
                                             dim3(static_cast<unsigned>(lead->grid * ranks.size())), dim3(kThreads),
                                             args, kStageBytes, s));
@@ -2234,7 +2245,7 @@ void hx_destroy(hx_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
-  dfree(c->rbar), dfree(c->team_dev);
+  dfree(c->rbar);
   free_problem(c);
   dfree(c->slots), dfree(c->scratch), dfree(c->ctl), dfree(c->bar), dfree(c->epochs), dfree(c->kparams), dfree(c->prof);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -2711,7 +2722,6 @@ int hx_set_partition(hx_ctx* c, int32_t nranks, int32_t rank, int64_t row0, int6
   HX_CUDA(c, dalloc(&c->slots, static_cast<size_t>(kRegions) * kReplicas * kMaxQ * c->grid * nranks));
   if (!c->rbar) HX_CUDA(c, dalloc(&c->rbar, 1));
   HX_CUDA(c, cudaMemset(c->rbar, 0, sizeof(RankBar)));
-  if (!c->team_dev) HX_CUDA(c, dalloc(&c->team_dev, kMaxRanks));
   return HPLP_OK;
 }
 
@@ -2757,6 +2767,7 @@ int hx_team_bind(hx_ctx** ctxs, int32_t count) {
   }
   for (hx_ctx* c : by) {
     Team& T = c->team;
+    T.sys = one_device ? 0 : 1;
     for (int r = 0; r < count; ++r) {
       T.px[r] = by[r]->xpool, T.py[r] = by[r]->ypool, T.pu[r] = by[r]->upool, T.ps[r] = by[r]->slots;
       T.pb[r] = by[r]->rbar;
@@ -2815,6 +2826,7 @@ int hx_team_import(hx_ctx* c, const void* blob, int64_t size) {
     c->ipc_open.push_back(p[k]);
   }
   Team& T = c->team;
+  T.sys = 1;  // a peer in another process: another GPU (one process per GPU)
   T.px[b.rank] = static_cast<double*>(p[0]);
   T.py[b.rank] = static_cast<double*>(p[1]);
   T.pu[b.rank] = static_cast<double*>(p[2]);

@@ -279,6 +279,38 @@ Solver::Solver(const std::vector<int>& devices, int nranks, int64_t m, int64_t n
   ctx_ = ranks_[0];
 }
 
+Solver::Solver(int device, int nranks, int rank, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+               const double* val, const double* b, const double* c)
+    : m_(m), n_(n), nnz_(row_ptr[m]) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("Solver: need 0 <= rank < nranks");
+  std::vector<int64_t> rb(static_cast<std::size_t>(nranks) + 1), cb(static_cast<std::size_t>(nranks) + 1);
+  if (hplp_plan_partition(m, n, row_ptr, col_idx, nranks, rb.data(), cb.data()) != HPLP_OK)
+    throw std::invalid_argument("Solver: partition plan failed");
+  int rc = hx_create(device, &ctx_);
+  if (rc != HPLP_OK) throw_hx(nullptr, rc);
+  rc = hx_set_partition(ctx_, nranks, rank, rb[rank], rb[rank + 1], cb[rank], cb[rank + 1], 0);
+  if (rc == HPLP_OK) rc = hx_upload_csr(ctx_, m, n, row_ptr, col_idx, val, b, c);
+  if (rc != HPLP_OK) {
+    const std::string msg = hx_last_error(ctx_);
+    hx_destroy(ctx_);
+    ctx_ = nullptr;
+    if (rc == HPLP_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error("hplp_gpu: " + msg);
+  }
+}
+
+std::vector<unsigned char> Solver::team_export() const {
+  int64_t size = 0;
+  check(ctx_, hx_team_export(ctx_, nullptr, 0, &size));
+  std::vector<unsigned char> blob(static_cast<std::size_t>(size));
+  check(ctx_, hx_team_export(ctx_, blob.data(), size, &size));
+  return blob;
+}
+
+void Solver::team_import(const void* blob, std::size_t size) {
+  check(ctx_, hx_team_import(ctx_, blob, static_cast<int64_t>(size)));
+}
+
 Solver::~Solver() {
   if (ranks_.empty()) hx_destroy(ctx_);
   for (hx_ctx* x : ranks_) hx_destroy(x);

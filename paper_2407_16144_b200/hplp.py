@@ -67,6 +67,9 @@ def lib() -> C.CDLL:
     sig("hplp_solver_solve", C.c_int, V, C.POINTER(abi.Config), C.POINTER(abi.IO), C.POINTER(abi.Result))
     sig("hplp_solver_create_team", C.c_int, PI32, I32, I32, I32, I64, I64, PI64, PI32, PD, PD, PD, PV)
     sig("hplp_solver_rank_hx", V, V, I32)
+    sig("hplp_solver_create_rank", C.c_int, I32, I32, I32, I64, I64, PI64, PI32, PD, PD, PD, PV)
+    sig("hplp_solver_team_export", C.c_int, V, C.c_char_p, I64, PI64)
+    sig("hplp_solver_team_import", C.c_int, V, C.c_char_p, I64)
     sig("hplp_plan_partition", C.c_int, I64, I64, PI64, PI32, I32, PI64, PI64)
     sig("hplp_solver_hx", V, V)
     sig("hplp_solver_free", None, V)
@@ -257,6 +260,36 @@ class Solver:
         self.nranks = int(nranks)
         self.hx = HX(L.hplp_solver_hx(h), owned=False)
         return self
+
+    @classmethod
+    def rank(cls, m, n, row_ptr, col_idx, val, b, c, nranks: int, rank: int, device: int = 0) -> "Solver":
+        """One rank of a team spread over processes (hplp_solver_create_rank):
+        exchange team_export() blobs between the processes (see
+        paper_2407_16144_b200.team.join) before the first solve()."""
+        self = cls.__new__(cls)
+        L = lib()
+        self.m, self.n = int(m), int(n)
+        rp, ci, v, bb, cc = (np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col_idx, np.int32),
+                             np.ascontiguousarray(val, np.float64), np.ascontiguousarray(b, np.float64),
+                             np.ascontiguousarray(c, np.float64))
+        h = C.c_void_p()
+        _check(L.hplp_solver_create_rank(int(device), int(nranks), int(rank), self.m, self.n, i64ptr(rp), i32ptr(ci),
+                                         dptr(v), dptr(bb), dptr(cc), C.byref(h)))
+        self.h = h
+        self._keep = None
+        self.nranks = int(nranks)
+        self.hx = HX(L.hplp_solver_hx(h), owned=False)
+        return self
+
+    def team_export(self) -> bytes:
+        size = C.c_int64()
+        _check(lib().hplp_solver_team_export(self.h, None, 0, C.byref(size)))
+        buf = C.create_string_buffer(size.value)
+        _check(lib().hplp_solver_team_export(self.h, buf, size.value, C.byref(size)))
+        return buf.raw[: size.value]
+
+    def team_import(self, blob: bytes):
+        _check(lib().hplp_solver_team_import(self.h, blob, len(blob)))
 
     def rank_hx(self, r: int) -> "HX":
         """hx context of rank r of a team (rank 0 = self.hx)."""

@@ -95,3 +95,31 @@ def test_row_partitioned_iteration_matches_oracle(name, restart):
     for (it, n_ep, k, x, y, _), tc in zip(trace, cpu["trace"]):
         assert (it, n_ep, k) == (tc["iteration"], tc["epoch"], tc["inner"])
         assert rel_inf(np.concatenate([x, y]), np.concatenate([tc["x"], tc["y"]])) <= 1e-10
+
+
+def _exchange_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2407_16144_b200 import team
+
+    q.put((rank, team.exchange(bytes([rank]) * (rank + 3))))
+    dist.destroy_process_group()
+
+
+def test_team_blob_exchange_gloo():
+    """The multi-process join plumbing (paper_2407_16144_b200/team.py): every
+    rank receives every rank's IPC blob in rank order."""
+    world = 2
+    q = mp.get_context("spawn").SimpleQueue()
+    port = _free_port()
+    ps = [mp.get_context("spawn").Process(target=_exchange_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    got = dict(q.get() for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(world):
+        assert got[r] == [bytes([k]) * (k + 3) for k in range(world)]

@@ -152,3 +152,66 @@ def test_team_low_level_api(gpu_required):
         hplp.HX(device=0).set_partition(9, 0, 0, 1, 0, 1)
     for h in hxs:
         h.close()
+
+
+# ---- one process per GPU (CUDA IPC) ----------------------------------------
+def test_rank_solver_parity(gpu_required):
+    """hplp_solver_create_rank + export/import + solve, as one rank of one: the
+    launch path a torchrun rank takes (team of one, IPC blob of itself)."""
+    g, s = std("cfg1_small")
+    r = hplp.Solver.rank(*csr_args(s), nranks=1, rank=0, device=0)
+    r.team_import(r.team_export())
+    got = r.solve(iteration_limit=100, tolerance=1e-12, trace=True)
+    r.close()
+    cpu = CpuLp("port", *csr_args(s)).solve(iteration_limit=100, tolerance=1e-12, trace=True)
+    _trace_cmp(got["trace"], cpu["trace"])
+    assert got["spmv_count"] == cpu["spmv_count"]
+
+
+def _ipc_worker(rank, port, q):
+    import os
+
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        from paper_2407_16144_b200 import gen, hplp as H, team
+
+        s = H.to_standard_form(gen.generate(0))
+        sol = H.Solver.rank(*s.csr(), nranks=2, rank=rank, device=0)
+        blobs = team.exchange(sol.team_export())
+        for b in blobs:  # opens the peer's CUDA IPC mappings (same device, other process)
+            sol.team_import(b)
+        dist.barrier()  # both mapped before either unmaps
+        sol.close()
+        q.put((rank, "ok", len(blobs), blobs[0] != blobs[1]))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e), 0, False))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_rank_ipc_mapping_two_processes(gpu_required):
+    """Two processes exchange IPC blobs over torch.distributed and map each
+    other's buffers.  No loop runs: two ranks whose kernels wait on one another
+    must not share one GPU (B200_PROFILING.md); the loop itself is covered by
+    the one-launch emulation above."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_ipc_worker, args=(r, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert [o[1] for o in out] == ["ok", "ok"], out
+    assert all(o[2] == 2 and o[3] for o in out)
