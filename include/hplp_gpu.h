@@ -89,6 +89,32 @@ void hplp_std_free(void* std_form);
 int hplp_solve_general(int32_t device, const hplp_general_t* g, const hplp_config_t* cfg, hplp_io_t* io,
                        hplp_result_t* result, double* x_orig, double* objective);
 
+/* ---- MPS ingestion and reports: the reference's declared (unimplemented)
+ * inc/hplp/mps_io.hpp:29-94, SPEC.md [MODULE] mps_io / cli cmd_solve ------
+ * hplp_mps_parse      parse_mps (fixed or free MPS) into a handle holding the
+ *                     GeneralFormLP; HPLP_EPARSE + "line N: ..." on errors.
+ * hplp_mps_view       its CSR-with-bounds view (pointers owned by the handle),
+ *                     ready for hplp_solve_general / hplp_to_standard_form.
+ * hplp_mps_names      0 problem name, 1 objective row, 2 warnings, 3 row
+ *                     names, 4 column names (newline separated).
+ * hplp_mps_write      write_mps: normalized free MPS, 17 significant digits.
+ * hplp_mps_from_general  write_mps of a CSR-with-bounds problem.
+ * hplp_solve_mps      cmd_solve: MPS text -> to_standard_form -> GPU solve ->
+ *                     write_solution_json (elide_above < 0: default 100000)
+ *                     and, with cfg->trace_period > 0, write_trace_csv.
+ * hplp_json_normalize parse_solution_json then write_solution_json.
+ * Text outputs: out == NULL -> *size = length; else cap >= length + 1. */
+int hplp_mps_parse(const char* text, void** handle, int64_t* m, int64_t* n, int64_t* nnz);
+int hplp_mps_view(void* handle, hplp_general_t* view);
+int hplp_mps_names(void* handle, int32_t what, char* out, int64_t cap, int64_t* size);
+int hplp_mps_write(void* handle, char* out, int64_t cap, int64_t* size);
+int hplp_mps_from_general(const hplp_general_t* g, char* out, int64_t cap, int64_t* size);
+void hplp_mps_free(void* handle);
+int hplp_solve_mps(int32_t device, const char* mps_text, const hplp_config_t* cfg, const char* instance,
+                   int64_t elide_above, char* json, int64_t json_cap, int64_t* json_size, char* trace_csv,
+                   int64_t trace_cap, int64_t* trace_size, int32_t* status);
+int hplp_json_normalize(const char* json, int32_t include_timing, char* out, int64_t cap, int64_t* size);
+
 /* Multi-GPU row partition plan: rank p owns rows
  * [row_bounds[p], row_bounds[p+1]) of A and columns [col_bounds[p],
  * col_bounds[p+1]) (rows of A^T), each cut balanced by nnz + 3 per row.

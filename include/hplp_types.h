@@ -22,7 +22,8 @@ enum {
   HPLP_ECUDA = 3,   /* CUDA runtime / launch failure                     */
   HPLP_ENOMEM = 4,  /* device or host allocation failure                 */
   HPLP_ESTATE = 5,  /* call out of order (no problem uploaded, ...)      */
-  HPLP_ETIMEOUT = 6 /* device watchdog fired inside a persistent kernel   */
+  HPLP_ETIMEOUT = 6, /* device watchdog fired inside a persistent kernel  */
+  HPLP_EPARSE = 7    /* MpsParseError (message carries the line number)    */
 };
 
 /* RestartScheme::Kind, inc/solver.hpp:32-44 (same enumerator order). */
@@ -115,8 +116,9 @@ typedef struct hplp_result {
   hplp_cert_meta_t dual_cert;
 } hplp_result_t;
 
-/* The TraceRecord fields the solve loop fills (inc/diagnostics.hpp:72-84);
- * the partition estimate is not part of the hot path. */
+/* TraceRecord (inc/diagnostics.hpp:72-84).  The partition estimate
+ * (PartitionEstimate, :28-33) is given as its three set sizes and one array
+ * holding the N, B1 and B2 index sets back to back (valid during the call). */
 typedef struct hplp_trace {
   int64_t epoch;
   int64_t inner;
@@ -126,6 +128,8 @@ typedef struct hplp_trace {
   double candidate_norm_normalized; /* NaN at k == 0 */
   double candidate_norm_difference;
   double wall_seconds;
+  int64_t partition_n, partition_b1, partition_b2;
+  const int64_t* partition_sets;
 } hplp_trace_t;
 
 /* Synchronous trace sink: SolverConfig::trace_sink(rec, z), called on the

@@ -159,6 +159,13 @@ int hx_get_iterate(hx_ctx* ctx, int32_t which, double* x, double* y);
 /* [make_certificate, src/solver.cpp:89-101] kind 0 primal (m), 1 dual (n). */
 int hx_get_certificate(hx_ctx* ctx, int32_t kind, double* vec);
 
+/* [TraceRecord fields, src/solver.cpp:279-287] for the last completed
+ * iteration: aty (n) = A^T y and c_out (n) = c of the device problem (the
+ * partition estimate's reduced costs are c + A^T y), and the canonical norm
+ * of the normalized candidate (2/k)(z - anchor); NaN when undefined (k = 0,
+ * multi-rank context).  Any output may be NULL. */
+int hx_trace_extras(hx_ctx* ctx, double* aty, double* c_out, double* cand_norm_normalized);
+
 /* [kkt_error, src/pdhg_core.cpp:70-73] at the current iterate with fresh
  * products (the limit path of src/solver.cpp:242-254 when no best exists). */
 int hx_kkt_current(hx_ctx* ctx, hplp_kkt_t* out);

@@ -503,7 +503,7 @@ void solve(const Lp& lp, const hplp_config_t& cfg, hplp_io_t* io, hplp_result_t*
       best_err = e;
     }
     if (cfg.trace_period > 0 && it % cfg.trace_period == 0 && io && io->trace_fn) {
-      hplp_trace_t t;  // :271-290 (partition estimate omitted: diagnostics only)
+      hplp_trace_t t;  // :271-290
       t.epoch = ep;
       t.inner = k;
       t.iteration = it;
@@ -518,6 +518,22 @@ void solve(const Lp& lp, const hplp_config_t& cfg, hplp_io_t* io, hplp_result_t*
                                                 scale(s, sub(a_x, a_x_anchor)), eta);
       }
       t.wall_seconds = since();
+      // partition_estimate_from_reduced_costs(z, c + A^T y, tol_active, sigma),
+      // src/diagnostics.cpp:26-43 via src/solver.cpp:279-280
+      std::vector<int64_t> pn, pb1, pb2;
+      const double r_tol = cfg.tol_active * sigma_used;
+      for (int64_t j = 0; j < n; ++j) {
+        const double r = lp.c[j] + sr.at_y[j];
+        if (r > r_tol) pn.push_back(j);
+        else if (std::abs(r) <= r_tol && x[j] > cfg.tol_active) pb1.push_back(j);
+        else pb2.push_back(j);
+      }
+      t.partition_n = static_cast<int64_t>(pn.size());
+      t.partition_b1 = static_cast<int64_t>(pb1.size());
+      t.partition_b2 = static_cast<int64_t>(pb2.size());
+      pn.insert(pn.end(), pb1.begin(), pb1.end());
+      pn.insert(pn.end(), pb2.begin(), pb2.end());
+      t.partition_sets = pn.data();
       io->trace_fn(&t, x.data(), n, y.data(), m, io->trace_user);
     }
     if (e.max <= cfg.tolerance) {  // :292-295

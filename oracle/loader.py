@@ -187,6 +187,7 @@ class CpuLp:
                              res=r.fixed_point_residual, kkt=r.kkt.as_tuple(),
                              cand_norm_normalized=r.candidate_norm_normalized,
                              cand_norm_difference=r.candidate_norm_difference,
+                             partition=abi.trace_partition(r),
                              x=np.ctypeslib.as_array(xp, (n,)).copy(),
                              y=np.ctypeslib.as_array(yp, (m,)).copy()))
 

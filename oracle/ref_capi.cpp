@@ -263,6 +263,13 @@ int ref_lp_solve(void* h, const hplp_config_t* cfg, hplp_io_t* io, hplp_result_t
         t.candidate_norm_normalized = rec.candidate_norm_normalized;
         t.candidate_norm_difference = rec.candidate_norm_difference;
         t.wall_seconds = rec.wall_seconds;
+        std::vector<int64_t> sets;
+        for (auto v : {&rec.partition.n_set, &rec.partition.b1_set, &rec.partition.b2_set})
+          for (auto i : *v) sets.push_back(static_cast<int64_t>(i));
+        t.partition_n = static_cast<int64_t>(rec.partition.n_set.size());
+        t.partition_b1 = static_cast<int64_t>(rec.partition.b1_set.size());
+        t.partition_b2 = static_cast<int64_t>(rec.partition.b2_set.size());
+        t.partition_sets = sets.data();
         io->trace_fn(&t, z.x.data(), z.x.size(), z.y.data(), z.y.size(), io->trace_user);
       };
     }

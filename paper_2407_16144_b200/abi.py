@@ -10,7 +10,7 @@ import math
 
 import numpy as np
 
-HPLP_OK, HPLP_EINVAL, HPLP_EDOMAIN, HPLP_ECUDA, HPLP_ENOMEM, HPLP_ESTATE, HPLP_ETIMEOUT = range(7)
+HPLP_OK, HPLP_EINVAL, HPLP_EDOMAIN, HPLP_ECUDA, HPLP_ENOMEM, HPLP_ESTATE, HPLP_ETIMEOUT, HPLP_EPARSE = range(8)
 
 RESTART_FIXED, RESTART_ADAPTIVE, RESTART_NONE = range(3)
 
@@ -154,7 +154,18 @@ class Trace(C.Structure):
         ("candidate_norm_normalized", C.c_double),
         ("candidate_norm_difference", C.c_double),
         ("wall_seconds", C.c_double),
+        ("partition_n", C.c_int64),
+        ("partition_b1", C.c_int64),
+        ("partition_b2", C.c_int64),
+        ("partition_sets", C.POINTER(C.c_int64)),
     ]
+
+
+def trace_partition(r):
+    """(N, B1, B2) index arrays of a Trace record (PartitionEstimate)."""
+    k = r.partition_n + r.partition_b1 + r.partition_b2
+    a = np.ctypeslib.as_array(r.partition_sets, (k,)).copy() if k else np.zeros(0, np.int64)
+    return a[: r.partition_n], a[r.partition_n: r.partition_n + r.partition_b1], a[r.partition_n + r.partition_b1:]
 
 
 TRACE_FN = C.CFUNCTYPE(None, C.POINTER(Trace), C.POINTER(C.c_double), C.c_int64,

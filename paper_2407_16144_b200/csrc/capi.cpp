@@ -18,6 +18,9 @@ int guarded(F&& f) {
   try {
     f();
     return HPLP_OK;
+  } catch (const hplp_gpu::MpsParseError& e) {
+    g_err = e.what();
+    return HPLP_EPARSE;
   } catch (const std::domain_error& e) {
     g_err = e.what();
     return HPLP_EDOMAIN;
@@ -90,6 +93,13 @@ hplp_gpu::SolverConfig config_with_io(const hplp_config_t* cfg, hplp_io_t* io, i
       t.candidate_norm_normalized = rec.candidate_norm_normalized;
       t.candidate_norm_difference = rec.candidate_norm_difference;
       t.wall_seconds = rec.wall_seconds;
+      std::vector<int64_t> sets;
+      for (auto v : {&rec.partition.n_set, &rec.partition.b1_set, &rec.partition.b2_set})
+        for (auto i : *v) sets.push_back(static_cast<int64_t>(i));
+      t.partition_n = static_cast<int64_t>(rec.partition.n_set.size());
+      t.partition_b1 = static_cast<int64_t>(rec.partition.b1_set.size());
+      t.partition_b2 = static_cast<int64_t>(rec.partition.b2_set.size());
+      t.partition_sets = sets.data();
       io->trace_fn(&t, z.x.data(), static_cast<int64_t>(z.x.size()), z.y.data(), static_cast<int64_t>(z.y.size()),
                    io->trace_user);
     };
@@ -256,6 +266,194 @@ int hplp_solve_general(int32_t device, const hplp_general_t* g, const hplp_confi
       std::memcpy(x_orig, xo.data(), xo.size() * sizeof(double));
     }
     if (objective) *objective = conv.second.recover_objective(cx);
+  });
+}
+
+// ---- MPS ingestion and reports (inc/hplp/mps_io.hpp; csrc/mps_io.cpp) ----
+
+namespace {
+struct MpsHandle {
+  hplp_gpu::GeneralFormLP g;
+  hplp_gpu::MpsDocument doc;
+  // hplp_general_t view (CSR rows from the triplets, row order kept)
+  std::vector<int64_t> rp;
+  std::vector<int32_t> ci;
+  std::vector<double> v, rhs, range, lo, up, obj;
+  std::vector<int32_t> rel;
+  hplp_general_t view{};
+  void build() {
+    const int64_t m = g.num_rows(), n = g.num_cols();
+    rp.assign(static_cast<std::size_t>(m) + 1, 0);
+    for (const auto& t : g.entries) ++rp[static_cast<std::size_t>(t.row) + 1];
+    for (int64_t i = 0; i < m; ++i) rp[i + 1] += rp[i];
+    ci.resize(g.entries.size());
+    v.resize(g.entries.size());
+    std::vector<int64_t> fill(rp.begin(), rp.end() - 1);
+    for (const auto& t : g.entries) {
+      const int64_t k = fill[t.row]++;
+      ci[k] = static_cast<int32_t>(t.col);
+      v[k] = t.value;
+    }
+    rel.resize(m), rhs.resize(m), range.resize(m);
+    for (int64_t i = 0; i < m; ++i) {
+      const auto& r = g.rows[i];
+      rel[i] = r.relation == hplp_gpu::RowRelation::kLessEqual      ? HPLP_ROW_LE
+               : r.relation == hplp_gpu::RowRelation::kGreaterEqual ? HPLP_ROW_GE
+                                                                    : HPLP_ROW_EQ;
+      rhs[i] = r.rhs;
+      range[i] = r.range ? *r.range : std::nan("");
+    }
+    lo.resize(n), up.resize(n), obj.resize(n);
+    for (int64_t j = 0; j < n; ++j) lo[j] = g.columns[j].lower, up[j] = g.columns[j].upper, obj[j] = g.objective[j];
+    view = hplp_general_t{m,          n,          static_cast<int64_t>(ci.size()), rp.data(), ci.data(), v.data(),
+                          rel.data(), rhs.data(), range.data(),                    lo.data(), up.data(), obj.data(),
+                          g.maximize ? 1 : 0,     0,          g.objective_constant};
+  }
+};
+
+int put_text(const std::string& s, char* out, int64_t cap, int64_t* size) {
+  if (size) *size = static_cast<int64_t>(s.size());
+  if (out) {
+    if (cap < static_cast<int64_t>(s.size()) + 1) throw std::invalid_argument("output buffer too small");
+    std::memcpy(out, s.c_str(), s.size() + 1);
+  }
+  return HPLP_OK;
+}
+}  // namespace
+
+int hplp_mps_parse(const char* text, void** handle, int64_t* m, int64_t* n, int64_t* nnz) {
+  return guarded([&] {
+    auto h = std::make_unique<MpsHandle>();
+    h->g = hplp_gpu::parse_mps(std::string(text), &h->doc);
+    h->build();
+    if (m) *m = h->view.m;
+    if (n) *n = h->view.n;
+    if (nnz) *nnz = h->view.nnz;
+    *handle = h.release();
+  });
+}
+
+int hplp_mps_view(void* handle, hplp_general_t* view) {
+  return guarded([&] { *view = static_cast<MpsHandle*>(handle)->view; });
+}
+
+int hplp_mps_names(void* handle, int32_t what, char* out, int64_t cap, int64_t* size) {
+  return guarded([&] {
+    const auto& h = *static_cast<MpsHandle*>(handle);
+    std::string s;
+    if (what == 0) s = h.g.name;
+    else if (what == 1) s = h.g.objective_name;
+    else if (what == 2)
+      for (const auto& w : h.doc.warnings) s += w + "\n";
+    else if (what == 3)
+      for (const auto& r : h.g.rows) s += r.name + "\n";
+    else if (what == 4)
+      for (const auto& c : h.g.columns) s += c.name + "\n";
+    else throw std::invalid_argument("hplp_mps_names: what in 0..4");
+    put_text(s, out, cap, size);
+  });
+}
+
+int hplp_mps_write(void* handle, char* out, int64_t cap, int64_t* size) {
+  return guarded([&] { put_text(hplp_gpu::write_mps(static_cast<MpsHandle*>(handle)->g), out, cap, size); });
+}
+
+void hplp_mps_free(void* handle) { delete static_cast<MpsHandle*>(handle); }
+
+int hplp_mps_from_general(const hplp_general_t* g, char* out, int64_t cap, int64_t* size) {
+  return guarded([&] {
+    hplp_gpu::GeneralFormLP lp;
+    lp.name = "GENERAL";
+    lp.objective_name = "OBJ";
+    lp.maximize = g->maximize != 0;
+    lp.objective_constant = g->objective_constant;
+    lp.rows.resize(static_cast<std::size_t>(g->m));
+    for (int64_t i = 0; i < g->m; ++i) {
+      auto& r = lp.rows[i];
+      r.name = "R" + std::to_string(i);
+      r.relation = g->row_relation[i] == HPLP_ROW_LE   ? hplp_gpu::RowRelation::kLessEqual
+                   : g->row_relation[i] == HPLP_ROW_GE ? hplp_gpu::RowRelation::kGreaterEqual
+                                                       : hplp_gpu::RowRelation::kEqual;
+      r.rhs = g->row_rhs[i];
+      if (g->row_range && !std::isnan(g->row_range[i])) r.range = g->row_range[i];
+    }
+    lp.columns.resize(static_cast<std::size_t>(g->n));
+    lp.objective.assign(g->objective, g->objective + g->n);
+    for (int64_t j = 0; j < g->n; ++j) {
+      lp.columns[j].name = "C" + std::to_string(j);
+      lp.columns[j].lower = g->col_lower[j];
+      lp.columns[j].upper = g->col_upper[j];
+    }
+    // column-major entries (the order an MPS COLUMNS section gives)
+    std::vector<std::vector<hplp_gpu::Triplet>> by_col(static_cast<std::size_t>(g->n));
+    for (int64_t i = 0; i < g->m; ++i)
+      for (int64_t p = g->row_ptr[i]; p < g->row_ptr[i + 1]; ++p)
+        by_col[g->col_idx[p]].push_back(hplp_gpu::Triplet{i, g->col_idx[p], g->val[p]});
+    for (const auto& v : by_col) lp.entries.insert(lp.entries.end(), v.begin(), v.end());
+    put_text(hplp_gpu::write_mps(lp), out, cap, size);
+  });
+}
+
+int hplp_solve_mps(int32_t device, const char* mps_text, const hplp_config_t* cfg, const char* instance,
+                   int64_t elide_above, char* json, int64_t json_cap, int64_t* json_size, char* trace_csv,
+                   int64_t trace_cap, int64_t* trace_size, int32_t* status) {
+  return guarded([&] {
+    hplp_gpu::MpsDocument doc;
+    const hplp_gpu::GeneralFormLP g = hplp_gpu::parse_mps(std::string(mps_text), &doc);
+    auto conv = hplp_gpu::to_standard_form(g);
+    const hplp_gpu::StandardFormLP& lp = conv.first;
+    hplp_gpu::Solver s(lp, device);
+    if (const int rc = hplp_validate_config(cfg); rc != HPLP_OK) throw std::invalid_argument(g_err);
+    hplp_gpu::SolverConfig c = hplp_gpu::from_pod(*cfg);
+    c.device = device;
+    std::vector<hplp_gpu::TraceRecord> trace;
+    if (c.trace_period > 0) c.trace_sink = [&](const hplp_gpu::TraceRecord& r, const hplp_gpu::Iterate&) { trace.push_back(r); };
+    const hplp_gpu::SolveResult r = s.solve(c);
+    hplp_gpu::SolutionReport rep;
+    rep.instance = instance ? instance : g.name;
+    rep.status = r.status;
+    double cx = 0.0, by = 0.0;
+    for (std::size_t j = 0; j < lp.c.size(); ++j) cx += lp.c[j] * r.final_iterate.x[j];
+    for (std::size_t i = 0; i < lp.b.size(); ++i) by += lp.b[i] * r.final_iterate.y[i];
+    rep.primal_objective = conv.second.recover_objective(cx);
+    rep.dual_objective = conv.second.recover_objective(-by);  // gap |c'x + b'y| -> dual value -b'y
+    rep.kkt = r.final_kkt;
+    rep.iterations = r.totals.iterations;
+    rep.epochs = static_cast<long>(r.epochs.size());
+    rep.spmv_count = r.totals.spmv_count;
+    rep.eta = r.totals.eta;
+    rep.sigma_estimate = r.totals.sigma_estimate;
+    rep.solve_seconds = r.totals.wall_seconds;
+    const bool infeasible = r.status == hplp_gpu::SolveStatus::kPrimalInfeasible ||
+                            r.status == hplp_gpu::SolveStatus::kDualInfeasible ||
+                            r.status == hplp_gpu::SolveStatus::kPrimalDualInfeasible;
+    if (!infeasible) {
+      rep.primal_solution = conv.second.recover_primal(r.final_iterate.x);
+      rep.dual_solution = r.final_iterate.y;
+    }
+    rep.primal_certificate = r.primal_certificate;
+    rep.dual_certificate = r.dual_certificate;
+    rep.config_echo = {{"tolerance", std::to_string(c.tolerance)},
+                       {"iteration_limit", std::to_string(c.iteration_limit)},
+                       {"restart", c.restart.kind == hplp_gpu::RestartScheme::Kind::kFixedFrequency ? "fixed"
+                                   : c.restart.kind == hplp_gpu::RestartScheme::Kind::kNone           ? "none"
+                                                                                                      : "adaptive"},
+                       {"infeasibility_check_period", std::to_string(c.infeasibility_check_period)},
+                       {"seed", std::to_string(c.seed)},
+                       {"device", std::to_string(device)}};
+    hplp_gpu::JsonWriteOptions opt;
+    if (elide_above >= 0) opt.vector_elision_threshold = elide_above;
+    put_text(hplp_gpu::write_solution_json(rep, opt), json, json_cap, json_size);
+    if (trace_csv || trace_size) put_text(hplp_gpu::write_trace_csv(trace), trace_csv, trace_cap, trace_size);
+    if (status) *status = static_cast<int32_t>(r.status);
+  });
+}
+
+int hplp_json_normalize(const char* json, int32_t include_timing, char* out, int64_t cap, int64_t* size) {
+  return guarded([&] {
+    hplp_gpu::JsonWriteOptions opt;
+    opt.include_timing = include_timing != 0;
+    put_text(hplp_gpu::write_solution_json(hplp_gpu::parse_solution_json(json), opt), out, cap, size);
   });
 }
 

@@ -8,8 +8,10 @@
 
 #include <cstdint>
 #include <functional>
+#include <iosfwd>
 #include <limits>
 #include <optional>
+#include <stdexcept>
 #include <string>
 #include <utility>
 #include <vector>
@@ -180,14 +182,29 @@ const char* to_string(SolveStatus status);
 enum class CandidateSource { kNormalizedIterate, kIterateDifference };
 enum class Orientation { kAsIs, kNegated };
 
-// inc/diagnostics.hpp:72-84 (the partition estimate is diagnostics-only and
-// left empty by the GPU loop).
+// inc/diagnostics.hpp:28-33 -- active-set partition of the primal
+// coordinates: N reduced cost > tol*sigma, B1 |reduced cost| <= tol*sigma and
+// x > tol, B2 the rest (src/diagnostics.cpp:26-43).
+struct PartitionEstimate {
+  std::vector<Index> n_set;
+  std::vector<Index> b1_set;
+  std::vector<Index> b2_set;
+  double tol_active = 1e-6;
+};
+
+// partition_estimate_from_reduced_costs, src/diagnostics.cpp:26-43.
+PartitionEstimate partition_estimate_from_reduced_costs(const Iterate& z, const Vector& reduced_costs,
+                                                        double tol_active, double sigma_estimate);
+
+// inc/diagnostics.hpp:72-84; filled as src/solver.cpp:271-290 does (the
+// reduced costs come from a device A^T y of the traced iterate).
 struct TraceRecord {
   long epoch = 0;
   long inner = 0;
   long iteration = 0;
   double fixed_point_residual = 0.0;
   KktError kkt;
+  PartitionEstimate partition;
   double candidate_norm_normalized = std::numeric_limits<double>::quiet_NaN();
   double candidate_norm_difference = std::numeric_limits<double>::quiet_NaN();
   double wall_seconds = 0.0;
@@ -303,5 +320,56 @@ SolveResult solve(const StandardFormLP& lp, const SolverConfig& config);
 // config <-> flat POD (include/hplp_types.h)
 SolverConfig from_pod(const hplp_config_t& c);
 hplp_config_t to_pod(const SolverConfig& c);
+
+// ---- MPS ingestion and reports: inc/hplp/mps_io.hpp:29-94 (declared by the
+// reference, implemented here in csrc/mps_io.cpp) --------------------------------
+class MpsParseError : public std::runtime_error {
+ public:
+  MpsParseError(long line, const std::string& message)
+      : std::runtime_error("line " + std::to_string(line) + ": " + message), line_(line) {}
+  long line() const { return line_; }
+
+ private:
+  long line_;
+};
+
+struct MpsDocument {
+  std::string problem_name;
+  std::string objective_row_name;
+  std::vector<std::string> warnings;
+};
+
+GeneralFormLP parse_mps(std::istream& in, MpsDocument* doc = nullptr);
+GeneralFormLP parse_mps(const std::string& text, MpsDocument* doc = nullptr);
+GeneralFormLP parse_mps_file(const std::string& path, MpsDocument* doc = nullptr);
+std::string write_mps(const GeneralFormLP& g);
+
+struct SolutionReport {
+  std::string instance;
+  SolveStatus status = SolveStatus::kIterationLimit;
+  double primal_objective = std::numeric_limits<double>::quiet_NaN();
+  double dual_objective = std::numeric_limits<double>::quiet_NaN();
+  KktError kkt;
+  long iterations = 0;
+  long epochs = 0;
+  long spmv_count = 0;
+  double eta = 0.0;
+  double sigma_estimate = 0.0;
+  double solve_seconds = 0.0;
+  std::optional<Vector> primal_solution;
+  std::optional<Vector> dual_solution;
+  std::optional<Certificate> primal_certificate;
+  std::optional<Certificate> dual_certificate;
+  std::vector<std::pair<std::string, std::string>> config_echo;
+};
+
+struct JsonWriteOptions {
+  bool include_timing = true;
+  Index vector_elision_threshold = 100000;
+};
+
+std::string write_solution_json(const SolutionReport& report, const JsonWriteOptions& options = {});
+SolutionReport parse_solution_json(const std::string& text);
+std::string write_trace_csv(const std::vector<TraceRecord>& trace);
 
 }  // namespace hplp_gpu

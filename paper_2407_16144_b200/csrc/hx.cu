@@ -85,7 +85,7 @@ struct Ctl {
   int status, error, paused, x_best_prev;  // x_best before this iteration's update
   long long last_it, last_n, last_k;
   double last_res, last_kkt[4];
-  int last_zx, last_y, last_xp, last_yp, last_xa, last_ya, last_ax, last_axp;
+  int last_zx, last_y, last_xp, last_yp, last_xa, last_ya, last_ax, last_axp, last_axa, pad1;
   double final_kkt[4];
   int final_x, final_y;
   int cfinite[4];
@@ -962,6 +962,7 @@ __device__ void main_logic(Ctl& C, const double* tot, const double* pre, hplp_ep
   C.last_ya = R.y_anchor;
   C.last_ax = R.ax_cur;
   C.last_axp = R.axp_out;
+  C.last_axa = R.ax_anchor;
   if (kkt[3] <= C.tol) {  // :292-295, returns z
     C.status = HPLP_STATUS_OPTIMAL;
     C.final_x = R.zx_out;
@@ -1729,6 +1730,28 @@ kkt_partials_kernel(int m, int n, const double* ax, const double* b, const doubl
     acc[5] += cj * cj;
   }
   block_to_slots<6, 0>(acc, slots, gridDim.x);
+}
+
+// Trace diagnostics (src/solver.cpp:283-287): sums of the normalized
+// candidate s (z - anchor) with its product s (a_x - a_x_anchor):
+// ||dx||^2, ||dy||^2, dy . d(Ax), each term rounded as the reference forms it.
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+cand_norm_kernel(int m, int n, double s, const double* zx, const double* xa, const double* y, const double* ya,
+                 const double* ax, const double* axa, double* slots) {
+  double acc[3];
+  acc_init<3, 0>(acc);
+  const int gtid = blockIdx.x * kThreads + threadIdx.x, gs = gridDim.x * kThreads;
+  for (int j = gtid; j < n; j += gs) {
+    const double d = s * (zx[j] - xa[j]);
+    acc[0] += d * d;
+  }
+  for (int i = gtid; i < m; i += gs) {
+    const double dy = s * (y[i] - ya[i]);
+    const double da = s * (ax[i] - axa[i]);
+    acc[1] += dy * dy;
+    acc[2] += dy * da;
+  }
+  block_to_slots<3, 0>(acc, slots, gridDim.x);
 }
 
 __global__ void final_reduce_kernel(const double* region, int grid, int q_count, double* out) {
@@ -2933,6 +2956,48 @@ int hx_get_certificate(hx_ctx* c, int32_t kind, double* vec) {
   c->launches += 1;
   HX_CUDA(c, cudaMemcpyAsync(vec, tmp, len * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   HX_CUDA(c, cudaStreamSynchronize(c->stream));
+  return HPLP_OK;
+}
+
+// Trace-point diagnostics of the last completed iteration (the fields of
+// TraceRecord the loop does not produce, src/solver.cpp:279-287): A^T y of
+// the traced y (the partition estimate's reduced costs are c + A^T y, on the
+// device problem) and the canonical norm of the normalized candidate
+// (2/k)(z - anchor) with its carried product; NaN when k = 0 (undefined), for
+// a multi-rank context (A x is rank-local), or when the quadratic form is
+// clearly negative.
+int hx_trace_extras(hx_ctx* c, double* aty, double* c_out, double* cand_norm_normalized) {
+  if (!c->setup_done) return set_err(c, HPLP_ESTATE, "hx_trace_extras: no solve state");
+  const Ctl& C = c->h;
+  cudaStream_t s = c->stream;
+  if (aty || c_out) {
+    double* dout = c->upool;
+    int rc = spmv_dev(c, true, ybuf(c, C.last_y), dout);
+    if (rc) return rc;
+    if (aty && c->n) HX_CUDA(c, cudaMemcpyAsync(aty, dout, c->n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (c_out && c->n) HX_CUDA(c, cudaMemcpyAsync(c_out, c->c, c->n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  }
+  if (cand_norm_normalized) {
+    *cand_norm_normalized = std::numeric_limits<double>::quiet_NaN();
+    if (C.last_k >= 1 && !c->ranked) {
+      const double scale = 2.0 / static_cast<double>(C.last_k);
+      cand_norm_kernel<<<c->grid, kThreads, 0, s>>>(static_cast<int>(c->m), static_cast<int>(c->n), scale,
+                                                    xbuf(c, C.last_zx), xbuf(c, C.last_xa), ybuf(c, C.last_y),
+                                                    ybuf(c, C.last_ya), axbuf(c, C.last_ax), axbuf(c, C.last_axa),
+                                                    c->slots);
+      final_reduce_kernel<<<1, 256, 0, s>>>(c->slots, c->grid, 3, c->scratch);
+      c->launches += 2;
+      double t[3];
+      HX_CUDA(c, cudaMemcpyAsync(t, c->scratch, sizeof(t), cudaMemcpyDeviceToHost, s));
+      HX_CUDA(c, cudaStreamSynchronize(s));
+      // canonical_norm_with_product, src/pdhg_core.cpp:37-51
+      const double eta = C.r.eta;
+      const double q = t[0] / eta - 2.0 * t[2] + t[1] / eta;
+      if (q >= 0.0) *cand_norm_normalized = std::sqrt(q);
+      else if (q >= -1e-9 * ((t[0] + t[1]) / eta)) *cand_norm_normalized = 0.0;
+    }
+  }
+  HX_CUDA(c, cudaStreamSynchronize(s));
   return HPLP_OK;
 }
 

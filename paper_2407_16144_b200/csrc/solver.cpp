@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <limits>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -415,9 +416,18 @@ SolveResult Solver::solve(const SolverConfig& config) {
       rec.fixed_point_residual = p.trace_res;
       rec.kkt = kkt_of(p.trace_kkt);
       rec.candidate_norm_difference = p.trace_res;  // ||T(z) - z|| == ||z - T(z)||
-      rec.wall_seconds = since();
       Iterate z{Vector(static_cast<std::size_t>(n_)), Vector(static_cast<std::size_t>(m_))};
       check(ctx, hx_get_iterate(ctx, HX_ITERATE_LAST, z.x.data(), z.y.data()));
+      // partition estimate from the reduced costs c + A^T y and the
+      // normalized candidate's norm (src/solver.cpp:279-287), on the LP the
+      // loop iterates (the scaled one when preconditioned)
+      Vector aty(static_cast<std::size_t>(n_)), cdev(static_cast<std::size_t>(n_));
+      double cnn = std::numeric_limits<double>::quiet_NaN();
+      check(ctx, hx_trace_extras(ctx, aty.data(), cdev.data(), &cnn));
+      for (std::size_t j = 0; j < aty.size(); ++j) aty[j] = cdev[j] + aty[j];
+      rec.partition = partition_estimate_from_reduced_costs(z, aty, config.tol_active, sigma_used);
+      rec.candidate_norm_normalized = cnn;
+      rec.wall_seconds = since();
       unscale(z.x, z.y);
       config.trace_sink(rec, z);
     }
@@ -475,6 +485,21 @@ SolveResult Solver::solve(const SolverConfig& config) {
   out.totals = {static_cast<long>(p.it), n_spmv + static_cast<long>(p.spmv_count) + extra_spmv, since(), eta,
                 sigma_used};
   return out;
+}
+
+// src/diagnostics.cpp:26-43
+PartitionEstimate partition_estimate_from_reduced_costs(const Iterate& z, const Vector& reduced_costs,
+                                                        double tol_active, double sigma_estimate) {
+  PartitionEstimate p;
+  p.tol_active = tol_active;
+  const double r_tol = tol_active * sigma_estimate;
+  for (std::size_t i = 0; i < reduced_costs.size(); ++i) {
+    const double r = reduced_costs[i];
+    if (r > r_tol) p.n_set.push_back(static_cast<Index>(i));
+    else if (std::abs(r) <= r_tol && z.x[i] > tol_active) p.b1_set.push_back(static_cast<Index>(i));
+    else p.b2_set.push_back(static_cast<Index>(i));
+  }
+  return p;
 }
 
 SolveResult solve(const StandardFormLP& lp, const SolverConfig& config) {

@@ -71,6 +71,16 @@ def lib() -> C.CDLL:
     sig("hplp_solver_team_export", C.c_int, V, C.c_char_p, I64, PI64)
     sig("hplp_solver_team_import", C.c_int, V, C.c_char_p, I64)
     sig("hplp_plan_partition", C.c_int, I64, I64, PI64, PI32, I32, PI64, PI64)
+    # MPS ingestion + reports (inc/hplp/mps_io.hpp)
+    sig("hplp_mps_parse", C.c_int, C.c_char_p, PV, PI64, PI64, PI64)
+    sig("hplp_mps_view", C.c_int, V, C.POINTER(abi.General))
+    sig("hplp_mps_names", C.c_int, V, I32, C.c_char_p, I64, PI64)
+    sig("hplp_mps_write", C.c_int, V, C.c_char_p, I64, PI64)
+    sig("hplp_mps_from_general", C.c_int, C.POINTER(abi.General), C.c_char_p, I64, PI64)
+    sig("hplp_mps_free", None, V)
+    sig("hplp_solve_mps", C.c_int, I32, C.c_char_p, C.POINTER(abi.Config), C.c_char_p, I64, C.c_char_p, I64, PI64,
+        C.c_char_p, I64, PI64, PI32)
+    sig("hplp_json_normalize", C.c_int, C.c_char_p, I32, C.c_char_p, I64, PI64)
     sig("hplp_solver_hx", V, V)
     sig("hplp_solver_free", None, V)
     sig("hplp_to_standard_form", C.c_int, C.POINTER(abi.General), PV, PI64, PI64, PI64)
@@ -112,11 +122,24 @@ def lib() -> C.CDLL:
     return L
 
 
+class MpsParseError(ValueError):
+    """MpsParseError of inc/hplp/mps_io.hpp:29-39 (message starts "line N: ")."""
+
+    def __init__(self, msg: str):
+        super().__init__(msg)
+        try:
+            self.line = int(msg.split(":", 1)[0].split()[1])
+        except (IndexError, ValueError):
+            self.line = -1
+
+
 def _check(rc: int, ctx=None) -> None:
     if rc == 0:
         return
     L = lib()
     msg = (L.hx_last_error(ctx) if ctx is not None else L.hplp_last_error()).decode()
+    if rc == abi.HPLP_EPARSE:
+        raise MpsParseError(msg)
     if rc == abi.HPLP_EINVAL:
         raise ValueError(msg)
     if rc == abi.HPLP_EDOMAIN:
@@ -198,7 +221,7 @@ def _io(m, n, init, trace, epochs_capacity):
         r = rec.contents
         recs.append(dict(epoch=r.epoch, inner=r.inner, iteration=r.iteration, res=r.fixed_point_residual,
                          kkt=r.kkt.as_tuple(), cand_norm_normalized=r.candidate_norm_normalized,
-                         cand_norm_difference=r.candidate_norm_difference,
+                         cand_norm_difference=r.candidate_norm_difference, partition=abi.trace_partition(r),
                          x=np.ctypeslib.as_array(xp, (nn,)).copy(), y=np.ctypeslib.as_array(yp, (mm,)).copy()))
 
     cb = abi.TRACE_FN(sink) if trace else abi.TRACE_FN()
@@ -539,6 +562,111 @@ def team_run(hxs, max_iters):
 def team_bind(hxs):
     arr = (C.c_void_p * len(hxs))(*[h.h.value for h in hxs])
     _check(lib().hx_team_bind(arr, len(hxs)), hxs[0].h)
+
+
+def _text(call) -> str:
+    """Two-call text protocol of the C ABI: size, then fill."""
+    size = C.c_int64()
+    _check(call(None, 0, C.byref(size)))
+    buf = C.create_string_buffer(size.value + 1)
+    _check(call(buf, size.value + 1, C.byref(size)))
+    return buf.value.decode()
+
+
+class MpsProblem:
+    """parse_mps result (inc/hplp/mps_io.hpp:54-57): the GeneralFormLP as a
+    CSR-with-bounds problem plus the document metadata."""
+
+    def __init__(self, text: str):
+        L = lib()
+        h, m, n, nnz = C.c_void_p(), C.c_int64(), C.c_int64(), C.c_int64()
+        _check(L.hplp_mps_parse(text.encode(), C.byref(h), C.byref(m), C.byref(n), C.byref(nnz)))
+        self.h = h
+        self.m, self.n, self.nnz = m.value, n.value, nnz.value
+
+    def _names(self, what):
+        return _text(lambda b, c, sz: lib().hplp_mps_names(self.h, what, b, c, sz))
+
+    @property
+    def name(self) -> str:
+        return self._names(0)
+
+    @property
+    def objective_name(self) -> str:
+        return self._names(1)
+
+    @property
+    def warnings(self) -> list:
+        return [w for w in self._names(2).split("\n") if w]
+
+    @property
+    def row_names(self) -> list:
+        return self._names(3).split("\n")[: self.m]
+
+    @property
+    def col_names(self) -> list:
+        return self._names(4).split("\n")[: self.n]
+
+    def general(self):
+        """The problem as gen.GeneralLP (numpy copies)."""
+        from .gen import GeneralLP
+
+        v = abi.General()
+        _check(lib().hplp_mps_view(self.h, C.byref(v)))
+        arr = lambda p, k, dt: np.ctypeslib.as_array(p, (k,)).astype(dt, copy=True) if k else np.zeros(0, dt)  # noqa
+        return GeneralLP(m=v.m, n=v.n, row_ptr=arr(v.row_ptr, v.m + 1, np.int64), col_idx=arr(v.col_idx, v.nnz, np.int32),
+                         val=arr(v.val, v.nnz, np.float64), row_relation=arr(v.row_relation, v.m, np.int32),
+                         row_rhs=arr(v.row_rhs, v.m, np.float64), col_lower=arr(v.col_lower, v.n, np.float64),
+                         col_upper=arr(v.col_upper, v.n, np.float64), objective=arr(v.objective, v.n, np.float64),
+                         row_range=arr(v.row_range, v.m, np.float64), maximize=bool(v.maximize),
+                         objective_constant=v.objective_constant)
+
+    def write(self) -> str:
+        """write_mps: normalized free MPS."""
+        return _text(lambda b, c, sz: lib().hplp_mps_write(self.h, b, c, sz))
+
+    def __del__(self):
+        try:
+            lib().hplp_mps_free(self.h)
+        except Exception:
+            pass
+
+
+def parse_mps(text: str) -> MpsProblem:
+    return MpsProblem(text)
+
+
+def mps_from_general(general) -> str:
+    """write_mps of a gen.GeneralLP (rows R<i>, columns C<j>)."""
+    ga = general.as_abi()
+    return _text(lambda b, c, sz: lib().hplp_mps_from_general(C.byref(ga), b, c, sz))
+
+
+def solve_mps(text: str, config=None, device: int = 0, instance: str | None = None, elide_above: int = -1, **kw):
+    """cmd_solve (SPEC.md [MODULE] cli): MPS text -> GPU solve -> (report
+    JSON text, trace CSV text, status string)."""
+    cfg = _config(config, False, kw)
+    L = lib()
+    args = [device, text.encode(), C.byref(cfg), instance.encode() if instance else None, int(elide_above)]
+    js, ts, st = C.c_int64(), C.c_int64(), C.c_int32()
+    jcap, tcap = 1 << 16, 1 << 12
+    n_guess = text.count("\n")
+    jcap += 64 * n_guess
+    if cfg.trace_period > 0:
+        tcap += 400 * (cfg.iteration_limit // cfg.trace_period + 2)
+    while True:  # report sizes are known only after the solve: retry once if too small
+        jb, tb = C.create_string_buffer(jcap), C.create_string_buffer(tcap)
+        rc = L.hplp_solve_mps(*args, jb, jcap, C.byref(js), tb, tcap, C.byref(ts), C.byref(st))
+        if rc == abi.HPLP_EINVAL and (js.value + 1 > jcap or ts.value + 1 > tcap):
+            jcap, tcap = max(jcap, js.value + 1), max(tcap, ts.value + 1)
+            continue
+        _check(rc)
+        return jb.value.decode(), tb.value.decode(), abi.STATUS_NAMES[st.value]
+
+
+def json_normalize(text: str, include_timing: bool = True) -> str:
+    """parse_solution_json then write_solution_json."""
+    return _text(lambda b, c, sz: lib().hplp_json_normalize(text.encode(), int(include_timing), b, c, sz))
 
 
 ITERATE_CURRENT, ITERATE_BEST, ITERATE_NEXT, ITERATE_LAST = range(4)

@@ -224,3 +224,25 @@ def test_invalid_inputs_raise(gpu_required):
     m, n, rp, ci, v = _csr([[(0, 1.0)]], 1, 1)
     with pytest.raises(ValueError):
         hplp.solve(m, n, rp, ci, v, np.array([1.0]), np.array([0.0]), tolerance=0.0)
+
+
+def test_trace_diagnostics_parity(gpu_required):
+    """TraceRecord's partition estimate and normalized-candidate norm
+    (src/solver.cpp:279-287) from the device path equal the oracle's: sets
+    identical (a reduced cost within rounding of the tol*sigma threshold may
+    flip one index), norms to 1e-9 relative."""
+    g, s = std("cfg1_small")
+    kw = dict(iteration_limit=100, tolerance=1e-12, trace=True)
+    cpu = CpuLp("port", *csr_args(s)).solve(**kw)
+    gpu = hplp.solve(*csr_args(s), **kw)
+    flips = 0
+    for tg, tc in zip(gpu["trace"], cpu["trace"]):
+        for u, v in zip(tg["partition"], tc["partition"]):
+            flips += len(np.setxor1d(u, v))
+        a, b = tg["cand_norm_normalized"], tc["cand_norm_normalized"]
+        if tc["inner"] == 0:
+            assert np.isnan(a) and np.isnan(b)
+        else:
+            assert abs(a - b) <= 1e-9 * max(abs(b), 1e-300), (tc["iteration"], a, b)
+        assert sum(len(p) for p in tg["partition"]) == s.n
+    assert flips <= 2
