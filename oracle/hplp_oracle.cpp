@@ -592,6 +592,195 @@ void solve(const Lp& lp, const hplp_config_t& cfg, hplp_io_t* io, hplp_result_t*
   }
 }
 
+// solve_baseline: src/solver.cpp:344-509 (mode 0 vanilla, 1 averaged, 2
+// restarted average) and update_average (src/baselines.cpp:20-31).
+void solve_baseline(const Lp& lp, const hplp_config_t& cfg, int mode, hplp_io_t* io, hplp_result_t* out) {
+  const auto t0 = Clock::now();
+  auto since = [&] { return std::chrono::duration<double>(Clock::now() - t0).count(); };
+  validate_config(cfg);
+  const Power pi = power_iteration(lp.a, 1e-4, 5000, cfg.seed);
+  const double sigma_used = pi.sigma * (1.0 + 1e-4);
+  int64_t n_spmv = 2 * pi.iterations;
+  double eta;
+  if (cfg.has_eta_override) eta = step_size(cfg.eta_override, sigma_used);
+  else eta = sigma_used <= 0.0 ? step_size(1.0, 0.0) : step_size(1.0 / (2.0 * sigma_used), sigma_used);
+  const bool averaged = mode != 0, restarted = mode == 2;
+  const int64_t m = lp.a.rows, n = lp.a.cols;
+  Vec x(static_cast<std::size_t>(n), 0.0), y(static_cast<std::size_t>(m), 0.0);
+  if (io && io->init_x && io->init_y) {
+    x.assign(io->init_x, io->init_x + n);
+    y.assign(io->init_y, io->init_y + m);
+  }
+  Vec a_x = spmv(lp.a, x);
+  ++n_spmv;
+  Vec mx, my, a_x_avg, at_y_avg;  // running mean (z-bar) and its products
+  int64_t count = 0;
+  bool ready = false;
+  int64_t ep = 0, k = 0, it = 0;
+  double res_epoch_start = 0.0;
+  std::vector<Epoch> epochs;
+  double best_kkt = kInf;
+  Vec best_x = x, best_y = y;
+  Kkt best_err;
+  Cert primal, dual;
+  auto finish = [&](int status, const Vec& fx, const Vec& fy, const Kkt& e) {
+    std::memset(out, 0, sizeof(*out));
+    out->status = status;
+    if (!epochs.empty() && epochs.back().len == 0) epochs.back().len = k;
+    out->iterations = it;
+    out->spmv_count = n_spmv;
+    out->wall_seconds = since();
+    out->eta = eta;
+    out->sigma_estimate = sigma_used;
+    out->final_kkt = {e.p, e.d, e.g, e.max};
+    out->n_epochs = static_cast<int64_t>(epochs.size());
+    auto put_cert = [&](const Cert& c, hplp_cert_meta_t* meta, double* dst) {
+      if (!c.present) return;
+      meta->present = 1;
+      meta->source = c.source;
+      meta->orientation = c.orientation;
+      meta->at_iteration = c.at;
+      meta->residual = c.residual;
+      meta->margin = c.margin;
+      if (dst) std::copy(c.vec.begin(), c.vec.end(), dst);
+    };
+    put_cert(primal, &out->primal_cert, io ? io->primal_cert : nullptr);
+    put_cert(dual, &out->dual_cert, io ? io->dual_cert : nullptr);
+    if (io) {
+      if (io->x) std::copy(fx.begin(), fx.end(), io->x);
+      if (io->y) std::copy(fy.begin(), fy.end(), io->y);
+      if (io->epochs)
+        for (std::size_t e2 = 0; e2 < epochs.size() && static_cast<int64_t>(e2) < io->epochs_capacity; ++e2)
+          io->epochs[e2] = {epochs[e2].epoch, epochs[e2].len, epochs[e2].res,
+                            {epochs[e2].kkt.p, epochs[e2].kkt.d, epochs[e2].kkt.g, epochs[e2].kkt.max}};
+    }
+  };
+  while (true) {
+    if (it >= cfg.iteration_limit || since() > cfg.time_limit_seconds) {  // :387-399
+      const int status = it >= cfg.iteration_limit ? HPLP_STATUS_ITERATION_LIMIT : HPLP_STATUS_TIME_LIMIT;
+      if (std::isfinite(best_kkt)) {
+        finish(status, best_x, best_y, best_err);
+      } else {
+        finish(status, x, y, kkt(x, y, lp, spmv(lp.a, x), spmv_t(lp.a, y)));
+        out->spmv_count += 2;
+      }
+      return;
+    }
+    Step sr = pdhg_step(x, y, lp, eta, a_x);  // :401-402
+    n_spmv += 2;
+    if (averaged) {  // :404-416
+      if (!ready) {
+        mx = x, my = y, count = 1;
+        a_x_avg = a_x;
+        at_y_avg = sr.at_y;
+        ready = true;
+      } else {
+        const double w = 1.0 / static_cast<double>(count + 1);
+        for (int64_t j = 0; j < n; ++j) mx[j] += w * (x[j] - mx[j]);
+        for (int64_t i = 0; i < m; ++i) my[i] += w * (y[i] - my[i]);
+        count += 1;
+        const double w2 = 1.0 / static_cast<double>(count);
+        for (int64_t i = 0; i < m; ++i) a_x_avg[i] += w2 * (a_x[i] - a_x_avg[i]);
+        for (int64_t j = 0; j < n; ++j) at_y_avg[j] += w2 * (sr.at_y[j] - at_y_avg[j]);
+      }
+    }
+    const Vec& cx = averaged ? mx : x;
+    const Vec& cy = averaged ? my : y;
+    const Kkt e = averaged ? kkt(mx, my, lp, a_x_avg, at_y_avg) : kkt(x, y, lp, a_x, sr.at_y);  // :418-421
+    const bool tracing = cfg.trace_period > 0 && it % cfg.trace_period == 0 && io && io->trace_fn;
+    double res;
+    if (averaged && (restarted || tracing || k == 0)) {  // :424-433
+      Step as = pdhg_step(mx, my, lp, eta, a_x_avg);
+      n_spmv += 2;
+      res = canonical(sub(mx, as.x), sub(my, as.y), sub(a_x_avg, as.a_x_next), eta);
+    } else if (!averaged) {
+      res = canonical(sub(x, sr.x), sub(y, sr.y), sub(a_x, sr.a_x_next), eta);
+    } else {
+      res = std::numeric_limits<double>::quiet_NaN();
+    }
+    if (k == 0) {  // :434-437
+      res_epoch_start = res;
+      epochs.push_back({ep, 0, res, e});
+    }
+    if (e.max < best_kkt) {  // :438-442
+      best_kkt = e.max;
+      best_x = cx;
+      best_y = cy;
+      best_err = e;
+    }
+    if (tracing) {  // :444-460
+      hplp_trace_t t;
+      t.epoch = ep;
+      t.inner = k;
+      t.iteration = it;
+      t.fixed_point_residual = res;
+      t.kkt = {e.p, e.d, e.g, e.max};
+      t.candidate_norm_difference = canonical(sub(sr.x, x), sub(sr.y, y), sub(sr.a_x_next, a_x), eta);
+      t.candidate_norm_normalized = std::numeric_limits<double>::quiet_NaN();
+      t.wall_seconds = since();
+      std::vector<int64_t> pn, pb1, pb2;
+      const double r_tol = cfg.tol_active * sigma_used;
+      const Vec& aty = averaged ? at_y_avg : sr.at_y;
+      for (int64_t j = 0; j < n; ++j) {
+        const double r = lp.c[j] + aty[j];
+        if (r > r_tol) pn.push_back(j);
+        else if (std::abs(r) <= r_tol && cx[j] > cfg.tol_active) pb1.push_back(j);
+        else pb2.push_back(j);
+      }
+      t.partition_n = static_cast<int64_t>(pn.size());
+      t.partition_b1 = static_cast<int64_t>(pb1.size());
+      t.partition_b2 = static_cast<int64_t>(pb2.size());
+      pn.insert(pn.end(), pb1.begin(), pb1.end());
+      pn.insert(pn.end(), pb2.begin(), pb2.end());
+      t.partition_sets = pn.data();
+      io->trace_fn(&t, cx.data(), n, cy.data(), m, io->trace_user);
+    }
+    if (e.max <= cfg.tolerance) {  // :462-465
+      finish(HPLP_STATUS_OPTIMAL, cx, cy, e);
+      return;
+    }
+    if (cfg.infeasibility_check_period > 0 && it > 0 && it % cfg.infeasibility_check_period == 0) {  // :467-481
+      const Vec vx = sub(sr.x, x), vy = sub(sr.y, y);
+      if (norm(vy) > 0.0) {
+        Farkas f = validate_primal(vy, lp, cfg.certificate_tolerance, sigma_used);
+        ++n_spmv;
+        if (f.valid) primal = make_cert(vy, HPLP_SOURCE_ITERATE_DIFFERENCE, it, f);
+      }
+      if (norm(vx) > 0.0) {
+        Farkas f = validate_dual(vx, lp, cfg.certificate_tolerance, sigma_used);
+        ++n_spmv;
+        if (f.valid) dual = make_cert(vx, HPLP_SOURCE_ITERATE_DIFFERENCE, it, f);
+      }
+      if (primal.present || dual.present) {
+        const int status = primal.present && dual.present ? HPLP_STATUS_PRIMAL_DUAL_INFEASIBLE
+                           : primal.present               ? HPLP_STATUS_PRIMAL_INFEASIBLE
+                                                          : HPLP_STATUS_DUAL_INFEASIBLE;
+        finish(status, cx, cy, e);
+        return;
+      }
+    }
+    bool restart = restarted && should_restart(cfg, ep, k, res, res_epoch_start);  // :483-489
+    if (restarted && !restart && cfg.restart_kind == HPLP_RESTART_ADAPTIVE && cfg.adaptive_stall_cap > 0 &&
+        k >= cfg.adaptive_stall_cap)
+      restart = true;
+    if (restart) {  // :490-500
+      epochs.back().len = k;
+      x = mx, y = my;
+      a_x = a_x_avg;
+      count = 0;
+      ready = false;
+      ++ep;
+      k = 0;
+    } else {
+      x = std::move(sr.x);
+      y = std::move(sr.y);
+      a_x = std::move(sr.a_x_next);
+      ++k;
+    }
+    ++it;
+  }
+}
+
 // ---- to_standard_form: src/lp_model.cpp:155-325 ----------------------------
 struct StdForm {
   Lp lp;
@@ -902,6 +1091,13 @@ int orc_should_restart(int32_t kind, int64_t k_star, double beta, int64_t tau0, 
 
 int orc_lp_solve(void* h, const hplp_config_t* cfg, hplp_io_t* io, hplp_result_t* res) {
   return guarded([&] { orc::solve(*static_cast<orc::Lp*>(h), *cfg, io, res); });
+}
+
+int orc_lp_solve_baseline(void* h, int32_t mode, const hplp_config_t* cfg, hplp_io_t* io, hplp_result_t* res) {
+  return guarded([&] {
+    if (mode < 0 || mode > 2) throw std::invalid_argument("solve_baseline: mode in 0..2");
+    orc::solve_baseline(*static_cast<orc::Lp*>(h), *cfg, mode, io, res);
+  });
 }
 
 int orc_to_standard_form(const hplp_general_t* g, void** out, int64_t* m_s, int64_t* n_s,

@@ -63,6 +63,7 @@ def load(kind: str = "port") -> C.CDLL:
     sig("validate_dual", C.c_int, V, PD, D, D, PD)
     sig("should_restart", C.c_int, I32, I64, D, I64, I64, I64, D, D)
     sig("lp_solve", C.c_int, V, C.POINTER(abi.Config), C.POINTER(abi.IO), C.POINTER(abi.Result))
+    sig("lp_solve_baseline", C.c_int, V, C.c_int32, C.POINTER(abi.Config), C.POINTER(abi.IO), C.POINTER(abi.Result))
     sig("to_standard_form", C.c_int, C.POINTER(abi.General), C.POINTER(V), PI64, PI64, PI64)
     sig("std_export", C.c_int, V, PI64, PI32, PD, PD, PD)
     sig("std_recover", C.c_int, V, PD, PD, D, PD)
@@ -171,7 +172,12 @@ class CpuLp:
     def should_restart(self, kind, n, k, res_now, res_start, k_star=0, beta=0.36787944117144233, tau0=32):
         return bool(_f(self.lib, "should_restart")(kind, k_star, beta, tau0, n, k, res_now, res_start))
 
-    def solve(self, config=None, init=None, trace=False, epochs_capacity=4096, **kw):
+    def solve_baseline(self, mode, config=None, init=None, trace=False, epochs_capacity=4096, **kw):
+        """solve_baseline() (src/solver.cpp:344-509): mode 0 vanilla PDHG, 1
+        averaged, 2 restarted average.  Same result dict as solve()."""
+        return self.solve(config, init, trace, epochs_capacity, _baseline=int(mode), **kw)
+
+    def solve(self, config=None, init=None, trace=False, epochs_capacity=4096, _baseline=-1, **kw):
         """solve() (src/solver.cpp:206-342).  Returns a dict with the result
         fields, final x/y, certificates, epochs and (trace=True) the per-
         iteration trace records with their iterates."""
@@ -200,7 +206,11 @@ class CpuLp:
             iy = np.ascontiguousarray(init[1], np.float64)
         io = abi.IO(dptr(ix), dptr(iy), dptr(x), dptr(y), dptr(pc), dptr(dc), eps, epochs_capacity, cb, None)
         res = abi.Result()
-        _chk(self.lib, _f(self.lib, "lp_solve")(self.h, C.byref(cfg), C.byref(io), C.byref(res)))
+        if _baseline < 0:
+            _chk(self.lib, _f(self.lib, "lp_solve")(self.h, C.byref(cfg), C.byref(io), C.byref(res)))
+        else:
+            _chk(self.lib, _f(self.lib, "lp_solve_baseline")(self.h, _baseline, C.byref(cfg), C.byref(io),
+                                                            C.byref(res)))
         ne = min(res.n_epochs, epochs_capacity)
         return dict(
             status=abi.STATUS_NAMES[res.status], status_code=res.status, iterations=res.iterations,

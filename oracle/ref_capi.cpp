@@ -245,7 +245,20 @@ const char* ref_status_string(int32_t status) {
   return hplp::to_string(static_cast<hplp::SolveStatus>(status));
 }
 
+int ref_lp_solve_impl(void* h, int32_t baseline, const hplp_config_t* cfg, hplp_io_t* io, hplp_result_t* res);
+
 int ref_lp_solve(void* h, const hplp_config_t* cfg, hplp_io_t* io, hplp_result_t* res) {
+  return ref_lp_solve_impl(h, -1, cfg, io, res);
+}
+
+// solve_baseline (src/solver.cpp:344-509): mode 0 vanilla, 1 averaged,
+// 2 restarted average.
+int ref_lp_solve_baseline(void* h, int32_t mode, const hplp_config_t* cfg, hplp_io_t* io, hplp_result_t* res) {
+  if (mode < 0 || mode > 2) return guarded([] { throw std::invalid_argument("solve_baseline: mode in 0..2"); });
+  return ref_lp_solve_impl(h, mode, cfg, io, res);
+}
+
+int ref_lp_solve_impl(void* h, int32_t baseline, const hplp_config_t* cfg, hplp_io_t* io, hplp_result_t* res) {
   return guarded([&] {
     const auto& lp = static_cast<RefLp*>(h)->lp;
     hplp::SolverConfig config = to_config(cfg);
@@ -273,7 +286,12 @@ int ref_lp_solve(void* h, const hplp_config_t* cfg, hplp_io_t* io, hplp_result_t
         io->trace_fn(&t, z.x.data(), z.x.size(), z.y.data(), z.y.size(), io->trace_user);
       };
     }
-    hplp::SolveResult r = hplp::solve(lp, config);
+    hplp::SolveResult r =
+        baseline < 0 ? hplp::solve(lp, config)
+                     : hplp::solve_baseline(lp, config,
+                                            baseline == 0   ? hplp::BaselineMode::kVanilla
+                                            : baseline == 1 ? hplp::BaselineMode::kAveraged
+                                                            : hplp::BaselineMode::kRestartedAverage);
     std::memset(res, 0, sizeof(*res));
     res->status = static_cast<int32_t>(r.status);
     res->iterations = r.totals.iterations;
