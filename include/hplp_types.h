@@ -69,9 +69,18 @@ typedef struct hplp_config {
    * preconditioning applied to the instance before the loop.  0 / -1 = off,
    * i.e. the reference's own semantics. */
   int32_t precondition_ruiz_iters;
-  int32_t reserved0;
+  /* Iteration scheme: HPLP_SCHEME_RHPDHG = solve() (src/solver.cpp:206-342);
+   * the others are solve_baseline(mode) (src/solver.cpp:344-509). */
+  int32_t scheme;
   double precondition_pc_alpha;
 } hplp_config_t;
+
+enum {
+  HPLP_SCHEME_RHPDHG = 0,
+  HPLP_SCHEME_VANILLA = 1,           /* BaselineMode::kVanilla */
+  HPLP_SCHEME_AVERAGED = 2,          /* BaselineMode::kAveraged */
+  HPLP_SCHEME_RESTARTED_AVERAGE = 3  /* BaselineMode::kRestartedAverage */
+};
 
 /* KktError, inc/pdhg_core.hpp:82-87. */
 typedef struct hplp_kkt {
@@ -190,7 +199,7 @@ static inline hplp_config_t hplp_config_default(void) {
   c.adaptive_stall_cap = 2000;
   c.seed = 12345u;
   c.precondition_ruiz_iters = 0;
-  c.reserved0 = 0;
+  c.scheme = HPLP_SCHEME_RHPDHG;
   c.precondition_pc_alpha = -1.0;
   return c;
 }

@@ -48,6 +48,8 @@ typedef struct hx_progress {
   hplp_cert_meta_t primal_cert, dual_cert;
   double device_ms;     /* CUDA-event time of the hx_run call */
   int64_t launches;     /* kernels launched by this call */
+  double trace_res_diff; /* ||T(z) - z|| of the last iteration (the candidate's residual differs for
+                            the averaged baselines) */
 } hx_progress_t;
 
 int hx_create(int32_t device, hx_ctx** out);

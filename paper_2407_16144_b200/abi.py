@@ -28,6 +28,7 @@ STATUS_NAMES = (
 SOURCE_NORMALIZED_ITERATE, SOURCE_ITERATE_DIFFERENCE = range(2)
 ORIENT_AS_IS, ORIENT_NEGATED = range(2)
 ROW_LE, ROW_EQ, ROW_GE = range(3)
+SCHEME_RHPDHG, SCHEME_VANILLA, SCHEME_AVERAGED, SCHEME_RESTARTED_AVERAGE = range(4)
 
 
 class Config(C.Structure):
@@ -50,7 +51,7 @@ class Config(C.Structure):
         ("adaptive_stall_cap", C.c_int64),
         ("seed", C.c_uint64),
         ("precondition_ruiz_iters", C.c_int32),
-        ("reserved0", C.c_int32),
+        ("scheme", C.c_int32),
         ("precondition_pc_alpha", C.c_double),
     ]
 
@@ -73,7 +74,7 @@ class Config(C.Structure):
             adaptive_stall_cap=2000,
             seed=12345,
             precondition_ruiz_iters=0,
-            reserved0=0,
+            scheme=0,
             precondition_pc_alpha=-1.0,
         )
         for k, v in kw.items():

@@ -233,6 +233,9 @@ struct SolverConfig {
   // final_kkt is the KKT error of the scaled instance the loop terminated on.
   int precondition_ruiz_iters = 0;
   double precondition_pc_alpha = -1.0;  // < 0: no Pock-Chambolle step
+  // Iteration scheme (HPLP_SCHEME_*): 0 = solve(); 1-3 = solve_baseline's
+  // modes (set by solve_baseline, or directly through the C ABI).
+  int scheme = 0;
 };
 
 // inc/solver.hpp:82-116
@@ -316,6 +319,11 @@ class Solver {
 
 // inc/solver.hpp:130 -- src/solver.cpp:206-342 on the GPU.
 SolveResult solve(const StandardFormLP& lp, const SolverConfig& config);
+
+// inc/solver.hpp:132-139 -- solve_baseline (src/solver.cpp:344-509) on the
+// GPU: vanilla PDHG, its running average, and the average restarted.
+enum class BaselineMode { kVanilla, kAveraged, kRestartedAverage };
+SolveResult solve_baseline(const StandardFormLP& lp, const SolverConfig& config, BaselineMode mode);
 
 // config <-> flat POD (include/hplp_types.h)
 SolverConfig from_pod(const hplp_config_t& c);

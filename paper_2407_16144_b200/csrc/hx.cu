@@ -69,6 +69,12 @@ struct Roles {
   double cand_scale; // 2/k for the normalized candidate
   double cn2[4];     // candidate l2 norms: 0 v_x diff, 1 v_y diff, 2 v_x norm, 3 v_y norm
   double pw_zn;
+  // baseline schemes (solve_baseline, src/solver.cpp:344-509): z may live in
+  // an average slot after a restart; the running average is updated from
+  // slot avg_cur into slot avg_out (avg_mode 1: copy z, 2: w-weighted update)
+  int x_src_avg, y_cur_avg, ax_cur_avg;
+  int avg_mode, avg_cur, avg_out, avg_step, pad3;
+  double w_avg;
 };
 
 // Controller state.  Lives in global memory between launches; during a
@@ -97,6 +103,15 @@ struct Ctl {
   double pw_tol, pw_sigma, pw_sigma_prev, pw_sigma_cur;
   int pw_converged, pw_redraw;
   unsigned long long team_epochs;  // cross-rank barriers passed so far (identical on every rank)
+  // baseline schemes
+  int scheme;          // HPLP_SCHEME_*
+  int avg_best;        // average slot holding the best candidate (-1: best is a z in the pools)
+  int final_avg;       // final iterate = average slot final_avg (>= 0)
+  int last_cand_avg;   // traced candidate = average slot (>= 0) or z (-1)
+  int last_y_avg;      // traced z's y lives in an average slot
+  int pad4;
+  long long avg_count; // iterates in the running average
+  double last_res_diff;  // ||T(z) - z|| of the last iteration (TraceRecord::candidate_norm_difference)
 };
 static_assert(sizeof(Ctl) % 8 == 0, "Ctl copied as 8-byte words");
 
@@ -162,7 +177,24 @@ struct KParams {
   hplp_epoch_t* epochs;  // ring of kEpochCap
   unsigned long long* prof;  // optional per-CTA phase timers [grid][8] (HX_PROFILE=1)
   Team T;                    // row partition + peers (loop_kernel_team only)
+  // baseline schemes (loop_kernel_baseline): kAvgPool slots each
+  double* xavg;   // n: mean x
+  double* tavg;   // n: mean A^T y
+  double* yavg;   // m: mean y
+  double* aavg;   // m: mean A x
+  double* xbar;   // n: x-part of the PDHG step taken at the average
 };
+
+// z's buffers: pool role, or an average slot after a baseline restart.
+__device__ __forceinline__ const double* xsrc_ptr(const KParams* P, const Roles* R) {
+  return (R->x_src_avg ? P->xavg : P->xpool) + static_cast<size_t>(R->x_src) * P->n;
+}
+__device__ __forceinline__ const double* ycur_ptr(const KParams* P, const Roles* R) {
+  return (R->y_cur_avg ? P->yavg : P->ypool) + static_cast<size_t>(R->y_cur) * P->m;
+}
+__device__ __forceinline__ const double* axcur_ptr(const KParams* P, const Roles* R) {
+  return (R->ax_cur_avg ? P->aavg : P->axpool) + static_cast<size_t>(R->ax_cur) * P->m;
+}
 
 // Where this CTA sits: its index among the CTAs of its rank (cta of nctas)
 // and its partial record among all ranks' records (rec of nrec).  Single GPU:
@@ -839,10 +871,12 @@ __device__ void set_final_limit(Ctl& C, int status) {
   if (C.best_kkt < INFINITY) {  // isfinite(best_kkt): it only ever decreases from +inf
     C.final_x = C.x_best;
     C.final_y = C.y_best;
+    C.final_avg = C.avg_best;  // averaged baselines: the best is an average slot
     for (int q = 0; q < 4; ++q) C.final_kkt[q] = C.best_err[q];
   } else {
     C.final_x = -1;  // host evaluates kkt_error(z) with fresh products
     C.final_y = -1;
+    C.final_avg = -1;
   }
   C.r.stop = 1;
 }
@@ -953,6 +987,7 @@ __device__ void main_logic(Ctl& C, const double* tot, const double* pre, hplp_ep
   C.last_n = C.n;
   C.last_k = C.k;
   C.last_res = res;
+  C.last_res_diff = res;  // ||T(z) - z|| == ||z - T(z)||
   for (int i = 0; i < 4; ++i) C.last_kkt[i] = kkt[i];
   C.last_zx = R.zx_out;
   C.last_xp = R.xp_out;
@@ -1038,6 +1073,8 @@ __device__ bool eval_dual(const Ctl& C, int c, hplp_cert_meta_t& rep) {
   return valid;
 }
 
+__device__ void finish_iteration_baseline(Ctl& C, hplp_epoch_t* epochs, bool writer, double res, bool time_up);
+
 // CertificateScan::check semantics, src/solver.cpp:108-135 (+ :300-317).
 // Candidates: 0 v_x diff, 1 v_y diff, 2 v_x normalized, 3 v_y normalized.
 __device__ void scan_logic(Ctl& C, hplp_epoch_t* epochs, bool writer, bool time_up) {
@@ -1045,7 +1082,7 @@ __device__ void scan_logic(Ctl& C, hplp_epoch_t* epochs, bool writer, bool time_
   hplp_cert_meta_t prim{}, dual{};
   bool have_p = false, have_d = false;
   for (int src = 0; src < 2; ++src) {  // difference first, then normalized
-    if (src == 1 && C.last_k < 1) break;
+    if (src == 1 && (C.last_k < 1 || C.scheme != HPLP_SCHEME_RHPDHG)) break;  // baselines: difference only
     const int cy = src == 0 ? 1 : 3, cx = src == 0 ? 0 : 2;
     const int source = src == 0 ? HPLP_SOURCE_ITERATE_DIFFERENCE : HPLP_SOURCE_NORMALIZED_ITERATE;
     if (!have_p && R.cn2[cy] > 0.0) {
@@ -1081,12 +1118,14 @@ __device__ void scan_logic(Ctl& C, hplp_epoch_t* epochs, bool writer, bool time_
                                 : HPLP_STATUS_DUAL_INFEASIBLE;
     C.final_x = C.last_zx;
     C.final_y = C.last_y;
+    C.final_avg = C.last_cand_avg;  // baselines return the candidate (the average when averaged)
     for (int i = 0; i < 4; ++i) C.final_kkt[i] = C.last_kkt[i];
     R.stop = 1;
     if (C.trace_period > 0 && C.last_it % C.trace_period == 0) C.paused = 1;
     return;
   }
-  finish_iteration(C, epochs, writer, C.last_res, time_up);
+  if (C.scheme != HPLP_SCHEME_RHPDHG) finish_iteration_baseline(C, epochs, writer, C.last_res, time_up);
+  else finish_iteration(C, epochs, writer, C.last_res, time_up);
 }
 
 // Roles of phase A for iteration it+1 assuming no restart and no stop
@@ -1142,7 +1181,7 @@ __device__ HX_PHASE_INLINE void phase_primal(const KParams* P, const Roles* R, i
   const int n = P->n, m = P->m;
   double acc[3];
   acc_init<3, 0>(acc);
-  EpiPrimal<RK> e{P->xpool + static_cast<size_t>(R->x_src) * n,
+  EpiPrimal<RK> e{xsrc_ptr(P, R),
               P->xpool + static_cast<size_t>(R->x_anchor) * n,
               P->c,
               P->xpool + static_cast<size_t>(R->zx_out) * n,
@@ -1156,7 +1195,7 @@ __device__ HX_PHASE_INLINE void phase_primal(const KParams* P, const Roles* R, i
 #ifdef HX_WPROF
   const unsigned long long w0 = clock64();
 #endif
-  spmv_rows<3, 0>(S, par, SrcVec{P->ypool + static_cast<size_t>(R->y_cur) * m}, e, acc, gwarp_id(g),
+  spmv_rows<3, 0>(S, par, SrcVec{ycur_ptr(P, R)}, e, acc, gwarp_id(g),
                   threadIdx.x & 31, stage, seq, head);
 #ifdef HX_WPROF
   if constexpr (!RK)
@@ -1173,8 +1212,8 @@ __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int
   const int n = P->n, m = P->m;
   double acc[4];
   acc_init<4, 0>(acc);
-  EpiDual<RK> e{P->ypool + static_cast<size_t>(R->y_cur) * m,
-            P->axpool + static_cast<size_t>(R->ax_cur) * m,
+  EpiDual<RK> e{ycur_ptr(P, R),
+            axcur_ptr(P, R),
             P->b,
             P->ypool + static_cast<size_t>(R->y_anchor) * m,
             P->axpool + static_cast<size_t>(R->ax_anchor) * m,
@@ -1280,7 +1319,7 @@ __device__ HX_PHASE_INLINE void cert_norms(const KParams* P, const Roles* R, con
   const double* zx = P->xpool + static_cast<size_t>(R->zx_out) * n;
   const double* xp = P->xpool + static_cast<size_t>(R->xp_out) * n;
   const double* xa = P->xpool + static_cast<size_t>(R->x_anchor) * n;
-  const double* yc = P->ypool + static_cast<size_t>(R->y_cur) * m;
+  const double* yc = ycur_ptr(P, R);
   const double* yp = P->ypool + static_cast<size_t>(R->yp_out) * m;
   const double* ya = P->ypool + static_cast<size_t>(R->y_anchor) * m;
   double acc[8];
@@ -1323,7 +1362,7 @@ __device__ HX_PHASE_INLINE void cert_units(const KParams* P, const Roles* R, con
   const double* zx = P->xpool + static_cast<size_t>(R->zx_out) * n;
   const double* xp = P->xpool + static_cast<size_t>(R->xp_out) * n;
   const double* xa = P->xpool + static_cast<size_t>(R->x_anchor) * n;
-  const double* yc = P->ypool + static_cast<size_t>(R->y_cur) * m;
+  const double* yc = ycur_ptr(P, R);
   const double* yp = P->ypool + static_cast<size_t>(R->yp_out) * m;
   const double* ya = P->ypool + static_cast<size_t>(R->y_anchor) * m;
   double acc[12];
@@ -1401,6 +1440,464 @@ __device__ HX_PHASE_INLINE void cert_products(const KParams* P, const Roles* R, 
     }
   }
   block_to_slots<6, 0x3Fu, RK>(acc, P, kRegC3, g);
+}
+
+// ---------------------------------------------------------------------------
+// Baseline schemes: solve_baseline (src/solver.cpp:344-509) on the device.
+// Vanilla PDHG runs the same fused phases as rHPDHG with z <- T(z) roles;
+// the averaged schemes fold the running average (update_average,
+// src/baselines.cpp:20-31, and the products' means, solver.cpp:404-416) into
+// the phase epilogues out of place (average slot avg_cur -> avg_out), so the
+// KKT at the average (solver.cpp:418-421) needs no extra pass; the residual
+// at the average (restarted average every iteration, averaged at epoch
+// starts and traced iterations, :424-433) takes two more fused phases: the
+// PDHG step at the average.  One thread-0 controller per CTA, replicated as
+// in the main loop; no speculation (phase A follows the controller).
+// ---------------------------------------------------------------------------
+struct EpiPrimalAvg {  // phase A + average update of x and A^T y
+  const double* xs;
+  const double* c;
+  double* zx;
+  double* xp;
+  const double* xa_in;
+  const double* ta_in;
+  double* xa_out;
+  double* ta_out;
+  double eta, w;
+  int copy;
+  struct In {
+    double xs, c, xa, ta;
+  };
+  __device__ __forceinline__ In load(int j) const {
+    return In{ldcg(xs + j), __ldg(c + j), copy ? 0.0 : ldcg(xa_in + j), copy ? 0.0 : ldcg(ta_in + j)};
+  }
+  __device__ __forceinline__ void apply(int j, double aty, const In& in, double (&t)[3]) const {
+    const double x = in.xs;
+    zx[j] = x;
+    double xn = x - eta * (aty + in.c);
+    xn = xn < 0.0 ? 0.0 : xn;
+    xp[j] = xn;
+    const double xa = copy ? x : in.xa + w * (x - in.xa);
+    const double ta = copy ? aty : in.ta + w * (aty - in.ta);
+    xa_out[j] = xa;
+    ta_out[j] = ta;
+    double rc = -(in.c + ta);  // dual residual at the average
+    rc = rc < 0.0 ? 0.0 : rc;
+    const double dx = x - xn;
+    t[0] = rc * rc;
+    t[1] = in.c * xa;
+    t[2] = dx * dx;
+  }
+};
+
+struct EpiDualAvg {  // phase B + average update of y and A x
+  const double* y;
+  const double* ax;
+  const double* b;
+  double* yp;
+  double* axp;
+  const double* ya_in;
+  const double* aa_in;
+  double* ya_out;
+  double* aa_out;
+  double eta, w;
+  int copy;
+  struct In {
+    double y, ax, b, ya, aa;
+  };
+  __device__ __forceinline__ In load(int i) const {
+    return In{ldcg(y + i), ldcg(ax + i), __ldg(b + i), copy ? 0.0 : ldcg(ya_in + i), copy ? 0.0 : ldcg(aa_in + i)};
+  }
+  __device__ __forceinline__ void apply(int i, double s, const In& in, double (&t)[4]) const {
+    const double ypi = in.y + eta * ((2.0 * s - in.ax) - in.b);
+    yp[i] = ypi;
+    axp[i] = s;
+    const double ya = copy ? in.y : in.ya + w * (in.y - in.ya);
+    const double aa = copy ? in.ax : in.aa + w * (in.ax - in.aa);
+    ya_out[i] = ya;
+    aa_out[i] = aa;
+    const double d = aa - in.b;  // primal residual at the average
+    const double dy = in.y - ypi;
+    const double dax = in.ax - s;
+    t[0] = d * d;
+    t[1] = in.b * ya;
+    t[2] = dy * dy;
+    t[3] = dy * dax;
+  }
+};
+
+struct EpiAvgStepPrimal {  // PDHG step at the average, primal half
+  const double* xa;
+  const double* c;
+  double* xbar;
+  double eta;
+  struct In {
+    double xa, c;
+  };
+  __device__ __forceinline__ In load(int j) const { return In{ldcg(xa + j), __ldg(c + j)}; }
+  __device__ __forceinline__ void apply(int j, double at, const In& in, double (&t)[1]) const {
+    double xn = in.xa - eta * (at + in.c);
+    xn = xn < 0.0 ? 0.0 : xn;
+    xbar[j] = xn;
+    const double d = in.xa - xn;
+    t[0] = d * d;
+  }
+};
+
+struct EpiAvgStepDual {  // PDHG step at the average, dual half (products only)
+  const double* ya;
+  const double* aa;
+  const double* b;
+  double eta;
+  struct In {
+    double ya, aa, b;
+  };
+  __device__ __forceinline__ In load(int i) const { return In{ldcg(ya + i), ldcg(aa + i), __ldg(b + i)}; }
+  __device__ __forceinline__ void apply(int, double s, const In& in, double (&t)[2]) const {
+    const double ypn = in.ya + eta * ((2.0 * s - in.aa) - in.b);
+    const double dy = in.ya - ypn;
+    const double dax = in.aa - s;
+    t[0] = dy * dy;
+    t[1] = dy * dax;
+  }
+};
+
+__device__ HX_PHASE_INLINE void phase_primal_avg(const KParams* P, const Roles* R, int par, WarpStage* stage,
+                                                 unsigned long long seq, const SpmvHead& head, const Geo& g) {
+  const int n = P->n;
+  double acc[3];
+  acc_init<3, 0>(acc);
+  const int cur = R->avg_cur < 0 ? 0 : R->avg_cur;
+  EpiPrimalAvg e{xsrc_ptr(P, R),
+                 P->c,
+                 P->xpool + static_cast<size_t>(R->zx_out) * n,
+                 P->xpool + static_cast<size_t>(R->xp_out) * n,
+                 P->xavg + static_cast<size_t>(cur) * n,
+                 P->tavg + static_cast<size_t>(cur) * n,
+                 P->xavg + static_cast<size_t>(R->avg_out) * n,
+                 P->tavg + static_cast<size_t>(R->avg_out) * n,
+                 R->eta,
+                 R->w_avg,
+                 R->avg_mode == 1};
+  spmv_rows<3, 0>(P->AT, par, SrcVec{ycur_ptr(P, R)}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq, head);
+  fold_long<3, 0>(P->AT, par, seq, acc, g.cta);
+  block_to_slots<3, 0, false>(acc, P, kRegA + par, g);
+}
+
+__device__ HX_PHASE_INLINE void phase_dual_avg(const KParams* P, const Roles* R, int par, WarpStage* stage,
+                                               unsigned long long seq, const SpmvHead& head, const Geo& g) {
+  const int n = P->n, m = P->m;
+  double acc[4];
+  acc_init<4, 0>(acc);
+  const int cur = R->avg_cur < 0 ? 0 : R->avg_cur;
+  EpiDualAvg e{ycur_ptr(P, R),
+               axcur_ptr(P, R),
+               P->b,
+               P->ypool + static_cast<size_t>(R->yp_out) * m,
+               P->axpool + static_cast<size_t>(R->axp_out) * m,
+               P->yavg + static_cast<size_t>(cur) * m,
+               P->aavg + static_cast<size_t>(cur) * m,
+               P->yavg + static_cast<size_t>(R->avg_out) * m,
+               P->aavg + static_cast<size_t>(R->avg_out) * m,
+               R->eta,
+               R->w_avg,
+               R->avg_mode == 1};
+  spmv_rows<4, 0>(P->A, par, SrcVec{P->xpool + static_cast<size_t>(R->xp_out) * n}, e, acc, gwarp_id(g),
+                  threadIdx.x & 31, stage, seq, head);
+  fold_long<4, 0>(P->A, par, seq, acc, g.cta);
+  block_to_slots<4, 0, false>(acc, P, kRegB + par, g);
+}
+
+__device__ HX_PHASE_INLINE void phase_avgstep_a(const KParams* P, const Roles* R, WarpStage* stage,
+                                                unsigned long long seq, const Geo& g) {
+  const int n = P->n, m = P->m;
+  double acc[1];
+  acc_init<1, 0>(acc);
+  EpiAvgStepPrimal e{P->xavg + static_cast<size_t>(R->avg_out) * n, P->c, P->xbar, R->eta};
+  spmv_rows<1, 0>(P->AT, 0, SrcVec{P->yavg + static_cast<size_t>(R->avg_out) * m}, e, acc, gwarp_id(g),
+                  threadIdx.x & 31, stage, seq);
+  fold_long<1, 0>(P->AT, 0, seq, acc, g.cta);
+  block_to_slots<1, 0, false>(acc, P, kRegPA, g);
+}
+
+__device__ HX_PHASE_INLINE void phase_avgstep_b(const KParams* P, const Roles* R, WarpStage* stage,
+                                                unsigned long long seq, const Geo& g) {
+  const int m = P->m;
+  double acc[2];
+  acc_init<2, 0>(acc);
+  EpiAvgStepDual e{P->yavg + static_cast<size_t>(R->avg_out) * m, P->aavg + static_cast<size_t>(R->avg_out) * m,
+                   P->b, R->eta};
+  spmv_rows<2, 0>(P->A, 1, SrcVec{P->xbar}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
+  fold_long<2, 0>(P->A, 1, seq, acc, g.cta);
+  block_to_slots<2, 0, false>(acc, P, kRegPB, g);
+}
+
+// canonical_norm_with_product, src/pdhg_core.cpp:37-51, from the three sums;
+// *bad = 1 on the domain_error branch.
+__device__ double canonical_from(double dx2, double dy2, double dyax, double eta, int* bad) {
+  const double q = dx2 / eta - 2.0 * dyax + dy2 / eta;
+  if (q < 0.0) {
+    if (q < -1e-9 * ((dx2 + dy2) / eta)) *bad = 1;
+    return 0.0;
+  }
+  return sqrt(q);
+}
+
+__device__ __forceinline__ bool tracing_at(const Ctl& C, long long it) {
+  return C.trace_period > 0 && it % C.trace_period == 0;
+}
+
+// Restart / next roles / limits of a baseline (src/solver.cpp:483-508).
+__device__ void finish_iteration_baseline(Ctl& C, hplp_epoch_t* epochs, bool writer, double res, bool time_up) {
+  Roles& R = C.r;
+  const bool averaged = C.scheme != HPLP_SCHEME_VANILLA;
+  bool restart = false;
+  if (C.scheme == HPLP_SCHEME_RESTARTED_AVERAGE) {
+    restart = should_restart(C, C.n, C.k, res, C.res_epoch_start);
+    if (!restart && C.restart_kind == HPLP_RESTART_ADAPTIVE && C.stall_cap > 0 && C.k >= C.stall_cap) restart = true;
+  }
+  const int avg_now = R.avg_out;  // the average after this iteration's update
+  if (averaged) C.avg_count = R.avg_mode == 1 ? 1 : C.avg_count + 1;
+  if (restart) {  // z <- z-bar, a_x <- a_x_avg, empty average (:490-497)
+    if (writer && C.n_epochs > 0) epochs[(C.n_epochs - 1) % kEpochCap].restart_length = C.k;
+    R.x_src = avg_now, R.x_src_avg = 1;
+    R.y_cur = avg_now, R.y_cur_avg = 1;
+    R.ax_cur = avg_now, R.ax_cur_avg = 1;
+    R.avg_mode = 1;
+    R.avg_cur = -1;
+    C.avg_count = 0;
+    C.n += 1;
+    C.k = 0;
+  } else {  // z <- T(z), a_x <- A x+ (:498-502)
+    R.x_src = R.xp_out, R.x_src_avg = 0;
+    R.y_cur = R.yp_out, R.y_cur_avg = 0;
+    R.ax_cur = R.axp_out, R.ax_cur_avg = 0;
+    if (averaged) {
+      R.avg_mode = 2;
+      R.avg_cur = avg_now;
+      R.w_avg = 1.0 / static_cast<double>(C.avg_count + 1);
+    }
+    C.k += 1;
+  }
+  R.x_mode = 0;
+  R.w_x = 0.0;
+  R.check = 0;
+  C.it += 1;
+  const int xs = R.x_src_avg ? -1 : R.x_src, yc = R.y_cur_avg ? -1 : R.y_cur, ac = R.ax_cur_avg ? -1 : R.ax_cur;
+  R.zx_out = pick_free(kXPool, xs, C.x_best, C.last_zx, -1);
+  R.xp_out = pick_free(kXPool, xs, C.x_best, C.last_zx, R.zx_out);
+  R.yp_out = pick_free(kYPool, yc, C.y_best, C.last_y_avg ? -1 : C.last_y, -1);
+  R.yc_out = pick_free(kYPool, yc, C.y_best, C.last_y_avg ? -1 : C.last_y, R.yp_out);
+  R.axp_out = pick_free(kAxPool, ac, -1, -1, -1);
+  R.axc_out = pick_free(kAxPool, ac, R.axp_out, -1, -1);
+  if (averaged) R.avg_out = pick_free(kAvgPool, R.avg_cur, C.avg_best, R.x_src_avg ? R.x_src : -1, avg_now);
+  R.w_next = 0.0;
+  R.avg_step = C.scheme == HPLP_SCHEME_RESTARTED_AVERAGE ||
+               (C.scheme == HPLP_SCHEME_AVERAGED && (C.k == 0 || tracing_at(C, C.it)));
+  if (C.it >= C.iteration_limit) set_final_limit(C, HPLP_STATUS_ITERATION_LIMIT);
+  else if (time_up) set_final_limit(C, HPLP_STATUS_TIME_LIMIT);
+  if (tracing_at(C, C.last_it)) {
+    C.paused = 1;
+    R.stop = 1;
+  }
+  if (C.it >= C.batch_end) R.stop = 1;
+}
+
+// One baseline iteration's decisions (src/solver.cpp:418-489): t[0..6] as
+// in the main loop (KKT terms at the candidate; z's own step terms), a[0..2]
+// the step at the average (when R.avg_step).
+__device__ void main_logic_baseline(Ctl& C, const double* t, const double* a, hplp_epoch_t* epochs, bool writer,
+                                    bool time_up) {
+  Roles& R = C.r;
+  const bool averaged = C.scheme != HPLP_SCHEME_VANILLA;
+  double kkt[4];
+  kkt[0] = sqrt(t[3]) / (1.0 + C.b_norm);
+  kkt[1] = sqrt(t[0]) / (1.0 + C.c_norm);
+  kkt[2] = fabs(t[1] + t[4]) / (1.0 + fabs(t[1]) + fabs(t[4]));
+  kkt[3] = dmax(dmax(kkt[0], kkt[1]), kkt[2]);
+  const double eta = R.eta;
+  int bad = 0;
+  const double res_z = canonical_from(t[2], t[5], t[6], eta, &bad);  // ||z - T(z)||, with products
+  double res;
+  C.spmv += 2;
+  if (averaged && R.avg_step) {
+    res = canonical_from(a[0], a[1], a[2], eta, &bad);
+    C.spmv += 2;
+  } else if (!averaged) {
+    res = res_z;
+  } else {
+    res = NAN;
+  }
+  if (bad) {
+    C.error = HPLP_EDOMAIN;
+    R.stop = 1;
+    return;
+  }
+  if (C.k == 0) {
+    C.res_epoch_start = res;
+    if (writer) {
+      hplp_epoch_t& e = epochs[C.n_epochs % kEpochCap];
+      e.epoch = C.n;
+      e.restart_length = 0;
+      e.residual_at_start = res;
+      e.kkt_at_start = {kkt[0], kkt[1], kkt[2], kkt[3]};
+    }
+    C.n_epochs += 1;
+  }
+  C.x_best_prev = C.x_best;
+  if (kkt[3] < C.best_kkt) {  // candidate: z, or the average slot just written
+    C.best_kkt = kkt[3];
+    for (int i = 0; i < 4; ++i) C.best_err[i] = kkt[i];
+    if (averaged) {
+      C.avg_best = R.avg_out;
+      C.x_best = C.y_best = -1;
+    } else {
+      C.x_best = R.zx_out;
+      C.y_best = R.y_cur;
+      C.avg_best = -1;
+    }
+  }
+  C.last_it = C.it;
+  C.last_n = C.n;
+  C.last_k = C.k;
+  C.last_res = res;
+  C.last_res_diff = res_z;
+  for (int i = 0; i < 4; ++i) C.last_kkt[i] = kkt[i];
+  C.last_zx = R.zx_out;
+  C.last_xp = R.xp_out;
+  C.last_y = R.y_cur;
+  C.last_y_avg = R.y_cur_avg;
+  C.last_yp = R.yp_out;
+  C.last_xa = R.x_anchor;
+  C.last_ya = R.y_anchor;
+  C.last_ax = R.ax_cur;
+  C.last_axp = R.axp_out;
+  C.last_cand_avg = averaged ? R.avg_out : -1;
+  if (kkt[3] <= C.tol) {  // :462-465, returns the candidate
+    C.status = HPLP_STATUS_OPTIMAL;
+    C.final_x = R.zx_out;
+    C.final_y = R.y_cur;
+    C.final_avg = C.last_cand_avg;
+    for (int i = 0; i < 4; ++i) C.final_kkt[i] = kkt[i];
+    R.stop = 1;
+    if (tracing_at(C, C.last_it)) C.paused = 1;
+    return;
+  }
+  if (C.check_period > 0 && C.it > 0 && C.it % C.check_period == 0) {  // :467-481, difference candidate only
+    R.check = 1;
+    R.cand_scale = 0.0;
+    return;
+  }
+  finish_iteration_baseline(C, epochs, writer, res, time_up);
+}
+
+__device__ __forceinline__ void loop_body_baseline(const KParams* P, const Geo& g) {
+  __shared__ Ctl C;
+  __shared__ double tot[kMaxQ];
+  __shared__ double atot[4];
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const bool writer = g.cta == 0;
+  WarpStage* stage = reinterpret_cast<WarpStage*>(dyn_smem) + warp;
+  const unsigned long long t_start = global_ns();
+  ctl_load(P->ctl, C);
+  const unsigned long long budget = C.time_budget_ns;
+  const Roles* R = &C.r;
+  GridBar* bar = P->bar;
+  unsigned long long target = 0;
+  unsigned long long seq = 1;
+  const bool vanilla = C.scheme == HPLP_SCHEME_VANILLA;
+  while (!R->stop) {
+    const int par = static_cast<int>(C.it & 1);
+    SpmvHead head;
+    spmv_head(P->AT, gwarp_id(g), lane, head);
+    if (vanilla) phase_primal<false>(P, R, par, stage, ++seq, head, g);
+    else phase_primal_avg(P, R, par, stage, ++seq, head, g);
+    if (writer && threadIdx.x == 0 && budget != 0ull)
+      bar->time_up[par] = (global_ns() - t_start) > budget ? 1u : 0u;
+    spmv_head(P->A, gwarp_id(g), lane, head);
+    if (!grid_sync(bar, target)) return;
+    if (vanilla) phase_dual<false>(P, R, par, stage, ++seq, head, g);
+    else phase_dual_avg(P, R, par, stage, ++seq, head, g);
+    if (!grid_sync(bar, target)) return;
+    if (R->avg_step) {  // the PDHG step at the average (:424-433)
+      phase_avgstep_a(P, R, stage, ++seq, g);
+      if (!grid_sync(bar, target)) return;
+      phase_avgstep_b(P, R, stage, ++seq, g);
+      if (!grid_sync(bar, target)) return;
+      {
+        const double* ra = region_ptr(P, kRegPA, g.nrec);
+        const double* rb = region_ptr(P, kRegPB, g.nrec);
+        block_totals(3, [&](int q) { return QSrc{q == 0 ? ra : rb, q == 0 ? 0 : q - 1, nullptr, 0, 0, false}; },
+                     atot, g);
+      }
+    }
+    if (warp == 0) {
+      double t[7];
+      warp_totals_main(P, par, t, g);
+      if (lane == 0) {
+        for (int i = 0; i < 7; ++i) tot[i] = t[i];
+        const bool time_up = budget != 0ull && *reinterpret_cast<volatile unsigned*>(&bar->time_up[par]) != 0u;
+        main_logic_baseline(C, tot, atot, P->epochs, writer, time_up);
+      }
+    }
+    __syncthreads();
+    if (R->check) {  // certificate scan, iterate-difference candidate (:467-481)
+      cert_norms<false>(P, R, g);
+      if (!grid_sync(bar, target)) return;
+      {
+        const double* rg = region_ptr(P, kRegC1, g.nrec);
+        block_totals(8, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, false}; }, tot, g);
+      }
+      if (threadIdx.x == 0) {
+        int any = 0;
+        for (int c = 0; c < 4; ++c) {
+          C.r.cn2[c] = sqrt(tot[c]);
+          C.cfinite[c] = tot[4 + c] == 0.0;
+          C.r.cand_on[c] = c < 2 && C.r.cn2[c] > 0.0 && C.cfinite[c];
+          any |= C.r.cand_on[c];
+        }
+        if (!any) scan_logic(C, P->epochs, writer, false);
+      }
+      __syncthreads();
+      if (R->check) {
+        cert_units<false>(P, R, g);
+        if (!grid_sync(bar, target)) return;
+        {
+          const double* rg = region_ptr(P, kRegC2, g.nrec);
+          block_totals(12, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, ((0x577u >> q) & 1u) != 0}; }, tot, g);
+        }
+        if (threadIdx.x == 0) {
+          C.cinf[0] = tot[0], C.cmax_u[0] = tot[1], C.cmax_negu[0] = tot[2], C.cdot[0] = tot[3];
+          C.cinf[1] = tot[8], C.cdot[1] = tot[9];
+        }
+        __syncthreads();
+        cert_products<false>(P, R, stage, ++seq, g);
+        if (!grid_sync(bar, target)) return;
+        {
+          const double* rg = region_ptr(P, kRegC3, g.nrec);
+          block_totals(6, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, true}; }, tot, g);
+        }
+        if (threadIdx.x == 0) {
+          C.cmax_at[1] = tot[0], C.cmax_negat[1] = tot[1];
+          C.cmax_abs_au[0] = tot[4];
+          const bool time_up = budget != 0ull && *reinterpret_cast<volatile unsigned*>(&bar->time_up[par]) != 0u;
+          scan_logic(C, P->epochs, writer, time_up);
+        }
+        __syncthreads();
+      }
+    }
+    if (R->stop) break;
+    if (!grid_sync(bar, target)) return;  // phase A of the next iteration rewrites this one's long-row counters
+  }
+  if (writer) ctl_store(C, P->ctl);
+}
+
+__global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_baseline(const __grid_constant__ KParams KP) {
+  const Geo g{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x),
+              static_cast<int>(gridDim.x)};
+  loop_body_baseline(&KP, g);
 }
 
 // ---------------------------------------------------------------------------
@@ -1904,6 +2401,11 @@ struct hx_ctx {
   double* ypool = nullptr;
   double* axpool = nullptr;
   double* upool = nullptr;
+  double* xavg = nullptr;  // baseline schemes: kAvgPool slots (allocated at hx_setup)
+  double* tavg = nullptr;
+  double* yavg = nullptr;
+  double* aavg = nullptr;
+  double* xbar = nullptr;
   double* slots = nullptr;
   double* scratch = nullptr;  // kMaxQ doubles
   Ctl* ctl = nullptr;
@@ -1964,6 +2466,8 @@ void free_sched(DevSched& s) {
 void free_problem(hx_ctx* c) {
   dfree(c->a_ptr), dfree(c->a_idx), dfree(c->a_val), dfree(c->t_ptr), dfree(c->t_idx), dfree(c->t_val);
   dfree(c->b), dfree(c->c), dfree(c->xpool), dfree(c->ypool), dfree(c->axpool), dfree(c->upool);
+  dfree(c->xavg), dfree(c->tavg), dfree(c->yavg), dfree(c->aavg), dfree(c->xbar);
+  c->xavg = c->tavg = c->yavg = c->aavg = c->xbar = nullptr;
   free_sched(c->sa);
   free_sched(c->st);
   free_sched(c->pa);
@@ -2043,6 +2547,7 @@ KParams params(hx_ctx* c) {
   P.bar = c->bar;
   P.epochs = c->epochs;
   P.prof = c->prof;
+  P.xavg = c->xavg, P.tavg = c->tavg, P.yavg = c->yavg, P.aavg = c->aavg, P.xbar = c->xbar;
   return P;
 }
 
@@ -2055,8 +2560,10 @@ int launch_loop(hx_ctx* c) {
     if (d->view.n_long)
       HX_CUDA(c, cudaMemsetAsync(d->flags, 0, 4 * static_cast<size_t>(d->view.n_long) * sizeof(unsigned long long),
                                  c->stream));
-  HX_CUDA(c, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(loop_kernel), dim3(c->grid), dim3(kThreads),
-                                         args, kStageBytes, c->stream));
+  const void* kernel = c->h.mode == kModeLoop && c->h.scheme != HPLP_SCHEME_RHPDHG
+                           ? reinterpret_cast<const void*>(loop_kernel_baseline)
+                           : reinterpret_cast<const void*>(loop_kernel);
+  HX_CUDA(c, cudaLaunchCooperativeKernel(kernel, dim3(c->grid), dim3(kThreads), args, kStageBytes, c->stream));
   c->launches += 1;
   HX_CUDA(c, cudaMemcpyAsync(&c->h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
   GridBar gb;
@@ -2185,6 +2692,9 @@ int spmv_dev(hx_ctx* c, bool transpose, const double* x, double* out) {
 }
 
 double* xbuf(hx_ctx* c, int i) { return c->xpool + static_cast<size_t>(i) * c->n; }
+// baseline schemes: a vector that may live in an average slot
+double* xbuf2(hx_ctx* c, int i, int avg) { return (avg ? c->xavg : c->xpool) + static_cast<size_t>(i) * c->n; }
+double* ybuf2(hx_ctx* c, int i, int avg) { return (avg ? c->yavg : c->ypool) + static_cast<size_t>(i) * c->m; }
 double* ybuf(hx_ctx* c, int i) { return c->ypool + static_cast<size_t>(i) * c->m; }
 double* axbuf(hx_ctx* c, int i) { return c->axpool + static_cast<size_t>(i) * c->m; }
 
@@ -2206,6 +2716,7 @@ void fill_progress(hx_ctx* c, hx_progress_t* p) {
   p->trace_n = C.last_n;
   p->trace_k = C.last_k;
   p->trace_res = C.last_res;
+  p->trace_res_diff = C.last_res_diff;
   p->trace_kkt = {C.last_kkt[0], C.last_kkt[1], C.last_kkt[2], C.last_kkt[3]};
   p->final_kkt = {C.final_kkt[0], C.final_kkt[1], C.final_kkt[2], C.final_kkt[3]};
   p->n_epochs = C.n_epochs;
@@ -2239,6 +2750,8 @@ int hx_create(int32_t device, hx_ctx** out) {
   HX_CUDA(nullptr, cudaFuncSetAttribute(spmv_store_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(kStageBytes)));
   HX_CUDA(nullptr, cudaFuncSetAttribute(loop_kernel_team, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kStageBytes)));
+  HX_CUDA(nullptr, cudaFuncSetAttribute(loop_kernel_baseline, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(kStageBytes)));
   int occ = 0;
   HX_CUDA(nullptr, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, loop_kernel, kThreads, kStageBytes));
@@ -2561,7 +3074,18 @@ int hx_power_iteration(hx_ctx* c, const double* x0, double tol, int64_t k0, int6
 int hx_setup(hx_ctx* c, const hplp_config_t* cfg, double sigma_used, double eta, const double* x0,
              const double* y0) {
   if (!c->uploaded) return set_err(c, HPLP_ESTATE, "hx_setup: no problem uploaded");
+  if (cfg->scheme < HPLP_SCHEME_RHPDHG || cfg->scheme > HPLP_SCHEME_RESTARTED_AVERAGE)
+    return set_err(c, HPLP_EINVAL, "hx_setup: unknown scheme");
+  if (cfg->scheme != HPLP_SCHEME_RHPDHG && c->ranked)
+    return set_err(c, HPLP_EINVAL, "hx_setup: the baseline schemes run on one device (no team)");
   cudaStream_t s = c->stream;
+  if (cfg->scheme >= HPLP_SCHEME_AVERAGED && !c->xavg) {  // running-average slots
+    HX_CUDA(c, dalloc(&c->xavg, static_cast<size_t>(kAvgPool) * c->n));
+    HX_CUDA(c, dalloc(&c->tavg, static_cast<size_t>(kAvgPool) * c->n));
+    HX_CUDA(c, dalloc(&c->yavg, static_cast<size_t>(kAvgPool) * c->m));
+    HX_CUDA(c, dalloc(&c->aavg, static_cast<size_t>(kAvgPool) * c->m));
+    HX_CUDA(c, dalloc(&c->xbar, c->n));
+  }
   if (x0) HX_CUDA(c, cudaMemcpyAsync(xbuf(c, 0), x0, c->n * sizeof(double), cudaMemcpyHostToDevice, s));
   else HX_CUDA(c, cudaMemsetAsync(xbuf(c, 0), 0, c->n * sizeof(double), s));
   if (y0) HX_CUDA(c, cudaMemcpyAsync(ybuf(c, 0), y0, c->m * sizeof(double), cudaMemcpyHostToDevice, s));
@@ -2591,7 +3115,13 @@ int hx_setup(hx_ctx* c, const hplp_config_t* cfg, double sigma_used, double eta,
   C.status = -1;
   C.final_x = C.final_y = -1;
   C.cert_cand[0] = C.cert_cand[1] = -1;
+  C.scheme = cfg->scheme;
+  C.avg_best = C.final_avg = C.last_cand_avg = -1;
   Roles& R = C.r;
+  if (C.scheme >= HPLP_SCHEME_AVERAGED) {  // the first iteration copies z into the average
+    R.avg_mode = 1, R.avg_cur = -1, R.avg_out = 0, R.w_avg = 1.0;
+  }
+  R.avg_step = C.scheme >= HPLP_SCHEME_AVERAGED;  // restarted: every iteration; averaged: k == 0 (it 0)
   R.eta = eta;
   R.x_src = 0, R.x_anchor = 0, R.x_mode = 0, R.w_x = 0.0;
   R.zx_out = 1, R.xp_out = 2;
@@ -2617,10 +3147,10 @@ bool run_begin(hx_ctx* c, int64_t max_iters) {
   auto limit = [&](int status) {
     C.status = status;
     if (C.best_kkt < std::numeric_limits<double>::infinity()) {
-      C.final_x = C.x_best, C.final_y = C.y_best;
+      C.final_x = C.x_best, C.final_y = C.y_best, C.final_avg = C.avg_best;
       std::memcpy(C.final_kkt, C.best_err, sizeof(C.final_kkt));
     } else {
-      C.final_x = C.final_y = -1;
+      C.final_x = C.final_y = C.final_avg = -1;
     }
   };
   if (C.it >= C.iteration_limit) {  // :242-248
@@ -2898,24 +3428,34 @@ int hx_get_iterate(hx_ctx* c, int32_t which, double* x, double* y) {
   cudaStream_t s = c->stream;
   switch (which) {
     case HX_ITERATE_BEST:
+      if (C.avg_best >= 0) {  // averaged baselines: the best candidate is an average
+        dx = xbuf2(c, C.avg_best, 1), dy = ybuf2(c, C.avg_best, 1);
+        break;
+      }
       if (C.x_best < 0) return set_err(c, HPLP_ESTATE, "hx_get_iterate: no best iterate yet");
       if (int rc = assemble_x(c, C.x_best)) return rc;
       dx = xbuf(c, C.x_best), dy = ybuf(c, C.y_best);
       break;
-    case HX_ITERATE_LAST:
+    case HX_ITERATE_LAST:  // the traced candidate (z, or the average for the averaged baselines)
       if (C.it == 0 && C.status < 0) return set_err(c, HPLP_ESTATE, "hx_get_iterate: no iteration completed");
+      if (C.last_cand_avg >= 0) {
+        dx = xbuf2(c, C.last_cand_avg, 1), dy = ybuf2(c, C.last_cand_avg, 1);
+        break;
+      }
       if (int rc = assemble_x(c, C.last_zx)) return rc;
-      dx = xbuf(c, C.last_zx), dy = ybuf(c, C.last_y);
+      dx = xbuf(c, C.last_zx), dy = ybuf2(c, C.last_y, C.last_y_avg);
       break;
     case HX_ITERATE_NEXT:
       dx = xbuf(c, C.last_xp), dy = ybuf(c, C.last_yp);
       break;
     default: {  // the iterate the next iteration starts from
-      if (C.status >= 0 && C.final_x >= 0) {
+      if (C.status >= 0 && C.final_avg >= 0) {
+        dx = xbuf2(c, C.final_avg, 1), dy = ybuf2(c, C.final_avg, 1);
+      } else if (C.status >= 0 && C.final_x >= 0) {
         if (int rc = assemble_x(c, C.final_x)) return rc;
         dx = xbuf(c, C.final_x), dy = ybuf(c, C.final_y);
       } else if (C.r.x_mode == 0) {
-        dx = xbuf(c, C.r.x_src), dy = ybuf(c, C.r.y_cur);
+        dx = xbuf2(c, C.r.x_src, C.r.x_src_avg), dy = ybuf2(c, C.r.y_cur, C.r.y_cur_avg);
       } else {
         double* tmp = c->upool;
         combine_kernel<<<4 * c->sm_count, 256, 0, s>>>(static_cast<int>(c->n), C.r.w_x, xbuf(c, C.r.x_src),
@@ -2946,7 +3486,7 @@ int hx_get_certificate(hx_ctx* c, int32_t kind, double* vec) {
     p = xbuf(c, C.last_zx);
     q = normalized ? xbuf(c, C.last_xa) : xbuf(c, C.last_xp);
   } else {
-    p = ybuf(c, C.last_y);
+    p = ybuf2(c, C.last_y, C.last_y_avg);
     q = normalized ? ybuf(c, C.last_ya) : ybuf(c, C.last_yp);
   }
   const double sgn = C.cert[kind].orientation == HPLP_ORIENT_NEGATED ? -1.0 : 1.0;
@@ -2971,15 +3511,21 @@ int hx_trace_extras(hx_ctx* c, double* aty, double* c_out, double* cand_norm_nor
   const Ctl& C = c->h;
   cudaStream_t s = c->stream;
   if (aty || c_out) {
-    double* dout = c->upool;
-    int rc = spmv_dev(c, true, ybuf(c, C.last_y), dout);
-    if (rc) return rc;
-    if (aty && c->n) HX_CUDA(c, cudaMemcpyAsync(aty, dout, c->n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    const double* src;
+    if (C.last_cand_avg >= 0) {  // averaged baselines: the mean of A^T y (src/solver.cpp:452-454)
+      src = c->tavg + static_cast<size_t>(C.last_cand_avg) * c->n;
+    } else {
+      double* dout = c->upool;
+      int rc = spmv_dev(c, true, ybuf2(c, C.last_y, C.last_y_avg), dout);
+      if (rc) return rc;
+      src = dout;
+    }
+    if (aty && c->n) HX_CUDA(c, cudaMemcpyAsync(aty, src, c->n * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (c_out && c->n) HX_CUDA(c, cudaMemcpyAsync(c_out, c->c, c->n * sizeof(double), cudaMemcpyDeviceToHost, s));
   }
   if (cand_norm_normalized) {
     *cand_norm_normalized = std::numeric_limits<double>::quiet_NaN();
-    if (C.last_k >= 1 && !c->ranked) {
+    if (C.last_k >= 1 && !c->ranked && C.scheme == HPLP_SCHEME_RHPDHG) {
       const double scale = 2.0 / static_cast<double>(C.last_k);
       cand_norm_kernel<<<c->grid, kThreads, 0, s>>>(static_cast<int>(c->m), static_cast<int>(c->n), scale,
                                                     xbuf(c, C.last_zx), xbuf(c, C.last_xa), ybuf(c, C.last_y),
@@ -3009,9 +3555,10 @@ int hx_kkt_current(hx_ctx* c, hplp_kkt_t* out) {
   double* xcur = c->upool;
   double* aty = c->upool + c->n;
   double* ax = c->upool + 2 * c->n;
-  const double* ycur = ybuf(c, C.r.y_cur);
+  const double* ycur = ybuf2(c, C.r.y_cur, C.r.y_cur_avg);
   if (C.r.x_mode == 0) {
-    HX_CUDA(c, cudaMemcpyAsync(xcur, xbuf(c, C.r.x_src), c->n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    HX_CUDA(c, cudaMemcpyAsync(xcur, xbuf2(c, C.r.x_src, C.r.x_src_avg), c->n * sizeof(double),
+                               cudaMemcpyDeviceToDevice, s));
   } else {
     combine_kernel<<<4 * c->sm_count, 256, 0, s>>>(static_cast<int>(c->n), C.r.w_x, xbuf(c, C.r.x_src),
                                                    xbuf(c, C.r.x_anchor), xcur);

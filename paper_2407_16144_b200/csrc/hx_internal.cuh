@@ -31,6 +31,7 @@ constexpr int kMaxQ = 16;                  // reduction quantities per phase
 constexpr int kXPool = 7;                  // n-vectors: iterates, anchors, best, T(z), speculative outputs
 constexpr int kYPool = 6;                  // m-vectors: y, anchors, best, T(z), combos
 constexpr int kAxPool = 4;                 // m-vectors: A x carried / anchor / products
+constexpr int kAvgPool = 4;                // running-average slots (baseline schemes): current, new, best, restart point
 constexpr int kEpochCap = 1 << 16;         // device epoch ring (host drains per hx_run)
 constexpr double kRowCost = 3.0;           // epilogue cost of one row in nnz units
 constexpr double kTaskCost = 64.0;         // fixed latency cost of one warp task in nnz units

@@ -49,6 +49,8 @@ void validate_config(const SolverConfig& config) {
     throw std::invalid_argument("SolverConfig: certificate_tolerance must be > 0");
   if (config.infeasibility_check_period < 0 || config.trace_period < 0 || config.adaptive_stall_cap < 0)
     throw std::invalid_argument("SolverConfig: periods must be >= 0");
+  if (config.scheme < HPLP_SCHEME_RHPDHG || config.scheme > HPLP_SCHEME_RESTARTED_AVERAGE)
+    throw std::invalid_argument("SolverConfig: unknown scheme");
   if (config.restart.kind == RestartScheme::Kind::kFixedFrequency && config.restart.k_star < 1)
     throw std::invalid_argument("RestartScheme: k_star must be >= 1");
   if (config.restart.kind == RestartScheme::Kind::kAdaptiveResidualDecay &&
@@ -198,6 +200,7 @@ hplp_config_t to_pod(const SolverConfig& c) {
   p.seed = c.seed;
   p.precondition_ruiz_iters = c.precondition_ruiz_iters;
   p.precondition_pc_alpha = c.precondition_pc_alpha;
+  p.scheme = c.scheme;
   return p;
 }
 
@@ -219,6 +222,7 @@ SolverConfig from_pod(const hplp_config_t& p) {
   c.seed = p.seed;
   c.precondition_ruiz_iters = p.precondition_ruiz_iters;
   c.precondition_pc_alpha = p.precondition_pc_alpha;
+  c.scheme = p.scheme;
   return c;
 }
 
@@ -415,7 +419,7 @@ SolveResult Solver::solve(const SolverConfig& config) {
       rec.iteration = p.trace_it;
       rec.fixed_point_residual = p.trace_res;
       rec.kkt = kkt_of(p.trace_kkt);
-      rec.candidate_norm_difference = p.trace_res;  // ||T(z) - z|| == ||z - T(z)||
+      rec.candidate_norm_difference = p.trace_res_diff;  // ||T(z) - z|| (== the residual for rHPDHG)
       Iterate z{Vector(static_cast<std::size_t>(n_)), Vector(static_cast<std::size_t>(m_))};
       check(ctx, hx_get_iterate(ctx, HX_ITERATE_LAST, z.x.data(), z.y.data()));
       // partition estimate from the reduced costs c + A^T y and the
@@ -505,6 +509,15 @@ PartitionEstimate partition_estimate_from_reduced_costs(const Iterate& z, const 
 SolveResult solve(const StandardFormLP& lp, const SolverConfig& config) {
   Solver s(lp, config.device);
   return s.solve(config);
+}
+
+SolveResult solve_baseline(const StandardFormLP& lp, const SolverConfig& config, BaselineMode mode) {
+  SolverConfig c = config;
+  c.scheme = mode == BaselineMode::kVanilla    ? HPLP_SCHEME_VANILLA
+             : mode == BaselineMode::kAveraged ? HPLP_SCHEME_AVERAGED
+                                               : HPLP_SCHEME_RESTARTED_AVERAGE;
+  Solver s(lp, config.device);
+  return s.solve(c);
 }
 
 }  // namespace hplp_gpu

@@ -35,7 +35,7 @@ class HxProgress(C.Structure):
         ("trace_it", C.c_int64), ("trace_n", C.c_int64), ("trace_k", C.c_int64),
         ("trace_res", C.c_double), ("trace_kkt", abi.Kkt), ("final_kkt", abi.Kkt),
         ("n_epochs", C.c_int64), ("primal_cert", abi.CertMeta), ("dual_cert", abi.CertMeta),
-        ("device_ms", C.c_double), ("launches", C.c_int64),
+        ("device_ms", C.c_double), ("launches", C.c_int64), ("trace_res_diff", C.c_double),
     ]
 
 
