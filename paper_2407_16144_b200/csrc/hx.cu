@@ -1994,7 +1994,14 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
   }
 
   unsigned long long* prof = (!RK && P->prof) ? P->prof + blockIdx.x * 16 : nullptr;
-  unsigned long long tp = clock64(), pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pacc2[3] = {0, 0, 0};
+  // phase timers live in shared memory (thread 0 only): per-thread arrays would
+  // hold registers across the whole loop in every thread
+  __shared__ unsigned long long pacc[8], pacc2[3], tp;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 8; ++k) pacc[k] = 0;
+    for (int k = 0; k < 3; ++k) pacc2[k] = 0;
+    tp = clock64();
+  }
   auto mark = [&](int k) {  // SM cycles (clock64); the host converts with the SM clock
     if (prof && threadIdx.x == 0) {
       const unsigned long long t = clock64();
@@ -2066,7 +2073,8 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
       }
     }
     mark(4);
-    // speculative phase A of iteration it+1
+    // speculative phase A of iteration it+1 (measured: worth ~10% against
+    // running phase A after the controller)
     phase_primal<RK>(P, &SR, par ^ 1, stage, ++seq, head, g);
     if (writer && threadIdx.x == 0 && budget != 0ull)
       set_time_up(par ^ 1, (global_ns() - t_start) > budget ? 1u : 0u);
