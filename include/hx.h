@@ -144,6 +144,8 @@ int hx_progress(hx_ctx* ctx, hx_progress_t* progress);
 int hx_set_partition(hx_ctx* ctx, int32_t nranks, int32_t rank, int64_t row0, int64_t row1, int64_t col0,
                      int64_t col1, int32_t ctas);
 int hx_team_bind(hx_ctx** ctxs, int32_t count);
+/* nranks of the context's team (1 for a plain context). */
+int32_t hx_team_size(hx_ctx* ctx);
 int hx_team_export(hx_ctx* ctx, void* blob, int64_t capacity, int64_t* size);
 int hx_team_import(hx_ctx* ctx, const void* blob, int64_t size);
 /* progress: count entries (one per ctxs[i]) or NULL. */

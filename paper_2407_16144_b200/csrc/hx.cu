@@ -1923,9 +1923,12 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
   unsigned long long target = 0;
   unsigned long long seq = 1;  // phase sequence number (long-row flags; reset per launch)
   unsigned long long repoch = C.team_epochs;  // team barriers passed (continues across launches)
+  const bool solo = !RK || P->T.nranks == 1;  // a team of one needs no cross-rank step
   auto sync = [&]() -> bool {
-    if constexpr (RK) return team_sync(bar, P->T, g, target, repoch);
-    else return grid_sync(bar, target);
+    if constexpr (RK) {
+      if (!solo) return team_sync(bar, P->T, g, target, repoch);
+    }
+    return grid_sync(bar, target);
   };
   // time-limit flag: decided by rank 0 alone so every rank stops together
   auto set_time_up = [&](int pr, unsigned v) {
@@ -3165,7 +3168,12 @@ bool run_begin(hx_ctx* c, int64_t max_iters) {
     limit(HPLP_STATUS_ITERATION_LIMIT);
     return false;
   }
-  if (c->loop_elapsed_s > c->time_limit_s) {  // :249-254 at the top of the next iteration
+  // :249-254 at the top of the next iteration.  A multi-rank team decides the
+  // time limit on rank 0's clock inside the kernel (every rank reads the flag
+  // rank 0 pushes): a host-side check here would let ranks disagree, and a
+  // rank that launches alone would stall at the first team barrier.
+  const bool team = c->ranked && c->team.nranks > 1;
+  if (!team && c->loop_elapsed_s > c->time_limit_s) {
     limit(HPLP_STATUS_TIME_LIMIT);
     return false;
   }
@@ -3173,9 +3181,9 @@ bool run_begin(hx_ctx* c, int64_t max_iters) {
   C.r.stop = 0;
   C.paused = 0;
   const double remaining = c->time_limit_s - c->loop_elapsed_s;
-  C.time_budget_ns = std::isinf(remaining)
-                         ? 0ull
-                         : std::max<unsigned long long>(1ull, static_cast<unsigned long long>(remaining * 1e9));
+  C.time_budget_ns = std::isinf(remaining) ? 0ull
+                     : remaining <= 1e-9    ? 1ull  // already over (a team rank): stop after one iteration
+                                            : std::max<unsigned long long>(1ull, static_cast<unsigned long long>(remaining * 1e9));
   return true;
 }
 
@@ -3285,6 +3293,8 @@ int hx_set_partition(hx_ctx* c, int32_t nranks, int32_t rank, int64_t row0, int6
   HX_CUDA(c, cudaMemset(c->rbar, 0, sizeof(RankBar)));
   return HPLP_OK;
 }
+
+int32_t hx_team_size(hx_ctx* c) { return c && c->ranked ? c->team.nranks : 1; }
 
 int hx_team_bind(hx_ctx** ctxs, int32_t count) {
   if (count < 1 || count > kMaxRanks || !ctxs) return set_err(nullptr, HPLP_EINVAL, "hx_team_bind: bad team size");

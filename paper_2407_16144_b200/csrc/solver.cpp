@@ -403,8 +403,11 @@ SolveResult Solver::solve(const SolverConfig& config) {
       check(ctx, hx_epochs(ctx, from, p.n_epochs - from, epochs.data() + from));
     }
   };
+  // a rank of a multi-rank team: the time limit is decided on the device by
+  // rank 0 (a per-rank host check could split the team)
+  const int32_t team_size = hx_team_size(ctx);
   while (p.status < 0) {
-    if (since() > config.time_limit_seconds && p.it < config.iteration_limit) {
+    if (team_size == 1 && since() > config.time_limit_seconds && p.it < config.iteration_limit) {
       // host-side guard for the time limit between batches (:249-254)
       break;
     }
