@@ -73,7 +73,8 @@ struct Roles {
   // an average slot after a restart; the running average is updated from
   // slot avg_cur into slot avg_out (avg_mode 1: copy z, 2: w-weighted update)
   int x_src_avg, y_cur_avg, ax_cur_avg;
-  int avg_mode, avg_cur, avg_out, avg_step, pad3;
+  int avg_mode, avg_cur, avg_out, avg_step;
+  int y_unpushed;  // team: y_cur is a y+ whose owned rows the peers have not received yet (after a restart)
   double w_avg;
 };
 
@@ -678,10 +679,9 @@ struct EpiDual {  // phase B, rows of A
     const double omw = 1.0 - w;
     const double yci = omw * ypi + w * in.ya;
     yc[i] = yci;
-    if constexpr (RK) {
-      push_peers(T, T->py, yp_off + i, ypi);
-      push_peers(T, T->py, yc_off + i, yci);
-    }
+    // only the combo -- the next y when there is no restart, which phase A
+    // gathers speculatively; after a restart the loop pushes y+ itself
+    if constexpr (RK) push_peers(T, T->py, yc_off + i, yci);
     axc[i] = omw * s + w * in.axa;
     const double d = axi - bi;
     const double dy = yi - ypi;
@@ -899,6 +899,7 @@ __device__ void finish_iteration(Ctl& C, hplp_epoch_t* epochs, bool writer, doub
     R.ax_cur = R.axp_out;
     R.ax_anchor = R.axp_out;
     R.w_x = 0.0;
+    R.y_unpushed = 1;
     C.n += 1;
     C.k = 0;
   } else {
@@ -908,6 +909,7 @@ __device__ void finish_iteration(Ctl& C, hplp_epoch_t* epochs, bool writer, doub
     R.w_x = w;
     R.y_cur = R.yc_out;
     R.ax_cur = R.axc_out;
+    R.y_unpushed = 0;
     C.k += 1;
   }
   R.check = 0;
@@ -2134,11 +2136,27 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
         __syncthreads();
       }
     }
-    if (R->stop) break;
     spec_done = same_phase_a(*R, SR);
+    bool synced = false;
+    if constexpr (RK) {
+      // a restart makes y+ the next y, but phase B pushed only the combo: push
+      // this rank's rows of y+ now, and barrier before anyone reads them --
+      // also when this launch ends here (the next launch starts with phase A)
+      if (R->y_unpushed && !solo) {
+        const double* yv = P->ypool + static_cast<size_t>(R->y_cur) * P->m;
+        const size_t off = static_cast<size_t>(R->y_cur) * P->m;
+        for (int i = P->T.row0 + g.cta * kThreads + threadIdx.x; i < P->T.row1; i += g.nctas * kThreads)
+          push_peers(&P->T, P->T.py, off + i, ldcg(yv + i));
+        if (!sync()) return;
+        synced = true;
+      }
+      __syncthreads();  // every thread has read y_unpushed before it is cleared
+      if (threadIdx.x == 0) C.r.y_unpushed = 0;
+    }
+    if (R->stop) break;
     // a redo reuses this parity's long-row counters: wait until every CTA's
     // speculative phase A is complete
-    if (!spec_done && !sync()) return;
+    if (!spec_done && !synced && !sync()) return;
     mark(6);
   }
   if (prof && threadIdx.x == 0) {
@@ -2434,6 +2452,7 @@ struct hx_ctx {
   bool ranked = false;
   Team team{};                       // own range + every rank's buffers
   int pcol0[kMaxRanks] = {}, pcol1[kMaxRanks] = {};  // every rank's column block (result assembly)
+  int prow0[kMaxRanks] = {}, prow1[kMaxRanks] = {};  // every rank's row block
   DevSched pa, pt;                   // rows [row0,row1) of A, [col0,col1) of A^T
   RankBar* rbar = nullptr;
   unsigned long long team_epochs = 0;
@@ -2694,6 +2713,20 @@ int assemble_x(hx_ctx* c, int role) {
   return HPLP_OK;
 }
 
+// The same for a y pool vector: y+ is pushed to the peers only on restarts,
+// so a y+ role read back for results is assembled from the peers' rows.
+int assemble_y(hx_ctx* c, int role) {
+  if (!c->ranked || role < 0) return HPLP_OK;
+  for (int r = 0; r < c->team.nranks; ++r) {
+    const int64_t len = c->prow1[r] - c->prow0[r];
+    if (r == c->team.rank || len <= 0) continue;
+    const size_t off = static_cast<size_t>(role) * c->m + c->prow0[r];
+    HX_CUDA(c, cudaMemcpyAsync(c->ypool + off, c->team.py[r] + off, len * sizeof(double), cudaMemcpyDefault,
+                               c->stream));
+  }
+  return HPLP_OK;
+}
+
 int spmv_dev(hx_ctx* c, bool transpose, const double* x, double* out) {
   const Sched& S = transpose ? c->st.view : c->sa.view;
   spmv_store_kernel<<<c->grid, kThreads, kStageBytes, c->stream>>>(S, x, out);
@@ -2938,6 +2971,7 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     T.px[T.rank] = c->xpool, T.py[T.rank] = c->ypool, T.pu[T.rank] = c->upool, T.ps[T.rank] = c->slots;
     T.pb[T.rank] = c->rbar;
     c->pcol0[T.rank] = T.col0, c->pcol1[T.rank] = T.col1;
+    c->prow0[T.rank] = T.row0, c->prow1[T.rank] = T.row1;
     c->local_team.assign(1, c);
   }
   // ||b||, ||c|| once (loop invariants of src/pdhg_core.cpp:60,62).
@@ -3343,6 +3377,7 @@ int hx_team_bind(hx_ctx** ctxs, int32_t count) {
       T.px[r] = by[r]->xpool, T.py[r] = by[r]->ypool, T.pu[r] = by[r]->upool, T.ps[r] = by[r]->slots;
       T.pb[r] = by[r]->rbar;
       c->pcol0[r] = by[r]->team.col0, c->pcol1[r] = by[r]->team.col1;
+      c->prow0[r] = by[r]->team.row0, c->prow1[r] = by[r]->team.row1;
     }
     c->local_team = by;
   }
@@ -3388,6 +3423,7 @@ int hx_team_import(hx_ctx* c, const void* blob, int64_t size) {
   if (b.m != c->m || b.n != c->n || b.nnz != c->nnz || b.grid != c->grid)
     return set_err(c, HPLP_EINVAL, "hx_team_import: ranks disagree on the problem or the CTA count");
   c->pcol0[b.rank] = b.col0, c->pcol1[b.rank] = b.col1;
+  c->prow0[b.rank] = b.row0, c->prow1[b.rank] = b.row1;
   if (b.rank == c->team.rank) return HPLP_OK;
   HX_CUDA(c, cudaSetDevice(c->device));
   void* p[5] = {};
@@ -3464,6 +3500,7 @@ int hx_get_iterate(hx_ctx* c, int32_t which, double* x, double* y) {
       dx = xbuf(c, C.last_zx), dy = ybuf2(c, C.last_y, C.last_y_avg);
       break;
     case HX_ITERATE_NEXT:
+      if (int rc = assemble_y(c, C.last_yp)) return rc;
       dx = xbuf(c, C.last_xp), dy = ybuf(c, C.last_yp);
       break;
     default: {  // the iterate the next iteration starts from
@@ -3504,6 +3541,8 @@ int hx_get_certificate(hx_ctx* c, int32_t kind, double* vec) {
     p = xbuf(c, C.last_zx);
     q = normalized ? xbuf(c, C.last_xa) : xbuf(c, C.last_xp);
   } else {
+    if (!normalized)
+      if (int rc = assemble_y(c, C.last_yp)) return rc;
     p = ybuf2(c, C.last_y, C.last_y_avg);
     q = normalized ? ybuf(c, C.last_ya) : ybuf(c, C.last_yp);
   }
