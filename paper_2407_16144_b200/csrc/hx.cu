@@ -44,6 +44,8 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <mutex>
+#include <unordered_set>
 #include <string>
 #include <type_traits>
 
@@ -2478,13 +2480,60 @@ int set_err(hx_ctx* ctx, int code, const std::string& msg) {
                      std::string(#expr) + ": " + cudaGetErrorString(e_));                     \
   } while (0)
 
-template <typename T>
-cudaError_t dalloc(T** p, size_t count) {
-  return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T));
+// Device memory comes from the device's stream-ordered pool with an
+// unlimited release threshold, so repeated solves reuse memory instead of
+// mapping and unmapping it: plain cudaMalloc / cudaFree of the ~100 MB a
+// configs[1] problem needs took 0.03-0.5 s per call on the B200 boxes, more
+// than the solve.  Buffers peers map through CUDA IPC must be cudaMalloc
+// memory (dalloc_ipc); dfree tells them apart.
+std::mutex g_mem_mu;
+std::unordered_set<void*> g_ipc_blocks;
+std::unordered_set<int> g_pool_ready;
+
+cudaError_t pool_ready() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_mem_mu);
+  if (g_pool_ready.count(dev)) return cudaSuccess;
+  cudaMemPool_t pool;
+  e = cudaDeviceGetDefaultMemPool(&pool, dev);
+  if (e != cudaSuccess) return e;
+  uint64_t keep = ~uint64_t{0};
+  e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  if (e == cudaSuccess) g_pool_ready.insert(dev);
+  return e;
 }
 
+template <typename T>
+cudaError_t dalloc(T** p, size_t count) {
+  cudaError_t e = pool_ready();
+  if (e != cudaSuccess) return e;
+  e = cudaMallocAsync(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T), 0);
+  return e != cudaSuccess ? e : cudaStreamSynchronize(0);
+}
+
+template <typename T>
+cudaError_t dalloc_ipc(T** p, size_t count) {
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T));
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(g_mem_mu);
+    g_ipc_blocks.insert(*p);
+  }
+  return e;
+}
+
+// Callers free only memory no pending work uses (the context's stream is
+// synchronized first).
 void dfree(void* p) {
-  if (p) cudaFree(p);
+  if (!p) return;
+  bool ipc;
+  {
+    std::lock_guard<std::mutex> lk(g_mem_mu);
+    ipc = g_ipc_blocks.erase(p) > 0;
+  }
+  if (ipc) cudaFree(p);
+  else cudaFreeAsync(p, 0);
 }
 
 void free_sched(DevSched& s) {
@@ -2494,6 +2543,7 @@ void free_sched(DevSched& s) {
 }
 
 void free_problem(hx_ctx* c) {
+  if (c->stream) cudaStreamSynchronize(c->stream);
   dfree(c->a_ptr), dfree(c->a_idx), dfree(c->a_val), dfree(c->t_ptr), dfree(c->t_idx), dfree(c->t_val);
   dfree(c->b), dfree(c->c), dfree(c->xpool), dfree(c->ypool), dfree(c->axpool), dfree(c->upool);
   dfree(c->xavg), dfree(c->tavg), dfree(c->yavg), dfree(c->aavg), dfree(c->xbar);
@@ -2920,7 +2970,7 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
                                     bits, s);
     cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, cnt, c->t_ptr, static_cast<int>(n + 1), s);
     void* tmp = nullptr;
-    HX_CUDA(c, cudaMalloc(&tmp, std::max<size_t>(1, std::max(tmp_bytes, scan_bytes))));
+    HX_CUDA(c, dalloc(reinterpret_cast<unsigned char**>(&tmp), std::max<size_t>(1, std::max(tmp_bytes, scan_bytes))));
     if (nnz)
       HX_CUDA(c, cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, c->a_idx, keys_out, iota, perm,
                                                  static_cast<int>(nnz), 0, bits, s));
@@ -2961,10 +3011,16 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
       if (rc) return rc;
     }
   }
-  HX_CUDA(c, dalloc(&c->xpool, static_cast<size_t>(kXPool) * n));
-  HX_CUDA(c, dalloc(&c->ypool, static_cast<size_t>(kYPool) * m));
+  if (c->ranked) {  // peers map these through CUDA IPC
+    HX_CUDA(c, dalloc_ipc(&c->xpool, static_cast<size_t>(kXPool) * n));
+    HX_CUDA(c, dalloc_ipc(&c->ypool, static_cast<size_t>(kYPool) * m));
+    HX_CUDA(c, dalloc_ipc(&c->upool, 2 * static_cast<size_t>(n) + 2 * static_cast<size_t>(m)));
+  } else {
+    HX_CUDA(c, dalloc(&c->xpool, static_cast<size_t>(kXPool) * n));
+    HX_CUDA(c, dalloc(&c->ypool, static_cast<size_t>(kYPool) * m));
+    HX_CUDA(c, dalloc(&c->upool, 2 * static_cast<size_t>(n) + 2 * static_cast<size_t>(m)));
+  }
   HX_CUDA(c, dalloc(&c->axpool, static_cast<size_t>(kAxPool) * m));
-  HX_CUDA(c, dalloc(&c->upool, 2 * static_cast<size_t>(n) + 2 * static_cast<size_t>(m)));
   if (c->ranked) {
     Team& T = c->team;
     for (int r = 0; r < kMaxRanks; ++r) T.px[r] = T.py[r] = T.pu[r] = T.ps[r] = nullptr, T.pb[r] = nullptr;
@@ -3322,8 +3378,8 @@ int hx_set_partition(hx_ctx* c, int32_t nranks, int32_t rank, int64_t row0, int6
   // slot regions hold every rank's records
   dfree(c->slots);
   c->slots = nullptr;
-  HX_CUDA(c, dalloc(&c->slots, static_cast<size_t>(kRegions) * kReplicas * kMaxQ * c->grid * nranks));
-  if (!c->rbar) HX_CUDA(c, dalloc(&c->rbar, 1));
+  HX_CUDA(c, dalloc_ipc(&c->slots, static_cast<size_t>(kRegions) * kReplicas * kMaxQ * c->grid * nranks));
+  if (!c->rbar) HX_CUDA(c, dalloc_ipc(&c->rbar, 1));
   HX_CUDA(c, cudaMemset(c->rbar, 0, sizeof(RankBar)));
   return HPLP_OK;
 }
