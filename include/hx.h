@@ -124,7 +124,11 @@ int hx_progress(hx_ctx* ctx, hx_progress_t* progress);
  * single-threaded); results equal the single-GPU solve within
  * reduction-order rounding.
  *
- * hx_set_partition  before hx_upload_csr (which still takes the FULL problem:
+ * hx_set_partition  before hx_upload_csr, with every rank's blocks (row_bounds
+ *                   and col_bounds, nranks + 1 entries: hplp_plan_partition's
+ *                   output); the upload derives which peers read each owned
+ *                   element, and pushes go only there.  hx_upload_csr still
+ *                   takes the FULL problem:
  *                   setup, power iteration and the boundary SpMVs run whole on
  *                   every rank, deterministically identical).  ctas = CTAs of
  *                   this rank (0 = one per SM; emulation splits one device).
@@ -141,8 +145,8 @@ int hx_progress(hx_ctx* ctx, hx_progress_t* progress);
  *                   missing rank into HPLP_ETIMEOUT).
  * Iterates and certificates read back from any rank are assembled from the
  * peers' blocks. */
-int hx_set_partition(hx_ctx* ctx, int32_t nranks, int32_t rank, int64_t row0, int64_t row1, int64_t col0,
-                     int64_t col1, int32_t ctas);
+int hx_set_partition(hx_ctx* ctx, int32_t nranks, int32_t rank, const int64_t* row_bounds,
+                     const int64_t* col_bounds, int32_t ctas);
 int hx_team_bind(hx_ctx** ctxs, int32_t count);
 /* nranks of the context's team (1 for a plain context). */
 int32_t hx_team_size(hx_ctx* ctx);

@@ -156,6 +156,12 @@ struct Team {
   double* pu[kMaxRanks];    // upool
   double* ps[kMaxRanks];    // slots
   RankBar* pb[kMaxRanks];   // cross-rank barrier words
+  // "needed by" rank masks of the owned elements: bit r of xneed[j - col0]
+  // is set when one of rank r's rows has column j (rank r gathers x+_j),
+  // bit r of yneed[i - row0] when one of rank r's columns has row i -- a
+  // push goes only to the ranks that read the element
+  const unsigned char* xneed;
+  const unsigned char* yneed;
 };
 
 // Slot regions (kMaxQ * grid doubles each).  A CTA may still be reading the
@@ -606,9 +612,9 @@ struct NoIn {};
 
 // Ranked epilogues push each owned element a peer gathers into every other
 // rank's pool at the same offset (P2P stores on a multi-GPU node).
-__device__ __forceinline__ void push_peers(const Team* T, double* const* base, size_t off, double v) {
+__device__ __forceinline__ void push_peers(const Team* T, double* const* base, size_t off, double v, unsigned mask) {
   for (int r = 0; r < T->nranks; ++r)
-    if (r != T->rank) base[r][off] = v;
+    if ((mask >> r) & 1u) base[r][off] = v;
 }
 
 template <bool RK>
@@ -641,7 +647,7 @@ struct EpiPrimal {  // phase A, rows of A^T
     double xn = x - eta * (aty + cj);
     xn = xn < 0.0 ? 0.0 : xn;
     xp[j] = xn;
-    if constexpr (RK) push_peers(T, T->px, xp_off + j, xn);
+    if constexpr (RK) push_peers(T, T->px, xp_off + j, xn, __ldg(T->xneed + (j - T->col0)));
     double rc = -(cj + aty);
     rc = rc < 0.0 ? 0.0 : rc;
     const double dx = x - xn;
@@ -683,7 +689,7 @@ struct EpiDual {  // phase B, rows of A
     yc[i] = yci;
     // only the combo -- the next y when there is no restart, which phase A
     // gathers speculatively; after a restart the loop pushes y+ itself
-    if constexpr (RK) push_peers(T, T->py, yc_off + i, yci);
+    if constexpr (RK) push_peers(T, T->py, yc_off + i, yci, __ldg(T->yneed + (i - T->row0)));
     axc[i] = omw * s + w * in.axa;
     const double d = axi - bi;
     const double dy = yi - ypi;
@@ -1359,9 +1365,17 @@ __device__ HX_PHASE_INLINE void cert_units(const KParams* P, const Roles* R, con
   owned_ranges<RK>(P, c0, c1, r0, r1);
   // u vectors are SpMV gather sources of the validation products: a ranked
   // CTA pushes its owned slices to the peers (same upool offsets)
-  auto put = [&](double* base, size_t off, double v) {
+  auto put = [&](double* base, size_t off, double v, unsigned mask) {
     base[off] = v;
-    if constexpr (RK) push_peers(&P->T, P->T.pu, off, v);
+    if constexpr (RK) push_peers(&P->T, P->T.pu, off, v, mask);
+  };
+  auto xmask = [&](int j) -> unsigned {
+    if constexpr (RK) return __ldg(P->T.xneed + (j - P->T.col0));
+    else return 0u;
+  };
+  auto ymask = [&](int i) -> unsigned {
+    if constexpr (RK) return __ldg(P->T.yneed + (i - P->T.row0));
+    else return 0u;
   };
   const double* zx = P->xpool + static_cast<size_t>(R->zx_out) * n;
   const double* xp = P->xpool + static_cast<size_t>(R->xp_out) * n;
@@ -1377,7 +1391,7 @@ __device__ HX_PHASE_INLINE void cert_units(const KParams* P, const Roles* R, con
     const double cj = __ldg(P->c + j);
     if (R->cand_on[0]) {
       const double u = (ldcg(xp + j) - x) / R->cn2[0];
-      put(P->upool, static_cast<size_t>(j), u);
+      put(P->upool, static_cast<size_t>(j), u, xmask(j));
       acc[0] = dmax(acc[0], fabs(u));
       acc[1] = dmax(acc[1], u);
       acc[2] = dmax(acc[2], -u);
@@ -1385,7 +1399,7 @@ __device__ HX_PHASE_INLINE void cert_units(const KParams* P, const Roles* R, con
     }
     if (R->cand_on[2]) {
       const double u = (s * (x - ldcg(xa + j))) / R->cn2[2];
-      put(P->upool, static_cast<size_t>(n) + j, u);
+      put(P->upool, static_cast<size_t>(n) + j, u, xmask(j));
       acc[4] = dmax(acc[4], fabs(u));
       acc[5] = dmax(acc[5], u);
       acc[6] = dmax(acc[6], -u);
@@ -1397,13 +1411,13 @@ __device__ HX_PHASE_INLINE void cert_units(const KParams* P, const Roles* R, con
     const double bi = __ldg(P->b + i);
     if (R->cand_on[1]) {
       const double u = (ldcg(yp + i) - y) / R->cn2[1];
-      put(P->upool, 2 * static_cast<size_t>(n) + i, u);
+      put(P->upool, 2 * static_cast<size_t>(n) + i, u, ymask(i));
       acc[8] = dmax(acc[8], fabs(u));
       acc[9] += bi * u;
     }
     if (R->cand_on[3]) {
       const double u = (s * (y - ldcg(ya + i))) / R->cn2[3];
-      put(P->upool, 2 * static_cast<size_t>(n) + m + i, u);
+      put(P->upool, 2 * static_cast<size_t>(n) + m + i, u, ymask(i));
       acc[10] = dmax(acc[10], fabs(u));
       acc[11] += bi * u;
     }
@@ -2148,7 +2162,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
         const double* yv = P->ypool + static_cast<size_t>(R->y_cur) * P->m;
         const size_t off = static_cast<size_t>(R->y_cur) * P->m;
         for (int i = P->T.row0 + g.cta * kThreads + threadIdx.x; i < P->T.row1; i += g.nctas * kThreads)
-          push_peers(&P->T, P->T.py, off + i, ldcg(yv + i));
+          push_peers(&P->T, P->T.py, off + i, ldcg(yv + i), __ldg(P->T.yneed + (i - P->T.row0)));
         if (!sync()) return;
         synced = true;
       }
@@ -2457,6 +2471,8 @@ struct hx_ctx {
   int prow0[kMaxRanks] = {}, prow1[kMaxRanks] = {};  // every rank's row block
   DevSched pa, pt;                   // rows [row0,row1) of A, [col0,col1) of A^T
   RankBar* rbar = nullptr;
+  unsigned char* xneed = nullptr;    // masks of Team::xneed / yneed (device)
+  unsigned char* yneed = nullptr;
   unsigned long long team_epochs = 0;
   std::vector<hx_ctx*> local_team;   // ranks launched together (same device), rank order
   std::vector<void*> ipc_open;       // peer mappings to close
@@ -2875,7 +2891,7 @@ void hx_destroy(hx_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
-  dfree(c->rbar);
+  dfree(c->rbar), dfree(c->xneed), dfree(c->yneed);
   free_problem(c);
   dfree(c->slots), dfree(c->scratch), dfree(c->ctl), dfree(c->bar), dfree(c->epochs), dfree(c->kparams), dfree(c->prof);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -3009,6 +3025,35 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
       rc = upload_sched(c, c->pt, pt.data(), T.col1 - T.col0, static_cast<int>(m), c->t_ptr, c->t_idx, c->t_val, lead,
                         T.col0);
       if (rc) return rc;
+      // who gathers what: x+_j is read by the owners of the rows in column j,
+      // y_i by the owners of the columns in row i
+      if (c->prow1[T.nranks - 1] != m || c->pcol1[T.nranks - 1] != n)
+        return set_err(c, HPLP_EINVAL, "hx_upload_csr: the partition does not cover the problem");
+      auto owner = [&](const int* lo, int v) {
+        int r = 0;
+        while (r + 1 < T.nranks && v >= lo[r + 1]) ++r;
+        return r;
+      };
+      std::vector<unsigned char> xm(static_cast<size_t>(T.col1 - T.col0), 0), ym(static_cast<size_t>(T.row1 - T.row0), 0);
+      for (int64_t i = 0; i < m; ++i) {
+        const int oi = owner(c->prow0, static_cast<int>(i));
+        const bool own_row = i >= T.row0 && i < T.row1;
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+          const int j = col_idx[p];
+          if (oi != T.rank && j >= T.col0 && j < T.col1) xm[j - T.col0] |= static_cast<unsigned char>(1u << oi);
+          if (own_row) {
+            const int oj = owner(c->pcol0, j);
+            if (oj != T.rank) ym[i - T.row0] |= static_cast<unsigned char>(1u << oj);
+          }
+        }
+      }
+      dfree(c->xneed), dfree(c->yneed);
+      HX_CUDA(c, dalloc(&c->xneed, xm.size()));
+      HX_CUDA(c, dalloc(&c->yneed, ym.size()));
+      if (!xm.empty()) HX_CUDA(c, cudaMemcpy(c->xneed, xm.data(), xm.size(), cudaMemcpyHostToDevice));
+      if (!ym.empty()) HX_CUDA(c, cudaMemcpy(c->yneed, ym.data(), ym.size(), cudaMemcpyHostToDevice));
+      T.xneed = c->xneed;
+      T.yneed = c->yneed;
     }
   }
   if (c->ranked) {  // peers map these through CUDA IPC
@@ -3026,8 +3071,6 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     for (int r = 0; r < kMaxRanks; ++r) T.px[r] = T.py[r] = T.pu[r] = T.ps[r] = nullptr, T.pb[r] = nullptr;
     T.px[T.rank] = c->xpool, T.py[T.rank] = c->ypool, T.pu[T.rank] = c->upool, T.ps[T.rank] = c->slots;
     T.pb[T.rank] = c->rbar;
-    c->pcol0[T.rank] = T.col0, c->pcol1[T.rank] = T.col1;
-    c->prow0[T.rank] = T.row0, c->prow1[T.rank] = T.row1;
     c->local_team.assign(1, c);
   }
   // ||b||, ||c|| once (loop invariants of src/pdhg_core.cpp:60,62).
@@ -3354,13 +3397,18 @@ int hx_run(hx_ctx* c, int64_t max_iters, hx_progress_t* p) {
 }
 
 // ---- row-partitioned team (include/hx.h) ---------------------------------
-int hx_set_partition(hx_ctx* c, int32_t nranks, int32_t rank, int64_t row0, int64_t row1, int64_t col0,
-                     int64_t col1, int32_t ctas) {
+int hx_set_partition(hx_ctx* c, int32_t nranks, int32_t rank, const int64_t* row_bounds, const int64_t* col_bounds,
+                     int32_t ctas) {
   if (c->uploaded) return set_err(c, HPLP_ESTATE, "hx_set_partition: call before hx_upload_csr");
-  if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks)
-    return set_err(c, HPLP_EINVAL, "hx_set_partition: need 1 <= nranks <= 8 and 0 <= rank < nranks");
-  if (row0 < 0 || row1 < row0 || col0 < 0 || col1 < col0 || row1 >= (int64_t{1} << 31) || col1 >= (int64_t{1} << 31))
-    return set_err(c, HPLP_EINVAL, "hx_set_partition: bad row / column block");
+  if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks || !row_bounds || !col_bounds)
+    return set_err(c, HPLP_EINVAL, "hx_set_partition: need 1 <= nranks <= 8, 0 <= rank < nranks and the bounds");
+  for (int r = 0; r < nranks; ++r)
+    if (row_bounds[r] < 0 || row_bounds[r + 1] < row_bounds[r] || col_bounds[r] < 0 ||
+        col_bounds[r + 1] < col_bounds[r] || row_bounds[r + 1] >= (int64_t{1} << 31) ||
+        col_bounds[r + 1] >= (int64_t{1} << 31) || row_bounds[0] != 0 || col_bounds[0] != 0)
+      return set_err(c, HPLP_EINVAL, "hx_set_partition: bounds must ascend from 0 (nranks + 1 entries each)");
+  const int64_t row0 = row_bounds[rank], row1 = row_bounds[rank + 1];
+  const int64_t col0 = col_bounds[rank], col1 = col_bounds[rank + 1];
   int occ = 0;
   HX_CUDA(c, cudaSetDevice(c->device));
   HX_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, loop_kernel_team, kThreads, kStageBytes));
@@ -3372,7 +3420,11 @@ int hx_set_partition(hx_ctx* c, int32_t nranks, int32_t rank, int64_t row0, int6
   c->team.rank = rank, c->team.nranks = nranks, c->team.grp_ctas = c->grid;
   c->team.row0 = static_cast<int>(row0), c->team.row1 = static_cast<int>(row1);
   c->team.col0 = static_cast<int>(col0), c->team.col1 = static_cast<int>(col1);
-  for (int r = 0; r < kMaxRanks; ++r) c->pcol0[r] = c->pcol1[r] = 0;
+  for (int r = 0; r < kMaxRanks; ++r) c->pcol0[r] = c->pcol1[r] = c->prow0[r] = c->prow1[r] = 0;
+  for (int r = 0; r < nranks; ++r) {
+    c->prow0[r] = static_cast<int>(row_bounds[r]), c->prow1[r] = static_cast<int>(row_bounds[r + 1]);
+    c->pcol0[r] = static_cast<int>(col_bounds[r]), c->pcol1[r] = static_cast<int>(col_bounds[r + 1]);
+  }
   c->local_team.clear();
   c->team_epochs = 0;
   // slot regions hold every rank's records
@@ -3426,14 +3478,17 @@ int hx_team_bind(hx_ctx** ctxs, int32_t count) {
           cudaGetLastError();
         }
   }
+  for (hx_ctx* c : by)
+    for (int r = 0; r < count; ++r)
+      if (c->pcol0[r] != by[r]->team.col0 || c->pcol1[r] != by[r]->team.col1 || c->prow0[r] != by[r]->team.row0 ||
+          c->prow1[r] != by[r]->team.row1)
+        return set_err(c, HPLP_EINVAL, "hx_team_bind: ranks were given different partitions");
   for (hx_ctx* c : by) {
     Team& T = c->team;
     T.sys = one_device ? 0 : 1;
     for (int r = 0; r < count; ++r) {
       T.px[r] = by[r]->xpool, T.py[r] = by[r]->ypool, T.pu[r] = by[r]->upool, T.ps[r] = by[r]->slots;
       T.pb[r] = by[r]->rbar;
-      c->pcol0[r] = by[r]->team.col0, c->pcol1[r] = by[r]->team.col1;
-      c->prow0[r] = by[r]->team.row0, c->prow1[r] = by[r]->team.row1;
     }
     c->local_team = by;
   }
@@ -3478,8 +3533,9 @@ int hx_team_import(hx_ctx* c, const void* blob, int64_t size) {
     return set_err(c, HPLP_EINVAL, "hx_team_import: blob of another team");
   if (b.m != c->m || b.n != c->n || b.nnz != c->nnz || b.grid != c->grid)
     return set_err(c, HPLP_EINVAL, "hx_team_import: ranks disagree on the problem or the CTA count");
-  c->pcol0[b.rank] = b.col0, c->pcol1[b.rank] = b.col1;
-  c->prow0[b.rank] = b.row0, c->prow1[b.rank] = b.row1;
+  if (c->pcol0[b.rank] != b.col0 || c->pcol1[b.rank] != b.col1 || c->prow0[b.rank] != b.row0 ||
+      c->prow1[b.rank] != b.row1)
+    return set_err(c, HPLP_EINVAL, "hx_team_import: the peer was given a different partition");
   if (b.rank == c->team.rank) return HPLP_OK;
   HX_CUDA(c, cudaSetDevice(c->device));
   void* p[5] = {};
@@ -3544,6 +3600,7 @@ int hx_get_iterate(hx_ctx* c, int32_t which, double* x, double* y) {
       }
       if (C.x_best < 0) return set_err(c, HPLP_ESTATE, "hx_get_iterate: no best iterate yet");
       if (int rc = assemble_x(c, C.x_best)) return rc;
+      if (int rc = assemble_y(c, C.y_best)) return rc;
       dx = xbuf(c, C.x_best), dy = ybuf(c, C.y_best);
       break;
     case HX_ITERATE_LAST:  // the traced candidate (z, or the average for the averaged baselines)
@@ -3553,9 +3610,11 @@ int hx_get_iterate(hx_ctx* c, int32_t which, double* x, double* y) {
         break;
       }
       if (int rc = assemble_x(c, C.last_zx)) return rc;
+      if (int rc = assemble_y(c, C.last_y)) return rc;
       dx = xbuf(c, C.last_zx), dy = ybuf2(c, C.last_y, C.last_y_avg);
       break;
     case HX_ITERATE_NEXT:
+      if (int rc = assemble_x(c, C.last_xp)) return rc;
       if (int rc = assemble_y(c, C.last_yp)) return rc;
       dx = xbuf(c, C.last_xp), dy = ybuf(c, C.last_yp);
       break;
@@ -3564,10 +3623,16 @@ int hx_get_iterate(hx_ctx* c, int32_t which, double* x, double* y) {
         dx = xbuf2(c, C.final_avg, 1), dy = ybuf2(c, C.final_avg, 1);
       } else if (C.status >= 0 && C.final_x >= 0) {
         if (int rc = assemble_x(c, C.final_x)) return rc;
+        if (int rc = assemble_y(c, C.final_y)) return rc;
         dx = xbuf(c, C.final_x), dy = ybuf(c, C.final_y);
       } else if (C.r.x_mode == 0) {
+        if (int rc = assemble_x(c, C.r.x_src)) return rc;
+        if (int rc = assemble_y(c, C.r.y_cur)) return rc;
         dx = xbuf2(c, C.r.x_src, C.r.x_src_avg), dy = ybuf2(c, C.r.y_cur, C.r.y_cur_avg);
       } else {
+        if (int rc = assemble_x(c, C.r.x_src)) return rc;
+        if (int rc = assemble_x(c, C.r.x_anchor)) return rc;
+        if (int rc = assemble_y(c, C.r.y_cur)) return rc;
         double* tmp = c->upool;
         combine_kernel<<<4 * c->sm_count, 256, 0, s>>>(static_cast<int>(c->n), C.r.w_x, xbuf(c, C.r.x_src),
                                                        xbuf(c, C.r.x_anchor), tmp);
@@ -3594,11 +3659,12 @@ int hx_get_certificate(hx_ctx* c, int32_t kind, double* vec) {
   const double* q;
   if (is_x) {
     if (int rc = assemble_x(c, C.last_zx)) return rc;
+    if (int rc = assemble_x(c, normalized ? C.last_xa : C.last_xp)) return rc;
     p = xbuf(c, C.last_zx);
     q = normalized ? xbuf(c, C.last_xa) : xbuf(c, C.last_xp);
   } else {
-    if (!normalized)
-      if (int rc = assemble_y(c, C.last_yp)) return rc;
+    if (int rc = assemble_y(c, normalized ? C.last_ya : C.last_yp)) return rc;
+    if (int rc = assemble_y(c, C.last_y)) return rc;
     p = ybuf2(c, C.last_y, C.last_y_avg);
     q = normalized ? ybuf(c, C.last_ya) : ybuf(c, C.last_yp);
   }
@@ -3629,6 +3695,7 @@ int hx_trace_extras(hx_ctx* c, double* aty, double* c_out, double* cand_norm_nor
       src = c->tavg + static_cast<size_t>(C.last_cand_avg) * c->n;
     } else {
       double* dout = c->upool;
+      if (int r2 = assemble_y(c, C.last_y)) return r2;
       int rc = spmv_dev(c, true, ybuf2(c, C.last_y, C.last_y_avg), dout);
       if (rc) return rc;
       src = dout;
@@ -3668,6 +3735,9 @@ int hx_kkt_current(hx_ctx* c, hplp_kkt_t* out) {
   double* xcur = c->upool;
   double* aty = c->upool + c->n;
   double* ax = c->upool + 2 * c->n;
+  if (int rc = assemble_x(c, C.r.x_src)) return rc;
+  if (int rc = assemble_x(c, C.r.x_anchor)) return rc;
+  if (int rc = assemble_y(c, C.r.y_cur)) return rc;
   const double* ycur = ybuf2(c, C.r.y_cur, C.r.y_cur_avg);
   if (C.r.x_mode == 0) {
     HX_CUDA(c, cudaMemcpyAsync(xcur, xbuf2(c, C.r.x_src, C.r.x_src_avg), c->n * sizeof(double),

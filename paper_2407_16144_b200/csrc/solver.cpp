@@ -274,7 +274,7 @@ Solver::Solver(const std::vector<int>& devices, int nranks, int64_t m, int64_t n
       hx_device_info(ctx, nullptr, &grid, nullptr);
       ctas = sharing > 1 ? std::max(1, grid / sharing) : 0;
     }
-    rc = hx_set_partition(ctx, nranks, r, rb[r], rb[r + 1], cb[r], cb[r + 1], ctas);
+    rc = hx_set_partition(ctx, nranks, r, rb.data(), cb.data(), ctas);
     if (rc != HPLP_OK) fail(ctx, rc);
     rc = hx_upload_csr(ctx, m, n, row_ptr, col_idx, val, b, c);
     if (rc != HPLP_OK) fail(ctx, rc);
@@ -293,7 +293,7 @@ Solver::Solver(int device, int nranks, int rank, int64_t m, int64_t n, const int
     throw std::invalid_argument("Solver: partition plan failed");
   int rc = hx_create(device, &ctx_);
   if (rc != HPLP_OK) throw_hx(nullptr, rc);
-  rc = hx_set_partition(ctx_, nranks, rank, rb[rank], rb[rank + 1], cb[rank], cb[rank + 1], 0);
+  rc = hx_set_partition(ctx_, nranks, rank, rb.data(), cb.data(), 0);
   if (rc == HPLP_OK) rc = hx_upload_csr(ctx_, m, n, row_ptr, col_idx, val, b, c);
   if (rc != HPLP_OK) {
     const std::string msg = hx_last_error(ctx_);

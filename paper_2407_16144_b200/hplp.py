@@ -113,7 +113,7 @@ def lib() -> C.CDLL:
     sig("hx_sched_tasks", C.c_int, V, I32, C.POINTER(C.c_int32), I64, C.POINTER(C.c_int64))
     sig("hx_precondition", C.c_int, V, I32, D, PD, PD)
     sig("hx_download_problem", C.c_int, V, PI64, PI32, PD, PD, PD)
-    sig("hx_set_partition", C.c_int, V, I32, I32, I64, I64, I64, I64, I32)
+    sig("hx_set_partition", C.c_int, V, I32, I32, PI64, PI64, I32)
     sig("hx_team_bind", C.c_int, PV, I32)
     sig("hx_team_export", C.c_int, V, C.c_char_p, I64, PI64)
     sig("hx_team_import", C.c_int, V, C.c_char_p, I64)
@@ -470,9 +470,12 @@ class HX:
         return rp, ci, v, b, c
 
     # ---- row-partitioned team (include/hx.h) ----
-    def set_partition(self, nranks, rank, row0, row1, col0, col1, ctas=0):
-        self._c(lib().hx_set_partition(self.h, int(nranks), int(rank), int(row0), int(row1), int(col0), int(col1),
-                                       int(ctas)))
+    def set_partition(self, nranks, rank, row_bounds, col_bounds, ctas=0):
+        """hx_set_partition: this context is rank `rank` of the partition given
+        by row_bounds / col_bounds (nranks + 1 entries each)."""
+        rb = np.ascontiguousarray(row_bounds, np.int64)
+        cb = np.ascontiguousarray(col_bounds, np.int64)
+        self._c(lib().hx_set_partition(self.h, int(nranks), int(rank), i64ptr(rb), i64ptr(cb), int(ctas)))
 
     def team_export(self) -> bytes:
         size = C.c_int64()

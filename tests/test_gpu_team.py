@@ -127,7 +127,7 @@ def test_team_low_level_api(gpu_required):
     hxs = [hplp.HX(device=0) for _ in range(2)]
     grid = hxs[0].info()["grid"]
     for r, h in enumerate(hxs):
-        h.set_partition(2, r, rb[r], rb[r + 1], cb[r], cb[r + 1], grid // 2)
+        h.set_partition(2, r, rb, cb, grid // 2)
         h.upload(*csr_args(s))
     assert len(hxs[0].team_export()) > 0
     with pytest.raises(hplp.HplpError):  # not bound yet: the peers are unknown
@@ -149,7 +149,9 @@ def test_team_low_level_api(gpu_required):
     x1, y1 = hxs[1].get_iterate(hplp.ITERATE_BEST)
     assert np.array_equal(x0, x1) and np.array_equal(y0, y1)
     with pytest.raises(ValueError):
-        hplp.HX(device=0).set_partition(9, 0, 0, 1, 0, 1)
+        hplp.HX(device=0).set_partition(9, 0, [0, 1], [0, 1])
+    with pytest.raises(ValueError):  # bounds must ascend from 0
+        hplp.HX(device=0).set_partition(2, 0, [0, 5, 3], [0, 1, 2])
     for h in hxs:
         h.close()
 
