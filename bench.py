@@ -39,7 +39,9 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-CONFIG_ID = 1
+CONFIG_ID = 1  # --config overrides (e.g. 4: the 100M-nnz instance the north star's 8-GPU claim is quoted on)
+WORKLOADS = {0: "configs[0] small planted LP", 1: "configs[1] medium planted LP", 2: "configs[2] infeasible LP",
+             3: "configs[3] transportation LP", 4: "configs[4] large Zipf planted LP"}
 ITERS_PER_STEP = 1000
 E2E_ITERS = 5000
 METRIC = "rHPDHG iters/sec & time-to-1e-4 rel KKT (1/2/4/8 B200) vs CPU; % HBM roofline"
@@ -177,11 +179,11 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "device": "cpu", "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded planted LP, configs[1])",
-        "config": {"workload": f"configs[{CONFIG_ID}] medium planted LP, standard form {s.m}x{s.n}, nnz {s.nnz}",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": f"synthetic (seeded, BASELINE configs[{CONFIG_ID}])",
+        "config": {"workload": f"{WORKLOADS[CONFIG_ID]}, standard form {s.m}x{s.n}, nnz {s.nnz}",
                    "iters_per_step": iters, "parallelism": "none (single-threaded reference)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind,
-                         "sample": f"{args.steps} x solve(iteration_limit={iters}) on configs[1]; power iteration "
+                         "sample": f"{args.steps} x solve(iteration_limit={iters}) on configs[{CONFIG_ID}]; power iteration "
                                    f"({pit} its, {t_power:.2f}s) timed separately and subtracted"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -258,7 +260,7 @@ def run_gpu(args):
     peak *= world  # sharded: the aggregate HBM of the N GPUs
     per_launch_s = elapsed / args.steps
     achieved = b_iter * ITERS_PER_STEP / per_launch_s / 1e9
-    traffic, prof = traffic_from_profile()
+    traffic, prof = traffic_from_profile() if CONFIG_ID == 1 else (None, None)
 
     # e2e through the public C ABI from host buffers (upload + setup + loop + download)
     e2e_times = []
@@ -330,7 +332,7 @@ def run_gpu(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         kind, cval, info = cpu_iters_per_sec(s, args.cpu_iters)
         cpu = {"value": cval, "unit": UNIT, "cores": 1, "kind": kind,
-               "sample": f"solve(iteration_limit={args.cpu_iters}) on configs[1], single thread; power iteration "
+               "sample": f"solve(iteration_limit={args.cpu_iters}) on configs[{CONFIG_ID}], single thread; power iteration "
                          f"({info['power_iterations']} its, {info['power_seconds']:.2f}s) timed separately and "
                          f"subtracted"}
 
@@ -339,8 +341,8 @@ def run_gpu(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded planted LP, BASELINE configs[1]; MIPLIB not available)",
-            "config": {"workload": f"configs[{CONFIG_ID}] medium planted LP, standard form {m}x{n}, nnz {nnz}",
+            "data": f"synthetic (seeded, BASELINE configs[{CONFIG_ID}]; MIPLIB not available)",
+            "config": {"workload": f"{WORKLOADS[CONFIG_ID]}, standard form {m}x{n}, nnz {nnz}",
                        "iters_per_step": ITERS_PER_STEP, "l2": "flushed (256 MiB write) before every timed step",
                        "parallelism": "single GPU" if world == 1 else
                        f"row-partitioned x{world}: one LP, rows/columns split by nnz, slices pushed over NVLink P2P"},
@@ -381,11 +383,25 @@ def main():
     ap.add_argument("--ttt-cap", type=float, default=60.0)
     ap.add_argument("--no-ttt", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--config", type=int, default=1, choices=sorted(WORKLOADS),
+                    help="BASELINE.json config to run (default 1, the metric's config; 4 = 100M nnz for 8-GPU scaling)")
+    ap.add_argument("--iters-per-step", type=int, default=None, help="iterations per timed step (default 1000)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-partitioned rank path even at N=1 (test of the N>1 code path)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    global CONFIG_ID, ITERS_PER_STEP, E2E_ITERS
+    CONFIG_ID = args.config
+    if args.iters_per_step:
+        ITERS_PER_STEP = args.iters_per_step
+    elif CONFIG_ID == 4:
+        ITERS_PER_STEP = 100  # ~0.3 s per step on one B200
+    if CONFIG_ID != 1:  # time-to-tolerance, the traffic capture and the sample sizes are configs[1]'s
+        args.no_ttt = True
+        E2E_ITERS = 500 if CONFIG_ID == 4 else E2E_ITERS
+        args.cpu_iters = min(args.cpu_iters, 5 if CONFIG_ID == 4 else args.cpu_iters)
+        args.ref_iters = min(args.ref_iters, 3 if CONFIG_ID == 4 else args.ref_iters)
     if args.impl == "reference":
         return run_reference(args)
     return run_gpu(args)
