@@ -246,3 +246,57 @@ def test_trace_diagnostics_parity(gpu_required):
             assert abs(a - b) <= 1e-9 * max(abs(b), 1e-300), (tc["iteration"], a, b)
         assert sum(len(p) for p in tg["partition"]) == s.n
     assert flips <= 2
+
+
+def _ragged_lp(seed=11, m=600, n=90000):
+    """Empty rows and columns, 1-entry rows, a 70k-entry row and a dense-ish
+    column: every task kind (stream rows, single pieces, multi-piece long rows
+    folded by their owner CTA) in one matrix."""
+    rng = np.random.default_rng(seed)
+    rows = []
+    for i in range(m):
+        if i % 97 == 0:
+            rows.append([])  # empty row
+        elif i == 5:
+            rows.append(sorted(rng.choice(n, 70000, replace=False).tolist()))  # very long row
+        elif i % 7 == 0:
+            rows.append([int(rng.integers(n))])  # single entry
+        else:
+            cols = set(rng.choice(n, int(rng.integers(2, 60)), replace=False).tolist())
+            cols.add(17)  # a column present in most rows
+            rows.append(sorted(cols))
+    rp = [0]
+    ci, v = [], []
+    for r in rows:
+        ci += r
+        v += rng.normal(size=len(r)).tolist()
+        rp.append(len(ci))
+    x0 = rng.random(n)
+    A_x0 = np.array([sum(v[p] * x0[ci[p]] for p in range(rp[i], rp[i + 1])) for i in range(m)])
+    c = rng.random(n) + 0.1
+    return m, n, np.array(rp, np.int64), np.array(ci, np.int32), np.array(v), A_x0, c
+
+
+def test_ragged_structure_parity(gpu_required):
+    args = _ragged_lp()
+    cpu = CpuLp("port", *args).solve(iteration_limit=100, tolerance=1e-12, trace=True)
+    gpu = hplp.solve(*args, iteration_limit=100, tolerance=1e-12, trace=True)
+    _trace_cmp(gpu["trace"], cpu["trace"])
+    assert gpu["spmv_count"] == cpu["spmv_count"]
+    cpu_s = CpuLp("port", *args)
+    rng = np.random.default_rng(5)
+    x, y = rng.normal(size=args[1]), rng.normal(size=args[0])
+    h = hplp.HX(device=0)
+    h.upload(*args)
+    assert rel_inf(h.spmv(x), cpu_s.spmv(x)) <= 1e-13
+    assert rel_inf(h.spmv_transpose(y), cpu_s.spmv_transpose(y)) <= 1e-13
+    h.close()
+
+
+def test_ragged_structure_team_parity(gpu_required):
+    args = _ragged_lp()
+    cpu = CpuLp("port", *args).solve(iteration_limit=60, tolerance=1e-12, trace=True)
+    t = hplp.Solver.team(*args, nranks=3)
+    gpu = t.solve(iteration_limit=60, tolerance=1e-12, trace=True)
+    t.close()
+    _trace_cmp(gpu["trace"], cpu["trace"])
