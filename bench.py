@@ -386,6 +386,14 @@ def run_gpu(args):
                          "kernel": "hx::loop_kernel" if world == 1 else "hx::loop_kernel_team",
                          "algorithmic_bytes_per_iter": b_iter, "peak_source": peak_kind,
                          "frac_of_8TBs": achieved / (8000.0 * world)},
+            # the access-pattern ceiling: every nonzero is one random fp64 gather
+            # per SpMV; tools/dsmem_micro.cu measured ~290 G random gathers/s on
+            # B200 whatever the number in flight (about one per SM per cycle),
+            # so 2 * nnz gathers cost at least this much per iteration
+            "gather_roofline": {"gathers_per_iter": 2 * nnz, "ceiling_gathers_per_s": 290e9,
+                                "source": "tools/dsmem_micro.cu (profiles/r01s2_gather_ceiling.txt)",
+                                "floor_us_per_iter": 2 * nnz / 290e9 * 1e6,
+                                "frac": (2 * nnz / 290e9) / (elapsed / iters_done)},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "iters_per_step": E2E_ITERS,
