@@ -391,7 +391,9 @@ def run_gpu(args):
             # B200 whatever the number in flight (about one per SM per cycle),
             # so 2 * nnz gathers cost at least this much per iteration
             "gather_roofline": {"gathers_per_iter": 2 * nnz, "ceiling_gathers_per_s": 290e9,
-                                "source": "tools/dsmem_micro.cu (profiles/r01s2_gather_ceiling.txt)",
+                                "source": "tools/dsmem_micro.cu (profiles/r01s2_gather_ceiling.txt); every nonzero "
+                                          "counted as a random gather (bound/slack entries coalesce, so the true "
+                                          "floor is somewhat lower)",
                                 "floor_us_per_iter": 2 * nnz / 290e9 * 1e6,
                                 "frac": (2 * nnz / 290e9) / (elapsed / iters_done)},
             "cpu_baseline": cpu,
