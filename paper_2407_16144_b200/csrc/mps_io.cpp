@@ -17,6 +17,7 @@
 //    infinities as "inf" / "-inf", vectors above a threshold elided with an
 //    explicit flag, wall time segregated under "timing".
 //  * write_trace_csv: fixed header, one row per TraceRecord.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -60,14 +61,28 @@ std::string trim(const std::string& s) {
 }
 
 // Fixed-format MPS fields (1-based columns 2-3, 5-12, 15-22, 25-36, 40-47,
-// 50-61); used when a line does not tokenize as free format.
+// 50-61); used when a line does not tokenize as free format.  Name fields are
+// positional (they may hold blanks); a numeric field is the token starting in
+// its columns, so a 17-significant-digit number may run past column 36 (the
+// writer then puts one pair per line).
 std::vector<std::string> fixed_fields(const std::string& line) {
   static const int kStart[] = {1, 4, 14, 24, 39, 49};
   static const int kLen[] = {2, 8, 8, 12, 8, 12};
   std::vector<std::string> f;
+  int consumed = 0;  // end of the last numeric token
   for (int k = 0; k < 6; ++k) {
-    if (static_cast<int>(line.size()) <= kStart[k]) break;
-    f.push_back(trim(line.substr(kStart[k], kLen[k])));
+    const int start = std::max(kStart[k], consumed);
+    if (static_cast<int>(line.size()) <= start) break;
+    if (k == 3 || k == 5) {  // numeric: the token from here to the next blank
+      int b = start;
+      while (b < static_cast<int>(line.size()) && line[b] == ' ') ++b;
+      int e = b;
+      while (e < static_cast<int>(line.size()) && line[e] != ' ') ++e;
+      f.push_back(line.substr(b, e - b));
+      consumed = e;
+    } else {
+      f.push_back(trim(line.substr(start, kLen[k] - (start - kStart[k]) > 0 ? kLen[k] - (start - kStart[k]) : 0)));
+    }
   }
   while (!f.empty() && f.back().empty()) f.pop_back();
   return f;
@@ -556,17 +571,50 @@ GeneralFormLP parse_mps_file(const std::string& path, MpsDocument* doc) {
 
 std::string write_mps(const GeneralFormLP& g) {
   const Index m = g.num_rows(), n = g.num_cols();
-  auto rname = [&](Index i) { return g.rows[i].name.empty() ? "R" + std::to_string(i) : g.rows[i].name; };
-  auto cname = [&](Index j) { return g.columns[j].name.empty() ? "C" + std::to_string(j) : g.columns[j].name; };
-  const std::string obj = g.objective_name.empty() ? "OBJ" : g.objective_name;
+  auto raw_r = [&](Index i) { return g.rows[i].name.empty() ? "R" + std::to_string(i) : g.rows[i].name; };
+  auto raw_c = [&](Index j) { return g.columns[j].name.empty() ? "C" + std::to_string(j) : g.columns[j].name; };
+  const std::string raw_obj = g.objective_name.empty() ? "OBJ" : g.objective_name;
+  // Names with blanks only survive in fixed format (8-character fields); if
+  // one does not fit, free format with the blanks replaced by '_'.
+  bool blanks = raw_obj.find(' ') != std::string::npos, fits = raw_obj.size() <= 8;
+  for (Index i = 0; i < m; ++i) blanks |= raw_r(i).find(' ') != std::string::npos, fits &= raw_r(i).size() <= 8;
+  for (Index j = 0; j < n; ++j) blanks |= raw_c(j).find(' ') != std::string::npos, fits &= raw_c(j).size() <= 8;
+  const bool fixed = blanks && fits;
+  auto clean = [&](std::string s) {
+    if (!fixed)
+      for (char& ch : s)
+        if (ch == ' ') ch = '_';
+    return s;
+  };
+  auto rname = [&](Index i) { return clean(raw_r(i)); };
+  auto cname = [&](Index j) { return clean(raw_c(j)); };
+  const std::string obj = clean(raw_obj);
+  // one data line: fields at 1-based columns 2, 5, 15, 25, 40, 50 (fixed) or
+  // blank separated (free)
+  auto line = [&](std::initializer_list<std::string> f) {
+    static const int kStart[] = {1, 4, 14, 24, 39, 49};
+    std::string l;
+    int k = 0;
+    for (const std::string& x : f) {
+      if (fixed) {
+        if (static_cast<int>(l.size()) < kStart[k]) l.resize(kStart[k], ' ');
+        else if (!x.empty() && k > 0) l += ' ';
+        l += x;
+      } else if (!x.empty()) {
+        l += (k == 0 ? " " : (k == 1 && l.empty() ? "    " : " ")) + x;
+      }
+      ++k;
+    }
+    return l + "\n";
+  };
   std::string o = "NAME " + g.name + "\n";
   if (g.maximize) o += "OBJSENSE\n    MAX\n";
-  o += "ROWS\n N " + obj + "\n";
+  o += "ROWS\n" + line({"N", obj});
   for (Index i = 0; i < m; ++i) {
     const char* t = g.rows[i].relation == RowRelation::kLessEqual      ? "L"
                     : g.rows[i].relation == RowRelation::kGreaterEqual ? "G"
                                                                        : "E";
-    o += std::string(" ") + t + " " + rname(i) + "\n";
+    o += line({t, rname(i)});
   }
   o += "COLUMNS\n";
   // entries grouped by column, in their order within the column
@@ -575,34 +623,37 @@ std::string write_mps(const GeneralFormLP& g) {
     if (t.row < 0 || t.row >= m || t.col < 0 || t.col >= n) throw std::invalid_argument("write_mps: entry out of range");
     by_col[t.col].push_back({t.row, t.value});
   }
+  // fixed fields are 12 characters wide for numbers: %.17g needs up to 24, so
+  // fixed-format numbers are written in free-form positions after the field
+  // start (the reader takes fields by position up to the next one)
   for (Index j = 0; j < n; ++j) {
     const double cj = j < static_cast<Index>(g.objective.size()) ? g.objective[j] : 0.0;
-    if (cj != 0.0 || by_col[j].empty()) o += "    " + cname(j) + " " + obj + " " + num17(cj) + "\n";
-    for (const auto& [i, v] : by_col[j]) o += "    " + cname(j) + " " + rname(i) + " " + num17(v) + "\n";
+    if (cj != 0.0 || by_col[j].empty()) o += line({"", cname(j), obj, num17(cj)});
+    for (const auto& [i, v] : by_col[j]) o += line({"", cname(j), rname(i), num17(v)});
   }
   o += "RHS\n";
-  if (g.objective_constant != 0.0) o += "    RHS " + obj + " " + num17(-g.objective_constant) + "\n";
+  if (g.objective_constant != 0.0) o += line({"", "RHS", obj, num17(-g.objective_constant)});
   for (Index i = 0; i < m; ++i)
-    if (g.rows[i].rhs != 0.0) o += "    RHS " + rname(i) + " " + num17(g.rows[i].rhs) + "\n";
+    if (g.rows[i].rhs != 0.0) o += line({"", "RHS", rname(i), num17(g.rows[i].rhs)});
   bool any_range = false;
   for (Index i = 0; i < m; ++i) any_range |= g.rows[i].range.has_value();
   if (any_range) {
     o += "RANGES\n";
     for (Index i = 0; i < m; ++i)
-      if (g.rows[i].range) o += "    RNG " + rname(i) + " " + num17(*g.rows[i].range) + "\n";
+      if (g.rows[i].range) o += line({"", "RNG", rname(i), num17(*g.rows[i].range)});
   }
   o += "BOUNDS\n";
   for (Index j = 0; j < n; ++j) {
     const double lo = g.columns[j].lower, up = g.columns[j].upper;
     const std::string c = cname(j);
     if (lo == -kInf && up == kInf) {
-      o += " FR BND " + c + "\n";
+      o += line({"FR", "BND", c});
     } else if (lo == up) {
-      o += " FX BND " + c + " " + num17(lo) + "\n";
+      o += line({"FX", "BND", c, num17(lo)});
     } else {
-      if (lo == -kInf) o += " MI BND " + c + "\n";
-      else if (lo != 0.0 || (up < 0.0)) o += " LO BND " + c + " " + num17(lo) + "\n";
-      if (up != kInf) o += " UP BND " + c + " " + num17(up) + "\n";
+      if (lo == -kInf) o += line({"MI", "BND", c});
+      else if (lo != 0.0 || (up < 0.0)) o += line({"LO", "BND", c, num17(lo)});
+      if (up != kInf) o += line({"UP", "BND", c, num17(up)});
     }
   }
   o += "ENDATA\n";

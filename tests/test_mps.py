@@ -214,3 +214,60 @@ def test_solution_json_round_trip_bit_identical():
 def test_solution_json_rejects_unknown_status():
     with pytest.raises(ValueError):
         hplp.json_normalize(json.dumps(dict(REPORT, status="solved")))
+
+
+# ---- fixture corpus (SPEC.md acceptance criterion 10) -----------------------
+from pathlib import Path  # noqa: E402
+
+CORPUS = Path(__file__).resolve().parent / "golden" / "mps"
+GOOD = sorted(p for p in CORPUS.glob("[0-9]*.mps"))
+BAD = {  # file: (line, message fragment)
+    "bad_01_unknown_section.mps": (5, "unknown section 'COLUMNZ'"),
+    "bad_02_undeclared_row.mps": (6, "undeclared row 'Q'"),
+    "bad_03_duplicate_entry.mps": (7, "duplicate entry (R, X)"),
+    "bad_04_malformed_number.mps": (8, "malformed number '1.2.3'"),
+    "bad_05_unknown_bound.mps": (8, "unknown bound type 'XX'"),
+    "bad_06_missing_endata.mps": (7, "missing ENDATA"),
+}
+
+
+def test_corpus_size():
+    assert len(GOOD) >= 12 and len(BAD) >= 6
+
+
+@pytest.mark.parametrize("path", GOOD, ids=lambda p: p.name)
+def test_corpus_round_trip(path):
+    """Every fixture parses; write -> parse reproduces it exactly, and the
+    normalized text is a fixed point."""
+    p = hplp.parse_mps(path.read_text())
+    g = p.general()
+    q = hplp.parse_mps(p.write())
+    _same_general(g, q.general())
+    assert q.row_names == p.row_names and q.col_names == p.col_names
+    assert q.write() == p.write()
+    if p.n:  # through to_standard_form as well
+        s1, s2 = hplp.to_standard_form(g), hplp.to_standard_form(q.general())
+        assert np.array_equal(s1.val, s2.val) and np.array_equal(s1.b, s2.b) and np.array_equal(s1.c, s2.c)
+
+
+@pytest.mark.parametrize("name", sorted(BAD))
+def test_corpus_corrupted(name):
+    line, needle = BAD[name]
+    with pytest.raises(MpsParseError) as e:
+        hplp.parse_mps((CORPUS / name).read_text())
+    assert e.value.line == line and needle in str(e.value), str(e.value)
+
+
+def test_corpus_semantics():
+    g = hplp.parse_mps((CORPUS / "04_all_bound_types.mps").read_text())
+    lo = dict(zip(g.col_names, g.general().col_lower))
+    up = dict(zip(g.col_names, g.general().col_upper))
+    assert (lo["LIV"], up["LIV"]) == (1.0, math.inf) and (lo["UIV"], up["UIV"]) == (0.0, 9.0)
+    assert (lo["PLV"], up["PLV"]) == (0.0, math.inf) and (lo["FRV"], up["FRV"]) == (-math.inf, math.inf)
+    m = hplp.parse_mps((CORPUS / "05_objsense_max_constant.mps").read_text()).general()
+    assert m.maximize and m.objective_constant == 12.5
+    e = hplp.parse_mps((CORPUS / "12_rhs_without_set_name.mps").read_text()).general()
+    assert list(e.row_rhs) == [2.0, 3.0] and e.row_range[0] == 1.0 and np.isnan(e.row_range[1])
+    w = hplp.parse_mps((CORPUS / "09_extra_objective_rows.mps").read_text())
+    assert w.objective_name == "FIRST" and any("SECOND" in x for x in w.warnings)
+    assert list(w.general().objective) == [1.0, 0.0]
