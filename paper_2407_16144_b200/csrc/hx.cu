@@ -131,10 +131,17 @@ struct GridBar {
 // is monotonic for the context's lifetime (never reset between launches, so a
 // fast peer can arrive before this rank's next launch starts); time_up is the
 // time-limit flag, written by rank 0 alone so every rank stops together.
+constexpr int kRankRecReplicas = 8;  // copies of the rank records: every CTA reads them (L2 hot spot)
+constexpr int kPreReduceRecords = 320;
 struct RankBar {
   unsigned long long arrive;
   unsigned time_up[2];
   unsigned long long pad[14];
+  // rank records of the main reduction, [parity][source rank][quantity]:
+  // each rank's leader reduces its own CTAs' phase A/B records and pushes
+  // the 7 totals here on every rank (team_sync with reduce), so a
+  // controller sums nranks records instead of nranks * grid
+  double rrec[2][kRankRecReplicas][kMaxRanks][8];
 };
 
 // Row partition of the team plus the peers' buffers.  Rank r
@@ -150,6 +157,7 @@ struct RankBar {
 struct Team {
   int rank, nranks, grp_ctas;
   int sys;                  // 1: some peer is another GPU -> system-scope release/acquire
+  int prereduce;            // 1: main reduction through rank records (team_sync reduce)
   int row0, row1, col0, col1;
   double* px[kMaxRanks];    // xpool of every rank (px[rank] = own)
   double* py[kMaxRanks];    // ypool
@@ -316,7 +324,11 @@ __device__ void block_to_slots(const double (&acc)[Q], const KP* P, int region, 
     const size_t off = static_cast<size_t>(region) * region_stride(g.nrec) +
                        (static_cast<size_t>(k) * g.nrec + g.rec) * kMaxQ + q;
     if constexpr (RK) {
-      for (int r = 0; r < P->T.nranks; ++r) P->T.ps[r][off] = v;
+      // with rank records the main reduction's records stay local: the leader
+      // pre-reduces them at the end-of-iteration barrier (team_sync)
+      if (P->T.prereduce && region < kRegC1) P->slots[off] = v;
+      else
+        for (int r = 0; r < P->T.nranks; ++r) P->T.ps[r][off] = v;
     } else {
       P->slots[off] = v;
     }
@@ -795,18 +807,71 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned 
 // barriers passed) continues across launches and is identical on all ranks.
 // Each spin has the same 10 s watchdog; a rank whose peer died stops with
 // HPLP_ETIMEOUT instead of hanging the GPU.
+//
+// With `reduce` >= 0 (the end-of-iteration barrier; value = iteration
+// parity) the leader's warp, once every local CTA has arrived, also sums
+// the rank's own phase A/B records (slot regions kRegA/kRegB + parity,
+// local records only, fixed order) and stores the 7 totals into every
+// rank's RankBar::rrec[parity][rank] before its arrival, which releases
+// them with the rest.
 __device__ bool team_sync(GridBar* bar, const Team& T, const Geo& g, unsigned long long& target,
-                          unsigned long long& repoch) {
+                          unsigned long long& repoch, const double* slots = nullptr, int reduce = -1) {
   __shared__ int s_ok;
   __syncthreads();
   target += g.nctas;
   repoch += 1;
+  if (reduce >= 0 && g.cta == 0) {
+    // whole leader CTA: thread (k, q) sums quantity q over local records
+    // k, k + 64, ...; warp q folds the 64 partials (fixed order)
+    __shared__ double part[64][8];
+    if (threadIdx.x == 0) {
+      s_ok = 1;
+      if (T.sys) asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(&bar->count), "l"(1ull) : "memory");
+      else asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(&bar->count), "l"(1ull) : "memory");
+      const unsigned long long t0 = global_ns();
+      unsigned spins = 0;
+      while ((T.sys ? ld_acquire_sys_u64(&bar->count) : ld_acquire_u64(&bar->count)) < target) {
+        if ((++spins & 255u) != 0u) continue;
+        if (*reinterpret_cast<volatile unsigned*>(&bar->abort) || global_ns() - t0 > 10000000000ull) {
+          atomicExch(&bar->abort, 1u);
+          s_ok = 0;
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    if (s_ok) {
+      const int q = threadIdx.x & 7, k = threadIdx.x >> 3;  // 512 threads: k < 64
+      if (q < 7) {
+        const size_t stride = region_stride(g.nrec);
+        const double* rg = slots + static_cast<size_t>(q < 3 ? kRegA + reduce : kRegB + reduce) * stride +
+                           (q < 3 ? q : q - 3);
+        const size_t r0 = static_cast<size_t>(T.rank) * g.nctas;
+        double v = 0.0;
+        for (int c = k; c < g.nctas; c += 64) v += ldcg(rg + (r0 + c) * kMaxQ);
+        part[k][q] = v;
+      }
+      __syncthreads();
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      if (warp < 7) {
+        const double v = warp_sum(part[lane][warp] + part[lane + 32][warp]);
+        for (int d = lane; d < T.nranks * kRankRecReplicas; d += 32)
+          T.pb[d % T.nranks]->rrec[reduce][d / T.nranks][T.rank][warp] = v;
+        if (T.sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
+        else __threadfence();
+      }
+    }
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
-    s_ok = 1;
+    const bool counted = reduce >= 0 && g.cta == 0;  // the leader arrived above
+    if (!counted) s_ok = 1;
     // peers on other GPUs see this CTA's P2P stores only through a
     // system-scope release; ranks sharing one device need gpu scope only
-    if (T.sys) asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(&bar->count), "l"(1ull) : "memory");
-    else asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(&bar->count), "l"(1ull) : "memory");
+    if (!counted) {
+      if (T.sys) asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(&bar->count), "l"(1ull) : "memory");
+      else asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(&bar->count), "l"(1ull) : "memory");
+    }
     const unsigned long long t0 = global_ns();
     unsigned spins = 0;
     auto alive = [&]() -> bool {
@@ -819,11 +884,12 @@ __device__ bool team_sync(GridBar* bar, const Team& T, const Geo& g, unsigned lo
       return true;
     };
     if (g.cta == 0) {
-      while ((T.sys ? ld_acquire_sys_u64(&bar->count) : ld_acquire_u64(&bar->count)) < target)
-        if (!alive()) {
-          s_ok = 0;
-          break;
-        }
+      if (!counted)
+        while ((T.sys ? ld_acquire_sys_u64(&bar->count) : ld_acquire_u64(&bar->count)) < target)
+          if (!alive()) {
+            s_ok = 0;
+            break;
+          }
       if (s_ok) {
         for (int r = 0; r < T.nranks; ++r) {
           if (T.sys)
@@ -1282,6 +1348,17 @@ __device__ __forceinline__ void warp_totals_main(const KParams* P, int par, doub
   }
 #pragma unroll
   for (int q = 0; q < 7; ++q) t[q] = warp_sum(t[q]);
+}
+
+// Team totals: the nranks rank records of this parity, summed in rank order
+// (every lane, identical on every rank).
+__device__ __forceinline__ void warp_totals_ranks(const KParams* P, int par, double (&t)[7], int cta) {
+  const double (*rr)[8] = P->T.pb[P->T.rank]->rrec[par][cta % kRankRecReplicas];
+#pragma unroll
+  for (int q = 0; q < 7; ++q) t[q] = ldcg(&rr[0][q]);
+  for (int r = 1; r < P->T.nranks; ++r)
+#pragma unroll
+    for (int q = 0; q < 7; ++q) t[q] += ldcg(&rr[r][q]);
 }
 
 // power iteration halves: w = A x (x = x0 or z / zn), z = A^T w
@@ -1948,6 +2025,14 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
     }
     return grid_sync(bar, target);
   };
+  // end-of-iteration barrier: a team also forms the rank records of the
+  // main reduction there
+  auto sync_reduce = [&](int pr) -> bool {
+    if constexpr (RK) {
+      if (!solo) return team_sync(bar, P->T, g, target, repoch, P->slots, P->T.prereduce ? pr : -1);
+    }
+    return grid_sync(bar, target);
+  };
   // time-limit flag: decided by rank 0 alone so every rank stops together
   auto set_time_up = [&](int pr, unsigned v) {
     if constexpr (RK) {
@@ -2056,12 +2141,13 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
     if (threadIdx.x == 0) make_spec(C, SR);
     mark(2);
     spmv_head(P->AT, gwarp_id(g), lane, head);
-    if (!sync()) return;
+    if (!sync_reduce(par)) return;
     mark(3);
     if (warp == 0) {
       unsigned long long cA = clock64(), cB = 0, cC = 0;
       double t[7];
-      warp_totals_main(P, par, t, g);
+      if (solo || !P->T.prereduce) warp_totals_main(P, par, t, g);
+      else warp_totals_ranks(P, par, t, g.cta);
       // the independent fp64 divides / square roots, one per lane, executed
       // uniformly (operands selected per lane, one sqrt + one divide)
       double num = 1.0, den = 1.0;
@@ -3418,6 +3504,12 @@ int hx_set_partition(hx_ctx* c, int32_t nranks, int32_t rank, const int64_t* row
   c->ranked = true;
   c->team = Team{};
   c->team.rank = rank, c->team.nranks = nranks, c->team.grp_ctas = c->grid;
+  // Rank records pay off once a controller would otherwise read several
+  // 160-record batches (nranks * grid records; measured on one device, where
+  // the leader's reduction competes with the other ranks' phases, the direct
+  // read wins for 148 records).  HPLP_TEAM_PREREDUCE=0/1 forces either path.
+  c->team.prereduce = nranks * c->grid > kPreReduceRecords ? 1 : 0;
+  if (const char* e = std::getenv("HPLP_TEAM_PREREDUCE")) c->team.prereduce = std::atoi(e) != 0 ? 1 : 0;
   c->team.row0 = static_cast<int>(row0), c->team.row1 = static_cast<int>(row1);
   c->team.col0 = static_cast<int>(col0), c->team.col1 = static_cast<int>(col1);
   for (int r = 0; r < kMaxRanks; ++r) c->pcol0[r] = c->pcol1[r] = c->prow0[r] = c->prow1[r] = 0;

@@ -75,6 +75,25 @@ def test_team_solve_tol_1e4(gpu_required, nranks):
     _same_controllers(prog)
 
 
+@pytest.mark.parametrize("name,nranks", [("cfg1_small", 3), ("zipf_small", 8), ("cfg0", 2)])
+def test_team_rank_records_path(gpu_required, monkeypatch, name, nranks):
+    """The rank-record reduction (each rank's leader pre-reduces its CTAs'
+    phase records at the end-of-iteration barrier; the default once
+    nranks * grid > 320 records, i.e. real multi-GPU teams) forced on for
+    the one-device team: same iterate bar, identical controllers."""
+    monkeypatch.setenv("HPLP_TEAM_PREREDUCE", "1")
+    g, s = std(name)
+    cpu = CpuLp("port", *csr_args(s)).solve(iteration_limit=100, tolerance=1e-12, trace=True)
+    gpu, prog = team_solve(s, nranks, iteration_limit=100, tolerance=1e-12, trace=True)
+    _trace_cmp(gpu["trace"], cpu["trace"])
+    assert [e[:2] for e in gpu["epochs"]] == [e[:2] for e in cpu["epochs"]]
+    _same_controllers(prog)
+    long, prog = team_solve(s, nranks, tolerance=1e-4, iteration_limit=200000)
+    ref = CpuLp("port", *csr_args(s)).solve(tolerance=1e-4, iteration_limit=200000)
+    assert long["status"] == ref["status"]
+    _same_controllers(prog)
+
+
 def test_team_matches_single_gpu_long_run(gpu_required):
     """2000 iterations (restarts, certificate scans every 100) on the team
     stay within rounding of the single-context solve."""

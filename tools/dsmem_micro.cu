@@ -40,6 +40,34 @@ __global__ void __launch_bounds__(kThreads, 1) gather_global(const double* v, un
   if (acc == 12345.678) out[0] = acc;
 }
 
+// The same gathers plus the stream tasks' shared-memory traffic: every
+// product stored to a per-warp buffer, then read back lane-per-row (stride
+// `rowlen`, the bank pattern of the row sums).
+template <int F>
+__global__ void __launch_bounds__(kThreads, 1) gather_plus_smem(const double* v, unsigned n, int rounds, int rowlen,
+                                                                double* out) {
+  __shared__ double buf[kThreads / 32][F * 32];
+  double* st = buf[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  unsigned s = hash(blockIdx.x * kThreads + threadIdx.x + 1);
+  double acc = 0.0;
+  for (int r = 0; r < rounds; ++r) {
+    double t[F];
+#pragma unroll
+    for (int k = 0; k < F; ++k) {
+      s = hash(s + k);
+      t[k] = __ldca(v + (s % n));
+    }
+#pragma unroll
+    for (int k = 0; k < F; ++k) st[k * 32 + lane] = t[k];
+    __syncwarp();
+    const int base = (lane * rowlen) % (F * 32);
+    for (int k = 0; k < F; ++k) acc += st[(base + k) % (F * 32)];
+    __syncwarp();
+  }
+  if (acc == 12345.678) out[0] = acc;
+}
+
 // slice = elements per CTA; cluster = CTAs per cluster (runtime dims)
 __global__ void __launch_bounds__(kThreads, 1) gather_dsmem(const double* v, unsigned slice, int rounds, double* out) {
   extern __shared__ double sm[];
@@ -98,6 +126,19 @@ int main() {
   run_g(gather_global<8>, 8, "global, 8 in flight / thread");
   run_g(gather_global<16>, 16, "global, 16 in flight / thread");
   run_g(gather_global<32>, 32, "global, 32 in flight / thread");
+  for (int rowlen : {1, 8, 20}) {
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(e0);
+      gather_plus_smem<8><<<sms, kThreads>>>(v, n, rounds, rowlen, out);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      char name[80];
+      snprintf(name, sizeof name, "global + smem products (row stride %d)", rowlen);
+      if (rep) report(name, sms, ms);
+    }
+  }
   cudaFuncSetAttribute(gather_dsmem, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(gather_dsmem, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   for (int csize : {8, 16}) {
