@@ -140,15 +140,31 @@ int hplp_validate_config(const hplp_config_t* cfg) {
   });
 }
 
+namespace {
+// SparseMatrix semantics (src/sparse_matrix.cpp: rows given in any order are
+// sorted, duplicates and bad entries rejected with the reference's messages).
+// A matrix that is already valid CSR with ascending rows -- the common case --
+// goes straight to the device, which validates ranges, finiteness, order and
+// duplicates itself (hx_upload_csr); only a matrix it rejects takes the host
+// path, which sorts it or reports the reference's error.
+hplp_gpu::Solver* create_solver(int32_t device, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                                const double* val, const double* b, const double* c) {
+  if (m >= 0 && n >= 0 && row_ptr && row_ptr[0] == 0) {
+    try {
+      return new hplp_gpu::Solver(device, m, n, row_ptr, col_idx, val, b, c);
+    } catch (const std::invalid_argument&) {
+      // fall through: the host path sorts or reports
+    }
+  }
+  hplp_gpu::SparseMatrix a = hplp_gpu::SparseMatrix::from_csr(m, n, row_ptr, col_idx, val);
+  hplp_gpu::StandardFormLP lp(std::move(a), std::vector<double>(b, b + m), std::vector<double>(c, c + n));
+  return new hplp_gpu::Solver(lp, device);
+}
+}  // namespace
+
 int hplp_solver_create(int32_t device, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
                        const double* val, const double* b, const double* c, void** solver) {
-  return guarded([&] {
-    // SparseMatrix semantics first (sorts rows given in any order, rejects
-    // duplicates), then the device copy.
-    hplp_gpu::SparseMatrix a = hplp_gpu::SparseMatrix::from_csr(m, n, row_ptr, col_idx, val);
-    hplp_gpu::StandardFormLP lp(std::move(a), std::vector<double>(b, b + m), std::vector<double>(c, c + n));
-    *solver = new hplp_gpu::Solver(lp, device);
-  });
+  return guarded([&] { *solver = create_solver(device, m, n, row_ptr, col_idx, val, b, c); });
 }
 
 int hplp_solver_create_team(const int32_t* devices, int32_t ndevices, int32_t nranks, int32_t ctas_per_rank,
@@ -206,8 +222,13 @@ int hplp_solve_csr(int32_t device, int64_t m, int64_t n, const int64_t* row_ptr,
                    const double* val, const double* b, const double* c, const hplp_config_t* cfg, hplp_io_t* io,
                    hplp_result_t* result) {
   void* s = nullptr;
+  // the power iteration's start vector is drawn on a host thread while the
+  // problem uploads
+  hplp_gpu::PowerStartFuture start;
+  if (cfg && n > 0) start = hplp_gpu::draw_power_start_async(n, cfg->seed);
   int rc = hplp_solver_create(device, m, n, row_ptr, col_idx, val, b, c, &s);
   if (rc != HPLP_OK) return rc;
+  if (start.valid()) static_cast<hplp_gpu::Solver*>(s)->use_power_start(cfg->seed, start);
   rc = hplp_solver_solve(s, cfg, io, result);
   hplp_solver_free(s);
   return rc;

@@ -8,8 +8,10 @@
 
 #include <cstdint>
 #include <functional>
+#include <future>
 #include <iosfwd>
 #include <limits>
+#include <memory>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -273,6 +275,15 @@ struct SolveResult {
   SolveTotals totals;
 };
 
+// The power iteration's random start (src/sparse_matrix.cpp:145-150): n
+// normal draws from std::mt19937_64(seed), normalised, plus the generator
+// state for a re-draw.  Sequential host work (~8 ms at n = 430k), so it is
+// drawn on a host thread while the problem uploads and kept for later
+// solves with the same seed.
+struct PowerStart;
+using PowerStartFuture = std::shared_future<std::shared_ptr<PowerStart>>;
+PowerStartFuture draw_power_start_async(int64_t n, uint64_t seed);
+
 // A device-resident problem: upload once, solve many times (bench, warm
 // starts).  Owns one hx context.
 class Solver {
@@ -306,8 +317,15 @@ class Solver {
   int nranks() const { return ranks_.empty() ? 1 : static_cast<int>(ranks_.size()); }
   int64_t rows() const { return m_; }
   int64_t cols() const { return n_; }
+  // a start vector drawn elsewhere (draw_power_start_async) for solves with `seed`
+  void use_power_start(uint64_t seed, PowerStartFuture start) {
+    start_seed_ = seed;
+    start_ = std::move(start);
+  }
 
  private:
+  uint64_t start_seed_ = 0;
+  PowerStartFuture start_;  // invalid until drawn
   ::hx_ctx* ctx_ = nullptr;          // the context (a team: rank 0)
   std::vector<::hx_ctx*> ranks_;      // team in rank order; empty for one context
   int64_t m_ = 0, n_ = 0, nnz_ = 0;

@@ -39,9 +39,11 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <future>
 #include <limits>
 #include <memory>
 #include <mutex>
@@ -2660,10 +2662,10 @@ void free_problem(hx_ctx* c) {
 }
 
 // Schedule of rows [row0, row0 + rows) of a CSR matrix (the whole matrix by
-// default; a rank's block in a team).  Task rows stay global indices.
-int upload_sched(hx_ctx* ctx, DevSched& d, const int* ptr_host, int rows, int cols, const int* dptr,
-                 const int* didx, const double* dval, double lead = 0.0, int row0 = 0) {
-  SchedHost h = build_schedule(ptr_host + row0, rows, ctx->grid * kWarps, lead);
+// default; a rank's block in a team), built on the host (h) and uploaded.
+// Task rows stay global indices.
+int upload_built_sched(hx_ctx* ctx, DevSched& d, SchedHost h, int rows, int cols, const int* dptr, const int* didx,
+                       const double* dval, int row0) {
   if (row0)
     for (int4& t : h.tasks)
       if (t.x != t.y || t.z != t.w) {
@@ -2710,6 +2712,12 @@ int upload_sched(hx_ctx* ctx, DevSched& d, const int* ptr_host, int rows, int co
   d.max_cost = h.max_warp_cost;
   d.mean_cost = h.mean_warp_cost;
   return HPLP_OK;
+}
+
+int upload_sched(hx_ctx* ctx, DevSched& d, const int* ptr_host, int rows, int cols, const int* dptr,
+                 const int* didx, const double* dval, double lead = 0.0, int row0 = 0) {
+  return upload_built_sched(ctx, d, build_schedule(ptr_host + row0, rows, ctx->grid * kWarps, lead), rows, cols, dptr,
+                            didx, dval, row0);
 }
 
 KParams params(hx_ctx* c) {
@@ -2926,6 +2934,7 @@ extern "C" {
 
 int hx_create(int32_t device, hx_ctx** out) {
   *out = nullptr;
+  const auto t_create = std::chrono::steady_clock::now();
   auto ctx = std::make_unique<hx_ctx>();
   ctx->device = device;
   int ndev = 0;
@@ -2934,13 +2943,16 @@ int hx_create(int32_t device, hx_ctx** out) {
   if (device < 0 || device >= ndev) return set_err(nullptr, HPLP_EINVAL, "hx_create: bad device index");
   hx_ctx* c = ctx.get();
   HX_CUDA(nullptr, cudaSetDevice(device));
-  cudaDeviceProp prop;
-  HX_CUDA(nullptr, cudaGetDeviceProperties(&prop, device));
-  if (prop.major < 10)
-    return set_err(nullptr, HPLP_ECUDA, "hx_create: this build targets sm_100a (B200); found sm_" +
-                                            std::to_string(prop.major * 10 + prop.minor));
-  if (!prop.cooperativeLaunch) return set_err(nullptr, HPLP_ECUDA, "hx_create: cooperative launch unsupported");
-  c->sm_count = prop.multiProcessorCount;
+  // single attributes: cudaGetDeviceProperties costs milliseconds per call
+  int major = 0, minor = 0, coop = 0;
+  HX_CUDA(nullptr, cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  HX_CUDA(nullptr, cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+  HX_CUDA(nullptr, cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+  HX_CUDA(nullptr, cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+  if (major < 10)
+    return set_err(nullptr, HPLP_ECUDA,
+                   "hx_create: this build targets sm_100a (B200); found sm_" + std::to_string(major * 10 + minor));
+  if (!coop) return set_err(nullptr, HPLP_ECUDA, "hx_create: cooperative launch unsupported");
   HX_CUDA(nullptr, cudaFuncSetAttribute(loop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(kStageBytes)));
   HX_CUDA(nullptr, cudaFuncSetAttribute(spmv_store_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2969,6 +2981,11 @@ int hx_create(int32_t device, hx_ctx** out) {
   HX_CUDA(nullptr, cudaMemset(c->bar, 0, sizeof(GridBar)));
   HX_CUDA(nullptr, cudaMemset(c->ctl, 0, sizeof(Ctl)));
   std::memset(&c->h, 0, sizeof(Ctl));
+  if (const char* e = std::getenv("HPLP_TIMING"); e && e[0] == '1') {
+    cudaDeviceSynchronize();
+    std::fprintf(stderr, "hx_create: %8.3f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_create).count());
+  }
   *out = ctx.release();
   return HPLP_OK;
 }
@@ -3019,8 +3036,34 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   for (int64_t j = 0; j < n; ++j)
     if (!std::isfinite(cc[j])) return set_err(c, HPLP_EINVAL, "StandardFormLP: non-finite b or c");
   c->m = m, c->n = n, c->nnz = nnz;
+  // A's schedule needs only the host row pointers: build it on a host thread
+  // while the matrix copies and A^T forms on the device
+  std::vector<int> ph(static_cast<size_t>(m) + 1);
+  bool monotone = true;
+  for (int64_t i = 0; i <= m; ++i) {
+    ph[i] = static_cast<int>(row_ptr[i]);
+    if (i && row_ptr[i] < row_ptr[i - 1]) monotone = false;
+  }
+  const int sched_warps = c->grid * kWarps;
+  std::future<SchedHost> sched_a;
+  if (monotone)  // else the device check below reports it
+    sched_a = std::async(std::launch::async, [&ph, m, sched_warps] {
+      return build_schedule(ph.data(), static_cast<int>(m), sched_warps, 0.0);
+    });
   cudaStream_t s = c->stream;
   const int nblk = 4 * c->sm_count;
+  // HPLP_TIMING=1: wall time of the upload stages on stderr
+  const bool timing = [] {
+    const char* e = std::getenv("HPLP_TIMING");
+    return e && e[0] == '1';
+  }();
+  auto tick = [&, t0 = std::chrono::steady_clock::now()](const char* what) mutable {
+    if (!timing) return;
+    cudaStreamSynchronize(s);
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "hx_upload_csr: %-12s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   // Matrix A (CSR), validated on the device.
   long long* rp64 = nullptr;
   unsigned* flags = nullptr;
@@ -3047,7 +3090,8 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   dfree(rp64);
   dfree(flags);
   c->launches += 2;
-  if (hflags & 16u) return set_err(c, HPLP_EINVAL, "hx_upload_csr: row_ptr is not monotone");
+  tick("copy+check");
+  if ((hflags & 16u) || !monotone) return set_err(c, HPLP_EINVAL, "hx_upload_csr: row_ptr is not monotone");
   if (hflags & 1u) return set_err(c, HPLP_EINVAL, "SparseMatrix: entry out of range");
   if (hflags & 2u) return set_err(c, HPLP_EINVAL, "SparseMatrix: non-finite value");
   if (hflags & 8u) return set_err(c, HPLP_EINVAL, "SparseMatrix: duplicate entry");
@@ -3085,13 +3129,13 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     c->launches += 5;
     dfree(tmp), dfree(row_of), dfree(iota), dfree(keys_out), dfree(perm), dfree(cnt);
   }
+  tick("transpose");
   // Schedules (host, from the pointer arrays).
   {
-    std::vector<int> ph(static_cast<size_t>(m) + 1), pt(static_cast<size_t>(n) + 1);
-    for (int64_t i = 0; i <= m; ++i) ph[i] = static_cast<int>(row_ptr[i]);
+    std::vector<int> pt(static_cast<size_t>(n) + 1);
     HX_CUDA(c, cudaMemcpy(pt.data(), c->t_ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost));
-    int rc = upload_sched(c, c->sa, ph.data(), static_cast<int>(m), static_cast<int>(n), c->a_ptr, c->a_idx,
-                          c->a_val);
+    int rc = upload_built_sched(c, c->sa, sched_a.get(), static_cast<int>(m), static_cast<int>(n), c->a_ptr,
+                                c->a_idx, c->a_val, 0);
     if (rc) return rc;
     // phase A (rows of A^T) runs speculatively while warp 0 of every CTA runs
     // the controller: warp 0 starts with a lead of about the controller's
@@ -3142,6 +3186,7 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
       T.yneed = c->yneed;
     }
   }
+  tick("schedules");
   if (c->ranked) {  // peers map these through CUDA IPC
     HX_CUDA(c, dalloc_ipc(&c->xpool, static_cast<size_t>(kXPool) * n));
     HX_CUDA(c, dalloc_ipc(&c->ypool, static_cast<size_t>(kYPool) * m));
@@ -3169,6 +3214,7 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   c->launches += 2;
   c->b_norm = std::sqrt(tot[4]);
   c->c_norm = std::sqrt(tot[5]);
+  tick("pools+norms");
   c->uploaded = true;
   return HPLP_OK;
 }

@@ -10,6 +10,9 @@
 // path: without a B200 the hx layer fails and solve() throws.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <future>
 #include <cmath>
 #include <limits>
 #include <random>
@@ -83,23 +86,44 @@ struct PowerResult {
   bool converged = false;
 };
 
+}  // namespace
+
+struct PowerStart {
+  Vector x;  // normalised
+  std::mt19937_64 gen;
+  std::normal_distribution<double> dist;
+};
+
+PowerStartFuture draw_power_start_async(int64_t n, uint64_t seed) {
+  return std::async(std::launch::async, [n, seed] {
+           auto s = std::make_shared<PowerStart>();
+           s->gen.seed(seed);
+           s->dist = std::normal_distribution<double>(0.0, 1.0);
+           s->x.resize(static_cast<std::size_t>(std::max<int64_t>(n, 0)));
+           for (auto& v : s->x) v = s->dist(s->gen);
+           double xn = seq_norm(s->x);
+           if (xn == 0.0) std::fill(s->x.begin(), s->x.end(), 1.0), xn = seq_norm(s->x);
+           for (auto& v : s->x) v /= xn;
+           return s;
+         })
+      .share();
+}
+
+namespace {
+
 // power_iteration, src/sparse_matrix.cpp:138-179: the start vector (and any
 // re-draw) comes from the same std::mt19937_64 stream as the reference; the
 // SpMVs and norms run on the device (hx_power_iteration).
 PowerResult power_iteration(hx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, double tol, int64_t max_iters,
-                            uint64_t seed) {
+                            const PowerStart& start) {
   PowerResult res;
   if (m == 0 || n == 0 || nnz == 0) {
     res.converged = true;
     return res;
   }
-  std::mt19937_64 gen(seed);
-  std::normal_distribution<double> dist(0.0, 1.0);
-  Vector x(static_cast<std::size_t>(n));
-  for (auto& v : x) v = dist(gen);
-  double xn = seq_norm(x);
-  if (xn == 0.0) std::fill(x.begin(), x.end(), 1.0), xn = seq_norm(x);
-  for (auto& v : x) v /= xn;
+  std::mt19937_64 gen = start.gen;  // a re-draw continues the stream
+  std::normal_distribution<double> dist = start.dist;
+  Vector x = start.x;
   int64_t k0 = 0;
   double sigma_prev = 0.0;
   while (true) {
@@ -325,6 +349,14 @@ Solver::~Solver() {
 SolveResult Solver::solve(const SolverConfig& config) {
   const auto t0 = Clock::now();
   auto since = [&] { return std::chrono::duration<double>(Clock::now() - t0).count(); };
+  // HPLP_TIMING=1: cumulative wall time of the solve stages on stderr
+  const bool timing = [] {
+    const char* e = std::getenv("HPLP_TIMING");
+    return e && e[0] == '1';
+  }();
+  auto stage = [&](const char* what) {
+    if (timing) std::fprintf(stderr, "solve: %-16s at %8.3f ms\n", what, 1e3 * since());
+  };
   validate_config(config);
   hx_ctx* ctx = ctx_;
   // optional diagonal preconditioning (extension), applied once per Solver
@@ -352,7 +384,9 @@ SolveResult Solver::solve(const SolverConfig& config) {
     for (std::size_t i = 0; i < y.size(); ++i) y[i] *= row_scale_[i];
   };
   // make_setup (:67-78)
-  const PowerResult pi = power_iteration(ctx, m_, n_, nnz_, kPowerTol, kPowerMaxIters, config.seed);
+  if (!start_.valid() || start_seed_ != config.seed) use_power_start(config.seed, draw_power_start_async(n_, config.seed));
+  const PowerResult pi = power_iteration(ctx, m_, n_, nnz_, kPowerTol, kPowerMaxIters, *start_.get());
+  stage("power iteration");
   const double sigma_used = pi.sigma * (1.0 + kPowerTol);
   long n_spmv = 2 * static_cast<long>(pi.iterations);
   const double eta = config.eta_override ? step_size(*config.eta_override, sigma_used)
@@ -381,6 +415,7 @@ SolveResult Solver::solve(const SolverConfig& config) {
   pod.time_limit_seconds = config.time_limit_seconds - since();  // device clock starts at the loop
   check(ctx, hx_setup(ctx, &pod, sigma_used, eta, x0, y0));
   for (std::size_t r = 1; r < ranks_.size(); ++r) check(ranks_[r], hx_setup(ranks_[r], &pod, sigma_used, eta, x0, y0));
+  stage("setup");
   n_spmv += 1;  // a_x = A x (:213-214)
   // one batch of the loop: the context, or every rank of the team together
   auto run_batch = [&](int64_t batch, hx_progress_t* prog) {
@@ -441,6 +476,7 @@ SolveResult Solver::solve(const SolverConfig& config) {
   }
   SolveStatus status = p.status >= 0 ? static_cast<SolveStatus>(p.status) : SolveStatus::kTimeLimit;
   out.status = status;
+  stage("loop");
   out.final_iterate.x.resize(static_cast<std::size_t>(n_));
   out.final_iterate.y.resize(static_cast<std::size_t>(m_));
   long extra_spmv = 0;
@@ -482,6 +518,7 @@ SolveResult Solver::solve(const SolverConfig& config) {
     c.margin = meta.margin;
     dst = std::move(c);
   };
+  stage("loop+readback");
   take_cert(0, p.primal_cert, out.primal_certificate, m_);
   take_cert(1, p.dual_cert, out.dual_certificate, n_);
   out.epochs.reserve(epochs.size());
