@@ -627,8 +627,11 @@ struct NoIn {};
 // Ranked epilogues push each owned element a peer gathers into every other
 // rank's pool at the same offset (P2P stores on a multi-GPU node).
 __device__ __forceinline__ void push_peers(const Team* T, double* const* base, size_t off, double v, unsigned mask) {
-  for (int r = 0; r < T->nranks; ++r)
-    if ((mask >> r) & 1u) base[r][off] = v;
+  while (mask) {
+    const int r = __ffs(mask) - 1;
+    mask &= mask - 1;
+    base[r][off] = v;
+  }
 }
 
 template <bool RK>
@@ -661,7 +664,8 @@ struct EpiPrimal {  // phase A, rows of A^T
     double xn = x - eta * (aty + cj);
     xn = xn < 0.0 ? 0.0 : xn;
     xp[j] = xn;
-    if constexpr (RK) push_peers(T, T->px, xp_off + j, xn, __ldg(T->xneed + (j - T->col0)));
+    if constexpr (RK)
+      if (T->nranks > 1) push_peers(T, T->px, xp_off + j, xn, __ldg(T->xneed + (j - T->col0)));
     double rc = -(cj + aty);
     rc = rc < 0.0 ? 0.0 : rc;
     const double dx = x - xn;
@@ -703,7 +707,8 @@ struct EpiDual {  // phase B, rows of A
     yc[i] = yci;
     // only the combo -- the next y when there is no restart, which phase A
     // gathers speculatively; after a restart the loop pushes y+ itself
-    if constexpr (RK) push_peers(T, T->py, yc_off + i, yci, __ldg(T->yneed + (i - T->row0)));
+    if constexpr (RK)
+      if (T->nranks > 1) push_peers(T, T->py, yc_off + i, yci, __ldg(T->yneed + (i - T->row0)));
     axc[i] = omw * s + w * in.axa;
     const double d = axi - bi;
     const double dy = yi - ypi;
@@ -2714,10 +2719,24 @@ int upload_built_sched(hx_ctx* ctx, DevSched& d, SchedHost h, int rows, int cols
   return HPLP_OK;
 }
 
+// HX_COSTS="rowT,taskT,rowA,taskA": schedule cost constants for the rows of
+// A^T (phase A) and of A (phase B), in nnz units (experiments)
+void sched_costs(bool transposed, double& row_cost, double& task_cost) {
+  row_cost = kRowCost, task_cost = kTaskCost;
+  if (const char* e = std::getenv("HX_COSTS")) {
+    double v[4] = {kRowCost, kTaskCost, kRowCost, kTaskCost};
+    std::sscanf(e, "%lf,%lf,%lf,%lf", &v[0], &v[1], &v[2], &v[3]);
+    row_cost = transposed ? v[0] : v[2];
+    task_cost = transposed ? v[1] : v[3];
+  }
+}
+
 int upload_sched(hx_ctx* ctx, DevSched& d, const int* ptr_host, int rows, int cols, const int* dptr,
-                 const int* didx, const double* dval, double lead = 0.0, int row0 = 0) {
-  return upload_built_sched(ctx, d, build_schedule(ptr_host + row0, rows, ctx->grid * kWarps, lead), rows, cols, dptr,
-                            didx, dval, row0);
+                 const int* didx, const double* dval, double lead = 0.0, int row0 = 0, bool transposed = false) {
+  double rc, tc;
+  sched_costs(transposed, rc, tc);
+  return upload_built_sched(ctx, d, build_schedule(ptr_host + row0, rows, ctx->grid * kWarps, lead, rc, tc), rows, cols,
+                            dptr, didx, dval, row0);
 }
 
 KParams params(hx_ctx* c) {
@@ -3048,7 +3067,9 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   std::future<SchedHost> sched_a;
   if (monotone)  // else the device check below reports it
     sched_a = std::async(std::launch::async, [&ph, m, sched_warps] {
-      return build_schedule(ph.data(), static_cast<int>(m), sched_warps, 0.0);
+      double rc, tc;
+      sched_costs(false, rc, tc);
+      return build_schedule(ph.data(), static_cast<int>(m), sched_warps, 0.0, rc, tc);
     });
   cudaStream_t s = c->stream;
   const int nblk = 4 * c->sm_count;
@@ -3143,7 +3164,7 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     double lead = 1200.0;
     if (const char* e = std::getenv("HX_LEAD")) lead = std::atof(e);
     rc = upload_sched(c, c->st, pt.data(), static_cast<int>(n), static_cast<int>(m), c->t_ptr, c->t_idx, c->t_val,
-                      lead);
+                      lead, 0, true);
     if (rc) return rc;
     if (c->ranked) {  // this rank's blocks: rows [row0,row1) of A, [col0,col1) of A^T
       Team& T = c->team;
@@ -3153,7 +3174,7 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
                         T.row0);
       if (rc) return rc;
       rc = upload_sched(c, c->pt, pt.data(), T.col1 - T.col0, static_cast<int>(m), c->t_ptr, c->t_idx, c->t_val, lead,
-                        T.col0);
+                        T.col0, true);
       if (rc) return rc;
       // who gathers what: x+_j is read by the owners of the rows in column j,
       // y_i by the owners of the columns in row i

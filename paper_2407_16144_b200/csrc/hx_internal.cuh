@@ -111,6 +111,7 @@ struct SchedHost {
 
 // lead: initial load (cost units) of warp 0 of every CTA, which runs the
 // controller before its own tasks in the speculative phase A.
-SchedHost build_schedule(const int* ptr_host, int rows, int warps, double lead = 0.0);
+SchedHost build_schedule(const int* ptr_host, int rows, int warps, double lead = 0.0, double row_cost = kRowCost,
+                         double task_cost = kTaskCost);
 
 }  // namespace hx

@@ -16,16 +16,16 @@
 
 namespace hx {
 
-SchedHost build_schedule(const int* ptr, int rows, int warps, double lead) {
+SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, double row_cost, double task_cost) {
   SchedHost s;
   const int64_t nnz = ptr[rows] - ptr[0];  // ptr may point into a larger matrix (a rank's block)
-  const double total = static_cast<double>(nnz) + kRowCost * rows;
+  const double total = static_cast<double>(nnz) + row_cost * rows;
 
   std::vector<double> cost;
   auto push = [&](int r0, int r1, int kind, int p0, int p1, int4 meta, double c) {
     s.tasks.push_back(int4{r0, r1 | (kind << kKindShift), p0, p1});
     s.meta.push_back(meta);
-    cost.push_back(c + kTaskCost);
+    cost.push_back(c + task_cost);
   };
   int r = 0;
   while (r < rows) {
@@ -36,7 +36,7 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead) {
         const int p0 = static_cast<int>(ptr[r] + len * q / np);
         const int p1 = static_cast<int>(ptr[r] + len * (q + 1) / np);
         push(r, r + 1, kTaskPiece, p0, p1, int4{s.n_slots + q, np, np > 1 ? s.n_long : -1, q},
-             static_cast<double>(p1 - p0) + (q + 1 == np ? kRowCost : 0.0));
+             static_cast<double>(p1 - p0) + (q + 1 == np ? row_cost : 0.0));
       }
       if (np > 1) {
         s.n_slots += np;
@@ -54,7 +54,7 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead) {
       ++r;
     }
     push(r0, r, kTaskStream, static_cast<int>(ptr[r0]), static_cast<int>(ptr[r]), int4{0, 0, 0, 0},
-         static_cast<double>(used) + kRowCost * (r - r0));
+         static_cast<double>(used) + row_cost * (r - r0));
   }
 
   // Longest-processing-time dealing: tasks heaviest first, each to the
