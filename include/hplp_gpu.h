@@ -44,6 +44,22 @@ int hplp_solve_csr(int32_t device, int64_t m, int64_t n, const int64_t* row_ptr,
 int hplp_solver_create(int32_t device, int64_t m, int64_t n, const int64_t* row_ptr,
                        const int32_t* col_idx, const double* val, const double* b, const double* c,
                        void** solver);
+/* [no reference counterpart: SURVEY.md §8f rank 4, a flagged mode] The box
+ * form of a standard-form LP: the trailing bound rows x_j + s_j = u_j that
+ * to_standard_form appends (src/lp_model.cpp:232-252) are detected and
+ * replaced by the projection x_j in [0, u_j] on the leading block (hx_set_box).
+ * hplp_solver_solve then runs rHPDHG on it -- a different iteration from the
+ * reference's, not iterate-comparable -- and returns x, y in the standard
+ * form's dimensions (slack u_j - x_j; bound-row dual max(0, -(c + A^T y)_j)).
+ * No infeasibility scan (the check period is ignored), final_kkt is the box
+ * form's KKT error, trace iterates are box-form vectors. */
+int hplp_solver_create_box(int32_t device, int64_t m, int64_t n, const int64_t* row_ptr,
+                           const int32_t* col_idx, const double* val, const double* b, const double* c,
+                           void** solver);
+/* Dimensions (m_box, n_box) of that box form and its upper bounds (n_box
+ * values, +inf = none; `upper` may be NULL or hold n values). Host only. */
+int hplp_box_form_dims(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const double* val,
+                       const double* b, const double* c, int64_t* m_box, int64_t* n_box, double* upper);
 /* The same LP row-partitioned across nranks contexts of this process (SURVEY.md
  * §8e): rank r on devices[r % ndevices], nnz-balanced blocks from
  * hplp_plan_partition, bound with hx_team_bind.  Ranks sharing a device are

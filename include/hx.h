@@ -79,6 +79,14 @@ int hx_dims(hx_ctx* ctx, int64_t* m, int64_t* n, int64_t* nnz);
  * pointers are non-NULL.  Iterates of the transformed LP map back as
  * x = C x', y = R y'. */
 int hx_precondition(hx_ctx* ctx, int32_t ruiz_iters, double pc_alpha, double* row_scale, double* col_scale);
+/* [no reference counterpart: SURVEY.md §8f rank 4, the flagged box form]
+ * Column upper bounds (length n, >= 0, +inf = none) enforced by the primal
+ * projection x+ = clamp(x - eta (A^T y + c), 0, u) instead of bound rows;
+ * the KKT dual residual counts only unbounded columns and the gap adds
+ * sum_j u_j [-(c + A^T y)_j]^+ to b^T y.  upper = NULL returns to the
+ * standard form.  Call after hx_upload_csr, before hx_precondition (which
+ * rescales u) and hx_setup; rHPDHG only, without infeasibility scans. */
+int hx_set_box(hx_ctx* ctx, const double* upper);
 /* The device problem (after any preconditioning): CSR A, b, c. */
 int hx_download_problem(hx_ctx* ctx, int64_t* row_ptr, int32_t* col_idx, double* val, double* b, double* c);
 

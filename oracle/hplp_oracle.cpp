@@ -212,6 +212,9 @@ Power power_iteration(const Csr& a, double tol, int64_t max_iters, uint64_t seed
 struct Lp {
   Csr a;
   Vec b, c;
+  // Box form (no reference counterpart): column upper
+  // bounds enforced by the projection; empty = the reference's standard form.
+  Vec u;
 };
 
 struct Kkt {
@@ -221,15 +224,27 @@ struct Kkt {
 // kkt_error_with_products: src/pdhg_core.cpp:57-68.
 Kkt kkt(const Vec& x, const Vec& y, const Lp& lp, const Vec& a_x, const Vec& at_y) {
   Kkt e;
-  e.p = norm(sub(a_x, lp.b)) / (1.0 + norm(lp.b));
+  double b_norm = norm(lp.b);
+  if (!lp.u.empty()) {  // box form: ||b|| of the standard form (b, then the bound rows' u)
+    double sq = sqnorm(lp.b);
+    for (double u : lp.u)
+      if (u < kInf) sq += u * u;
+    b_norm = std::sqrt(sq);
+  }
+  e.p = norm(sub(a_x, lp.b)) / (1.0 + b_norm);
   Vec r(lp.c.size());
+  double ul = 0.0;  // box form: sum over bounded columns of u_j [-(c + A^T y)_j]^+
   for (std::size_t j = 0; j < r.size(); ++j) {
     const double v = -(lp.c[j] + at_y[j]);
     r[j] = v < 0.0 ? 0.0 : v;
+    if (!lp.u.empty() && lp.u[j] < kInf) {
+      ul += lp.u[j] * r[j];
+      r[j] = 0.0;
+    }
   }
   e.d = norm(r) / (1.0 + norm(lp.c));
   const double cx = dot(lp.c, x);
-  const double by = dot(lp.b, y);
+  const double by = dot(lp.b, y) + ul;
   e.g = std::abs(cx + by) / (1.0 + std::abs(cx) + std::abs(by));
   e.max = std::max({e.p, e.d, e.g});
   return e;
@@ -260,6 +275,7 @@ Step pdhg_step(const Vec& x, const Vec& y, const Lp& lp, double eta, const Vec& 
   for (std::size_t j = 0; j < x.size(); ++j) {
     const double v = x[j] - eta * (r.at_y[j] + lp.c[j]);
     r.x[j] = v < 0.0 ? 0.0 : v;
+    if (!lp.u.empty() && r.x[j] > lp.u[j]) r.x[j] = lp.u[j];  // box form
   }
   r.a_x_next = spmv(lp.a, r.x);
   r.y.resize(y.size());
@@ -416,6 +432,8 @@ void solve(const Lp& lp, const hplp_config_t& cfg, hplp_io_t* io, hplp_result_t*
   const auto t0 = Clock::now();
   auto since = [&] { return std::chrono::duration<double>(Clock::now() - t0).count(); };
   validate_config(cfg);
+  if (!lp.u.empty() && cfg.infeasibility_check_period > 0)
+    throw std::invalid_argument("box form: no infeasibility scan (set infeasibility_check_period 0)");
   const Power pi = power_iteration(lp.a, 1e-4, 5000, cfg.seed);
   const double sigma_used = pi.sigma * (1.0 + 1e-4);
   int64_t n_spmv = 2 * pi.iterations;
@@ -598,6 +616,7 @@ void solve_baseline(const Lp& lp, const hplp_config_t& cfg, int mode, hplp_io_t*
   const auto t0 = Clock::now();
   auto since = [&] { return std::chrono::duration<double>(Clock::now() - t0).count(); };
   validate_config(cfg);
+  if (!lp.u.empty()) throw std::invalid_argument("box form: rHPDHG only");
   const Power pi = power_iteration(lp.a, 1e-4, 5000, cfg.seed);
   const double sigma_used = pi.sigma * (1.0 + 1e-4);
   int64_t n_spmv = 2 * pi.iterations;
@@ -993,7 +1012,7 @@ const char* orc_last_error(void) { return orc::g_err.c_str(); }
 int orc_lp_create(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
                   const double* val, const double* b, const double* c, void** out) {
   return guarded([&] {
-    auto* lp = new orc::Lp{orc::make_csr(m, n, row_ptr, col_idx, val), orc::vec(b, m), orc::vec(c, n)};
+    auto* lp = new orc::Lp{orc::make_csr(m, n, row_ptr, col_idx, val), orc::vec(b, m), orc::vec(c, n), {}};
     if (!orc::all_finite(lp->b) || !orc::all_finite(lp->c)) {
       delete lp;
       throw std::invalid_argument("StandardFormLP: non-finite b or c");
@@ -1003,6 +1022,20 @@ int orc_lp_create(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* c
 }
 
 void orc_lp_free(void* h) { delete static_cast<orc::Lp*>(h); }
+
+// Box form: upper bounds u (n values, >= 0, +inf = none); NULL clears.
+int orc_lp_set_box(void* h, const double* u) {
+  return guarded([&] {
+    auto& lp = *static_cast<orc::Lp*>(h);
+    if (!u) {
+      lp.u.clear();
+      return;
+    }
+    lp.u = orc::vec(u, lp.a.cols);
+    for (double v : lp.u)
+      if (std::isnan(v) || v < 0.0) throw std::invalid_argument("box form: upper bounds must be >= 0 (or +inf)");
+  });
+}
 
 int orc_spmv(void* h, const double* x, double* out) {
   return guarded([&] {

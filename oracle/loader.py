@@ -119,6 +119,18 @@ class CpuLp:
         except Exception:
             pass
 
+    def set_box(self, u):
+        """Box form (port only; no reference counterpart): column upper bounds u
+        (+inf = none) enforced by the primal projection; None clears."""
+        if self.kind != "port":
+            raise ValueError("the box form exists only in the port (the reference has no counterpart)")
+        if u is None:
+            _chk(self.lib, _f(self.lib, "lp_set_box")(self.h, None))
+            return self
+        self._box_u = np.ascontiguousarray(u, np.float64)
+        _chk(self.lib, _f(self.lib, "lp_set_box")(self.h, dptr(self._box_u)))
+        return self
+
     def spmv(self, x):
         x = np.ascontiguousarray(x, np.float64)
         out = np.empty(self.m)

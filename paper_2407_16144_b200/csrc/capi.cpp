@@ -1,4 +1,5 @@
 // C ABI (include/hplp_gpu.h) over the C++ host driver (hplp_gpu.hpp).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -165,6 +166,29 @@ hplp_gpu::Solver* create_solver(int32_t device, int64_t m, int64_t n, const int6
 int hplp_solver_create(int32_t device, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
                        const double* val, const double* b, const double* c, void** solver) {
   return guarded([&] { *solver = create_solver(device, m, n, row_ptr, col_idx, val, b, c); });
+}
+
+int hplp_solver_create_box(int32_t device, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                           const double* val, const double* b, const double* c, void** solver) {
+  return guarded([&] {
+    // validated with SparseMatrix semantics first (the box form keeps the
+    // caller's ascending rows as they are)
+    hplp_gpu::SparseMatrix a = hplp_gpu::SparseMatrix::from_csr(m, n, row_ptr, col_idx, val);
+    hplp_gpu::StandardFormLP lp(std::move(a), std::vector<double>(b, b + m), std::vector<double>(c, c + n));
+    *solver = new hplp_gpu::Solver(hplp_gpu::Solver::BoxFormTag{}, device, m, n, lp.a.row_ptr().data(),
+                                   lp.a.col_idx().data(), lp.a.values().data(), lp.b.data(), lp.c.data());
+  });
+}
+
+int hplp_box_form_dims(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const double* val,
+                       const double* b, const double* c, int64_t* m_box, int64_t* n_box, double* upper) {
+  return guarded([&] {
+    hplp_gpu::SparseMatrix a = hplp_gpu::SparseMatrix::from_csr(m, n, row_ptr, col_idx, val);
+    const hplp_gpu::BoxForm f = hplp_gpu::detect_box_form(m, n, a.row_ptr().data(), a.col_idx().data(),
+                                                          a.values().data(), b, c);
+    *m_box = f.m, *n_box = f.n;
+    if (upper) std::copy(f.upper.begin(), f.upper.end(), upper);
+  });
 }
 
 int hplp_solver_create_team(const int32_t* devices, int32_t ndevices, int32_t nranks, int32_t ctas_per_rank,

@@ -284,10 +284,34 @@ struct PowerStart;
 using PowerStartFuture = std::shared_future<std::shared_ptr<PowerStart>>;
 PowerStartFuture draw_power_start_async(int64_t n, uint64_t seed);
 
+// Box form (no reference counterpart, a flagged
+// mode): the trailing bound rows x_j + s_j = u_j that to_standard_form
+// appends (src/lp_model.cpp:232-252) become column upper bounds enforced by
+// the primal projection, leaving the leading m x n block of the standard
+// form.  Detected structurally: trailing rows with entries (j, s), both 1.0,
+// where s is the matching trailing column, appears in no other row and has
+// c_s = 0; rhs >= 0.
+struct BoxForm {
+  int64_t m = 0, n = 0;             // the box LP: leading rows / columns
+  std::vector<int64_t> bound_col;   // per removed bound row t (row m + t, slack column n + t): column j
+  Vector upper;                     // length n: u_j, +inf where unbounded
+};
+BoxForm detect_box_form(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const double* val,
+                        const double* b, const double* c);
+
 // A device-resident problem: upload once, solve many times (bench, warm
 // starts).  Owns one hx context.
 class Solver {
  public:
+  struct BoxFormTag {};
+  // The box form of a standard-form LP (detect_box_form): solve() runs rHPDHG
+  // on it and maps the result back to the standard form's dimensions
+  // (slack s_j = u_j - x_j; bound-row dual max(0, -(c + A^T y)_j)).  No
+  // infeasibility scan; final_kkt is the box form's KKT error; trace iterates
+  // are box-form vectors.
+  Solver(BoxFormTag, int device, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+         const double* val, const double* b, const double* c);
+  bool box_form() const { return box_.has_value(); }
   Solver(const StandardFormLP& lp, int device = 0);
   Solver(int device, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const double* val,
          const double* b, const double* c);
@@ -315,8 +339,8 @@ class Solver {
                           : (r >= 0 && r < static_cast<int>(ranks_.size()) ? ranks_[r] : nullptr);
   }
   int nranks() const { return ranks_.empty() ? 1 : static_cast<int>(ranks_.size()); }
-  int64_t rows() const { return m_; }
-  int64_t cols() const { return n_; }
+  int64_t rows() const { return box_ ? box_->m_std : m_; }  // the standard form's dimensions
+  int64_t cols() const { return box_ ? box_->n_std : n_; }
   // a start vector drawn elsewhere (draw_power_start_async) for solves with `seed`
   void use_power_start(uint64_t seed, PowerStartFuture start) {
     start_seed_ = seed;
@@ -326,6 +350,13 @@ class Solver {
  private:
   uint64_t start_seed_ = 0;
   PowerStartFuture start_;  // invalid until drawn
+  struct BoxInfo {
+    int64_t m_std = 0, n_std = 0;
+    std::vector<int64_t> bound_col;
+    Vector bound_upper;  // u of each removed bound row (unscaled)
+  };
+  std::optional<BoxInfo> box_;
+  SolveResult solve_core(const SolverConfig& config);
   ::hx_ctx* ctx_ = nullptr;          // the context (a team: rank 0)
   std::vector<::hx_ctx*> ranks_;      // team in rank order; empty for one context
   int64_t m_ = 0, n_ = 0, nnz_ = 0;

@@ -196,6 +196,7 @@ struct KParams {
   hplp_epoch_t* epochs;  // ring of kEpochCap
   unsigned long long* prof;  // optional per-CTA phase timers [grid][8] (HX_PROFILE=1)
   Team T;                    // row partition + peers (loop_kernel_team only)
+  const double* ub;          // box form: column upper bounds (+inf: none); null: standard form
   // baseline schemes (loop_kernel_baseline): kAvgPool slots each
   double* xavg;   // n: mean x
   double* tavg;   // n: mean A^T y
@@ -634,8 +635,14 @@ __device__ __forceinline__ void push_peers(const Team* T, double* const* base, s
   }
 }
 
-template <bool RK>
+// BOX: the box form -- column upper
+// bounds u enforced by the projection instead of bound rows: x+ is clamped to
+// [0, u], the dual residual counts only columns without a finite bound, and a
+// fourth partial carries u_j [-(c + A^T y)_j]^+ (the bound part of the dual
+// objective).
+template <bool RK, bool BOX = false>
 struct EpiPrimal {  // phase A, rows of A^T
+  static constexpr int NQ = BOX ? 4 : 3;
   const double* xs;
   const double* xa;
   const double* c;
@@ -645,13 +652,14 @@ struct EpiPrimal {  // phase A, rows of A^T
   int mode;
   const Team* T;   // RK: peers of the x+ push
   size_t xp_off;   // offset of x+ in the x pools
+  const double* ub;  // BOX: upper bounds (+inf: none)
   struct In {
-    double xs, xa, c;
+    double xs, xa, c, u;
   };
   __device__ __forceinline__ In load(int j) const {
-    return In{ldcg(xs + j), mode ? ldcg(xa + j) : 0.0, __ldg(c + j)};
+    return In{ldcg(xs + j), mode ? ldcg(xa + j) : 0.0, __ldg(c + j), BOX ? __ldg(ub + j) : 0.0};
   }
-  __device__ __forceinline__ void apply(int j, double aty, const In& in, double (&t)[3]) const {
+  __device__ __forceinline__ void apply(int j, double aty, const In& in, double (&t)[NQ]) const {
     double x;
     if (mode) {
       const double omw = 1.0 - w;
@@ -663,13 +671,20 @@ struct EpiPrimal {  // phase A, rows of A^T
     const double cj = in.c;
     double xn = x - eta * (aty + cj);
     xn = xn < 0.0 ? 0.0 : xn;
+    if constexpr (BOX) xn = xn > in.u ? in.u : xn;
     xp[j] = xn;
     if constexpr (RK)
       if (T->nranks > 1) push_peers(T, T->px, xp_off + j, xn, __ldg(T->xneed + (j - T->col0)));
     double rc = -(cj + aty);
     rc = rc < 0.0 ? 0.0 : rc;
     const double dx = x - xn;
-    t[0] = rc * rc;
+    if constexpr (BOX) {
+      const bool bounded = in.u < INFINITY;
+      t[0] = bounded ? 0.0 : rc * rc;
+      t[3] = bounded ? in.u * rc : 0.0;
+    } else {
+      t[0] = rc * rc;
+    }
     t[1] = cj * x;
     t[2] = dx * dx;
   }
@@ -822,7 +837,8 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned 
 // rank's RankBar::rrec[parity][rank] before its arrival, which releases
 // them with the rest.
 __device__ bool team_sync(GridBar* bar, const Team& T, const Geo& g, unsigned long long& target,
-                          unsigned long long& repoch, const double* slots = nullptr, int reduce = -1) {
+                          unsigned long long& repoch, const double* slots = nullptr, int reduce = -1,
+                          bool box = false) {
   __shared__ int s_ok;
   __syncthreads();
   target += g.nctas;
@@ -848,19 +864,21 @@ __device__ bool team_sync(GridBar* bar, const Team& T, const Geo& g, unsigned lo
     }
     __syncthreads();
     if (s_ok) {
+      // q 0..2: phase A, 3..6: phase B, 7: the box term (phase A's fourth)
       const int q = threadIdx.x & 7, k = threadIdx.x >> 3;  // 512 threads: k < 64
-      if (q < 7) {
+      {
         const size_t stride = region_stride(g.nrec);
-        const double* rg = slots + static_cast<size_t>(q < 3 ? kRegA + reduce : kRegB + reduce) * stride +
-                           (q < 3 ? q : q - 3);
+        const double* rg = slots + static_cast<size_t>(q < 3 || q == 7 ? kRegA + reduce : kRegB + reduce) * stride +
+                           (q < 3 ? q : q == 7 ? 3 : q - 3);
         const size_t r0 = static_cast<size_t>(T.rank) * g.nctas;
         double v = 0.0;
-        for (int c = k; c < g.nctas; c += 64) v += ldcg(rg + (r0 + c) * kMaxQ);
+        if (q < 7 || box)
+          for (int c = k; c < g.nctas; c += 64) v += ldcg(rg + (r0 + c) * kMaxQ);
         part[k][q] = v;
       }
       __syncthreads();
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-      if (warp < 7) {
+      if (warp < 8) {
         const double v = warp_sum(part[lane][warp] + part[lane + 32][warp]);
         for (int d = lane; d < T.nranks * kRankRecReplicas; d += 32)
           T.pb[d % T.nranks]->rrec[reduce][d / T.nranks][T.rank][warp] = v;
@@ -1258,34 +1276,43 @@ __device__ __forceinline__ double* region_ptr(const KParams* P, int r, int nrec)
 __device__ __forceinline__ int gwarp_id(const Geo& g) { return g.cta * kWarps + (threadIdx.x >> 5); }
 
 // phase A: A^T y, primal step (+ Halpern formation of x), primal partials
-template <bool RK>
-__device__ HX_PHASE_INLINE void phase_primal(const KParams* P, const Roles* R, int par, WarpStage* stage,
-                                             unsigned long long seq, const SpmvHead& head, const Geo& g) {
+template <bool RK, bool BOX>
+__device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R, int par, WarpStage* stage,
+                                               unsigned long long seq, const SpmvHead& head, const Geo& g) {
+  constexpr int NQ = EpiPrimal<RK, BOX>::NQ;
   const int n = P->n, m = P->m;
-  double acc[3];
-  acc_init<3, 0>(acc);
-  EpiPrimal<RK> e{xsrc_ptr(P, R),
-              P->xpool + static_cast<size_t>(R->x_anchor) * n,
-              P->c,
-              P->xpool + static_cast<size_t>(R->zx_out) * n,
-              P->xpool + static_cast<size_t>(R->xp_out) * n,
-              R->w_x,
-              R->eta,
-              R->x_mode,
-              &P->T,
-              static_cast<size_t>(R->xp_out) * n};
+  double acc[NQ];
+  acc_init<NQ, 0>(acc);
+  EpiPrimal<RK, BOX> e{xsrc_ptr(P, R),
+                       P->xpool + static_cast<size_t>(R->x_anchor) * n,
+                       P->c,
+                       P->xpool + static_cast<size_t>(R->zx_out) * n,
+                       P->xpool + static_cast<size_t>(R->xp_out) * n,
+                       R->w_x,
+                       R->eta,
+                       R->x_mode,
+                       &P->T,
+                       static_cast<size_t>(R->xp_out) * n,
+                       P->ub};
   const Sched S = P->AT;
 #ifdef HX_WPROF
   const unsigned long long w0 = clock64();
 #endif
-  spmv_rows<3, 0>(S, par, SrcVec{ycur_ptr(P, R)}, e, acc, gwarp_id(g),
-                  threadIdx.x & 31, stage, seq, head);
+  spmv_rows<NQ, 0>(S, par, SrcVec{ycur_ptr(P, R)}, e, acc, gwarp_id(g),
+                   threadIdx.x & 31, stage, seq, head);
 #ifdef HX_WPROF
   if constexpr (!RK)
     if (P->prof && (threadIdx.x & 31) == 0) P->prof[gridDim.x * 16 + gwarp_id(g)] += clock64() - w0;
 #endif
-  fold_long<3, 0>(S, par, seq, acc, g.cta);
-  block_to_slots<3, 0, RK>(acc, P, kRegA + par, g);
+  fold_long<NQ, 0>(S, par, seq, acc, g.cta);
+  block_to_slots<NQ, 0, RK>(acc, P, kRegA + par, g);
+}
+
+template <bool RK>
+__device__ __forceinline__ void phase_primal(const KParams* P, const Roles* R, int par, WarpStage* stage,
+                                             unsigned long long seq, const SpmvHead& head, const Geo& g) {
+  if (P->ub) phase_primal_t<RK, true>(P, R, par, stage, seq, head, g);
+  else phase_primal_t<RK, false>(P, R, par, stage, seq, head, g);
 }
 
 // phase B: A x+, dual step, speculative Halpern combos, dual partials
@@ -1328,15 +1355,18 @@ __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int
 // and a xor butterfly finishes -- commutative pairwise adds, so every lane of
 // every CTA holds bit-identical totals.
 constexpr int kTotRounds = 5;  // 160 records in one round of loads
-__device__ __forceinline__ void warp_totals_main(const KParams* P, int par, double (&t)[7], const Geo& g) {
+// t[0..2]: phase A partials, t[3..6]: phase B, t[7]: the box form's bound
+// term of the dual objective (phase A's fourth partial; 0 in standard form)
+__device__ __forceinline__ void warp_totals_main(const KParams* P, int par, double (&t)[8], const Geo& g) {
   const int lane = threadIdx.x & 31, G = g.nrec;
   const size_t rep = static_cast<size_t>(g.cta % kReplicas) * G * kMaxQ;
   const double* ra = region_ptr(P, kRegA + par, G) + rep;
   const double* rb = region_ptr(P, kRegB + par, G) + rep;
+  const bool box = P->ub != nullptr;
 #pragma unroll
-  for (int q = 0; q < 7; ++q) t[q] = 0.0;
+  for (int q = 0; q < 8; ++q) t[q] = 0.0;
   for (int base = 0; base < G; base += 32 * kTotRounds) {
-    double v[kTotRounds][7];
+    double v[kTotRounds][8];
 #pragma unroll
     for (int i = 0; i < kTotRounds; ++i) {
       const int c = base + 32 * i + lane;
@@ -1347,25 +1377,26 @@ __device__ __forceinline__ void warp_totals_main(const KParams* P, int par, doub
       for (int q = 0; q < 3; ++q) v[i][q] = ok ? ldcg(a + q) : 0.0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) v[i][3 + q] = ok ? ldcg(b + q) : 0.0;
+      v[i][7] = ok && box ? ldcg(a + 3) : 0.0;
     }
 #pragma unroll
     for (int i = 0; i < kTotRounds; ++i)
 #pragma unroll
-      for (int q = 0; q < 7; ++q) t[q] += v[i][q];
+      for (int q = 0; q < 8; ++q) t[q] += v[i][q];
   }
 #pragma unroll
-  for (int q = 0; q < 7; ++q) t[q] = warp_sum(t[q]);
+  for (int q = 0; q < 8; ++q) t[q] = warp_sum(t[q]);
 }
 
 // Team totals: the nranks rank records of this parity, summed in rank order
 // (every lane, identical on every rank).
-__device__ __forceinline__ void warp_totals_ranks(const KParams* P, int par, double (&t)[7], int cta) {
+__device__ __forceinline__ void warp_totals_ranks(const KParams* P, int par, double (&t)[8], int cta) {
   const double (*rr)[8] = P->T.pb[P->T.rank]->rrec[par][cta % kRankRecReplicas];
 #pragma unroll
-  for (int q = 0; q < 7; ++q) t[q] = ldcg(&rr[0][q]);
+  for (int q = 0; q < 8; ++q) t[q] = ldcg(&rr[0][q]);
   for (int r = 1; r < P->T.nranks; ++r)
 #pragma unroll
-    for (int q = 0; q < 7; ++q) t[q] += ldcg(&rr[r][q]);
+    for (int q = 0; q < 8; ++q) t[q] += ldcg(&rr[r][q]);
 }
 
 // power iteration halves: w = A x (x = x0 or z / zn), z = A^T w
@@ -1936,7 +1967,7 @@ __device__ __forceinline__ void loop_body_baseline(const KParams* P, const Geo& 
       }
     }
     if (warp == 0) {
-      double t[7];
+      double t[8];
       warp_totals_main(P, par, t, g);
       if (lane == 0) {
         for (int i = 0; i < 7; ++i) tot[i] = t[i];
@@ -2036,7 +2067,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
   // main reduction there
   auto sync_reduce = [&](int pr) -> bool {
     if constexpr (RK) {
-      if (!solo) return team_sync(bar, P->T, g, target, repoch, P->slots, P->T.prereduce ? pr : -1);
+      if (!solo) return team_sync(bar, P->T, g, target, repoch, P->slots, P->T.prereduce ? pr : -1, P->ub != nullptr);
     }
     return grid_sync(bar, target);
   };
@@ -2152,7 +2183,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
     mark(3);
     if (warp == 0) {
       unsigned long long cA = clock64(), cB = 0, cC = 0;
-      double t[7];
+      double t[8];
       if (solo || !P->T.prereduce) warp_totals_main(P, par, t, g);
       else warp_totals_ranks(P, par, t, g.cta);
       // the independent fp64 divides / square roots, one per lane, executed
@@ -2160,7 +2191,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
       double num = 1.0, den = 1.0;
       if (lane == 0) num = t[3], den = 1.0 + C.b_norm;
       else if (lane == 1) num = t[0], den = 1.0 + C.c_norm;
-      else if (lane == 2) num = fabs(t[1] + t[4]), den = 1.0 + fabs(t[1]) + fabs(t[4]);
+      else if (lane == 2) num = fabs(t[1] + (t[4] + t[7])), den = 1.0 + fabs(t[1]) + fabs(t[4] + t[7]);
       else if (lane == 3) num = t[2], den = C.r.eta;
       else if (lane == 4) num = t[5], den = C.r.eta;
       else if (lane == 5) den = static_cast<double>(C.k + 2);
@@ -2341,9 +2372,9 @@ __global__ void cert_kernel(int len, int normalized, double scale, double factor
 // Fixed-order partial sums for the setup norms and kkt_current.
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 kkt_partials_kernel(int m, int n, const double* ax, const double* b, const double* aty,
-                    const double* c, const double* x, const double* y, double* slots) {
-  double acc[6];
-  acc_init<6, 0>(acc);
+                    const double* c, const double* x, const double* y, double* slots, const double* ub = nullptr) {
+  double acc[7];
+  acc_init<7, 0>(acc);
   const int gtid = blockIdx.x * kThreads + threadIdx.x, gs = gridDim.x * kThreads;
   for (int i = gtid; i < m; i += gs) {
     const double bi = b[i];
@@ -2359,12 +2390,14 @@ kkt_partials_kernel(int m, int n, const double* ax, const double* b, const doubl
     if (aty) {
       double r = -(cj + aty[j]);
       r = r < 0.0 ? 0.0 : r;
-      acc[1] += r * r;
+      const double u = ub ? ub[j] : INFINITY;  // box form: bounded columns enter the dual objective
+      if (u < INFINITY) acc[6] += u * r;
+      else acc[1] += r * r;
       acc[2] += cj * x[j];
     }
     acc[5] += cj * cj;
   }
-  block_to_slots<6, 0>(acc, slots, gridDim.x);
+  block_to_slots<7, 0>(acc, slots, gridDim.x);
 }
 
 // Trace diagnostics (src/solver.cpp:283-287): sums of the normalized
@@ -2485,6 +2518,10 @@ __global__ void scale_csr_kernel(int rows, const int* rp, const int* ci, double*
     }
 }
 
+__global__ void div_vec_kernel(int len, double* v, const double* d) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) v[i] /= d[i];
+}
+
 __global__ void scale_vec_kernel(int len, double* v, const double* d) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) v[i] = v[i] * d[i];
 }
@@ -2544,6 +2581,7 @@ struct hx_ctx {
   double* yavg = nullptr;
   double* aavg = nullptr;
   double* xbar = nullptr;
+  double* ub = nullptr;  // box form: column upper bounds (hx_set_box)
   double* slots = nullptr;
   double* scratch = nullptr;  // kMaxQ doubles
   Ctl* ctl = nullptr;
@@ -2553,6 +2591,7 @@ struct hx_ctx {
   hplp_epoch_t* epochs = nullptr;
   Ctl h;  // host mirror
   double b_norm = 0, c_norm = 0;
+  double b_sq = 0, u_sq = 0;  // ||b||^2 of the device problem; box form: sum of finite u_j^2
   double time_limit_s = 0, loop_elapsed_s = 0;  // SolverConfig::time_limit_seconds budget of the loop
   // Row-partitioned team (hx_set_partition / hx_team_*).  The
   // context keeps the full problem (setup kernels, power iteration and the
@@ -2655,8 +2694,8 @@ void free_problem(hx_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   dfree(c->a_ptr), dfree(c->a_idx), dfree(c->a_val), dfree(c->t_ptr), dfree(c->t_idx), dfree(c->t_val);
   dfree(c->b), dfree(c->c), dfree(c->xpool), dfree(c->ypool), dfree(c->axpool), dfree(c->upool);
-  dfree(c->xavg), dfree(c->tavg), dfree(c->yavg), dfree(c->aavg), dfree(c->xbar);
-  c->xavg = c->tavg = c->yavg = c->aavg = c->xbar = nullptr;
+  dfree(c->xavg), dfree(c->tavg), dfree(c->yavg), dfree(c->aavg), dfree(c->xbar), dfree(c->ub);
+  c->xavg = c->tavg = c->yavg = c->aavg = c->xbar = c->ub = nullptr;
   free_sched(c->sa);
   free_sched(c->st);
   free_sched(c->pa);
@@ -2752,6 +2791,7 @@ KParams params(hx_ctx* c) {
   P.axpool = c->axpool;
   P.upool = c->upool;
   P.slots = c->slots;
+  P.ub = c->ub;
   P.ctl = c->ctl;
   P.bar = c->bar;
   P.epochs = c->epochs;
@@ -3233,6 +3273,7 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   HX_CUDA(c, cudaMemcpyAsync(tot, c->scratch, sizeof(tot), cudaMemcpyDeviceToHost, s));
   HX_CUDA(c, cudaStreamSynchronize(s));
   c->launches += 2;
+  c->b_sq = tot[4];
   c->b_norm = std::sqrt(tot[4]);
   c->c_norm = std::sqrt(tot[5]);
   tick("pools+norms");
@@ -3266,7 +3307,8 @@ int hx_precondition(hx_ctx* c, int32_t ruiz_iters, double pc_alpha, double* row_
     scale_csr_kernel<<<nb, 256, 0, s>>>(n, c->t_ptr, c->t_idx, c->t_val, dr, dc, 1);
     scale_vec_kernel<<<nb, 256, 0, s>>>(m, c->b, dr);
     scale_vec_kernel<<<nb, 256, 0, s>>>(n, c->c, dc);
-    c->launches += 6;
+    if (c->ub) div_vec_kernel<<<nb, 256, 0, s>>>(n, c->ub, dc);  // x = C x': x' <= u / C
+    c->launches += c->ub ? 7 : 6;
     HX_CUDA(c, cudaGetLastError());
     return HPLP_OK;
   };
@@ -3293,9 +3335,49 @@ int hx_precondition(hx_ctx* c, int32_t ruiz_iters, double pc_alpha, double* row_
   HX_CUDA(c, cudaMemcpyAsync(tot, c->scratch, sizeof(tot), cudaMemcpyDeviceToHost, s));
   HX_CUDA(c, cudaStreamSynchronize(s));
   c->launches += 2;
-  c->b_norm = std::sqrt(tot[4]);
+  c->b_sq = tot[4];
+  if (c->ub) {  // box form: ||b|| of the standard form it stands for (rescaled u)
+    std::vector<double> u(static_cast<size_t>(n));
+    if (n) HX_CUDA(c, cudaMemcpy(u.data(), c->ub, n * sizeof(double), cudaMemcpyDeviceToHost));
+    c->u_sq = 0.0;
+    for (double v : u)
+      if (v < INFINITY) c->u_sq += v * v;
+  }
+  c->b_norm = std::sqrt(c->b_sq + (c->ub ? c->u_sq : 0.0));
   c->c_norm = std::sqrt(tot[5]);
   dfree(dr), dfree(dc), dfree(R), dfree(Cs);
+  c->setup_done = false;
+  return HPLP_OK;
+}
+
+// Box form: column upper bounds enforced by the primal
+// projection, x in [0, u] (u = +inf: no bound); NULL returns to the standard
+// form.  Set after hx_upload_csr and before hx_precondition / hx_setup.
+int hx_set_box(hx_ctx* c, const double* upper) {
+  if (!c->uploaded) return set_err(c, HPLP_ESTATE, "hx_set_box: no problem uploaded");
+  HX_CUDA(c, cudaSetDevice(c->device));
+  if (!upper) {
+    dfree(c->ub);
+    c->ub = nullptr;
+    c->u_sq = 0.0;
+    c->b_norm = std::sqrt(c->b_sq);
+    c->setup_done = false;
+    return HPLP_OK;
+  }
+  double u_sq = 0.0;
+  for (int64_t j = 0; j < c->n; ++j) {
+    if (std::isnan(upper[j]) || upper[j] < 0.0)
+      return set_err(c, HPLP_EINVAL, "hx_set_box: upper bounds must be >= 0 (or +inf)");
+    if (upper[j] < INFINITY) u_sq += upper[j] * upper[j];
+  }
+  // the KKT primal residual is relative to the standard form's ||b|| (b and
+  // the bound rows' u), so the box form's KKT equals the standard form's at
+  // the mapped iterate and tolerances mean the same
+  c->u_sq = u_sq;
+  c->b_norm = std::sqrt(c->b_sq + u_sq);
+  if (!c->ub) HX_CUDA(c, dalloc(&c->ub, std::max<int64_t>(c->n, 1)));
+  if (c->n) HX_CUDA(c, cudaMemcpyAsync(c->ub, upper, c->n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  HX_CUDA(c, cudaStreamSynchronize(c->stream));
   c->setup_done = false;
   return HPLP_OK;
 }
@@ -3375,6 +3457,10 @@ int hx_setup(hx_ctx* c, const hplp_config_t* cfg, double sigma_used, double eta,
     return set_err(c, HPLP_EINVAL, "hx_setup: unknown scheme");
   if (cfg->scheme != HPLP_SCHEME_RHPDHG && c->ranked)
     return set_err(c, HPLP_EINVAL, "hx_setup: the baseline schemes run on one device (no team)");
+  if (c->ub && cfg->scheme != HPLP_SCHEME_RHPDHG)
+    return set_err(c, HPLP_EINVAL, "hx_setup: the box form runs rHPDHG only");
+  if (c->ub && cfg->infeasibility_check_period > 0)
+    return set_err(c, HPLP_EINVAL, "hx_setup: the box form has no infeasibility scan (set infeasibility_check_period 0)");
   cudaStream_t s = c->stream;
   if (cfg->scheme >= HPLP_SCHEME_AVERAGED && !c->xavg) {  // running-average slots
     HX_CUDA(c, dalloc(&c->xavg, static_cast<size_t>(kAvgPool) * c->n));
@@ -3911,16 +3997,17 @@ int hx_kkt_current(hx_ctx* c, hplp_kkt_t* out) {
   rc = spmv_dev(c, true, ycur, aty);
   if (rc) return rc;
   kkt_partials_kernel<<<c->grid, kThreads, 0, s>>>(static_cast<int>(c->m), static_cast<int>(c->n), ax, c->b, aty,
-                                                   c->c, xcur, ycur, c->slots);
-  final_reduce_kernel<<<1, 256, 0, s>>>(c->slots, c->grid, 6, c->scratch);
+                                                   c->c, xcur, ycur, c->slots, c->ub);
+  final_reduce_kernel<<<1, 256, 0, s>>>(c->slots, c->grid, 7, c->scratch);
   c->launches += 2;
-  double tot[6];
+  double tot[7];
   HX_CUDA(c, cudaMemcpyAsync(tot, c->scratch, sizeof(tot), cudaMemcpyDeviceToHost, s));
   HX_CUDA(c, cudaStreamSynchronize(s));
-  // kkt_error_with_products, src/pdhg_core.cpp:57-68 (scalar epilogue)
+  // kkt_error_with_products, src/pdhg_core.cpp:57-68 (scalar epilogue); box
+  // form: b^T y + sum u_j [-(c + A^T y)_j]^+ in the gap (tot[6] = 0 otherwise)
   out->primal_residual = std::sqrt(tot[0]) / (1.0 + c->b_norm);
   out->dual_residual = std::sqrt(tot[1]) / (1.0 + c->c_norm);
-  out->gap_residual = std::fabs(tot[2] + tot[3]) / (1.0 + std::fabs(tot[2]) + std::fabs(tot[3]));
+  out->gap_residual = std::fabs(tot[2] + (tot[3] + tot[6])) / (1.0 + std::fabs(tot[2]) + std::fabs(tot[3] + tot[6]));
   out->max_relative = std::max({out->primal_residual, out->dual_residual, out->gap_residual});
   return HPLP_OK;
 }

@@ -345,8 +345,123 @@ Solver::~Solver() {
   for (hx_ctx* x : ranks_) hx_destroy(x);
 }
 
-// solve(): src/solver.cpp:206-342.
+BoxForm detect_box_form(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const double* val,
+                        const double* b, const double* c) {
+  BoxForm f;
+  f.m = m, f.n = n;
+  if (m <= 0 || n <= 0) {
+    f.upper.assign(static_cast<std::size_t>(std::max<int64_t>(n, 0)), std::numeric_limits<double>::infinity());
+    return f;
+  }
+  std::vector<int32_t> count(static_cast<std::size_t>(n), 0);
+  for (int64_t p = 0; p < row_ptr[m]; ++p) ++count[col_idx[p]];
+  // trailing rows t = 0, 1, ... from the end: row m-1-t pairs a column with slack n-1-t
+  std::vector<int64_t> cols;
+  std::vector<double> rhs;
+  while (static_cast<int64_t>(cols.size()) < std::min(m, n - 1)) {
+    const int64_t k = static_cast<int64_t>(cols.size());
+    const int64_t i = m - 1 - k, s = n - 1 - k;
+    if (row_ptr[i + 1] - row_ptr[i] != 2) break;
+    const int64_t p = row_ptr[i];
+    if (col_idx[p + 1] != s || col_idx[p] >= s || val[p] != 1.0 || val[p + 1] != 1.0) break;
+    if (count[s] != 1 || c[s] != 0.0 || !(b[i] >= 0.0)) break;
+    cols.push_back(col_idx[p]);
+    rhs.push_back(b[i]);
+  }
+  // the bounded columns must lie in the remaining block, one bound each
+  int64_t T = static_cast<int64_t>(cols.size());
+  while (T > 0) {
+    std::vector<char> seen(static_cast<std::size_t>(n - T), 0);
+    bool ok = true;
+    for (int64_t t = 0; t < T && ok; ++t) {
+      const int64_t j = cols[static_cast<std::size_t>(t)];
+      if (j >= n - T || seen[static_cast<std::size_t>(j)]) ok = false;
+      else seen[static_cast<std::size_t>(j)] = 1;
+    }
+    if (ok) break;
+    --T;
+  }
+  f.m = m - T, f.n = n - T;
+  f.upper.assign(static_cast<std::size_t>(f.n), std::numeric_limits<double>::infinity());
+  f.bound_col.resize(static_cast<std::size_t>(T));
+  for (int64_t t = 0; t < T; ++t) {  // row f.m + t is cols[T - 1 - t] (found from the end)
+    const int64_t j = cols[static_cast<std::size_t>(T - 1 - t)];
+    f.bound_col[static_cast<std::size_t>(t)] = j;
+    f.upper[static_cast<std::size_t>(j)] = rhs[static_cast<std::size_t>(T - 1 - t)];
+  }
+  return f;
+}
+
+Solver::Solver(BoxFormTag, int device, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+               const double* val, const double* b, const double* c) {
+  BoxForm f = detect_box_form(m, n, row_ptr, col_idx, val, b, c);
+  // the leading block: its rows reference only leading columns (each slack
+  // appears in its bound row alone), so the caller's arrays serve as they are
+  m_ = f.m, n_ = f.n, nnz_ = row_ptr[f.m];
+  int rc = hx_create(device, &ctx_);
+  if (rc != HPLP_OK) throw_hx(nullptr, rc);
+  auto fail = [&](int code) {
+    const std::string msg = hx_last_error(ctx_);
+    hx_destroy(ctx_);
+    ctx_ = nullptr;
+    if (code == HPLP_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error("hplp_gpu: " + msg);
+  };
+  rc = hx_upload_csr(ctx_, f.m, f.n, row_ptr, col_idx, val, b, c);
+  if (rc != HPLP_OK) fail(rc);
+  rc = hx_set_box(ctx_, f.upper.data());
+  if (rc != HPLP_OK) fail(rc);
+  BoxInfo info;
+  info.m_std = m, info.n_std = n;
+  info.bound_col = std::move(f.bound_col);
+  info.bound_upper.resize(info.bound_col.size());
+  for (std::size_t t = 0; t < info.bound_col.size(); ++t)
+    info.bound_upper[t] = f.upper[static_cast<std::size_t>(info.bound_col[t])];
+  box_ = std::move(info);
+}
+
 SolveResult Solver::solve(const SolverConfig& config) {
+  if (!box_) return solve_core(config);
+  const BoxInfo& B = *box_;
+  if (config.scheme != HPLP_SCHEME_RHPDHG) throw std::invalid_argument("box form: rHPDHG only");
+  SolverConfig cfg = config;
+  cfg.infeasibility_check_period = 0;  // no certificates in the box form
+  if (cfg.initial_iterate) {  // standard-form dimensions: the leading parts
+    Iterate z = *cfg.initial_iterate;
+    if (static_cast<int64_t>(z.x.size()) == B.n_std && static_cast<int64_t>(z.y.size()) == B.m_std) {
+      z.x.resize(static_cast<std::size_t>(n_));
+      z.y.resize(static_cast<std::size_t>(m_));
+      cfg.initial_iterate = std::move(z);
+    }
+  }
+  SolveResult r = solve_core(cfg);
+  // back to the standard form: slack s_j = u_j - x_j, bound-row dual
+  // max(0, -(c + A^T y)_j), evaluated on the device problem (scaled by C, R
+  // when preconditioned: c' + A'^T y' = C (c + A^T y), y' = y / R)
+  Iterate& z = r.final_iterate;
+  Vector ys(z.y);
+  if (scaled_)
+    for (std::size_t i = 0; i < ys.size(); ++i) ys[i] /= row_scale_[i];
+  Vector aty(static_cast<std::size_t>(n_)), cdev(static_cast<std::size_t>(n_));
+  check(ctx_, hx_spmv_transpose(ctx_, ys.data(), aty.data()));
+  check(ctx_, hx_download_problem(ctx_, nullptr, nullptr, nullptr, nullptr, cdev.data()));
+  const std::size_t T = B.bound_col.size();
+  z.x.resize(static_cast<std::size_t>(B.n_std));
+  z.y.resize(static_cast<std::size_t>(B.m_std));
+  for (std::size_t t = 0; t < T; ++t) {
+    const std::size_t j = static_cast<std::size_t>(B.bound_col[t]);
+    // (a Halpern combination of two points at u_j may exceed it by an ulp)
+    const double slack = B.bound_upper[t] - z.x[j];
+    z.x[static_cast<std::size_t>(n_) + t] = slack < 0.0 ? 0.0 : slack;
+    double lam = cdev[j] + aty[j];
+    if (scaled_) lam /= col_scale_[j];
+    z.y[static_cast<std::size_t>(m_) + t] = lam < 0.0 ? -lam : 0.0;
+  }
+  return r;
+}
+
+// solve(): src/solver.cpp:206-342.
+SolveResult Solver::solve_core(const SolverConfig& config) {
   const auto t0 = Clock::now();
   auto since = [&] { return std::chrono::duration<double>(Clock::now() - t0).count(); };
   // HPLP_TIMING=1: cumulative wall time of the solve stages on stderr

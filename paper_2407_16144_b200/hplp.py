@@ -71,6 +71,8 @@ def lib() -> C.CDLL:
     sig("hplp_solver_team_export", C.c_int, V, C.c_char_p, I64, PI64)
     sig("hplp_solver_team_import", C.c_int, V, C.c_char_p, I64)
     sig("hplp_plan_partition", C.c_int, I64, I64, PI64, PI32, I32, PI64, PI64)
+    sig("hplp_solver_create_box", C.c_int, I32, I64, I64, PI64, PI32, PD, PD, PD, PV)
+    sig("hplp_box_form_dims", C.c_int, I64, I64, PI64, PI32, PD, PD, PD, PI64, PI64, PD)
     # MPS ingestion + reports (inc/hplp/mps_io.hpp)
     sig("hplp_mps_parse", C.c_int, C.c_char_p, PV, PI64, PI64, PI64)
     sig("hplp_mps_view", C.c_int, V, C.POINTER(abi.General))
@@ -281,6 +283,26 @@ class Solver:
         self.h = h
         self._keep = None
         self.nranks = int(nranks)
+        self.hx = HX(L.hplp_solver_hx(h), owned=False)
+        return self
+
+    @classmethod
+    def box(cls, m, n, row_ptr, col_idx, val, b, c, device: int = 0) -> "Solver":
+        """The box form of a standard-form LP (hplp_solver_create_box; no
+        reference counterpart): bound rows become the
+        projection x in [0, u].  solve() returns standard-form x, y; no
+        infeasibility scan; final KKT of the box form."""
+        self = cls.__new__(cls)
+        L = lib()
+        self.m, self.n = int(m), int(n)
+        rp, ci, v, bb, cc = (np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col_idx, np.int32),
+                             np.ascontiguousarray(val, np.float64), np.ascontiguousarray(b, np.float64),
+                             np.ascontiguousarray(c, np.float64))
+        h = C.c_void_p()
+        _check(L.hplp_solver_create_box(int(device), self.m, self.n, i64ptr(rp), i32ptr(ci), dptr(v), dptr(bb),
+                                        dptr(cc), C.byref(h)))
+        self.h = h
+        self._keep = None
         self.hx = HX(L.hplp_solver_hx(h), owned=False)
         return self
 
@@ -543,6 +565,18 @@ class HX:
             self.close()
         except Exception:
             pass
+
+
+def box_form(m, n, row_ptr, col_idx, val, b, c):
+    """hplp_box_form_dims: (m_box, n_box, upper[n_box]) of a standard-form LP."""
+    rp, ci, v, bb, cc = (np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col_idx, np.int32),
+                         np.ascontiguousarray(val, np.float64), np.ascontiguousarray(b, np.float64),
+                         np.ascontiguousarray(c, np.float64))
+    mb, nb = C.c_int64(), C.c_int64()
+    up = np.empty(int(n))
+    _check(lib().hplp_box_form_dims(int(m), int(n), i64ptr(rp), i32ptr(ci), dptr(v), dptr(bb), dptr(cc),
+                                    C.byref(mb), C.byref(nb), dptr(up)))
+    return mb.value, nb.value, up[: nb.value].copy()
 
 
 def plan_partition(m, n, row_ptr, col_idx, parts):
