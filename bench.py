@@ -365,6 +365,50 @@ def run_gpu(args):
                                       "margin": meta["margin"], "at_iteration": meta["at_iteration"]}
             ttt[label] = rec
 
+    # box form (flagged: a different iteration, not the
+    # reference's): loop rate on the same LP with the bound rows replaced by
+    # the projection, and its time to 1e-4 (its KKT equals the standard
+    # form's at the mapped iterate)
+    box = None
+    if world == 1 and not sharded and not args.no_box:
+        bs = hplp.Solver.box(*s.csr(), device=local)
+        bcfg = abi.Config.default(tolerance=1e-4, iteration_limit=10**9, infeasibility_check_period=0)
+        b0 = bs.solve(iteration_limit=0)
+        bhx = bs.hx
+        bstream = torch.cuda.ExternalStream(bhx.stream(), device=torch.device("cuda", local))
+        bhx.setup(bcfg, b0["sigma_estimate"], b0["eta"])
+        bhx.run(ITERS_PER_STEP)
+        btimes = []
+        for _ in range(3):
+            if bhx.progress().status >= 0:
+                bhx.setup(bcfg, b0["sigma_estimate"], b0["eta"])
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(bstream)
+            bhx.run(ITERS_PER_STEP)
+            e1.record(bstream)
+            e1.synchronize()
+            btimes.append(e0.elapsed_time(e1) / 1e3)
+        mb, nb, nnzb = bhx.m, bhx.n, bhx.nnz
+        bval = ITERS_PER_STEP * len(btimes) / sum(btimes)
+        bb = algorithmic_bytes(mb, nb, nnzb) + 8 * nb  # + the bounds u
+        bs.close()
+        box = {"value": bval, "unit": UNIT, "standard_form": [m, n, nnz], "box_form": [mb, nb, nnzb],
+               "algorithmic_bytes_per_iter": bb, "roofline_frac": bb * bval / 1e9 / peak,
+               "note": "hplp_solver_create_box: bound rows -> projection x in [0,u]; not the reference's iteration"}
+        if not args.no_ttt:
+            opts = dict(precondition_ruiz_iters=0, precondition_pc_alpha=0.5)
+            t0 = time.perf_counter()
+            bs = hplp.Solver.box(*s.csr(), device=local)
+            rr = bs.solve(tolerance=1e-4, time_limit_seconds=args.ttt_cap, **opts)
+            bs.close()
+            dt = time.perf_counter() - t0
+            _, obj = s.recover(rr["x"])
+            box["time_to_1e-4"] = {"status": rr["status"], "seconds": round(dt, 4), "iterations": rr["iterations"],
+                                   "kkt_max": rr["kkt"][3], "objective": obj,
+                                   "planted_objective": g.planted_objective, "settings": opts}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         kind, cval, info = cpu_iters_per_sec(s, args.cpu_iters)
@@ -406,6 +450,7 @@ def run_gpu(args):
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "time_to_1e-4": ttt,
+            "box_form": box,
             "team_check": team_check,
             "per_step_ms": [round(1e3 * t, 3) for t in times],
         }
@@ -441,6 +486,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-box", action="store_true", help="skip the box-form leg")
     ap.add_argument("--cpu-iters", type=int, default=40)
     ap.add_argument("--ref-iters", type=int, default=30)
     ap.add_argument("--ttt-cap", type=float, default=60.0)

@@ -1308,13 +1308,6 @@ __device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R,
   block_to_slots<NQ, 0, RK>(acc, P, kRegA + par, g);
 }
 
-template <bool RK>
-__device__ __forceinline__ void phase_primal(const KParams* P, const Roles* R, int par, WarpStage* stage,
-                                             unsigned long long seq, const SpmvHead& head, const Geo& g) {
-  if (P->ub) phase_primal_t<RK, true>(P, R, par, stage, seq, head, g);
-  else phase_primal_t<RK, false>(P, R, par, stage, seq, head, g);
-}
-
 // phase B: A x+, dual step, speculative Halpern combos, dual partials
 template <bool RK>
 __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int par, WarpStage* stage,
@@ -1357,12 +1350,12 @@ __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int
 constexpr int kTotRounds = 5;  // 160 records in one round of loads
 // t[0..2]: phase A partials, t[3..6]: phase B, t[7]: the box form's bound
 // term of the dual objective (phase A's fourth partial; 0 in standard form)
+template <bool BOX>
 __device__ __forceinline__ void warp_totals_main(const KParams* P, int par, double (&t)[8], const Geo& g) {
   const int lane = threadIdx.x & 31, G = g.nrec;
   const size_t rep = static_cast<size_t>(g.cta % kReplicas) * G * kMaxQ;
   const double* ra = region_ptr(P, kRegA + par, G) + rep;
   const double* rb = region_ptr(P, kRegB + par, G) + rep;
-  const bool box = P->ub != nullptr;
 #pragma unroll
   for (int q = 0; q < 8; ++q) t[q] = 0.0;
   for (int base = 0; base < G; base += 32 * kTotRounds) {
@@ -1377,15 +1370,15 @@ __device__ __forceinline__ void warp_totals_main(const KParams* P, int par, doub
       for (int q = 0; q < 3; ++q) v[i][q] = ok ? ldcg(a + q) : 0.0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) v[i][3 + q] = ok ? ldcg(b + q) : 0.0;
-      v[i][7] = ok && box ? ldcg(a + 3) : 0.0;
+      v[i][7] = BOX && ok ? ldcg(a + 3) : 0.0;
     }
 #pragma unroll
     for (int i = 0; i < kTotRounds; ++i)
 #pragma unroll
-      for (int q = 0; q < 8; ++q) t[q] += v[i][q];
+      for (int q = 0; q < (BOX ? 8 : 7); ++q) t[q] += v[i][q];
   }
 #pragma unroll
-  for (int q = 0; q < 8; ++q) t[q] = warp_sum(t[q]);
+  for (int q = 0; q < (BOX ? 8 : 7); ++q) t[q] = warp_sum(t[q]);
 }
 
 // Team totals: the nranks rank records of this parity, summed in rank order
@@ -1945,7 +1938,7 @@ __device__ __forceinline__ void loop_body_baseline(const KParams* P, const Geo& 
     const int par = static_cast<int>(C.it & 1);
     SpmvHead head;
     spmv_head(P->AT, gwarp_id(g), lane, head);
-    if (vanilla) phase_primal<false>(P, R, par, stage, ++seq, head, g);
+    if (vanilla) phase_primal_t<false, false>(P, R, par, stage, ++seq, head, g);
     else phase_primal_avg(P, R, par, stage, ++seq, head, g);
     if (writer && threadIdx.x == 0 && budget != 0ull)
       bar->time_up[par] = (global_ns() - t_start) > budget ? 1u : 0u;
@@ -1968,7 +1961,7 @@ __device__ __forceinline__ void loop_body_baseline(const KParams* P, const Geo& 
     }
     if (warp == 0) {
       double t[8];
-      warp_totals_main(P, par, t, g);
+      warp_totals_main<false>(P, par, t, g);
       if (lane == 0) {
         for (int i = 0; i < 7; ++i) tot[i] = t[i];
         const bool time_up = budget != 0ull && *reinterpret_cast<volatile unsigned*>(&bar->time_up[par]) != 0u;
@@ -2038,7 +2031,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_baseline(con
 // ---------------------------------------------------------------------------
 // RK = false: one GPU, P in the constant bank (loop_kernel).  RK = true: one
 // rank of a row-partitioned team (loop_kernel_team), P in shared memory.
-template <bool RK>
+template <bool RK, bool BOX = false>
 __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
   __shared__ Ctl C;
   __shared__ double tot[kMaxQ];
@@ -2067,7 +2060,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
   // main reduction there
   auto sync_reduce = [&](int pr) -> bool {
     if constexpr (RK) {
-      if (!solo) return team_sync(bar, P->T, g, target, repoch, P->slots, P->T.prereduce ? pr : -1, P->ub != nullptr);
+      if (!solo) return team_sync(bar, P->T, g, target, repoch, P->slots, P->T.prereduce ? pr : -1, BOX);
     }
     return grid_sync(bar, target);
   };
@@ -2168,7 +2161,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
     SpmvHead head;
     if (!spec_done) {
       spmv_head(P->AT, gwarp_id(g), lane, head);
-      phase_primal<RK>(P, R, par, stage, ++seq, head, g);
+      phase_primal_t<RK, BOX>(P, R, par, stage, ++seq, head, g);
       if (writer && threadIdx.x == 0 && budget != 0ull) set_time_up(par, (global_ns() - t_start) > budget ? 1u : 0u);
     }
     mark(0);
@@ -2184,7 +2177,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
     if (warp == 0) {
       unsigned long long cA = clock64(), cB = 0, cC = 0;
       double t[8];
-      if (solo || !P->T.prereduce) warp_totals_main(P, par, t, g);
+      if (solo || !P->T.prereduce) warp_totals_main<BOX>(P, par, t, g);
       else warp_totals_ranks(P, par, t, g.cta);
       // the independent fp64 divides / square roots, one per lane, executed
       // uniformly (operands selected per lane, one sqrt + one divide)
@@ -2220,7 +2213,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
     mark(4);
     // speculative phase A of iteration it+1 (measured: worth ~10% against
     // running phase A after the controller)
-    phase_primal<RK>(P, &SR, par ^ 1, stage, ++seq, head, g);
+    phase_primal_t<RK, BOX>(P, &SR, par ^ 1, stage, ++seq, head, g);
     if (writer && threadIdx.x == 0 && budget != 0ull)
       set_time_up(par ^ 1, (global_ns() - t_start) > budget ? 1u : 0u);
     __syncthreads();
@@ -2316,6 +2309,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
   const Geo g{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x),
               static_cast<int>(gridDim.x)};
   loop_body<false>(&KP, g);
+}
+
+// The box form (hx_set_box) as its own kernel: the standard loop keeps its code.
+__global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_box(const __grid_constant__ KParams KP) {
+  const Geo g{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x),
+              static_cast<int>(gridDim.x)};
+  loop_body<false, true>(&KP, g);
 }
 
 static_assert(sizeof(KParams) % 8 == 0, "KParams copied as 8-byte words");
@@ -2811,7 +2811,8 @@ int launch_loop(hx_ctx* c) {
                                  c->stream));
   const void* kernel = c->h.mode == kModeLoop && c->h.scheme != HPLP_SCHEME_RHPDHG
                            ? reinterpret_cast<const void*>(loop_kernel_baseline)
-                           : reinterpret_cast<const void*>(loop_kernel);
+                           : c->ub ? reinterpret_cast<const void*>(loop_kernel_box)
+                                   : reinterpret_cast<const void*>(loop_kernel);
   HX_CUDA(c, cudaLaunchCooperativeKernel(kernel, dim3(c->grid), dim3(kThreads), args, kStageBytes, c->stream));
   c->launches += 1;
   HX_CUDA(c, cudaMemcpyAsync(&c->h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
@@ -3019,6 +3020,8 @@ int hx_create(int32_t device, hx_ctx** out) {
   HX_CUDA(nullptr, cudaFuncSetAttribute(loop_kernel_team, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(kStageBytes)));
   HX_CUDA(nullptr, cudaFuncSetAttribute(loop_kernel_baseline, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kStageBytes)));
+  HX_CUDA(nullptr, cudaFuncSetAttribute(loop_kernel_box, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(kStageBytes)));
   int occ = 0;
   HX_CUDA(nullptr, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, loop_kernel, kThreads, kStageBytes));
@@ -3459,6 +3462,7 @@ int hx_setup(hx_ctx* c, const hplp_config_t* cfg, double sigma_used, double eta,
     return set_err(c, HPLP_EINVAL, "hx_setup: the baseline schemes run on one device (no team)");
   if (c->ub && cfg->scheme != HPLP_SCHEME_RHPDHG)
     return set_err(c, HPLP_EINVAL, "hx_setup: the box form runs rHPDHG only");
+  if (c->ub && c->ranked) return set_err(c, HPLP_EINVAL, "hx_setup: the box form runs on one device (no team)");
   if (c->ub && cfg->infeasibility_check_period > 0)
     return set_err(c, HPLP_EINVAL, "hx_setup: the box form has no infeasibility scan (set infeasibility_check_period 0)");
   cudaStream_t s = c->stream;
