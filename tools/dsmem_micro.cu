@@ -40,6 +40,30 @@ __global__ void __launch_bounds__(kThreads, 1) gather_global(const double* v, un
   if (acc == 12345.678) out[0] = acc;
 }
 
+// Cache-operator variants of the same random gather (K: 0 .cg, 1
+// L1::no_allocate, 2 .nc (read-only path; only valid for data the kernel
+// never writes), 3 .lu / last use)
+template <int F, int K>
+__global__ void __launch_bounds__(kThreads, 1) gather_op(const double* v, unsigned n, int rounds, double* out) {
+  unsigned s = hash(blockIdx.x * kThreads + threadIdx.x + 1);
+  double acc = 0.0;
+  for (int r = 0; r < rounds; ++r) {
+    double t[F];
+#pragma unroll
+    for (int k = 0; k < F; ++k) {
+      s = hash(s + k);
+      const double* p = v + (s % n);
+      if constexpr (K == 0) t[k] = __ldcg(p);
+      else if constexpr (K == 1) asm volatile("ld.global.L1::no_allocate.f64 %0, [%1];" : "=d"(t[k]) : "l"(p));
+      else if constexpr (K == 2) t[k] = __ldg(p);
+      else t[k] = __ldlu(p);
+    }
+#pragma unroll
+    for (int k = 0; k < F; ++k) acc += t[k];
+  }
+  if (acc == 12345.678) out[0] = acc;
+}
+
 // The same gathers plus the stream tasks' shared-memory traffic: every
 // product stored to a per-warp buffer, then read back lane-per-row (stride
 // `rowlen`, the bank pattern of the row sums).
@@ -126,6 +150,10 @@ int main() {
   run_g(gather_global<8>, 8, "global, 8 in flight / thread");
   run_g(gather_global<16>, 16, "global, 16 in flight / thread");
   run_g(gather_global<32>, 32, "global, 32 in flight / thread");
+  run_g(gather_op<8, 0>, 8, "ld.global.cg, 8 in flight");
+  run_g(gather_op<8, 1>, 8, "ld.global.L1::no_allocate, 8");
+  run_g(gather_op<8, 2>, 8, "ld.global.nc (read-only), 8");
+  run_g(gather_op<8, 3>, 8, "ld.global.lu, 8");
   for (int rowlen : {1, 8, 20}) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(e0);

@@ -18,12 +18,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", type=int, default=1)
 ap.add_argument("--iters", type=int, default=200)
 ap.add_argument("--launches", type=int, default=3)
+ap.add_argument("--box", action="store_true", help="the box form (loop_kernel_box)")
 a = ap.parse_args()
 g = gen.generate(a.cfg)
 s = hplp.to_standard_form(g)
-solver = hplp.Solver.from_std(s)
+solver = hplp.Solver.box(*s.csr()) if a.box else hplp.Solver.from_std(s)
 r0 = solver.solve(iteration_limit=0)
-cfg = abi.Config.default(tolerance=1e-4, iteration_limit=10**9)
+cfg = abi.Config.default(tolerance=1e-4, iteration_limit=10**9, infeasibility_check_period=0 if a.box else 100)
 solver.hx.setup(cfg, r0["sigma_estimate"], r0["eta"])
 for i in range(a.launches):
     t = time.perf_counter()
