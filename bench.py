@@ -429,7 +429,7 @@ def run_gpu(args):
                        f"row-partitioned x{world}: one LP, rows/columns split by nnz, slices pushed over NVLink P2P"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic if world == 1 else None,
-                         "kernel": "hx::loop_kernel" if world == 1 else "hx::loop_kernel_team",
+                         "kernel": hx.loop_kernel() if world == 1 else "hx::loop_kernel_team",
                          "algorithmic_bytes_per_iter": b_iter, "peak_source": peak_kind,
                          "frac_of_8TBs": achieved / (8000.0 * world)},
             # the access-pattern ceiling: every nonzero is one random fp64 gather

@@ -431,13 +431,55 @@ struct TaskRegs {
   double cv[kLoadsPerLane];
 };
 
+// L2 eviction priority for the matrix streams (createpolicy): they are read
+// once per phase, so when the per-iteration working set exceeds what the
+// 126 MB L2 keeps (Sched::stream_hint, set at upload), they are loaded
+// evict_first and without L1 allocation -- the vectors every SM gathers from
+// and the epilogue's pools then stay in L2 between phases.  Measured on
+// configs[1] (tools/quick_rate.py A/B): 25.65k -> 26.79k it/s; the box form's
+// working set fits in L2 and runs faster without the hint (32.3k vs 30.6k).
+__device__ __forceinline__ unsigned long long l2_policy_first() {
+  unsigned long long p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int ldg_stream(const int* p, unsigned long long pol) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ldg_stream(const double* p, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long l2_policy_normal() {
+  unsigned long long p;
+  asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// LM: 0 plain read-only loads, 1 evict_first streams, 2 chosen at run time by
+// S.stream_hint (one load sequence with a selected policy)
+template <int LM>
 __device__ __forceinline__ void load_task(const Sched& S, const int4& tk, int lane, TaskRegs& r) {
   const int p0 = tk.z, len = tk.w - tk.z;
+  if constexpr (LM == 0) {
 #pragma unroll
-  for (int j = 0; j < kLoadsPerLane; ++j) {
-    const int q = j * 32 + lane;
-    r.ci[j] = q < len ? __ldg(S.idx + p0 + q) : 0;
-    r.cv[j] = q < len ? __ldg(S.val + p0 + q) : 0.0;
+    for (int j = 0; j < kLoadsPerLane; ++j) {
+      const int q = j * 32 + lane;
+      r.ci[j] = q < len ? __ldg(S.idx + p0 + q) : 0;
+      r.cv[j] = q < len ? __ldg(S.val + p0 + q) : 0.0;
+    }
+  } else {
+    const unsigned long long pol = LM == 1 || S.stream_hint ? l2_policy_first() : l2_policy_normal();
+#pragma unroll
+    for (int j = 0; j < kLoadsPerLane; ++j) {
+      const int q = j * 32 + lane;
+      r.ci[j] = q < len ? ldg_stream(S.idx + p0 + q, pol) : 0;
+      r.cv[j] = q < len ? ldg_stream(S.val + p0 + q, pol) : 0.0;
+    }
   }
 }
 
@@ -450,16 +492,17 @@ struct SpmvHead {
   TaskRegs cur;
 };
 
+template <int LM = 0>
 __device__ __forceinline__ void spmv_head(const Sched& S, int gwarp, int lane, SpmvHead& h) {
   const int W = S.W;
   const int n = S.n_tasks;
   const int4 kNone{0, 0, 0, 0};
   h.tk = gwarp < n ? __ldg(S.tasks + gwarp) : kNone;
   h.tk1 = gwarp + W < n ? __ldg(S.tasks + gwarp + W) : kNone;
-  load_task(S, h.tk, lane, h.cur);
+  load_task<LM>(S, h.tk, lane, h.cur);
 }
 
-template <int Q, unsigned MaxMask, class Src, class Epi>
+template <int Q, unsigned MaxMask, int LM = 0, class Src, class Epi>
 __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& src, Epi& epi, double (&acc)[Q],
                                           int gwarp, int lane, WarpStage* st, unsigned long long seq,
                                           const SpmvHead& head) {
@@ -476,7 +519,7 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
   for (; t < n; t += W) {
     const int4 tk2 = t + 2 * W < n ? __ldg(S.tasks + t + 2 * W) : kNone;
     TaskRegs nxt;
-    load_task(S, tk1, lane, nxt);
+    load_task<LM>(S, tk1, lane, nxt);
     const int r0 = tk.x, r1 = tk.y & kRowMask, kind = tk.y >> kKindShift;
     const int p0 = tk.z, len = tk.w - tk.z;
     // stream tasks: up to two rows per lane (lane, lane + 32); their bounds and
@@ -569,12 +612,12 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
   }
 }
 
-template <int Q, unsigned MaxMask, class Src, class Epi>
+template <int Q, unsigned MaxMask, int LM = 0, class Src, class Epi>
 __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& src, Epi& epi, double (&acc)[Q],
                                           int gwarp, int lane, WarpStage* st, unsigned long long seq = 1) {
   SpmvHead head;
-  spmv_head(S, gwarp, lane, head);
-  spmv_rows<Q, MaxMask>(S, set, src, epi, acc, gwarp, lane, st, seq, head);
+  spmv_head<LM>(S, gwarp, lane, head);
+  spmv_rows<Q, MaxMask, LM>(S, set, src, epi, acc, gwarp, lane, st, seq, head);
 }
 
 // Owner side of the long-row protocol: warp 0 waits for each owned long row
@@ -612,10 +655,24 @@ __device__ __forceinline__ void fold_long(const Sched& S, int set, unsigned long
 // Kernel-written vectors are gathered through L1 (ld.global.ca would also
 // do): every grid barrier's gpu-scope fence invalidates L1 (CCTL.IVALL), so
 // no stale line survives into the next phase.
-struct SrcVec {
+// Gather source.  LAST: loads ask L2 for evict_last (the stream kernel, whose
+// matrix streams are evict_first): +0.4% on configs[1].
+template <bool LAST = false>
+struct SrcVecT {
   const double* v;
-  __device__ __forceinline__ double operator()(int j) const { return ldca(v + j); }
+  __device__ __forceinline__ double operator()(int j) const {
+    if constexpr (LAST) {
+      unsigned long long pol;
+      asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+      double r;
+      asm volatile("ld.global.ca.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(v + j), "l"(pol));
+      return r;
+    } else {
+      return ldca(v + j);
+    }
+  }
 };
+using SrcVec = SrcVecT<false>;
 struct SrcDiv {  // power iteration: x = z / ||z|| formed on the fly (same rounding)
   const double* v;
   double d;
@@ -1276,7 +1333,7 @@ __device__ __forceinline__ double* region_ptr(const KParams* P, int r, int nrec)
 __device__ __forceinline__ int gwarp_id(const Geo& g) { return g.cta * kWarps + (threadIdx.x >> 5); }
 
 // phase A: A^T y, primal step (+ Halpern formation of x), primal partials
-template <bool RK, bool BOX>
+template <bool RK, bool BOX, int LM = 2>
 __device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R, int par, WarpStage* stage,
                                                unsigned long long seq, const SpmvHead& head, const Geo& g) {
   constexpr int NQ = EpiPrimal<RK, BOX>::NQ;
@@ -1298,8 +1355,8 @@ __device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R,
 #ifdef HX_WPROF
   const unsigned long long w0 = clock64();
 #endif
-  spmv_rows<NQ, 0>(S, par, SrcVec{ycur_ptr(P, R)}, e, acc, gwarp_id(g),
-                   threadIdx.x & 31, stage, seq, head);
+  spmv_rows<NQ, 0, LM>(S, par, SrcVecT<LM == 1>{ycur_ptr(P, R)}, e, acc, gwarp_id(g),
+                       threadIdx.x & 31, stage, seq, head);
 #ifdef HX_WPROF
   if constexpr (!RK)
     if (P->prof && (threadIdx.x & 31) == 0) P->prof[gridDim.x * 16 + gwarp_id(g)] += clock64() - w0;
@@ -1309,7 +1366,7 @@ __device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R,
 }
 
 // phase B: A x+, dual step, speculative Halpern combos, dual partials
-template <bool RK>
+template <bool RK, int LM = 2>
 __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int par, WarpStage* stage,
                                            unsigned long long seq, const SpmvHead& head, const Geo& g) {
   const int n = P->n, m = P->m;
@@ -1333,8 +1390,8 @@ __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int
 #ifdef HX_WPROF
   const unsigned long long w0 = clock64();
 #endif
-  spmv_rows<4, 0>(S, par, SrcVec{P->xpool + static_cast<size_t>(R->xp_out) * n}, e, acc, gwarp_id(g),
-                  threadIdx.x & 31, stage, seq, head);
+  spmv_rows<4, 0, LM>(S, par, SrcVecT<LM == 1>{P->xpool + static_cast<size_t>(R->xp_out) * n}, e, acc, gwarp_id(g),
+                      threadIdx.x & 31, stage, seq, head);
 #ifdef HX_WPROF
   if constexpr (!RK)
     if (P->prof && (threadIdx.x & 31) == 0) P->prof[gridDim.x * (16 + kWarps) + gwarp_id(g)] += clock64() - w0;
@@ -1395,24 +1452,27 @@ __device__ __forceinline__ void warp_totals_ranks(const KParams* P, int par, dou
 // power iteration halves: w = A x (x = x0 or z / zn), z = A^T w
 // (single-rank only: a team computes sigma redundantly on every rank, each
 // with its full-matrix schedules -- deterministic and identical, no exchange)
+template <int LM = 0>
 __device__ HX_PHASE_INLINE void power_a(const KParams* P, const Roles* R, WarpStage* stage, unsigned long long seq,
                                         const Geo& g) {
   double acc[1];
   acc_init<1, 0>(acc);
   EpiStoreSq e{P->ypool};
   const Sched S = P->A;
-  if (R->pw_mode == 0) spmv_rows<1, 0>(S, 0, SrcVec{P->xpool}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
-  else spmv_rows<1, 0>(S, 0, SrcDiv{P->xpool + P->n, R->pw_zn}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
+  if (R->pw_mode == 0) spmv_rows<1, 0, LM>(S, 0, SrcVec{P->xpool}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
+  else
+    spmv_rows<1, 0, LM>(S, 0, SrcDiv{P->xpool + P->n, R->pw_zn}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
   fold_long<1, 0>(S, 0, seq, acc, g.cta);
   block_to_slots<1, 0, false>(acc, P, kRegPA, g);
 }
 
+template <int LM = 0>
 __device__ HX_PHASE_INLINE void power_b(const KParams* P, WarpStage* stage, unsigned long long seq, const Geo& g) {
   double acc[1];
   acc_init<1, 0>(acc);
   EpiStoreSq e{P->xpool + P->n};
   const Sched S = P->AT;
-  spmv_rows<1, 0>(S, 0, SrcVec{P->ypool}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
+  spmv_rows<1, 0, LM>(S, 0, SrcVec{P->ypool}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
   fold_long<1, 0>(S, 0, seq, acc, g.cta);
   block_to_slots<1, 0, false>(acc, P, kRegPB, g);
 }
@@ -1534,7 +1594,7 @@ __device__ HX_PHASE_INLINE void cert_units(const KParams* P, const Roles* R, con
 }
 
 // certificate scan C3: the validation SpMVs, up to four independent products
-template <bool RK>
+template <bool RK, int LM = 0>
 __device__ HX_PHASE_INLINE void cert_products(const KParams* P, const Roles* R, WarpStage* stage,
                                               unsigned long long seq, const Geo& g) {
   const int n = P->n, m = P->m;
@@ -1552,7 +1612,7 @@ __device__ HX_PHASE_INLINE void cert_products(const KParams* P, const Roles* R, 
       double a2[2];
       acc_init<2, 3u>(a2);
       EpiPosNeg e;
-      spmv_rows<2, 3u>(AT, 2 + k, SrcVec{k ? u3 : u1}, e, a2, gw, lane, stage, seq);
+      spmv_rows<2, 3u, LM>(AT, 2 + k, SrcVec{k ? u3 : u1}, e, a2, gw, lane, stage, seq);
       fold_long<2, 3u>(AT, 2 + k, seq, a2, g.cta);
       acc[2 * k] = a2[0], acc[2 * k + 1] = a2[1];
     }
@@ -1560,7 +1620,7 @@ __device__ HX_PHASE_INLINE void cert_products(const KParams* P, const Roles* R, 
       double a1[1];
       acc_init<1, 1u>(a1);
       EpiAbs e;
-      spmv_rows<1, 1u>(A, 2 + k, SrcVec{k ? u2 : u0}, e, a1, gw, lane, stage, seq);
+      spmv_rows<1, 1u, LM>(A, 2 + k, SrcVec{k ? u2 : u0}, e, a1, gw, lane, stage, seq);
       fold_long<1, 1u>(A, 2 + k, seq, a1, g.cta);
       acc[4 + k] = a1[0];
     }
@@ -2031,7 +2091,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_baseline(con
 // ---------------------------------------------------------------------------
 // RK = false: one GPU, P in the constant bank (loop_kernel).  RK = true: one
 // rank of a row-partitioned team (loop_kernel_team), P in shared memory.
-template <bool RK, bool BOX = false>
+template <bool RK, bool BOX = false, int LM = 2>
 __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
   __shared__ Ctl C;
   __shared__ double tot[kMaxQ];
@@ -2081,7 +2141,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
   if (!RK && C.mode == kModePower) {
     // power_iteration loop body, src/sparse_matrix.cpp:153-177
     while (!R->stop) {
-      power_a(P, R, stage, ++seq, g);
+      power_a<LM>(P, R, stage, ++seq, g);
       if (!sync()) return;
       {
         const double* rg = region_ptr(P, kRegPA, g.nrec);
@@ -2098,7 +2158,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
       }
       __syncthreads();
       if (R->stop) break;
-      power_b(P, stage, ++seq, g);
+      power_b<LM>(P, stage, ++seq, g);
       if (!sync()) return;
       {
         const double* rg = region_ptr(P, kRegPB, g.nrec);
@@ -2160,18 +2220,18 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
     const int par = static_cast<int>(C.it & 1);
     SpmvHead head;
     if (!spec_done) {
-      spmv_head(P->AT, gwarp_id(g), lane, head);
-      phase_primal_t<RK, BOX>(P, R, par, stage, ++seq, head, g);
+      spmv_head<LM>(P->AT, gwarp_id(g), lane, head);
+      phase_primal_t<RK, BOX, LM>(P, R, par, stage, ++seq, head, g);
       if (writer && threadIdx.x == 0 && budget != 0ull) set_time_up(par, (global_ns() - t_start) > budget ? 1u : 0u);
     }
     mark(0);
-    spmv_head(P->A, gwarp_id(g), lane, head);
+    spmv_head<LM>(P->A, gwarp_id(g), lane, head);
     if (!sync()) return;
     mark(1);
-    phase_dual<RK>(P, R, par, stage, ++seq, head, g);
+    phase_dual<RK, LM>(P, R, par, stage, ++seq, head, g);
     if (threadIdx.x == 0) make_spec(C, SR);
     mark(2);
-    spmv_head(P->AT, gwarp_id(g), lane, head);
+    spmv_head<LM>(P->AT, gwarp_id(g), lane, head);
     if (!sync_reduce(par)) return;
     mark(3);
     if (warp == 0) {
@@ -2213,7 +2273,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
     mark(4);
     // speculative phase A of iteration it+1 (measured: worth ~10% against
     // running phase A after the controller)
-    phase_primal_t<RK, BOX>(P, &SR, par ^ 1, stage, ++seq, head, g);
+    phase_primal_t<RK, BOX, LM>(P, &SR, par ^ 1, stage, ++seq, head, g);
     if (writer && threadIdx.x == 0 && budget != 0ull)
       set_time_up(par ^ 1, (global_ns() - t_start) > budget ? 1u : 0u);
     __syncthreads();
@@ -2254,7 +2314,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
           C.cinf[3] = tot[10], C.cdot[3] = tot[11];
         }
         __syncthreads();
-        cert_products<RK>(P, R, stage, ++seq, g);
+        cert_products<RK, LM>(P, R, stage, ++seq, g);
         if (!sync()) return;
         {
           const double* rg = region_ptr(P, kRegC3, g.nrec);
@@ -2308,14 +2368,22 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
   // constant bank; no local copy (grid_constant)
   const Geo g{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x),
               static_cast<int>(gridDim.x)};
-  loop_body<false>(&KP, g);
+  loop_body<false, false, 0>(&KP, g);
+}
+
+// The same loop with the matrix streams loaded evict_first (working set
+// beyond L2: Sched::stream_hint).
+__global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_stream(const __grid_constant__ KParams KP) {
+  const Geo g{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x),
+              static_cast<int>(gridDim.x)};
+  loop_body<false, false, 1>(&KP, g);
 }
 
 // The box form (hx_set_box) as its own kernel: the standard loop keeps its code.
 __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_box(const __grid_constant__ KParams KP) {
   const Geo g{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x),
               static_cast<int>(gridDim.x)};
-  loop_body<false, true>(&KP, g);
+  loop_body<false, true, 0>(&KP, g);
 }
 
 static_assert(sizeof(KParams) % 8 == 0, "KParams copied as 8-byte words");
@@ -2338,7 +2406,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_team(const _
   const KParams* P = &L.p[group];
   const int cta = blockIdx.x % L.grp_ctas;
   const Geo g{cta, L.grp_ctas, P->T.rank * L.grp_ctas + cta, P->T.nranks * L.grp_ctas};
-  loop_body<true>(P, g);
+  loop_body<true, false, 2>(P, g);
 }
 
 // ---------------------------------------------------------------------------
@@ -2811,8 +2879,9 @@ int launch_loop(hx_ctx* c) {
                                  c->stream));
   const void* kernel = c->h.mode == kModeLoop && c->h.scheme != HPLP_SCHEME_RHPDHG
                            ? reinterpret_cast<const void*>(loop_kernel_baseline)
-                           : c->ub ? reinterpret_cast<const void*>(loop_kernel_box)
-                                   : reinterpret_cast<const void*>(loop_kernel);
+                           : c->ub                     ? reinterpret_cast<const void*>(loop_kernel_box)
+                           : c->sa.view.stream_hint    ? reinterpret_cast<const void*>(loop_kernel_stream)
+                                                       : reinterpret_cast<const void*>(loop_kernel);
   HX_CUDA(c, cudaLaunchCooperativeKernel(kernel, dim3(c->grid), dim3(kThreads), args, kStageBytes, c->stream));
   c->launches += 1;
   HX_CUDA(c, cudaMemcpyAsync(&c->h, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->stream));
@@ -3022,6 +3091,8 @@ int hx_create(int32_t device, hx_ctx** out) {
   HX_CUDA(nullptr, cudaFuncSetAttribute(loop_kernel_baseline, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(kStageBytes)));
   HX_CUDA(nullptr, cudaFuncSetAttribute(loop_kernel_box, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kStageBytes)));
+  HX_CUDA(nullptr, cudaFuncSetAttribute(loop_kernel_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(kStageBytes)));
   int occ = 0;
   HX_CUDA(nullptr, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, loop_kernel, kThreads, kStageBytes));
@@ -3250,6 +3321,27 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
       T.yneed = c->yneed;
     }
   }
+  {
+    // per-iteration working set of the loop: the matrix copies this context
+    // streams (a rank: its blocks) plus the ~6 n- and ~10 m-vectors an
+    // iteration touches; beyond ~70% of L2 the matrix streams get evict_first
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device);
+    int64_t streamed = 2 * nnz;
+    if (c->ranked) {
+      const Team& T = c->team;
+      streamed = row_ptr[T.row1] - row_ptr[T.row0];
+      int tp0 = 0, tp1 = 0;
+      cudaMemcpy(&tp0, c->t_ptr + T.col0, sizeof(int), cudaMemcpyDeviceToHost);
+      cudaMemcpy(&tp1, c->t_ptr + T.col1, sizeof(int), cudaMemcpyDeviceToHost);
+      streamed += tp1 - tp0;
+    }
+    const double footprint = 12.0 * static_cast<double>(streamed) + 8.0 * (6.0 * n + 10.0 * m);
+    int hint = footprint > 0.7 * static_cast<double>(l2) ? 1 : 0;
+    if (const char* e = std::getenv("HPLP_L2_STREAM")) hint = std::atoi(e) != 0 ? 1 : 0;
+    c->sa.view.stream_hint = c->st.view.stream_hint = hint;
+    c->pa.view.stream_hint = c->pt.view.stream_hint = hint;
+  }
   tick("schedules");
   if (c->ranked) {  // peers map these through CUDA IPC
     HX_CUDA(c, dalloc_ipc(&c->xpool, static_cast<size_t>(kXPool) * n));
@@ -3356,6 +3448,11 @@ int hx_precondition(hx_ctx* c, int32_t ruiz_iters, double pc_alpha, double* row_
 // Box form: column upper bounds enforced by the primal
 // projection, x in [0, u] (u = +inf: no bound); NULL returns to the standard
 // form.  Set after hx_upload_csr and before hx_precondition / hx_setup.
+int32_t hx_loop_variant(hx_ctx* c) {
+  if (!c || !c->uploaded) return -1;
+  return c->ub ? 2 : c->sa.view.stream_hint ? 1 : 0;
+}
+
 int hx_set_box(hx_ctx* c, const double* upper) {
   if (!c->uploaded) return set_err(c, HPLP_ESTATE, "hx_set_box: no problem uploaded");
   HX_CUDA(c, cudaSetDevice(c->device));

@@ -72,6 +72,7 @@ struct Sched {
   const int4* meta = nullptr;      // piece tasks: {slot, npieces, counter, index}
   int n_tasks = 0;
   int n_long = 0;
+  int stream_hint = 0;             // 1: idx/val loaded evict_first (working set > L2; hx_upload_csr)
   // Long-row scratch per "set" (base + set * stride; no dynamically indexed
   // arrays, which would force the kernel parameters into local memory):
   // sets 0/1 alternate by iteration parity in the main phases, sets 2/3

@@ -100,6 +100,7 @@ def lib() -> C.CDLL:
     sig("hx_launch_count", I64, V)
     sig("hx_upload_csr", C.c_int, V, I64, I64, PI64, PI32, PD, PD, PD)
     sig("hx_dims", C.c_int, V, PI64, PI64, PI64)
+    sig("hx_loop_variant", I32, V)
     sig("hx_spmv", C.c_int, V, PD, PD)
     sig("hx_spmv_transpose", C.c_int, V, PD, PD)
     sig("hx_power_iteration", C.c_int, V, PD, D, I64, I64, D, PD, PI64, PI32, PI32)
@@ -423,6 +424,13 @@ class HX:
         sm, g, t = C.c_int32(), C.c_int32(), C.c_int32()
         lib().hx_device_info(self.h, C.byref(sm), C.byref(g), C.byref(t))
         return dict(sm_count=sm.value, grid=g.value, threads=t.value)
+
+    LOOP_KERNELS = ("hx::loop_kernel", "hx::loop_kernel_stream", "hx::loop_kernel_box")
+
+    def loop_kernel(self) -> str:
+        """Name of the loop kernel hx_run launches for this problem."""
+        v = lib().hx_loop_variant(self.h)
+        return self.LOOP_KERNELS[v] if v >= 0 else ""
 
     def stream(self) -> int:
         return lib().hx_stream(self.h) or 0

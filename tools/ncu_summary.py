@@ -25,7 +25,7 @@ its = 100
 scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
 rd = float(d["dram__bytes_read.sum"]["value"]) * scale[d["dram__bytes_read.sum"]["unit"]] / its
 wr = float(d["dram__bytes_write.sum"]["value"]) * scale[d["dram__bytes_write.sum"]["unit"]] / its
-out = {"source": f"ncu --set full --clock-control none --import-source on, 1 launch of hx::loop_kernel = {its} rHPDHG "
+out = {"source": f"ncu --set full --clock-control none --import-source on, 1 launch of hx::loop_kernel_stream = {its} rHPDHG "
                  f"iterations on configs[1] (tools/profile_loop.py --iters 100 --launches 2; -k regex:loop_kernel -s 2 "
                  f"-c 1); {label}",
        "dram_bytes_read_per_iter": rd, "dram_bytes_write_per_iter": wr, "dram_bytes_per_iter": rd + wr,
