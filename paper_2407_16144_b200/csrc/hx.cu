@@ -53,6 +53,25 @@
 
 #include "hx_internal.cuh"
 
+// HX_CHECKED builds (tools/variant.sh checked -DHX_CHECKED): device-side
+// bounds checks on the SpMV engine's indices; a violation prints and traps.
+// compute-sanitizer is unavailable on the GPU pool, so this is the
+// out-of-bounds check the GPU test suite runs against.
+#ifdef HX_CHECKED
+#define HX_CHECK(cond, what, a, b)                                                                      \
+  do {                                                                                                  \
+    if (!(cond)) {                                                                                      \
+      printf("HX_CHECK failed: %s (%lld, %lld) at %s:%d\n", what, (long long)(a), (long long)(b), __FILE__, \
+             __LINE__);                                                                                 \
+      __trap();                                                                                         \
+    }                                                                                                   \
+  } while (0)
+#else
+#define HX_CHECK(cond, what, a, b) \
+  do {                             \
+  } while (0)
+#endif
+
 namespace hx {
 
 enum Mode : int { kModeLoop = 0, kModePower = 1 };
@@ -465,6 +484,7 @@ __device__ __forceinline__ unsigned long long l2_policy_normal() {
 template <int LM>
 __device__ __forceinline__ void load_task(const Sched& S, const int4& tk, int lane, TaskRegs& r) {
   const int p0 = tk.z, len = tk.w - tk.z;
+  HX_CHECK(len >= 0 && len <= kChunk && p0 >= 0, "task nnz range", p0, len);
   if constexpr (LM == 0) {
 #pragma unroll
     for (int j = 0; j < kLoadsPerLane; ++j) {
@@ -522,6 +542,7 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
     load_task<LM>(S, tk1, lane, nxt);
     const int r0 = tk.x, r1 = tk.y & kRowMask, kind = tk.y >> kKindShift;
     const int p0 = tk.z, len = tk.w - tk.z;
+    HX_CHECK(r0 >= 0 && r1 >= r0 && r1 <= S.row_limit, "task rows", r0, r1);
     // stream tasks: up to two rows per lane (lane, lane + 32); their bounds and
     // epilogue inputs are loaded before the gathers so the latencies overlap
     const int nrows = r1 - r0;
@@ -532,16 +553,19 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
     if (has_row) {
       ra = __ldg(S.ptr + r0 + lane);
       rb = __ldg(S.ptr + r0 + lane + 1);
+      HX_CHECK(ra >= p0 && rb >= ra && rb - p0 <= kChunk, "stream row in task", ra - p0, rb - p0);
       in = epi.load(r0 + lane);
     }
     if (has_row2) {
       ra2 = __ldg(S.ptr + r0 + lane + 32);
       rb2 = __ldg(S.ptr + r0 + lane + 33);
+      HX_CHECK(ra2 >= p0 && rb2 >= ra2 && rb2 - p0 <= kChunk, "stream row 2 in task", ra2 - p0, rb2 - p0);
       in2 = epi.load(r0 + lane + 32);
     }
 #pragma unroll
     for (int j = 0; j < kLoadsPerLane; ++j) {
       const int q = j * 32 + lane;
+      HX_CHECK(q >= len || (cur.ci[j] >= 0 && cur.ci[j] < S.cols), "gather index", cur.ci[j], S.cols);
       if (q < len) cur.cv[j] = cur.cv[j] * src(cur.ci[j]);
     }
     if (kind == kTaskStream) {
@@ -580,6 +604,8 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
       s = warp_sum(s);
       if (lane == 0) {
         const int4 meta = __ldg(S.meta + t);  // {slot, npieces, counter, index}
+        HX_CHECK(meta.x >= 0 && meta.x < S.n_slots + (meta.y == 1 ? 1 : 0) && meta.z < S.n_long, "piece slot", meta.x,
+                 meta.z);
         if (meta.y == 1) {
           double tm[Q];
           epi.apply(r0, s, epi.load(r0), tm);
@@ -3340,6 +3366,8 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     int hint = footprint > 0.7 * static_cast<double>(l2) ? 1 : 0;
     if (const char* e = std::getenv("HPLP_L2_STREAM")) hint = std::atoi(e) != 0 ? 1 : 0;
     c->sa.view.stream_hint = c->st.view.stream_hint = hint;
+    c->sa.view.row_limit = c->pa.view.row_limit = static_cast<int>(m);  // output dimension (HX_CHECKED)
+    c->st.view.row_limit = c->pt.view.row_limit = static_cast<int>(n);
     c->pa.view.stream_hint = c->pt.view.stream_hint = hint;
   }
   tick("schedules");

@@ -73,6 +73,7 @@ struct Sched {
   int n_tasks = 0;
   int n_long = 0;
   int stream_hint = 0;             // 1: idx/val loaded evict_first (working set > L2; hx_upload_csr)
+  int row_limit = 0;               // dimension of the output vector (bounds checks in HX_CHECKED builds)
   // Long-row scratch per "set" (base + set * stride; no dynamically indexed
   // arrays, which would force the kernel parameters into local memory):
   // sets 0/1 alternate by iteration parity in the main phases, sets 2/3
