@@ -428,8 +428,8 @@ def run_gpu(args):
                        "parallelism": "single GPU" if world == 1 else
                        f"row-partitioned x{world}: one LP, rows/columns split by nnz, slices pushed over NVLink P2P"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic if world == 1 else None,
-                         "kernel": hx.loop_kernel() if world == 1 else "hx::loop_kernel_team",
+                         "frac": achieved / peak, "traffic": None if sharded else traffic,
+                         "kernel": "hx::loop_kernel_team" if sharded else hx.loop_kernel(),
                          "algorithmic_bytes_per_iter": b_iter, "peak_source": peak_kind,
                          "frac_of_8TBs": achieved / (8000.0 * world)},
             # the access-pattern ceiling: every nonzero is one random fp64 gather
@@ -445,8 +445,8 @@ def run_gpu(args):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "iters_per_step": E2E_ITERS,
-                    "path": "hplp_solve_csr (C ABI): upload + A^T build + power iteration + loop + download"
-                    if world == 1 else "hplp_solver_create_rank + IPC join + hplp_solver_solve per rank"},
+                    "path": "hplp_solver_create_rank + IPC join + hplp_solver_solve per rank" if sharded
+                    else "hplp_solve_csr (C ABI): upload + A^T build + power iteration + loop + download"},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "time_to_1e-4": ttt,
