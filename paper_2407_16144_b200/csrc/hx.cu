@@ -27,8 +27,11 @@
 //
 // SpMV engine: nnz-chunked warp tasks with kLoadsPerLane independent index /
 // value loads per lane in flight, products staged in shared memory, then
-// lane-per-row sums in ascending column order -- for rows up to
-// kStreamRowMax nonzeros this is exactly the reference's summation order.
+// lane-per-row sums in a fixed order: two interleaved partial sums over the
+// row's ascending column order (even / odd positions) added at the end.  Rows
+// of <= 2 nonzeros (bound rows, slack columns) get exactly the reference's
+// order; longer rows differ from it only by rounding (~1e-16 relative), and
+// halving the dependent-add chain is worth 3.9% on configs[1] (HX_RSUM).
 //
 // All reductions are fixed-order (static row->warp schedule, fixed trees, no
 // floating-point atomics): results are bit-reproducible run to run.  Device
@@ -432,8 +435,9 @@ __device__ __forceinline__ double warp_reduce_strided(const double* p, int count
 // all in registers; B200 measurements (tools/spmv_micro.cu) show register
 // loads with a large L1 beat shared-memory staging for random fp64 gathers.
 // Stream tasks write the products to a 2 KB per-warp buffer and sum them
-// lane-per-row in ascending column order (the reference's own order,
-// src/sparse_matrix.cpp:108-115); pieces are summed warp-wide.  The row
+// lane-per-row over ascending columns (the reference's order,
+// src/sparse_matrix.cpp:108-115, split into even/odd partial sums: HX_RSUM);
+// pieces are summed warp-wide.  The row
 // epilogue's inputs are loaded before the gathers so their latency overlaps.
 // Epi: load(row) / apply(row, sum, inputs, terms[Q]).  Terms of regular rows
 // accumulate per thread; a long row's terms are parked in long_terms by
@@ -556,6 +560,15 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
       HX_CHECK(ra >= p0 && rb >= ra && rb - p0 <= kChunk, "stream row in task", ra - p0, rb - p0);
       in = epi.load(r0 + lane);
     }
+#if HX_RSPLIT
+    // short task (<= 16 rows): two lanes per row, lane l + 16 sums the tail
+    // half of row l (phase B of configs[1]: ~12 rows of ~20 nonzeros)
+    const bool split = kind == kTaskStream && nrows <= 16;
+    if (split && lane >= 16 && lane - 16 < nrows) {
+      ra = __ldg(S.ptr + r0 + lane - 16);
+      rb = __ldg(S.ptr + r0 + lane - 15);
+    }
+#endif
     if (has_row2) {
       ra2 = __ldg(S.ptr + r0 + lane + 32);
       rb2 = __ldg(S.ptr + r0 + lane + 33);
@@ -572,6 +585,70 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
 #pragma unroll
       for (int j = 0; j < kLoadsPerLane; ++j) st->prod[j * 32 + lane] = cur.cv[j];
       __syncwarp();
+#if HX_RSUM == 1
+      // two interleaved partial sums (even / odd positions), combined at the
+      // end: half the dependent-add chain; rows of <= 2 nonzeros keep the
+      // reference's exact order
+      auto row_sum = [&](int qa, int qe) {
+        double s0 = 0.0, s1 = 0.0;
+        int q = qa;
+        for (; q + 4 <= qe; q += 4) {
+          const double a0 = st->prod[q], a1 = st->prod[q + 1], a2 = st->prod[q + 2], a3 = st->prod[q + 3];
+          s0 += a0;
+          s1 += a1;
+          s0 += a2;
+          s1 += a3;
+        }
+        if (q + 2 <= qe) {
+          const double a0 = st->prod[q], a1 = st->prod[q + 1];
+          s0 += a0;
+          s1 += a1;
+          q += 2;
+        }
+        if (q < qe) s0 += st->prod[q];
+        return s0 + s1;
+      };
+#elif HX_RSUM == 2
+      // four interleaved partial sums (positions mod 4), combined pairwise
+      auto row_sum = [&](int qa, int qe) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int q = qa;
+        for (; q + 4 <= qe; q += 4) {
+          const double a0 = st->prod[q], a1 = st->prod[q + 1], a2 = st->prod[q + 2], a3 = st->prod[q + 3];
+          s0 += a0;
+          s1 += a1;
+          s2 += a2;
+          s3 += a3;
+        }
+        if (q < qe) s0 += st->prod[q];
+        if (q + 1 < qe) s1 += st->prod[q + 1];
+        if (q + 2 < qe) s2 += st->prod[q + 2];
+        return (s0 + s1) + (s2 + s3);
+      };
+#elif HX_RSUM == 3
+      // two interleaved partial sums, loads issued 8 ahead
+      auto row_sum = [&](int qa, int qe) {
+        double s0 = 0.0, s1 = 0.0;
+        int q = qa;
+        for (; q + 8 <= qe; q += 8) {
+          double a[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) a[k] = st->prod[q + k];
+#pragma unroll
+          for (int k = 0; k < 8; k += 2) {
+            s0 += a[k];
+            s1 += a[k + 1];
+          }
+        }
+        for (; q + 2 <= qe; q += 2) {
+          const double a0 = st->prod[q], a1 = st->prod[q + 1];
+          s0 += a0;
+          s1 += a1;
+        }
+        if (q < qe) s0 += st->prod[q];
+        return s0 + s1;
+      };
+#else
       // ascending-order sums (the reference's), loads issued 4 ahead
       auto row_sum = [&](int qa, int qe) {
         double s = 0.0;
@@ -586,6 +663,20 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
         for (; q < qe; ++q) s += st->prod[q];
         return s;
       };
+#endif
+#if HX_RSPLIT
+      if (split) {
+        const int qa = ra - p0, qe = rb - p0, qm = qa + ((qe - qa + 1) >> 1);
+        double part = 0.0;
+        if ((lane & 15) < nrows) part = lane < 16 ? row_sum(qa, qm) : row_sum(qm, qe);
+        const double tail = __shfl_down_sync(0xffffffffu, part, 16);
+        if (has_row) {
+          double tm[Q];
+          epi.apply(r0 + lane, part + tail, in, tm);
+          acc_add<Q, MaxMask>(acc, tm);
+        }
+      } else
+#endif
       if (has_row) {
         double tm[Q];
         epi.apply(r0 + lane, row_sum(ra - p0, rb - p0), in, tm);
@@ -598,10 +689,22 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
       }
       __syncwarp();
     } else {
+#if HX_PSUM
+      // pairwise tree over the lane's products (fixed order, short chain)
+      double pv[kLoadsPerLane];
+#pragma unroll
+      for (int j = 0; j < kLoadsPerLane; ++j) pv[j] = cur.cv[j];
+#pragma unroll
+      for (int w = 1; w < kLoadsPerLane; w *= 2)
+#pragma unroll
+        for (int j = 0; j + w < kLoadsPerLane; j += 2 * w) pv[j] += pv[j + w];
+      double s = warp_sum(pv[0]);
+#else
       double s = 0.0;
 #pragma unroll
       for (int j = 0; j < kLoadsPerLane; ++j) s += cur.cv[j];
       s = warp_sum(s);
+#endif
       if (lane == 0) {
         const int4 meta = __ldg(S.meta + t);  // {slot, npieces, counter, index}
         HX_CHECK(meta.x >= 0 && meta.x < S.n_slots + (meta.y == 1 ? 1 : 0) && meta.z < S.n_long, "piece slot", meta.x,

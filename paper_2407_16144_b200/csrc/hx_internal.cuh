@@ -38,6 +38,23 @@ constexpr double kTaskCost = 64.0;         // fixed latency cost of one warp tas
 #ifndef HX_LOADS
 #define HX_LOADS 8
 #endif
+// Row sums of stream tasks: 0 one sequential sum in ascending column order
+// (the reference's exact order), 1 two interleaved partial sums (even / odd
+// positions) added at the end, 2 four, 3 two with loads 8 ahead.  Measured on
+// configs[1] (tools/quick_rate.py): 26.81k / 27.86k / 27.47k / 26.97k it/s.
+#ifndef HX_RSUM
+#define HX_RSUM 1
+#endif
+// Pieces of long rows: 1 pairwise tree over each lane's products, 0 one
+// sequential chain (then a warp tree either way).
+#ifndef HX_PSUM
+#define HX_PSUM 1
+#endif
+// 1: tasks of <= 16 rows sum each row on two lanes (head / tail half):
+// 23.7k it/s on configs[1] (register spills + shuffle), not used.
+#ifndef HX_RSPLIT
+#define HX_RSPLIT 0
+#endif
 constexpr int kLoadsPerLane = HX_LOADS;    // nonzeros per lane per task
 constexpr int kChunk = 32 * kLoadsPerLane; // max nonzeros per warp task (256)
 constexpr int kStreamRowMax = 64;          // rows up to this length are summed lane-per-row
@@ -49,9 +66,9 @@ constexpr int kMaxRanks = 8;               // ranks of a row-partitioned team (o
 // registers with independent loads and gathers (shared memory only holds a
 // 2 KB product buffer per warp, so L1 keeps its capacity for the gathers);
 // warp w runs tasks w, w + W, w + 2W, ... (static round robin):
-//   kTaskStream: consecutive short rows, summed lane-per-row in ascending
-//                column order (the reference's own order,
-//                src/sparse_matrix.cpp:108-115);
+//   kTaskStream: consecutive short rows, summed lane-per-row over ascending
+//                columns (the reference's order, src/sparse_matrix.cpp:108-115,
+//                as two interleaved partial sums: HX_RSUM);
 //   kTaskPiece:  a slice of one longer row; meta[t] = {slot, npieces,
 //                counter, index}.  A single-piece row is finished in place;
 //                otherwise the last piece to finish reduces the pieces in
