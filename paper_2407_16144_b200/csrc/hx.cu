@@ -483,6 +483,28 @@ __device__ __forceinline__ unsigned long long l2_policy_normal() {
   return p;
 }
 
+// Epilogue streams of the stream kernel (EF, HX_EPI_EF): 1 loads evict_first,
+// 2 loads and stores evict_first -- for working sets far beyond L2, where the
+// gather targets should own the cache.
+template <int EF>
+__device__ __forceinline__ double ld_epi(const double* p) {
+  if constexpr (EF >= 1) {
+    double v;
+    asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_policy_first()));
+    return v;
+  } else {
+    return ldcg(p);
+  }
+}
+template <int EF>
+__device__ __forceinline__ void st_epi(double* p, double v) {
+  if constexpr (EF >= 2) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(l2_policy_first()) : "memory");
+  } else {
+    *p = v;
+  }
+}
+
 // LM: 0 plain read-only loads, 1 evict_first streams, 2 chosen at run time by
 // S.stream_hint (one load sequence with a selected policy)
 template <int LM>
@@ -540,11 +562,12 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
   int4 tk = head.tk;
   int4 tk1 = head.tk1;
   TaskRegs cur = head.cur;
+  double run_acc = 0.0;  // partial sum of the current run of long-row pieces
   for (; t < n; t += W) {
     const int4 tk2 = t + 2 * W < n ? __ldg(S.tasks + t + 2 * W) : kNone;
     TaskRegs nxt;
     load_task<LM>(S, tk1, lane, nxt);
-    const int r0 = tk.x, r1 = tk.y & kRowMask, kind = tk.y >> kKindShift;
+    const int r0 = tk.x, r1 = tk.y & kRowMask, kind = task_kind(tk.y);
     const int p0 = tk.z, len = tk.w - tk.z;
     HX_CHECK(r0 >= 0 && r1 >= r0 && r1 <= S.row_limit, "task rows", r0, r1);
     // stream tasks: up to two rows per lane (lane, lane + 32); their bounds and
@@ -705,8 +728,15 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
       for (int j = 0; j < kLoadsPerLane; ++j) s += cur.cv[j];
       s = warp_sum(s);
 #endif
-      if (lane == 0) {
-        const int4 meta = __ldg(S.meta + t);  // {slot, npieces, counter, index}
+      // a run's pieces: the partial stays in registers until its last piece
+      if (kind == kTaskPieceRun) {
+        run_acc += s;
+      } else {
+        s = run_acc + s;
+        run_acc = 0.0;
+      }
+      if (lane == 0 && kind == kTaskPiece) {
+        const int4 meta = __ldg(S.meta + t);  // {slot, nruns, counter, run index}
         HX_CHECK(meta.x >= 0 && meta.x < S.n_slots + (meta.y == 1 ? 1 : 0) && meta.z < S.n_long, "piece slot", meta.x,
                  meta.z);
         if (meta.y == 1) {
@@ -826,7 +856,7 @@ __device__ __forceinline__ void push_peers(const Team* T, double* const* base, s
 // [0, u], the dual residual counts only columns without a finite bound, and a
 // fourth partial carries u_j [-(c + A^T y)_j]^+ (the bound part of the dual
 // objective).
-template <bool RK, bool BOX = false>
+template <bool RK, bool BOX = false, int EF = 0>
 struct EpiPrimal {  // phase A, rows of A^T
   static constexpr int NQ = BOX ? 4 : 3;
   const double* xs;
@@ -843,7 +873,8 @@ struct EpiPrimal {  // phase A, rows of A^T
     double xs, xa, c, u;
   };
   __device__ __forceinline__ In load(int j) const {
-    return In{ldcg(xs + j), mode ? ldcg(xa + j) : 0.0, __ldg(c + j), BOX ? __ldg(ub + j) : 0.0};
+    return In{ld_epi<EF>(xs + j), mode ? ld_epi<EF>(xa + j) : 0.0, EF ? ld_epi<EF>(c + j) : __ldg(c + j),
+              BOX ? __ldg(ub + j) : 0.0};
   }
   __device__ __forceinline__ void apply(int j, double aty, const In& in, double (&t)[NQ]) const {
     double x;
@@ -853,7 +884,7 @@ struct EpiPrimal {  // phase A, rows of A^T
     } else {
       x = in.xs;
     }
-    zx[j] = x;
+    st_epi<EF>(zx + j, x);
     const double cj = in.c;
     double xn = x - eta * (aty + cj);
     xn = xn < 0.0 ? 0.0 : xn;
@@ -876,7 +907,7 @@ struct EpiPrimal {  // phase A, rows of A^T
   }
 };
 
-template <bool RK>
+template <bool RK, int EF = 0>
 struct EpiDual {  // phase B, rows of A
   const double* y;
   const double* ax;
@@ -894,15 +925,16 @@ struct EpiDual {  // phase B, rows of A
     double y, ax, b, ya, axa;
   };
   __device__ __forceinline__ In load(int i) const {
-    return In{ldcg(y + i), ldcg(ax + i), __ldg(b + i), ldcg(ya + i), ldcg(axa + i)};
+    return In{ld_epi<EF>(y + i), ld_epi<EF>(ax + i), EF ? ld_epi<EF>(b + i) : __ldg(b + i), ld_epi<EF>(ya + i),
+              ld_epi<EF>(axa + i)};
   }
   __device__ __forceinline__ void apply(int i, double s, const In& in, double (&t)[4]) const {
     const double yi = in.y;
     const double axi = in.ax;
     const double bi = in.b;
     const double ypi = yi + eta * ((2.0 * s - axi) - bi);
-    yp[i] = ypi;
-    axp[i] = s;
+    st_epi<EF>(yp + i, ypi);
+    st_epi<EF>(axp + i, s);
     const double omw = 1.0 - w;
     const double yci = omw * ypi + w * in.ya;
     yc[i] = yci;
@@ -910,7 +942,7 @@ struct EpiDual {  // phase B, rows of A
     // gathers speculatively; after a restart the loop pushes y+ itself
     if constexpr (RK)
       if (T->nranks > 1) push_peers(T, T->py, yc_off + i, yci, __ldg(T->yneed + (i - T->row0)));
-    axc[i] = omw * s + w * in.axa;
+    st_epi<EF>(axc + i, omw * s + w * in.axa);
     const double d = axi - bi;
     const double dy = yi - ypi;
     const double dax = axi - s;
@@ -1469,7 +1501,7 @@ __device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R,
   const int n = P->n, m = P->m;
   double acc[NQ];
   acc_init<NQ, 0>(acc);
-  EpiPrimal<RK, BOX> e{xsrc_ptr(P, R),
+  EpiPrimal<RK, BOX, LM == 1 ? HX_EPI_EF : 0> e{xsrc_ptr(P, R),
                        P->xpool + static_cast<size_t>(R->x_anchor) * n,
                        P->c,
                        P->xpool + static_cast<size_t>(R->zx_out) * n,
@@ -1484,7 +1516,7 @@ __device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R,
 #ifdef HX_WPROF
   const unsigned long long w0 = clock64();
 #endif
-  spmv_rows<NQ, 0, LM>(S, par, SrcVecT<LM == 1>{ycur_ptr(P, R)}, e, acc, gwarp_id(g),
+  spmv_rows<NQ, 0, LM>(S, par, SrcVecT<LM == 1 && HX_GATHER_LAST>{ycur_ptr(P, R)}, e, acc, gwarp_id(g),
                        threadIdx.x & 31, stage, seq, head);
 #ifdef HX_WPROF
   if constexpr (!RK)
@@ -1501,7 +1533,7 @@ __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int
   const int n = P->n, m = P->m;
   double acc[4];
   acc_init<4, 0>(acc);
-  EpiDual<RK> e{ycur_ptr(P, R),
+  EpiDual<RK, LM == 1 ? HX_EPI_EF : 0> e{ycur_ptr(P, R),
             axcur_ptr(P, R),
             P->b,
             P->ypool + static_cast<size_t>(R->y_anchor) * m,
@@ -1519,7 +1551,8 @@ __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int
 #ifdef HX_WPROF
   const unsigned long long w0 = clock64();
 #endif
-  spmv_rows<4, 0, LM>(S, par, SrcVecT<LM == 1>{P->xpool + static_cast<size_t>(R->xp_out) * n}, e, acc, gwarp_id(g),
+  spmv_rows<4, 0, LM>(S, par, SrcVecT<LM == 1 && HX_GATHER_LAST>{P->xpool + static_cast<size_t>(R->xp_out) * n}, e,
+                      acc, gwarp_id(g),
                       threadIdx.x & 31, stage, seq, head);
 #ifdef HX_WPROF
   if constexpr (!RK)
@@ -2910,9 +2943,9 @@ int upload_built_sched(hx_ctx* ctx, DevSched& d, SchedHost h, int rows, int cols
   if (row0)
     for (int4& t : h.tasks)
       if (t.x != t.y || t.z != t.w) {
-        const int kind = t.y >> kKindShift;
+        const int kind = task_kind(t.y);
         t.x += row0;
-        t.y = ((t.y & kRowMask) + row0) | (kind << kKindShift);
+        t.y = task_y((t.y & kRowMask) + row0, kind);
       }
   HX_CUDA(ctx, dalloc(&d.tasks, h.tasks.size()));
   HX_CUDA(ctx, dalloc(&d.meta, h.meta.size()));

@@ -52,6 +52,12 @@ constexpr double kTaskCost = 64.0;         // fixed latency cost of one warp tas
 #endif
 // 1: tasks of <= 16 rows sum each row on two lanes (head / tail half):
 // 23.7k it/s on configs[1] (register spills + shuffle), not used.
+#ifndef HX_EPI_EF
+#define HX_EPI_EF 0
+#endif
+#ifndef HX_GATHER_LAST
+#define HX_GATHER_LAST 1
+#endif
 #ifndef HX_RSPLIT
 #define HX_RSPLIT 0
 #endif
@@ -73,9 +79,27 @@ constexpr int kMaxRanks = 8;               // ranks of a row-partitioned team (o
 //                counter, index}.  A single-piece row is finished in place;
 //                otherwise the last piece to finish reduces the pieces in
 //                index order and runs the row's epilogue (deterministic).
-enum TaskKind : int { kTaskStream = 0, kTaskPiece = 1 };
+//   kTaskPieceRun: a piece that is not the last of its run -- a long row's
+//                consecutive pieces are dealt to one warp in runs, which
+//                carries the run's partial sum in registers; only the run's
+//                last piece (kTaskPiece) publishes it, so a run of r pieces
+//                costs one fence + atomic instead of r (configs[4]'s Zipf rows).
+enum TaskKind : int { kTaskStream = 0, kTaskPiece = 1, kTaskPieceRun = 2 };
 constexpr int kKindShift = 30;
 constexpr int kRowMask = (1 << kKindShift) - 1;
+__host__ __device__ __forceinline__ int task_kind(int y) {
+  return static_cast<int>(static_cast<unsigned>(y) >> kKindShift);
+}
+__host__ __device__ __forceinline__ int task_y(int row_end, int kind) {
+  return static_cast<int>(static_cast<unsigned>(row_end) | (static_cast<unsigned>(kind) << kKindShift));
+}
+// A run's cost is at most the mean warp cost / kRunFrac (balance), and at
+// most kRunMax pieces.
+#ifndef HX_RUN_FRAC
+#define HX_RUN_FRAC 4.0
+#endif
+constexpr double kRunFrac = HX_RUN_FRAC;
+constexpr int kRunMax = 64;
 
 // Device view of one CSR matrix plus its nnz-balanced warp schedule.
 struct Sched {

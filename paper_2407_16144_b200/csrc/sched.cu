@@ -2,7 +2,8 @@
 //
 // Rows of length <= kStreamRowMax are packed into stream tasks of at most
 // kChunk nonzeros / kStreamRowsMax rows; every longer row is cut into pieces
-// of at most kChunk nonzeros (a single piece when it fits).  The row-ordered
+// of at most kChunk nonzeros (a single piece when it fits), grouped into runs
+// of consecutive pieces that one warp processes back to back.  The row-ordered
 // task list is then cut into one contiguous, equal-cost slice per warp
 // (cost = nnz + kRowCost per row).  Static and deterministic: the same matrix
 // and grid always give the same row -> (warp, lane) map, which is what makes
@@ -22,24 +23,37 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, doubl
   const double total = static_cast<double>(nnz) + row_cost * rows;
 
   std::vector<double> cost;
+  std::vector<std::size_t> unit;  // first task of each dealing unit (a stream task or a run of pieces)
   auto push = [&](int r0, int r1, int kind, int p0, int p1, int4 meta, double c) {
-    s.tasks.push_back(int4{r0, r1 | (kind << kKindShift), p0, p1});
+    s.tasks.push_back(int4{r0, task_y(r1, kind), p0, p1});
     s.meta.push_back(meta);
     cost.push_back(c + task_cost);
   };
+  // a run of pieces is dealt to one warp as a unit: at most 1/kRunFrac of the
+  // mean warp cost, so the dealing stays balanced
+  const double run_budget = std::max(1.0, total / warps / kRunFrac);
   int r = 0;
   while (r < rows) {
     const int64_t len = ptr[r + 1] - ptr[r];
     if (len > kStreamRowMax) {
       const int np = static_cast<int>((len + kChunk - 1) / kChunk);
-      for (int q = 0; q < np; ++q) {
-        const int p0 = static_cast<int>(ptr[r] + len * q / np);
-        const int p1 = static_cast<int>(ptr[r] + len * (q + 1) / np);
-        push(r, r + 1, kTaskPiece, p0, p1, int4{s.n_slots + q, np, np > 1 ? s.n_long : -1, q},
-             static_cast<double>(p1 - p0) + (q + 1 == np ? row_cost : 0.0));
+      const double pc = static_cast<double>(len) / np + task_cost;
+      const int per = std::max(1, std::min(kRunMax, static_cast<int>(run_budget / pc)));
+      const int nr = (np + per - 1) / per;
+      for (int k = 0; k < nr; ++k) {
+        unit.push_back(s.tasks.size());
+        const int q0 = static_cast<int>(static_cast<int64_t>(np) * k / nr);
+        const int q1 = static_cast<int>(static_cast<int64_t>(np) * (k + 1) / nr);
+        for (int q = q0; q < q1; ++q) {
+          const int p0 = static_cast<int>(ptr[r] + len * q / np);
+          const int p1 = static_cast<int>(ptr[r] + len * (q + 1) / np);
+          push(r, r + 1, q + 1 == q1 ? kTaskPiece : kTaskPieceRun, p0, p1,
+               int4{s.n_slots + k, nr, nr > 1 ? s.n_long : -1, k},
+               static_cast<double>(p1 - p0) + (q + 1 == np ? row_cost : 0.0));
+        }
       }
-      if (np > 1) {
-        s.n_slots += np;
+      if (nr > 1) {
+        s.n_slots += nr;
         s.n_long += 1;
       }
       ++r;
@@ -53,19 +67,26 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, doubl
       used += l;
       ++r;
     }
+    unit.push_back(s.tasks.size());
     push(r0, r, kTaskStream, static_cast<int>(ptr[r0]), static_cast<int>(ptr[r]), int4{0, 0, 0, 0},
          static_cast<double>(used) + row_cost * (r - r0));
   }
+  const std::size_t nt = s.tasks.size();
+  unit.push_back(nt);
 
-  // Longest-processing-time dealing: tasks heaviest first, each to the
+  // Longest-processing-time dealing: units heaviest first, each to the
   // currently least-loaded warp (ties to the lower warp id).  Warp w's tasks are
   // laid out at positions w, w + W, w + 2W, ... (padded with empty tasks),
-  // which is how the kernels walk them.  Deterministic and balanced;
-  // reductions stay fixed-order because every row keeps one (warp, lane) owner.
-  const std::size_t nt = s.tasks.size();
-  std::vector<int> order(nt);
-  for (std::size_t t = 0; t < nt; ++t) order[t] = static_cast<int>(t);
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  // which is how the kernels walk them; a run's pieces stay consecutive.
+  // Deterministic and balanced; reductions stay fixed-order because every row
+  // keeps one (warp, lane) owner.
+  const std::size_t nu = unit.size() - 1;
+  std::vector<double> ucost(nu, 0.0);
+  for (std::size_t u = 0; u < nu; ++u)
+    for (std::size_t t = unit[u]; t < unit[u + 1]; ++t) ucost[u] += cost[t];
+  std::vector<int> order(nu);
+  for (std::size_t u = 0; u < nu; ++u) order[u] = static_cast<int>(u);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return ucost[a] > ucost[b]; });
   using Load = std::pair<double, int>;  // (load, warp)
   std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
   std::vector<std::vector<int>> per_warp(static_cast<std::size_t>(warps));
@@ -74,11 +95,11 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, doubl
     wcost[w] = w % kWarps == 0 ? lead : 0.0;
     heap.push({wcost[w], w});
   }
-  for (int t : order) {
+  for (int u : order) {
     auto [load, w] = heap.top();
     heap.pop();
-    per_warp[w].push_back(t);
-    wcost[w] = load + cost[t];
+    for (std::size_t t = unit[u]; t < unit[u + 1]; ++t) per_warp[w].push_back(static_cast<int>(t));
+    wcost[w] = load + ucost[u];
     heap.push({wcost[w], w});
   }
   std::size_t rounds = 0;
@@ -101,7 +122,7 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, doubl
   for (std::size_t k = 0; k < s.tasks.size(); ++k) {
     const int4& tk = s.tasks[k];
     const int4& mt = s.meta[k];
-    if ((tk.y >> kKindShift) == kTaskPiece && mt.y > 1 && mt.w == 0)
+    if (task_kind(tk.y) == kTaskPiece && mt.y > 1 && mt.w == 0)
       owner[mt.z] = static_cast<int>(k % static_cast<std::size_t>(warps)) / kWarps;
   }
   s.owned_ptr.assign(static_cast<std::size_t>(grid) + 1, 0);
