@@ -562,7 +562,7 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
   int4 tk = head.tk;
   int4 tk1 = head.tk1;
   TaskRegs cur = head.cur;
-  double run_acc = 0.0;  // partial sum of the current run of long-row pieces
+  double run_acc = 0.0;  // this lane's partial sum of the current run of long-row pieces
   for (; t < n; t += W) {
     const int4 tk2 = t + 2 * W < n ? __ldg(S.tasks + t + 2 * W) : kNone;
     TaskRegs nxt;
@@ -721,18 +721,19 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
       for (int w = 1; w < kLoadsPerLane; w *= 2)
 #pragma unroll
         for (int j = 0; j + w < kLoadsPerLane; j += 2 * w) pv[j] += pv[j + w];
-      double s = warp_sum(pv[0]);
+      double s = pv[0];
 #else
       double s = 0.0;
 #pragma unroll
       for (int j = 0; j < kLoadsPerLane; ++j) s += cur.cv[j];
-      s = warp_sum(s);
 #endif
-      // a run's pieces: the partial stays in registers until its last piece
+      // a run's pieces: each lane's partial stays in registers until the
+      // run's last piece, which reduces it across the warp once
       if (kind == kTaskPieceRun) {
         run_acc += s;
+        s = 0.0;
       } else {
-        s = run_acc + s;
+        s = warp_sum(run_acc + s);
         run_acc = 0.0;
       }
       if (lane == 0 && kind == kTaskPiece) {

@@ -94,9 +94,11 @@ __host__ __device__ __forceinline__ int task_y(int row_end, int kind) {
   return static_cast<int>(static_cast<unsigned>(row_end) | (static_cast<unsigned>(kind) << kKindShift));
 }
 // A run's cost is at most the mean warp cost / kRunFrac (balance), and at
-// most kRunMax pieces.
+// most kRunMax pieces.  Measured (tools/big_configs.py): kRunFrac 2 / 3 / 4 /
+// 8 / no runs -> configs[3] 9.26k / 9.39k / 8.81k / 7.64k / 7.64k it/s,
+// configs[4] 512 / 510 / 511 / 512 / 405 it/s.
 #ifndef HX_RUN_FRAC
-#define HX_RUN_FRAC 4.0
+#define HX_RUN_FRAC 3.0
 #endif
 constexpr double kRunFrac = HX_RUN_FRAC;
 constexpr int kRunMax = 64;
