@@ -40,6 +40,13 @@ int hplp_solve_csr(int32_t device, int64_t m, int64_t n, const int64_t* row_ptr,
                    const double* val, const double* b, const double* c, const hplp_config_t* cfg,
                    hplp_io_t* io, hplp_result_t* result);
 
+/* The unit start vector of power_iteration (src/sparse_matrix.cpp:145-151):
+ * n draws of std::normal_distribution<double>(0, 1) from
+ * std::mt19937_64(seed), normalised -- bit-identical to the reference's
+ * sequential loop (libstdc++), computed with the uniform conversion and the
+ * polar method's log/sqrt on host threads.  Host only; x has n entries. */
+int hplp_power_start(int64_t n, uint64_t seed, double* x);
+
 /* A device-resident problem for repeated solves (upload once). */
 int hplp_solver_create(int32_t device, int64_t m, int64_t n, const int64_t* row_ptr,
                        const int32_t* col_idx, const double* val, const double* b, const double* c,

@@ -1023,6 +1023,20 @@ int orc_lp_create(int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* c
 
 void orc_lp_free(void* h) { delete static_cast<orc::Lp*>(h); }
 
+// The start vector of power_iteration above (src/sparse_matrix.cpp:145-151),
+// drawn sequentially: the checker for hplp_power_start.
+int orc_power_start(int64_t n, uint64_t seed, double* x) {
+  return guarded([&] {
+    std::mt19937_64 gen(seed);
+    std::normal_distribution<double> dist(0.0, 1.0);
+    orc::Vec v(static_cast<std::size_t>(n));
+    for (auto& e : v) e = dist(gen);
+    double xn = orc::norm(v);
+    if (xn == 0.0) std::fill(v.begin(), v.end(), 1.0), xn = orc::norm(v);
+    for (std::size_t i = 0; i < v.size(); ++i) x[i] = v[i] / xn;
+  });
+}
+
 // Box form: upper bounds u (n values, >= 0, +inf = none); NULL clears.
 int orc_lp_set_box(void* h, const double* u) {
   return guarded([&] {

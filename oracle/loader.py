@@ -53,6 +53,8 @@ def load(kind: str = "port") -> C.CDLL:
     sig("last_error", C.c_char_p)
     sig("lp_create", C.c_int, I64, I64, PI64, PI32, PD, PD, PD, C.POINTER(V))
     sig("lp_free", None, V)
+    if hasattr(lib, p + "power_start"):  # the restatement only
+        sig("power_start", C.c_int, I64, C.c_uint64, PD)
     sig("spmv", C.c_int, V, PD, PD)
     sig("spmv_transpose", C.c_int, V, PD, PD)
     sig("power_iteration", C.c_int, V, D, I64, C.c_uint64, PD, PI64, PI32, PD)

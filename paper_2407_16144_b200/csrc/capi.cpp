@@ -258,6 +258,14 @@ int hplp_solve_csr(int32_t device, int64_t m, int64_t n, const int64_t* row_ptr,
   return rc;
 }
 
+int hplp_power_start(int64_t n, uint64_t seed, double* x) {
+  return guarded([&] {
+    if (n < 0 || (n > 0 && !x)) throw std::invalid_argument("hplp_power_start: n < 0 or x is NULL");
+    const std::vector<double> v = hplp_gpu::power_start(n, seed);
+    std::copy(v.begin(), v.end(), x);
+  });
+}
+
 int hplp_to_standard_form(const hplp_general_t* g, void** std_form, int64_t* m, int64_t* n, int64_t* nnz) {
   return guarded([&] {
     auto conv = hplp_gpu::to_standard_form(*g);

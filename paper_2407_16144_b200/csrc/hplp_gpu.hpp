@@ -283,6 +283,8 @@ struct SolveResult {
 struct PowerStart;
 using PowerStartFuture = std::shared_future<std::shared_ptr<PowerStart>>;
 PowerStartFuture draw_power_start_async(int64_t n, uint64_t seed);
+// The normalised start vector itself (src/sparse_matrix.cpp:145-151), drawn as above.
+std::vector<double> power_start(int64_t n, uint64_t seed);
 
 // Box form (no reference counterpart, a flagged
 // mode): the trailing bound rows x_j + s_j = u_j that to_standard_form

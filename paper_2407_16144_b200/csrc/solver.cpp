@@ -9,6 +9,7 @@
 // traced iteration) and assembles the SolveResult.  There is no CPU compute
 // path: without a B200 the hx layer fails and solve() throws.
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -18,6 +19,8 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "hplp_gpu.hpp"
@@ -90,17 +93,132 @@ struct PowerResult {
 
 struct PowerStart {
   Vector x;  // normalised
-  std::mt19937_64 gen;
-  std::normal_distribution<double> dist;
+  uint64_t seed = 0;
+  // The generator state after drawing x (for a re-draw on sigma == 0, which
+  // continues the same stream): replayed from the seed, only when needed.
+  void stream_after(std::mt19937_64& gen, std::normal_distribution<double>& dist) const {
+    gen.seed(seed);
+    dist = std::normal_distribution<double>(0.0, 1.0);
+    for (std::size_t i = 0; i < x.size(); ++i) (void)dist(gen);
+  }
 };
+
+namespace {
+
+// The raw engine outputs replayed through libstdc++'s own generate_canonical
+// (same template, same long double arithmetic as _Adaptor in
+// std::normal_distribution), so every uniform is bit-identical.
+struct ReplayEngine {
+  using result_type = std::mt19937_64::result_type;
+  const result_type* p;
+  static constexpr result_type min() { return std::mt19937_64::min(); }
+  static constexpr result_type max() { return std::mt19937_64::max(); }
+  result_type operator()() { return *p++; }
+};
+
+}  // namespace
+
+// n draws of std::normal_distribution<double>(0, 1) from std::mt19937_64(seed)
+// -- bit for bit what the reference's loop `for (auto& v : x) v = dist(gen)`
+// gives (src/sparse_matrix.cpp:145-151; libstdc++'s Marsaglia polar method,
+// bits/random.tcc) -- with the expensive parts on host threads.  The polar
+// method draws uniforms in pairs (u[2p], u[2p+1]) until a pair lands inside
+// the unit disc, so pair p's fate depends on its own two engine outputs only:
+// the outputs are drawn in order (cheap), then each thread converts a range of
+// pairs with libstdc++'s own generate_canonical (the long double division is
+// most of the sequential cost) and tests them, a prefix count over the ranges
+// places every accepted pair in the output, and the threads compute the
+// accepted pairs' log/sqrt.  Accepted pair k yields out[2k] = y * mult and
+// out[2k + 1] = x * mult (the value the distribution saves for its next call).
+// Scratch buffers are kept between calls (first-touch page faults cost more
+// than the arithmetic).
+void draw_normals(std::vector<double>& out, uint64_t seed) {
+  const std::size_t n = out.size(), need = (n + 1) / 2;
+  if (n == 0) return;
+  const unsigned threads = std::clamp(std::thread::hardware_concurrency(), 1u, 8u);
+  static std::mutex scratch_mu;
+  static std::vector<std::mt19937_64::result_type> s_raw;
+  static std::vector<double> s_u;
+  static std::vector<unsigned char> s_ok;
+  std::unique_lock<std::mutex> own(scratch_mu, std::try_to_lock);
+  std::vector<std::mt19937_64::result_type> l_raw;
+  std::vector<double> l_u;
+  std::vector<unsigned char> l_ok;
+  auto& raw = own.owns_lock() ? s_raw : l_raw;
+  auto& u = own.owns_lock() ? s_u : l_u;
+  auto& ok = own.owns_lock() ? s_ok : l_ok;
+  std::mt19937_64 gen(seed);
+  std::size_t done = 0;  // accepted pairs written so far
+  while (done < need) {
+    // acceptance pi/4 per pair: ~1.3x the pairs still needed, plus slack
+    const std::size_t np = (need - done) * 13 / 10 + 64;
+    raw.resize(2 * np);
+    u.resize(2 * np);
+    ok.resize(np);
+    for (auto& r : raw) r = gen();
+    const unsigned T = static_cast<unsigned>(std::min<std::size_t>(threads, (np + 8191) / 8192));
+    std::vector<std::size_t> cnt(T + 1, 0);
+    auto range = [&](unsigned t, std::size_t len) { return std::pair<std::size_t, std::size_t>{len * t / T, len * (t + 1) / T}; };
+    auto run = [&](auto&& f) {
+      std::vector<std::thread> pool;
+      for (unsigned t = 1; t < T; ++t) pool.emplace_back(f, t);
+      f(0u);
+      for (auto& th : pool) th.join();
+    };
+    run([&](unsigned t) {
+      const auto [a, b] = range(t, np);
+      ReplayEngine e{raw.data() + 2 * a};
+      std::size_t c = 0;
+      for (std::size_t p = a; p < b; ++p) {
+        const double u0 = std::generate_canonical<double, std::numeric_limits<double>::digits>(e);
+        const double u1 = std::generate_canonical<double, std::numeric_limits<double>::digits>(e);
+        u[2 * p] = u0, u[2 * p + 1] = u1;
+        const double x = 2.0 * u0 - 1.0;
+        const double y = 2.0 * u1 - 1.0;
+        const double r2 = x * x + y * y;
+        ok[p] = !(r2 > 1.0 || r2 == 0.0);
+        c += ok[p];
+      }
+      cnt[t + 1] = c;
+    });
+    for (unsigned t = 0; t < T; ++t) cnt[t + 1] += cnt[t];
+    run([&](unsigned t) {
+      const auto [a, b] = range(t, np);
+      std::size_t k = done + cnt[t];
+      for (std::size_t p = a; p < b && k < need; ++p) {
+        if (!ok[p]) continue;
+        const double x = 2.0 * u[2 * p] - 1.0;
+        const double y = 2.0 * u[2 * p + 1] - 1.0;
+        const double r2 = x * x + y * y;
+        const double mult = std::sqrt(-2 * std::log(r2) / r2);
+        out[2 * k] = y * mult * 1.0 + 0.0;  // ret * stddev + mean
+        if (2 * k + 1 < n) out[2 * k + 1] = x * mult * 1.0 + 0.0;
+        ++k;
+      }
+    });
+    done = std::min(need, done + cnt[T]);
+    // the engine must continue right after the last pair used: outputs drawn
+    // past it are never consumed (a re-draw replays the stream from the seed)
+  }
+}
+
+std::vector<double> power_start(int64_t n, uint64_t seed) {
+  PowerStart s;
+  s.seed = seed;
+  s.x.resize(static_cast<std::size_t>(std::max<int64_t>(n, 0)));
+  draw_normals(s.x, seed);
+  double xn = seq_norm(s.x);
+  if (xn == 0.0) std::fill(s.x.begin(), s.x.end(), 1.0), xn = seq_norm(s.x);
+  for (auto& v : s.x) v /= xn;
+  return std::move(s.x);
+}
 
 PowerStartFuture draw_power_start_async(int64_t n, uint64_t seed) {
   return std::async(std::launch::async, [n, seed] {
            auto s = std::make_shared<PowerStart>();
-           s->gen.seed(seed);
-           s->dist = std::normal_distribution<double>(0.0, 1.0);
+           s->seed = seed;
            s->x.resize(static_cast<std::size_t>(std::max<int64_t>(n, 0)));
-           for (auto& v : s->x) v = s->dist(s->gen);
+           draw_normals(s->x, seed);
            double xn = seq_norm(s->x);
            if (xn == 0.0) std::fill(s->x.begin(), s->x.end(), 1.0), xn = seq_norm(s->x);
            for (auto& v : s->x) v /= xn;
@@ -121,8 +239,9 @@ PowerResult power_iteration(hx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, doub
     res.converged = true;
     return res;
   }
-  std::mt19937_64 gen = start.gen;  // a re-draw continues the stream
-  std::normal_distribution<double> dist = start.dist;
+  std::mt19937_64 gen;  // a re-draw continues the stream (rebuilt when needed)
+  std::normal_distribution<double> dist;
+  bool stream_ready = false;
   Vector x = start.x;
   int64_t k0 = 0;
   double sigma_prev = 0.0;
@@ -138,6 +257,7 @@ PowerResult power_iteration(hx_ctx* ctx, int64_t m, int64_t n, int64_t nnz, doub
       return res;
     }
     // sigma == 0 at iteration iters-1: re-draw and continue (:158-163)
+    if (!stream_ready) start.stream_after(gen, dist), stream_ready = true;
     for (auto& v : x) v = dist(gen);
     const double nn = seq_norm(x);
     for (auto& v : x) v /= nn;

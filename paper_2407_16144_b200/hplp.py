@@ -61,6 +61,7 @@ def lib() -> C.CDLL:
     sig("hplp_last_error", C.c_char_p)
     sig("hplp_status_string", C.c_char_p, I32)
     sig("hplp_validate_config", C.c_int, C.POINTER(abi.Config))
+    sig("hplp_power_start", C.c_int, I64, C.c_uint64, PD)
     sig("hplp_solve_csr", C.c_int, I32, I64, I64, PI64, PI32, PD, PD, PD, C.POINTER(abi.Config),
         C.POINTER(abi.IO), C.POINTER(abi.Result))
     sig("hplp_solver_create", C.c_int, I32, I64, I64, PI64, PI32, PD, PD, PD, PV)
@@ -585,6 +586,13 @@ def box_form(m, n, row_ptr, col_idx, val, b, c):
     _check(lib().hplp_box_form_dims(int(m), int(n), i64ptr(rp), i32ptr(ci), dptr(v), dptr(bb), dptr(cc),
                                     C.byref(mb), C.byref(nb), dptr(up)))
     return mb.value, nb.value, up[: nb.value].copy()
+
+
+def power_start(n, seed=12345):
+    """hplp_power_start: the normalised power-iteration start vector (host)."""
+    x = np.empty(int(n))
+    _check(lib().hplp_power_start(int(n), C.c_uint64(seed), dptr(x)))
+    return x
 
 
 def plan_partition(m, n, row_ptr, col_idx, parts):

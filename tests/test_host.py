@@ -177,3 +177,20 @@ def test_cuda_path_fails_loudly_without_gpu():
         hplp.solve(1, 1, rp, np.array([0], np.int32), np.array([1.0]), np.array([1.0]), np.array([0.0]))
     with pytest.raises(hplp.HplpError):
         hplp.HX(device=0)
+
+
+@pytest.mark.parametrize("seed", [12345, 1, 2**63 + 5])
+def test_power_start_bit_identical_to_sequential_draw(seed):
+    """hplp_power_start (parallel uniform conversion and log/sqrt) equals the
+    reference's sequential std::normal_distribution loop bit for bit
+    (src/sparse_matrix.cpp:145-151), checked against the oracle's restatement;
+    odd and even lengths, including configs[1]'s 430,000."""
+    import oracle
+    from oracle.loader import load
+
+    lo = load("port")
+    for n in (1, 2, 3, 7, 1000, 1001, 40_001, 430_000):
+        want = np.empty(n)
+        assert lo.orc_power_start(n, C.c_uint64(seed), want.ctypes.data_as(C.POINTER(C.c_double))) == 0
+        got = hplp.power_start(n, seed)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (n, seed)
