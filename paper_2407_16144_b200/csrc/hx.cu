@@ -443,7 +443,7 @@ __device__ __forceinline__ double warp_reduce_strided(const double* p, int count
 // accumulate per thread; a long row's terms are parked in long_terms by
 // whichever warp finishes it, so every reduction keeps a fixed order.
 // ---------------------------------------------------------------------------
-struct WarpStage {
+struct alignas(16) WarpStage {
   double prod[kChunk];
 };
 constexpr size_t kStageBytes = sizeof(WarpStage) * kWarps;
@@ -507,6 +507,46 @@ __device__ __forceinline__ void st_epi(double* p, double v) {
 
 // LM: 0 plain read-only loads, 1 evict_first streams, 2 chosen at run time by
 // S.stream_hint (one load sequence with a selected policy)
+#if HX_VEC
+// Vectorised task loads (HX_VEC): the window starts at the even index
+// pa = p0 & ~1 and lane l holds elements e = 64 (j / 2) + 2 l + (j & 1) of
+// it, loaded as int2 / double2 pairs (half the load instructions); elements
+// outside [p0, p1) are zero.  Tasks hold at most kChunk - 1 nonzeros so the
+// shifted window fits kChunk slots; the matrix arrays carry a few padding
+// elements, so a pair starting at the last nonzero stays in bounds.
+__device__ __forceinline__ int vec_e(int j, int lane) { return (j >> 1) * 64 + 2 * lane + (j & 1); }
+template <int LM>
+__device__ __forceinline__ void load_task(const Sched& S, const int4& tk, int lane, TaskRegs& r) {
+  const int p0 = tk.z, pa = p0 & ~1, e0 = p0 - pa, e1 = tk.w - pa;
+  HX_CHECK(tk.w - p0 >= 0 && e1 <= kChunk && p0 >= 0, "task nnz range", p0, tk.w - p0);
+  [[maybe_unused]] const unsigned long long pol =
+      LM == 0 ? 0ull : (LM == 1 || S.stream_hint ? l2_policy_first() : l2_policy_normal());
+#pragma unroll
+  for (int jj = 0; jj < kLoadsPerLane / 2; ++jj) {
+    const int e = jj * 64 + 2 * lane;
+    int2 iv = make_int2(0, 0);
+    double2 vv = make_double2(0.0, 0.0);
+    if (e < e1) {
+      const int2* ip = reinterpret_cast<const int2*>(S.idx + pa + e);
+      const double2* vp = reinterpret_cast<const double2*>(S.val + pa + e);
+      if constexpr (LM == 0) {
+        iv = __ldg(ip);
+        vv = __ldg(vp);
+      } else {
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
+                     : "=r"(iv.x), "=r"(iv.y) : "l"(ip), "l"(pol));
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                     : "=d"(vv.x), "=d"(vv.y) : "l"(vp), "l"(pol));
+      }
+    }
+    const bool v0 = e >= e0 && e < e1, v1 = e + 1 < e1;
+    r.ci[2 * jj] = v0 ? iv.x : 0;
+    r.cv[2 * jj] = v0 ? vv.x : 0.0;
+    r.ci[2 * jj + 1] = v1 ? iv.y : 0;
+    r.cv[2 * jj + 1] = v1 ? vv.y : 0.0;
+  }
+}
+#else
 template <int LM>
 __device__ __forceinline__ void load_task(const Sched& S, const int4& tk, int lane, TaskRegs& r) {
   const int p0 = tk.z, len = tk.w - tk.z;
@@ -528,6 +568,7 @@ __device__ __forceinline__ void load_task(const Sched& S, const int4& tk, int la
     }
   }
 }
+#endif
 
 // The pipeline's head: the first two task descriptors and the first task's
 // index/value registers.  They depend only on the (read-only) matrix, so a
@@ -568,7 +609,11 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
     TaskRegs nxt;
     load_task<LM>(S, tk1, lane, nxt);
     const int r0 = tk.x, r1 = tk.y & kRowMask, kind = task_kind(tk.y);
+#if HX_VEC
+    const int p0 = tk.z & ~1, len = tk.w - p0;  // the window's base and extent
+#else
     const int p0 = tk.z, len = tk.w - tk.z;
+#endif
     HX_CHECK(r0 >= 0 && r1 >= r0 && r1 <= S.row_limit, "task rows", r0, r1);
     // stream tasks: up to two rows per lane (lane, lane + 32); their bounds and
     // epilogue inputs are loaded before the gathers so the latencies overlap
@@ -600,13 +645,25 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
     }
 #pragma unroll
     for (int j = 0; j < kLoadsPerLane; ++j) {
+#if HX_VEC
+      const int q = vec_e(j, lane);
+      const bool live = q >= tk.z - p0 && q < len;
+#else
       const int q = j * 32 + lane;
-      HX_CHECK(q >= len || (cur.ci[j] >= 0 && cur.ci[j] < S.cols), "gather index", cur.ci[j], S.cols);
-      if (q < len) cur.cv[j] = cur.cv[j] * src(cur.ci[j]);
+      const bool live = q < len;
+#endif
+      HX_CHECK(!live || (cur.ci[j] >= 0 && cur.ci[j] < S.cols), "gather index", cur.ci[j], S.cols);
+      if (live) cur.cv[j] = cur.cv[j] * src(cur.ci[j]);
     }
     if (kind == kTaskStream) {
+#if HX_VEC
+#pragma unroll
+      for (int jj = 0; jj < kLoadsPerLane / 2; ++jj)
+        reinterpret_cast<double2*>(st->prod)[jj * 32 + lane] = make_double2(cur.cv[2 * jj], cur.cv[2 * jj + 1]);
+#else
 #pragma unroll
       for (int j = 0; j < kLoadsPerLane; ++j) st->prod[j * 32 + lane] = cur.cv[j];
+#endif
       __syncwarp();
 #if HX_RSUM == 1
       // two interleaved partial sums (even / odd positions), combined at the
@@ -3368,8 +3425,8 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   HX_CUDA(c, dalloc(&rp64, m + 1));
   HX_CUDA(c, dalloc(&flags, 1));
   HX_CUDA(c, dalloc(&c->a_ptr, m + 1));
-  HX_CUDA(c, dalloc(&c->a_idx, nnz));
-  HX_CUDA(c, dalloc(&c->a_val, nnz));
+  HX_CUDA(c, dalloc(&c->a_idx, nnz + kMatrixPad));
+  HX_CUDA(c, dalloc(&c->a_val, nnz + kMatrixPad));
   HX_CUDA(c, dalloc(&c->b, m));
   HX_CUDA(c, dalloc(&c->c, n));
   HX_CUDA(c, cudaMemcpyAsync(rp64, row_ptr, (m + 1) * sizeof(long long), cudaMemcpyHostToDevice, s));
@@ -3404,8 +3461,8 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     HX_CUDA(c, dalloc(&perm, nnz));
     HX_CUDA(c, dalloc(&cnt, n + 1));
     HX_CUDA(c, dalloc(&c->t_ptr, n + 1));
-    HX_CUDA(c, dalloc(&c->t_idx, nnz));
-    HX_CUDA(c, dalloc(&c->t_val, nnz));
+    HX_CUDA(c, dalloc(&c->t_idx, nnz + kMatrixPad));
+    HX_CUDA(c, dalloc(&c->t_val, nnz + kMatrixPad));
     row_of_kernel<<<nblk, 256, 0, s>>>(static_cast<int>(m), c->a_ptr, row_of, iota);
     int bits = 1;
     while ((int64_t{1} << bits) < n + 1) ++bits;

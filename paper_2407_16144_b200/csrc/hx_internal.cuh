@@ -62,7 +62,14 @@ constexpr double kTaskCost = 64.0;         // fixed latency cost of one warp tas
 #define HX_RSPLIT 0
 #endif
 constexpr int kLoadsPerLane = HX_LOADS;    // nonzeros per lane per task
-constexpr int kChunk = 32 * kLoadsPerLane; // max nonzeros per warp task (256)
+constexpr int kChunk = 32 * kLoadsPerLane; // nonzero slots per warp task (256)
+// Vectorised idx/val loads (int2 / double2 from an even-aligned window, see
+// load_task): 1 on, 0 scalar loads.
+#ifndef HX_VEC
+#define HX_VEC 0
+#endif
+constexpr int kTaskNnz = HX_VEC ? kChunk - 1 : kChunk;  // max nonzeros per warp task
+constexpr int kMatrixPad = 4;              // padding elements after idx / val (vector loads)
 constexpr int kStreamRowMax = 64;          // rows up to this length are summed lane-per-row
 constexpr int kStreamRowsMax = 64;         // rows per stream task (two per lane)
 constexpr int kMaxRanks = 8;               // ranks of a row-partitioned team (one node)

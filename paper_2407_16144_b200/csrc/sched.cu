@@ -36,7 +36,7 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, doubl
   while (r < rows) {
     const int64_t len = ptr[r + 1] - ptr[r];
     if (len > kStreamRowMax) {
-      const int np = static_cast<int>((len + kChunk - 1) / kChunk);
+      const int np = static_cast<int>((len + kTaskNnz - 1) / kTaskNnz);
       const double pc = static_cast<double>(len) / np + task_cost;
       const int per = std::max(1, std::min(kRunMax, static_cast<int>(run_budget / pc)));
       const int nr = (np + per - 1) / per;
@@ -63,7 +63,7 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, doubl
     int64_t used = 0;
     while (r < rows && r - r0 < kStreamRowsMax) {
       const int64_t l = ptr[r + 1] - ptr[r];
-      if (l > kStreamRowMax || used + l > kChunk) break;
+      if (l > kStreamRowMax || used + l > kTaskNnz) break;
       used += l;
       ++r;
     }
