@@ -42,6 +42,8 @@ constexpr double kTaskCost = 64.0;         // fixed latency cost of one warp tas
 // (the reference's exact order), 1 two interleaved partial sums (even / odd
 // positions) added at the end, 2 four, 3 two with loads 8 ahead.  Measured on
 // configs[1] (tools/quick_rate.py): 26.81k / 27.86k / 27.47k / 26.97k it/s.
+// Reading 1's products as 16-byte pairs (LDS.128, same sums): 27.23k vs
+// 27.76k (8 B of spills), not kept.
 #ifndef HX_RSUM
 #define HX_RSUM 1
 #endif
