@@ -619,7 +619,7 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
     // epilogue inputs are loaded before the gathers so the latencies overlap
     const int nrows = r1 - r0;
     const bool has_row = kind == kTaskStream && lane < nrows;
-    const bool has_row2 = kind == kTaskStream && lane + 32 < nrows;
+    const bool has_row2 = kStreamRowsMax > 32 && kind == kTaskStream && lane + 32 < nrows;
     int ra = 0, rb = 0, ra2 = 0, rb2 = 0;
     typename Epi::In in{}, in2{};
     if (has_row) {

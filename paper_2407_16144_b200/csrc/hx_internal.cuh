@@ -73,7 +73,12 @@ constexpr int kChunk = 32 * kLoadsPerLane; // nonzero slots per warp task (256)
 constexpr int kTaskNnz = HX_VEC ? kChunk - 1 : kChunk;  // max nonzeros per warp task
 constexpr int kMatrixPad = 4;              // padding elements after idx / val (vector loads)
 constexpr int kStreamRowMax = 64;          // rows up to this length are summed lane-per-row
-constexpr int kStreamRowsMax = 64;         // rows per stream task (two per lane)
+#ifndef HX_ROWS
+#define HX_ROWS 64
+#endif
+// 32 (one row per lane, fewer registers): configs[1] 25.7k vs 27.7k it/s,
+// configs[2] 45.4k vs 44.2k -- 64 kept.
+constexpr int kStreamRowsMax = HX_ROWS;    // rows per stream task (64: two per lane)
 constexpr int kMaxRanks = 8;               // ranks of a row-partitioned team (one node)
 
 // Warp tasks, int4 {row_begin, row_end | kind << 30, p_begin, p_end}; every
