@@ -89,7 +89,9 @@ int hx_precondition(hx_ctx* ctx, int32_t ruiz_iters, double pc_alpha, double* ro
 int hx_set_box(hx_ctx* ctx, const double* upper);
 /* Which loop kernel hx_run launches: 0 loop_kernel, 1 loop_kernel_stream (the
  * matrix streams loaded L2 evict_first: the working set exceeds ~70% of L2;
- * HPLP_L2_STREAM=0/1 overrides), 2 loop_kernel_box; -1 before an upload. */
+ * HPLP_L2_STREAM=0/1 overrides), 2 loop_kernel_box, 3 loop_kernel_stream_cb
+ * (the stream kernel with phase B swept in two column blocks: x+ far larger
+ * than L2; HX_COLBLOCK=0/1 overrides); -1 before an upload. */
 int32_t hx_loop_variant(hx_ctx* ctx);
 /* The device problem (after any preconditioning): CSR A, b, c. */
 int hx_download_problem(hx_ctx* ctx, int64_t* row_ptr, int32_t* col_idx, double* val, double* b, double* c);

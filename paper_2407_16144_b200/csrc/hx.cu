@@ -225,6 +225,11 @@ struct KParams {
   double* yavg;   // m: mean y
   double* aavg;   // m: mean A x
   double* xbar;   // n: x-part of the PDHG step taken at the average
+  // column-blocked phase B (loop_kernel_stream_cb): A split at a column into
+  // A0 (leading columns) and A1, swept one after the other so each sweep's
+  // gathers of x+ stay in L2; bpart holds A0's row sums
+  Sched A0, A1;
+  double* bpart;  // m
 };
 
 // z's buffers: pool role, or an average slot after a baseline restart.
@@ -965,7 +970,7 @@ struct EpiPrimal {  // phase A, rows of A^T
   }
 };
 
-template <bool RK, int EF = 0>
+template <bool RK, int EF = 0, bool PART = false>
 struct EpiDual {  // phase B, rows of A
   const double* y;
   const double* ax;
@@ -979,14 +984,17 @@ struct EpiDual {  // phase B, rows of A
   double eta, w;
   const Team* T;          // RK: peers of the y+ / combo push
   size_t yp_off, yc_off;  // offsets of y+ and the combo in the y pools
+  const double* part;     // PART: the leading column block's row sums (column-blocked phase B)
   struct In {
-    double y, ax, b, ya, axa;
+    double y, ax, b, ya, axa, p;
   };
   __device__ __forceinline__ In load(int i) const {
-    return In{ld_epi<EF>(y + i), ld_epi<EF>(ax + i), EF ? ld_epi<EF>(b + i) : __ldg(b + i), ld_epi<EF>(ya + i),
-              ld_epi<EF>(axa + i)};
+    return In{ld_epi<EF>(y + i),  ld_epi<EF>(ax + i), EF ? ld_epi<EF>(b + i) : __ldg(b + i), ld_epi<EF>(ya + i),
+              ld_epi<EF>(axa + i), PART ? ldcg(part + i) : 0.0};
   }
-  __device__ __forceinline__ void apply(int i, double s, const In& in, double (&t)[4]) const {
+  __device__ __forceinline__ void apply(int i, double s1, const In& in, double (&t)[4]) const {
+    // column-blocked: the row's sum is the leading block's plus this block's
+    const double s = PART ? in.p + s1 : s1;
     const double yi = in.y;
     const double axi = in.ax;
     const double bi = in.b;
@@ -1585,13 +1593,14 @@ __device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R,
 }
 
 // phase B: A x+, dual step, speculative Halpern combos, dual partials
-template <bool RK, int LM = 2>
+template <bool RK, int LM = 2, bool CB = false>
 __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int par, WarpStage* stage,
-                                           unsigned long long seq, const SpmvHead& head, const Geo& g) {
+                                           unsigned long long seq, const SpmvHead& head, const Geo& g,
+                                           unsigned long long* target = nullptr) {
   const int n = P->n, m = P->m;
   double acc[4];
   acc_init<4, 0>(acc);
-  EpiDual<RK, LM == 1 ? HX_EPI_EF : 0> e{ycur_ptr(P, R),
+  EpiDual<RK, LM == 1 ? HX_EPI_EF : 0, CB> e{ycur_ptr(P, R),
             axcur_ptr(P, R),
             P->b,
             P->ypool + static_cast<size_t>(R->y_anchor) * m,
@@ -1604,14 +1613,26 @@ __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int
             R->w_next,
             &P->T,
             static_cast<size_t>(R->yp_out) * m,
-            static_cast<size_t>(R->yc_out) * m};
-  const Sched S = P->A;
+            static_cast<size_t>(R->yc_out) * m,
+            P->bpart};
+  const double* xsrc = P->xpool + static_cast<size_t>(R->xp_out) * n;
+  SpmvHead h1;
+  if constexpr (CB) {
+    // sweep 1: the leading column block's row sums into bpart, then a grid
+    // barrier, then sweep 2 over the trailing block with the full epilogue
+    double a0[1] = {0.0};
+    EpiStore st0{P->bpart};
+    spmv_rows<1, 0, LM>(P->A0, par, SrcVecT<LM == 1 && HX_GATHER_LAST>{xsrc}, st0, a0, gwarp_id(g),
+                        threadIdx.x & 31, stage, seq, head);
+    spmv_head<LM>(P->A1, gwarp_id(g), threadIdx.x & 31, h1);
+    grid_sync(P->bar, *target);
+  }
+  const Sched S = CB ? P->A1 : P->A;
 #ifdef HX_WPROF
   const unsigned long long w0 = clock64();
 #endif
-  spmv_rows<4, 0, LM>(S, par, SrcVecT<LM == 1 && HX_GATHER_LAST>{P->xpool + static_cast<size_t>(R->xp_out) * n}, e,
-                      acc, gwarp_id(g),
-                      threadIdx.x & 31, stage, seq, head);
+  spmv_rows<4, 0, LM>(S, par, SrcVecT<LM == 1 && HX_GATHER_LAST>{xsrc}, e, acc, gwarp_id(g), threadIdx.x & 31, stage,
+                      seq, CB ? h1 : head);
 #ifdef HX_WPROF
   if constexpr (!RK)
     if (P->prof && (threadIdx.x & 31) == 0) P->prof[gridDim.x * (16 + kWarps) + gwarp_id(g)] += clock64() - w0;
@@ -2311,7 +2332,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_baseline(con
 // ---------------------------------------------------------------------------
 // RK = false: one GPU, P in the constant bank (loop_kernel).  RK = true: one
 // rank of a row-partitioned team (loop_kernel_team), P in shared memory.
-template <bool RK, bool BOX = false, int LM = 2>
+template <bool RK, bool BOX = false, int LM = 2, bool CB = false>
 __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
   __shared__ Ctl C;
   __shared__ double tot[kMaxQ];
@@ -2445,10 +2466,10 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
       if (writer && threadIdx.x == 0 && budget != 0ull) set_time_up(par, (global_ns() - t_start) > budget ? 1u : 0u);
     }
     mark(0);
-    spmv_head<LM>(P->A, gwarp_id(g), lane, head);
+    spmv_head<LM>(CB ? P->A0 : P->A, gwarp_id(g), lane, head);
     if (!sync()) return;
     mark(1);
-    phase_dual<RK, LM>(P, R, par, stage, ++seq, head, g);
+    phase_dual<RK, LM, CB>(P, R, par, stage, ++seq, head, g, &target);
     if (threadIdx.x == 0) make_spec(C, SR);
     mark(2);
     spmv_head<LM>(P->AT, gwarp_id(g), lane, head);
@@ -2597,6 +2618,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_stream(const
   const Geo g{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x),
               static_cast<int>(gridDim.x)};
   loop_body<false, false, 1>(&KP, g);
+}
+
+// The stream kernel with phase B swept in two column blocks (hx_upload_csr
+// enables it when x+ is far larger than L2: configs[4]).
+__global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_stream_cb(const __grid_constant__ KParams KP) {
+  const Geo g{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x),
+              static_cast<int>(gridDim.x)};
+  loop_body<false, false, 1, true>(&KP, g);
 }
 
 // The box form (hx_set_box) as its own kernel: the standard loop keeps its code.
@@ -2860,6 +2889,14 @@ struct hx_ctx {
   double* b = nullptr;
   double* c = nullptr;
   DevSched sa, st;
+  // column-blocked phase B (loop_kernel_stream_cb): A's leading / trailing
+  // column blocks as CSR with their schedules, and the leading block's row sums
+  int colblock = 0;
+  int* cb_ptr[2] = {nullptr, nullptr};
+  int* cb_idx[2] = {nullptr, nullptr};
+  double* cb_val[2] = {nullptr, nullptr};
+  DevSched sb0, sb1;
+  double* bpart = nullptr;
   double* xpool = nullptr;
   double* ypool = nullptr;
   double* axpool = nullptr;
@@ -2988,6 +3025,16 @@ void free_problem(hx_ctx* c) {
   free_sched(c->st);
   free_sched(c->pa);
   free_sched(c->pt);
+  free_sched(c->sb0);
+  free_sched(c->sb1);
+  for (int k = 0; k < 2; ++k) {
+    dfree(c->cb_ptr[k]), dfree(c->cb_idx[k]), dfree(c->cb_val[k]);
+    c->cb_ptr[k] = c->cb_idx[k] = nullptr;
+    c->cb_val[k] = nullptr;
+  }
+  dfree(c->bpart);
+  c->bpart = nullptr;
+  c->colblock = 0;
   c->a_ptr = c->a_idx = c->t_ptr = c->t_idx = nullptr;
   c->a_val = c->t_val = c->b = c->c = c->xpool = c->ypool = c->axpool = c->upool = nullptr;
   c->uploaded = c->setup_done = false;
@@ -3085,6 +3132,9 @@ KParams params(hx_ctx* c) {
   P.epochs = c->epochs;
   P.prof = c->prof;
   P.xavg = c->xavg, P.tavg = c->tavg, P.yavg = c->yavg, P.aavg = c->aavg, P.xbar = c->xbar;
+  P.A0 = c->sb0.view;
+  P.A1 = c->sb1.view;
+  P.bpart = c->bpart;
   return P;
 }
 
@@ -3093,13 +3143,15 @@ int launch_loop(hx_ctx* c) {
   void* args[] = {&P};
   HX_CUDA(c, cudaMemcpyAsync(c->ctl, &c->h, sizeof(Ctl), cudaMemcpyHostToDevice, c->stream));
   HX_CUDA(c, cudaMemsetAsync(c->bar, 0, sizeof(GridBar), c->stream));
-  for (DevSched* d : {&c->sa, &c->st})  // long-row flags restart with the per-launch sequence
+  for (DevSched* d : {&c->sa, &c->st, &c->sb0, &c->sb1})  // long-row flags restart with the per-launch sequence
     if (d->view.n_long)
       HX_CUDA(c, cudaMemsetAsync(d->flags, 0, 4 * static_cast<size_t>(d->view.n_long) * sizeof(unsigned long long),
                                  c->stream));
   const void* kernel = c->h.mode == kModeLoop && c->h.scheme != HPLP_SCHEME_RHPDHG
                            ? reinterpret_cast<const void*>(loop_kernel_baseline)
                            : c->ub                     ? reinterpret_cast<const void*>(loop_kernel_box)
+                           : c->sa.view.stream_hint && c->colblock && c->h.mode == kModeLoop
+                               ? reinterpret_cast<const void*>(loop_kernel_stream_cb)
                            : c->sa.view.stream_hint    ? reinterpret_cast<const void*>(loop_kernel_stream)
                                                        : reinterpret_cast<const void*>(loop_kernel);
   HX_CUDA(c, cudaLaunchCooperativeKernel(kernel, dim3(c->grid), dim3(kThreads), args, kStageBytes, c->stream));
@@ -3313,6 +3365,8 @@ int hx_create(int32_t device, hx_ctx** out) {
   HX_CUDA(nullptr, cudaFuncSetAttribute(loop_kernel_box, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(kStageBytes)));
   HX_CUDA(nullptr, cudaFuncSetAttribute(loop_kernel_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kStageBytes)));
+  HX_CUDA(nullptr, cudaFuncSetAttribute(loop_kernel_stream_cb, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(kStageBytes)));
   int occ = 0;
   HX_CUDA(nullptr, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, loop_kernel, kThreads, kStageBytes));
@@ -3563,6 +3617,60 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     c->sa.view.row_limit = c->pa.view.row_limit = static_cast<int>(m);  // output dimension (HX_CHECKED)
     c->st.view.row_limit = c->pt.view.row_limit = static_cast<int>(n);
     c->pa.view.stream_hint = c->pt.view.stream_hint = hint;
+    // Column-blocked phase B (loop_kernel_stream_cb): when x+ is far larger
+    // than L2 its random gathers miss (configs[4]: 9.5 GB of DRAM traffic per
+    // iteration against 5.0 GB algorithmic, L2 hit rate 38%), so A is split at
+    // the column that halves its nonzeros and phase B sweeps the two blocks
+    // one after the other (a grid barrier between), each sweep gathering from
+    // half of x+.  Auto when 8 n > 64 MB on the stream path; HX_COLBLOCK=0/1
+    // forces.  Row sums become (leading block) + (trailing block), each in
+    // ascending column order.
+    int want = hint && 8.0 * static_cast<double>(n) > 64e6 ? 1 : 0;
+    if (const char* e = std::getenv("HX_COLBLOCK")) want = std::atoi(e) != 0 ? 1 : 0;
+    if (want && !c->ranked && nnz > 0) {
+      std::vector<int> pt(static_cast<size_t>(n) + 1);
+      HX_CUDA(c, cudaMemcpy(pt.data(), c->t_ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+      const int split = static_cast<int>(std::lower_bound(pt.begin(), pt.end(), static_cast<int>(nnz / 2)) - pt.begin());
+      std::vector<int> p0(static_cast<size_t>(m) + 1, 0), p1(static_cast<size_t>(m) + 1, 0);
+      for (int64_t i = 0; i < m; ++i) {
+        const int32_t* rb = col_idx + row_ptr[i];
+        const int32_t* re = col_idx + row_ptr[i + 1];
+        const int k = static_cast<int>(std::lower_bound(rb, re, split) - rb);
+        p0[i + 1] = p0[i] + k;
+        p1[i + 1] = p1[i] + static_cast<int>(re - rb) - k;
+      }
+      std::vector<int> i0(static_cast<size_t>(p0[m])), i1(static_cast<size_t>(p1[m]));
+      std::vector<double> v0(i0.size()), v1(i1.size());
+      for (int64_t i = 0; i < m; ++i) {
+        const int64_t a = row_ptr[i], k = p0[i + 1] - p0[i], l = row_ptr[i + 1] - a - k;
+        std::copy(col_idx + a, col_idx + a + k, i0.begin() + p0[i]);
+        std::copy(val + a, val + a + k, v0.begin() + p0[i]);
+        std::copy(col_idx + a + k, col_idx + a + k + l, i1.begin() + p1[i]);
+        std::copy(val + a + k, val + a + k + l, v1.begin() + p1[i]);
+      }
+      const std::vector<int>* ps[2] = {&p0, &p1};
+      const std::vector<int>* is[2] = {&i0, &i1};
+      const std::vector<double>* vs[2] = {&v0, &v1};
+      DevSched* ds[2] = {&c->sb0, &c->sb1};
+      for (int k = 0; k < 2; ++k) {
+        const size_t nz = is[k]->size();
+        HX_CUDA(c, dalloc(&c->cb_ptr[k], static_cast<size_t>(m) + 1));
+        HX_CUDA(c, dalloc(&c->cb_idx[k], nz + kMatrixPad));
+        HX_CUDA(c, dalloc(&c->cb_val[k], nz + kMatrixPad));
+        HX_CUDA(c, cudaMemcpy(c->cb_ptr[k], ps[k]->data(), (m + 1) * sizeof(int), cudaMemcpyHostToDevice));
+        if (nz) {
+          HX_CUDA(c, cudaMemcpy(c->cb_idx[k], is[k]->data(), nz * sizeof(int), cudaMemcpyHostToDevice));
+          HX_CUDA(c, cudaMemcpy(c->cb_val[k], vs[k]->data(), nz * sizeof(double), cudaMemcpyHostToDevice));
+        }
+        const int rc = upload_sched(c, *ds[k], ps[k]->data(), static_cast<int>(m), static_cast<int>(n), c->cb_ptr[k],
+                                    c->cb_idx[k], c->cb_val[k]);
+        if (rc) return rc;
+        ds[k]->view.stream_hint = hint;
+        ds[k]->view.row_limit = static_cast<int>(m);
+      }
+      HX_CUDA(c, dalloc(&c->bpart, static_cast<size_t>(std::max<int64_t>(m, 1))));
+      c->colblock = 1;
+    }
   }
   tick("schedules");
   if (c->ranked) {  // peers map these through CUDA IPC
@@ -3672,7 +3780,7 @@ int hx_precondition(hx_ctx* c, int32_t ruiz_iters, double pc_alpha, double* row_
 // form.  Set after hx_upload_csr and before hx_precondition / hx_setup.
 int32_t hx_loop_variant(hx_ctx* c) {
   if (!c || !c->uploaded) return -1;
-  return c->ub ? 2 : c->sa.view.stream_hint ? 1 : 0;
+  return c->ub ? 2 : c->sa.view.stream_hint ? (c->colblock ? 3 : 1) : 0;
 }
 
 int hx_set_box(hx_ctx* c, const double* upper) {

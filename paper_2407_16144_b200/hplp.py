@@ -426,7 +426,7 @@ class HX:
         lib().hx_device_info(self.h, C.byref(sm), C.byref(g), C.byref(t))
         return dict(sm_count=sm.value, grid=g.value, threads=t.value)
 
-    LOOP_KERNELS = ("hx::loop_kernel", "hx::loop_kernel_stream", "hx::loop_kernel_box")
+    LOOP_KERNELS = ("hx::loop_kernel", "hx::loop_kernel_stream", "hx::loop_kernel_box", "hx::loop_kernel_stream_cb")
 
     def loop_kernel(self) -> str:
         """Name of the loop kernel hx_run launches for this problem."""

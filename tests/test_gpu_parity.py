@@ -300,3 +300,32 @@ def test_ragged_structure_team_parity(gpu_required):
     gpu = t.solve(iteration_limit=60, tolerance=1e-12, trace=True)
     t.close()
     _trace_cmp(gpu["trace"], cpu["trace"])
+
+
+@pytest.mark.parametrize("name", ["cfg1_small", "zipf_small", "ragged"])
+def test_column_blocked_phase_b_parity(gpu_required, name, monkeypatch):
+    """loop_kernel_stream_cb (phase B swept in two column blocks, the path
+    configs[4] takes; forced here with HX_COLBLOCK=1 on the stream kernel):
+    first 100 iterates within 1e-10 of the oracle, same restarts and SpMV
+    counts, then a solve to 1e-4 with the same status and objective."""
+    monkeypatch.setenv("HX_COLBLOCK", "1")
+    monkeypatch.setenv("HPLP_L2_STREAM", "1")
+    args = _ragged_lp() if name == "ragged" else csr_args(std(name)[1])
+    cpu = CpuLp("port", *args).solve(iteration_limit=100, tolerance=1e-12, trace=True)
+    sol = hplp.Solver(*args)
+    assert sol.hx.loop_kernel() == "hx::loop_kernel_stream_cb"
+    gpu = sol.solve(iteration_limit=100, tolerance=1e-12, trace=True)
+    _trace_cmp(gpu["trace"], cpu["trace"])
+    assert gpu["spmv_count"] == cpu["spmv_count"]
+    assert [e[:2] for e in gpu["epochs"]] == [e[:2] for e in cpu["epochs"]]
+    if name != "ragged":  # to 1e-4 against the unblocked kernel
+        g4 = sol.solve(iteration_limit=300000, tolerance=1e-4)
+        monkeypatch.setenv("HX_COLBLOCK", "0")
+        ref = hplp.Solver(*args)
+        assert ref.hx.loop_kernel() == "hx::loop_kernel_stream"
+        r4 = ref.solve(iteration_limit=300000, tolerance=1e-4)
+        ref.close()
+        assert g4["status"] == r4["status"]
+        c = args[6]
+        assert abs(float(c @ g4["x"]) - float(c @ r4["x"])) <= 1e-4 * max(1.0, abs(float(c @ r4["x"])))
+    sol.close()
