@@ -42,6 +42,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -3543,16 +3544,22 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   {
     std::vector<int> pt(static_cast<size_t>(n) + 1);
     HX_CUDA(c, cudaMemcpy(pt.data(), c->t_ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost));
-    int rc = upload_built_sched(c, c->sa, sched_a.get(), static_cast<int>(m), static_cast<int>(n), c->a_ptr,
-                                c->a_idx, c->a_val, 0);
-    if (rc) return rc;
     // phase A (rows of A^T) runs speculatively while warp 0 of every CTA runs
     // the controller: warp 0 starts with a lead of about the controller's
     // latency, in schedule cost units (~100 per microsecond on B200)
     double lead = 1200.0;
     if (const char* e = std::getenv("HX_LEAD")) lead = std::atof(e);
-    rc = upload_sched(c, c->st, pt.data(), static_cast<int>(n), static_cast<int>(m), c->t_ptr, c->t_idx, c->t_val,
-                      lead, 0, true);
+    // A^T's schedule is built on a host thread while A's uploads
+    auto sched_t = std::async(std::launch::async, [&pt, n, sched_warps, lead] {
+      double rc, tc;
+      sched_costs(true, rc, tc);
+      return build_schedule(pt.data(), static_cast<int>(n), sched_warps, lead, rc, tc);
+    });
+    int rc = upload_built_sched(c, c->sa, sched_a.get(), static_cast<int>(m), static_cast<int>(n), c->a_ptr,
+                                c->a_idx, c->a_val, 0);
+    if (rc) return rc;
+    rc = upload_built_sched(c, c->st, sched_t.get(), static_cast<int>(n), static_cast<int>(m), c->t_ptr, c->t_idx,
+                            c->t_val, 0);
     if (rc) return rc;
     if (c->ranked) {  // this rank's blocks: rows [row0,row1) of A, [col0,col1) of A^T
       Team& T = c->team;
@@ -3631,27 +3638,48 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
       std::vector<int> pt(static_cast<size_t>(n) + 1);
       HX_CUDA(c, cudaMemcpy(pt.data(), c->t_ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost));
       const int split = static_cast<int>(std::lower_bound(pt.begin(), pt.end(), static_cast<int>(nnz / 2)) - pt.begin());
+      // rows split on host threads: per-row counts, a prefix sum, then copies
+      const unsigned nth = std::clamp(std::thread::hardware_concurrency(), 1u, 16u);
+      auto par_rows = [&](auto&& f) {
+        std::vector<std::thread> pool;
+        for (unsigned t = 1; t < nth; ++t) pool.emplace_back(f, m * t / nth, m * (t + 1) / nth);
+        f(int64_t{0}, m / nth);
+        for (auto& th : pool) th.join();
+      };
       std::vector<int> p0(static_cast<size_t>(m) + 1, 0), p1(static_cast<size_t>(m) + 1, 0);
-      for (int64_t i = 0; i < m; ++i) {
-        const int32_t* rb = col_idx + row_ptr[i];
-        const int32_t* re = col_idx + row_ptr[i + 1];
-        const int k = static_cast<int>(std::lower_bound(rb, re, split) - rb);
-        p0[i + 1] = p0[i] + k;
-        p1[i + 1] = p1[i] + static_cast<int>(re - rb) - k;
-      }
+      par_rows([&](int64_t lo, int64_t hi) {
+        for (int64_t i = lo; i < hi; ++i) {
+          const int32_t* rb = col_idx + row_ptr[i];
+          const int32_t* re = col_idx + row_ptr[i + 1];
+          const int k = static_cast<int>(std::lower_bound(rb, re, split) - rb);
+          p0[i + 1] = k;
+          p1[i + 1] = static_cast<int>(re - rb) - k;
+        }
+      });
+      for (int64_t i = 0; i < m; ++i) p0[i + 1] += p0[i], p1[i + 1] += p1[i];
       std::vector<int> i0(static_cast<size_t>(p0[m])), i1(static_cast<size_t>(p1[m]));
       std::vector<double> v0(i0.size()), v1(i1.size());
-      for (int64_t i = 0; i < m; ++i) {
-        const int64_t a = row_ptr[i], k = p0[i + 1] - p0[i], l = row_ptr[i + 1] - a - k;
-        std::copy(col_idx + a, col_idx + a + k, i0.begin() + p0[i]);
-        std::copy(val + a, val + a + k, v0.begin() + p0[i]);
-        std::copy(col_idx + a + k, col_idx + a + k + l, i1.begin() + p1[i]);
-        std::copy(val + a + k, val + a + k + l, v1.begin() + p1[i]);
-      }
+      par_rows([&](int64_t lo, int64_t hi) {
+        for (int64_t i = lo; i < hi; ++i) {
+          const int64_t a = row_ptr[i], k = p0[i + 1] - p0[i], l = row_ptr[i + 1] - a - k;
+          std::copy(col_idx + a, col_idx + a + k, i0.begin() + p0[i]);
+          std::copy(val + a, val + a + k, v0.begin() + p0[i]);
+          std::copy(col_idx + a + k, col_idx + a + k + l, i1.begin() + p1[i]);
+          std::copy(val + a + k, val + a + k + l, v1.begin() + p1[i]);
+        }
+      });
       const std::vector<int>* ps[2] = {&p0, &p1};
       const std::vector<int>* is[2] = {&i0, &i1};
       const std::vector<double>* vs[2] = {&v0, &v1};
       DevSched* ds[2] = {&c->sb0, &c->sb1};
+      // both blocks' schedules are built on host threads while the blocks upload
+      std::future<SchedHost> sb[2];
+      for (int k = 0; k < 2; ++k)
+        sb[k] = std::async(std::launch::async, [pk = ps[k], m, sched_warps] {
+          double rc, tc;
+          sched_costs(false, rc, tc);
+          return build_schedule(pk->data(), static_cast<int>(m), sched_warps, 0.0, rc, tc);
+        });
       for (int k = 0; k < 2; ++k) {
         const size_t nz = is[k]->size();
         HX_CUDA(c, dalloc(&c->cb_ptr[k], static_cast<size_t>(m) + 1));
@@ -3662,8 +3690,10 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
           HX_CUDA(c, cudaMemcpy(c->cb_idx[k], is[k]->data(), nz * sizeof(int), cudaMemcpyHostToDevice));
           HX_CUDA(c, cudaMemcpy(c->cb_val[k], vs[k]->data(), nz * sizeof(double), cudaMemcpyHostToDevice));
         }
-        const int rc = upload_sched(c, *ds[k], ps[k]->data(), static_cast<int>(m), static_cast<int>(n), c->cb_ptr[k],
-                                    c->cb_idx[k], c->cb_val[k]);
+      }
+      for (int k = 0; k < 2; ++k) {
+        const int rc = upload_built_sched(c, *ds[k], sb[k].get(), static_cast<int>(m), static_cast<int>(n),
+                                          c->cb_ptr[k], c->cb_idx[k], c->cb_val[k], 0);
         if (rc) return rc;
         ds[k]->view.stream_hint = hint;
         ds[k]->view.row_limit = static_cast<int>(m);
