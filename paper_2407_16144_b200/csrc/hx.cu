@@ -2783,6 +2783,41 @@ __global__ void row_of_kernel(int m, const int* rp, int* row_of, int* iota) {
     }
 }
 
+// Column blocks of A (column-blocked phase B): per row, the split point in
+// its ascending columns, then the two halves copied to their CSR arrays (one
+// warp per row).  cnt0 / cnt1 have m + 1 entries, [0] = 0, so an inclusive
+// scan gives the row pointers.
+__global__ void split_count_kernel(int m, const int* ptr, const int* idx, int split, int* cnt0, int* cnt1) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const int lo = ptr[i], hi = ptr[i + 1];
+    int a = lo, b = hi;
+    while (a < b) {
+      const int mid = (a + b) >> 1;
+      if (idx[mid] < split) a = mid + 1;
+      else b = mid;
+    }
+    cnt0[i + 1] = a - lo;
+    cnt1[i + 1] = hi - a;
+  }
+}
+
+__global__ void split_copy_kernel(int m, const int* ptr, const int* idx, const double* val, const int* p0,
+                                  const int* p1, int* i0, double* v0, int* i1, double* v1) {
+  const int lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < m; i += (gridDim.x * blockDim.x) >> 5) {
+    const int a = ptr[i], len = ptr[i + 1] - a, k = p0[i + 1] - p0[i];
+    for (int q = lane; q < len; q += 32) {
+      if (q < k) {
+        i0[p0[i] + q] = idx[a + q];
+        v0[p0[i] + q] = val[a + q];
+      } else {
+        i1[p1[i] + q - k] = idx[a + q];
+        v1[p1[i] + q - k] = val[a + q];
+      }
+    }
+  }
+}
+
 __global__ void col_count_kernel(int nnz, const int* ci, int* count) {
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += gridDim.x * blockDim.x)
     atomicAdd(count + ci[p], 1);
@@ -3558,9 +3593,11 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     int rc = upload_built_sched(c, c->sa, sched_a.get(), static_cast<int>(m), static_cast<int>(n), c->a_ptr,
                                 c->a_idx, c->a_val, 0);
     if (rc) return rc;
+    tick("sched A");
     rc = upload_built_sched(c, c->st, sched_t.get(), static_cast<int>(n), static_cast<int>(m), c->t_ptr, c->t_idx,
                             c->t_val, 0);
     if (rc) return rc;
+    tick("sched A^T");
     if (c->ranked) {  // this rank's blocks: rows [row0,row1) of A, [col0,col1) of A^T
       Team& T = c->team;
       if (T.row1 > m || T.col1 > n)
@@ -3638,41 +3675,40 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
       std::vector<int> pt(static_cast<size_t>(n) + 1);
       HX_CUDA(c, cudaMemcpy(pt.data(), c->t_ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost));
       const int split = static_cast<int>(std::lower_bound(pt.begin(), pt.end(), static_cast<int>(nnz / 2)) - pt.begin());
-      // rows split on host threads: per-row counts, a prefix sum, then copies
-      const unsigned nth = std::clamp(std::thread::hardware_concurrency(), 1u, 16u);
-      auto par_rows = [&](auto&& f) {
-        std::vector<std::thread> pool;
-        for (unsigned t = 1; t < nth; ++t) pool.emplace_back(f, m * t / nth, m * (t + 1) / nth);
-        f(int64_t{0}, m / nth);
-        for (auto& th : pool) th.join();
-      };
-      std::vector<int> p0(static_cast<size_t>(m) + 1, 0), p1(static_cast<size_t>(m) + 1, 0);
-      par_rows([&](int64_t lo, int64_t hi) {
-        for (int64_t i = lo; i < hi; ++i) {
-          const int32_t* rb = col_idx + row_ptr[i];
-          const int32_t* re = col_idx + row_ptr[i + 1];
-          const int k = static_cast<int>(std::lower_bound(rb, re, split) - rb);
-          p0[i + 1] = k;
-          p1[i + 1] = static_cast<int>(re - rb) - k;
-        }
-      });
-      for (int64_t i = 0; i < m; ++i) p0[i + 1] += p0[i], p1[i + 1] += p1[i];
-      std::vector<int> i0(static_cast<size_t>(p0[m])), i1(static_cast<size_t>(p1[m]));
-      std::vector<double> v0(i0.size()), v1(i1.size());
-      par_rows([&](int64_t lo, int64_t hi) {
-        for (int64_t i = lo; i < hi; ++i) {
-          const int64_t a = row_ptr[i], k = p0[i + 1] - p0[i], l = row_ptr[i + 1] - a - k;
-          std::copy(col_idx + a, col_idx + a + k, i0.begin() + p0[i]);
-          std::copy(val + a, val + a + k, v0.begin() + p0[i]);
-          std::copy(col_idx + a + k, col_idx + a + k + l, i1.begin() + p1[i]);
-          std::copy(val + a + k, val + a + k + l, v1.begin() + p1[i]);
-        }
-      });
+      // the blocks are cut on the device (the matrix is resident); only their
+      // row pointers come back for the host schedules
+      int* cnt[2] = {nullptr, nullptr};
+      for (int k = 0; k < 2; ++k) {
+        HX_CUDA(c, dalloc(&cnt[k], static_cast<size_t>(m) + 1));
+        HX_CUDA(c, cudaMemsetAsync(cnt[k], 0, sizeof(int), s));
+        HX_CUDA(c, dalloc(&c->cb_ptr[k], static_cast<size_t>(m) + 1));
+      }
+      split_count_kernel<<<nblk, 256, 0, s>>>(static_cast<int>(m), c->a_ptr, c->a_idx, split, cnt[0], cnt[1]);
+      size_t scan_bytes = 0;
+      cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, cnt[0], c->cb_ptr[0], static_cast<int>(m + 1), s);
+      unsigned char* scan_tmp = nullptr;
+      HX_CUDA(c, dalloc(&scan_tmp, std::max<size_t>(1, scan_bytes)));
+      for (int k = 0; k < 2; ++k)
+        HX_CUDA(c, cub::DeviceScan::InclusiveSum(scan_tmp, scan_bytes, cnt[k], c->cb_ptr[k], static_cast<int>(m + 1), s));
+      std::vector<int> p0(static_cast<size_t>(m) + 1), p1(static_cast<size_t>(m) + 1);
+      HX_CUDA(c, cudaMemcpyAsync(p0.data(), c->cb_ptr[0], (m + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+      HX_CUDA(c, cudaMemcpyAsync(p1.data(), c->cb_ptr[1], (m + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+      HX_CUDA(c, cudaStreamSynchronize(s));
+      for (int k = 0; k < 2; ++k) {
+        const size_t nz = static_cast<size_t>((k == 0 ? p0 : p1)[m]);
+        HX_CUDA(c, dalloc(&c->cb_idx[k], nz + kMatrixPad));
+        HX_CUDA(c, dalloc(&c->cb_val[k], nz + kMatrixPad));
+      }
+      split_copy_kernel<<<nblk, 256, 0, s>>>(static_cast<int>(m), c->a_ptr, c->a_idx, c->a_val, c->cb_ptr[0],
+                                             c->cb_ptr[1], c->cb_idx[0], c->cb_val[0], c->cb_idx[1], c->cb_val[1]);
+      HX_CUDA(c, cudaStreamSynchronize(s));
+      HX_CUDA(c, cudaGetLastError());
+      c->launches += 4;
+      dfree(cnt[0]), dfree(cnt[1]), dfree(scan_tmp);
+      tick("cb split");
       const std::vector<int>* ps[2] = {&p0, &p1};
-      const std::vector<int>* is[2] = {&i0, &i1};
-      const std::vector<double>* vs[2] = {&v0, &v1};
       DevSched* ds[2] = {&c->sb0, &c->sb1};
-      // both blocks' schedules are built on host threads while the blocks upload
+      // both blocks' schedules are built concurrently on host threads
       std::future<SchedHost> sb[2];
       for (int k = 0; k < 2; ++k)
         sb[k] = std::async(std::launch::async, [pk = ps[k], m, sched_warps] {
@@ -3680,17 +3716,6 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
           sched_costs(false, rc, tc);
           return build_schedule(pk->data(), static_cast<int>(m), sched_warps, 0.0, rc, tc);
         });
-      for (int k = 0; k < 2; ++k) {
-        const size_t nz = is[k]->size();
-        HX_CUDA(c, dalloc(&c->cb_ptr[k], static_cast<size_t>(m) + 1));
-        HX_CUDA(c, dalloc(&c->cb_idx[k], nz + kMatrixPad));
-        HX_CUDA(c, dalloc(&c->cb_val[k], nz + kMatrixPad));
-        HX_CUDA(c, cudaMemcpy(c->cb_ptr[k], ps[k]->data(), (m + 1) * sizeof(int), cudaMemcpyHostToDevice));
-        if (nz) {
-          HX_CUDA(c, cudaMemcpy(c->cb_idx[k], is[k]->data(), nz * sizeof(int), cudaMemcpyHostToDevice));
-          HX_CUDA(c, cudaMemcpy(c->cb_val[k], vs[k]->data(), nz * sizeof(double), cudaMemcpyHostToDevice));
-        }
-      }
       for (int k = 0; k < 2; ++k) {
         const int rc = upload_built_sched(c, *ds[k], sb[k].get(), static_cast<int>(m), static_cast<int>(n),
                                           c->cb_ptr[k], c->cb_idx[k], c->cb_val[k], 0);
