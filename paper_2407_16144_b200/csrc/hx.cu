@@ -1076,7 +1076,12 @@ __device__ bool grid_sync(GridBar* bar, unsigned long long& target) {
     unsigned spins = 0;
     // acquire (SASS: LDG.STRONG.GPU + CCTL.IVALL): later reads, L1-cached
     // ones included, see every CTA's released writes
+#if HX_BAR_RELAXED
+    // relaxed polls (no L1 invalidation per poll), one acquire load at the end
+    while (*reinterpret_cast<volatile unsigned long long*>(&bar->count) < target) {
+#else
     while (ld_acquire_u64(&bar->count) < target) {
+#endif
       if ((++spins & 255u) == 0u) {
         if (*reinterpret_cast<volatile unsigned*>(&bar->abort)) {
           s_ok = 0;
@@ -1089,6 +1094,9 @@ __device__ bool grid_sync(GridBar* bar, unsigned long long& target) {
         }
       }
     }
+#if HX_BAR_RELAXED
+    (void)ld_acquire_u64(&bar->count);
+#endif
   }
   __syncthreads();
   return s_ok != 0;
