@@ -1074,8 +1074,8 @@ __device__ bool grid_sync(GridBar* bar, unsigned long long& target) {
     asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(&bar->count), "l"(1ull) : "memory");
     const unsigned long long t0 = global_ns();
     unsigned spins = 0;
-    // acquire (SASS: LDG.STRONG.GPU + CCTL.IVALL): later reads, L1-cached
-    // ones included, see every CTA's released writes
+    // poll, then acquire (SASS: LDG.STRONG.GPU + CCTL.IVALL): later reads,
+    // L1-cached ones included, see every CTA's released writes
 #if HX_BAR_RELAXED
     // relaxed polls (no L1 invalidation per poll), one acquire load at the end
     while (*reinterpret_cast<volatile unsigned long long*>(&bar->count) < target) {
