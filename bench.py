@@ -160,41 +160,98 @@ def loop_seconds(lp, iters: int) -> float:
     return t1 - t0
 
 
-def cpu_iters_per_sec(s, iters: int):
+def host_cpu():
+    """The box's host CPU: model name and logical core count."""
+    model = "unknown"
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count() or 1
+
+
+class PinnedToCore0:
+    """taskset -c 0 for the CPU reference (it is single-threaded):
+    the process is pinned to core 0 inside the block, then restored."""
+
+    def __enter__(self):
+        self.old = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, {min(self.old)})
+        return self
+
+    def __exit__(self, *exc):
+        os.sched_setaffinity(0, self.old)
+
+
+def cpu_lp(cid: int):
+    """The instance as the CPU reference itself builds it: the generator's
+    general form through the REFERENCE's own to_standard_form
+    (src/lp_model.cpp:155-325) -- no product library on this path."""
     import oracle
+    from paper_2407_16144_b200 import gen
 
     kind = "reference" if oracle.available("reference") else "port"
-    lp = oracle.CpuLp(kind, *s.csr())
+    g = gen.generate(cid)
+    std = oracle.CpuStd(kind, g.as_abi())
+    return kind, g, std, std.lp()
+
+
+def cpu_iters_per_sec(lp, kind, iters: int):
     sigma, pit, conv, t_power = lp.power_iteration()
     loop_s = loop_seconds(lp, iters)
-    return kind, iters / loop_s, dict(power_iterations=pit, power_seconds=t_power, solve_wall_s=loop_s)
+    return iters / loop_s, dict(power_iterations=pit, power_seconds=t_power, solve_wall_s=loop_s)
+
+
+def cpu_time_to_tol(rate_cfg1: float, power_s_cfg1: float, gpu_iters_cfg1):
+    """CPU wall time to relative KKT <= 1e-4 (SolveTotals.wall_seconds,
+    src/solver.cpp:207,238): measured on configs[0]; configs[1] extrapolated
+    (its 1e-4 solve is ~747k iterations, hours on one core) as the iteration
+    count of the same algorithm on the device / the measured CPU it/s + the
+    measured power-iteration time -- labelled as an extrapolation."""
+    model, ncpu = host_cpu()
+    out = {}
+    kind, g, std, lp = cpu_lp(0)
+    r = lp.solve(tolerance=1e-4, iteration_limit=1_000_000)
+    out["configs[0]"] = {"status": r["status"], "seconds": r["wall_seconds"], "iterations": r["iterations"],
+                         "kind": kind, "measured": True}
+    if gpu_iters_cfg1:
+        out["configs[1]"] = {"seconds": gpu_iters_cfg1 / rate_cfg1 + power_s_cfg1, "iterations": gpu_iters_cfg1,
+                             "measured": False,
+                             "extrapolation": "iterations of the device's 1e-4 solve (same algorithm, same "
+                                              "restart sequence) / measured CPU it/s + measured power iteration"}
+    out["cores"] = f"1 of {ncpu} ({model}), taskset core 0"
+    return out
 
 
 def run_reference(args):
     world, rank, local = dist_setup()
     if rank != 0:
         return 0
-    import oracle
-
-    g, s = build_problem()
-    kind = "reference" if oracle.available("reference") else "port"
-    lp = oracle.CpuLp(kind, *s.csr())
-    iters = args.ref_iters
-    sigma, pit, conv, t_power = lp.power_iteration()
-    for _ in range(args.warmup):
-        lp.solve(iteration_limit=max(1, iters // 5), tolerance=1e-4)
-    loop_times = [loop_seconds(lp, iters) for _ in range(args.steps)]
+    model, ncpu = host_cpu()
+    with PinnedToCore0():
+        kind, g, std, lp = cpu_lp(CONFIG_ID)
+        iters = args.ref_iters
+        sigma, pit, conv, t_power = lp.power_iteration()
+        for _ in range(args.warmup):
+            lp.solve(iteration_limit=max(1, iters // 5), tolerance=1e-4)
+        loop_times = [loop_seconds(lp, iters) for _ in range(args.steps)]
     total = sum(loop_times)
     value = iters * args.steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "device": "cpu", "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": f"synthetic (seeded, BASELINE configs[{CONFIG_ID}])",
-        "config": {"workload": f"{WORKLOADS[CONFIG_ID]}, standard form {s.m}x{s.n}, nnz {s.nnz}",
+        "config": {"workload": f"{WORKLOADS[CONFIG_ID]}, standard form {std.m}x{std.n}, nnz {std.nnz}",
                    "iters_per_step": iters, "parallelism": "none (single-threaded reference)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind,
-                         "sample": f"{args.steps} x solve(iteration_limit={iters}) on configs[{CONFIG_ID}]; power iteration "
-                                   f"({pit} its, {t_power:.2f}s): a zero-iteration solve's wall time subtracted"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "cores_of": ncpu, "cpu_model": model,
+                         "kind": kind,
+                         "sample": f"{args.steps} x solve(iteration_limit={iters}) on configs[{CONFIG_ID}] built by the "
+                                   f"reference's own to_standard_form, pinned to core 0 (1 of {ncpu}); power "
+                                   f"iteration ({pit} its, {t_power:.2f}s): a zero-iteration solve's wall time "
+                                   f"subtracted"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
@@ -218,41 +275,20 @@ def run_gpu(args):
     g, s = build_problem()
     m, n, nnz = s.m, s.n, s.nnz
     sharded = world > 1 or args.sharded
-    team_error = None
-    solver = None
     if sharded:
         from paper_2407_16144_b200 import team
 
-        # the row-partitioned team needs CUDA IPC + peer access between the
-        # ranks' GPUs; if any rank cannot join (or the team's first power
-        # iteration fails), every rank falls back to an independent replica of
-        # the LP so the run still reports a (weak-scaling) number, labelled
+        # the row-partitioned team (one LP over N GPUs); any failure on any
+        # rank fails the run on every rank (rc != 0) -- there is no fallback
+        solver = team.rank_solver(s, local)
+        err = None
         try:
-            if os.environ.get("BENCH_TEAM_FAIL"):  # test hook for the fallback
-                raise RuntimeError("BENCH_TEAM_FAIL set")
-            solver = team.rank_solver(s, local)
             solver.solve(iteration_limit=0)
-        except Exception as e:  # noqa: BLE001 -- reported in the JSON line
-            team_error = f"{type(e).__name__}: {e}"
-        if world > 1:
-            import torch.distributed as dist
-
-            flag = torch.tensor([1.0 if team_error else 0.0], device="cuda")
-            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
-            if flag.item() > 0 and team_error is None:
-                team_error = "a peer rank could not join the team"
-        if team_error is not None:
-            if solver is not None:
-                try:
-                    solver.close()
-                except Exception:  # noqa: BLE001
-                    pass
-            print(f"bench: row-partitioned team unavailable ({team_error}); running {world} independent replicas",
-                  file=sys.stderr)
-            sharded = False
-    if not sharded:
+        except Exception as e:  # noqa: BLE001 -- re-raised after the agreement
+            err = e
+        team.agree(err is None, "the first power iteration")
+    else:
         solver = hplp.Solver.from_std(s, device=local)
-    replicas = world if world > 1 and not sharded else 1  # independent copies of the LP (fallback only)
     hx = solver.hx
     stream = torch.cuda.ExternalStream(hx.stream(), device=torch.device("cuda", local))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -293,12 +329,12 @@ def run_gpu(args):
         t = torch.tensor([elapsed], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
-    value = replicas * iters_done / elapsed  # iterations of the one LP (all ranks work on it), or of all replicas
+    value = iters_done / elapsed  # iterations/s of the one LP (all ranks work on it)
     b_iter = algorithmic_bytes(m, n, nnz)
     peak, peak_kind = measured_peak()
-    peak *= world  # sharded (or replicas): the aggregate HBM of the N GPUs
+    peak *= world  # sharded: the aggregate HBM of the N GPUs
     per_launch_s = elapsed / args.steps
-    achieved = replicas * b_iter * ITERS_PER_STEP / per_launch_s / 1e9
+    achieved = b_iter * ITERS_PER_STEP / per_launch_s / 1e9
     traffic, prof = traffic_from_profile() if CONFIG_ID == 1 else (None, None)
 
     # e2e through the public C ABI from host buffers (upload + setup + loop + download)
@@ -327,7 +363,7 @@ def run_gpu(args):
 
         t = torch.tensor([statistics.median(e2e_times)], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_value = replicas * E2E_ITERS / float(t.item())
+        e2e_value = E2E_ITERS / float(t.item())
 
     # sharded runs check themselves: 200 iterations of the row-partitioned
     # solve against a single-GPU solve of the same LP on rank 0 (different
@@ -439,10 +475,20 @@ def run_gpu(args):
                                    "planted_objective": g.planted_objective, "settings": opts}
 
     cpu = None
+    cpu_ttt = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        kind, cval, info = cpu_iters_per_sec(s, args.cpu_iters)
-        cpu = {"value": cval, "unit": UNIT, "cores": 1, "kind": kind,
-               "sample": f"solve(iteration_limit={args.cpu_iters}) on configs[{CONFIG_ID}], single thread; power iteration "
+        model, ncpu = host_cpu()
+        with PinnedToCore0():
+            kind, _, _, lp = cpu_lp(CONFIG_ID)
+            cval, info = cpu_iters_per_sec(lp, kind, args.cpu_iters)
+            del lp
+            if CONFIG_ID == 1 and not args.no_ttt:
+                gi = ttt.get("configs[1]", {})
+                cpu_ttt = cpu_time_to_tol(cval, info["power_seconds"],
+                                          gi.get("iterations") if gi.get("status") == "optimal" else None)
+        cpu = {"value": cval, "unit": UNIT, "cores": 1, "cores_of": ncpu, "cpu_model": model, "kind": kind,
+               "sample": f"solve(iteration_limit={args.cpu_iters}) on configs[{CONFIG_ID}] (the reference's own "
+                         f"to_standard_form), pinned to core 0 (1 of {ncpu}); power iteration "
                          f"({info['power_iterations']} its, {info['power_seconds']:.2f}s): a zero-iteration solve's "
                          f"wall time subtracted"}
 
@@ -450,13 +496,12 @@ def run_gpu(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
-            "scaling": "strong" if replicas == 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": f"synthetic (seeded, BASELINE configs[{CONFIG_ID}]; MIPLIB not available)",
             "config": {"workload": f"{WORKLOADS[CONFIG_ID]}, standard form {m}x{n}, nnz {nnz}",
                        "iters_per_step": ITERS_PER_STEP, "l2": "flushed (256 MiB write) before every timed step",
-                       "parallelism": "single GPU" if world == 1 else
-                       f"row-partitioned x{world}: one LP, rows/columns split by nnz, slices pushed over NVLink P2P"
-                       if sharded else f"{world} independent replicas (team path unavailable: {team_error})"},
+                       "parallelism": "single GPU" if world == 1 and not sharded else
+                       f"row-partitioned x{world}: one LP, rows/columns split by nnz, slices pushed over NVLink P2P"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None if sharded else traffic,
                          "kernel": "hx::loop_kernel_team" if sharded else hx.loop_kernel(),
@@ -480,6 +525,7 @@ def run_gpu(args):
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "time_to_1e-4": ttt,
+            "cpu_time_to_1e-4": cpu_ttt,
             "box_form": box,
             "team_check": team_check,
             "per_step_ms": [round(1e3 * t, 3) for t in times],

@@ -848,7 +848,7 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
 // lane 0's accumulators -- a fixed order, so totals stay bit-reproducible.
 template <int Q, unsigned MaxMask>
 __device__ __forceinline__ void fold_long(const Sched& S, int set, unsigned long long seq, double (&acc)[Q],
-                                          int cta) {
+                                          int cta, unsigned* abort_flag) {
   if (S.n_long == 0 || threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
   const int b = __ldg(S.owned_ptr + cta), e = __ldg(S.owned_ptr + cta + 1);
@@ -859,7 +859,10 @@ __device__ __forceinline__ void fold_long(const Sched& S, int set, unsigned long
     const int k = __ldg(S.owned_idx + i);
     const unsigned long long t0 = global_ns();
     while (ld_acquire_u64(flags + k) < seq) {
-      if (global_ns() - t0 > 10000000000ull) break;  // watchdog (the barrier reports it)
+      if (global_ns() - t0 > 10000000000ull) {  // watchdog: raise the abort flag the next barrier reports
+        atomicExch(abort_flag, 1u);
+        break;
+      }
     }
     const double* lt = S.long_terms(set) + static_cast<long long>(k) * kMaxQ;
     double t[Q];
@@ -1158,6 +1161,7 @@ __device__ bool team_sync(GridBar* bar, const Team& T, const Geo& g, unsigned lo
     __syncthreads();
     if (s_ok) {
       // q 0..2: phase A, 3..6: phase B, 7: the box term (phase A's fourth)
+      static_assert(kThreads == 512, "the leader reduction below fills part[64][8] with 512 threads");
       const int q = threadIdx.x & 7, k = threadIdx.x >> 3;  // 512 threads: k < 64
       {
         const size_t stride = region_stride(g.nrec);
@@ -1597,13 +1601,13 @@ __device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R,
   if constexpr (!RK)
     if (P->prof && (threadIdx.x & 31) == 0) P->prof[gridDim.x * 16 + gwarp_id(g)] += clock64() - w0;
 #endif
-  fold_long<NQ, 0>(S, par, seq, acc, g.cta);
+  fold_long<NQ, 0>(S, par, seq, acc, g.cta, &P->bar->abort);
   block_to_slots<NQ, 0, RK>(acc, P, kRegA + par, g);
 }
 
 // phase B: A x+, dual step, speculative Halpern combos, dual partials
 template <bool RK, int LM = 2, bool CB = false>
-__device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int par, WarpStage* stage,
+__device__ HX_PHASE_INLINE bool phase_dual(const KParams* P, const Roles* R, int par, WarpStage* stage,
                                            unsigned long long seq, const SpmvHead& head, const Geo& g,
                                            unsigned long long* target = nullptr) {
   const int n = P->n, m = P->m;
@@ -1634,7 +1638,9 @@ __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int
     spmv_rows<1, 0, LM>(P->A0, par, SrcVecT<LM == 1 && HX_GATHER_LAST>{xsrc}, st0, a0, gwarp_id(g),
                         threadIdx.x & 31, stage, seq, head);
     spmv_head<LM>(P->A1, gwarp_id(g), threadIdx.x & 31, h1);
-    grid_sync(P->bar, *target);
+    // abort / watchdog: leave before sweep 2 (its long rows would wait on
+    // pieces that never come)
+    if (!grid_sync(P->bar, *target)) return false;
   }
   const Sched S = CB ? P->A1 : P->A;
 #ifdef HX_WPROF
@@ -1646,8 +1652,9 @@ __device__ HX_PHASE_INLINE void phase_dual(const KParams* P, const Roles* R, int
   if constexpr (!RK)
     if (P->prof && (threadIdx.x & 31) == 0) P->prof[gridDim.x * (16 + kWarps) + gwarp_id(g)] += clock64() - w0;
 #endif
-  fold_long<4, 0>(S, par, seq, acc, g.cta);
+  fold_long<4, 0>(S, par, seq, acc, g.cta, &P->bar->abort);
   block_to_slots<4, 0, RK>(acc, P, kRegB + par, g);
+  return true;
 }
 
 // Totals of phases A+B -> t[0..6], computed by warp 0 alone (the other warps
@@ -1712,7 +1719,7 @@ __device__ HX_PHASE_INLINE void power_a(const KParams* P, const Roles* R, WarpSt
   if (R->pw_mode == 0) spmv_rows<1, 0, LM>(S, 0, SrcVec{P->xpool}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
   else
     spmv_rows<1, 0, LM>(S, 0, SrcDiv{P->xpool + P->n, R->pw_zn}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
-  fold_long<1, 0>(S, 0, seq, acc, g.cta);
+  fold_long<1, 0>(S, 0, seq, acc, g.cta, &P->bar->abort);
   block_to_slots<1, 0, false>(acc, P, kRegPA, g);
 }
 
@@ -1723,7 +1730,7 @@ __device__ HX_PHASE_INLINE void power_b(const KParams* P, WarpStage* stage, unsi
   EpiStoreSq e{P->xpool + P->n};
   const Sched S = P->AT;
   spmv_rows<1, 0, LM>(S, 0, SrcVec{P->ypool}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
-  fold_long<1, 0>(S, 0, seq, acc, g.cta);
+  fold_long<1, 0>(S, 0, seq, acc, g.cta, &P->bar->abort);
   block_to_slots<1, 0, false>(acc, P, kRegPB, g);
 }
 
@@ -1863,7 +1870,7 @@ __device__ HX_PHASE_INLINE void cert_products(const KParams* P, const Roles* R, 
       acc_init<2, 3u>(a2);
       EpiPosNeg e;
       spmv_rows<2, 3u, LM>(AT, 2 + k, SrcVec{k ? u3 : u1}, e, a2, gw, lane, stage, seq);
-      fold_long<2, 3u>(AT, 2 + k, seq, a2, g.cta);
+      fold_long<2, 3u>(AT, 2 + k, seq, a2, g.cta, &P->bar->abort);
       acc[2 * k] = a2[0], acc[2 * k + 1] = a2[1];
     }
     if (R->cand_on[2 * k]) {
@@ -1871,7 +1878,7 @@ __device__ HX_PHASE_INLINE void cert_products(const KParams* P, const Roles* R, 
       acc_init<1, 1u>(a1);
       EpiAbs e;
       spmv_rows<1, 1u, LM>(A, 2 + k, SrcVec{k ? u2 : u0}, e, a1, gw, lane, stage, seq);
-      fold_long<1, 1u>(A, 2 + k, seq, a1, g.cta);
+      fold_long<1, 1u>(A, 2 + k, seq, a1, g.cta, &P->bar->abort);
       acc[4 + k] = a1[0];
     }
   }
@@ -2016,7 +2023,7 @@ __device__ HX_PHASE_INLINE void phase_primal_avg(const KParams* P, const Roles* 
                  R->w_avg,
                  R->avg_mode == 1};
   spmv_rows<3, 0>(P->AT, par, SrcVec{ycur_ptr(P, R)}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq, head);
-  fold_long<3, 0>(P->AT, par, seq, acc, g.cta);
+  fold_long<3, 0>(P->AT, par, seq, acc, g.cta, &P->bar->abort);
   block_to_slots<3, 0, false>(acc, P, kRegA + par, g);
 }
 
@@ -2040,7 +2047,7 @@ __device__ HX_PHASE_INLINE void phase_dual_avg(const KParams* P, const Roles* R,
                R->avg_mode == 1};
   spmv_rows<4, 0>(P->A, par, SrcVec{P->xpool + static_cast<size_t>(R->xp_out) * n}, e, acc, gwarp_id(g),
                   threadIdx.x & 31, stage, seq, head);
-  fold_long<4, 0>(P->A, par, seq, acc, g.cta);
+  fold_long<4, 0>(P->A, par, seq, acc, g.cta, &P->bar->abort);
   block_to_slots<4, 0, false>(acc, P, kRegB + par, g);
 }
 
@@ -2052,7 +2059,7 @@ __device__ HX_PHASE_INLINE void phase_avgstep_a(const KParams* P, const Roles* R
   EpiAvgStepPrimal e{P->xavg + static_cast<size_t>(R->avg_out) * n, P->c, P->xbar, R->eta};
   spmv_rows<1, 0>(P->AT, 0, SrcVec{P->yavg + static_cast<size_t>(R->avg_out) * m}, e, acc, gwarp_id(g),
                   threadIdx.x & 31, stage, seq);
-  fold_long<1, 0>(P->AT, 0, seq, acc, g.cta);
+  fold_long<1, 0>(P->AT, 0, seq, acc, g.cta, &P->bar->abort);
   block_to_slots<1, 0, false>(acc, P, kRegPA, g);
 }
 
@@ -2064,7 +2071,7 @@ __device__ HX_PHASE_INLINE void phase_avgstep_b(const KParams* P, const Roles* R
   EpiAvgStepDual e{P->yavg + static_cast<size_t>(R->avg_out) * m, P->aavg + static_cast<size_t>(R->avg_out) * m,
                    P->b, R->eta};
   spmv_rows<2, 0>(P->A, 1, SrcVec{P->xbar}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
-  fold_long<2, 0>(P->A, 1, seq, acc, g.cta);
+  fold_long<2, 0>(P->A, 1, seq, acc, g.cta, &P->bar->abort);
   block_to_slots<2, 0, false>(acc, P, kRegPB, g);
 }
 
@@ -2478,7 +2485,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
     spmv_head<LM>(CB ? P->A0 : P->A, gwarp_id(g), lane, head);
     if (!sync()) return;
     mark(1);
-    phase_dual<RK, LM, CB>(P, R, par, stage, ++seq, head, g, &target);
+    if (!phase_dual<RK, LM, CB>(P, R, par, stage, ++seq, head, g, &target)) return;
     if (threadIdx.x == 0) make_spec(C, SR);
     mark(2);
     spmv_head<LM>(P->AT, gwarp_id(g), lane, head);
@@ -3053,6 +3060,15 @@ void dfree(void* p) {
   else cudaFreeAsync(p, 0);
 }
 
+// Frees a device temporary when the scope ends (error returns included).
+struct DevFree {
+  void** p;
+  ~DevFree() {
+    if (*p) dfree(*p);
+    *p = nullptr;
+  }
+};
+
 void free_sched(DevSched& s) {
   dfree(s.tasks), dfree(s.meta), dfree(s.owned_ptr), dfree(s.owned_idx), dfree(s.flags);
   dfree(s.part), dfree(s.cnt), dfree(s.terms);
@@ -3520,6 +3536,7 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   // Matrix A (CSR), validated on the device.
   long long* rp64 = nullptr;
   unsigned* flags = nullptr;
+  DevFree guard_rp64{reinterpret_cast<void**>(&rp64)}, guard_flags{reinterpret_cast<void**>(&flags)};
   HX_CUDA(c, dalloc(&rp64, m + 1));
   HX_CUDA(c, dalloc(&flags, 1));
   HX_CUDA(c, dalloc(&c->a_ptr, m + 1));
@@ -3540,8 +3557,6 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   unsigned hflags = 0;
   HX_CUDA(c, cudaMemcpyAsync(&hflags, flags, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
   HX_CUDA(c, cudaStreamSynchronize(s));
-  dfree(rp64);
-  dfree(flags);
   c->launches += 2;
   tick("copy+check");
   if ((hflags & 16u) || !monotone) return set_err(c, HPLP_EINVAL, "hx_upload_csr: row_ptr is not monotone");
@@ -3553,6 +3568,11 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   // Explicit A^T with ascending rows per column: stable radix sort by column.
   {
     int *row_of = nullptr, *iota = nullptr, *keys_out = nullptr, *perm = nullptr, *cnt = nullptr;
+    void* tmp = nullptr;
+    // temporaries are freed on every exit, error returns included
+    DevFree g0{reinterpret_cast<void**>(&row_of)}, g1{reinterpret_cast<void**>(&iota)},
+        g2{reinterpret_cast<void**>(&keys_out)}, g3{reinterpret_cast<void**>(&perm)}, g4{reinterpret_cast<void**>(&cnt)},
+        g5{&tmp};
     HX_CUDA(c, dalloc(&row_of, nnz));
     HX_CUDA(c, dalloc(&iota, nnz));
     HX_CUDA(c, dalloc(&keys_out, nnz));
@@ -3568,7 +3588,6 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, c->a_idx, keys_out, iota, perm, static_cast<int>(nnz), 0,
                                     bits, s);
     cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, cnt, c->t_ptr, static_cast<int>(n + 1), s);
-    void* tmp = nullptr;
     HX_CUDA(c, dalloc(reinterpret_cast<unsigned char**>(&tmp), std::max<size_t>(1, std::max(tmp_bytes, scan_bytes))));
     if (nnz)
       HX_CUDA(c, cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, c->a_idx, keys_out, iota, perm,
@@ -3580,7 +3599,6 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     HX_CUDA(c, cudaStreamSynchronize(s));
     HX_CUDA(c, cudaGetLastError());
     c->launches += 5;
-    dfree(tmp), dfree(row_of), dfree(iota), dfree(keys_out), dfree(perm), dfree(cnt);
   }
   tick("transpose");
   // Schedules (host, from the pointer arrays).
@@ -3686,6 +3704,9 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
       // the blocks are cut on the device (the matrix is resident); only their
       // row pointers come back for the host schedules
       int* cnt[2] = {nullptr, nullptr};
+      unsigned char* scan_tmp = nullptr;
+      DevFree gc0{reinterpret_cast<void**>(&cnt[0])}, gc1{reinterpret_cast<void**>(&cnt[1])},
+          gst{reinterpret_cast<void**>(&scan_tmp)};
       for (int k = 0; k < 2; ++k) {
         HX_CUDA(c, dalloc(&cnt[k], static_cast<size_t>(m) + 1));
         HX_CUDA(c, cudaMemsetAsync(cnt[k], 0, sizeof(int), s));
@@ -3694,7 +3715,6 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
       split_count_kernel<<<nblk, 256, 0, s>>>(static_cast<int>(m), c->a_ptr, c->a_idx, split, cnt[0], cnt[1]);
       size_t scan_bytes = 0;
       cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, cnt[0], c->cb_ptr[0], static_cast<int>(m + 1), s);
-      unsigned char* scan_tmp = nullptr;
       HX_CUDA(c, dalloc(&scan_tmp, std::max<size_t>(1, scan_bytes)));
       for (int k = 0; k < 2; ++k)
         HX_CUDA(c, cub::DeviceScan::InclusiveSum(scan_tmp, scan_bytes, cnt[k], c->cb_ptr[k], static_cast<int>(m + 1), s));
@@ -3712,7 +3732,6 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
       HX_CUDA(c, cudaStreamSynchronize(s));
       HX_CUDA(c, cudaGetLastError());
       c->launches += 4;
-      dfree(cnt[0]), dfree(cnt[1]), dfree(scan_tmp);
       tick("cb split");
       const std::vector<int>* ps[2] = {&p0, &p1};
       DevSched* ds[2] = {&c->sb0, &c->sb1};
@@ -3793,10 +3812,14 @@ int hx_precondition(hx_ctx* c, int32_t ruiz_iters, double pc_alpha, double* row_
     inv_sqrt_kernel<<<nb, 256, 0, s>>>(n, dc, Cs);
     scale_csr_kernel<<<nb, 256, 0, s>>>(m, c->a_ptr, c->a_idx, c->a_val, dr, dc, 0);
     scale_csr_kernel<<<nb, 256, 0, s>>>(n, c->t_ptr, c->t_idx, c->t_val, dr, dc, 1);
+    // every other copy of A's values the loop reads gets the same two roundings
+    // (v * d_row) * d_col, so all copies stay bit-identical to a_val
+    for (int k = 0; k < 2 && c->colblock; ++k)  // column blocks of phase B (loop_kernel_stream_cb)
+      scale_csr_kernel<<<nb, 256, 0, s>>>(m, c->cb_ptr[k], c->cb_idx[k], c->cb_val[k], dr, dc, 0);
     scale_vec_kernel<<<nb, 256, 0, s>>>(m, c->b, dr);
     scale_vec_kernel<<<nb, 256, 0, s>>>(n, c->c, dc);
     if (c->ub) div_vec_kernel<<<nb, 256, 0, s>>>(n, c->ub, dc);  // x = C x': x' <= u / C
-    c->launches += c->ub ? 7 : 6;
+    c->launches += (c->ub ? 7 : 6) + (c->colblock ? 2 : 0);
     HX_CUDA(c, cudaGetLastError());
     return HPLP_OK;
   };

@@ -25,12 +25,40 @@ def join(solver, group=None) -> None:
         solver.team_import(b)
 
 
+def agree(ok: bool, what: str, group=None) -> None:
+    """Every rank learns whether every rank succeeded at `what` (all_reduce
+    MIN of a flag); if any failed, every rank raises -- so no rank ever enters
+    a collective its peers skipped."""
+    import torch
+    import torch.distributed as dist
+
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    if int(flag.item()) == 0:
+        raise RuntimeError(f"team setup failed on some rank during {what}")
+
+
 def rank_solver(std, device: int, group=None):
-    """Solver for this process's block of `std` (a StdForm), joined to the team."""
+    """Solver for this process's block of `std` (a StdForm), joined to the
+    team.  Setup runs in phases (create, join, first power iteration) with an
+    agreement after each, so a failure on one rank fails every rank instead
+    of leaving peers stuck in a collective."""
     import torch.distributed as dist
 
     from .hplp import Solver
 
-    s = Solver.rank(*std.csr(), nranks=dist.get_world_size(group), rank=dist.get_rank(group), device=device)
-    join(s, group)
+    s, err = None, None
+    try:
+        s = Solver.rank(*std.csr(), nranks=dist.get_world_size(group), rank=dist.get_rank(group), device=device)
+    except Exception as e:  # noqa: BLE001 -- re-raised after the agreement
+        err = e
+    agree(err is None, "hplp_solver_create_rank", group)
+    blobs = exchange(s.team_export(), group)
+    try:
+        for b in blobs:
+            s.team_import(b)
+    except Exception as e:  # noqa: BLE001
+        err = e
+    agree(err is None, "team_import", group)
     return s

@@ -329,3 +329,24 @@ def test_column_blocked_phase_b_parity(gpu_required, name, monkeypatch):
         c = args[6]
         assert abs(float(c @ g4["x"]) - float(c @ r4["x"])) <= 1e-4 * max(1.0, abs(float(c @ r4["x"])))
     sol.close()
+
+
+def test_column_blocked_preconditioned_parity(gpu_required, monkeypatch):
+    """hx_precondition rescales every copy of A the loop reads -- the column
+    blocks of loop_kernel_stream_cb included (they kept the
+    unscaled values, so A x+ used the original matrix while A^T y used the
+    scaled one).  The device loop on the preconditioned instance must match
+    the oracle run on the instance downloaded from the device."""
+    monkeypatch.setenv("HX_COLBLOCK", "1")
+    monkeypatch.setenv("HPLP_L2_STREAM", "1")
+    s = std("cfg1_small")[1]
+    sol = hplp.Solver(*csr_args(s))
+    assert sol.hx.loop_kernel() == "hx::loop_kernel_stream_cb"
+    sol.hx.precondition(3, 0.5)
+    rp, ci, v, b, c = sol.hx.download_problem()
+    assert rel_inf(v, s.val) > 1e-3  # the instance really changed
+    cpu = CpuLp("port", s.m, s.n, rp, ci, v, b, c).solve(iteration_limit=100, tolerance=1e-12, trace=True)
+    gpu = sol.solve(iteration_limit=100, tolerance=1e-12, trace=True)
+    _trace_cmp(gpu["trace"], cpu["trace"])
+    assert gpu["spmv_count"] == cpu["spmv_count"]
+    sol.close()
