@@ -68,6 +68,26 @@ int64_t hx_launch_count(hx_ctx* ctx);
  * nnz-balanced warp schedules of both matrices. */
 int hx_upload_csr(hx_ctx* ctx, int64_t m, int64_t n, const int64_t* row_ptr,
                   const int32_t* col_idx, const double* val, const double* b, const double* c);
+/* [spmv / spmv_transpose summation order, src/sparse_matrix.cpp:108-115 and
+ *  :127-134; SURVEY.md §8d "deterministic-reduction mode"]
+ * HX_SUM_FAST (default): every row sum is deterministic (fixed order, run to
+ * run bit-identical) but not the reference's order -- short rows as two
+ * interleaved partial sums, long rows as lane-strided partials + trees.
+ * HX_SUM_REFERENCE: every row of A and A^T is summed as ONE sequential chain
+ * in ascending index order, `acc = 0; acc += a_ij * x_j`, bit-identical to
+ * the reference's loops (products rounded once, no FMA); long rows become a
+ * single run carried by one warp.  Iterates then differ from the reference
+ * only through its norms/dots (restart tests, sigma): used for the full-size
+ * parity tests on the Zipf instance (configs[4]).  Set before hx_upload_csr
+ * (HPLP_ESTATE after). */
+#define HX_SUM_FAST 0
+#define HX_SUM_REFERENCE 1
+int hx_set_sum_order(hx_ctx* ctx, int32_t order);
+/* The order contexts created afterwards start with (all solver constructors
+ * of include/hplp_gpu.h go through hx_create); -1 returns to the default,
+ * HPLP_SUM_ORDER=reference in the environment, else HX_SUM_FAST. */
+int hx_set_default_sum_order(int32_t order);
+int32_t hx_sum_order(hx_ctx* ctx);
 /* Same with device-resident inputs (no host copies; used by re-uploads). */
 int hx_dims(hx_ctx* ctx, int64_t* m, int64_t* n, int64_t* nnz);
 

@@ -191,27 +191,34 @@ class CpuLp:
         averaged, 2 restarted average.  Same result dict as solve()."""
         return self.solve(config, init, trace, epochs_capacity, _baseline=int(mode), **kw)
 
-    def solve(self, config=None, init=None, trace=False, epochs_capacity=4096, _baseline=-1, **kw):
+    def solve(self, config=None, init=None, trace=False, epochs_capacity=4096, _baseline=-1, sink=None, **kw):
         """solve() (src/solver.cpp:206-342).  Returns a dict with the result
         fields, final x/y, certificates, epochs and (trace=True) the per-
-        iteration trace records with their iterates."""
+        iteration trace records with their iterates.  sink(record, x, y):
+        called per trace record instead of keeping copies (x, y are views
+        valid during the call) -- for instances too large to keep 100
+        iterates of."""
         cfg = config if config is not None else abi.Config.default(**kw)
         x, y = np.empty(self.n), np.empty(self.m)
         pc, dc = np.zeros(self.m), np.zeros(self.n)
         eps = (abi.Epoch * epochs_capacity)()
         recs = []
 
-        def sink(rec, xp, n, yp, m, user):
+        def record(rec, xp, n, yp, m, user):
             r = rec.contents
-            recs.append(dict(epoch=r.epoch, inner=r.inner, iteration=r.iteration,
-                             res=r.fixed_point_residual, kkt=r.kkt.as_tuple(),
-                             cand_norm_normalized=r.candidate_norm_normalized,
-                             cand_norm_difference=r.candidate_norm_difference,
-                             partition=abi.trace_partition(r),
-                             x=np.ctypeslib.as_array(xp, (n,)).copy(),
-                             y=np.ctypeslib.as_array(yp, (m,)).copy()))
+            d = dict(epoch=r.epoch, inner=r.inner, iteration=r.iteration,
+                     res=r.fixed_point_residual, kkt=r.kkt.as_tuple(),
+                     cand_norm_normalized=r.candidate_norm_normalized,
+                     cand_norm_difference=r.candidate_norm_difference,
+                     partition=abi.trace_partition(r))
+            if sink is not None:
+                sink(d, np.ctypeslib.as_array(xp, (n,)), np.ctypeslib.as_array(yp, (m,)))
+                return
+            d["x"] = np.ctypeslib.as_array(xp, (n,)).copy()
+            d["y"] = np.ctypeslib.as_array(yp, (m,)).copy()
+            recs.append(d)
 
-        cb = abi.TRACE_FN(sink) if trace else abi.TRACE_FN()
+        cb = abi.TRACE_FN(record) if trace else abi.TRACE_FN()
         if trace and cfg.trace_period == 0:
             cfg.trace_period = 1
         ix = iy = None

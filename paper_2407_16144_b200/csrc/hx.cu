@@ -41,6 +41,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <thread>
 #include <cstdio>
@@ -595,10 +596,14 @@ __device__ __forceinline__ void spmv_head(const Sched& S, int gwarp, int lane, S
   load_task<LM>(S, h.tk, lane, h.cur);
 }
 
-template <int Q, unsigned MaxMask, int LM = 0, class Src, class Epi>
+// EX: summation order -- 0 the fast order, 1 the reference's (Sched::exact),
+// 2 chosen at run time by S.exact (the main loop kernels compile it out: the
+// run-time branch costs them registers)
+template <int Q, unsigned MaxMask, int LM = 0, int EX = 2, class Src, class Epi>
 __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& src, Epi& epi, double (&acc)[Q],
                                           int gwarp, int lane, WarpStage* st, unsigned long long seq,
                                           const SpmvHead& head) {
+  const bool exact = EX == 1 || (EX == 2 && S.exact);
   const int W = S.W;
   const int n = S.n_tasks;
   const int4 kNone{0, 0, 0, 0};
@@ -674,8 +679,14 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
 #if HX_RSUM == 1
       // two interleaved partial sums (even / odd positions), combined at the
       // end: half the dependent-add chain; rows of <= 2 nonzeros keep the
-      // reference's exact order
+      // reference's exact order.  S.exact: one sequential chain (the
+      // reference's order for every row).
       auto row_sum = [&](int qa, int qe) {
+        if (exact) {
+          double s = 0.0;
+          for (int q = qa; q < qe; ++q) s += st->prod[q];
+          return s;
+        }
         double s0 = 0.0, s1 = 0.0;
         int q = qa;
         for (; q + 4 <= qe; q += 4) {
@@ -774,6 +785,27 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
         acc_add<Q, MaxMask>(acc, tm);
       }
       __syncwarp();
+    } else if (exact) {
+      // reference order: the products go through the staging buffer and lane 0
+      // adds them, in ascending index order, onto the sum the run carries
+      // (every long row is a single run in this mode: build_schedule exact)
+#pragma unroll
+      for (int j = 0; j < kLoadsPerLane; ++j) st->prod[j * 32 + lane] = cur.cv[j];
+      __syncwarp();
+      if (lane == 0) {
+        double a = run_acc;
+        for (int q = 0; q < len; ++q) a += st->prod[q];
+        run_acc = a;
+      }
+      __syncwarp();
+      if (kind == kTaskPiece && lane == 0) {
+        const int4 meta = __ldg(S.meta + t);
+        HX_CHECK(meta.y == 1, "exact-order long row split into runs", meta.y, t);
+        double tm[Q];
+        epi.apply(r0, run_acc, epi.load(r0), tm);
+        acc_add<Q, MaxMask>(acc, tm);
+      }
+      if (kind == kTaskPiece) run_acc = 0.0;
     } else {
 #if HX_PSUM
       // pairwise tree over the lane's products (fixed order, short chain)
@@ -835,12 +867,12 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
   }
 }
 
-template <int Q, unsigned MaxMask, int LM = 0, class Src, class Epi>
+template <int Q, unsigned MaxMask, int LM = 0, int EX = 2, class Src, class Epi>
 __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& src, Epi& epi, double (&acc)[Q],
                                           int gwarp, int lane, WarpStage* st, unsigned long long seq = 1) {
   SpmvHead head;
   spmv_head<LM>(S, gwarp, lane, head);
-  spmv_rows<Q, MaxMask, LM>(S, set, src, epi, acc, gwarp, lane, st, seq, head);
+  spmv_rows<Q, MaxMask, LM, EX>(S, set, src, epi, acc, gwarp, lane, st, seq, head);
 }
 
 // Owner side of the long-row protocol: warp 0 waits for each owned long row
@@ -1573,7 +1605,7 @@ __device__ __forceinline__ double* region_ptr(const KParams* P, int r, int nrec)
 __device__ __forceinline__ int gwarp_id(const Geo& g) { return g.cta * kWarps + (threadIdx.x >> 5); }
 
 // phase A: A^T y, primal step (+ Halpern formation of x), primal partials
-template <bool RK, bool BOX, int LM = 2>
+template <bool RK, bool BOX, int LM = 2, int EX = 2>
 __device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R, int par, WarpStage* stage,
                                                unsigned long long seq, const SpmvHead& head, const Geo& g) {
   constexpr int NQ = EpiPrimal<RK, BOX>::NQ;
@@ -1595,7 +1627,7 @@ __device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R,
 #ifdef HX_WPROF
   const unsigned long long w0 = clock64();
 #endif
-  spmv_rows<NQ, 0, LM>(S, par, SrcVecT<LM == 1 && HX_GATHER_LAST>{ycur_ptr(P, R)}, e, acc, gwarp_id(g),
+  spmv_rows<NQ, 0, LM, EX>(S, par, SrcVecT<LM == 1 && HX_GATHER_LAST>{ycur_ptr(P, R)}, e, acc, gwarp_id(g),
                        threadIdx.x & 31, stage, seq, head);
 #ifdef HX_WPROF
   if constexpr (!RK)
@@ -1606,7 +1638,7 @@ __device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R,
 }
 
 // phase B: A x+, dual step, speculative Halpern combos, dual partials
-template <bool RK, int LM = 2, bool CB = false>
+template <bool RK, int LM = 2, bool CB = false, int EX = 2>
 __device__ HX_PHASE_INLINE bool phase_dual(const KParams* P, const Roles* R, int par, WarpStage* stage,
                                            unsigned long long seq, const SpmvHead& head, const Geo& g,
                                            unsigned long long* target = nullptr) {
@@ -1635,7 +1667,7 @@ __device__ HX_PHASE_INLINE bool phase_dual(const KParams* P, const Roles* R, int
     // barrier, then sweep 2 over the trailing block with the full epilogue
     double a0[1] = {0.0};
     EpiStore st0{P->bpart};
-    spmv_rows<1, 0, LM>(P->A0, par, SrcVecT<LM == 1 && HX_GATHER_LAST>{xsrc}, st0, a0, gwarp_id(g),
+    spmv_rows<1, 0, LM, EX>(P->A0, par, SrcVecT<LM == 1 && HX_GATHER_LAST>{xsrc}, st0, a0, gwarp_id(g),
                         threadIdx.x & 31, stage, seq, head);
     spmv_head<LM>(P->A1, gwarp_id(g), threadIdx.x & 31, h1);
     // abort / watchdog: leave before sweep 2 (its long rows would wait on
@@ -1646,7 +1678,7 @@ __device__ HX_PHASE_INLINE bool phase_dual(const KParams* P, const Roles* R, int
 #ifdef HX_WPROF
   const unsigned long long w0 = clock64();
 #endif
-  spmv_rows<4, 0, LM>(S, par, SrcVecT<LM == 1 && HX_GATHER_LAST>{xsrc}, e, acc, gwarp_id(g), threadIdx.x & 31, stage,
+  spmv_rows<4, 0, LM, EX>(S, par, SrcVecT<LM == 1 && HX_GATHER_LAST>{xsrc}, e, acc, gwarp_id(g), threadIdx.x & 31, stage,
                       seq, CB ? h1 : head);
 #ifdef HX_WPROF
   if constexpr (!RK)
@@ -1709,27 +1741,27 @@ __device__ __forceinline__ void warp_totals_ranks(const KParams* P, int par, dou
 // power iteration halves: w = A x (x = x0 or z / zn), z = A^T w
 // (single-rank only: a team computes sigma redundantly on every rank, each
 // with its full-matrix schedules -- deterministic and identical, no exchange)
-template <int LM = 0>
+template <int LM = 0, int EX = 2>
 __device__ HX_PHASE_INLINE void power_a(const KParams* P, const Roles* R, WarpStage* stage, unsigned long long seq,
                                         const Geo& g) {
   double acc[1];
   acc_init<1, 0>(acc);
   EpiStoreSq e{P->ypool};
   const Sched S = P->A;
-  if (R->pw_mode == 0) spmv_rows<1, 0, LM>(S, 0, SrcVec{P->xpool}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
+  if (R->pw_mode == 0) spmv_rows<1, 0, LM, EX>(S, 0, SrcVec{P->xpool}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
   else
-    spmv_rows<1, 0, LM>(S, 0, SrcDiv{P->xpool + P->n, R->pw_zn}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
+    spmv_rows<1, 0, LM, EX>(S, 0, SrcDiv{P->xpool + P->n, R->pw_zn}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
   fold_long<1, 0>(S, 0, seq, acc, g.cta, &P->bar->abort);
   block_to_slots<1, 0, false>(acc, P, kRegPA, g);
 }
 
-template <int LM = 0>
+template <int LM = 0, int EX = 2>
 __device__ HX_PHASE_INLINE void power_b(const KParams* P, WarpStage* stage, unsigned long long seq, const Geo& g) {
   double acc[1];
   acc_init<1, 0>(acc);
   EpiStoreSq e{P->xpool + P->n};
   const Sched S = P->AT;
-  spmv_rows<1, 0, LM>(S, 0, SrcVec{P->ypool}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
+  spmv_rows<1, 0, LM, EX>(S, 0, SrcVec{P->ypool}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
   fold_long<1, 0>(S, 0, seq, acc, g.cta, &P->bar->abort);
   block_to_slots<1, 0, false>(acc, P, kRegPB, g);
 }
@@ -1851,7 +1883,7 @@ __device__ HX_PHASE_INLINE void cert_units(const KParams* P, const Roles* R, con
 }
 
 // certificate scan C3: the validation SpMVs, up to four independent products
-template <bool RK, int LM = 0>
+template <bool RK, int LM = 0, int EX = 2>
 __device__ HX_PHASE_INLINE void cert_products(const KParams* P, const Roles* R, WarpStage* stage,
                                               unsigned long long seq, const Geo& g) {
   const int n = P->n, m = P->m;
@@ -1869,7 +1901,7 @@ __device__ HX_PHASE_INLINE void cert_products(const KParams* P, const Roles* R, 
       double a2[2];
       acc_init<2, 3u>(a2);
       EpiPosNeg e;
-      spmv_rows<2, 3u, LM>(AT, 2 + k, SrcVec{k ? u3 : u1}, e, a2, gw, lane, stage, seq);
+      spmv_rows<2, 3u, LM, EX>(AT, 2 + k, SrcVec{k ? u3 : u1}, e, a2, gw, lane, stage, seq);
       fold_long<2, 3u>(AT, 2 + k, seq, a2, g.cta, &P->bar->abort);
       acc[2 * k] = a2[0], acc[2 * k + 1] = a2[1];
     }
@@ -1877,7 +1909,7 @@ __device__ HX_PHASE_INLINE void cert_products(const KParams* P, const Roles* R, 
       double a1[1];
       acc_init<1, 1u>(a1);
       EpiAbs e;
-      spmv_rows<1, 1u, LM>(A, 2 + k, SrcVec{k ? u2 : u0}, e, a1, gw, lane, stage, seq);
+      spmv_rows<1, 1u, LM, EX>(A, 2 + k, SrcVec{k ? u2 : u0}, e, a1, gw, lane, stage, seq);
       fold_long<1, 1u>(A, 2 + k, seq, a1, g.cta, &P->bar->abort);
       acc[4 + k] = a1[0];
     }
@@ -2348,7 +2380,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_baseline(con
 // ---------------------------------------------------------------------------
 // RK = false: one GPU, P in the constant bank (loop_kernel).  RK = true: one
 // rank of a row-partitioned team (loop_kernel_team), P in shared memory.
-template <bool RK, bool BOX = false, int LM = 2, bool CB = false>
+template <bool RK, bool BOX = false, int LM = 2, bool CB = false, int EX = 2>
 __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
   __shared__ Ctl C;
   __shared__ double tot[kMaxQ];
@@ -2398,7 +2430,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
   if (!RK && C.mode == kModePower) {
     // power_iteration loop body, src/sparse_matrix.cpp:153-177
     while (!R->stop) {
-      power_a<LM>(P, R, stage, ++seq, g);
+      power_a<LM, EX>(P, R, stage, ++seq, g);
       if (!sync()) return;
       {
         const double* rg = region_ptr(P, kRegPA, g.nrec);
@@ -2415,7 +2447,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
       }
       __syncthreads();
       if (R->stop) break;
-      power_b<LM>(P, stage, ++seq, g);
+      power_b<LM, EX>(P, stage, ++seq, g);
       if (!sync()) return;
       {
         const double* rg = region_ptr(P, kRegPB, g.nrec);
@@ -2478,14 +2510,14 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
     SpmvHead head;
     if (!spec_done) {
       spmv_head<LM>(P->AT, gwarp_id(g), lane, head);
-      phase_primal_t<RK, BOX, LM>(P, R, par, stage, ++seq, head, g);
+      phase_primal_t<RK, BOX, LM, EX>(P, R, par, stage, ++seq, head, g);
       if (writer && threadIdx.x == 0 && budget != 0ull) set_time_up(par, (global_ns() - t_start) > budget ? 1u : 0u);
     }
     mark(0);
     spmv_head<LM>(CB ? P->A0 : P->A, gwarp_id(g), lane, head);
     if (!sync()) return;
     mark(1);
-    if (!phase_dual<RK, LM, CB>(P, R, par, stage, ++seq, head, g, &target)) return;
+    if (!phase_dual<RK, LM, CB, EX>(P, R, par, stage, ++seq, head, g, &target)) return;
     if (threadIdx.x == 0) make_spec(C, SR);
     mark(2);
     spmv_head<LM>(P->AT, gwarp_id(g), lane, head);
@@ -2530,7 +2562,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
     mark(4);
     // speculative phase A of iteration it+1 (measured: worth ~10% against
     // running phase A after the controller)
-    phase_primal_t<RK, BOX, LM>(P, &SR, par ^ 1, stage, ++seq, head, g);
+    phase_primal_t<RK, BOX, LM, EX>(P, &SR, par ^ 1, stage, ++seq, head, g);
     if (writer && threadIdx.x == 0 && budget != 0ull)
       set_time_up(par ^ 1, (global_ns() - t_start) > budget ? 1u : 0u);
     __syncthreads();
@@ -2571,7 +2603,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
           C.cinf[3] = tot[10], C.cdot[3] = tot[11];
         }
         __syncthreads();
-        cert_products<RK, LM>(P, R, stage, ++seq, g);
+        cert_products<RK, LM, EX>(P, R, stage, ++seq, g);
         if (!sync()) return;
         {
           const double* rg = region_ptr(P, kRegC3, g.nrec);
@@ -2625,7 +2657,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
   // constant bank; no local copy (grid_constant)
   const Geo g{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x),
               static_cast<int>(gridDim.x)};
-  loop_body<false, false, 0>(&KP, g);
+  loop_body<false, false, 0, false, 0>(&KP, g);
 }
 
 // The same loop with the matrix streams loaded evict_first (working set
@@ -2633,7 +2665,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel(const __grid
 __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_stream(const __grid_constant__ KParams KP) {
   const Geo g{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x),
               static_cast<int>(gridDim.x)};
-  loop_body<false, false, 1>(&KP, g);
+  loop_body<false, false, 1, false, 0>(&KP, g);
+}
+
+// The reference summation order (hx_set_sum_order): every row one
+// sequential chain; matrix-stream policy chosen at run time.
+__global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_exact(const __grid_constant__ KParams KP) {
+  const Geo g{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x),
+              static_cast<int>(gridDim.x)};
+  loop_body<false, false, 2, false, 1>(&KP, g);
 }
 
 // The stream kernel with phase B swept in two column blocks (hx_upload_csr
@@ -2641,7 +2681,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_stream(const
 __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_stream_cb(const __grid_constant__ KParams KP) {
   const Geo g{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x),
               static_cast<int>(gridDim.x)};
-  loop_body<false, false, 1, true>(&KP, g);
+  loop_body<false, false, 1, true, 0>(&KP, g);
 }
 
 // The box form (hx_set_box) as its own kernel: the standard loop keeps its code.
@@ -2929,6 +2969,7 @@ struct hx_ctx {
   std::string err;
   int64_t m = 0, n = 0, nnz = 0;
   bool uploaded = false, setup_done = false;
+  int sum_order = 0;  // hx_set_sum_order: 1 = the reference's sequential row sums
   int64_t launches = 0;
   // device data
   int* a_ptr = nullptr;
@@ -3169,8 +3210,9 @@ int upload_sched(hx_ctx* ctx, DevSched& d, const int* ptr_host, int rows, int co
                  const int* didx, const double* dval, double lead = 0.0, int row0 = 0, bool transposed = false) {
   double rc, tc;
   sched_costs(transposed, rc, tc);
-  return upload_built_sched(ctx, d, build_schedule(ptr_host + row0, rows, ctx->grid * kWarps, lead, rc, tc), rows, cols,
-                            dptr, didx, dval, row0);
+  return upload_built_sched(ctx, d,
+                            build_schedule(ptr_host + row0, rows, ctx->grid * kWarps, lead, rc, tc, ctx->sum_order == 1),
+                            rows, cols, dptr, didx, dval, row0);
 }
 
 KParams params(hx_ctx* c) {
@@ -3210,6 +3252,7 @@ int launch_loop(hx_ctx* c) {
   const void* kernel = c->h.mode == kModeLoop && c->h.scheme != HPLP_SCHEME_RHPDHG
                            ? reinterpret_cast<const void*>(loop_kernel_baseline)
                            : c->ub                     ? reinterpret_cast<const void*>(loop_kernel_box)
+                           : c->sum_order == HX_SUM_REFERENCE ? reinterpret_cast<const void*>(loop_kernel_exact)
                            : c->sa.view.stream_hint && c->colblock && c->h.mode == kModeLoop
                                ? reinterpret_cast<const void*>(loop_kernel_stream_cb)
                            : c->sa.view.stream_hint    ? reinterpret_cast<const void*>(loop_kernel_stream)
@@ -3393,11 +3436,32 @@ void fill_progress(hx_ctx* c, hx_progress_t* p) {
 
 extern "C" {
 
+namespace {
+// Summation order new contexts start with: hx_set_default_sum_order, else
+// the environment (HPLP_SUM_ORDER=reference), else HX_SUM_FAST.
+std::atomic<int> g_sum_order{-1};
+int default_sum_order() {
+  int v = g_sum_order.load();
+  if (v < 0) {
+    const char* e = std::getenv("HPLP_SUM_ORDER");
+    v = e && (std::strcmp(e, "reference") == 0 || std::strcmp(e, "1") == 0) ? HX_SUM_REFERENCE : HX_SUM_FAST;
+  }
+  return v;
+}
+}  // namespace
+
+int hx_set_default_sum_order(int32_t order) {
+  if (order != HX_SUM_FAST && order != HX_SUM_REFERENCE && order != -1) return HPLP_EINVAL;
+  g_sum_order.store(order);
+  return HPLP_OK;
+}
+
 int hx_create(int32_t device, hx_ctx** out) {
   *out = nullptr;
   const auto t_create = std::chrono::steady_clock::now();
   auto ctx = std::make_unique<hx_ctx>();
   ctx->device = device;
+  ctx->sum_order = default_sum_order();
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return set_err(nullptr, HPLP_ECUDA, "hx_create: no CUDA device visible (the B200 path has no CPU fallback)");
@@ -3512,12 +3576,13 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     if (i && row_ptr[i] < row_ptr[i - 1]) monotone = false;
   }
   const int sched_warps = c->grid * kWarps;
+  const bool exact = c->sum_order == 1;
   std::future<SchedHost> sched_a;
   if (monotone)  // else the device check below reports it
-    sched_a = std::async(std::launch::async, [&ph, m, sched_warps] {
+    sched_a = std::async(std::launch::async, [&ph, m, sched_warps, exact] {
       double rc, tc;
       sched_costs(false, rc, tc);
-      return build_schedule(ph.data(), static_cast<int>(m), sched_warps, 0.0, rc, tc);
+      return build_schedule(ph.data(), static_cast<int>(m), sched_warps, 0.0, rc, tc, exact);
     });
   cudaStream_t s = c->stream;
   const int nblk = 4 * c->sm_count;
@@ -3611,10 +3676,10 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     double lead = 1200.0;
     if (const char* e = std::getenv("HX_LEAD")) lead = std::atof(e);
     // A^T's schedule is built on a host thread while A's uploads
-    auto sched_t = std::async(std::launch::async, [&pt, n, sched_warps, lead] {
+    auto sched_t = std::async(std::launch::async, [&pt, n, sched_warps, lead, exact] {
       double rc, tc;
       sched_costs(true, rc, tc);
-      return build_schedule(pt.data(), static_cast<int>(n), sched_warps, lead, rc, tc);
+      return build_schedule(pt.data(), static_cast<int>(n), sched_warps, lead, rc, tc, exact);
     });
     int rc = upload_built_sched(c, c->sa, sched_a.get(), static_cast<int>(m), static_cast<int>(n), c->a_ptr,
                                 c->a_idx, c->a_val, 0);
@@ -3687,6 +3752,7 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     c->sa.view.row_limit = c->pa.view.row_limit = static_cast<int>(m);  // output dimension (HX_CHECKED)
     c->st.view.row_limit = c->pt.view.row_limit = static_cast<int>(n);
     c->pa.view.stream_hint = c->pt.view.stream_hint = hint;
+    c->sa.view.exact = c->st.view.exact = c->pa.view.exact = c->pt.view.exact = exact ? 1 : 0;
     // Column-blocked phase B (loop_kernel_stream_cb): when x+ is far larger
     // than L2 its random gathers miss (configs[4]: 9.5 GB of DRAM traffic per
     // iteration against 5.0 GB algorithmic, L2 hit rate 38%), so A is split at
@@ -3697,7 +3763,8 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     // ascending column order.
     int want = hint && 8.0 * static_cast<double>(n) > 64e6 ? 1 : 0;
     if (const char* e = std::getenv("HX_COLBLOCK")) want = std::atoi(e) != 0 ? 1 : 0;
-    if (want && !c->ranked && nnz > 0) {
+    // the reference order sums each row in one chain: no split at a column
+    if (want && !c->ranked && nnz > 0 && !exact) {
       std::vector<int> pt(static_cast<size_t>(n) + 1);
       HX_CUDA(c, cudaMemcpy(pt.data(), c->t_ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost));
       const int split = static_cast<int>(std::lower_bound(pt.begin(), pt.end(), static_cast<int>(nnz / 2)) - pt.begin());
@@ -3793,6 +3860,17 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
 // rounds of Ruiz infinity-norm equilibration, then (pc_alpha >= 0) one
 // Pock-Chambolle step with exponent alpha.  Writes the accumulated row
 // scales R (m) and column scales C (n) when the pointers are non-NULL.
+int hx_set_sum_order(hx_ctx* c, int32_t order) {
+  if (order != HX_SUM_FAST && order != HX_SUM_REFERENCE)
+    return set_err(c, HPLP_EINVAL, "hx_set_sum_order: order must be HX_SUM_FAST or HX_SUM_REFERENCE");
+  if (c->uploaded && order != c->sum_order)
+    return set_err(c, HPLP_ESTATE, "hx_set_sum_order: set before hx_upload_csr (the schedules depend on it)");
+  c->sum_order = order;
+  return HPLP_OK;
+}
+
+int32_t hx_sum_order(hx_ctx* c) { return c ? c->sum_order : -1; }
+
 int hx_precondition(hx_ctx* c, int32_t ruiz_iters, double pc_alpha, double* row_scale, double* col_scale) {
   if (!c->uploaded) return set_err(c, HPLP_ESTATE, "hx_precondition: no problem uploaded");
   if (ruiz_iters < 0) return set_err(c, HPLP_EINVAL, "hx_precondition: ruiz_iters must be >= 0");
@@ -3866,7 +3944,7 @@ int hx_precondition(hx_ctx* c, int32_t ruiz_iters, double pc_alpha, double* row_
 // form.  Set after hx_upload_csr and before hx_precondition / hx_setup.
 int32_t hx_loop_variant(hx_ctx* c) {
   if (!c || !c->uploaded) return -1;
-  return c->ub ? 2 : c->sa.view.stream_hint ? (c->colblock ? 3 : 1) : 0;
+  return c->ub ? 2 : c->sum_order == HX_SUM_REFERENCE ? 4 : c->sa.view.stream_hint ? (c->colblock ? 3 : 1) : 0;
 }
 
 int hx_set_box(hx_ctx* c, const double* upper) {

@@ -136,6 +136,14 @@ struct Sched {
   int n_long = 0;
   int stream_hint = 0;             // 1: idx/val loaded evict_first (working set > L2; hx_upload_csr)
   int row_limit = 0;               // dimension of the output vector (bounds checks in HX_CHECKED builds)
+  // 1: reference summation order (hx_set_sum_order): every row summed as one
+  // sequential chain in ascending index order, exactly the reference's
+  // `acc += value * x[col]` (src/sparse_matrix.cpp:108-115, :127-134), so row
+  // sums are bit-identical to it; long rows are one run of pieces whose
+  // products lane 0 adds in order.  0: the fast order (two interleaved
+  // partial sums per short row, lane-strided partials + trees for long rows).
+  int exact = 0;
+  int pad_exact = 0;
   // Long-row scratch per "set" (base + set * stride; no dynamically indexed
   // arrays, which would force the kernel parameters into local memory):
   // sets 0/1 alternate by iteration parity in the main phases, sets 2/3
@@ -175,7 +183,9 @@ struct SchedHost {
 
 // lead: initial load (cost units) of warp 0 of every CTA, which runs the
 // controller before its own tasks in the speculative phase A.
+// exact: reference summation order -- every long row becomes ONE run of
+// pieces (one warp carries the sequential sum through all of them).
 SchedHost build_schedule(const int* ptr_host, int rows, int warps, double lead = 0.0, double row_cost = kRowCost,
-                         double task_cost = kTaskCost);
+                         double task_cost = kTaskCost, bool exact = false);
 
 }  // namespace hx

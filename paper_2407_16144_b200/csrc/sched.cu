@@ -17,7 +17,8 @@
 
 namespace hx {
 
-SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, double row_cost, double task_cost) {
+SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, double row_cost, double task_cost,
+                         bool exact) {
   SchedHost s;
   const int64_t nnz = ptr[rows] - ptr[0];  // ptr may point into a larger matrix (a rank's block)
   const double total = static_cast<double>(nnz) + row_cost * rows;
@@ -37,9 +38,11 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, doubl
     const int64_t len = ptr[r + 1] - ptr[r];
     if (len > kStreamRowMax) {
       const int np = static_cast<int>((len + kTaskNnz - 1) / kTaskNnz);
-      const double pc = static_cast<double>(len) / np + task_cost;
+      // exact order: lane 0 adds every product in sequence, about as long
+      // again as the gathers -- the piece costs twice as much
+      const double pc = static_cast<double>(len) / np * (exact ? 2.0 : 1.0) + task_cost;
       const int per = std::max(1, std::min(kRunMax, static_cast<int>(run_budget / pc)));
-      const int nr = (np + per - 1) / per;
+      const int nr = exact ? 1 : (np + per - 1) / per;
       for (int k = 0; k < nr; ++k) {
         unit.push_back(s.tasks.size());
         const int q0 = static_cast<int>(static_cast<int64_t>(np) * k / nr);
@@ -49,7 +52,7 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, doubl
           const int p1 = static_cast<int>(ptr[r] + len * (q + 1) / np);
           push(r, r + 1, q + 1 == q1 ? kTaskPiece : kTaskPieceRun, p0, p1,
                int4{s.n_slots + k, nr, nr > 1 ? s.n_long : -1, k},
-               static_cast<double>(p1 - p0) + (q + 1 == np ? row_cost : 0.0));
+               static_cast<double>(p1 - p0) * (exact ? 2.0 : 1.0) + (q + 1 == np ? row_cost : 0.0));
         }
       }
       if (nr > 1) {

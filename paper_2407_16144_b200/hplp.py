@@ -116,6 +116,9 @@ def lib() -> C.CDLL:
     sig("hx_profile", C.c_int, V, C.POINTER(C.c_uint64), I32)
     sig("hx_sched_tasks", C.c_int, V, I32, C.POINTER(C.c_int32), I64, C.POINTER(C.c_int64))
     sig("hx_precondition", C.c_int, V, I32, D, PD, PD)
+    sig("hx_set_sum_order", C.c_int, V, I32)
+    sig("hx_sum_order", I32, V)
+    sig("hx_set_default_sum_order", C.c_int, I32)
     sig("hx_download_problem", C.c_int, V, PI64, PI32, PD, PD, PD)
     sig("hx_set_partition", C.c_int, V, I32, I32, PI64, PI64, I32)
     sig("hx_team_bind", C.c_int, PV, I32)
@@ -215,20 +218,25 @@ def _result(res: abi.Result, x, y, pc, dc, eps, recs) -> dict:
     )
 
 
-def _io(m, n, init, trace, epochs_capacity):
+def _io(m, n, init, trace, epochs_capacity, sink=None):
     x, y = np.empty(n), np.empty(m)
     pc, dc = np.zeros(m), np.zeros(n)
     eps = (abi.Epoch * epochs_capacity)()
     recs = []
 
-    def sink(rec, xp, nn, yp, mm, user):
+    def record(rec, xp, nn, yp, mm, user):
         r = rec.contents
-        recs.append(dict(epoch=r.epoch, inner=r.inner, iteration=r.iteration, res=r.fixed_point_residual,
-                         kkt=r.kkt.as_tuple(), cand_norm_normalized=r.candidate_norm_normalized,
-                         cand_norm_difference=r.candidate_norm_difference, partition=abi.trace_partition(r),
-                         x=np.ctypeslib.as_array(xp, (nn,)).copy(), y=np.ctypeslib.as_array(yp, (mm,)).copy()))
+        d = dict(epoch=r.epoch, inner=r.inner, iteration=r.iteration, res=r.fixed_point_residual,
+                 kkt=r.kkt.as_tuple(), cand_norm_normalized=r.candidate_norm_normalized,
+                 cand_norm_difference=r.candidate_norm_difference, partition=abi.trace_partition(r))
+        if sink is not None:  # per-record callback instead of kept copies (large instances)
+            sink(d, np.ctypeslib.as_array(xp, (nn,)), np.ctypeslib.as_array(yp, (mm,)))
+            return
+        d["x"] = np.ctypeslib.as_array(xp, (nn,)).copy()
+        d["y"] = np.ctypeslib.as_array(yp, (mm,)).copy()
+        recs.append(d)
 
-    cb = abi.TRACE_FN(sink) if trace else abi.TRACE_FN()
+    cb = abi.TRACE_FN(record) if trace else abi.TRACE_FN()
     ix = iy = None
     if init is not None:
         ix = np.ascontiguousarray(init[0], np.float64)
@@ -342,9 +350,10 @@ class Solver:
         """hx context of rank r of a team (rank 0 = self.hx)."""
         return HX(lib().hplp_solver_rank_hx(self.h, int(r)), owned=False)
 
-    def solve(self, config=None, init=None, trace=False, epochs_capacity=1 << 16, **kw) -> dict:
+    def solve(self, config=None, init=None, trace=False, epochs_capacity=1 << 16, sink=None, **kw) -> dict:
+        """sink(record, x, y): per-trace-record callback instead of kept copies."""
         cfg = _config(config, trace, kw)
-        io, x, y, pc, dc, eps, recs, keep = _io(self.m, self.n, init, trace, epochs_capacity)
+        io, x, y, pc, dc, eps, recs, keep = _io(self.m, self.n, init, trace, epochs_capacity, sink)
         res = abi.Result()
         _check(lib().hplp_solver_solve(self.h, C.byref(cfg), C.byref(io), C.byref(res)))
         del keep
@@ -360,6 +369,25 @@ class Solver:
             self.close()
         except Exception:
             pass
+
+
+SUM_FAST, SUM_REFERENCE = 0, 1
+
+
+class sum_order:
+    """Context manager: solvers created inside start with this SpMV summation
+    order (hx_set_default_sum_order) -- "reference" gives row sums
+    bit-identical to the reference's sequential loops (include/hx.h)."""
+
+    def __init__(self, order):
+        self.order = {"fast": SUM_FAST, "reference": SUM_REFERENCE}.get(order, order)
+
+    def __enter__(self):
+        _check(lib().hx_set_default_sum_order(int(self.order)))
+        return self
+
+    def __exit__(self, *exc):
+        lib().hx_set_default_sum_order(-1)
 
 
 def solve(m, n, row_ptr, col_idx, val, b, c, config=None, init=None, trace=False, device=0,
@@ -426,12 +454,21 @@ class HX:
         lib().hx_device_info(self.h, C.byref(sm), C.byref(g), C.byref(t))
         return dict(sm_count=sm.value, grid=g.value, threads=t.value)
 
-    LOOP_KERNELS = ("hx::loop_kernel", "hx::loop_kernel_stream", "hx::loop_kernel_box", "hx::loop_kernel_stream_cb")
+    LOOP_KERNELS = ("hx::loop_kernel", "hx::loop_kernel_stream", "hx::loop_kernel_box", "hx::loop_kernel_stream_cb",
+                    "hx::loop_kernel_exact")
 
     def loop_kernel(self) -> str:
         """Name of the loop kernel hx_run launches for this problem."""
         v = lib().hx_loop_variant(self.h)
         return self.LOOP_KERNELS[v] if v >= 0 else ""
+
+    def sum_order(self) -> int:
+        """hx_sum_order: SUM_FAST or SUM_REFERENCE."""
+        return int(lib().hx_sum_order(self.h))
+
+    def set_sum_order(self, order):
+        """hx_set_sum_order (before upload)."""
+        self._c(lib().hx_set_sum_order(self.h, int(order)))
 
     def stream(self) -> int:
         return lib().hx_stream(self.h) or 0

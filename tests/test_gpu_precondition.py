@@ -124,24 +124,4 @@ def test_preconditioned_infeasibility_certificate_is_valid_on_original(gpu_requi
     assert rep["valid"], rep
 
 
-@pytest.mark.slow
-def test_configs2_full_size_infeasibility_certificate(gpu_required):
-    """BASELINE configs[2] at full size (150,200 x 215,000 standard form): with
-    Ruiz + Pock-Chambolle preconditioning and the adaptive stall cap off the
-    device reports primal infeasibility; the certificate, mapped back to the
-    ORIGINAL LP (y = R y', renormalised), passes the oracle's
-    validate_primal_infeasibility at the reference's 1e-6 tolerance with the
-    original matrix's sigma."""
-    from oracle import CpuLp
-    from paper_2407_16144_b200 import gen
-
-    s = hplp.to_standard_form(gen.generate(2))
-    r = hplp.solve(*s.csr(), tolerance=1e-4, iteration_limit=1_000_000, precondition_ruiz_iters=10,
-                   precondition_pc_alpha=1.0, adaptive_stall_cap=0)
-    assert r["status"] == "primal_infeasible"
-    vec, meta = r["primal_cert"]
-    assert meta["residual"] <= 1e-6 * max(1.0, r["sigma_estimate"])
-    cpu = CpuLp("port", *s.csr())
-    sigma_orig = cpu.power_iteration()[0] * (1 + 1e-4)
-    rep = cpu.validate_primal(vec, 1e-6, sigma_orig)
-    assert rep["valid"], rep
+# configs[2] at full size: tests/test_gpu_full_parity.py (validated by the reference itself)
