@@ -88,6 +88,11 @@ int hx_set_sum_order(hx_ctx* ctx, int32_t order);
  * HPLP_SUM_ORDER=reference in the environment, else HX_SUM_FAST. */
 int hx_set_default_sum_order(int32_t order);
 int32_t hx_sum_order(hx_ctx* ctx);
+/* Nonzeros of A and of A^T this context stores on its device: nnz and nnz
+ * for one GPU; for a rank of a team (hx_set_partition) only its row block of
+ * A and its column block (= rows of A^T), about 2 nnz / nranks together --
+ * the full matrix is never on a rank's device. */
+int hx_stored_nonzeros(hx_ctx* ctx, int64_t* nnz_a, int64_t* nnz_t);
 /* Same with device-resident inputs (no host copies; used by re-uploads). */
 int hx_dims(hx_ctx* ctx, int64_t* m, int64_t* n, int64_t* nnz);
 
@@ -113,10 +118,13 @@ int hx_set_box(hx_ctx* ctx, const double* upper);
  * (the stream kernel with phase B swept in two column blocks: x+ far larger
  * than L2; HX_COLBLOCK=0/1 overrides); -1 before an upload. */
 int32_t hx_loop_variant(hx_ctx* ctx);
-/* The device problem (after any preconditioning): CSR A, b, c. */
+/* The device problem (after any preconditioning): CSR A, b, c (one GPU;
+ * HPLP_EINVAL for a rank, which stores only its blocks). */
 int hx_download_problem(hx_ctx* ctx, int64_t* row_ptr, int32_t* col_idx, double* val, double* b, double* c);
 
-/* [spmv, src/sparse_matrix.cpp:101-117]  out = A x, host vectors. */
+/* [spmv, src/sparse_matrix.cpp:101-117]  out = A x, host vectors.  A rank of
+ * a team computes its own rows (columns for the transpose); the rest of out
+ * is 0. */
 int hx_spmv(hx_ctx* ctx, const double* x, double* out);
 /* [spmv_transpose, src/sparse_matrix.cpp:119-136]  out = A^T y. */
 int hx_spmv_transpose(hx_ctx* ctx, const double* y, double* out);
@@ -207,6 +215,12 @@ int hx_get_certificate(hx_ctx* ctx, int32_t kind, double* vec);
  * of the normalized candidate (2/k)(z - anchor); NaN when undefined (k = 0,
  * multi-rank context).  Any output may be NULL. */
 int hx_trace_extras(hx_ctx* ctx, double* aty, double* c_out, double* cand_norm_normalized);
+/* [src/solver.cpp:278-279, partition_estimate_from_reduced_costs's input]
+ * rc (n) = c + A^T y of the last traced iteration, on the device problem.  A
+ * rank of a team takes it from the trace slots the loop kernel's phase A
+ * fills (every rank its own columns; read back through CUDA IPC), so no
+ * boundary SpMV over the whole matrix is needed. */
+int hx_trace_reduced_costs(hx_ctx* ctx, double* rc);
 
 /* [kkt_error, src/pdhg_core.cpp:70-73] at the current iterate with fresh
  * products (the limit path of src/solver.cpp:242-254 when no best exists). */

@@ -79,7 +79,11 @@
 
 namespace hx {
 
-enum Mode : int { kModeLoop = 0, kModePower = 1 };
+// kModePower: power iteration (src/sparse_matrix.cpp:138-179).  Teams only:
+// kModeKkt (KKT of the current iterate with fresh products) and kModeScale
+// (the diagonal preconditioning rounds), every rank on its own blocks with
+// the cross-rank exchange through pushes and team barriers.
+enum Mode : int { kModeLoop = 0, kModePower = 1, kModeKkt = 2, kModeScale = 3 };
 
 // Buffer roles and per-iteration scalars every thread needs.
 struct Roles {
@@ -103,6 +107,8 @@ struct Roles {
   int x_src_avg, y_cur_avg, ax_cur_avg;
   int avg_mode, avg_cur, avg_out, avg_step;
   int y_unpushed;  // team: y_cur is a y+ whose owned rows the peers have not received yet (after a restart)
+  int tr_slot;     // team: phase A's iteration is traced -> reduced costs into trace slot tr_slot (-1: not traced)
+  int pad_tr;
   double w_avg;
 };
 
@@ -132,6 +138,12 @@ struct Ctl {
   double pw_tol, pw_sigma, pw_sigma_prev, pw_sigma_cur;
   int pw_converged, pw_redraw;
   unsigned long long team_epochs;  // cross-rank barriers passed so far (identical on every rank)
+  // team setup modes: kModeKkt totals (||Ax - b||^2, ||[-(c + A^T y)]+||^2,
+  // c.x, b.y); kModeScale rounds (sc_ruiz Ruiz rounds, then Pock-Chambolle
+  // with sc_alpha when sc_pc) and the scaled ||b||^2, ||c||^2
+  double kk_tot[4];
+  int sc_ruiz, sc_pc;
+  double sc_alpha, sc_bsq, sc_csq;
   // baseline schemes
   int scheme;          // HPLP_SCHEME_*
   int avg_best;        // average slot holding the best candidate (-1: best is a z in the pools)
@@ -232,6 +244,9 @@ struct KParams {
   // gathers of x+ stay in L2; bpart holds A0's row sums
   Sched A0, A1;
   double* bpart;  // m
+  // team: reduced costs c + A^T y of traced iterations, two parity slots of n
+  // (peers read them back through CUDA IPC for the trace's partition estimate)
+  double* trbuf;
 };
 
 // z's buffers: pool role, or an average slot after a baseline restart.
@@ -968,6 +983,7 @@ struct EpiPrimal {  // phase A, rows of A^T
   const Team* T;   // RK: peers of the x+ push
   size_t xp_off;   // offset of x+ in the x pools
   const double* ub;  // BOX: upper bounds (+inf: none)
+  double* tr;        // RK: reduced costs c + A^T y of a traced iteration (src/solver.cpp:278-279), or null
   struct In {
     double xs, xa, c, u;
   };
@@ -991,6 +1007,8 @@ struct EpiPrimal {  // phase A, rows of A^T
     xp[j] = xn;
     if constexpr (RK)
       if (T->nranks > 1) push_peers(T, T->px, xp_off + j, xn, __ldg(T->xneed + (j - T->col0)));
+    if constexpr (RK)
+      if (tr) tr[j] = cj + aty;
     double rc = -(cj + aty);
     rc = rc < 0.0 ? 0.0 : rc;
     const double dx = x - xn;
@@ -1062,6 +1080,67 @@ struct EpiStoreSq {  // out = s, term s^2 (power iteration)
   __device__ __forceinline__ void apply(int r, double s, const In&, double (&t)[1]) const {
     out[r] = s;
     t[0] = s * s;
+  }
+};
+
+// Power iteration in a team: out = s, term s^2, and the entry pushed to the
+// peers that gather it (w_i to the owners of the columns in row i, z_j to the
+// owners of the rows in column j).
+template <bool RK>
+struct EpiStoreSqPush {
+  double* out;
+  const Team* T;
+  double* const* base;        // T->py / T->px: the peers' pools
+  size_t off;                 // offset of out within the pools
+  const unsigned char* need;  // T->yneed / T->xneed
+  int lo;                     // row0 / col0
+  using In = NoIn;
+  __device__ __forceinline__ In load(int) const { return {}; }
+  __device__ __forceinline__ void apply(int r, double s, const In&, double (&t)[1]) const {
+    out[r] = s;
+    t[0] = s * s;
+    if constexpr (RK)
+      if (T->nranks > 1) push_peers(T, base, off + r, s, __ldg(need + (r - lo)));
+  }
+};
+
+// kModeKkt (teams): kkt_error_with_products at z with fresh products,
+// src/pdhg_core.cpp:57-68.  Rows of A^T: [-(c + A^T y)]+^2 and c.x with x
+// formed as in phase A; rows of A: (Ax - b)^2 and b.y.
+struct SrcComb {  // x = x_src, or (1 - w) x_src + w anchor (the rounding phase A uses)
+  const double* xs;
+  const double* xa;
+  double w;
+  int mode;
+  __device__ __forceinline__ double operator()(int j) const {
+    return mode ? (1.0 - w) * ldca(xs + j) + w * ldca(xa + j) : ldca(xs + j);
+  }
+};
+struct EpiKktA {
+  SrcComb x;
+  const double* c;
+  struct In {
+    double x, c;
+  };
+  __device__ __forceinline__ In load(int j) const { return In{x(j), __ldg(c + j)}; }
+  __device__ __forceinline__ void apply(int, double aty, const In& in, double (&t)[2]) const {
+    double rc = -(in.c + aty);
+    rc = rc < 0.0 ? 0.0 : rc;
+    t[0] = rc * rc;
+    t[1] = in.c * in.x;
+  }
+};
+struct EpiKktB {
+  const double* b;
+  const double* y;
+  struct In {
+    double b, y;
+  };
+  __device__ __forceinline__ In load(int i) const { return In{__ldg(b + i), ldcg(y + i)}; }
+  __device__ __forceinline__ void apply(int, double ax, const In& in, double (&t)[2]) const {
+    const double d = ax - in.b;
+    t[0] = d * d;
+    t[1] = in.b * in.y;
   }
 };
 
@@ -1342,6 +1421,7 @@ __device__ void finish_iteration(Ctl& C, hplp_epoch_t* epochs, bool writer, doub
   }
   R.check = 0;
   C.it += 1;
+  R.tr_slot = C.trace_period > 0 && C.it % C.trace_period == 0 ? static_cast<int>(C.it & 1) : -1;
   // x outputs avoid this iteration's T(z) and the best iterate before and
   // after its update too, so that without a restart the picks equal the
   // speculative ones (make_spec), which cannot know the update yet
@@ -1571,13 +1651,15 @@ __device__ void make_spec(const Ctl& C, Roles& S) {
   S.w_x = 1.0 / static_cast<double>(C.k + 2);
   S.y_cur = R.yc_out;
   S.zx_out = pick_free(kXPool, S.x_src, S.x_anchor, C.x_best, R.zx_out);
+  const long long nit = C.it + 1;
+  S.tr_slot = C.trace_period > 0 && nit % C.trace_period == 0 ? static_cast<int>(nit & 1) : -1;
   S.xp_out = pick_free(kXPool, S.x_src, S.x_anchor, C.x_best, R.zx_out, S.zx_out);
 }
 
 // Did the speculative phase A compute exactly what phase A with roles R would?
 __device__ __forceinline__ bool same_phase_a(const Roles& R, const Roles& S) {
   return R.x_mode == S.x_mode && R.x_src == S.x_src && R.x_anchor == S.x_anchor && R.zx_out == S.zx_out &&
-         R.xp_out == S.xp_out && R.y_cur == S.y_cur && R.w_x == S.w_x && R.eta == S.eta;
+         R.xp_out == S.xp_out && R.y_cur == S.y_cur && R.w_x == S.w_x && R.eta == S.eta && R.tr_slot == S.tr_slot;
 }
 
 __device__ void ctl_load(const Ctl* g, Ctl& s) {
@@ -1622,7 +1704,8 @@ __device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R,
                        R->x_mode,
                        &P->T,
                        static_cast<size_t>(R->xp_out) * n,
-                       P->ub};
+                       P->ub,
+                       RK && R->tr_slot >= 0 && P->trbuf ? P->trbuf + static_cast<size_t>(R->tr_slot) * n : nullptr};
   const Sched S = P->AT;
 #ifdef HX_WPROF
   const unsigned long long w0 = clock64();
@@ -1739,31 +1822,115 @@ __device__ __forceinline__ void warp_totals_ranks(const KParams* P, int par, dou
 }
 
 // power iteration halves: w = A x (x = x0 or z / zn), z = A^T w
-// (single-rank only: a team computes sigma redundantly on every rank, each
-// with its full-matrix schedules -- deterministic and identical, no exchange)
-template <int LM = 0, int EX = 2>
+// (a team: every rank its own rows of w = A x and columns of z = A^T w,
+// pushed to the peers that gather them; the norms reduced over all ranks'
+// records -- identical on every rank)
+template <int LM = 0, int EX = 2, bool RK = false>
 __device__ HX_PHASE_INLINE void power_a(const KParams* P, const Roles* R, WarpStage* stage, unsigned long long seq,
                                         const Geo& g) {
   double acc[1];
   acc_init<1, 0>(acc);
-  EpiStoreSq e{P->ypool};
+  EpiStoreSqPush<RK> e{P->ypool, &P->T, P->T.py, 0, P->T.yneed, P->T.row0};
   const Sched S = P->A;
   if (R->pw_mode == 0) spmv_rows<1, 0, LM, EX>(S, 0, SrcVec{P->xpool}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
   else
     spmv_rows<1, 0, LM, EX>(S, 0, SrcDiv{P->xpool + P->n, R->pw_zn}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
   fold_long<1, 0>(S, 0, seq, acc, g.cta, &P->bar->abort);
-  block_to_slots<1, 0, false>(acc, P, kRegPA, g);
+  block_to_slots<1, 0, RK>(acc, P, kRegPA, g);
 }
 
-template <int LM = 0, int EX = 2>
+template <int LM = 0, int EX = 2, bool RK = false>
 __device__ HX_PHASE_INLINE void power_b(const KParams* P, WarpStage* stage, unsigned long long seq, const Geo& g) {
   double acc[1];
   acc_init<1, 0>(acc);
-  EpiStoreSq e{P->xpool + P->n};
+  EpiStoreSqPush<RK> e{P->xpool + P->n, &P->T, P->T.px, static_cast<size_t>(P->n), P->T.xneed, P->T.col0};
   const Sched S = P->AT;
   spmv_rows<1, 0, LM, EX>(S, 0, SrcVec{P->ypool}, e, acc, gwarp_id(g), threadIdx.x & 31, stage, seq);
   fold_long<1, 0>(S, 0, seq, acc, g.cta, &P->bar->abort);
-  block_to_slots<1, 0, false>(acc, P, kRegPB, g);
+  block_to_slots<1, 0, RK>(acc, P, kRegPB, g);
+}
+
+// kModeKkt (teams): this rank's columns (A^T y) and rows (A x), partials into
+// region C1 (4 quantities), every rank's records on every rank.
+template <int LM, int EX>
+__device__ HX_PHASE_INLINE void team_kkt(const KParams* P, const Roles* R, WarpStage* stage, unsigned long long seq,
+                                         const Geo& g) {
+  const int n = P->n, m = P->m;
+  const SrcComb xf{xsrc_ptr(P, R), P->xpool + static_cast<size_t>(R->x_anchor) * n, R->w_x, R->x_mode};
+  const double* y = ycur_ptr(P, R);
+  double a2[2], b2[2];
+  acc_init<2, 0>(a2);
+  acc_init<2, 0>(b2);
+  EpiKktA ea{xf, P->c};
+  spmv_rows<2, 0, LM, EX>(P->AT, 0, SrcVec{y}, ea, a2, gwarp_id(g), threadIdx.x & 31, stage, seq);
+  fold_long<2, 0>(P->AT, 0, seq, a2, g.cta, &P->bar->abort);
+  EpiKktB eb{P->b, y};
+  spmv_rows<2, 0, LM, EX>(P->A, 1, xf, eb, b2, gwarp_id(g), threadIdx.x & 31, stage, seq + 1);
+  fold_long<2, 0>(P->A, 1, seq + 1, b2, g.cta, &P->bar->abort);
+  (void)m;
+  const double a4[4] = {b2[0], a2[0], a2[1], b2[1]};
+  block_to_slots<4, 0, true>(a4, P, kRegC1, g);
+}
+
+// kModeScale (teams), one round of hx_precondition on this rank's blocks:
+// the row / column norms of the rows and columns it owns (row_norm_kernel's
+// formulas), their inverse square roots into the u-pool regions (u1: d_row,
+// u0: d_col, peers' copies through pushes), accumulated into R (u3) / C (u2).
+__device__ void team_scale_norms(const KParams* P, const Geo& g, int kind, double prow, double pcol) {
+  const Team& T = P->T;
+  const int n = P->n, m = P->m;
+  double* dcol = P->upool;
+  double* ccum = P->upool + n;
+  double* drow = P->upool + 2 * static_cast<size_t>(n);
+  double* rcum = drow + m;
+  const int tid = g.cta * kThreads + threadIdx.x, nth = g.nctas * kThreads;
+  auto norm = [&](const Sched& S, int r, double pw) {
+    double acc = 0.0;
+    for (int p = __ldg(S.ptr + r); p < __ldg(S.ptr + r + 1); ++p) {
+      const double a = fabs(ldcg(S.val + p));
+      if (kind == 0) acc = a > acc ? a : acc;
+      else acc += pw == 1.0 ? a : pow(a, pw);
+    }
+    return acc > 0.0 ? 1.0 / sqrt(acc) : 1.0;
+  };
+  for (int i = T.row0 + tid; i < T.row1; i += nth) {
+    const double f = norm(P->A, i, prow);
+    drow[i] = f;
+    rcum[i] = rcum[i] * f;
+    if (T.nranks > 1) push_peers(&T, T.pu, 2 * static_cast<size_t>(n) + i, f, __ldg(T.yneed + (i - T.row0)));
+  }
+  for (int j = T.col0 + tid; j < T.col1; j += nth) {
+    const double f = norm(P->AT, j, pcol);
+    dcol[j] = f;
+    ccum[j] = ccum[j] * f;
+    if (T.nranks > 1) push_peers(&T, T.pu, static_cast<size_t>(j), f, __ldg(T.xneed + (j - T.col0)));
+  }
+}
+
+// ... then (after a team barrier) this rank's blocks scaled with the
+// scale_csr_kernel rounding (v d_row) d_col, its b and c entries with
+// scale_vec_kernel's.
+__device__ void team_scale_apply(const KParams* P, const Geo& g) {
+  const Team& T = P->T;
+  const int n = P->n;
+  const double* dcol = P->upool;
+  const double* drow = P->upool + 2 * static_cast<size_t>(n);
+  const int tid = g.cta * kThreads + threadIdx.x, nth = g.nctas * kThreads;
+  double* av = const_cast<double*>(P->A.val);
+  double* tv = const_cast<double*>(P->AT.val);
+  double* b = const_cast<double*>(P->b);
+  double* c = const_cast<double*>(P->c);
+  for (int i = T.row0 + tid; i < T.row1; i += nth) {
+    const double di = drow[i];
+    for (int p = __ldg(P->A.ptr + i); p < __ldg(P->A.ptr + i + 1); ++p) av[p] = (av[p] * di) * dcol[__ldg(P->A.idx + p)];
+    b[i] = b[i] * di;
+  }
+  for (int j = T.col0 + tid; j < T.col1; j += nth) {
+    const double dj = dcol[j];
+    for (int p = __ldg(P->AT.ptr + j); p < __ldg(P->AT.ptr + j + 1); ++p)
+      tv[p] = (tv[p] * drow[__ldg(P->AT.idx + p)]) * dj;
+    c[j] = c[j] * dj;
+  }
 }
 
 // certificate scan C1: candidate norms and finiteness
@@ -2380,7 +2547,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_baseline(con
 // ---------------------------------------------------------------------------
 // RK = false: one GPU, P in the constant bank (loop_kernel).  RK = true: one
 // rank of a row-partitioned team (loop_kernel_team), P in shared memory.
-template <bool RK, bool BOX = false, int LM = 2, bool CB = false, int EX = 2>
+// SU (teams): the setup modes (power iteration, KKT, preconditioning) in their
+// own kernel (team_setup_kernel), so the loop's register allocation is not
+// charged for them.
+template <bool RK, bool BOX = false, int LM = 2, bool CB = false, int EX = 2, bool SU = false>
 __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
   __shared__ Ctl C;
   __shared__ double tot[kMaxQ];
@@ -2427,10 +2597,11 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
     else return *reinterpret_cast<volatile unsigned*>(&bar->time_up[pr]);
   };
 
-  if (!RK && C.mode == kModePower) {
-    // power_iteration loop body, src/sparse_matrix.cpp:153-177
+  if ((!RK || SU) && C.mode == kModePower) {
+    // power_iteration loop body, src/sparse_matrix.cpp:153-177 (a team: each
+    // rank its rows / columns, the norms over every rank's records)
     while (!R->stop) {
-      power_a<LM, EX>(P, R, stage, ++seq, g);
+      power_a<LM, EX, RK>(P, R, stage, ++seq, g);
       if (!sync()) return;
       {
         const double* rg = region_ptr(P, kRegPA, g.nrec);
@@ -2447,7 +2618,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
       }
       __syncthreads();
       if (R->stop) break;
-      power_b<LM, EX>(P, stage, ++seq, g);
+      power_b<LM, EX, RK>(P, stage, ++seq, g);
       if (!sync()) return;
       {
         const double* rg = region_ptr(P, kRegPB, g.nrec);
@@ -2475,8 +2646,61 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
       }
       __syncthreads();
     }
+    if (threadIdx.x == 0) C.team_epochs = repoch;
     if (writer) ctl_store(C, P->ctl);
     return;
+  }
+  if constexpr (RK && SU) {
+    if (C.mode == kModeKkt) {
+      team_kkt<LM, EX>(P, R, stage, seq + 1, g);
+      seq += 2;
+      if (!sync()) return;
+      const double* rg = region_ptr(P, kRegC1, g.nrec);
+      block_totals(4, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, false}; }, tot, g);
+      if (threadIdx.x == 0) {
+        for (int q = 0; q < 4; ++q) C.kk_tot[q] = tot[q];
+        C.team_epochs = repoch;
+      }
+      if (writer) ctl_store(C, P->ctl);
+      return;
+    }
+    if (C.mode == kModeScale) {
+      // hx_precondition on the team: ruiz rounds, then the
+      // Pock-Chambolle round; every exchange is a push + team barrier
+      const Team& T = P->T;
+      const int n = P->n, m = P->m;
+      const int tid = g.cta * kThreads + threadIdx.x, nth = g.nctas * kThreads;
+      for (int i = T.row0 + tid; i < T.row1; i += nth) P->upool[2 * static_cast<size_t>(n) + m + i] = 1.0;
+      for (int j = T.col0 + tid; j < T.col1; j += nth) P->upool[n + j] = 1.0;
+      for (int k = 0; k < C.sc_ruiz + C.sc_pc; ++k) {
+        const bool ruiz = k < C.sc_ruiz;
+        team_scale_norms(P, g, ruiz ? 0 : 1, ruiz ? 1.0 : 2.0 - C.sc_alpha, ruiz ? 1.0 : C.sc_alpha);
+        if (!sync()) return;
+        team_scale_apply(P, g);
+        if (!sync()) return;
+      }
+      double a2[2] = {0.0, 0.0};
+      for (int i = T.row0 + tid; i < T.row1; i += nth) {
+        const double v = ldcg(P->b + i);
+        a2[0] += v * v;
+      }
+      for (int j = T.col0 + tid; j < T.col1; j += nth) {
+        const double v = ldcg(P->c + j);
+        a2[1] += v * v;
+      }
+      block_to_slots<2, 0, true>(a2, P, kRegC1, g);
+      if (!sync()) return;
+      const double* rg = region_ptr(P, kRegC1, g.nrec);
+      block_totals(2, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, false}; }, tot, g);
+      if (threadIdx.x == 0) {
+        C.sc_bsq = tot[0];
+        C.sc_csq = tot[1];
+        C.team_epochs = repoch;
+      }
+      if (writer) ctl_store(C, P->ctl);
+      return;
+    }
+    return;  // no loop in the setup kernel
   }
 
   unsigned long long* prof = (!RK && P->prof) ? P->prof + blockIdx.x * 16 : nullptr;
@@ -2712,6 +2936,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_team(const _
   const int cta = blockIdx.x % L.grp_ctas;
   const Geo g{cta, L.grp_ctas, P->T.rank * L.grp_ctas + cta, P->T.nranks * L.grp_ctas};
   loop_body<true, false, 2>(P, g);
+}
+
+// The team's setup modes (kModePower / kModeKkt / kModeScale), launched like
+// loop_kernel_team.
+__global__ void __launch_bounds__(kThreads, kMinBlocks) team_setup_kernel(const __grid_constant__ TeamLaunch L) {
+  const int group = blockIdx.x / L.grp_ctas;
+  const KParams* P = &L.p[group];
+  const int cta = blockIdx.x % L.grp_ctas;
+  const Geo g{cta, L.grp_ctas, P->T.rank * L.grp_ctas + cta, P->T.nranks * L.grp_ctas};
+  loop_body<true, false, 2, false, 2, true>(P, g);
 }
 
 // ---------------------------------------------------------------------------
@@ -2968,6 +3202,7 @@ struct hx_ctx {
   int grid = 0;
   std::string err;
   int64_t m = 0, n = 0, nnz = 0;
+  int64_t nnz_a = 0, nnz_t = 0;  // nonzeros this context stores of A and A^T (a rank: its blocks)
   bool uploaded = false, setup_done = false;
   int sum_order = 0;  // hx_set_sum_order: 1 = the reference's sequential row sums
   int64_t launches = 0;
@@ -3025,6 +3260,8 @@ struct hx_ctx {
   unsigned long long team_epochs = 0;
   std::vector<hx_ctx*> local_team;   // ranks launched together (same device), rank order
   std::vector<void*> ipc_open;       // peer mappings to close
+  double* trbuf = nullptr;           // KParams::trbuf (a rank)
+  double* peer_tr[kMaxRanks] = {};   // every rank's trbuf (own included)
 };
 
 namespace {
@@ -3135,6 +3372,8 @@ void free_problem(hx_ctx* c) {
   }
   dfree(c->bpart);
   c->bpart = nullptr;
+  dfree(c->trbuf);
+  c->trbuf = nullptr;
   c->colblock = 0;
   c->a_ptr = c->a_idx = c->t_ptr = c->t_idx = nullptr;
   c->a_val = c->t_val = c->b = c->c = c->xpool = c->ypool = c->axpool = c->upool = nullptr;
@@ -3278,6 +3517,7 @@ KParams team_params(hx_ctx* c) {
   P.AT = c->pt.view;
   P.prof = nullptr;
   P.T = c->team;
+  P.trbuf = c->trbuf;
   return P;
 }
 
@@ -3308,7 +3548,9 @@ int team_issue(const std::vector<hx_ctx*>& ranks, std::vector<KParams>& hp) {
   tl->ranks = static_cast<int>(hp.size());
   tl->grp_ctas = lead->grid;
   void* args[] = {tl.get()};
-  HX_CUDA(lead, cudaLaunchCooperativeKernel(reinterpret_cast<void*>(loop_kernel_team),
+  const void* kernel = lead->h.mode == kModeLoop ? reinterpret_cast<const void*>(loop_kernel_team)
+                                                 : reinterpret_cast<const void*>(team_setup_kernel);
+  HX_CUDA(lead, cudaLaunchCooperativeKernel(kernel,
                                             dim3(static_cast<unsigned>(lead->grid * ranks.size())), dim3(kThreads),
                                             args, kStageBytes, s));
   lead->launches += 1;
@@ -3391,8 +3633,9 @@ int assemble_y(hx_ctx* c, int role) {
   return HPLP_OK;
 }
 
+// A x (A^T y): a rank computes its own rows (columns) only -- the blocks it stores.
 int spmv_dev(hx_ctx* c, bool transpose, const double* x, double* out) {
-  const Sched& S = transpose ? c->st.view : c->sa.view;
+  const Sched& S = c->ranked ? (transpose ? c->pt.view : c->pa.view) : (transpose ? c->st.view : c->sa.view);
   spmv_store_kernel<<<c->grid, kThreads, kStageBytes, c->stream>>>(S, x, out);
   c->launches += 1;
   HX_CUDA(c, cudaGetLastError());
@@ -3546,12 +3789,206 @@ int hx_device_info(hx_ctx* c, int32_t* sm_count, int32_t* grid_ctas, int32_t* ct
 void* hx_stream(hx_ctx* c) { return c->stream; }
 int64_t hx_launch_count(hx_ctx* c) { return c->launches; }
 
+int hx_stored_nonzeros(hx_ctx* c, int64_t* nnz_a, int64_t* nnz_t) {
+  if (!c->uploaded) return set_err(c, HPLP_ESTATE, "hx_stored_nonzeros: no problem uploaded");
+  if (nnz_a) *nnz_a = c->nnz_a;
+  if (nnz_t) *nnz_t = c->nnz_t;
+  return HPLP_OK;
+}
+
 int hx_dims(hx_ctx* c, int64_t* m, int64_t* n, int64_t* nnz) {
   if (m) *m = c->m;
   if (n) *n = c->n;
   if (nnz) *nnz = c->nnz;
   return c->uploaded ? HPLP_OK : set_err(c, HPLP_ESTATE, "hx_dims: no problem uploaded");
 }
+
+namespace {
+// The ranks this process launches together (hx_team_bind / a lone rank of a
+// multi-process team), rank order, checked complete.
+int team_ranks(hx_ctx* c, std::vector<hx_ctx*>& ranks) {
+  ranks = c->local_team.empty() ? std::vector<hx_ctx*>{c} : c->local_team;
+  std::sort(ranks.begin(), ranks.end(), [](hx_ctx* a, hx_ctx* b) { return a->team.rank < b->team.rank; });
+  for (hx_ctx* r : ranks) {
+    if (!r->ranked || r->team.nranks == 0)
+      return set_err(c, HPLP_ESTATE, "hx: rank is not part of a usable team");
+    for (int q = 0; q < r->team.nranks; ++q)
+      if (!r->team.px[q] || !r->team.py[q] || !r->team.pu[q] || !r->team.ps[q] || !r->team.pb[q] || !r->peer_tr[q])
+        return set_err(c, HPLP_ESTATE, "hx: team incomplete (bind or import every rank first)");
+  }
+  return HPLP_OK;
+}
+
+// One launch of a team setup mode (kModePower / kModeKkt / kModeScale) with
+// the controllers the caller prepared in every rank's host mirror.
+int team_mode_launch(hx_ctx* c, const std::vector<hx_ctx*>& ranks) {
+  const int rc = team_launch(ranks);
+  if (rc) c->err = ranks.front()->err;
+  return rc;
+}
+}  // namespace
+
+namespace {
+// One rank of a row-partitioned team (hx_set_partition): the
+// context stores ONLY its blocks -- rows [row0, row1) of A and columns
+// [col0, col1) of A (the rows of A^T it owns), both cut on the host from the
+// caller's CSR -- plus full-length b, c and iterate pools (the pools double
+// as receive buffers: peers push the x+ / y entries this rank gathers into
+// them at their global offsets).  Device memory is O(nnz / nranks + m + n),
+// so an LP whose matrix exceeds one GPU fits on the team.  The schedules
+// index the blocks through pointers offset by row0 / col0, so the kernels
+// keep global row indices.
+int upload_ranked(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx, const double* val,
+                  const double* b, const double* cc) {
+  Team& T = c->team;
+  if (T.row1 > m || T.col1 > n)
+    return set_err(c, HPLP_EINVAL, "hx_upload_csr: partition range exceeds the problem (hx_set_partition)");
+  if (c->prow1[T.nranks - 1] != m || c->pcol1[T.nranks - 1] != n)
+    return set_err(c, HPLP_EINVAL, "hx_upload_csr: the partition does not cover the problem");
+  const int64_t nnz = row_ptr[m];
+  // the whole matrix is validated on every rank (the same error everywhere);
+  // the checks of validate_kernel, on the host copy the caller passed
+  for (int64_t i = 0; i < m; ++i) {
+    if (row_ptr[i + 1] < row_ptr[i]) return set_err(c, HPLP_EINVAL, "hx_upload_csr: row_ptr is not monotone");
+    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+      const int j = col_idx[p];
+      if (j < 0 || j >= n) return set_err(c, HPLP_EINVAL, "SparseMatrix: entry out of range");
+      if (!std::isfinite(val[p])) return set_err(c, HPLP_EINVAL, "SparseMatrix: non-finite value");
+      if (p > row_ptr[i] && j == col_idx[p - 1]) return set_err(c, HPLP_EINVAL, "SparseMatrix: duplicate entry");
+      if (p > row_ptr[i] && j < col_idx[p - 1])
+        return set_err(c, HPLP_EINVAL, "hx_upload_csr: columns must ascend within each row (sort on the host)");
+    }
+  }
+  const int row0 = T.row0, row1 = T.row1, col0 = T.col0, col1 = T.col1;
+  const int ml = row1 - row0, nl = col1 - col0;
+  // A's row block: the caller's arrays from row_ptr[row0]
+  std::vector<int> ap(static_cast<size_t>(ml) + 1);
+  const int64_t pa0 = row_ptr[row0];
+  for (int i = 0; i <= ml; ++i) ap[i] = static_cast<int>(row_ptr[row0 + i] - pa0);
+  const int64_t nnz_a = ap[ml];
+  // A^T's row block = A's columns [col0, col1), rows ascending per column
+  std::vector<int> tp(static_cast<size_t>(nl) + 1, 0);
+  for (int64_t p = 0; p < nnz; ++p) {
+    const int j = col_idx[p];
+    if (j >= col0 && j < col1) ++tp[j - col0 + 1];
+  }
+  for (int k = 0; k < nl; ++k) tp[k + 1] += tp[k];
+  const int64_t nnz_t = tp[nl];
+  std::vector<int> ti(static_cast<size_t>(nnz_t));
+  std::vector<double> tv(static_cast<size_t>(nnz_t));
+  {
+    std::vector<int> fill(tp.begin(), tp.end() - 1);
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+        const int j = col_idx[p];
+        if (j < col0 || j >= col1) continue;
+        const int q = fill[j - col0]++;
+        ti[q] = static_cast<int>(i);
+        tv[q] = val[p];
+      }
+  }
+  cudaStream_t s = c->stream;
+  c->m = m, c->n = n, c->nnz = nnz;
+  c->nnz_a = nnz_a, c->nnz_t = nnz_t;
+  HX_CUDA(c, dalloc(&c->a_ptr, static_cast<size_t>(ml) + 1));
+  HX_CUDA(c, dalloc(&c->a_idx, static_cast<size_t>(nnz_a) + kMatrixPad));
+  HX_CUDA(c, dalloc(&c->a_val, static_cast<size_t>(nnz_a) + kMatrixPad));
+  HX_CUDA(c, dalloc(&c->t_ptr, static_cast<size_t>(nl) + 1));
+  HX_CUDA(c, dalloc(&c->t_idx, static_cast<size_t>(nnz_t) + kMatrixPad));
+  HX_CUDA(c, dalloc(&c->t_val, static_cast<size_t>(nnz_t) + kMatrixPad));
+  HX_CUDA(c, dalloc(&c->b, m));
+  HX_CUDA(c, dalloc(&c->c, n));
+  HX_CUDA(c, cudaMemcpyAsync(c->a_ptr, ap.data(), ap.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  if (nnz_a) {
+    HX_CUDA(c, cudaMemcpyAsync(c->a_idx, col_idx + pa0, nnz_a * sizeof(int), cudaMemcpyHostToDevice, s));
+    HX_CUDA(c, cudaMemcpyAsync(c->a_val, val + pa0, nnz_a * sizeof(double), cudaMemcpyHostToDevice, s));
+  }
+  HX_CUDA(c, cudaMemcpyAsync(c->t_ptr, tp.data(), tp.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  if (nnz_t) {
+    HX_CUDA(c, cudaMemcpyAsync(c->t_idx, ti.data(), nnz_t * sizeof(int), cudaMemcpyHostToDevice, s));
+    HX_CUDA(c, cudaMemcpyAsync(c->t_val, tv.data(), nnz_t * sizeof(double), cudaMemcpyHostToDevice, s));
+  }
+  if (m) HX_CUDA(c, cudaMemcpyAsync(c->b, b, m * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (n) HX_CUDA(c, cudaMemcpyAsync(c->c, cc, n * sizeof(double), cudaMemcpyHostToDevice, s));
+  HX_CUDA(c, cudaStreamSynchronize(s));  // the host vectors go out of scope
+  // schedules of the blocks; rows / columns stay global through offset pointers
+  double lead = 1200.0;
+  if (const char* e = std::getenv("HX_LEAD")) lead = std::atof(e);
+  const bool exact = c->sum_order == HX_SUM_REFERENCE;
+  const int warps = c->grid * kWarps;
+  double rca, tca, rct, tct;
+  sched_costs(false, rca, tca);
+  sched_costs(true, rct, tct);
+  int rc = upload_built_sched(c, c->pa, build_schedule(ap.data(), ml, warps, 0.0, rca, tca, exact), ml,
+                              static_cast<int>(n), c->a_ptr - row0, c->a_idx, c->a_val, row0);
+  if (rc) return rc;
+  rc = upload_built_sched(c, c->pt, build_schedule(tp.data(), nl, warps, lead, rct, tct, exact), nl,
+                          static_cast<int>(m), c->t_ptr - col0, c->t_idx, c->t_val, col0);
+  if (rc) return rc;
+  // who gathers what: x+_j is read by the owners of the rows in column j,
+  // y_i by the owners of the columns in row i
+  auto owner = [&](const int* lo, int v) {
+    int r = 0;
+    while (r + 1 < T.nranks && v >= lo[r + 1]) ++r;
+    return r;
+  };
+  std::vector<unsigned char> xm(static_cast<size_t>(nl), 0), ym(static_cast<size_t>(ml), 0);
+  for (int64_t i = 0; i < m; ++i) {
+    const int oi = owner(c->prow0, static_cast<int>(i));
+    const bool own_row = i >= row0 && i < row1;
+    for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+      const int j = col_idx[p];
+      if (oi != T.rank && j >= col0 && j < col1) xm[j - col0] |= static_cast<unsigned char>(1u << oi);
+      if (own_row) {
+        const int oj = owner(c->pcol0, j);
+        if (oj != T.rank) ym[i - row0] |= static_cast<unsigned char>(1u << oj);
+      }
+    }
+  }
+  dfree(c->xneed), dfree(c->yneed);
+  HX_CUDA(c, dalloc(&c->xneed, std::max<size_t>(1, xm.size())));
+  HX_CUDA(c, dalloc(&c->yneed, std::max<size_t>(1, ym.size())));
+  if (!xm.empty()) HX_CUDA(c, cudaMemcpy(c->xneed, xm.data(), xm.size(), cudaMemcpyHostToDevice));
+  if (!ym.empty()) HX_CUDA(c, cudaMemcpy(c->yneed, ym.data(), ym.size(), cudaMemcpyHostToDevice));
+  T.xneed = c->xneed;
+  T.yneed = c->yneed;
+  // L2 policy from this rank's blocks and vectors
+  int l2 = 0;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device);
+  const double footprint = 12.0 * static_cast<double>(nnz_a + nnz_t) + 8.0 * (6.0 * n + 10.0 * m);
+  int hint = footprint > 0.7 * static_cast<double>(l2) ? 1 : 0;
+  if (const char* e = std::getenv("HPLP_L2_STREAM")) hint = std::atoi(e) != 0 ? 1 : 0;
+  c->pa.view.stream_hint = c->pt.view.stream_hint = hint;
+  c->pa.view.row_limit = static_cast<int>(m);
+  c->pt.view.row_limit = static_cast<int>(n);
+  c->pa.view.exact = c->pt.view.exact = exact ? 1 : 0;
+  // pools (peers map them through CUDA IPC)
+  HX_CUDA(c, dalloc_ipc(&c->xpool, static_cast<size_t>(kXPool) * n));
+  HX_CUDA(c, dalloc_ipc(&c->ypool, static_cast<size_t>(kYPool) * m));
+  HX_CUDA(c, dalloc_ipc(&c->upool, 2 * static_cast<size_t>(n) + 2 * static_cast<size_t>(m)));
+  HX_CUDA(c, dalloc(&c->axpool, static_cast<size_t>(kAxPool) * m));
+  HX_CUDA(c, dalloc_ipc(&c->trbuf, 2 * static_cast<size_t>(std::max<int64_t>(n, 1))));
+  for (int r = 0; r < kMaxRanks; ++r) c->peer_tr[r] = nullptr;
+  c->peer_tr[T.rank] = c->trbuf;
+  for (int r = 0; r < kMaxRanks; ++r) T.px[r] = T.py[r] = T.pu[r] = T.ps[r] = nullptr, T.pb[r] = nullptr;
+  T.px[T.rank] = c->xpool, T.py[T.rank] = c->ypool, T.pu[T.rank] = c->upool, T.ps[T.rank] = c->slots;
+  T.pb[T.rank] = c->rbar;
+  c->local_team.assign(1, c);
+  // ||b||, ||c|| once, from the full vectors every rank holds
+  kkt_partials_kernel<<<c->grid, kThreads, 0, s>>>(static_cast<int>(m), static_cast<int>(n), nullptr, c->b, nullptr,
+                                                   c->c, nullptr, nullptr, c->slots);
+  final_reduce_kernel<<<1, 256, 0, s>>>(c->slots, c->grid, 6, c->scratch);
+  double tot[6];
+  HX_CUDA(c, cudaMemcpyAsync(tot, c->scratch, sizeof(tot), cudaMemcpyDeviceToHost, s));
+  HX_CUDA(c, cudaStreamSynchronize(s));
+  c->launches += 2 + (nnz_a || nnz_t ? 2 : 0);
+  c->b_sq = tot[4];
+  c->b_norm = std::sqrt(tot[4]);
+  c->c_norm = std::sqrt(tot[5]);
+  c->uploaded = true;
+  return HPLP_OK;
+}
+}  // namespace
 
 int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
                   const double* val, const double* b, const double* cc) {
@@ -3566,7 +4003,9 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     if (!std::isfinite(b[i])) return set_err(c, HPLP_EINVAL, "StandardFormLP: non-finite b or c");
   for (int64_t j = 0; j < n; ++j)
     if (!std::isfinite(cc[j])) return set_err(c, HPLP_EINVAL, "StandardFormLP: non-finite b or c");
+  if (c->ranked) return upload_ranked(c, m, n, row_ptr, col_idx, val, b, cc);
   c->m = m, c->n = n, c->nnz = nnz;
+  c->nnz_a = c->nnz_t = nnz;
   // A's schedule needs only the host row pointers: build it on a host thread
   // while the matrix copies and A^T forms on the device
   std::vector<int> ph(static_cast<size_t>(m) + 1);
@@ -3689,46 +4128,6 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
                             c->t_val, 0);
     if (rc) return rc;
     tick("sched A^T");
-    if (c->ranked) {  // this rank's blocks: rows [row0,row1) of A, [col0,col1) of A^T
-      Team& T = c->team;
-      if (T.row1 > m || T.col1 > n)
-        return set_err(c, HPLP_EINVAL, "hx_upload_csr: partition range exceeds the problem (hx_set_partition)");
-      rc = upload_sched(c, c->pa, ph.data(), T.row1 - T.row0, static_cast<int>(n), c->a_ptr, c->a_idx, c->a_val, 0.0,
-                        T.row0);
-      if (rc) return rc;
-      rc = upload_sched(c, c->pt, pt.data(), T.col1 - T.col0, static_cast<int>(m), c->t_ptr, c->t_idx, c->t_val, lead,
-                        T.col0, true);
-      if (rc) return rc;
-      // who gathers what: x+_j is read by the owners of the rows in column j,
-      // y_i by the owners of the columns in row i
-      if (c->prow1[T.nranks - 1] != m || c->pcol1[T.nranks - 1] != n)
-        return set_err(c, HPLP_EINVAL, "hx_upload_csr: the partition does not cover the problem");
-      auto owner = [&](const int* lo, int v) {
-        int r = 0;
-        while (r + 1 < T.nranks && v >= lo[r + 1]) ++r;
-        return r;
-      };
-      std::vector<unsigned char> xm(static_cast<size_t>(T.col1 - T.col0), 0), ym(static_cast<size_t>(T.row1 - T.row0), 0);
-      for (int64_t i = 0; i < m; ++i) {
-        const int oi = owner(c->prow0, static_cast<int>(i));
-        const bool own_row = i >= T.row0 && i < T.row1;
-        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
-          const int j = col_idx[p];
-          if (oi != T.rank && j >= T.col0 && j < T.col1) xm[j - T.col0] |= static_cast<unsigned char>(1u << oi);
-          if (own_row) {
-            const int oj = owner(c->pcol0, j);
-            if (oj != T.rank) ym[i - T.row0] |= static_cast<unsigned char>(1u << oj);
-          }
-        }
-      }
-      dfree(c->xneed), dfree(c->yneed);
-      HX_CUDA(c, dalloc(&c->xneed, xm.size()));
-      HX_CUDA(c, dalloc(&c->yneed, ym.size()));
-      if (!xm.empty()) HX_CUDA(c, cudaMemcpy(c->xneed, xm.data(), xm.size(), cudaMemcpyHostToDevice));
-      if (!ym.empty()) HX_CUDA(c, cudaMemcpy(c->yneed, ym.data(), ym.size(), cudaMemcpyHostToDevice));
-      T.xneed = c->xneed;
-      T.yneed = c->yneed;
-    }
   }
   {
     // per-iteration working set of the loop: the matrix copies this context
@@ -3736,23 +4135,14 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     // iteration touches; beyond ~70% of L2 the matrix streams get evict_first
     int l2 = 0;
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device);
-    int64_t streamed = 2 * nnz;
-    if (c->ranked) {
-      const Team& T = c->team;
-      streamed = row_ptr[T.row1] - row_ptr[T.row0];
-      int tp0 = 0, tp1 = 0;
-      cudaMemcpy(&tp0, c->t_ptr + T.col0, sizeof(int), cudaMemcpyDeviceToHost);
-      cudaMemcpy(&tp1, c->t_ptr + T.col1, sizeof(int), cudaMemcpyDeviceToHost);
-      streamed += tp1 - tp0;
-    }
+    const int64_t streamed = 2 * nnz;
     const double footprint = 12.0 * static_cast<double>(streamed) + 8.0 * (6.0 * n + 10.0 * m);
     int hint = footprint > 0.7 * static_cast<double>(l2) ? 1 : 0;
     if (const char* e = std::getenv("HPLP_L2_STREAM")) hint = std::atoi(e) != 0 ? 1 : 0;
     c->sa.view.stream_hint = c->st.view.stream_hint = hint;
-    c->sa.view.row_limit = c->pa.view.row_limit = static_cast<int>(m);  // output dimension (HX_CHECKED)
-    c->st.view.row_limit = c->pt.view.row_limit = static_cast<int>(n);
-    c->pa.view.stream_hint = c->pt.view.stream_hint = hint;
-    c->sa.view.exact = c->st.view.exact = c->pa.view.exact = c->pt.view.exact = exact ? 1 : 0;
+    c->sa.view.row_limit = static_cast<int>(m);  // output dimension (HX_CHECKED)
+    c->st.view.row_limit = static_cast<int>(n);
+    c->sa.view.exact = c->st.view.exact = exact ? 1 : 0;
     // Column-blocked phase B (loop_kernel_stream_cb): when x+ is far larger
     // than L2 its random gathers miss (configs[4]: 9.5 GB of DRAM traffic per
     // iteration against 5.0 GB algorithmic, L2 hit rate 38%), so A is split at
@@ -3764,7 +4154,7 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     int want = hint && 8.0 * static_cast<double>(n) > 64e6 ? 1 : 0;
     if (const char* e = std::getenv("HX_COLBLOCK")) want = std::atoi(e) != 0 ? 1 : 0;
     // the reference order sums each row in one chain: no split at a column
-    if (want && !c->ranked && nnz > 0 && !exact) {
+    if (want && nnz > 0 && !exact) {
       std::vector<int> pt(static_cast<size_t>(n) + 1);
       HX_CUDA(c, cudaMemcpy(pt.data(), c->t_ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost));
       const int split = static_cast<int>(std::lower_bound(pt.begin(), pt.end(), static_cast<int>(nnz / 2)) - pt.begin());
@@ -3822,23 +4212,10 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     }
   }
   tick("schedules");
-  if (c->ranked) {  // peers map these through CUDA IPC
-    HX_CUDA(c, dalloc_ipc(&c->xpool, static_cast<size_t>(kXPool) * n));
-    HX_CUDA(c, dalloc_ipc(&c->ypool, static_cast<size_t>(kYPool) * m));
-    HX_CUDA(c, dalloc_ipc(&c->upool, 2 * static_cast<size_t>(n) + 2 * static_cast<size_t>(m)));
-  } else {
-    HX_CUDA(c, dalloc(&c->xpool, static_cast<size_t>(kXPool) * n));
-    HX_CUDA(c, dalloc(&c->ypool, static_cast<size_t>(kYPool) * m));
-    HX_CUDA(c, dalloc(&c->upool, 2 * static_cast<size_t>(n) + 2 * static_cast<size_t>(m)));
-  }
+  HX_CUDA(c, dalloc(&c->xpool, static_cast<size_t>(kXPool) * n));
+  HX_CUDA(c, dalloc(&c->ypool, static_cast<size_t>(kYPool) * m));
+  HX_CUDA(c, dalloc(&c->upool, 2 * static_cast<size_t>(n) + 2 * static_cast<size_t>(m)));
   HX_CUDA(c, dalloc(&c->axpool, static_cast<size_t>(kAxPool) * m));
-  if (c->ranked) {
-    Team& T = c->team;
-    for (int r = 0; r < kMaxRanks; ++r) T.px[r] = T.py[r] = T.pu[r] = T.ps[r] = nullptr, T.pb[r] = nullptr;
-    T.px[T.rank] = c->xpool, T.py[T.rank] = c->ypool, T.pu[T.rank] = c->upool, T.ps[T.rank] = c->slots;
-    T.pb[T.rank] = c->rbar;
-    c->local_team.assign(1, c);
-  }
   // ||b||, ||c|| once (loop invariants of src/pdhg_core.cpp:60,62).
   kkt_partials_kernel<<<c->grid, kThreads, 0, s>>>(static_cast<int>(m), static_cast<int>(n), nullptr, c->b,
                                                    nullptr, c->c, nullptr, nullptr, c->slots);
@@ -3874,6 +4251,43 @@ int32_t hx_sum_order(hx_ctx* c) { return c ? c->sum_order : -1; }
 int hx_precondition(hx_ctx* c, int32_t ruiz_iters, double pc_alpha, double* row_scale, double* col_scale) {
   if (!c->uploaded) return set_err(c, HPLP_ESTATE, "hx_precondition: no problem uploaded");
   if (ruiz_iters < 0) return set_err(c, HPLP_EINVAL, "hx_precondition: ruiz_iters must be >= 0");
+  if (c->ranked) {
+    // a team: kModeScale on every rank of this process at once (every
+    // process calls it for its rank); the scales of the rows / columns a rank
+    // owns are pushed to the peers that scale entries of them, and the
+    // accumulated R (u3) / C (u2) come back from their owners
+    std::vector<hx_ctx*> ranks;
+    if (int rc = team_ranks(c, ranks)) return rc;
+    for (hx_ctx* r : ranks) {
+      Ctl& C = r->h;
+      std::memset(&C, 0, sizeof(Ctl));
+      C.mode = kModeScale;
+      C.sc_ruiz = ruiz_iters;
+      C.sc_pc = pc_alpha >= 0.0 ? 1 : 0;
+      C.sc_alpha = pc_alpha;
+      r->setup_done = false;
+    }
+    int rc = team_mode_launch(c, ranks);
+    for (hx_ctx* r : ranks) r->h.mode = kModeLoop;
+    if (rc) return rc;
+    for (hx_ctx* r : ranks) {
+      r->b_sq = r->h.sc_bsq;
+      r->b_norm = std::sqrt(r->h.sc_bsq);
+      r->c_norm = std::sqrt(r->h.sc_csq);
+    }
+    HX_CUDA(c, cudaSetDevice(c->device));
+    const int64_t m = c->m, n = c->n;
+    for (int q = 0; q < c->team.nranks; ++q) {
+      const double* pu = c->team.pu[q];
+      if (row_scale && c->prow1[q] > c->prow0[q])
+        HX_CUDA(c, cudaMemcpy(row_scale + c->prow0[q], pu + 2 * n + m + c->prow0[q],
+                              (c->prow1[q] - c->prow0[q]) * sizeof(double), cudaMemcpyDefault));
+      if (col_scale && c->pcol1[q] > c->pcol0[q])
+        HX_CUDA(c, cudaMemcpy(col_scale + c->pcol0[q], pu + n + c->pcol0[q],
+                              (c->pcol1[q] - c->pcol0[q]) * sizeof(double), cudaMemcpyDefault));
+    }
+    return HPLP_OK;
+  }
   cudaStream_t s = c->stream;
   const int m = static_cast<int>(c->m), n = static_cast<int>(c->n);
   const int nb = 4 * c->sm_count;
@@ -3977,8 +4391,10 @@ int hx_set_box(hx_ctx* c, const double* upper) {
 }
 
 // The device problem (after any preconditioning) as CSR + b + c.
+
 int hx_download_problem(hx_ctx* c, int64_t* row_ptr, int32_t* col_idx, double* val, double* b, double* cc) {
   if (!c->uploaded) return set_err(c, HPLP_ESTATE, "hx_download_problem: no problem uploaded");
+  if (c->ranked) return set_err(c, HPLP_EINVAL, "hx_download_problem: a rank stores only its blocks");
   cudaStream_t s = c->stream;
   if (row_ptr) {
     std::vector<int> rp(static_cast<size_t>(c->m) + 1);
@@ -3998,6 +4414,7 @@ int hx_spmv(hx_ctx* c, const double* x, double* out) {
   double* dx = c->upool;
   double* dout = c->upool + 2 * c->n;
   HX_CUDA(c, cudaMemcpyAsync(dx, x, c->n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  if (c->ranked) HX_CUDA(c, cudaMemsetAsync(dout, 0, c->m * sizeof(double), c->stream));  // a rank: its rows only
   int rc = spmv_dev(c, false, dx, dout);
   if (rc) return rc;
   HX_CUDA(c, cudaMemcpyAsync(out, dout, c->m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -4010,6 +4427,7 @@ int hx_spmv_transpose(hx_ctx* c, const double* y, double* out) {
   double* dy = c->upool + 2 * c->n;
   double* dout = c->upool;
   HX_CUDA(c, cudaMemcpyAsync(dy, y, c->m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  if (c->ranked) HX_CUDA(c, cudaMemsetAsync(dout, 0, c->n * sizeof(double), c->stream));  // a rank: its columns only
   int rc = spmv_dev(c, true, dy, dout);
   if (rc) return rc;
   HX_CUDA(c, cudaMemcpyAsync(out, dout, c->n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -4020,20 +4438,32 @@ int hx_spmv_transpose(hx_ctx* c, const double* y, double* out) {
 int hx_power_iteration(hx_ctx* c, const double* x0, double tol, int64_t k0, int64_t max_iters, double sigma_prev,
                        double* sigma, int64_t* iters, int32_t* converged, int32_t* need_redraw) {
   if (!c->uploaded) return set_err(c, HPLP_ESTATE, "hx_power_iteration: no problem uploaded");
-  HX_CUDA(c, cudaMemcpyAsync(xbuf(c, 0), x0, c->n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  // a team: every rank of this process (every process calls it for its own
+  // rank), each on its blocks; the start vector is on every rank in full
+  std::vector<hx_ctx*> ranks{c};
+  if (c->ranked)
+    if (int rc = team_ranks(c, ranks)) return rc;
+  for (hx_ctx* r : ranks) {
+    HX_CUDA(c, cudaSetDevice(r->device));
+    HX_CUDA(c, cudaMemcpyAsync(xbuf(r, 0), x0, r->n * sizeof(double), cudaMemcpyHostToDevice, r->stream));
+    HX_CUDA(c, cudaStreamSynchronize(r->stream));
+    Ctl& C = r->h;
+    std::memset(&C, 0, sizeof(Ctl));
+    C.mode = kModePower;
+    C.pw_k = k0;
+    C.pw_max = max_iters;
+    C.pw_tol = tol;
+    C.pw_sigma_prev = sigma_prev;
+    C.pw_sigma = sigma_prev;  // res.sigma == sigma_prev between iterations
+    C.pw_iters = k0;
+    C.r.pw_mode = 0;
+    C.r.stop = k0 >= max_iters ? 1 : 0;
+    r->setup_done = false;
+  }
+  HX_CUDA(c, cudaSetDevice(c->device));
   Ctl& C = c->h;
-  std::memset(&C, 0, sizeof(Ctl));
-  C.mode = kModePower;
-  C.pw_k = k0;
-  C.pw_max = max_iters;
-  C.pw_tol = tol;
-  C.pw_sigma_prev = sigma_prev;
-  C.pw_sigma = sigma_prev;  // res.sigma == sigma_prev between iterations
-  C.pw_iters = k0;
-  C.r.pw_mode = 0;
-  C.r.stop = k0 >= max_iters ? 1 : 0;
   if (!C.r.stop) {
-    int rc = launch_loop(c);
+    int rc = c->ranked ? team_mode_launch(c, ranks) : launch_loop(c);
     if (rc) return rc;
   }
   *sigma = C.pw_sigma;
@@ -4106,6 +4536,7 @@ int hx_setup(hx_ctx* c, const hplp_config_t* cfg, double sigma_used, double eta,
   R.y_cur = 0, R.y_anchor = 0, R.yp_out = 1, R.yc_out = 2;
   R.ax_cur = 0, R.ax_anchor = 0, R.axp_out = 1, R.axc_out = 2;
   R.w_next = 0.5;  // 1/(k+2) at k = 0
+  R.tr_slot = C.trace_period > 0 && C.scheme == HPLP_SCHEME_RHPDHG ? 0 : -1;  // iteration 0
   R.stop = 0;
   HX_CUDA(c, cudaMemsetAsync(c->epochs, 0, kEpochCap * sizeof(hplp_epoch_t), s));
   HX_CUDA(c, cudaStreamSynchronize(s));
@@ -4329,6 +4760,7 @@ int hx_team_bind(hx_ctx** ctxs, int32_t count) {
     for (int r = 0; r < count; ++r) {
       T.px[r] = by[r]->xpool, T.py[r] = by[r]->ypool, T.pu[r] = by[r]->upool, T.ps[r] = by[r]->slots;
       T.pb[r] = by[r]->rbar;
+      c->peer_tr[r] = by[r]->trbuf;
     }
     c->local_team = by;
   }
@@ -4340,7 +4772,7 @@ struct TeamBlob {
   int32_t magic, rank, nranks, grid;
   int64_t m, n, nnz;
   int32_t row0, row1, col0, col1;
-  cudaIpcMemHandle_t hx, hy, hu, hs, hb;
+  cudaIpcMemHandle_t hx, hy, hu, hs, hb, ht;
 };
 constexpr int32_t kBlobMagic = 0x48585442;  // "HXTB"
 }  // namespace
@@ -4360,6 +4792,7 @@ int hx_team_export(hx_ctx* c, void* blob, int64_t capacity, int64_t* size) {
   HX_CUDA(c, cudaIpcGetMemHandle(&b.hu, c->upool));
   HX_CUDA(c, cudaIpcGetMemHandle(&b.hs, c->slots));
   HX_CUDA(c, cudaIpcGetMemHandle(&b.hb, c->rbar));
+  HX_CUDA(c, cudaIpcGetMemHandle(&b.ht, c->trbuf));
   std::memcpy(blob, &b, sizeof(b));
   return HPLP_OK;
 }
@@ -4378,9 +4811,9 @@ int hx_team_import(hx_ctx* c, const void* blob, int64_t size) {
     return set_err(c, HPLP_EINVAL, "hx_team_import: the peer was given a different partition");
   if (b.rank == c->team.rank) return HPLP_OK;
   HX_CUDA(c, cudaSetDevice(c->device));
-  void* p[5] = {};
-  const cudaIpcMemHandle_t* h[5] = {&b.hx, &b.hy, &b.hu, &b.hs, &b.hb};
-  for (int k = 0; k < 5; ++k) {
+  void* p[6] = {};
+  const cudaIpcMemHandle_t* h[6] = {&b.hx, &b.hy, &b.hu, &b.hs, &b.hb, &b.ht};
+  for (int k = 0; k < 6; ++k) {
     HX_CUDA(c, cudaIpcOpenMemHandle(&p[k], *h[k], cudaIpcMemLazyEnablePeerAccess));
     c->ipc_open.push_back(p[k]);
   }
@@ -4391,6 +4824,7 @@ int hx_team_import(hx_ctx* c, const void* blob, int64_t size) {
   T.pu[b.rank] = static_cast<double*>(p[2]);
   T.ps[b.rank] = static_cast<double*>(p[3]);
   T.pb[b.rank] = static_cast<RankBar*>(p[4]);
+  c->peer_tr[b.rank] = static_cast<double*>(p[5]);
   return HPLP_OK;
 }
 
@@ -4525,8 +4959,36 @@ int hx_get_certificate(hx_ctx* c, int32_t kind, double* vec) {
 // (2/k)(z - anchor) with its carried product; NaN when k = 0 (undefined), for
 // a multi-rank context (A x is rank-local), or when the quadratic form is
 // clearly negative.
+int hx_trace_reduced_costs(hx_ctx* c, double* rc) {
+  if (!c->setup_done) return set_err(c, HPLP_ESTATE, "hx_trace_reduced_costs: no solve state");
+  const Ctl& C = c->h;
+  if (c->ranked) {
+    // phase A of the traced iteration wrote c_j + (A^T y)_j of its own
+    // columns into its trace slot; the team's final barrier ordered every
+    // rank's writes before this launch ended
+    if (C.trace_period <= 0 || C.last_it % C.trace_period != 0)
+      return set_err(c, HPLP_ESTATE, "hx_trace_reduced_costs: the last iteration was not traced");
+    const size_t slot = static_cast<size_t>(C.last_it & 1) * c->n;
+    HX_CUDA(c, cudaSetDevice(c->device));
+    for (int q = 0; q < c->team.nranks; ++q) {
+      if (!c->peer_tr[q]) return set_err(c, HPLP_ESTATE, "hx_trace_reduced_costs: team incomplete");
+      const int64_t len = c->pcol1[q] - c->pcol0[q];
+      if (len > 0)
+        HX_CUDA(c, cudaMemcpy(rc + c->pcol0[q], c->peer_tr[q] + slot + c->pcol0[q], len * sizeof(double),
+                              cudaMemcpyDefault));
+    }
+    return HPLP_OK;
+  }
+  std::vector<double> cv(static_cast<size_t>(c->n));
+  if (int r = hx_trace_extras(c, rc, cv.data(), nullptr)) return r;
+  for (int64_t j = 0; j < c->n; ++j) rc[j] = cv[j] + rc[j];  // lp.c + sr.at_y (src/solver.cpp:278-279)
+  return HPLP_OK;
+}
+
 int hx_trace_extras(hx_ctx* c, double* aty, double* c_out, double* cand_norm_normalized) {
   if (!c->setup_done) return set_err(c, HPLP_ESTATE, "hx_trace_extras: no solve state");
+  if (c->ranked && (aty || c_out))
+    return set_err(c, HPLP_EINVAL, "hx_trace_extras: a rank stores only its blocks (hx_trace_reduced_costs)");
   const Ctl& C = c->h;
   cudaStream_t s = c->stream;
   if (aty || c_out) {
@@ -4569,6 +5031,23 @@ int hx_trace_extras(hx_ctx* c, double* aty, double* c_out, double* cand_norm_nor
 
 int hx_kkt_current(hx_ctx* c, hplp_kkt_t* out) {
   if (!c->setup_done) return set_err(c, HPLP_ESTATE, "hx_kkt_current: no solve state");
+  if (c->ranked) {
+    // a team: kModeKkt -- each rank's rows / columns with fresh products
+    // gathered from its pools (the x / y entries it reads were pushed to it),
+    // totals over every rank's records
+    std::vector<hx_ctx*> ranks;
+    if (int rc = team_ranks(c, ranks)) return rc;
+    for (hx_ctx* r : ranks) r->h.mode = kModeKkt;
+    const int rc = team_mode_launch(c, ranks);
+    for (hx_ctx* r : ranks) r->h.mode = kModeLoop;
+    if (rc) return rc;
+    const double* t = c->h.kk_tot;
+    out->primal_residual = std::sqrt(t[0]) / (1.0 + c->b_norm);
+    out->dual_residual = std::sqrt(t[1]) / (1.0 + c->c_norm);
+    out->gap_residual = std::fabs(t[2] + t[3]) / (1.0 + std::fabs(t[2]) + std::fabs(t[3]));
+    out->max_relative = std::max({out->primal_residual, out->dual_residual, out->gap_residual});
+    return HPLP_OK;
+  }
   const Ctl& C = c->h;
   cudaStream_t s = c->stream;
   // current z: materialize x into u-scratch, y from its buffer

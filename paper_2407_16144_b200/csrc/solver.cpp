@@ -605,9 +605,8 @@ SolveResult Solver::solve_core(const SolverConfig& config) {
       col_scale_.assign(static_cast<std::size_t>(n_), 1.0);
       check(ctx, hx_precondition(ctx, config.precondition_ruiz_iters, config.precondition_pc_alpha, row_scale_.data(),
                                  col_scale_.data()));
-      for (std::size_t r = 1; r < ranks_.size(); ++r)  // every rank holds the same transformed problem
-        check(ranks_[r], hx_precondition(ranks_[r], config.precondition_ruiz_iters, config.precondition_pc_alpha,
-                                         nullptr, nullptr));
+      // a team: that one call scaled every rank's blocks together (the
+      // exchange of the row / column scales runs inside the team kernel)
       scaled_ = true;
       ruiz_ = config.precondition_ruiz_iters;
       pc_alpha_ = config.precondition_pc_alpha;
@@ -698,11 +697,11 @@ SolveResult Solver::solve_core(const SolverConfig& config) {
       // partition estimate from the reduced costs c + A^T y and the
       // normalized candidate's norm (src/solver.cpp:279-287), on the LP the
       // loop iterates (the scaled one when preconditioned)
-      Vector aty(static_cast<std::size_t>(n_)), cdev(static_cast<std::size_t>(n_));
+      Vector rcost(static_cast<std::size_t>(n_));
       double cnn = std::numeric_limits<double>::quiet_NaN();
-      check(ctx, hx_trace_extras(ctx, aty.data(), cdev.data(), &cnn));
-      for (std::size_t j = 0; j < aty.size(); ++j) aty[j] = cdev[j] + aty[j];
-      rec.partition = partition_estimate_from_reduced_costs(z, aty, config.tol_active, sigma_used);
+      check(ctx, hx_trace_reduced_costs(ctx, rcost.data()));
+      check(ctx, hx_trace_extras(ctx, nullptr, nullptr, &cnn));
+      rec.partition = partition_estimate_from_reduced_costs(z, rcost, config.tol_active, sigma_used);
       rec.candidate_norm_normalized = cnn;
       rec.wall_seconds = since();
       unscale(z.x, z.y);

@@ -117,6 +117,8 @@ def lib() -> C.CDLL:
     sig("hx_sched_tasks", C.c_int, V, I32, C.POINTER(C.c_int32), I64, C.POINTER(C.c_int64))
     sig("hx_precondition", C.c_int, V, I32, D, PD, PD)
     sig("hx_set_sum_order", C.c_int, V, I32)
+    sig("hx_stored_nonzeros", C.c_int, V, C.POINTER(C.c_int64), C.POINTER(C.c_int64))
+    sig("hx_trace_reduced_costs", C.c_int, V, PD)
     sig("hx_sum_order", I32, V)
     sig("hx_set_default_sum_order", C.c_int, I32)
     sig("hx_download_problem", C.c_int, V, PI64, PI32, PD, PD, PD)
@@ -461,6 +463,12 @@ class HX:
         """Name of the loop kernel hx_run launches for this problem."""
         v = lib().hx_loop_variant(self.h)
         return self.LOOP_KERNELS[v] if v >= 0 else ""
+
+    def stored_nonzeros(self):
+        """(nnz of A, nnz of A^T) this context keeps on its device (a rank: its blocks)."""
+        a, t = C.c_int64(), C.c_int64()
+        self._c(lib().hx_stored_nonzeros(self.h, C.byref(a), C.byref(t)))
+        return a.value, t.value
 
     def sum_order(self) -> int:
         """hx_sum_order: SUM_FAST or SUM_REFERENCE."""

@@ -236,3 +236,71 @@ def test_rank_ipc_mapping_two_processes(gpu_required):
         p.join(timeout=60)
     assert [o[1] for o in out] == ["ok", "ok"], out
     assert all(o[2] == 2 and o[3] for o in out)
+
+
+# ---- memory partition: a rank stores only its blocks -----------------------
+@pytest.mark.parametrize("name,nranks", [("cfg1_small", 2), ("zipf_small", 4), ("transport_small", 8)])
+def test_rank_stores_only_its_blocks(gpu_required, name, nranks):
+    """Every rank keeps its row block of A and its column block (rows of A^T)
+    only: together the ranks store each nonzero exactly twice (once per
+    copy), and each rank about 2 nnz / nranks -- the full matrix is on no
+    rank's device (hx_stored_nonzeros), which is what lets an LP larger than
+    one GPU run on the team."""
+    g, s = std(name)
+    rb, cb = hplp.plan_partition(s.m, s.n, s.row_ptr, s.col_idx, nranks)
+    t = hplp.Solver.team(*csr_args(s), nranks=nranks)
+    try:
+        stored = [t.rank_hx(q).stored_nonzeros() for q in range(nranks)]
+        for q, (na, nt) in enumerate(stored):
+            assert na == s.row_ptr[rb[q + 1]] - s.row_ptr[rb[q]]
+            assert nt == int(np.count_nonzero((s.col_idx >= cb[q]) & (s.col_idx < cb[q + 1])))
+            assert na + nt <= 2 * s.nnz / nranks * 1.6 + 4 * 256, (q, na + nt, 2 * s.nnz / nranks)
+        assert sum(a for a, _ in stored) == sum(b for _, b in stored) == s.nnz
+        one = hplp.Solver(*csr_args(s))
+        assert one.hx.stored_nonzeros() == (s.nnz, s.nnz)
+        one.close()
+        # the partitioned team still solves the LP: 100 iterates against the oracle
+        got = t.solve(iteration_limit=100, tolerance=1e-12, trace=True)
+    finally:
+        t.close()
+    cpu = CpuLp("port", *csr_args(s)).solve(iteration_limit=100, tolerance=1e-12, trace=True)
+    _trace_cmp(got["trace"], cpu["trace"])
+    assert got["spmv_count"] == cpu["spmv_count"]
+
+
+def test_team_power_iteration_and_zero_iteration_kkt(gpu_required):
+    """Power iteration on the team (each rank its rows of A x and columns of
+    A^T w, the slices pushed to the peers, sigma from every rank's records)
+    and the zero-iteration solve's KKT with fresh products (kModeKkt), against
+    the oracle."""
+    g, s = std("cfg1_small")
+    cpu = CpuLp("port", *csr_args(s)).solve(iteration_limit=0, tolerance=1e-4)
+    for nranks in (2, 5):
+        t = hplp.Solver.team(*csr_args(s), nranks=nranks)
+        try:
+            got = t.solve(iteration_limit=0, tolerance=1e-4)
+        finally:
+            t.close()
+        assert abs(got["sigma_estimate"] - cpu["sigma_estimate"]) <= 1e-12 * cpu["sigma_estimate"]
+        assert got["spmv_count"] == cpu["spmv_count"]
+        for a, b in zip(got["kkt"], cpu["kkt"]):
+            assert abs(a - b) <= 1e-12 * max(abs(b), 1e-300)
+
+
+def test_team_preconditioning_matches_single_device(gpu_required):
+    """Ruiz + Pock-Chambolle on the team (kModeScale: each rank scales its
+    blocks with the row / column scales its peers pushed): the scaled
+    instance is the one the single device builds, so the solves agree."""
+    g, s = std("zipf_small")
+    kw = dict(iteration_limit=200, tolerance=1e-12, precondition_ruiz_iters=5, precondition_pc_alpha=0.5,
+              trace=True, trace_period=20)
+    one = hplp.solve(*csr_args(s), **kw)
+    team, prog = team_solve(s, 4, **kw)
+    _same_controllers(prog)
+    assert [e[:2] for e in team["epochs"]] == [e[:2] for e in one["epochs"]]
+    for a, b in zip(team["trace"], one["trace"]):
+        assert rel_inf(np.concatenate([a["x"], a["y"]]), np.concatenate([b["x"], b["y"]])) <= 1e-10
+        # the partition estimate from the team's trace slots (hx_trace_reduced_costs);
+        # long-row sums may differ in the last bit between the two schedules
+        moved = sum(len(np.setxor1d(pa, pb)) for pa, pb in zip(a["partition"], b["partition"]))
+        assert moved <= 2, moved
