@@ -261,6 +261,78 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+def loop_rate(solver, iters: int, steps: int, world: int, local: int, flush) -> float:
+    """iterations/s of hx_run batches on a device-resident problem (CUDA
+    events on the solver's stream, max over ranks), L2 flushed per step."""
+    import torch
+
+    from paper_2407_16144_b200 import abi
+
+    hx = solver.hx
+    stream = torch.cuda.ExternalStream(hx.stream(), device=torch.device("cuda", local))
+    r0 = solver.solve(iteration_limit=0)
+    cfg = abi.Config.default(tolerance=1e-4, iteration_limit=10**9)
+    hx.setup(cfg, r0["sigma_estimate"], r0["eta"])
+    hx.run(max(1, iters // 5))
+    elapsed = 0.0
+    for _ in range(steps):
+        if hx.progress().status >= 0:
+            hx.setup(cfg, r0["sigma_estimate"], r0["eta"])
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        hx.run(iters)
+        e1.record(stream)
+        e1.synchronize()
+        elapsed += e0.elapsed_time(e1) / 1e3
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([elapsed], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    return iters * steps / elapsed
+
+
+def configs4_leg(args, world: int, rank: int, local: int, sharded: bool, flush):
+    """BASELINE configs[4] (the 100M-nnz instance the north star's "5x at 8
+    GPUs" is quoted on): the rate of the row-partitioned team on all N GPUs
+    (each rank stores only its blocks) and, on rank 0, of one GPU alone --
+    the speed-up of the N-GPU team over one GPU, both measured in this run."""
+    from paper_2407_16144_b200 import gen, hplp
+
+    s4 = hplp.to_standard_form(gen.generate(4))
+    b4 = algorithmic_bytes(s4.m, s4.n, s4.nnz)
+    peak, _ = measured_peak()
+    out = {"workload": f"{WORKLOADS[4]}, standard form {s4.m}x{s4.n}, nnz {s4.nnz}", "iters_per_step": args.cfg4_iters,
+           "steps": args.cfg4_steps, "algorithmic_bytes_per_iter": b4}
+    team_value = None
+    if sharded:
+        from paper_2407_16144_b200 import team
+
+        sol = team.rank_solver(s4, local)
+        na, nt = sol.hx.stored_nonzeros()
+        team_value = loop_rate(sol, args.cfg4_iters, args.cfg4_steps, world, local, flush)
+        sol.close()
+        out.update(team_value=team_value, n_gpus=world, rank0_stored_nonzeros=[na, nt],
+                   team_roofline_frac=b4 * team_value / 1e9 / (peak * world))
+    if rank == 0:
+        one = hplp.Solver.from_std(s4, device=local)
+        single = loop_rate(one, args.cfg4_iters, args.cfg4_steps, 1, local, flush)
+        kern = one.hx.loop_kernel()
+        one.close()
+        out.update(single_gpu_value=single, single_gpu_kernel=kern,
+                   single_gpu_roofline_frac=b4 * single / 1e9 / peak)
+        if team_value:
+            out["speedup_vs_1_gpu"] = team_value / single
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    return out if rank == 0 else None
+
+
 def run_gpu(args):
     import torch
 
@@ -434,6 +506,10 @@ def run_gpu(args):
     # reference's): loop rate on the same LP with the bound rows replaced by
     # the projection, and its time to 1e-4 (its KKT equals the standard
     # form's at the mapped iterate)
+    cfg4 = None
+    if not args.no_cfg4 and CONFIG_ID != 4:
+        cfg4 = configs4_leg(args, world, rank, local, sharded, flush)
+
     box = None
     if world == 1 and not sharded and not args.no_box:
         bs = hplp.Solver.box(*s.csr(), device=local)
@@ -527,6 +603,7 @@ def run_gpu(args):
             "time_to_1e-4": ttt,
             "cpu_time_to_1e-4": cpu_ttt,
             "box_form": box,
+            "configs4_leg": cfg4,
             "team_check": team_check,
             "per_step_ms": [round(1e3 * t, 3) for t in times],
         }
@@ -568,6 +645,9 @@ def main():
     ap.add_argument("--ttt-cap", type=float, default=60.0)
     ap.add_argument("--no-ttt", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cfg4", action="store_true", help="skip the configs[4] leg (team vs one GPU on 100M nnz)")
+    ap.add_argument("--cfg4-iters", type=int, default=100)
+    ap.add_argument("--cfg4-steps", type=int, default=3)
     ap.add_argument("--config", type=int, default=1, choices=sorted(WORKLOADS),
                     help="BASELINE.json config to run (default 1, the metric's config; 4 = 100M nnz for 8-GPU scaling)")
     ap.add_argument("--iters-per-step", type=int, default=None, help="iterations per timed step (default 1000)")
