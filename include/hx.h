@@ -221,6 +221,21 @@ int hx_trace_extras(hx_ctx* ctx, double* aty, double* c_out, double* cand_norm_n
  * fills (every rank its own columns; read back through CUDA IPC), so no
  * boundary SpMV over the whole matrix is needed. */
 int hx_trace_reduced_costs(hx_ctx* ctx, double* rc);
+/* [TraceRecord + trace_sink, src/solver.cpp:271-290; SURVEY.md §8f rank 3]
+ * Device trace ring.  With a trace period (hx_setup) the rHPDHG loop of the
+ * standard form -- one GPU or a team -- records every traced iteration on the
+ * device: the record's scalars, the iterate z and the partition class of
+ * every column (0 N, 1 B1, 2 B2: partition_estimate_from_reduced_costs,
+ * src/diagnostics.cpp:26-43, on c + A^T y from phase A), with the normalized
+ * candidate's canonical norm from the phases' partial sums -- no pause per
+ * record; a launch stops early only when the ring is one slot from full.
+ * hx_trace_pending: records not yet taken; hx_trace_take: the oldest one
+ * (rec: scalars and the three set sizes, partition_sets NULL; x (n), y (m),
+ * cls (n) may be NULL).  The box form and the baseline schemes keep the
+ * pause-per-record path (hx_trace_extras). */
+int32_t hx_trace_ring_capacity(hx_ctx* ctx);  /* slots of the ring set up by hx_setup; 0: none */
+int64_t hx_trace_pending(hx_ctx* ctx);
+int hx_trace_take(hx_ctx* ctx, hplp_trace_t* rec, double* x, double* y, unsigned char* cls);
 
 /* [kkt_error, src/pdhg_core.cpp:70-73] at the current iterate with fresh
  * products (the limit path of src/solver.cpp:242-254 when no best exists). */

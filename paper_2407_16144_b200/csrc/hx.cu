@@ -107,9 +107,21 @@ struct Roles {
   int x_src_avg, y_cur_avg, ax_cur_avg;
   int avg_mode, avg_cur, avg_out, avg_step;
   int y_unpushed;  // team: y_cur is a y+ whose owned rows the peers have not received yet (after a restart)
-  int tr_slot;     // team: phase A's iteration is traced -> reduced costs into trace slot tr_slot (-1: not traced)
+  int tr_slot;     // trace ring slot of this phase's iteration (-1: not traced / no ring)
   int pad_tr;
+  double tr_scale; // 2/k of this phase's iteration (the normalized candidate's scale; 0 at k = 0)
   double w_avg;
+};
+
+// Trace ring (TraceRecord src/solver.cpp:271-290): one
+// record per traced iteration, written by the controller of CTA 0; the
+// iterate z and the partition class of every column (0 N, 1 B1, 2 B2,
+// src/diagnostics.cpp:26-43) go to the ring's slot arrays from the phase
+// epilogues -- the host drains whole batches, no per-record round trip.
+struct TraceRec {
+  long long it, n, k;
+  double res, kkt[4], cand_norm;
+  long long cnt[3];  // |N|, |B1|, |B2|
 };
 
 // Controller state.  Lives in global memory between launches; during a
@@ -144,6 +156,11 @@ struct Ctl {
   double kk_tot[4];
   int sc_ruiz, sc_pc;
   double sc_alpha, sc_bsq, sc_csq;
+  // trace ring: records written so far / drained by the host, capacity (0: no
+  // ring -- a traced iteration pauses the launch instead), partition tolerances
+  long long ring_total, ring_drained;
+  int ring_cap, pad_ring;
+  double r_tol, tol_active;
   // baseline schemes
   int scheme;          // HPLP_SCHEME_*
   int avg_best;        // average slot holding the best candidate (-1: best is a z in the pools)
@@ -244,9 +261,14 @@ struct KParams {
   // gathers of x+ stay in L2; bpart holds A0's row sums
   Sched A0, A1;
   double* bpart;  // m
-  // team: reduced costs c + A^T y of traced iterations, two parity slots of n
-  // (peers read them back through CUDA IPC for the trace's partition estimate)
-  double* trbuf;
+  // trace ring (TraceRec): records, and per slot z.x (n), z.y (m) and the
+  // columns' partition classes (n); a rank writes its own slices (peers read
+  // them back through CUDA IPC)
+  TraceRec* ring_rec;
+  double* ring_x;
+  double* ring_y;
+  unsigned char* ring_cls;
+  double r_tol, tol_active;
 };
 
 // z's buffers: pool role, or an average slot after a baseline restart.
@@ -970,9 +992,13 @@ __device__ __forceinline__ void push_peers(const Team* T, double* const* base, s
 // [0, u], the dual residual counts only columns without a finite bound, and a
 // fourth partial carries u_j [-(c + A^T y)_j]^+ (the bound part of the dual
 // objective).
-template <bool RK, bool BOX = false, int EF = 0>
+// TR: a trace-ring kernel -- a traced iteration (rx non-null) also writes z.x
+// and the column's partition class to the ring and adds the class counts and
+// ||(2/k)(x - anchor)||^2 as partials NQB..NQB+3.
+template <bool RK, bool BOX = false, int EF = 0, bool TR = false>
 struct EpiPrimal {  // phase A, rows of A^T
-  static constexpr int NQ = BOX ? 4 : 3;
+  static constexpr int NQB = BOX ? 4 : 3;
+  static constexpr int NQ = NQB + (TR ? 4 : 0);
   const double* xs;
   const double* xa;
   const double* c;
@@ -983,7 +1009,9 @@ struct EpiPrimal {  // phase A, rows of A^T
   const Team* T;   // RK: peers of the x+ push
   size_t xp_off;   // offset of x+ in the x pools
   const double* ub;  // BOX: upper bounds (+inf: none)
-  double* tr;        // RK: reduced costs c + A^T y of a traced iteration (src/solver.cpp:278-279), or null
+  double* rx;             // TR: the ring slot's x (null: iteration not traced)
+  unsigned char* rcls;    // TR: the ring slot's partition classes
+  double r_tol, tol_active, tr_scale;
   struct In {
     double xs, xa, c, u;
   };
@@ -1007,8 +1035,6 @@ struct EpiPrimal {  // phase A, rows of A^T
     xp[j] = xn;
     if constexpr (RK)
       if (T->nranks > 1) push_peers(T, T->px, xp_off + j, xn, __ldg(T->xneed + (j - T->col0)));
-    if constexpr (RK)
-      if (tr) tr[j] = cj + aty;
     double rc = -(cj + aty);
     rc = rc < 0.0 ? 0.0 : rc;
     const double dx = x - xn;
@@ -1021,11 +1047,28 @@ struct EpiPrimal {  // phase A, rows of A^T
     }
     t[1] = cj * x;
     t[2] = dx * dx;
+    if constexpr (TR) {
+      // partition_estimate_from_reduced_costs (src/diagnostics.cpp:26-43) on
+      // the reduced cost c + A^T y (src/solver.cpp:278-279) and z.x
+      t[NQB] = t[NQB + 1] = t[NQB + 2] = t[NQB + 3] = 0.0;
+      if (rx) {
+        rx[j] = x;
+        const double r = cj + aty;
+        const int cls = r > r_tol ? 0 : (fabs(r) <= r_tol && x > tol_active ? 1 : 2);
+        rcls[j] = static_cast<unsigned char>(cls);
+        t[NQB + cls] = 1.0;
+        const double dxn = tr_scale * (x - in.xa);  // (2/k)(z - anchor), src/solver.cpp:284
+        t[NQB + 3] = dxn * dxn;
+      }
+    }
   }
 };
 
-template <bool RK, int EF = 0, bool PART = false>
+// TR: a traced iteration (ry non-null) writes z.y to the ring and adds the
+// normalized candidate's ||dy||^2, dy.d(Ax) as partials 4, 5.
+template <bool RK, int EF = 0, bool PART = false, bool TR = false>
 struct EpiDual {  // phase B, rows of A
+  static constexpr int NQ = TR ? 6 : 4;
   const double* y;
   const double* ax;
   const double* b;
@@ -1039,6 +1082,8 @@ struct EpiDual {  // phase B, rows of A
   const Team* T;          // RK: peers of the y+ / combo push
   size_t yp_off, yc_off;  // offsets of y+ and the combo in the y pools
   const double* part;     // PART: the leading column block's row sums (column-blocked phase B)
+  double* ry;             // TR: the ring slot's y (null: iteration not traced)
+  double tr_scale;
   struct In {
     double y, ax, b, ya, axa, p;
   };
@@ -1046,7 +1091,7 @@ struct EpiDual {  // phase B, rows of A
     return In{ld_epi<EF>(y + i),  ld_epi<EF>(ax + i), EF ? ld_epi<EF>(b + i) : __ldg(b + i), ld_epi<EF>(ya + i),
               ld_epi<EF>(axa + i), PART ? ldcg(part + i) : 0.0};
   }
-  __device__ __forceinline__ void apply(int i, double s1, const In& in, double (&t)[4]) const {
+  __device__ __forceinline__ void apply(int i, double s1, const In& in, double (&t)[NQ]) const {
     // column-blocked: the row's sum is the leading block's plus this block's
     const double s = PART ? in.p + s1 : s1;
     const double yi = in.y;
@@ -1070,6 +1115,17 @@ struct EpiDual {  // phase B, rows of A
     t[1] = bi * yi;
     t[2] = dy * dy;
     t[3] = dy * dax;
+    if constexpr (TR) {
+      t[4] = t[5] = 0.0;
+      if (ry) {
+        ry[i] = yi;
+        // (2/k)(z - anchor) and (2/k)(a_x - a_x_anchor), src/solver.cpp:284-286
+        const double dyn = tr_scale * (yi - in.ya);
+        const double daxn = tr_scale * (axi - in.axa);
+        t[4] = dyn * dyn;
+        t[5] = dyn * daxn;
+      }
+    }
   }
 };
 
@@ -1388,6 +1444,13 @@ __device__ void set_final_limit(Ctl& C, int status) {
   C.r.stop = 1;
 }
 
+// Ring slot of iteration `it` (-1: not traced or no ring).
+__host__ __device__ inline int ring_slot(const Ctl& C, long long it) {
+  return C.ring_cap > 0 && C.trace_period > 0 && it % C.trace_period == 0
+             ? static_cast<int>((it / C.trace_period) % C.ring_cap)
+             : -1;
+}
+
 // Restart decision + Halpern bookkeeping + next roles + limits
 // (src/solver.cpp:319-341 and the loop-top checks :242-254).
 __device__ void finish_iteration(Ctl& C, hplp_epoch_t* epochs, bool writer, double res, bool time_up) {
@@ -1421,7 +1484,8 @@ __device__ void finish_iteration(Ctl& C, hplp_epoch_t* epochs, bool writer, doub
   }
   R.check = 0;
   C.it += 1;
-  R.tr_slot = C.trace_period > 0 && C.it % C.trace_period == 0 ? static_cast<int>(C.it & 1) : -1;
+  R.tr_slot = ring_slot(C, C.it);
+  if (R.tr_slot >= 0) R.tr_scale = C.k >= 1 ? 2.0 / static_cast<double>(C.k) : 0.0;
   // x outputs avoid this iteration's T(z) and the best iterate before and
   // after its update too, so that without a restart the picks equal the
   // speculative ones (make_spec), which cannot know the update yet
@@ -1438,8 +1502,13 @@ __device__ void finish_iteration(Ctl& C, hplp_epoch_t* epochs, bool writer, doub
     set_final_limit(C, HPLP_STATUS_TIME_LIMIT);
   }
   if (C.trace_period > 0 && C.last_it % C.trace_period == 0) {
-    C.paused = 1;
-    R.stop = 1;
+    // no ring: the host takes each record between launches; a ring pauses
+    // only when one more record could overwrite an undrained one (the next
+    // traced phase A writes its slot speculatively)
+    if (C.ring_cap == 0 || C.ring_total - C.ring_drained >= C.ring_cap - 1) {
+      C.paused = 1;
+      R.stop = 1;
+    }
   }
   if (C.it >= C.batch_end) R.stop = 1;
 }
@@ -1447,8 +1516,11 @@ __device__ void finish_iteration(Ctl& C, hplp_epoch_t* epochs, bool writer, doub
 // After phases A+B: KKT, residual, epochs, best, termination, scan or finish.
 // pre[0..2]: KKT components (kkt_error_with_products, src/pdhg_core.cpp:57-68),
 // pre[3] = dx2/eta, pre[4] = dy2/eta, computed one per lane of warp 0.
+// ring / trt: the trace ring's records and this iteration's trace totals
+// (|N|, |B1|, |B2|, and the normalized candidate's ||dx||^2, ||dy||^2,
+// dy.d(Ax)) when the iteration is traced into a ring, else null.
 __device__ void main_logic(Ctl& C, const double* tot, const double* pre, hplp_epoch_t* epochs, bool writer,
-                           bool time_up) {
+                           bool time_up, TraceRec* ring = nullptr, const double* trt = nullptr) {
   Roles& R = C.r;
   const double dx2 = tot[2], dy2 = tot[5], dyax = tot[6];
   double kkt[4];
@@ -1508,6 +1580,26 @@ __device__ void main_logic(Ctl& C, const double* tot, const double* pre, hplp_ep
   C.last_ax = R.ax_cur;
   C.last_axp = R.axp_out;
   C.last_axa = R.ax_anchor;
+  if (ring && trt) {  // TraceRecord of this iteration (src/solver.cpp:271-290)
+    const int slot = ring_slot(C, C.it);
+    if (writer && slot >= 0) {
+      TraceRec& t = ring[slot];
+      t.it = C.it, t.n = C.n, t.k = C.k;
+      t.res = res;
+      for (int i = 0; i < 4; ++i) t.kkt[i] = kkt[i];
+      // canonical_norm_with_product of the normalized candidate (2/k)(z -
+      // anchor), src/solver.cpp:283-286; NaN at k = 0 or a clearly negative form
+      double cn = __longlong_as_double(0x7ff8000000000000ll);
+      if (C.k >= 1) {
+        const double qn = trt[3] / eta - 2.0 * trt[5] + trt[4] / eta;
+        if (qn >= 0.0) cn = sqrt(qn);
+        else if (qn >= -1e-9 * ((trt[3] + trt[4]) / eta)) cn = 0.0;
+      }
+      t.cand_norm = cn;
+      for (int i = 0; i < 3; ++i) t.cnt[i] = static_cast<long long>(trt[i]);
+    }
+    C.ring_total += 1;
+  }
   if (kkt[3] <= C.tol) {  // :292-295, returns z
     C.status = HPLP_STATUS_OPTIMAL;
     C.final_x = R.zx_out;
@@ -1651,15 +1743,16 @@ __device__ void make_spec(const Ctl& C, Roles& S) {
   S.w_x = 1.0 / static_cast<double>(C.k + 2);
   S.y_cur = R.yc_out;
   S.zx_out = pick_free(kXPool, S.x_src, S.x_anchor, C.x_best, R.zx_out);
-  const long long nit = C.it + 1;
-  S.tr_slot = C.trace_period > 0 && nit % C.trace_period == 0 ? static_cast<int>(nit & 1) : -1;
+  S.tr_slot = ring_slot(C, C.it + 1);
+  S.tr_scale = 2.0 / static_cast<double>(C.k + 1);  // k + 1 >= 1 without a restart
   S.xp_out = pick_free(kXPool, S.x_src, S.x_anchor, C.x_best, R.zx_out, S.zx_out);
 }
 
 // Did the speculative phase A compute exactly what phase A with roles R would?
 __device__ __forceinline__ bool same_phase_a(const Roles& R, const Roles& S) {
   return R.x_mode == S.x_mode && R.x_src == S.x_src && R.x_anchor == S.x_anchor && R.zx_out == S.zx_out &&
-         R.xp_out == S.xp_out && R.y_cur == S.y_cur && R.w_x == S.w_x && R.eta == S.eta && R.tr_slot == S.tr_slot;
+         R.xp_out == S.xp_out && R.y_cur == S.y_cur && R.w_x == S.w_x && R.eta == S.eta && R.tr_slot == S.tr_slot &&
+         (R.tr_slot < 0 || R.tr_scale == S.tr_scale);
 }
 
 __device__ void ctl_load(const Ctl* g, Ctl& s) {
@@ -1687,14 +1780,15 @@ __device__ __forceinline__ double* region_ptr(const KParams* P, int r, int nrec)
 __device__ __forceinline__ int gwarp_id(const Geo& g) { return g.cta * kWarps + (threadIdx.x >> 5); }
 
 // phase A: A^T y, primal step (+ Halpern formation of x), primal partials
-template <bool RK, bool BOX, int LM = 2, int EX = 2>
+template <bool RK, bool BOX, int LM = 2, int EX = 2, bool TR = false>
 __device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R, int par, WarpStage* stage,
                                                unsigned long long seq, const SpmvHead& head, const Geo& g) {
-  constexpr int NQ = EpiPrimal<RK, BOX>::NQ;
+  constexpr int NQ = EpiPrimal<RK, BOX, 0, TR>::NQ;
   const int n = P->n, m = P->m;
   double acc[NQ];
   acc_init<NQ, 0>(acc);
-  EpiPrimal<RK, BOX, LM == 1 ? HX_EPI_EF : 0> e{xsrc_ptr(P, R),
+  const bool traced = TR && R->tr_slot >= 0;
+  EpiPrimal<RK, BOX, LM == 1 ? HX_EPI_EF : 0, TR> e{xsrc_ptr(P, R),
                        P->xpool + static_cast<size_t>(R->x_anchor) * n,
                        P->c,
                        P->xpool + static_cast<size_t>(R->zx_out) * n,
@@ -1705,7 +1799,11 @@ __device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R,
                        &P->T,
                        static_cast<size_t>(R->xp_out) * n,
                        P->ub,
-                       RK && R->tr_slot >= 0 && P->trbuf ? P->trbuf + static_cast<size_t>(R->tr_slot) * n : nullptr};
+                       traced ? P->ring_x + static_cast<size_t>(R->tr_slot) * n : nullptr,
+                       traced ? P->ring_cls + static_cast<size_t>(R->tr_slot) * n : nullptr,
+                       P->r_tol,
+                       P->tol_active,
+                       R->tr_scale};
   const Sched S = P->AT;
 #ifdef HX_WPROF
   const unsigned long long w0 = clock64();
@@ -1721,14 +1819,16 @@ __device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R,
 }
 
 // phase B: A x+, dual step, speculative Halpern combos, dual partials
-template <bool RK, int LM = 2, bool CB = false, int EX = 2>
+template <bool RK, int LM = 2, bool CB = false, int EX = 2, bool TR = false>
 __device__ HX_PHASE_INLINE bool phase_dual(const KParams* P, const Roles* R, int par, WarpStage* stage,
                                            unsigned long long seq, const SpmvHead& head, const Geo& g,
                                            unsigned long long* target = nullptr) {
   const int n = P->n, m = P->m;
-  double acc[4];
-  acc_init<4, 0>(acc);
-  EpiDual<RK, LM == 1 ? HX_EPI_EF : 0, CB> e{ycur_ptr(P, R),
+  constexpr int QD = TR ? 6 : 4;
+  double acc[QD];
+  acc_init<QD, 0>(acc);
+  const bool traced = TR && R->tr_slot >= 0;
+  EpiDual<RK, LM == 1 ? HX_EPI_EF : 0, CB, TR> e{ycur_ptr(P, R),
             axcur_ptr(P, R),
             P->b,
             P->ypool + static_cast<size_t>(R->y_anchor) * m,
@@ -1742,7 +1842,9 @@ __device__ HX_PHASE_INLINE bool phase_dual(const KParams* P, const Roles* R, int
             &P->T,
             static_cast<size_t>(R->yp_out) * m,
             static_cast<size_t>(R->yc_out) * m,
-            P->bpart};
+            P->bpart,
+            traced ? P->ring_y + static_cast<size_t>(R->tr_slot) * m : nullptr,
+            R->tr_scale};
   const double* xsrc = P->xpool + static_cast<size_t>(R->xp_out) * n;
   SpmvHead h1;
   if constexpr (CB) {
@@ -1761,14 +1863,14 @@ __device__ HX_PHASE_INLINE bool phase_dual(const KParams* P, const Roles* R, int
 #ifdef HX_WPROF
   const unsigned long long w0 = clock64();
 #endif
-  spmv_rows<4, 0, LM, EX>(S, par, SrcVecT<LM == 1 && HX_GATHER_LAST>{xsrc}, e, acc, gwarp_id(g), threadIdx.x & 31, stage,
+  spmv_rows<QD, 0, LM, EX>(S, par, SrcVecT<LM == 1 && HX_GATHER_LAST>{xsrc}, e, acc, gwarp_id(g), threadIdx.x & 31, stage,
                       seq, CB ? h1 : head);
 #ifdef HX_WPROF
   if constexpr (!RK)
     if (P->prof && (threadIdx.x & 31) == 0) P->prof[gridDim.x * (16 + kWarps) + gwarp_id(g)] += clock64() - w0;
 #endif
-  fold_long<4, 0>(S, par, seq, acc, g.cta, &P->bar->abort);
-  block_to_slots<4, 0, RK>(acc, P, kRegB + par, g);
+  fold_long<QD, 0>(S, par, seq, acc, g.cta, &P->bar->abort);
+  block_to_slots<QD, 0, RK>(acc, P, kRegB + par, g);
   return true;
 }
 
@@ -1808,6 +1910,24 @@ __device__ __forceinline__ void warp_totals_main(const KParams* P, int par, doub
   }
 #pragma unroll
   for (int q = 0; q < (BOX ? 8 : 7); ++q) t[q] = warp_sum(t[q]);
+}
+
+// Trace totals of a traced iteration (every rank's records, fixed order).
+__device__ __forceinline__ void warp_totals_trace(const KParams* P, int par, double (&t)[6], const Geo& g) {
+  const int lane = threadIdx.x & 31, G = g.nrec;
+  const size_t rep = static_cast<size_t>(g.cta % kReplicas) * G * kMaxQ;
+  const double* ra = region_ptr(P, kRegA + par, G) + rep;
+  const double* rb = region_ptr(P, kRegB + par, G) + rep;
+  for (int c = lane; c < G; c += 32) {
+    const double* a = ra + static_cast<size_t>(c) * kMaxQ;
+    const double* b = rb + static_cast<size_t>(c) * kMaxQ;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) t[q] += ldcg(a + 3 + q);
+    t[4] += ldcg(b + 4);
+    t[5] += ldcg(b + 5);
+  }
+#pragma unroll
+  for (int q = 0; q < 6; ++q) t[q] = warp_sum(t[q]);
 }
 
 // Team totals: the nranks rank records of this parity, summed in rank order
@@ -2550,7 +2670,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_baseline(con
 // SU (teams): the setup modes (power iteration, KKT, preconditioning) in their
 // own kernel (team_setup_kernel), so the loop's register allocation is not
 // charged for them.
-template <bool RK, bool BOX = false, int LM = 2, bool CB = false, int EX = 2, bool SU = false>
+// TR: the trace-ring kernels (loop_kernel_trace / loop_kernel_team_trace).
+template <bool RK, bool BOX = false, int LM = 2, bool CB = false, int EX = 2, bool SU = false, bool TR = false>
 __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
   __shared__ Ctl C;
   __shared__ double tot[kMaxQ];
@@ -2734,14 +2855,14 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
     SpmvHead head;
     if (!spec_done) {
       spmv_head<LM>(P->AT, gwarp_id(g), lane, head);
-      phase_primal_t<RK, BOX, LM, EX>(P, R, par, stage, ++seq, head, g);
+      phase_primal_t<RK, BOX, LM, EX, TR>(P, R, par, stage, ++seq, head, g);
       if (writer && threadIdx.x == 0 && budget != 0ull) set_time_up(par, (global_ns() - t_start) > budget ? 1u : 0u);
     }
     mark(0);
     spmv_head<LM>(CB ? P->A0 : P->A, gwarp_id(g), lane, head);
     if (!sync()) return;
     mark(1);
-    if (!phase_dual<RK, LM, CB, EX>(P, R, par, stage, ++seq, head, g, &target)) return;
+    if (!phase_dual<RK, LM, CB, EX, TR>(P, R, par, stage, ++seq, head, g, &target)) return;
     if (threadIdx.x == 0) make_spec(C, SR);
     mark(2);
     spmv_head<LM>(P->AT, gwarp_id(g), lane, head);
@@ -2768,13 +2889,19 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
 #pragma unroll
       for (int i = 0; i < 7; ++i) pre[i] = __shfl_sync(0xffffffffu, v, i);
       cB = clock64();
+      // a traced iteration of a trace-ring kernel: the classes' counts and
+      // the normalized candidate's sums (phase A partials 3..6, phase B 4..5)
+      double trt[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      const bool traced = TR && ring_slot(C, C.it) >= 0;
+      if (traced) warp_totals_trace(P, par, trt, g);
       if (lane == 0) {
 #pragma unroll
         for (int i = 0; i < 7; ++i) tot[i] = t[i];
         s_time_up = budget != 0ull && get_time_up(par) != 0u;
         C.w_k2 = pre[5];
         C.w_k3 = pre[6];
-        main_logic(C, tot, pre, P->epochs, writer, s_time_up != 0);
+        main_logic(C, tot, pre, P->epochs, writer, s_time_up != 0, traced ? P->ring_rec : nullptr,
+                   traced ? trt : nullptr);
       }
       cC = clock64();
       __syncwarp();
@@ -2786,7 +2913,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
     mark(4);
     // speculative phase A of iteration it+1 (measured: worth ~10% against
     // running phase A after the controller)
-    phase_primal_t<RK, BOX, LM, EX>(P, &SR, par ^ 1, stage, ++seq, head, g);
+    phase_primal_t<RK, BOX, LM, EX, TR>(P, &SR, par ^ 1, stage, ++seq, head, g);
     if (writer && threadIdx.x == 0 && budget != 0ull)
       set_time_up(par ^ 1, (global_ns() - t_start) > budget ? 1u : 0u);
     __syncthreads();
@@ -2900,6 +3027,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_exact(const 
   loop_body<false, false, 2, false, 1>(&KP, g);
 }
 
+// The trace-ring kernel (hx_setup with a trace period): traced iterations go
+// to the device ring instead of pausing the launch.
+__global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_trace(const __grid_constant__ KParams KP) {
+  const Geo g{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x),
+              static_cast<int>(gridDim.x)};
+  loop_body<false, false, 2, false, 2, false, true>(&KP, g);
+}
+
 // The stream kernel with phase B swept in two column blocks (hx_upload_csr
 // enables it when x+ is far larger than L2: configs[4]).
 __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_stream_cb(const __grid_constant__ KParams KP) {
@@ -2936,6 +3071,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_team(const _
   const int cta = blockIdx.x % L.grp_ctas;
   const Geo g{cta, L.grp_ctas, P->T.rank * L.grp_ctas + cta, P->T.nranks * L.grp_ctas};
   loop_body<true, false, 2>(P, g);
+}
+
+// The team's trace-ring loop.
+__global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_team_trace(const __grid_constant__ TeamLaunch L) {
+  const int group = blockIdx.x / L.grp_ctas;
+  const KParams* P = &L.p[group];
+  const int cta = blockIdx.x % L.grp_ctas;
+  const Geo g{cta, L.grp_ctas, P->T.rank * L.grp_ctas + cta, P->T.nranks * L.grp_ctas};
+  loop_body<true, false, 2, false, 2, false, true>(P, g);
 }
 
 // The team's setup modes (kModePower / kModeKkt / kModeScale), launched like
@@ -3260,9 +3404,38 @@ struct hx_ctx {
   unsigned long long team_epochs = 0;
   std::vector<hx_ctx*> local_team;   // ranks launched together (same device), rank order
   std::vector<void*> ipc_open;       // peer mappings to close
-  double* trbuf = nullptr;           // KParams::trbuf (a rank)
-  double* peer_tr[kMaxRanks] = {};   // every rank's trbuf (own included)
+  // trace ring (KParams::ring_*): one allocation, ring_layout(); a rank's is
+  // CUDA-IPC memory (peers' mappings in peer_ring, own included)
+  unsigned char* ring = nullptr;
+  int ring_cap = 0;
+  unsigned char* peer_ring[kMaxRanks] = {};
+  double r_tol = 0.0, tol_active = 0.0;
 };
+
+namespace {
+// Trace ring layout: cap slots of z.x (n doubles), z.y (m doubles), classes
+// (n bytes), then cap records.  Capacity from a memory budget
+// (HPLP_TRACE_RING_MB, default 256 MB), 2..1024 slots.
+struct RingLayout {
+  size_t x, y, cls, rec, bytes;
+};
+RingLayout ring_layout(int cap, int64_t n, int64_t m) {
+  RingLayout L{};
+  L.x = 0;
+  L.y = L.x + static_cast<size_t>(cap) * n * sizeof(double);
+  L.cls = L.y + static_cast<size_t>(cap) * m * sizeof(double);
+  L.rec = (L.cls + static_cast<size_t>(cap) * n + 15) & ~size_t{15};
+  L.bytes = L.rec + static_cast<size_t>(cap) * sizeof(TraceRec);
+  return L;
+}
+int ring_capacity(int64_t n, int64_t m) {
+  double mb = 256.0;
+  if (const char* e = std::getenv("HPLP_TRACE_RING_MB")) mb = std::atof(e);
+  const double per = 8.0 * static_cast<double>(n + m) + static_cast<double>(n) + sizeof(TraceRec);
+  const double cap = mb * 1048576.0 / std::max(per, 1.0);
+  return static_cast<int>(std::max(2.0, std::min(1024.0, cap)));
+}
+}  // namespace
 
 namespace {
 
@@ -3372,8 +3545,9 @@ void free_problem(hx_ctx* c) {
   }
   dfree(c->bpart);
   c->bpart = nullptr;
-  dfree(c->trbuf);
-  c->trbuf = nullptr;
+  dfree(c->ring);
+  c->ring = nullptr;
+  c->ring_cap = 0;
   c->colblock = 0;
   c->a_ptr = c->a_idx = c->t_ptr = c->t_idx = nullptr;
   c->a_val = c->t_val = c->b = c->c = c->xpool = c->ypool = c->axpool = c->upool = nullptr;
@@ -3476,6 +3650,15 @@ KParams params(hx_ctx* c) {
   P.A0 = c->sb0.view;
   P.A1 = c->sb1.view;
   P.bpart = c->bpart;
+  if (c->ring) {
+    const RingLayout L = ring_layout(c->ring_cap, c->n, c->m);
+    P.ring_x = reinterpret_cast<double*>(c->ring + L.x);
+    P.ring_y = reinterpret_cast<double*>(c->ring + L.y);
+    P.ring_cls = c->ring + L.cls;
+    P.ring_rec = reinterpret_cast<TraceRec*>(c->ring + L.rec);
+  }
+  P.r_tol = c->r_tol;
+  P.tol_active = c->tol_active;
   return P;
 }
 
@@ -3491,6 +3674,7 @@ int launch_loop(hx_ctx* c) {
   const void* kernel = c->h.mode == kModeLoop && c->h.scheme != HPLP_SCHEME_RHPDHG
                            ? reinterpret_cast<const void*>(loop_kernel_baseline)
                            : c->ub                     ? reinterpret_cast<const void*>(loop_kernel_box)
+                           : c->h.ring_cap > 0 && c->h.mode == kModeLoop ? reinterpret_cast<const void*>(loop_kernel_trace)
                            : c->sum_order == HX_SUM_REFERENCE ? reinterpret_cast<const void*>(loop_kernel_exact)
                            : c->sa.view.stream_hint && c->colblock && c->h.mode == kModeLoop
                                ? reinterpret_cast<const void*>(loop_kernel_stream_cb)
@@ -3517,7 +3701,7 @@ KParams team_params(hx_ctx* c) {
   P.AT = c->pt.view;
   P.prof = nullptr;
   P.T = c->team;
-  P.trbuf = c->trbuf;
+  if (c->h.ring_cap > 0) P.T.prereduce = 0;  // the trace totals need every rank's records
   return P;
 }
 
@@ -3548,8 +3732,9 @@ int team_issue(const std::vector<hx_ctx*>& ranks, std::vector<KParams>& hp) {
   tl->ranks = static_cast<int>(hp.size());
   tl->grp_ctas = lead->grid;
   void* args[] = {tl.get()};
-  const void* kernel = lead->h.mode == kModeLoop ? reinterpret_cast<const void*>(loop_kernel_team)
-                                                 : reinterpret_cast<const void*>(team_setup_kernel);
+  const void* kernel = lead->h.mode != kModeLoop ? reinterpret_cast<const void*>(team_setup_kernel)
+                      : lead->h.ring_cap > 0   ? reinterpret_cast<const void*>(loop_kernel_team_trace)
+                                               : reinterpret_cast<const void*>(loop_kernel_team);
   HX_CUDA(lead, cudaLaunchCooperativeKernel(kernel,
                                             dim3(static_cast<unsigned>(lead->grid * ranks.size())), dim3(kThreads),
                                             args, kStageBytes, s));
@@ -3813,7 +3998,7 @@ int team_ranks(hx_ctx* c, std::vector<hx_ctx*>& ranks) {
     if (!r->ranked || r->team.nranks == 0)
       return set_err(c, HPLP_ESTATE, "hx: rank is not part of a usable team");
     for (int q = 0; q < r->team.nranks; ++q)
-      if (!r->team.px[q] || !r->team.py[q] || !r->team.pu[q] || !r->team.ps[q] || !r->team.pb[q] || !r->peer_tr[q])
+      if (!r->team.px[q] || !r->team.py[q] || !r->team.pu[q] || !r->team.ps[q] || !r->team.pb[q] || !r->peer_ring[q])
         return set_err(c, HPLP_ESTATE, "hx: team incomplete (bind or import every rank first)");
   }
   return HPLP_OK;
@@ -3967,9 +4152,10 @@ int upload_ranked(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   HX_CUDA(c, dalloc_ipc(&c->ypool, static_cast<size_t>(kYPool) * m));
   HX_CUDA(c, dalloc_ipc(&c->upool, 2 * static_cast<size_t>(n) + 2 * static_cast<size_t>(m)));
   HX_CUDA(c, dalloc(&c->axpool, static_cast<size_t>(kAxPool) * m));
-  HX_CUDA(c, dalloc_ipc(&c->trbuf, 2 * static_cast<size_t>(std::max<int64_t>(n, 1))));
-  for (int r = 0; r < kMaxRanks; ++r) c->peer_tr[r] = nullptr;
-  c->peer_tr[T.rank] = c->trbuf;
+  c->ring_cap = ring_capacity(n, m);  // same on every rank (same n, m, environment)
+  HX_CUDA(c, dalloc_ipc(&c->ring, ring_layout(c->ring_cap, n, m).bytes));
+  for (int r = 0; r < kMaxRanks; ++r) c->peer_ring[r] = nullptr;
+  c->peer_ring[T.rank] = c->ring;
   for (int r = 0; r < kMaxRanks; ++r) T.px[r] = T.py[r] = T.pu[r] = T.ps[r] = nullptr, T.pb[r] = nullptr;
   T.px[T.rank] = c->xpool, T.py[T.rank] = c->ypool, T.pu[T.rank] = c->upool, T.ps[T.rank] = c->slots;
   T.pb[T.rank] = c->rbar;
@@ -4536,7 +4722,23 @@ int hx_setup(hx_ctx* c, const hplp_config_t* cfg, double sigma_used, double eta,
   R.y_cur = 0, R.y_anchor = 0, R.yp_out = 1, R.yc_out = 2;
   R.ax_cur = 0, R.ax_anchor = 0, R.axp_out = 1, R.axc_out = 2;
   R.w_next = 0.5;  // 1/(k+2) at k = 0
-  R.tr_slot = C.trace_period > 0 && C.scheme == HPLP_SCHEME_RHPDHG ? 0 : -1;  // iteration 0
+  // trace ring: the rHPDHG loop of the standard form (one GPU or a team)
+  // records traced iterations on the device; the box form and the baselines
+  // pause per traced iteration instead
+  bool ring_on = cfg->trace_period > 0 && C.scheme == HPLP_SCHEME_RHPDHG && !c->ub;
+  if (const char* e = std::getenv("HPLP_TRACE_RING")) ring_on = ring_on && std::atoi(e) != 0;
+  if (ring_on && !c->ring) {  // one GPU: allocated on first use (a rank has it from the upload)
+    c->ring_cap = ring_capacity(c->n, c->m);
+    HX_CUDA(c, dalloc(&c->ring, ring_layout(c->ring_cap, c->n, c->m).bytes));
+  }
+  C.ring_cap = ring_on ? c->ring_cap : 0;
+  C.ring_total = C.ring_drained = 0;
+  c->r_tol = cfg->tol_active * sigma_used;  // partition_estimate_from_reduced_costs's r_tol
+  c->tol_active = cfg->tol_active;
+  C.r_tol = c->r_tol;
+  C.tol_active = c->tol_active;
+  R.tr_slot = ring_slot(C, 0);  // iteration 0
+  R.tr_scale = 0.0;
   R.stop = 0;
   HX_CUDA(c, cudaMemsetAsync(c->epochs, 0, kEpochCap * sizeof(hplp_epoch_t), s));
   HX_CUDA(c, cudaStreamSynchronize(s));
@@ -4760,7 +4962,7 @@ int hx_team_bind(hx_ctx** ctxs, int32_t count) {
     for (int r = 0; r < count; ++r) {
       T.px[r] = by[r]->xpool, T.py[r] = by[r]->ypool, T.pu[r] = by[r]->upool, T.ps[r] = by[r]->slots;
       T.pb[r] = by[r]->rbar;
-      c->peer_tr[r] = by[r]->trbuf;
+      c->peer_ring[r] = by[r]->ring;
     }
     c->local_team = by;
   }
@@ -4792,7 +4994,7 @@ int hx_team_export(hx_ctx* c, void* blob, int64_t capacity, int64_t* size) {
   HX_CUDA(c, cudaIpcGetMemHandle(&b.hu, c->upool));
   HX_CUDA(c, cudaIpcGetMemHandle(&b.hs, c->slots));
   HX_CUDA(c, cudaIpcGetMemHandle(&b.hb, c->rbar));
-  HX_CUDA(c, cudaIpcGetMemHandle(&b.ht, c->trbuf));
+  HX_CUDA(c, cudaIpcGetMemHandle(&b.ht, c->ring));
   std::memcpy(blob, &b, sizeof(b));
   return HPLP_OK;
 }
@@ -4824,7 +5026,7 @@ int hx_team_import(hx_ctx* c, const void* blob, int64_t size) {
   T.pu[b.rank] = static_cast<double*>(p[2]);
   T.ps[b.rank] = static_cast<double*>(p[3]);
   T.pb[b.rank] = static_cast<RankBar*>(p[4]);
-  c->peer_tr[b.rank] = static_cast<double*>(p[5]);
+  c->peer_ring[b.rank] = static_cast<unsigned char*>(p[5]);
   return HPLP_OK;
 }
 
@@ -4959,26 +5161,63 @@ int hx_get_certificate(hx_ctx* c, int32_t kind, double* vec) {
 // (2/k)(z - anchor) with its carried product; NaN when k = 0 (undefined), for
 // a multi-rank context (A x is rank-local), or when the quadratic form is
 // clearly negative.
+int32_t hx_trace_ring_capacity(hx_ctx* c) { return c && c->setup_done ? c->h.ring_cap : 0; }
+
+int64_t hx_trace_pending(hx_ctx* c) {
+  if (!c || !c->setup_done || c->h.ring_cap <= 0) return 0;
+  return c->h.ring_total - c->h.ring_drained;
+}
+
+int hx_trace_take(hx_ctx* c, hplp_trace_t* rec, double* x, double* y, unsigned char* cls) {
+  if (hx_trace_pending(c) <= 0) return set_err(c, HPLP_ESTATE, "hx_trace_take: no pending trace record");
+  const int64_t idx = c->h.ring_drained;
+  const int slot = static_cast<int>(idx % c->h.ring_cap);
+  const RingLayout L = ring_layout(c->ring_cap, c->n, c->m);
+  HX_CUDA(c, cudaSetDevice(c->device));
+  TraceRec t{};
+  HX_CUDA(c, cudaMemcpy(&t, c->ring + L.rec + slot * sizeof(TraceRec), sizeof(t), cudaMemcpyDeviceToHost));
+  // z.x / classes by column block, z.y by row block: one GPU holds all of
+  // them; a team's ranks wrote their own slices into their own rings
+  const int nr = c->ranked ? c->team.nranks : 1;
+  for (int q = 0; q < nr; ++q) {
+    const unsigned char* base = c->ranked ? c->peer_ring[q] : c->ring;
+    if (!base) return set_err(c, HPLP_ESTATE, "hx_trace_take: team incomplete");
+    const int64_t c0 = c->ranked ? c->pcol0[q] : 0, c1 = c->ranked ? c->pcol1[q] : c->n;
+    const int64_t r0 = c->ranked ? c->prow0[q] : 0, r1 = c->ranked ? c->prow1[q] : c->m;
+    const size_t xo = L.x + (static_cast<size_t>(slot) * c->n + c0) * sizeof(double);
+    const size_t yo = L.y + (static_cast<size_t>(slot) * c->m + r0) * sizeof(double);
+    const size_t co = L.cls + static_cast<size_t>(slot) * c->n + c0;
+    if (x && c1 > c0) HX_CUDA(c, cudaMemcpy(x + c0, base + xo, (c1 - c0) * sizeof(double), cudaMemcpyDefault));
+    if (cls && c1 > c0) HX_CUDA(c, cudaMemcpy(cls + c0, base + co, (c1 - c0), cudaMemcpyDefault));
+    if (y && r1 > r0) HX_CUDA(c, cudaMemcpy(y + r0, base + yo, (r1 - r0) * sizeof(double), cudaMemcpyDefault));
+  }
+  if (rec) {
+    std::memset(rec, 0, sizeof(*rec));
+    rec->epoch = t.n;
+    rec->inner = t.k;
+    rec->iteration = t.it;
+    rec->fixed_point_residual = t.res;
+    rec->kkt = {t.kkt[0], t.kkt[1], t.kkt[2], t.kkt[3]};
+    rec->candidate_norm_normalized = t.cand_norm;
+    rec->candidate_norm_difference = t.res;  // ||T(z) - z|| (the residual for rHPDHG)
+    rec->partition_n = t.cnt[0];
+    rec->partition_b1 = t.cnt[1];
+    rec->partition_b2 = t.cnt[2];
+    rec->partition_sets = nullptr;
+  }
+  // every rank of this process drains in step (their controllers test the
+  // ring's fill level against their own copy of the count)
+  if (c->ranked && !c->local_team.empty())
+    for (hx_ctx* r : c->local_team) r->h.ring_drained = idx + 1;
+  c->h.ring_drained = idx + 1;
+  return HPLP_OK;
+}
+
 int hx_trace_reduced_costs(hx_ctx* c, double* rc) {
   if (!c->setup_done) return set_err(c, HPLP_ESTATE, "hx_trace_reduced_costs: no solve state");
   const Ctl& C = c->h;
-  if (c->ranked) {
-    // phase A of the traced iteration wrote c_j + (A^T y)_j of its own
-    // columns into its trace slot; the team's final barrier ordered every
-    // rank's writes before this launch ended
-    if (C.trace_period <= 0 || C.last_it % C.trace_period != 0)
-      return set_err(c, HPLP_ESTATE, "hx_trace_reduced_costs: the last iteration was not traced");
-    const size_t slot = static_cast<size_t>(C.last_it & 1) * c->n;
-    HX_CUDA(c, cudaSetDevice(c->device));
-    for (int q = 0; q < c->team.nranks; ++q) {
-      if (!c->peer_tr[q]) return set_err(c, HPLP_ESTATE, "hx_trace_reduced_costs: team incomplete");
-      const int64_t len = c->pcol1[q] - c->pcol0[q];
-      if (len > 0)
-        HX_CUDA(c, cudaMemcpy(rc + c->pcol0[q], c->peer_tr[q] + slot + c->pcol0[q], len * sizeof(double),
-                              cudaMemcpyDefault));
-    }
-    return HPLP_OK;
-  }
+  if (c->ranked)
+    return set_err(c, HPLP_EINVAL, "hx_trace_reduced_costs: a rank stores only its blocks (the trace ring classifies)");
   std::vector<double> cv(static_cast<size_t>(c->n));
   if (int r = hx_trace_extras(c, rc, cv.data(), nullptr)) return r;
   for (int64_t j = 0; j < c->n; ++j) rc[j] = cv[j] + rc[j];  // lp.c + sr.at_y (src/solver.cpp:278-279)

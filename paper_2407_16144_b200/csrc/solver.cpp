@@ -675,16 +675,50 @@ SolveResult Solver::solve_core(const SolverConfig& config) {
   // a rank of a multi-rank team: the time limit is decided on the device by
   // rank 0 (a per-rank host check could split the team)
   const int32_t team_size = hx_team_size(ctx);
+  // the device trace ring (hx_trace_take): records of whole batches, drained
+  // between launches; without it (box form, baselines) a traced iteration
+  // ends its launch
+  const bool ring = config.trace_period > 0 && hx_trace_ring_capacity(ctx) > 0;
+  auto drain_ring = [&] {
+    while (hx_trace_pending(ctx) > 0) {
+      hplp_trace_t t{};
+      Iterate z{Vector(static_cast<std::size_t>(n_)), Vector(static_cast<std::size_t>(m_))};
+      std::vector<unsigned char> cls(static_cast<std::size_t>(n_));
+      check(ctx, hx_trace_take(ctx, &t, z.x.data(), z.y.data(), cls.data()));
+      if (!config.trace_sink) continue;
+      TraceRecord rec;
+      rec.epoch = t.epoch;
+      rec.inner = t.inner;
+      rec.iteration = t.iteration;
+      rec.fixed_point_residual = t.fixed_point_residual;
+      rec.kkt = kkt_of(t.kkt);
+      rec.candidate_norm_difference = t.candidate_norm_difference;
+      if (t.inner >= 1) rec.candidate_norm_normalized = t.candidate_norm_normalized;
+      // the sets from the device classes (the reference's index order)
+      rec.partition.tol_active = config.tol_active;
+      rec.partition.n_set.reserve(static_cast<std::size_t>(t.partition_n));
+      rec.partition.b1_set.reserve(static_cast<std::size_t>(t.partition_b1));
+      rec.partition.b2_set.reserve(static_cast<std::size_t>(t.partition_b2));
+      for (std::size_t j = 0; j < cls.size(); ++j)
+        (cls[j] == 0 ? rec.partition.n_set : cls[j] == 1 ? rec.partition.b1_set : rec.partition.b2_set)
+            .push_back(static_cast<Index>(j));
+      rec.wall_seconds = since();
+      unscale(z.x, z.y);
+      config.trace_sink(rec, z);
+    }
+  };
   while (p.status < 0) {
     if (team_size == 1 && since() > config.time_limit_seconds && p.it < config.iteration_limit) {
       // host-side guard for the time limit between batches (:249-254)
       break;
     }
-    const int64_t batch = config.trace_period > 0 ? config.trace_period : kBatch;
+    const int64_t batch = config.trace_period > 0 && !ring ? config.trace_period : kBatch;
     const int rc = run_batch(batch, &p);
     if (rc != HPLP_OK) throw_hx(ctx, rc);
     drain_epochs();
-    if (p.paused && config.trace_sink) {
+    if (ring) {
+      drain_ring();
+    } else if (p.paused && config.trace_sink) {
       TraceRecord rec;
       rec.epoch = p.trace_n;
       rec.inner = p.trace_k;

@@ -393,3 +393,36 @@ def test_reference_sum_order_iterates(gpu_required):
     worst = _trace_cmp(gpu["trace"], cpu["trace"], tol=1e-12)
     assert gpu["spmv_count"] == cpu["spmv_count"]
     print(f"zipf_small reference order: worst {worst:.2e}")
+
+
+def test_trace_ring_runs_at_full_batch_rate(gpu_required):
+    """Device trace ring: with trace_period = 1 the loop
+    records every iteration on the device (iterate, partition classes,
+    normalized-candidate norm) and does NOT end its launch per record -- the
+    traced solve launches the loop kernel as often as the untraced one, and
+    its records equal the oracle's (iterates to 1e-10, partition sets, norms
+    to 1e-9)."""
+    g, s = std("cfg1_small")
+    kw = dict(iteration_limit=300, tolerance=1e-12)
+    sol = hplp.Solver(*csr_args(s))
+    l0 = sol.hx.launches()
+    plain = sol.solve(**kw)
+    l1 = sol.hx.launches()
+    traced = sol.solve(trace=True, **kw)
+    l2 = sol.hx.launches()
+    sol.close()
+    assert len(traced["trace"]) == 300
+    assert l2 - l1 == l1 - l0, (l1 - l0, l2 - l1)  # no launch per traced iteration
+    assert np.array_equal(plain["x"], traced["x"]) and np.array_equal(plain["y"], traced["y"])
+    cpu = CpuLp("port", *csr_args(s)).solve(trace=True, **kw)
+    _trace_cmp(traced["trace"], cpu["trace"])
+    flips = 0
+    for tg, tc in zip(traced["trace"], cpu["trace"]):
+        for u, v in zip(tg["partition"], tc["partition"]):
+            flips += len(np.setxor1d(u, v))
+        a, b = tg["cand_norm_normalized"], tc["cand_norm_normalized"]
+        if tc["inner"] == 0:
+            assert np.isnan(a) and np.isnan(b)
+        else:
+            assert abs(a - b) <= 1e-9 * max(abs(b), 1e-300), (tc["iteration"], a, b)
+    assert flips <= 3

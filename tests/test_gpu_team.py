@@ -89,8 +89,11 @@ def test_team_rank_records_path(gpu_required, monkeypatch, name, nranks):
     assert [e[:2] for e in gpu["epochs"]] == [e[:2] for e in cpu["epochs"]]
     _same_controllers(prog)
     long, prog = team_solve(s, nranks, tolerance=1e-4, iteration_limit=200000)
-    ref = CpuLp("port", *csr_args(s)).solve(tolerance=1e-4, iteration_limit=200000)
+    # the long run against the single-device solve (itself pinned to the
+    # oracle by test_gpu_parity; the oracle's own 1e-4 run takes minutes here)
+    ref = hplp.solve(*csr_args(s), tolerance=1e-4, iteration_limit=200000)
     assert long["status"] == ref["status"]
+    assert abs(long["iterations"] - ref["iterations"]) <= max(10, ref["iterations"] // 100)
     _same_controllers(prog)
 
 
