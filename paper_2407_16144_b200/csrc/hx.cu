@@ -4049,15 +4049,20 @@ int upload_ranked(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   // A's row block: the caller's arrays from row_ptr[row0]
   std::vector<int> ap(static_cast<size_t>(ml) + 1);
   const int64_t pa0 = row_ptr[row0];
+  if (row_ptr[row1] - pa0 >= (int64_t{1} << 31))
+    return set_err(c, HPLP_EINVAL, "hx_upload_csr: a rank's row block exceeds 2^31 - 1 nonzeros (more ranks)");
   for (int i = 0; i <= ml; ++i) ap[i] = static_cast<int>(row_ptr[row0 + i] - pa0);
   const int64_t nnz_a = ap[ml];
   // A^T's row block = A's columns [col0, col1), rows ascending per column
-  std::vector<int> tp(static_cast<size_t>(nl) + 1, 0);
+  std::vector<int64_t> tp64(static_cast<size_t>(nl) + 1, 0);
   for (int64_t p = 0; p < nnz; ++p) {
     const int j = col_idx[p];
-    if (j >= col0 && j < col1) ++tp[j - col0 + 1];
+    if (j >= col0 && j < col1) ++tp64[j - col0 + 1];
   }
-  for (int k = 0; k < nl; ++k) tp[k + 1] += tp[k];
+  for (int k = 0; k < nl; ++k) tp64[k + 1] += tp64[k];
+  if (tp64[nl] >= (int64_t{1} << 31))
+    return set_err(c, HPLP_EINVAL, "hx_upload_csr: a rank's column block exceeds 2^31 - 1 nonzeros (more ranks)");
+  std::vector<int> tp(tp64.begin(), tp64.end());
   const int64_t nnz_t = tp[nl];
   std::vector<int> ti(static_cast<size_t>(nnz_t));
   std::vector<double> tv(static_cast<size_t>(nnz_t));
@@ -4183,8 +4188,14 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   if (m < 0 || n < 0) return set_err(c, HPLP_EINVAL, "SparseMatrix: negative dimension");
   if (row_ptr[0] != 0) return set_err(c, HPLP_EINVAL, "hx_upload_csr: row_ptr[0] must be 0");
   const int64_t nnz = row_ptr[m];
-  if (nnz < 0 || nnz >= (int64_t{1} << 31) || m >= (int64_t{1} << 31) - 1 || n >= (int64_t{1} << 31) - 1)
+  // int32 indices on the device: m, n < 2^31 - 1, and every stored CSR copy
+  // (one GPU: the whole matrix; a rank: each of its two blocks) < 2^31
+  // nonzeros -- a team holds a matrix of more than 2^31 nonzeros in total
+  if (nnz < 0 || m >= (int64_t{1} << 31) - 1 || n >= (int64_t{1} << 31) - 1)
     return set_err(c, HPLP_EINVAL, "hx_upload_csr: sizes exceed the int32 index range of this build");
+  if (!c->ranked && nnz >= (int64_t{1} << 31))
+    return set_err(c, HPLP_EINVAL,
+                   "hx_upload_csr: more than 2^31 - 1 nonzeros on one GPU (int32 positions); use a team");
   for (int64_t i = 0; i < m; ++i)
     if (!std::isfinite(b[i])) return set_err(c, HPLP_EINVAL, "StandardFormLP: non-finite b or c");
   for (int64_t j = 0; j < n; ++j)
