@@ -123,3 +123,46 @@ def test_team_blob_exchange_gloo():
         p.join(timeout=60)
     for r in range(world):
         assert got[r] == [bytes([k]) * (k + 3) for k in range(world)]
+
+
+def _agree_worker(rank, world, port, fail_rank, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2407_16144_b200 import team
+
+    out = []
+    for phase in ("create", "join", "power"):
+        try:
+            team.agree(not (rank == fail_rank and phase == "join"), phase)
+            out.append(phase)
+        except RuntimeError as e:
+            out.append(f"raised:{phase}:{'join' in str(e)}")
+            break
+    q.put((rank, out))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank", [None, 0, 1])
+def test_team_setup_failure_fails_every_rank(fail_rank):
+    """team.agree (the bench's team setup, paper_2407_16144_b200/team.py): a
+    rank that fails a setup phase makes EVERY rank raise at that phase -- no
+    rank goes on into a collective its peers skipped, and there is no
+    fallback to independent replicas."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    ps = [ctx.Process(target=_agree_worker, args=(r, world, port, fail_rank, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    got = dict(q.get() for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(world):
+        if fail_rank is None:
+            assert got[r] == ["create", "join", "power"]
+        else:
+            assert got[r] == ["create", "raised:join:True"], got
