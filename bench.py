@@ -186,17 +186,25 @@ class PinnedToCore0:
         os.sched_setaffinity(0, self.old)
 
 
+REF_BUILD = {"reference_fast": "the reference's sources built -O3 -march=x86-64-v3 (AVX2, FMA contraction)",
+             "reference": "the reference's sources built -O2, SSE2 (the parity build)",
+             "port": "the oracle restatement (oracle/_ref absent)"}
+
+
 def cpu_lp(cid: int):
     """The instance as the CPU reference itself builds it: the generator's
     general form through the REFERENCE's own to_standard_form
-    (src/lp_model.cpp:155-325) -- no product library on this path."""
+    (src/lp_model.cpp:155-325) -- no product library on this path.  Timed
+    with the reference's sources in their fastest build here (oracle/Makefile
+    ref_fast) -- returned as kind "reference" with `build` naming it."""
     import oracle
     from paper_2407_16144_b200 import gen
 
-    kind = "reference" if oracle.available("reference") else "port"
+    lib = next(k for k in ("reference_fast", "reference", "port") if oracle.available(k))
     g = gen.generate(cid)
-    std = oracle.CpuStd(kind, g.as_abi())
-    return kind, g, std, std.lp()
+    std = oracle.CpuStd(lib, g.as_abi())
+    cpu_lp.build = REF_BUILD[lib]
+    return ("port" if lib == "port" else "reference"), g, std, std.lp()
 
 
 def cpu_iters_per_sec(lp, kind, iters: int):
@@ -248,6 +256,7 @@ def run_reference(args):
                    "iters_per_step": iters, "parallelism": "none (single-threaded reference)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "cores_of": ncpu, "cpu_model": model,
                          "kind": kind,
+                         "build": cpu_lp.build,
                          "sample": f"{args.steps} x solve(iteration_limit={iters}) on configs[{CONFIG_ID}] built by the "
                                    f"reference's own to_standard_form, pinned to core 0 (1 of {ncpu}); power "
                                    f"iteration ({pit} its, {t_power:.2f}s): a zero-iteration solve's wall time "
@@ -563,6 +572,7 @@ def run_gpu(args):
                 cpu_ttt = cpu_time_to_tol(cval, info["power_seconds"],
                                           gi.get("iterations") if gi.get("status") == "optimal" else None)
         cpu = {"value": cval, "unit": UNIT, "cores": 1, "cores_of": ncpu, "cpu_model": model, "kind": kind,
+               "build": cpu_lp.build,
                "sample": f"solve(iteration_limit={args.cpu_iters}) on configs[{CONFIG_ID}] (the reference's own "
                          f"to_standard_form), pinned to core 0 (1 of {ncpu}); power iteration "
                          f"({info['power_iterations']} its, {info['power_seconds']:.2f}s): a zero-iteration solve's "

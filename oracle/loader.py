@@ -12,7 +12,9 @@ from paper_2407_16144_b200 import abi
 from paper_2407_16144_b200.abi import dptr, i32ptr, i64ptr
 
 HERE = Path(__file__).resolve().parent
-LIBS = {"port": (HERE / "liboracle.so", "orc_"), "reference": (HERE / "_ref" / "libhplp_ref.so", "ref_")}
+LIBS = {"port": (HERE / "liboracle.so", "orc_"), "reference": (HERE / "_ref" / "libhplp_ref.so", "ref_"),
+        # the same reference sources built -O3 / AVX2 + FMA: timing only (bench.py)
+        "reference_fast": (HERE / "_ref" / "libhplp_ref_fast.so", "ref_")}
 REF_SRC = Path(os.environ.get("HPLP_REFERENCE", "/root/reference/proj"))
 
 _cache: dict[str, C.CDLL] = {}
@@ -26,7 +28,7 @@ def build(kinds=("port", "reference"), quiet=True) -> None:
     if "port" in kinds:
         subprocess.run(["make", "-s", "liboracle.so"], cwd=HERE, check=True, stdout=out)
     if "reference" in kinds and (REF_SRC / "src").is_dir():
-        subprocess.run(["make", "-s", "ref", f"REF={REF_SRC}"], cwd=HERE, check=True, stdout=out)
+        subprocess.run(["make", "-s", "ref", "ref_fast", f"REF={REF_SRC}"], cwd=HERE, check=True, stdout=out)
 
 
 def available(kind: str) -> bool:
