@@ -4985,6 +4985,7 @@ struct TeamBlob {
   int32_t magic, rank, nranks, grid;
   int64_t m, n, nnz;
   int32_t row0, row1, col0, col1;
+  int32_t ring_cap, pad;
   cudaIpcMemHandle_t hx, hy, hu, hs, hb, ht;
 };
 constexpr int32_t kBlobMagic = 0x48585442;  // "HXTB"
@@ -4999,6 +5000,7 @@ int hx_team_export(hx_ctx* c, void* blob, int64_t capacity, int64_t* size) {
   b.magic = kBlobMagic, b.rank = c->team.rank, b.nranks = c->team.nranks, b.grid = c->grid;
   b.m = c->m, b.n = c->n, b.nnz = c->nnz;
   b.row0 = c->team.row0, b.row1 = c->team.row1, b.col0 = c->team.col0, b.col1 = c->team.col1;
+  b.ring_cap = c->ring_cap;
   HX_CUDA(c, cudaSetDevice(c->device));
   HX_CUDA(c, cudaIpcGetMemHandle(&b.hx, c->xpool));
   HX_CUDA(c, cudaIpcGetMemHandle(&b.hy, c->ypool));
@@ -5019,6 +5021,8 @@ int hx_team_import(hx_ctx* c, const void* blob, int64_t size) {
     return set_err(c, HPLP_EINVAL, "hx_team_import: blob of another team");
   if (b.m != c->m || b.n != c->n || b.nnz != c->nnz || b.grid != c->grid)
     return set_err(c, HPLP_EINVAL, "hx_team_import: ranks disagree on the problem or the CTA count");
+  if (b.ring_cap != c->ring_cap)  // same n, m: only a different HPLP_TRACE_RING_MB gets here
+    return set_err(c, HPLP_EINVAL, "hx_team_import: ranks disagree on the trace ring (HPLP_TRACE_RING_MB)");
   if (c->pcol0[b.rank] != b.col0 || c->pcol1[b.rank] != b.col1 || c->prow0[b.rank] != b.row0 ||
       c->prow1[b.rank] != b.row1)
     return set_err(c, HPLP_EINVAL, "hx_team_import: the peer was given a different partition");
