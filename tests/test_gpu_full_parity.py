@@ -52,9 +52,11 @@ def reference_instance(cid: int):
     return _cache[cid]
 
 
-def lockstep(std, iters: int, order: str, **kw):
+def lockstep(std, iters: int, order: str, nranks: int = 0, **kw):
     """Run the reference and the device solve side by side for `iters`
     iterations with a trace record per iteration; compare every record.
+    nranks > 0: the device side is a row-partitioned team of that many ranks
+    (emulated as CTA groups of one launch on this GPU).
     Returns (cpu result, gpu result, per-iteration errors)."""
     cpu_lp = std.lp()
     q: queue.Queue = queue.Queue(maxsize=2)
@@ -91,7 +93,8 @@ def lockstep(std, iters: int, order: str, **kw):
     th = threading.Thread(target=run_cpu, daemon=True)
     th.start()
     with hplp.sum_order(order):
-        sol = hplp.Solver(std.m, std.n, std.row_ptr, std.col_idx, std.val, std.b, std.c)
+        args = (std.m, std.n, std.row_ptr, std.col_idx, std.val, std.b, std.c)
+        sol = hplp.Solver.team(*args, nranks=nranks) if nranks else hplp.Solver(*args)
     try:
         assert sol.hx.sum_order() == (hplp.SUM_REFERENCE if order == "reference" else hplp.SUM_FAST)
         gpu = sol.solve(iteration_limit=iters, tolerance=1e-12, trace=True, sink=gpu_sink, **kw)
@@ -133,6 +136,17 @@ def test_full_size_first_100_iterates(gpu_required, cid):
     cpu, gpu, errs = lockstep(std, 100, "fast")
     worst = _check_first_100(cpu, gpu, errs)
     print(f"configs[{cid}] {std.m}x{std.n} nnz {std.nnz}: worst of 100 iterates {worst:.3e}")
+
+
+@pytest.mark.parametrize("nranks", [3, 8])
+def test_full_size_first_100_iterates_team_configs1(gpu_required, nranks):
+    """configs[1] at full size on a row-partitioned team (each rank storing
+    only its blocks; power iteration, pushes and reductions across ranks)
+    against the reference: the same bar as one GPU."""
+    g, std = reference_instance(1)
+    cpu, gpu, errs = lockstep(std, 100, "fast", nranks=nranks)
+    worst = _check_first_100(cpu, gpu, errs)
+    print(f"configs[1] on {nranks} ranks: worst of 100 iterates {worst:.3e}")
 
 
 def test_full_size_first_100_iterates_configs4(gpu_required):
