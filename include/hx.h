@@ -213,7 +213,9 @@ int hx_get_certificate(hx_ctx* ctx, int32_t kind, double* vec);
  * iteration: aty (n) = A^T y and c_out (n) = c of the device problem (the
  * partition estimate's reduced costs are c + A^T y), and the canonical norm
  * of the normalized candidate (2/k)(z - anchor); NaN when undefined (k = 0,
- * multi-rank context).  Any output may be NULL. */
+ * multi-rank context).  Any output may be NULL.  A rank of a team stores
+ * only its blocks: aty / c_out give HPLP_EINVAL there (its traces come from
+ * the device trace ring, hx_trace_take). */
 int hx_trace_extras(hx_ctx* ctx, double* aty, double* c_out, double* cand_norm_normalized);
 /* [src/solver.cpp:278-279, partition_estimate_from_reduced_costs's input]
  * rc (n) = c + A^T y of the last traced iteration, on the device problem.  A
