@@ -590,7 +590,7 @@ def run_gpu(args):
                        f"row-partitioned x{world}: one LP, rows/columns split by nnz, slices pushed over NVLink P2P"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None if sharded else traffic,
-                         "kernel": "hx::loop_kernel_team" if sharded else hx.loop_kernel(),
+                         "kernel": hx.loop_kernel(),
                          "algorithmic_bytes_per_iter": b_iter, "peak_source": peak_kind,
                          "frac_of_8TBs": achieved / (8000.0 * world)},
             # the access-pattern ceiling: every nonzero is one random fp64 gather

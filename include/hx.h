@@ -116,7 +116,10 @@ int hx_set_box(hx_ctx* ctx, const double* upper);
  * matrix streams loaded L2 evict_first: the working set exceeds ~70% of L2;
  * HPLP_L2_STREAM=0/1 overrides), 2 loop_kernel_box, 3 loop_kernel_stream_cb
  * (the stream kernel with phase B swept in two column blocks: x+ far larger
- * than L2; HX_COLBLOCK=0/1 overrides); -1 before an upload. */
+ * than L2; HX_COLBLOCK=0/1 overrides), 4 loop_kernel_exact (the reference
+ * summation order), 5 loop_kernel_team / 6 loop_kernel_team_stream (a rank of
+ * a team); -1 before an upload.  With a trace period the trace-ring kernels
+ * (loop_kernel_trace, loop_kernel_team_trace) run instead. */
 int32_t hx_loop_variant(hx_ctx* ctx);
 /* The device problem (after any preconditioning): CSR A, b, c (one GPU;
  * HPLP_EINVAL for a rank, which stores only its blocks). */

@@ -3073,6 +3073,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_team(const _
   loop_body<true, false, 2>(P, g);
 }
 
+// The team loop with the matrix streams loaded evict_first at compile time
+// (Sched::stream_hint: the rank's working set is beyond L2), like
+// loop_kernel_stream -- the run-time policy choice costs ~2%.
+__global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_team_stream(const __grid_constant__ TeamLaunch L) {
+  const int group = blockIdx.x / L.grp_ctas;
+  const KParams* P = &L.p[group];
+  const int cta = blockIdx.x % L.grp_ctas;
+  const Geo g{cta, L.grp_ctas, P->T.rank * L.grp_ctas + cta, P->T.nranks * L.grp_ctas};
+  loop_body<true, false, 1>(P, g);
+}
+
 // The team's trace-ring loop.
 __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_team_trace(const __grid_constant__ TeamLaunch L) {
   const int group = blockIdx.x / L.grp_ctas;
@@ -3732,8 +3743,11 @@ int team_issue(const std::vector<hx_ctx*>& ranks, std::vector<KParams>& hp) {
   tl->ranks = static_cast<int>(hp.size());
   tl->grp_ctas = lead->grid;
   void* args[] = {tl.get()};
+  bool stream = true;  // every rank of the launch streams its blocks evict_first
+  for (hx_ctx* c : ranks) stream = stream && c->pa.view.stream_hint && c->pt.view.stream_hint;
   const void* kernel = lead->h.mode != kModeLoop ? reinterpret_cast<const void*>(team_setup_kernel)
                       : lead->h.ring_cap > 0   ? reinterpret_cast<const void*>(loop_kernel_team_trace)
+                      : stream                 ? reinterpret_cast<const void*>(loop_kernel_team_stream)
                                                : reinterpret_cast<const void*>(loop_kernel_team);
   HX_CUDA(lead, cudaLaunchCooperativeKernel(kernel,
                                             dim3(static_cast<unsigned>(lead->grid * ranks.size())), dim3(kThreads),
@@ -4555,6 +4569,7 @@ int hx_precondition(hx_ctx* c, int32_t ruiz_iters, double pc_alpha, double* row_
 // form.  Set after hx_upload_csr and before hx_precondition / hx_setup.
 int32_t hx_loop_variant(hx_ctx* c) {
   if (!c || !c->uploaded) return -1;
+  if (c->ranked) return c->pa.view.stream_hint && c->pt.view.stream_hint ? 6 : 5;
   return c->ub ? 2 : c->sum_order == HX_SUM_REFERENCE ? 4 : c->sa.view.stream_hint ? (c->colblock ? 3 : 1) : 0;
 }
 
