@@ -426,3 +426,27 @@ def test_trace_ring_runs_at_full_batch_rate(gpu_required):
         else:
             assert abs(a - b) <= 1e-9 * max(abs(b), 1e-300), (tc["iteration"], a, b)
     assert flips <= 3
+
+
+def test_trace_ring_minimum_capacity_and_disabled(gpu_required, monkeypatch):
+    """The ring at its minimum of 2 slots (a launch ends after every record)
+    and switched off (HPLP_TRACE_RING=0: the pause-per-record path with the
+    host's partition estimate) give the same records as the default ring."""
+    g, s = std("cfg0")
+    kw = dict(iteration_limit=120, tolerance=1e-12, trace=True, trace_period=3)
+    base = hplp.solve(*csr_args(s), **kw)
+    monkeypatch.setenv("HPLP_TRACE_RING_MB", "0.0001")
+    small = hplp.solve(*csr_args(s), **kw)
+    monkeypatch.delenv("HPLP_TRACE_RING_MB")
+    monkeypatch.setenv("HPLP_TRACE_RING", "0")
+    off = hplp.solve(*csr_args(s), **kw)
+    assert len(base["trace"]) == len(small["trace"]) == len(off["trace"]) == 40
+    for a, b, c in zip(base["trace"], small["trace"], off["trace"]):
+        assert (a["iteration"], a["epoch"], a["inner"]) == (b["iteration"], b["epoch"], b["inner"])
+        assert (a["iteration"], a["epoch"], a["inner"]) == (c["iteration"], c["epoch"], c["inner"])
+        assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["y"], b["y"])
+        assert np.array_equal(a["x"], c["x"]) and np.array_equal(a["y"], c["y"])
+        assert all(np.array_equal(u, v) for u, v in zip(a["partition"], b["partition"]))
+        assert sum(len(np.setxor1d(u, v)) for u, v in zip(a["partition"], c["partition"])) <= 1
+        assert a["kkt"] == b["kkt"] == c["kkt"]
+    assert np.array_equal(base["x"], small["x"]) and np.array_equal(base["x"], off["x"])
