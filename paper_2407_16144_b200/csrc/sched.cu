@@ -18,7 +18,7 @@
 namespace hx {
 
 SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, double row_cost, double task_cost,
-                         bool exact) {
+                         bool exact, int bound_from) {
   SchedHost s;
   const int64_t nnz = ptr[rows] - ptr[0];  // ptr may point into a larger matrix (a rank's block)
   const double total = static_cast<double>(nnz) + row_cost * rows;
@@ -63,16 +63,20 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, doubl
       continue;
     }
     const int r0 = r;
+    // a task never mixes bound rows with others
+    const bool bound = bound_from >= 0 && r0 >= bound_from;
+    const int stop = !bound && bound_from >= 0 ? bound_from : rows;
     int64_t used = 0;
-    while (r < rows && r - r0 < kStreamRowsMax) {
+    while (r < stop && r - r0 < kStreamRowsMax) {
       const int64_t l = ptr[r + 1] - ptr[r];
       if (l > kStreamRowMax || used + l > kTaskNnz) break;
       used += l;
       ++r;
     }
     unit.push_back(s.tasks.size());
-    push(r0, r, kTaskStream, static_cast<int>(ptr[r0]), static_cast<int>(ptr[r]), int4{0, 0, 0, 0},
-         static_cast<double>(used) + row_cost * (r - r0));
+    // a bound row also carries its slack column's primal step: one more row's worth
+    push(r0, r, bound ? kTaskBound : kTaskStream, static_cast<int>(ptr[r0]), static_cast<int>(ptr[r]),
+         int4{0, 0, 0, 0}, static_cast<double>(used) + row_cost * (r - r0) * (bound ? 2.0 : 1.0));
   }
   const std::size_t nt = s.tasks.size();
   unit.push_back(nt);
