@@ -118,9 +118,7 @@ int hx_set_box(hx_ctx* ctx, const double* upper);
  * (the stream kernel with phase B swept in two column blocks: x+ far larger
  * than L2; HX_COLBLOCK=0/1 overrides), 4 loop_kernel_exact (the reference
  * summation order), 5 loop_kernel_team / 6 loop_kernel_team_stream (a rank of
- * a team), 7 loop_kernel_fused / 8 loop_kernel_stream_fused (0 / 1 when the
- * standard form has bound rows: their slack columns' primal steps run in
- * phase B; HX_FUSE=0 turns it off); -1 before an upload.  With a trace period the trace-ring kernels
+ * a team); -1 before an upload.  With a trace period the trace-ring kernels
  * (loop_kernel_trace, loop_kernel_team_trace) run instead. */
 int32_t hx_loop_variant(hx_ctx* ctx);
 /* The device problem (after any preconditioning): CSR A, b, c (one GPU;

@@ -269,9 +269,6 @@ struct KParams {
   double* ring_y;
   unsigned char* ring_cls;
   double r_tol, tol_active;
-  // the fused loop (loop_kernel_fused): A with its trailing bound rows as
-  // kTaskBound tasks, and A^T without their slack columns (rows 0 .. n - nb)
-  Sched AL, ATL;
 };
 
 // z's buffers: pool role, or an average slot after a baseline restart.
@@ -375,16 +372,10 @@ __device__ void block_to_slots(const double (&acc)[Q], double* region, int grid)
   }
 }
 
-// The fused loop's CTA totals of phase A (quantities 0..2) by parity.
-__device__ __forceinline__ double (*fused_apart())[3] {
-  __shared__ double a[2][3];
-  return a;
-}
-
 // Loop-kernel version: record g.rec of g.nrec in slot region `region`; a
 // ranked CTA writes it into every rank's slots (own included), so all ranks
-// hold all records.  FO: the fused loop's phase A / phase B (fused_apart).
-template <int Q, unsigned MaxMask, bool RK, class KP, bool FO = false>
+// hold all records.
+template <int Q, unsigned MaxMask, bool RK, class KP>
 __device__ void block_to_slots(const double (&acc)[Q], const KP* P, int region, const Geo& g) {
   double (*red)[kMaxQ] = red_buf();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -399,20 +390,8 @@ __device__ void block_to_slots(const double (&acc)[Q], const KP* P, int region, 
     const bool mx = (MaxMask >> q) & 1u;
     double v = red[0][q];
     for (int w = 1; w < kWarps; ++w) v = mx ? dmax(v, red[w][q]) : v + red[w][q];
-    size_t off = static_cast<size_t>(region) * region_stride(g.nrec) +
-                 (static_cast<size_t>(k) * g.nrec + g.rec) * kMaxQ + q;
-    if constexpr (FO) {
-      // the fused loop: phase A keeps its CTA totals 0..2; phase B's slack
-      // partials 4..6 complete them in phase A's record (same parity)
-      const int par = region - kRegB;
-      if (region == kRegA || region == kRegA + 1) {
-        if (k == 0) fused_apart()[region - kRegA][q] = v;
-      } else if (q >= 4) {
-        v = fused_apart()[par][q - 4] + v;
-        off = static_cast<size_t>(kRegA + par) * region_stride(g.nrec) +
-              (static_cast<size_t>(k) * g.nrec + g.rec) * kMaxQ + (q - 4);
-      }
-    }
+    const size_t off = static_cast<size_t>(region) * region_stride(g.nrec) +
+                       (static_cast<size_t>(k) * g.nrec + g.rec) * kMaxQ + q;
     if constexpr (RK) {
       // with rank records the main reduction's records stay local: the leader
       // pre-reduces them at the end-of-iteration barrier (team_sync)
@@ -654,12 +633,6 @@ __device__ __forceinline__ void spmv_head(const Sched& S, int gwarp, int lane, S
   load_task<LM>(S, h.tk, lane, h.cur);
 }
 
-// An epilogue with a slack(...) step for kTaskBound tasks (EpiDualFused).
-template <class E, class = void>
-struct FusedEpi : std::false_type {};
-template <class E>
-struct FusedEpi<E, std::void_t<decltype(E::kFused)>> : std::bool_constant<E::kFused> {};
-
 // EX: summation order -- 0 the fast order, 1 the reference's (Sched::exact),
 // 2 chosen at run time by S.exact (the main loop kernels compile it out: the
 // run-time branch costs them registers)
@@ -668,7 +641,6 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
                                           int gwarp, int lane, WarpStage* st, unsigned long long seq,
                                           const SpmvHead& head) {
   const bool exact = EX == 1 || (EX == 2 && S.exact);
-  constexpr bool FUS = FusedEpi<Epi>::value;
   const int W = S.W;
   const int n = S.n_tasks;
   const int4 kNone{0, 0, 0, 0};
@@ -694,10 +666,8 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
     // stream tasks: up to two rows per lane (lane, lane + 32); their bounds and
     // epilogue inputs are loaded before the gathers so the latencies overlap
     const int nrows = r1 - r0;
-    // bound tasks (fused phase B) are stream tasks of two-entry rows
-    const bool streamish = kind == kTaskStream || (FUS && kind == kTaskBound);
-    const bool has_row = streamish && lane < nrows;
-    const bool has_row2 = kStreamRowsMax > 32 && streamish && lane + 32 < nrows;
+    const bool has_row = kind == kTaskStream && lane < nrows;
+    const bool has_row2 = kStreamRowsMax > 32 && kind == kTaskStream && lane + 32 < nrows;
     int ra = 0, rb = 0, ra2 = 0, rb2 = 0;
     typename Epi::In in{}, in2{};
     if (has_row) {
@@ -731,13 +701,9 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
       const bool live = q < len;
 #endif
       HX_CHECK(!live || (cur.ci[j] >= 0 && cur.ci[j] < S.cols), "gather index", cur.ci[j], S.cols);
-      // a bound row's second entry is its slack column, whose x+ this task
-      // computes itself (Epi::slack): the coefficient stays in place
-      bool gather = live;
-      if constexpr (FUS) gather = live && !(kind == kTaskBound && (q & 1));
-      if (gather) cur.cv[j] = cur.cv[j] * src(cur.ci[j]);
+      if (live) cur.cv[j] = cur.cv[j] * src(cur.ci[j]);
     }
-    if (streamish) {
+    if (kind == kTaskStream) {
 #if HX_VEC
 #pragma unroll
       for (int jj = 0; jj < kLoadsPerLane / 2; ++jj)
@@ -747,13 +713,6 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
       for (int j = 0; j < kLoadsPerLane; ++j) st->prod[j * 32 + lane] = cur.cv[j];
 #endif
       __syncwarp();
-      if constexpr (FUS) {
-        // the slack columns' primal steps; each lane rewrites only its own
-        // rows' slack products, which only it sums
-        if (kind == kTaskBound) {
-          epi.slack_task(r0, has_row, has_row2, st->prod + (rb - 1 - p0), st->prod + (rb2 - 1 - p0), in, in2);
-        }
-      }
 #if HX_RSUM == 1
       // two interleaved partial sums (even / odd positions), combined at the
       // end: half the dependent-add chain; rows of <= 2 nonzeros keep the
@@ -1167,91 +1126,6 @@ struct EpiDual {  // phase B, rows of A
         t[5] = dyn * daxn;
       }
     }
-  }
-};
-
-// The fused loop's phase B epilogue (loop_kernel_fused).  The standard form
-// turns each finite column bound into a row x_j + s_i = u_i with a slack
-// column s_i of its own (the reference's to_standard_form); those rows are
-// A's last nb rows and their slacks A's last nb columns.  A slack column has
-// one entry, in its bound row, so its A^T y is a_is y_i -- and the bound row's
-// A x+ needs x+_s.  So phase A skips the slack columns (the loop's A^T
-// schedule stops at n - nb) and the bound row's lane runs the slack's primal
-// step (EpiPrimal's arithmetic, operand for operand) right before the row
-// sum, with y_i already in its registers: a quarter fewer phase A tasks on
-// configs[1].  The slack partials are this phase's quantities 4..6, which
-// the controller adds to phase A's 0..2.
-template <int EF>
-struct EpiDualFused : EpiDual<false, EF, false, false> {
-  using Base = EpiDual<false, EF, false, false>;
-  static constexpr bool kFused = true;
-  const KParams* P;
-  const Roles* R;
-  // each lane's slack partials, per warp in shared memory ([q][lane]): no
-  // accumulator registers held across the phase
-  __device__ __forceinline__ static double (*slack_acc())[32] {
-    __shared__ double buf[kWarps][3][32];
-    return buf[threadIdx.x >> 5];
-  }
-  // the slack steps of a bound task's rows r0 + lane (h1) and r0 + lane + 32
-  // (h2); p1 / p2: their staged slack entries, a_is on entry, a_is x+_s on
-  // exit.  The roles are read once per task (volatile: no role held in
-  // registers across the phase), the partials flushed once per task.
-  __device__ __forceinline__ void slack_task(int r0, bool h1, bool h2, double* p1, double* p2,
-                                             const typename Base::In& in1, const typename Base::In& in2) const {
-    const volatile Roles* r = R;
-    const int n = P->n, lane = threadIdx.x & 31;
-    const bool mode = r->x_mode != 0;
-    const double w = r->w_x, eta = r->eta;
-    const size_t off = static_cast<size_t>(n - P->m) + r0 + lane;
-    double* zx = P->xpool + static_cast<size_t>(r->zx_out) * n + off;
-    double* xp = P->xpool + static_cast<size_t>(r->xp_out) * n + off;
-    // loaded here, after the gathers: prefetching them into shared memory
-    // with cp.async before the gathers measured 2.7% slower on configs[1]
-    const double* xsp = (r->x_src_avg ? P->xavg : P->xpool) + static_cast<size_t>(r->x_src) * n + off;
-    const double* xap = P->xpool + static_cast<size_t>(r->x_anchor) * n + off;
-    double xs[2] = {0.0, 0.0}, xa[2] = {0.0, 0.0}, cc[2] = {0.0, 0.0};
-    if (h1) {
-      xs[0] = ld_epi<EF>(xsp);
-      if (mode) xa[0] = ld_epi<EF>(xap);
-      cc[0] = __ldg(P->c + off);
-    }
-    if (h2) {
-      xs[1] = ld_epi<EF>(xsp + 32);
-      if (mode) xa[1] = ld_epi<EF>(xap + 32);
-      cc[1] = __ldg(P->c + off + 32);
-    }
-    double q0 = 0.0, q1 = 0.0, q2 = 0.0;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      if (!(k ? h2 : h1)) continue;
-      double* prod = k ? p2 : p1;
-      const double a = *prod;
-      const double aty = 0.0 + a * (k ? in2.y : in1.y);  // the column's one-term row sum
-      double x;
-      if (mode) {
-        const double omw = 1.0 - w;
-        x = omw * xs[k] + w * xa[k];
-      } else {
-        x = xs[k];
-      }
-      const double cj = cc[k];
-      st_epi<EF>(zx + 32 * k, x);
-      double xn = x - eta * (aty + cj);
-      xn = xn < 0.0 ? 0.0 : xn;
-      xp[32 * k] = xn;
-      double rc = -(cj + aty);
-      rc = rc < 0.0 ? 0.0 : rc;
-      const double dx = x - xn;
-      q0 += rc * rc;
-      q1 += cj * x;
-      q2 += dx * dx;
-      *prod = a * xn;
-    }
-    double(*sa)[32] = slack_acc();
-    sa[0][lane] += q0;
-    sa[1][lane] += q1;
-    sa[2][lane] += q2;
   }
 };
 
@@ -1906,7 +1780,7 @@ __device__ __forceinline__ double* region_ptr(const KParams* P, int r, int nrec)
 __device__ __forceinline__ int gwarp_id(const Geo& g) { return g.cta * kWarps + (threadIdx.x >> 5); }
 
 // phase A: A^T y, primal step (+ Halpern formation of x), primal partials
-template <bool RK, bool BOX, int LM = 2, int EX = 2, bool TR = false, bool FU = false>
+template <bool RK, bool BOX, int LM = 2, int EX = 2, bool TR = false>
 __device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R, int par, WarpStage* stage,
                                                unsigned long long seq, const SpmvHead& head, const Geo& g) {
   constexpr int NQ = EpiPrimal<RK, BOX, 0, TR>::NQ;
@@ -1930,7 +1804,7 @@ __device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R,
                        P->r_tol,
                        P->tol_active,
                        R->tr_scale};
-  const Sched S = FU ? P->ATL : P->AT;
+  const Sched S = P->AT;
 #ifdef HX_WPROF
   const unsigned long long w0 = clock64();
 #endif
@@ -1941,11 +1815,11 @@ __device__ HX_PHASE_INLINE void phase_primal_t(const KParams* P, const Roles* R,
     if (P->prof && (threadIdx.x & 31) == 0) P->prof[gridDim.x * 16 + gwarp_id(g)] += clock64() - w0;
 #endif
   fold_long<NQ, 0>(S, par, seq, acc, g.cta, &P->bar->abort);
-  block_to_slots<NQ, 0, RK, KParams, FU>(acc, P, kRegA + par, g);
+  block_to_slots<NQ, 0, RK>(acc, P, kRegA + par, g);
 }
 
 // phase B: A x+, dual step, speculative Halpern combos, dual partials
-template <bool RK, int LM = 2, bool CB = false, int EX = 2, bool TR = false, bool FU = false>
+template <bool RK, int LM = 2, bool CB = false, int EX = 2, bool TR = false>
 __device__ HX_PHASE_INLINE bool phase_dual(const KParams* P, const Roles* R, int par, WarpStage* stage,
                                            unsigned long long seq, const SpmvHead& head, const Geo& g,
                                            unsigned long long* target = nullptr) {
@@ -1972,22 +1846,6 @@ __device__ HX_PHASE_INLINE bool phase_dual(const KParams* P, const Roles* R, int
             traced ? P->ring_y + static_cast<size_t>(R->tr_slot) * m : nullptr,
             R->tr_scale};
   const double* xsrc = P->xpool + static_cast<size_t>(R->xp_out) * n;
-  if constexpr (FU) {
-    static_assert(!RK && !CB && !TR, "the fused loop is single-GPU, unblocked, untraced");
-    using EF = EpiDualFused<LM == 1 ? HX_EPI_EF : 0>;
-    EF ef{e, P, R};
-    double(*sa)[32] = EF::slack_acc();
-    const int lane = threadIdx.x & 31;
-    sa[0][lane] = sa[1][lane] = sa[2][lane] = 0.0;
-    spmv_rows<QD, 0, LM, EX>(P->AL, par, SrcVecT<LM == 1 && HX_GATHER_LAST>{xsrc}, ef, acc, gwarp_id(g), lane, stage,
-                             seq, head);
-    fold_long<QD, 0>(P->AL, par, seq, acc, g.cta, &P->bar->abort);
-    // phase B's 4 quantities, then the slack partials (folded into phase A's
-    // record by block_to_slots)
-    const double af[7] = {acc[0], acc[1], acc[2], acc[3], sa[0][lane], sa[1][lane], sa[2][lane]};
-    block_to_slots<7, 0, RK, KParams, true>(af, P, kRegB + par, g);
-    return true;
-  }
   SpmvHead h1;
   if constexpr (CB) {
     // sweep 1: the leading column block's row sums into bpart, then a grid
@@ -2813,8 +2671,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_baseline(con
 // own kernel (team_setup_kernel), so the loop's register allocation is not
 // charged for them.
 // TR: the trace-ring kernels (loop_kernel_trace / loop_kernel_team_trace).
-template <bool RK, bool BOX = false, int LM = 2, bool CB = false, int EX = 2, bool SU = false, bool TR = false,
-          bool FU = false>
+template <bool RK, bool BOX = false, int LM = 2, bool CB = false, int EX = 2, bool SU = false, bool TR = false>
 __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
   __shared__ Ctl C;
   __shared__ double tot[kMaxQ];
@@ -2997,18 +2854,18 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
     const int par = static_cast<int>(C.it & 1);
     SpmvHead head;
     if (!spec_done) {
-      spmv_head<LM>(FU ? P->ATL : P->AT, gwarp_id(g), lane, head);
-      phase_primal_t<RK, BOX, LM, EX, TR, FU>(P, R, par, stage, ++seq, head, g);
+      spmv_head<LM>(P->AT, gwarp_id(g), lane, head);
+      phase_primal_t<RK, BOX, LM, EX, TR>(P, R, par, stage, ++seq, head, g);
       if (writer && threadIdx.x == 0 && budget != 0ull) set_time_up(par, (global_ns() - t_start) > budget ? 1u : 0u);
     }
     mark(0);
-    spmv_head<LM>(CB ? P->A0 : FU ? P->AL : P->A, gwarp_id(g), lane, head);
+    spmv_head<LM>(CB ? P->A0 : P->A, gwarp_id(g), lane, head);
     if (!sync()) return;
     mark(1);
-    if (!phase_dual<RK, LM, CB, EX, TR, FU>(P, R, par, stage, ++seq, head, g, &target)) return;
+    if (!phase_dual<RK, LM, CB, EX, TR>(P, R, par, stage, ++seq, head, g, &target)) return;
     if (threadIdx.x == 0) make_spec(C, SR);
     mark(2);
-    spmv_head<LM>(FU ? P->ATL : P->AT, gwarp_id(g), lane, head);
+    spmv_head<LM>(P->AT, gwarp_id(g), lane, head);
     if (!sync_reduce(par)) return;
     mark(3);
     if (warp == 0) {
@@ -3056,7 +2913,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
     mark(4);
     // speculative phase A of iteration it+1 (measured: worth ~10% against
     // running phase A after the controller)
-    phase_primal_t<RK, BOX, LM, EX, TR, FU>(P, &SR, par ^ 1, stage, ++seq, head, g);
+    phase_primal_t<RK, BOX, LM, EX, TR>(P, &SR, par ^ 1, stage, ++seq, head, g);
     if (writer && threadIdx.x == 0 && budget != 0ull)
       set_time_up(par ^ 1, (global_ns() - t_start) > budget ? 1u : 0u);
     __syncthreads();
@@ -3160,18 +3017,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_stream(const
   const Geo g{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x),
               static_cast<int>(gridDim.x)};
   loop_body<false, false, 1, false, 0>(&KP, g);
-}
-
-// The fused loop (EpiDualFused): bound rows' slack columns stepped in phase B.
-__global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_fused(const __grid_constant__ KParams KP) {
-  const Geo g{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x),
-              static_cast<int>(gridDim.x)};
-  loop_body<false, false, 0, false, 0, false, false, true>(&KP, g);
-}
-__global__ void __launch_bounds__(kThreads, kMinBlocks) loop_kernel_stream_fused(const __grid_constant__ KParams KP) {
-  const Geo g{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), static_cast<int>(blockIdx.x),
-              static_cast<int>(gridDim.x)};
-  loop_body<false, false, 1, false, 0, false, false, true>(&KP, g);
 }
 
 // The reference summation order (hx_set_sum_order): every row one
@@ -3526,9 +3371,6 @@ struct hx_ctx {
   double* b = nullptr;
   double* c = nullptr;
   DevSched sa, st;
-  // the fused loop (loop_kernel_fused): nb trailing bound rows / slack columns
-  DevSched sfa, sft;
-  int nb = 0;
   // column-blocked phase B (loop_kernel_stream_cb): A's leading / trailing
   // column blocks as CSR with their schedules, and the leading block's row sums
   int colblock = 0;
@@ -3703,9 +3545,6 @@ void free_problem(hx_ctx* c) {
   c->xavg = c->tavg = c->yavg = c->aavg = c->xbar = c->ub = nullptr;
   free_sched(c->sa);
   free_sched(c->st);
-  free_sched(c->sfa);
-  free_sched(c->sft);
-  c->nb = 0;
   free_sched(c->pa);
   free_sched(c->pt);
   free_sched(c->sb0);
@@ -3821,8 +3660,6 @@ KParams params(hx_ctx* c) {
   P.xavg = c->xavg, P.tavg = c->tavg, P.yavg = c->yavg, P.aavg = c->aavg, P.xbar = c->xbar;
   P.A0 = c->sb0.view;
   P.A1 = c->sb1.view;
-  P.AL = c->sfa.view;
-  P.ATL = c->sft.view;
   P.bpart = c->bpart;
   if (c->ring) {
     const RingLayout L = ring_layout(c->ring_cap, c->n, c->m);
@@ -3841,7 +3678,7 @@ int launch_loop(hx_ctx* c) {
   void* args[] = {&P};
   HX_CUDA(c, cudaMemcpyAsync(c->ctl, &c->h, sizeof(Ctl), cudaMemcpyHostToDevice, c->stream));
   HX_CUDA(c, cudaMemsetAsync(c->bar, 0, sizeof(GridBar), c->stream));
-  for (DevSched* d : {&c->sa, &c->st, &c->sb0, &c->sb1, &c->sfa, &c->sft})  // long-row flags restart per launch
+  for (DevSched* d : {&c->sa, &c->st, &c->sb0, &c->sb1})  // long-row flags restart with the per-launch sequence
     if (d->view.n_long)
       HX_CUDA(c, cudaMemsetAsync(d->flags, 0, 4 * static_cast<size_t>(d->view.n_long) * sizeof(unsigned long long),
                                  c->stream));
@@ -3852,8 +3689,6 @@ int launch_loop(hx_ctx* c) {
                            : c->sum_order == HX_SUM_REFERENCE ? reinterpret_cast<const void*>(loop_kernel_exact)
                            : c->sa.view.stream_hint && c->colblock && c->h.mode == kModeLoop
                                ? reinterpret_cast<const void*>(loop_kernel_stream_cb)
-                           : c->nb && c->sa.view.stream_hint ? reinterpret_cast<const void*>(loop_kernel_stream_fused)
-                           : c->nb                     ? reinterpret_cast<const void*>(loop_kernel_fused)
                            : c->sa.view.stream_hint    ? reinterpret_cast<const void*>(loop_kernel_stream)
                                                        : reinterpret_cast<const void*>(loop_kernel);
   HX_CUDA(c, cudaLaunchCooperativeKernel(kernel, dim3(c->grid), dim3(kThreads), args, kStageBytes, c->stream));
@@ -4098,10 +3933,6 @@ int hx_create(int32_t device, hx_ctx** out) {
   HX_CUDA(nullptr, cudaFuncSetAttribute(loop_kernel_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(kStageBytes)));
   HX_CUDA(nullptr, cudaFuncSetAttribute(loop_kernel_stream_cb, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(kStageBytes)));
-  HX_CUDA(nullptr, cudaFuncSetAttribute(loop_kernel_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(kStageBytes)));
-  HX_CUDA(nullptr, cudaFuncSetAttribute(loop_kernel_stream_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(kStageBytes)));
   int occ = 0;
   HX_CUDA(nullptr, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, loop_kernel, kThreads, kStageBytes));
@@ -4486,22 +4317,19 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   }
   tick("transpose");
   // Schedules (host, from the pointer arrays).
-  std::vector<int> pt(static_cast<size_t>(n) + 1);
-  double lead_t = 0.0;
   {
+    std::vector<int> pt(static_cast<size_t>(n) + 1);
     HX_CUDA(c, cudaMemcpy(pt.data(), c->t_ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost));
     // phase A (rows of A^T) runs speculatively while warp 0 of every CTA runs
     // the controller: warp 0 starts with a lead of about the controller's
     // latency, in schedule cost units (~100 per microsecond on B200)
     double lead = 1200.0;
     if (const char* e = std::getenv("HX_LEAD")) lead = std::atof(e);
-    lead_t = lead;
     // A^T's schedule is built on a host thread while A's uploads
     auto sched_t = std::async(std::launch::async, [&pt, n, sched_warps, lead, exact] {
       double rc, tc;
       sched_costs(true, rc, tc);
-      int skip = std::getenv("HX_HACK_SKIP") ? std::atoi(std::getenv("HX_HACK_SKIP")) : 0;
-      return build_schedule(pt.data(), static_cast<int>(n) - skip, sched_warps, lead, rc, tc, exact);
+      return build_schedule(pt.data(), static_cast<int>(n), sched_warps, lead, rc, tc, exact);
     });
     int rc = upload_built_sched(c, c->sa, sched_a.get(), static_cast<int>(m), static_cast<int>(n), c->a_ptr,
                                 c->a_idx, c->a_val, 0);
@@ -4526,47 +4354,6 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     c->sa.view.row_limit = static_cast<int>(m);  // output dimension (HX_CHECKED)
     c->st.view.row_limit = static_cast<int>(n);
     c->sa.view.exact = c->st.view.exact = exact ? 1 : 0;
-    // The fused loop (EpiDualFused): the standard form's bound rows
-    // x_j + s_i = u_i are A's trailing rows, each of two entries whose second
-    // is its own slack column -- the trailing columns, one entry each.  Count
-    // them; the loop then runs on two more schedules: A with those rows as
-    // kTaskBound tasks, A^T without the slack columns.  Fast order only (the
-    // reference order keeps its kernel); HX_FUSE=0 turns it off.
-    int nb = 0;
-    bool fuse = !exact && nnz > 0;
-    if (const char* e = std::getenv("HX_FUSE")) fuse = fuse && std::atoi(e) != 0;
-    if (fuse) {
-      while (nb < m && nb < n) {
-        const int64_t i = m - 1 - nb, sc = n - 1 - nb;
-        if (row_ptr[i + 1] - row_ptr[i] != 2 || col_idx[row_ptr[i] + 1] != sc || pt[sc + 1] - pt[sc] != 1) break;
-        ++nb;
-      }
-      for (int64_t i = m - nb; i < m; ++i)
-        if (col_idx[row_ptr[i]] >= n - nb) {  // a bound row on another slack: not this shape
-          nb = 0;
-          break;
-        }
-    }
-    if (nb > 0) {
-      const int mi = static_cast<int>(m), nl = static_cast<int>(n) - nb;
-      auto fa = std::async(std::launch::async, [&ph, mi, nb, sched_warps] {
-        double rc, tc;
-        sched_costs(false, rc, tc);
-        return build_schedule(ph.data(), mi, sched_warps, 0.0, rc, tc, false, mi - nb);
-      });
-      double rc, tc;
-      sched_costs(true, rc, tc);
-      int e = upload_built_sched(c, c->sft, build_schedule(pt.data(), nl, sched_warps, lead_t, rc, tc), nl, mi, c->t_ptr,
-                                 c->t_idx, c->t_val, 0);
-      if (e) return e;
-      e = upload_built_sched(c, c->sfa, fa.get(), mi, static_cast<int>(n), c->a_ptr, c->a_idx, c->a_val, 0);
-      if (e) return e;
-      c->sfa.view.stream_hint = c->sft.view.stream_hint = hint;
-      c->sfa.view.row_limit = mi;
-      c->sft.view.row_limit = static_cast<int>(n);
-      c->nb = nb;
-      tick("fused sched");
-    }
     // Column-blocked phase B (loop_kernel_stream_cb): when x+ is far larger
     // than L2 its random gathers miss (configs[4]: 9.5 GB of DRAM traffic per
     // iteration against 5.0 GB algorithmic, L2 hit rate 38%), so A is split at
@@ -4783,11 +4570,7 @@ int hx_precondition(hx_ctx* c, int32_t ruiz_iters, double pc_alpha, double* row_
 int32_t hx_loop_variant(hx_ctx* c) {
   if (!c || !c->uploaded) return -1;
   if (c->ranked) return c->pa.view.stream_hint && c->pt.view.stream_hint ? 6 : 5;
-  if (c->ub) return 2;
-  if (c->sum_order == HX_SUM_REFERENCE) return 4;
-  if (c->sa.view.stream_hint && c->colblock) return 3;
-  if (c->nb) return c->sa.view.stream_hint ? 8 : 7;
-  return c->sa.view.stream_hint ? 1 : 0;
+  return c->ub ? 2 : c->sum_order == HX_SUM_REFERENCE ? 4 : c->sa.view.stream_hint ? (c->colblock ? 3 : 1) : 0;
 }
 
 int hx_set_box(hx_ctx* c, const double* upper) {

@@ -68,7 +68,6 @@ constexpr double kTaskCost = 64.0;         // fixed latency cost of one warp tas
 #ifndef HX_RSPLIT
 #define HX_RSPLIT 0
 #endif
-
 constexpr int kLoadsPerLane = HX_LOADS;    // nonzeros per lane per task
 constexpr int kChunk = 32 * kLoadsPerLane; // nonzero slots per warp task (256)
 // Vectorised idx/val loads (int2 / double2 from an even-aligned window, see
@@ -104,11 +103,7 @@ constexpr int kMaxRanks = 8;               // ranks of a row-partitioned team (o
 //                carries the run's partial sum in registers; only the run's
 //                last piece (kTaskPiece) publishes it, so a run of r pieces
 //                costs one fence + atomic instead of r (configs[4]'s Zipf rows).
-//   kTaskBound:  (the fused loop's phase B schedule only) consecutive bound
-//                rows x_j + s = u of the standard form, each {j, its slack
-//                column s} -- a stream task whose lanes also run the slack
-//                column's primal step (fused_bounds in hx.cu).
-enum TaskKind : int { kTaskStream = 0, kTaskPiece = 1, kTaskPieceRun = 2, kTaskBound = 3 };
+enum TaskKind : int { kTaskStream = 0, kTaskPiece = 1, kTaskPieceRun = 2 };
 constexpr int kKindShift = 30;
 constexpr int kRowMask = (1 << kKindShift) - 1;
 __host__ __device__ __forceinline__ int task_kind(int y) {
@@ -190,9 +185,7 @@ struct SchedHost {
 // controller before its own tasks in the speculative phase A.
 // exact: reference summation order -- every long row becomes ONE run of
 // pieces (one warp carries the sequential sum through all of them).
-// bound_from: rows from this index on are bound rows, packed into kTaskBound
-// tasks of their own (-1: none).
 SchedHost build_schedule(const int* ptr_host, int rows, int warps, double lead = 0.0, double row_cost = kRowCost,
-                         double task_cost = kTaskCost, bool exact = false, int bound_from = -1);
+                         double task_cost = kTaskCost, bool exact = false);
 
 }  // namespace hx

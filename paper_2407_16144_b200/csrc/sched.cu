@@ -3,13 +3,15 @@
 // Rows of length <= kStreamRowMax are packed into stream tasks of at most
 // kChunk nonzeros / kStreamRowsMax rows; every longer row is cut into pieces
 // of at most kChunk nonzeros (a single piece when it fits), grouped into runs
-// of consecutive pieces that one warp processes back to back.  The row-ordered
-// task list is then cut into one contiguous, equal-cost slice per warp
-// (cost = nnz + kRowCost per row).  Static and deterministic: the same matrix
-// and grid always give the same row -> (warp, lane) map, which is what makes
-// every reduction in the solver reproducible bit for bit.
+// of consecutive pieces that one warp processes back to back.  The units
+// (a stream task, a run) are then dealt heaviest first, each to the
+// least-loaded CTA and within it to the least-loaded warp (cost = nnz +
+// kRowCost per row + kTaskCost per task).  Static and deterministic: the same
+// matrix and grid always give the same row -> (warp, lane) map, which is what
+// makes every reduction in the solver reproducible bit for bit.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <functional>
 #include <queue>
 
@@ -18,7 +20,7 @@
 namespace hx {
 
 SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, double row_cost, double task_cost,
-                         bool exact, int bound_from) {
+                         bool exact) {
   SchedHost s;
   const int64_t nnz = ptr[rows] - ptr[0];  // ptr may point into a larger matrix (a rank's block)
   const double total = static_cast<double>(nnz) + row_cost * rows;
@@ -33,6 +35,8 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, doubl
   // a run of pieces is dealt to one warp as a unit: at most 1/kRunFrac of the
   // mean warp cost, so the dealing stays balanced
   const double run_budget = std::max(1.0, total / warps / kRunFrac);
+  int64_t task_nnz = kTaskNnz;
+  if (const char* e = std::getenv("HX_TASK_NNZ")) task_nnz = std::max(8, std::min<int>(kTaskNnz, std::atoi(e)));
   int r = 0;
   while (r < rows) {
     const int64_t len = ptr[r + 1] - ptr[r];
@@ -63,28 +67,25 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, doubl
       continue;
     }
     const int r0 = r;
-    // a task never mixes bound rows with others
-    const bool bound = bound_from >= 0 && r0 >= bound_from;
-    const int stop = !bound && bound_from >= 0 ? bound_from : rows;
     int64_t used = 0;
-    while (r < stop && r - r0 < kStreamRowsMax) {
+    while (r < rows && r - r0 < kStreamRowsMax) {
       const int64_t l = ptr[r + 1] - ptr[r];
-      if (l > kStreamRowMax || used + l > kTaskNnz) break;
+      if (l > kStreamRowMax || used + l > task_nnz) break;
       used += l;
       ++r;
     }
     unit.push_back(s.tasks.size());
-    // a bound row also carries its slack column's primal step: one more row's worth
-    push(r0, r, bound ? kTaskBound : kTaskStream, static_cast<int>(ptr[r0]), static_cast<int>(ptr[r]),
-         int4{0, 0, 0, 0}, static_cast<double>(used) + row_cost * (r - r0) * (bound ? 2.0 : 1.0));
+    push(r0, r, kTaskStream, static_cast<int>(ptr[r0]), static_cast<int>(ptr[r]), int4{0, 0, 0, 0},
+         static_cast<double>(used) + row_cost * (r - r0));
   }
   const std::size_t nt = s.tasks.size();
   unit.push_back(nt);
 
   // Longest-processing-time dealing: units heaviest first, each to the
-  // currently least-loaded warp (ties to the lower warp id).  Warp w's tasks are
-  // laid out at positions w, w + W, w + 2W, ... (padded with empty tasks),
-  // which is how the kernels walk them; a run's pieces stay consecutive.
+  // currently least-loaded CTA, then its least-loaded warp (ties to the lower
+  // id).  Warp w's tasks are laid out at positions w, w + W, w + 2W, ...
+  // (padded with empty tasks), which is how the kernels walk them; a run's
+  // pieces stay consecutive.
   // Deterministic and balanced; reductions stay fixed-order because every row
   // keeps one (warp, lane) owner.
   const std::size_t nu = unit.size() - 1;
@@ -98,16 +99,40 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, doubl
   std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
   std::vector<std::vector<int>> per_warp(static_cast<std::size_t>(warps));
   std::vector<double> wcost(static_cast<std::size_t>(warps), 0.0);
-  for (int w = 0; w < warps; ++w) {
-    wcost[w] = w % kWarps == 0 ? lead : 0.0;
-    heap.push({wcost[w], w});
-  }
-  for (int u : order) {
-    auto [load, w] = heap.top();
-    heap.pop();
-    for (std::size_t t = unit[u]; t < unit[u + 1]; ++t) per_warp[w].push_back(static_cast<int>(t));
-    wcost[w] = load + ucost[u];
-    heap.push({wcost[w], w});
+  for (int w = 0; w < warps; ++w) wcost[w] = w % kWarps == 0 ? lead : 0.0;
+  int deal = 1;
+  if (const char* e = std::getenv("HX_DEAL")) deal = std::atoi(e);
+  if (deal == 1 && warps % kWarps == 0) {
+    // two levels: each unit to the least-loaded CTA (the SM's warps share its
+    // load/store pipes, so CTA sums set the phase time as much as the
+    // longest warp), then to that CTA's least-loaded warp.  Against dealing
+    // to the least-loaded warp alone (HX_DEAL=0; CTA sums up to 17% apart on
+    // configs[1]'s A^T): configs[1] 27.45k -> 28.29k it/s, configs[2] 42.9k
+    // -> 47.9k.  HX_TASK_NNZ (a smaller cap on a stream task's nonzeros)
+    // measured slower at every cap: 224 / 192 / 128 -> 25.9k / 24.3k / 22.2k.
+    const int grid = warps / kWarps;
+    std::vector<double> ccost(static_cast<std::size_t>(grid), 0.0);
+    for (int c = 0; c < grid; ++c) heap.push({0.0, c});
+    for (int u : order) {
+      auto [load, c] = heap.top();
+      heap.pop();
+      int w = c * kWarps;
+      for (int i = 1; i < kWarps; ++i)
+        if (wcost[c * kWarps + i] < wcost[w]) w = c * kWarps + i;
+      for (std::size_t t = unit[u]; t < unit[u + 1]; ++t) per_warp[w].push_back(static_cast<int>(t));
+      wcost[w] += ucost[u];
+      ccost[c] = load + ucost[u];
+      heap.push({ccost[c], c});
+    }
+  } else {
+    for (int w = 0; w < warps; ++w) heap.push({wcost[w], w});
+    for (int u : order) {
+      auto [load, w] = heap.top();
+      heap.pop();
+      for (std::size_t t = unit[u]; t < unit[u + 1]; ++t) per_warp[w].push_back(static_cast<int>(t));
+      wcost[w] = load + ucost[u];
+      heap.push({wcost[w], w});
+    }
   }
   std::size_t rounds = 0;
   for (const auto& v : per_warp) rounds = std::max(rounds, v.size());

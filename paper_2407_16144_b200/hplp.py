@@ -457,8 +457,7 @@ class HX:
         return dict(sm_count=sm.value, grid=g.value, threads=t.value)
 
     LOOP_KERNELS = ("hx::loop_kernel", "hx::loop_kernel_stream", "hx::loop_kernel_box", "hx::loop_kernel_stream_cb",
-                    "hx::loop_kernel_exact", "hx::loop_kernel_team", "hx::loop_kernel_team_stream",
-                    "hx::loop_kernel_fused", "hx::loop_kernel_stream_fused")
+                    "hx::loop_kernel_exact", "hx::loop_kernel_team", "hx::loop_kernel_team_stream")
 
     def loop_kernel(self) -> str:
         """Name of the loop kernel hx_run launches for this problem."""

@@ -327,7 +327,7 @@ def test_column_blocked_phase_b_parity(gpu_required, name, monkeypatch):
         g4 = sol.solve(iteration_limit=300000, tolerance=1e-4)
         monkeypatch.setenv("HX_COLBLOCK", "0")
         ref = hplp.Solver(*args)
-        assert ref.hx.loop_kernel() in ("hx::loop_kernel_stream", "hx::loop_kernel_stream_fused")
+        assert ref.hx.loop_kernel() == "hx::loop_kernel_stream"
         r4 = ref.solve(iteration_limit=300000, tolerance=1e-4)
         ref.close()
         assert g4["status"] == r4["status"]
@@ -448,69 +448,5 @@ def test_trace_ring_minimum_capacity_and_disabled(gpu_required, monkeypatch):
         assert np.array_equal(a["x"], c["x"]) and np.array_equal(a["y"], c["y"])
         assert all(np.array_equal(u, v) for u, v in zip(a["partition"], b["partition"]))
         assert sum(len(np.setxor1d(u, v)) for u, v in zip(a["partition"], c["partition"])) <= 1
-        assert a["kkt"] == b["kkt"]
-        # the pause-per-record path runs the plain loop kernel -- the fused one
-        # on this instance (bound rows), whose totals add the slack columns'
-        # partials in another order: same iterates, KKT within rounding
-        np.testing.assert_allclose(c["kkt"], a["kkt"], rtol=1e-12, atol=0.0)
+        assert a["kkt"] == b["kkt"] == c["kkt"]
     assert np.array_equal(base["x"], small["x"]) and np.array_equal(base["x"], off["x"])
-
-
-@pytest.mark.parametrize("name", ["cfg0", "cfg1_small", "cfg2_small"])
-def test_fused_bound_rows_parity(gpu_required, monkeypatch, name):
-    """loop_kernel_fused: the standard form's bound rows x_j + s = u are A's
-    trailing rows and their slacks its trailing columns; the fused loop steps
-    those slack columns inside phase B's bound-row tasks instead of phase A.
-    Per iteration (pause-per-record traces, which run the fused kernel) it
-    matches the port, and its iterates equal the unfused loop's bit for bit;
-    to tolerance, same status and iteration count."""
-    g, s = std(name)
-    args = csr_args(s)
-    monkeypatch.setenv("HPLP_TRACE_RING", "0")
-    sol = hplp.Solver(*args)
-    assert sol.hx.loop_kernel() in ("hx::loop_kernel_fused", "hx::loop_kernel_stream_fused")
-    kw = dict(iteration_limit=150, tolerance=1e-12, trace=True)
-    fused = sol.solve(**kw)
-    cpu = CpuLp("port", *args).solve(**kw)
-    _trace_cmp(fused["trace"], cpu["trace"])
-    assert fused["spmv_count"] == cpu["spmv_count"]
-    f4 = sol.solve(iteration_limit=200000, tolerance=1e-4)
-    sol.close()
-    monkeypatch.setenv("HX_FUSE", "0")
-    ref = hplp.Solver(*args)
-    assert ref.hx.loop_kernel() in ("hx::loop_kernel", "hx::loop_kernel_stream")
-    plain = ref.solve(**kw)
-    r4 = ref.solve(iteration_limit=200000, tolerance=1e-4)
-    ref.close()
-    for a, b in zip(fused["trace"], plain["trace"]):
-        assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["y"], b["y"])
-    assert np.array_equal(fused["x"], plain["x"]) and np.array_equal(fused["y"], plain["y"])
-    assert (f4["status"], f4["iterations"]) == (r4["status"], r4["iterations"])
-    c = args[6]
-    assert abs(float(c @ f4["x"]) - float(c @ r4["x"])) <= 1e-9 * max(1.0, abs(float(c @ r4["x"])))
-
-
-def test_fused_needs_the_bound_row_shape(gpu_required, monkeypatch):
-    """Without trailing bound rows (or with HX_FUSE=0, or the reference
-    summation order) the plain loop kernel runs."""
-    m, n = 3, 5
-    rp = np.array([0, 2, 4, 6], np.int64)
-    ci = np.array([0, 1, 1, 2, 3, 4], np.int32)
-    val = np.ones(6)
-    b = np.ones(m)
-    c = np.ones(n)
-    # the last row {3, 4}: its second column is the last column, which has
-    # no other entry -- one bound row, fused
-    sol = hplp.Solver(m, n, rp, ci, val, b, c)
-    assert sol.hx.loop_kernel() == "hx::loop_kernel_fused"
-    sol.close()
-    # a second entry in the last column: no bound rows
-    rp2 = np.array([0, 3, 5, 7], np.int64)
-    ci2 = np.array([0, 1, 4, 1, 2, 3, 4], np.int32)
-    sol = hplp.Solver(m, n, rp2, ci2, np.ones(7), b, c)
-    assert sol.hx.loop_kernel() == "hx::loop_kernel"
-    sol.close()
-    monkeypatch.setenv("HX_FUSE", "0")
-    sol = hplp.Solver(m, n, rp, ci, val, b, c)
-    assert sol.hx.loop_kernel() == "hx::loop_kernel"
-    sol.close()
