@@ -33,8 +33,13 @@ constexpr int kYPool = 6;                  // m-vectors: y, anchors, best, T(z),
 constexpr int kAxPool = 4;                 // m-vectors: A x carried / anchor / products
 constexpr int kAvgPool = 4;                // running-average slots (baseline schemes): current, new, best, restart point
 constexpr int kEpochCap = 1 << 16;         // device epoch ring (host drains per hx_run)
-constexpr double kRowCost = 3.0;           // epilogue cost of one row in nnz units
-constexpr double kTaskCost = 64.0;         // fixed latency cost of one warp task in nnz units
+// Schedule cost model (nnz units).  With CTA-first dealing (sched.cu),
+// tools/cost_sweep.sh on configs[1] / [2]: row cost 2 / 3 / 5 / 7 / 10 ->
+// 27.2k / 28.3k / 28.5k / 28.5k / 28.0k and 46.9k / 47.9k / 48.9k / 48.9k /
+// 47.3k it/s (phase A sets it; phase B is flat from 5 to 10); the task cost
+// is flat from 32 to 200.
+constexpr double kRowCost = 5.0;           // epilogue cost of one row
+constexpr double kTaskCost = 64.0;         // fixed latency cost of one warp task
 #ifndef HX_LOADS
 #define HX_LOADS 8
 #endif

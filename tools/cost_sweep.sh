@@ -1,3 +1,5 @@
-for c in "3,64,3,64" "4.6,64,3,64" "4.6,20,3,64" "3,64,0.5,91" "4.6,20,0.5,91" "6,64,3,64" "3,64,1,120" "3,64,3,64"; do
-  echo -n "$c: "; HX_COSTS=$c python tools/quick_rate.py 1
+# schedule cost model (HX_COSTS = rowA,taskA,rowB,taskB in nnz units; A = A^T's
+# rows in phase A, B = A's rows in phase B) against configs[1] / [2]
+for c in "5,64,5,64" "7,64,7,64" "10,64,10,64" "14,64,14,64" "5,64,10,64" "10,64,5,64" "20,64,20,64"; do
+  for g in 1 2; do echo -n "$c cfg$g: "; HX_COSTS=$c python tools/quick_rate.py $g; done
 done
