@@ -1520,7 +1520,7 @@ __device__ void finish_iteration(Ctl& C, hplp_epoch_t* epochs, bool writer, doub
 // (|N|, |B1|, |B2|, and the normalized candidate's ||dx||^2, ||dy||^2,
 // dy.d(Ax)) when the iteration is traced into a ring, else null.
 __device__ void main_logic(Ctl& C, const double* tot, const double* pre, hplp_epoch_t* epochs, bool writer,
-                           bool time_up, TraceRec* ring = nullptr, const double* trt = nullptr) {
+                           bool time_up, TraceRec* ring = nullptr, const double* trt = nullptr, bool check_due = false) {
   Roles& R = C.r;
   const double dx2 = tot[2], dy2 = tot[5], dyax = tot[6];
   double kkt[4];
@@ -1609,7 +1609,9 @@ __device__ void main_logic(Ctl& C, const double* tot, const double* pre, hplp_ep
     if (C.trace_period > 0 && C.last_it % C.trace_period == 0) C.paused = 1;
     return;
   }
-  if (C.check_period > 0 && C.it > 0 && (C.it % C.check_period == 0 || C.k == 0)) {  // :297-298
+  // check_due: C.it % C.check_period == 0, a 64-bit remainder warp 0 forms
+  // on another lane beside the KKT divides
+  if (C.check_period > 0 && C.it > 0 && (check_due || C.k == 0)) {  // :297-298
     R.check = 1;
     R.cand_scale = C.k >= 1 ? 2.0 / static_cast<double>(C.k) : 0.0;
     return;
@@ -1875,41 +1877,51 @@ __device__ HX_PHASE_INLINE bool phase_dual(const KParams* P, const Roles* R, int
 }
 
 // Totals of phases A+B -> t[0..6], computed by warp 0 alone (the other warps
-// are in the speculative phase A by then): lane l sums records l, l + 32, ...
-// and a xor butterfly finishes -- commutative pairwise adds, so every lane of
-// every CTA holds bit-identical totals.
-constexpr int kTotRounds = 5;  // 160 records in one round of loads
+// are in the speculative phase A by then).  Lane l reads record l / 2 + 16 k
+// of phase A's (even lanes) or phase B's (odd lanes) region as one 256-bit
+// load of quantities 0..3: all 148 records of a single GPU in one round of
+// 10 independent loads per lane (one L2 round trip; the loads queue behind
+// the speculative phase A's gathers, so each extra round trip costs ~0.7 us
+// -- configs[2]: lane-per-record scalar loads 3.7 us, this ~1.5).  Each lane
+// sums its records in order, then a xor butterfly over the 16 lanes of a
+// region finishes -- a fixed order, so every CTA holds bit-identical totals.
 // t[0..2]: phase A partials, t[3..6]: phase B, t[7]: the box form's bound
 // term of the dual objective (phase A's fourth partial; 0 in standard form)
+constexpr int kTotBatch = 10;  // records per lane per round: 16 * 10 = 160 >= 148
 template <bool BOX>
 __device__ __forceinline__ void warp_totals_main(const KParams* P, int par, double (&t)[8], const Geo& g) {
   const int lane = threadIdx.x & 31, G = g.nrec;
   const size_t rep = static_cast<size_t>(g.cta % kReplicas) * G * kMaxQ;
-  const double* ra = region_ptr(P, kRegA + par, G) + rep;
-  const double* rb = region_ptr(P, kRegB + par, G) + rep;
+  const double* base = region_ptr(P, (lane & 1) ? kRegB + par : kRegA + par, G) + rep;
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int c0 = lane >> 1; c0 < G; c0 += 16 * kTotBatch) {
+    double v[kTotBatch][4];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) t[q] = 0.0;
-  for (int base = 0; base < G; base += 32 * kTotRounds) {
-    double v[kTotRounds][8];
-#pragma unroll
-    for (int i = 0; i < kTotRounds; ++i) {
-      const int c = base + 32 * i + lane;
-      const bool ok = c < G;
-      const double* a = ra + static_cast<size_t>(c) * kMaxQ;
-      const double* b = rb + static_cast<size_t>(c) * kMaxQ;
-#pragma unroll
-      for (int q = 0; q < 3; ++q) v[i][q] = ok ? ldcg(a + q) : 0.0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) v[i][3 + q] = ok ? ldcg(b + q) : 0.0;
-      v[i][7] = BOX && ok ? ldcg(a + 3) : 0.0;
+    for (int k = 0; k < kTotBatch; ++k) {
+      const int c = c0 + 16 * k;
+      if (c < G) {
+        asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
+                     : "=d"(v[k][0]), "=d"(v[k][1]), "=d"(v[k][2]), "=d"(v[k][3])
+                     : "l"(base + static_cast<size_t>(c) * kMaxQ));
+      } else {
+        v[k][0] = v[k][1] = v[k][2] = v[k][3] = 0.0;
+      }
     }
 #pragma unroll
-    for (int i = 0; i < kTotRounds; ++i)
+    for (int k = 0; k < kTotBatch; ++k)
 #pragma unroll
-      for (int q = 0; q < (BOX ? 8 : 7); ++q) t[q] += v[i][q];
+      for (int q = 0; q < 4; ++q) s[q] += v[k][q];
   }
 #pragma unroll
-  for (int q = 0; q < (BOX ? 8 : 7); ++q) t[q] = warp_sum(t[q]);
+  for (int m = 2; m < 32; m *= 2)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) s[q] += __shfl_xor_sync(0xffffffffu, s[q], m);
+  t[0] = __shfl_sync(0xffffffffu, s[0], 0);
+  t[1] = __shfl_sync(0xffffffffu, s[1], 0);
+  t[2] = __shfl_sync(0xffffffffu, s[2], 0);
+  t[7] = BOX ? __shfl_sync(0xffffffffu, s[3], 0) : 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) t[3 + q] = __shfl_sync(0xffffffffu, s[q], 1);
 }
 
 // Trace totals of a traced iteration (every rank's records, fixed order).
@@ -2870,6 +2882,9 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
     mark(3);
     if (warp == 0) {
       unsigned long long cA = clock64(), cB = 0, cC = 0;
+      // (issuing these loads before the other warps start the speculative
+      // phase A -- a named barrier -- measured slower: the 40 registers they
+      // hold across the barrier spill)
       double t[8];
       if (solo || !P->T.prereduce) warp_totals_main<BOX>(P, par, t, g);
       else warp_totals_ranks(P, par, t, g.cta);
@@ -2888,6 +2903,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
       double pre[7];
 #pragma unroll
       for (int i = 0; i < 7; ++i) pre[i] = __shfl_sync(0xffffffffu, v, i);
+      const int due = __shfl_sync(0xffffffffu, lane == 7 && C.check_period > 0 && C.it % C.check_period == 0, 7);
       cB = clock64();
       // a traced iteration of a trace-ring kernel: the classes' counts and
       // the normalized candidate's sums (phase A partials 3..6, phase B 4..5)
@@ -2901,7 +2917,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
         C.w_k2 = pre[5];
         C.w_k3 = pre[6];
         main_logic(C, tot, pre, P->epochs, writer, s_time_up != 0, traced ? P->ring_rec : nullptr,
-                   traced ? trt : nullptr);
+                   traced ? trt : nullptr, due != 0);
       }
       cC = clock64();
       __syncwarp();
@@ -4116,7 +4132,7 @@ int upload_ranked(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   if (n) HX_CUDA(c, cudaMemcpyAsync(c->c, cc, n * sizeof(double), cudaMemcpyHostToDevice, s));
   HX_CUDA(c, cudaStreamSynchronize(s));  // the host vectors go out of scope
   // schedules of the blocks; rows / columns stay global through offset pointers
-  double lead = 1200.0;
+  double lead = kLead;
   if (const char* e = std::getenv("HX_LEAD")) lead = std::atof(e);
   const bool exact = c->sum_order == HX_SUM_REFERENCE;
   const int warps = c->grid * kWarps;
@@ -4321,9 +4337,8 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     std::vector<int> pt(static_cast<size_t>(n) + 1);
     HX_CUDA(c, cudaMemcpy(pt.data(), c->t_ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost));
     // phase A (rows of A^T) runs speculatively while warp 0 of every CTA runs
-    // the controller: warp 0 starts with a lead of about the controller's
-    // latency, in schedule cost units (~100 per microsecond on B200)
-    double lead = 1200.0;
+    // the controller: warp 0 starts with a lead (kLead)
+    double lead = kLead;
     if (const char* e = std::getenv("HX_LEAD")) lead = std::atof(e);
     // A^T's schedule is built on a host thread while A's uploads
     auto sched_t = std::async(std::launch::async, [&pt, n, sched_warps, lead, exact] {

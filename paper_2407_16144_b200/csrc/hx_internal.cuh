@@ -40,6 +40,12 @@ constexpr int kEpochCap = 1 << 16;         // device epoch ring (host drains per
 // is flat from 32 to 200.
 constexpr double kRowCost = 5.0;           // epilogue cost of one row
 constexpr double kTaskCost = 64.0;         // fixed latency cost of one warp task
+// Warp 0 of every CTA runs the controller while warps 1..15 start the
+// speculative phase A: its schedule share starts with this lead (cost
+// units).  tools/lead_sweep.sh with CTA-first dealing, configs[1]: 600 / 1200
+// / 2200 / 3000 / 6000 / no tasks -> 27.99k / 28.54k / 28.70k / 28.70k /
+// 28.69k / 28.67k it/s (configs[0], [2] flat from 900 on).
+constexpr double kLead = 3000.0;
 #ifndef HX_LOADS
 #define HX_LOADS 8
 #endif
