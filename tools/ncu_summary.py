@@ -2,7 +2,7 @@
 launch, tools/profile_loop.py) into profiles/: traffic JSON (per iteration and
 per 1000-iteration bench launch) and the stall share per hx.cu source line.
 
-  python tools/ncu_summary.py gpurun_out/loop_full3.ncu-rep "label"
+  python tools/ncu_summary.py gpurun_out/loop_full3.ncu-rep "label" [stalls.csv]
 """
 import csv
 import json
@@ -54,7 +54,7 @@ for r in rows[hi + 1:]:
     if len(r) > 2 and r[2]:
         agg[cur] = agg.get(cur, 0) + s
 T = sum(agg.values())
-with open("profiles/r01_loop_stalls_by_line.csv", "w") as f:
+with open(sys.argv[3] if len(sys.argv) > 3 else "profiles/loop_stalls_by_line.csv", "w") as f:
     f.write(f"# {label}\nshare_pct,hx.cu_line,source\n")
     for line, s in sorted(agg.items(), key=lambda x: -x[1])[:30]:
         f.write(f"{s / T * 100:.2f},{line},\"{text.get(line, '').strip()[:120].replace(chr(34), chr(39))}\"\n")
