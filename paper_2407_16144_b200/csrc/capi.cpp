@@ -1,6 +1,9 @@
 // C ABI (include/hplp_gpu.h) over the C++ host driver (hplp_gpu.hpp).
 #include <algorithm>
 #include <cmath>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -250,11 +253,23 @@ int hplp_solve_csr(int32_t device, int64_t m, int64_t n, const int64_t* row_ptr,
   // problem uploads
   hplp_gpu::PowerStartFuture start;
   if (cfg && n > 0) start = hplp_gpu::draw_power_start_async(n, cfg->seed);
+  // HPLP_TIMING=1: the three stages' wall times on stderr
+  const char* te = std::getenv("HPLP_TIMING");
+  const bool timing = te && te[0] == '1';
+  const auto t0 = std::chrono::steady_clock::now();
+  auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double, std::milli>(b - a).count();
+  };
   int rc = hplp_solver_create(device, m, n, row_ptr, col_idx, val, b, c, &s);
   if (rc != HPLP_OK) return rc;
+  const auto t1 = std::chrono::steady_clock::now();
   if (start.valid()) static_cast<hplp_gpu::Solver*>(s)->use_power_start(cfg->seed, start);
   rc = hplp_solver_solve(s, cfg, io, result);
+  const auto t2 = std::chrono::steady_clock::now();
   hplp_solver_free(s);
+  if (timing)
+    std::fprintf(stderr, "hplp_solve_csr: create+upload %.3f ms, solve %.3f ms, free %.3f ms\n", ms(t0, t1), ms(t1, t2),
+                 ms(t2, std::chrono::steady_clock::now()));
   return rc;
 }
 
