@@ -256,10 +256,14 @@ struct KParams {
   double* yavg;   // m: mean y
   double* aavg;   // m: mean A x
   double* xbar;   // n: x-part of the PDHG step taken at the average
-  // column-blocked phase B (loop_kernel_stream_cb): A split at a column into
-  // A0 (leading columns) and A1, swept one after the other so each sweep's
-  // gathers of x+ stay in L2; bpart holds A0's row sums
-  Sched A0, A1;
+  // column-blocked phase B (loop_kernel_stream_cb): A split at ncb - 1
+  // columns into ncb blocks (device array cbs of their schedules), swept one
+  // after the other so each sweep's gathers of x+ stay in L2; bpart carries
+  // the leading blocks' row sums.  Indexed at run time: the kernels take
+  // KParams as __grid_constant__, so that is a register-indexed constant-bank
+  // load, not a local copy
+  Sched cbs[kMaxColBlocks];
+  int ncb;
   double* bpart;  // m
   // trace ring (TraceRec): records, and per slot z.x (n), z.y (m) and the
   // columns' partition classes (n); a rank writes its own slices (peers read
@@ -1210,6 +1214,20 @@ struct EpiStore {
   }
 };
 
+// Column-blocked sweeps before the last: out = s on the first, out + s after
+// (a row's sum is ((s_0 + s_1) + s_2) + ..., each block's part in ascending
+// column order; the last sweep adds its own through EpiDual's PART input).
+struct EpiAccum {
+  double* out;
+  int first;
+  using In = NoIn;
+  __device__ __forceinline__ In load(int) const { return {}; }
+  __device__ __forceinline__ void apply(int r, double s, const In&, double (&t)[1]) const {
+    out[r] = first ? s : ldcg(out + r) + s;
+    t[0] = 0.0;
+  }
+};
+
 struct EpiPosNeg {  // primal certificate: max(A^T u), max(-A^T u)
   using In = NoIn;
   __device__ __forceinline__ In load(int) const { return {}; }
@@ -1850,18 +1868,24 @@ __device__ HX_PHASE_INLINE bool phase_dual(const KParams* P, const Roles* R, int
   const double* xsrc = P->xpool + static_cast<size_t>(R->xp_out) * n;
   SpmvHead h1;
   if constexpr (CB) {
-    // sweep 1: the leading column block's row sums into bpart, then a grid
-    // barrier, then sweep 2 over the trailing block with the full epilogue
+    // sweeps 0 .. ncb - 2: the leading column blocks' row sums carried in
+    // bpart, a grid barrier after each; then the last block with the full
+    // epilogue
     double a0[1] = {0.0};
-    EpiStore st0{P->bpart};
-    spmv_rows<1, 0, LM, EX>(P->A0, par, SrcVecT<LM == 1 && HX_GATHER_LAST>{xsrc}, st0, a0, gwarp_id(g),
-                        threadIdx.x & 31, stage, seq, head);
-    spmv_head<LM>(P->A1, gwarp_id(g), threadIdx.x & 31, h1);
-    // abort / watchdog: leave before sweep 2 (its long rows would wait on
-    // pieces that never come)
-    if (!grid_sync(P->bar, *target)) return false;
+    h1 = head;
+    for (int k = 0; k + 1 < P->ncb; ++k) {
+      const Sched Sk = P->cbs[k];
+      EpiAccum st0{P->bpart, k == 0};
+      spmv_rows<1, 0, LM, EX>(Sk, par, SrcVecT<LM == 1 && HX_GATHER_LAST>{xsrc}, st0, a0, gwarp_id(g),
+                              threadIdx.x & 31, stage, seq, h1);
+      const Sched Sn = P->cbs[k + 1];
+      spmv_head<LM>(Sn, gwarp_id(g), threadIdx.x & 31, h1);
+      // abort / watchdog: leave before the next sweep (its long rows would
+      // wait on pieces that never come)
+      if (!grid_sync(P->bar, *target)) return false;
+    }
   }
-  const Sched S = CB ? P->A1 : P->A;
+  const Sched S = CB ? P->cbs[P->ncb - 1] : P->A;
 #ifdef HX_WPROF
   const unsigned long long w0 = clock64();
 #endif
@@ -2871,7 +2895,7 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
       if (writer && threadIdx.x == 0 && budget != 0ull) set_time_up(par, (global_ns() - t_start) > budget ? 1u : 0u);
     }
     mark(0);
-    spmv_head<LM>(CB ? P->A0 : P->A, gwarp_id(g), lane, head);
+    spmv_head<LM>(CB ? P->cbs[0] : P->A, gwarp_id(g), lane, head);
     if (!sync()) return;
     mark(1);
     if (!phase_dual<RK, LM, CB, EX, TR>(P, R, par, stage, ++seq, head, g, &target)) return;
@@ -3247,33 +3271,53 @@ __global__ void row_of_kernel(int m, const int* rp, int* row_of, int* iota) {
 // its ascending columns, then the two halves copied to their CSR arrays (one
 // warp per row).  cnt0 / cnt1 have m + 1 entries, [0] = 0, so an inclusive
 // scan gives the row pointers.
-__global__ void split_count_kernel(int m, const int* ptr, const int* idx, int split, int* cnt0, int* cnt1) {
+// Column blocks of A (phase B of loop_kernel_stream_cb): block k holds the
+// columns [split[k - 1], split[k]) (split[-1] = 0, split[K - 1] = n), rows
+// kept whole and ascending inside each block.
+struct ColSplit {
+  int K;
+  int split[kMaxColBlocks];  // exclusive upper column of each block
+  int* cnt[kMaxColBlocks];   // per row counts at [i + 1] (inclusive-scanned into the block's row pointers)
+  const int* ptr[kMaxColBlocks];
+  int* idx[kMaxColBlocks];
+  double* val[kMaxColBlocks];
+};
+
+__global__ void split_count_kernel(int m, const int* ptr, const int* idx, ColSplit sp) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
     const int lo = ptr[i], hi = ptr[i + 1];
-    int a = lo, b = hi;
-    while (a < b) {
-      const int mid = (a + b) >> 1;
-      if (idx[mid] < split) a = mid + 1;
-      else b = mid;
+    int prev = lo;
+    for (int k = 0; k < sp.K; ++k) {
+      int a = prev, b = hi;
+      if (k + 1 < sp.K) {
+        while (a < b) {
+          const int mid = (a + b) >> 1;
+          if (idx[mid] < sp.split[k]) a = mid + 1;
+          else b = mid;
+        }
+      } else {
+        a = hi;
+      }
+      sp.cnt[k][i + 1] = a - prev;
+      prev = a;
     }
-    cnt0[i + 1] = a - lo;
-    cnt1[i + 1] = hi - a;
   }
 }
 
-__global__ void split_copy_kernel(int m, const int* ptr, const int* idx, const double* val, const int* p0,
-                                  const int* p1, int* i0, double* v0, int* i1, double* v1) {
+__global__ void split_copy_kernel(int m, const int* ptr, const int* idx, const double* val, ColSplit sp) {
   const int lane = threadIdx.x & 31;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < m; i += (gridDim.x * blockDim.x) >> 5) {
-    const int a = ptr[i], len = ptr[i + 1] - a, k = p0[i + 1] - p0[i];
+    const int a = ptr[i], len = ptr[i + 1] - a;
     for (int q = lane; q < len; q += 32) {
-      if (q < k) {
-        i0[p0[i] + q] = idx[a + q];
-        v0[p0[i] + q] = val[a + q];
-      } else {
-        i1[p1[i] + q - k] = idx[a + q];
-        v1[p1[i] + q - k] = val[a + q];
+      const int col = idx[a + q];
+      int k = 0, before = 0;  // block of this entry, entries of the row in earlier blocks
+      while (k + 1 < sp.K && col >= sp.split[k]) {
+        before += sp.ptr[k][i + 1] - sp.ptr[k][i];
+        ++k;
       }
+      const int o = sp.ptr[k][i] + q - before;
+      sp.idx[k][o] = col;
+      sp.val[k][o] = val[a + q];
     }
   }
 }
@@ -3389,11 +3433,11 @@ struct hx_ctx {
   DevSched sa, st;
   // column-blocked phase B (loop_kernel_stream_cb): A's leading / trailing
   // column blocks as CSR with their schedules, and the leading block's row sums
-  int colblock = 0;
-  int* cb_ptr[2] = {nullptr, nullptr};
-  int* cb_idx[2] = {nullptr, nullptr};
-  double* cb_val[2] = {nullptr, nullptr};
-  DevSched sb0, sb1;
+  int colblock = 0;  // column blocks of phase B (0: none)
+  int* cb_ptr[kMaxColBlocks] = {};
+  int* cb_idx[kMaxColBlocks] = {};
+  double* cb_val[kMaxColBlocks] = {};
+  DevSched sb[kMaxColBlocks];
   double* bpart = nullptr;
   double* xpool = nullptr;
   double* ypool = nullptr;
@@ -3563,13 +3607,13 @@ void free_problem(hx_ctx* c) {
   free_sched(c->st);
   free_sched(c->pa);
   free_sched(c->pt);
-  free_sched(c->sb0);
-  free_sched(c->sb1);
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < kMaxColBlocks; ++k) {
+    free_sched(c->sb[k]);
     dfree(c->cb_ptr[k]), dfree(c->cb_idx[k]), dfree(c->cb_val[k]);
     c->cb_ptr[k] = c->cb_idx[k] = nullptr;
     c->cb_val[k] = nullptr;
   }
+
   dfree(c->bpart);
   c->bpart = nullptr;
   dfree(c->ring);
@@ -3674,8 +3718,8 @@ KParams params(hx_ctx* c) {
   P.epochs = c->epochs;
   P.prof = c->prof;
   P.xavg = c->xavg, P.tavg = c->tavg, P.yavg = c->yavg, P.aavg = c->aavg, P.xbar = c->xbar;
-  P.A0 = c->sb0.view;
-  P.A1 = c->sb1.view;
+  for (int k = 0; k < c->colblock; ++k) P.cbs[k] = c->sb[k].view;
+  P.ncb = c->colblock;
   P.bpart = c->bpart;
   if (c->ring) {
     const RingLayout L = ring_layout(c->ring_cap, c->n, c->m);
@@ -3694,10 +3738,12 @@ int launch_loop(hx_ctx* c) {
   void* args[] = {&P};
   HX_CUDA(c, cudaMemcpyAsync(c->ctl, &c->h, sizeof(Ctl), cudaMemcpyHostToDevice, c->stream));
   HX_CUDA(c, cudaMemsetAsync(c->bar, 0, sizeof(GridBar), c->stream));
-  for (DevSched* d : {&c->sa, &c->st, &c->sb0, &c->sb1})  // long-row flags restart with the per-launch sequence
+  for (int k = -2; k < c->colblock; ++k) {  // long-row flags restart with the per-launch sequence
+    const DevSched* d = k == -2 ? &c->sa : k == -1 ? &c->st : &c->sb[k];
     if (d->view.n_long)
       HX_CUDA(c, cudaMemsetAsync(d->flags, 0, 4 * static_cast<size_t>(d->view.n_long) * sizeof(unsigned long long),
                                  c->stream));
+  }
   const void* kernel = c->h.mode == kModeLoop && c->h.scheme != HPLP_SCHEME_RHPDHG
                            ? reinterpret_cast<const void*>(loop_kernel_baseline)
                            : c->ub                     ? reinterpret_cast<const void*>(loop_kernel_box)
@@ -4372,69 +4418,84 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     // Column-blocked phase B (loop_kernel_stream_cb): when x+ is far larger
     // than L2 its random gathers miss (configs[4]: 9.5 GB of DRAM traffic per
     // iteration against 5.0 GB algorithmic, L2 hit rate 38%), so A is split at
-    // the column that halves its nonzeros and phase B sweeps the two blocks
-    // one after the other (a grid barrier between), each sweep gathering from
-    // half of x+.  Auto when 8 n > 64 MB on the stream path; HX_COLBLOCK=0/1
-    // forces.  Row sums become (leading block) + (trailing block), each in
-    // ascending column order.
-    int want = hint && 8.0 * static_cast<double>(n) > 64e6 ? 1 : 0;
-    if (const char* e = std::getenv("HX_COLBLOCK")) want = std::atoi(e) != 0 ? 1 : 0;
+    // the columns that cut its nonzeros into K equal parts and phase B sweeps
+    // the blocks one after the other (a grid barrier between), each sweep
+    // gathering from 1/K of x+.  Auto (K = 2) when 8 n > 64 MB on the stream
+    // path; HX_COLBLOCK=0/1 forces it off / on (K = 2), HX_COLBLOCK=K (2..8)
+    // sets K.  Row sums become ((block 0) + (block 1)) + ..., each block's
+    // part in ascending column order.
+    int want = hint && 8.0 * static_cast<double>(n) > 64e6 ? 2 : 0;
+    if (const char* e = std::getenv("HX_COLBLOCK")) {
+      want = std::atoi(e);
+      want = want == 1 ? 2 : std::min(want, kMaxColBlocks);
+    }
     // the reference order sums each row in one chain: no split at a column
-    if (want && nnz > 0 && !exact) {
+    if (want >= 2 && nnz > 0 && !exact && n >= want) {
+      const int K = want;
       std::vector<int> pt(static_cast<size_t>(n) + 1);
       HX_CUDA(c, cudaMemcpy(pt.data(), c->t_ptr, (n + 1) * sizeof(int), cudaMemcpyDeviceToHost));
-      const int split = static_cast<int>(std::lower_bound(pt.begin(), pt.end(), static_cast<int>(nnz / 2)) - pt.begin());
+      ColSplit sp{};
+      sp.K = K;
+      for (int k = 0; k + 1 < K; ++k)
+        sp.split[k] = static_cast<int>(std::lower_bound(pt.begin(), pt.end(),
+                                                        static_cast<int>(nnz * (k + 1) / K)) - pt.begin());
+      sp.split[K - 1] = static_cast<int>(n);
       // the blocks are cut on the device (the matrix is resident); only their
       // row pointers come back for the host schedules
-      int* cnt[2] = {nullptr, nullptr};
+      int* cnt[kMaxColBlocks] = {};
       unsigned char* scan_tmp = nullptr;
-      DevFree gc0{reinterpret_cast<void**>(&cnt[0])}, gc1{reinterpret_cast<void**>(&cnt[1])},
-          gst{reinterpret_cast<void**>(&scan_tmp)};
-      for (int k = 0; k < 2; ++k) {
+      DevFree gst{reinterpret_cast<void**>(&scan_tmp)};
+      static_assert(kMaxColBlocks == 8, "one guard per block count array");
+      DevFree gcnt[kMaxColBlocks] = {{reinterpret_cast<void**>(&cnt[0])}, {reinterpret_cast<void**>(&cnt[1])},
+                                     {reinterpret_cast<void**>(&cnt[2])}, {reinterpret_cast<void**>(&cnt[3])},
+                                     {reinterpret_cast<void**>(&cnt[4])}, {reinterpret_cast<void**>(&cnt[5])},
+                                     {reinterpret_cast<void**>(&cnt[6])}, {reinterpret_cast<void**>(&cnt[7])}};
+      for (int k = 0; k < K; ++k) {
         HX_CUDA(c, dalloc(&cnt[k], static_cast<size_t>(m) + 1));
         HX_CUDA(c, cudaMemsetAsync(cnt[k], 0, sizeof(int), s));
         HX_CUDA(c, dalloc(&c->cb_ptr[k], static_cast<size_t>(m) + 1));
+        sp.cnt[k] = cnt[k];
       }
-      split_count_kernel<<<nblk, 256, 0, s>>>(static_cast<int>(m), c->a_ptr, c->a_idx, split, cnt[0], cnt[1]);
+      split_count_kernel<<<nblk, 256, 0, s>>>(static_cast<int>(m), c->a_ptr, c->a_idx, sp);
       size_t scan_bytes = 0;
       cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, cnt[0], c->cb_ptr[0], static_cast<int>(m + 1), s);
       HX_CUDA(c, dalloc(&scan_tmp, std::max<size_t>(1, scan_bytes)));
-      for (int k = 0; k < 2; ++k)
+      for (int k = 0; k < K; ++k)
         HX_CUDA(c, cub::DeviceScan::InclusiveSum(scan_tmp, scan_bytes, cnt[k], c->cb_ptr[k], static_cast<int>(m + 1), s));
-      std::vector<int> p0(static_cast<size_t>(m) + 1), p1(static_cast<size_t>(m) + 1);
-      HX_CUDA(c, cudaMemcpyAsync(p0.data(), c->cb_ptr[0], (m + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
-      HX_CUDA(c, cudaMemcpyAsync(p1.data(), c->cb_ptr[1], (m + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+      std::vector<std::vector<int>> ph_k(static_cast<size_t>(K), std::vector<int>(static_cast<size_t>(m) + 1));
+      for (int k = 0; k < K; ++k)
+        HX_CUDA(c, cudaMemcpyAsync(ph_k[k].data(), c->cb_ptr[k], (m + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
       HX_CUDA(c, cudaStreamSynchronize(s));
-      for (int k = 0; k < 2; ++k) {
-        const size_t nz = static_cast<size_t>((k == 0 ? p0 : p1)[m]);
+      for (int k = 0; k < K; ++k) {
+        const size_t nz = static_cast<size_t>(ph_k[k][m]);
         HX_CUDA(c, dalloc(&c->cb_idx[k], nz + kMatrixPad));
         HX_CUDA(c, dalloc(&c->cb_val[k], nz + kMatrixPad));
+        sp.ptr[k] = c->cb_ptr[k];
+        sp.idx[k] = c->cb_idx[k];
+        sp.val[k] = c->cb_val[k];
       }
-      split_copy_kernel<<<nblk, 256, 0, s>>>(static_cast<int>(m), c->a_ptr, c->a_idx, c->a_val, c->cb_ptr[0],
-                                             c->cb_ptr[1], c->cb_idx[0], c->cb_val[0], c->cb_idx[1], c->cb_val[1]);
+      split_copy_kernel<<<nblk, 256, 0, s>>>(static_cast<int>(m), c->a_ptr, c->a_idx, c->a_val, sp);
       HX_CUDA(c, cudaStreamSynchronize(s));
       HX_CUDA(c, cudaGetLastError());
-      c->launches += 4;
+      c->launches += 2 + K;
       tick("cb split");
-      const std::vector<int>* ps[2] = {&p0, &p1};
-      DevSched* ds[2] = {&c->sb0, &c->sb1};
-      // both blocks' schedules are built concurrently on host threads
-      std::future<SchedHost> sb[2];
-      for (int k = 0; k < 2; ++k)
-        sb[k] = std::async(std::launch::async, [pk = ps[k], m, sched_warps] {
+      // the blocks' schedules are built concurrently on host threads
+      std::vector<std::future<SchedHost>> sb(static_cast<size_t>(K));
+      for (int k = 0; k < K; ++k)
+        sb[k] = std::async(std::launch::async, [pk = &ph_k[k], m, sched_warps] {
           double rc, tc;
           sched_costs(false, rc, tc);
           return build_schedule(pk->data(), static_cast<int>(m), sched_warps, 0.0, rc, tc);
         });
-      for (int k = 0; k < 2; ++k) {
-        const int rc = upload_built_sched(c, *ds[k], sb[k].get(), static_cast<int>(m), static_cast<int>(n),
+      for (int k = 0; k < K; ++k) {
+        const int rc = upload_built_sched(c, c->sb[k], sb[k].get(), static_cast<int>(m), static_cast<int>(n),
                                           c->cb_ptr[k], c->cb_idx[k], c->cb_val[k], 0);
         if (rc) return rc;
-        ds[k]->view.stream_hint = hint;
-        ds[k]->view.row_limit = static_cast<int>(m);
+        c->sb[k].view.stream_hint = hint;
+        c->sb[k].view.row_limit = static_cast<int>(m);
       }
       HX_CUDA(c, dalloc(&c->bpart, static_cast<size_t>(std::max<int64_t>(m, 1))));
-      c->colblock = 1;
+      c->colblock = K;
     }
   }
   tick("schedules");
@@ -4532,12 +4593,12 @@ int hx_precondition(hx_ctx* c, int32_t ruiz_iters, double pc_alpha, double* row_
     scale_csr_kernel<<<nb, 256, 0, s>>>(n, c->t_ptr, c->t_idx, c->t_val, dr, dc, 1);
     // every other copy of A's values the loop reads gets the same two roundings
     // (v * d_row) * d_col, so all copies stay bit-identical to a_val
-    for (int k = 0; k < 2 && c->colblock; ++k)  // column blocks of phase B (loop_kernel_stream_cb)
+    for (int k = 0; k < c->colblock; ++k)  // column blocks of phase B (loop_kernel_stream_cb)
       scale_csr_kernel<<<nb, 256, 0, s>>>(m, c->cb_ptr[k], c->cb_idx[k], c->cb_val[k], dr, dc, 0);
     scale_vec_kernel<<<nb, 256, 0, s>>>(m, c->b, dr);
     scale_vec_kernel<<<nb, 256, 0, s>>>(n, c->c, dc);
     if (c->ub) div_vec_kernel<<<nb, 256, 0, s>>>(n, c->ub, dc);  // x = C x': x' <= u / C
-    c->launches += (c->ub ? 7 : 6) + (c->colblock ? 2 : 0);
+    c->launches += (c->ub ? 7 : 6) + c->colblock;
     HX_CUDA(c, cudaGetLastError());
     return HPLP_OK;
   };

@@ -96,6 +96,7 @@ constexpr int kStreamRowMax = 64;          // rows up to this length are summed 
 // configs[2] 45.4k vs 44.2k -- 64 kept.
 constexpr int kStreamRowsMax = HX_ROWS;    // rows per stream task (64: two per lane)
 constexpr int kMaxRanks = 8;               // ranks of a row-partitioned team (one node)
+constexpr int kMaxColBlocks = 8;           // column blocks of phase B (loop_kernel_stream_cb)
 
 // Warp tasks, int4 {row_begin, row_end | kind << 30, p_begin, p_end}; every
 // task covers at most kChunk nonzeros, loaded kLoadsPerLane per lane into

@@ -28,6 +28,7 @@ the same 4.5e-11 (profiles/r02_full_parity.txt).
 """
 from __future__ import annotations
 
+import os
 import queue
 import threading
 
@@ -95,10 +96,22 @@ def lockstep(std, iters: int, order: str, nranks: int = 0, **kw):
     with hplp.sum_order(order):
         args = (std.m, std.n, std.row_ptr, std.col_idx, std.val, std.b, std.c)
         sol = hplp.Solver.team(*args, nranks=nranks) if nranks else hplp.Solver(*args)
+    # one GPU: no device trace ring -- a traced iteration pauses the launch,
+    # so the records come from the production loop kernel (loop_kernel_stream,
+    # loop_kernel_stream_cb) rather than the trace-ring one.  A team keeps the
+    # ring (a rank cannot classify the host-side way; loop_kernel_team_trace)
+    saved = os.environ.get("HPLP_TRACE_RING")
+    if not nranks:
+        os.environ["HPLP_TRACE_RING"] = "0"
     try:
         assert sol.hx.sum_order() == (hplp.SUM_REFERENCE if order == "reference" else hplp.SUM_FAST)
         gpu = sol.solve(iteration_limit=iters, tolerance=1e-12, trace=True, sink=gpu_sink, **kw)
+        gpu["loop_kernel"] = sol.hx.loop_kernel()
     finally:
+        if saved is None:
+            os.environ.pop("HPLP_TRACE_RING", None)
+        else:
+            os.environ["HPLP_TRACE_RING"] = saved
         sol.close()
         while th.is_alive():  # never leave the reference blocked on a full queue
             try:
@@ -135,7 +148,8 @@ def test_full_size_first_100_iterates(gpu_required, cid):
     g, std = reference_instance(cid)
     cpu, gpu, errs = lockstep(std, 100, "fast")
     worst = _check_first_100(cpu, gpu, errs)
-    print(f"configs[{cid}] {std.m}x{std.n} nnz {std.nnz}: worst of 100 iterates {worst:.3e}")
+    assert gpu["loop_kernel"] in ("hx::loop_kernel", "hx::loop_kernel_stream")
+    print(f"configs[{cid}] {std.m}x{std.n} nnz {std.nnz} ({gpu['loop_kernel']}): worst of 100 iterates {worst:.3e}")
 
 
 @pytest.mark.parametrize("nranks", [3, 8])
@@ -158,7 +172,8 @@ def test_full_size_first_100_iterates_configs4(gpu_required):
     g, std = reference_instance(4)
     cpu, gpu, errs = lockstep(std, 100, "fast")
     worst = _check_first_100(cpu, gpu, errs)
-    print(f"configs[4] {std.m}x{std.n} nnz {std.nnz}: worst of 100 iterates {worst:.3e}; "
+    assert gpu["loop_kernel"] == "hx::loop_kernel_stream_cb"
+    print(f"configs[4] {std.m}x{std.n} nnz {std.nnz} ({gpu['loop_kernel']}): worst of 100 iterates {worst:.3e}; "
           f"iterations 1/10/50/100: {errs[1]:.3e} {errs[10]:.3e} {errs[50]:.3e} {errs[99]:.3e}")
 
 

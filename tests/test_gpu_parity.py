@@ -307,14 +307,16 @@ def test_ragged_structure_team_parity(gpu_required):
     _trace_cmp(gpu["trace"], cpu["trace"])
 
 
-@pytest.mark.parametrize("name", ["cfg1_small", "zipf_small", "ragged"])
-def test_column_blocked_phase_b_parity(gpu_required, name, monkeypatch):
-    """loop_kernel_stream_cb (phase B swept in two column blocks, the path
-    configs[4] takes; forced here with HX_COLBLOCK=1 on the stream kernel):
+@pytest.mark.parametrize("name,blocks", [("cfg1_small", 2), ("zipf_small", 2), ("ragged", 2), ("cfg1_small", 3),
+                                         ("zipf_small", 4), ("ragged", 8)])
+def test_column_blocked_phase_b_parity(gpu_required, name, blocks, monkeypatch):
+    """loop_kernel_stream_cb (phase B swept in K column blocks, the path
+    configs[4] takes; forced here with HX_COLBLOCK=K on the stream kernel):
     first 100 iterates within 1e-10 of the oracle, same restarts and SpMV
     counts, then a solve to 1e-4 with the same status and objective."""
-    monkeypatch.setenv("HX_COLBLOCK", "1")
+    monkeypatch.setenv("HX_COLBLOCK", str(blocks))
     monkeypatch.setenv("HPLP_L2_STREAM", "1")
+    monkeypatch.setenv("HPLP_TRACE_RING", "0")  # traced iterations from the blocked kernel itself
     args = _ragged_lp() if name == "ragged" else csr_args(std(name)[1])
     cpu = CpuLp("port", *args).solve(iteration_limit=100, tolerance=1e-12, trace=True)
     sol = hplp.Solver(*args)
@@ -342,8 +344,9 @@ def test_column_blocked_preconditioned_parity(gpu_required, monkeypatch):
     unscaled values, so A x+ used the original matrix while A^T y used the
     scaled one).  The device loop on the preconditioned instance must match
     the oracle run on the instance downloaded from the device."""
-    monkeypatch.setenv("HX_COLBLOCK", "1")
+    monkeypatch.setenv("HX_COLBLOCK", "4")
     monkeypatch.setenv("HPLP_L2_STREAM", "1")
+    monkeypatch.setenv("HPLP_TRACE_RING", "0")  # traced iterations from the blocked kernel itself
     s = std("cfg1_small")[1]
     sol = hplp.Solver(*csr_args(s))
     assert sol.hx.loop_kernel() == "hx::loop_kernel_stream_cb"
@@ -379,10 +382,11 @@ def test_reference_sum_order_spmv_bit_exact(gpu_required, name):
     hx.close()
 
 
-def test_reference_sum_order_iterates(gpu_required):
+def test_reference_sum_order_iterates(gpu_required, monkeypatch):
     """The loop in the reference order (loop_kernel_exact) on a Zipf instance
     with rows of several thousand nonzeros: 100 iterates against the
     reference itself, identical restarts and SpMV counts."""
+    monkeypatch.setenv("HPLP_TRACE_RING", "0")  # traced iterations from loop_kernel_exact itself
     g, s = std("zipf_small")
     with hplp.sum_order("reference"):
         sol = hplp.Solver(*csr_args(s))
