@@ -97,7 +97,7 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, doubl
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return ucost[a] > ucost[b]; });
   using Load = std::pair<double, int>;  // (load, warp)
   std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
-  std::vector<std::vector<int>> per_warp(static_cast<std::size_t>(warps));
+  std::vector<int> uwarp(nu);  // the warp each unit is dealt to
   std::vector<double> wcost(static_cast<std::size_t>(warps), 0.0);
   for (int w = 0; w < warps; ++w) wcost[w] = w % kWarps == 0 ? lead : 0.0;
   int deal = 1;
@@ -119,7 +119,7 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, doubl
       int w = c * kWarps;
       for (int i = 1; i < kWarps; ++i)
         if (wcost[c * kWarps + i] < wcost[w]) w = c * kWarps + i;
-      for (std::size_t t = unit[u]; t < unit[u + 1]; ++t) per_warp[w].push_back(static_cast<int>(t));
+      uwarp[u] = w;
       wcost[w] += ucost[u];
       ccost[c] = load + ucost[u];
       heap.push({ccost[c], c});
@@ -129,19 +129,26 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, doubl
     for (int u : order) {
       auto [load, w] = heap.top();
       heap.pop();
-      for (std::size_t t = unit[u]; t < unit[u + 1]; ++t) per_warp[w].push_back(static_cast<int>(t));
+      uwarp[u] = w;
       wcost[w] = load + ucost[u];
       heap.push({wcost[w], w});
     }
   }
+  // warp w's k-th task (in dealing order) goes to position k * warps + w
+  std::vector<std::size_t> wpos(static_cast<std::size_t>(warps), 0);
+  for (std::size_t u = 0; u < nu; ++u) wpos[uwarp[u]] += unit[u + 1] - unit[u];
   std::size_t rounds = 0;
-  for (const auto& v : per_warp) rounds = std::max(rounds, v.size());
+  for (std::size_t v : wpos) rounds = std::max(rounds, v);
+  std::fill(wpos.begin(), wpos.end(), 0);
   std::vector<int4> tasks(rounds * warps, int4{0, 0, 0, 0}), meta(rounds * warps, int4{0, 0, 0, 0});
-  for (int w = 0; w < warps; ++w)
-    for (std::size_t k = 0; k < per_warp[w].size(); ++k) {
-      tasks[k * warps + w] = s.tasks[per_warp[w][k]];
-      meta[k * warps + w] = s.meta[per_warp[w][k]];
+  for (int u : order) {
+    const int w = uwarp[u];
+    for (std::size_t t = unit[u]; t < unit[u + 1]; ++t) {
+      const std::size_t k = wpos[w]++;
+      tasks[k * warps + w] = s.tasks[t];
+      meta[k * warps + w] = s.meta[t];
     }
+  }
   while (!tasks.empty() && tasks.back().x == 0 && tasks.back().y == 0 && tasks.back().w == 0) {
     tasks.pop_back();
     meta.pop_back();
