@@ -95,6 +95,17 @@ int32_t hx_sum_order(hx_ctx* ctx);
 int hx_stored_nonzeros(hx_ctx* ctx, int64_t* nnz_a, int64_t* nnz_t);
 /* Same with device-resident inputs (no host copies; used by re-uploads). */
 int hx_dims(hx_ctx* ctx, int64_t* m, int64_t* n, int64_t* nnz);
+/* Host-only diagnostic (no GPU needed): the warp schedule hx_upload_csr
+ * builds for a CSR row-pointer array of `rows` rows on `ctas` CTAs of the
+ * loop kernel's width (lead: warp 0's starting load, as phase A uses).
+ * Writes up to `capacity` tasks as 4 int32 each {row_begin, row_end | kind <<
+ * 30, nz_begin, nz_end} in the kernels' layout (warp w's k-th task at k * W +
+ * w, W = ctas * warps per CTA; empty slots are zeros) and the number of slots
+ * to *n_tasks; stats (may be NULL) receives {W, max warp cost, mean warp
+ * cost, max CTA cost, mean CTA cost} in the schedule's cost units.
+ * HPLP_EINVAL on a capacity below the slot count (with *n_tasks set). */
+int hx_schedule_info(const int32_t* row_ptr, int32_t rows, int32_t ctas, double lead, int32_t* tasks,
+                     int64_t capacity, int64_t* n_tasks, double* stats);
 
 /* Diagonal preconditioning of the uploaded problem in place (no reference
  * counterpart; SPEC.md:101,259 name Ruiz / Pock-Chambolle as extension

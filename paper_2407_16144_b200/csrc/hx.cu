@@ -4057,6 +4057,35 @@ int hx_stored_nonzeros(hx_ctx* c, int64_t* nnz_a, int64_t* nnz_t) {
   return HPLP_OK;
 }
 
+int hx_schedule_info(const int32_t* row_ptr, int32_t rows, int32_t ctas, double lead, int32_t* tasks,
+                     int64_t capacity, int64_t* n_tasks, double* stats) {
+  if (!row_ptr || rows < 0 || ctas < 1 || !n_tasks || capacity < 0)
+    return set_err(nullptr, HPLP_EINVAL, "hx_schedule_info: bad arguments");
+  for (int32_t i = 0; i < rows; ++i)
+    if (row_ptr[i + 1] < row_ptr[i]) return set_err(nullptr, HPLP_EINVAL, "hx_schedule_info: row_ptr is not monotone");
+  const int warps = ctas * kWarps;
+  double rc, tc;
+  sched_costs(true, rc, tc);
+  const SchedHost h = build_schedule(row_ptr, rows, warps, lead, rc, tc, false);
+  *n_tasks = static_cast<int64_t>(h.tasks.size());
+  if (stats) {
+    std::vector<double> cta(static_cast<size_t>(ctas), 0.0);
+    for (size_t k = 0; k < h.tasks.size(); ++k) {
+      const int4 t = h.tasks[k];
+      if (t.x == 0 && t.y == 0 && t.w == 0) continue;
+      cta[(k % warps) / kWarps] += (t.w - t.z) + rc * ((t.y & kRowMask) - t.x) + tc;
+    }
+    double mx = 0.0, sum = 0.0;
+    for (double v : cta) mx = std::max(mx, v), sum += v;
+    stats[0] = warps, stats[1] = h.max_warp_cost, stats[2] = h.mean_warp_cost;
+    stats[3] = mx, stats[4] = sum / ctas;
+  }
+  if (static_cast<int64_t>(h.tasks.size()) > capacity)
+    return set_err(nullptr, HPLP_EINVAL, "hx_schedule_info: capacity below the task slot count");
+  if (tasks) std::memcpy(tasks, h.tasks.data(), h.tasks.size() * sizeof(int4));
+  return HPLP_OK;
+}
+
 int hx_dims(hx_ctx* c, int64_t* m, int64_t* n, int64_t* nnz) {
   if (m) *m = c->m;
   if (n) *n = c->n;

@@ -118,6 +118,8 @@ def lib() -> C.CDLL:
     sig("hx_precondition", C.c_int, V, I32, D, PD, PD)
     sig("hx_set_sum_order", C.c_int, V, I32)
     sig("hx_stored_nonzeros", C.c_int, V, C.POINTER(C.c_int64), C.POINTER(C.c_int64))
+    sig("hx_schedule_info", C.c_int, C.POINTER(C.c_int32), C.c_int32, C.c_int32, C.c_double, C.POINTER(C.c_int32),
+        C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_double))
     sig("hx_trace_reduced_costs", C.c_int, V, PD)
     sig("hx_sum_order", I32, V)
     sig("hx_set_default_sum_order", C.c_int, I32)
@@ -405,6 +407,26 @@ def solve(m, n, row_ptr, col_idx, val, b, c, config=None, init=None, trace=False
                                 C.byref(cfg), C.byref(io), C.byref(res)))
     del keep
     return _result(res, x, y, pc, dc, eps, recs)
+
+
+def schedule_info(row_ptr, ctas: int = 148, lead: float = 0.0):
+    """The loop kernels' warp schedule for a CSR row-pointer array (host
+    only, hx_schedule_info): (tasks int32[slots, 4] in the kernels' layout,
+    stats dict W / max_warp / mean_warp / max_cta / mean_cta)."""
+    rp = np.ascontiguousarray(row_ptr, np.int32)
+    rows = len(rp) - 1
+    n = C.c_int64()
+    st = (C.c_double * 5)()
+    L = lib()
+    p = rp.ctypes.data_as(C.POINTER(C.c_int32))
+    rc = L.hx_schedule_info(p, rows, ctas, lead, None, 0, C.byref(n), st)  # sizes first
+    if rc and not (rc == abi.HPLP_EINVAL and n.value > 0):
+        raise ValueError(L.hx_last_error(None).decode())
+    tasks = np.zeros((n.value, 4), np.int32)
+    if n.value and L.hx_schedule_info(p, rows, ctas, lead, tasks.ctypes.data_as(C.POINTER(C.c_int32)), n.value,
+                                      C.byref(n), st):
+        raise ValueError(L.hx_last_error(None).decode())
+    return tasks, dict(W=int(st[0]), max_warp=st[1], mean_warp=st[2], max_cta=st[3], mean_cta=st[4])
 
 
 def solve_general(general, config=None, device=0, **kw):

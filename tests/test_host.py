@@ -194,3 +194,71 @@ def test_power_start_bit_identical_to_sequential_draw(seed):
         assert lo.orc_power_start(n, C.c_uint64(seed), want.ctypes.data_as(C.POINTER(C.c_double))) == 0
         got = hplp.power_start(n, seed)
         assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (n, seed)
+
+
+def _sched_matrix(seed, rows, lo, hi, long_every=0, long_len=0):
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(lo, hi + 1, size=rows)
+    if long_every:
+        lens[::long_every] = long_len
+    return np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+
+
+@pytest.mark.parametrize("rows,lo,hi,long_every,long_len", [(20000, 1, 40, 0, 0), (5000, 0, 64, 997, 5000),
+                                                            (30000, 1, 2, 0, 0), (0, 1, 1, 0, 0)])
+def test_schedule_covers_every_nonzero_once(rows, lo, hi, long_every, long_len):
+    """hx_schedule_info (host only): the warp schedule the loop kernels walk
+    covers every row and nonzero exactly once -- stream tasks of <= 64 rows /
+    <= 256 nonzeros, longer rows cut into pieces of <= 256 -- and the same
+    input always gives the same table (what makes the device reductions
+    reproducible)."""
+    rp = _sched_matrix(1, rows, lo, hi, long_every, long_len)
+    tasks, st = hplp.schedule_info(rp, ctas=148)
+    tasks2, _ = hplp.schedule_info(rp, ctas=148)
+    assert np.array_equal(tasks, tasks2)
+    live = tasks[~((tasks[:, 0] == 0) & (tasks[:, 1] == 0) & (tasks[:, 3] == 0))]
+    kind = (live[:, 1].astype(np.int64) & 0xFFFFFFFF) >> 30
+    r1 = live[:, 1] & ((1 << 30) - 1)
+    nz = np.zeros(int(rp[-1]) + 1, np.int64)
+    for (r0, _, p0, p1), e, k in zip(live, r1, kind):
+        assert 0 < p1 - p0 <= 256 or (p1 == p0 and k == 0)
+        if k == 0:  # stream task: whole rows, their nonzeros exactly
+            assert e - r0 <= 64 and rp[r0] == p0 and rp[e] == p1
+        else:  # a piece of one long row
+            assert e == r0 + 1 and rp[r0] <= p0 < p1 <= rp[r0 + 1]
+        nz[p0:p1] += 1
+    assert np.all(nz[: int(rp[-1])] == 1)
+    covered = np.zeros(max(rows, 1), np.int64)
+    for (r0, _, p0, p1), e, k in zip(live, r1, kind):
+        if k == 0:
+            covered[r0:e] += 1
+        elif p0 == rp[r0]:
+            covered[r0] += 1
+    if rows:
+        assert np.all(covered[:rows] == 1)
+
+
+def test_schedule_balances_ctas_and_leads_warp0():
+    """Units are dealt to the least-loaded CTA first (its warps share one L1
+    pipe), so CTA sums end within ~1% of each other even where warp sums
+    differ by 20%; warp 0's lead (it runs the controller while the others
+    start phase A) moves work to the CTA's other warps."""
+    rp = _sched_matrix(7, 230000, 1, 20)
+    tasks, st = hplp.schedule_info(rp, ctas=148)
+    assert st["max_cta"] <= 1.02 * st["mean_cta"], st
+    W = st["W"]
+    live = ~((tasks[:, 0] == 0) & (tasks[:, 1] == 0) & (tasks[:, 3] == 0))
+    warp = np.arange(len(tasks)) % W
+    w0 = np.count_nonzero(live & (warp % 16 == 0))
+    tasks_l, st_l = hplp.schedule_info(rp, ctas=148, lead=3000.0)
+    live_l = ~((tasks_l[:, 0] == 0) & (tasks_l[:, 1] == 0) & (tasks_l[:, 3] == 0))
+    warp_l = np.arange(len(tasks_l)) % W
+    assert np.count_nonzero(live_l & (warp_l % 16 == 0)) < w0
+    assert st_l["max_cta"] <= 1.02 * st_l["mean_cta"], st_l
+
+
+def test_schedule_info_rejects_bad_input():
+    with pytest.raises(ValueError, match="monotone"):
+        hplp.schedule_info(np.array([0, 5, 3], np.int32))
+    with pytest.raises(ValueError, match="bad arguments"):
+        hplp.schedule_info(np.array([0, 1], np.int32), ctas=0)
