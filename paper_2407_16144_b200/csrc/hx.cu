@@ -1695,6 +1695,31 @@ __device__ bool eval_dual(const Ctl& C, int c, hplp_cert_meta_t& rep) {
   return valid;
 }
 
+// Whether candidate c can still validate once its product is known: the
+// parts of eval_primal / eval_dual that do not need the SpMV, operand for
+// operand (a y-candidate's margin test; an x-candidate's sign and margin
+// tests).  False means the evaluation fails whatever the product is.
+__device__ bool cert_may_pass(const Ctl& C, int c) {
+  const double tol = C.cert_tol;
+  if (c & 1) {  // y-candidate: primal certificate, margin s (b . u) > 0 and >= tol ||b||
+    for (int si = 0; si < 2; ++si) {
+      const double margin = (si == 0 ? 1.0 : -1.0) * C.cdot[c];
+      if (margin > 0.0 && margin >= tol * C.b_norm) return true;
+    }
+    return false;
+  }
+  double inf_u = C.cinf[c];  // x-candidate: dual certificate
+  if (inf_u < 0.0) inf_u = 0.0;
+  const double nonneg_threshold = tol * dmax(1.0, inf_u);
+  const double margin_threshold = -tol * dmax(1.0, C.c_norm);
+  for (int si = 0; si < 2; ++si) {
+    const double sign = dmax(0.0, si == 0 ? C.cmax_negu[c] : C.cmax_u[c]);
+    const double margin = (si == 0 ? 1.0 : -1.0) * C.cdot[c];
+    if (sign <= nonneg_threshold && margin <= margin_threshold) return true;
+  }
+  return false;
+}
+
 __device__ void finish_iteration_baseline(Ctl& C, hplp_epoch_t* epochs, bool writer, double res, bool time_up);
 
 // CertificateScan::check semantics, src/solver.cpp:108-135 (+ :300-317).
@@ -2987,23 +3012,42 @@ __device__ __forceinline__ void loop_body(const KParams* P, const Geo& g) {
           const double* rg = region_ptr(P, kRegC2, g.nrec);
           block_totals(12, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, ((0x577u >> q) & 1u) != 0}; }, tot, g);
         }
+        __shared__ int s_skip;  // candidates whose validation SpMV is skipped (bit c)
         if (threadIdx.x == 0) {
           C.cinf[0] = tot[0], C.cmax_u[0] = tot[1], C.cmax_negu[0] = tot[2], C.cdot[0] = tot[3];
           C.cinf[2] = tot[4], C.cmax_u[2] = tot[5], C.cmax_negu[2] = tot[6], C.cdot[2] = tot[7];
           C.cinf[1] = tot[8], C.cdot[1] = tot[9];
           C.cinf[3] = tot[10], C.cdot[3] = tot[11];
+          // a candidate whose margin / sign tests already fail cannot pass
+          // whatever its product: no SpMV for it (cert_may_pass)
+          int skip = 0;
+          for (int c = 0; c < 4; ++c)
+            if (C.r.cand_on[c] && !cert_may_pass(C, c)) {
+              C.r.cand_on[c] = 0;
+              skip |= 1 << c;
+            }
+          s_skip = skip;
         }
         __syncthreads();
-        cert_products<RK, LM, EX>(P, R, stage, ++seq, g);
-        if (!sync()) return;
-        {
+        const bool products = R->cand_on[0] || R->cand_on[1] || R->cand_on[2] || R->cand_on[3];
+        if (products) {
+          cert_products<RK, LM, EX>(P, R, stage, ++seq, g);
+          if (!sync()) return;
           const double* rg = region_ptr(P, kRegC3, g.nrec);
           block_totals(6, [&](int q) { return QSrc{rg, q, nullptr, 0, 0, true}; }, tot, g);
         }
         if (threadIdx.x == 0) {
-          C.cmax_at[1] = tot[0], C.cmax_negat[1] = tot[1];
-          C.cmax_at[3] = tot[2], C.cmax_negat[3] = tot[3];
-          C.cmax_abs_au[0] = tot[4], C.cmax_abs_au[2] = tot[5];
+          if (products) {
+            C.cmax_at[1] = tot[0], C.cmax_negat[1] = tot[1];
+            C.cmax_at[3] = tot[2], C.cmax_negat[3] = tot[3];
+            C.cmax_abs_au[0] = tot[4], C.cmax_abs_au[2] = tot[5];
+          }
+          // a skipped candidate's residual reads +inf: it fails as it would have
+          const int sk = s_skip;
+          if (sk & 2) C.cmax_at[1] = C.cmax_negat[1] = INFINITY;
+          if (sk & 8) C.cmax_at[3] = C.cmax_negat[3] = INFINITY;
+          if (sk & 1) C.cmax_abs_au[0] = INFINITY;
+          if (sk & 4) C.cmax_abs_au[2] = INFINITY;
           scan_logic(C, P->epochs, writer, s_time_up != 0);
         }
         __syncthreads();
