@@ -3298,6 +3298,29 @@ __global__ void validate_kernel(int m, int n, const long long* rp, const int* ci
   }
 }
 
+// The bank-staggered copy of a CSR matrix (build_schedule's stagger), one
+// warp per row: row r's entries at pptr[r], then its pad slots up to
+// pptr[r + 1] with value 0 and the column of the row's last entry (the lane
+// before a pad gathers the same line, so a pad costs no extra wavefront);
+// an empty row's pads take the next row's first column.
+__global__ void pad_copy_kernel(int rows, const int* ptr, const int* idx, const double* val, const int* pptr,
+                                int* pidx, double* pval) {
+  const int lane = threadIdx.x & 31;
+  const int nnz = ptr[rows];
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += (gridDim.x * blockDim.x) >> 5) {
+    const int a = ptr[r], e = ptr[r + 1], pa = pptr[r], pe = pptr[r + 1];
+    for (int k = lane; k < e - a; k += 32) {
+      pidx[pa + k] = idx[a + k];
+      pval[pa + k] = val[a + k];
+    }
+    const int fill = e > a ? idx[e - 1] : e < nnz ? idx[e] : 0;
+    for (int k = pa + (e - a) + lane; k < pe; k += 32) {
+      pidx[k] = fill;
+      pval[k] = 0.0;
+    }
+  }
+}
+
 __global__ void narrow_ptr_kernel(int len, const long long* src, int* dst) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x)
     dst[i] = static_cast<int>(src[i]);
@@ -3447,6 +3470,11 @@ struct DevSched {
   int* owned_ptr = nullptr;
   int* owned_idx = nullptr;
   unsigned long long* flags = nullptr;  // 4 * n_long
+  // bank-staggered copy of the matrix the tasks index (SchedHost::pptr);
+  // null: the view reads the CSR arrays themselves
+  int* pptr = nullptr;
+  int* pidx = nullptr;
+  double* pval = nullptr;
   Sched view;
   double max_cost = 0, mean_cost = 0;
 };
@@ -3638,6 +3666,7 @@ struct DevFree {
 void free_sched(DevSched& s) {
   dfree(s.tasks), dfree(s.meta), dfree(s.owned_ptr), dfree(s.owned_idx), dfree(s.flags);
   dfree(s.part), dfree(s.cnt), dfree(s.terms);
+  dfree(s.pptr), dfree(s.pidx), dfree(s.pval);
   s = DevSched{};
 }
 
@@ -3698,6 +3727,22 @@ int upload_built_sched(hx_ctx* ctx, DevSched& d, SchedHost h, int rows, int cols
   HX_CUDA(ctx, cp(d.meta, h.meta.data(), h.meta.size() * sizeof(int4)));
   HX_CUDA(ctx, cudaMemsetAsync(d.cnt, 0, std::max<size_t>(1, 4 * static_cast<size_t>(h.n_long)) * sizeof(unsigned),
                                ctx->stream));
+  if (!h.pptr.empty()) {
+    // the staggered copy: row r's entries at pptr[r], its trailing pads zero
+    const int64_t pn = h.padded_nnz;
+    HX_CUDA(ctx, dalloc(&d.pptr, h.pptr.size()));
+    HX_CUDA(ctx, dalloc(&d.pidx, pn + kMatrixPad));
+    HX_CUDA(ctx, dalloc(&d.pval, pn + kMatrixPad));
+    HX_CUDA(ctx, cp(d.pptr, h.pptr.data(), h.pptr.size() * sizeof(int)));
+    HX_CUDA(ctx, cudaMemsetAsync(d.pidx, 0, (pn + kMatrixPad) * sizeof(int), ctx->stream));
+    HX_CUDA(ctx, cudaMemsetAsync(d.pval, 0, (pn + kMatrixPad) * sizeof(double), ctx->stream));
+    pad_copy_kernel<<<4 * ctx->sm_count, 256, 0, ctx->stream>>>(rows, dptr, didx, dval, d.pptr, d.pidx, d.pval);
+    HX_CUDA(ctx, cudaGetLastError());
+    ctx->launches += 1;
+    dptr = d.pptr;
+    didx = d.pidx;
+    dval = d.pval;
+  }
   HX_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // host vectors go out of scope
   Sched& v = d.view;
   v.rows = rows;
@@ -4362,12 +4407,17 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   }
   const int sched_warps = c->grid * kWarps;
   const bool exact = c->sum_order == 1;
+  // bank-staggered stream tasks (build_schedule): at most kStaggerA / kStaggerT
+  // pad slots before a row of >= kStaggerLmin nonzeros; HX_STAGGER="a,t,lmin"
+  // overrides (0,0 turns it off)
+  int stagger_a = kStaggerA, stagger_t = kStaggerT, stagger_lmin = kStaggerLmin;
+  if (const char* e = std::getenv("HX_STAGGER")) std::sscanf(e, "%d,%d,%d", &stagger_a, &stagger_t, &stagger_lmin);
   std::future<SchedHost> sched_a;
   if (monotone)  // else the device check below reports it
-    sched_a = std::async(std::launch::async, [&ph, m, sched_warps, exact] {
+    sched_a = std::async(std::launch::async, [&ph, m, sched_warps, exact, stagger_a, stagger_lmin] {
       double rc, tc;
       sched_costs(false, rc, tc);
-      return build_schedule(ph.data(), static_cast<int>(m), sched_warps, 0.0, rc, tc, exact);
+      return build_schedule(ph.data(), static_cast<int>(m), sched_warps, 0.0, rc, tc, exact, stagger_a, stagger_lmin);
     });
   cudaStream_t s = c->stream;
   const int nblk = 4 * c->sm_count;
@@ -4460,10 +4510,10 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     double lead = kLead;
     if (const char* e = std::getenv("HX_LEAD")) lead = std::atof(e);
     // A^T's schedule is built on a host thread while A's uploads
-    auto sched_t = std::async(std::launch::async, [&pt, n, sched_warps, lead, exact] {
+    auto sched_t = std::async(std::launch::async, [&pt, n, sched_warps, lead, exact, stagger_t, stagger_lmin] {
       double rc, tc;
       sched_costs(true, rc, tc);
-      return build_schedule(pt.data(), static_cast<int>(n), sched_warps, lead, rc, tc, exact);
+      return build_schedule(pt.data(), static_cast<int>(n), sched_warps, lead, rc, tc, exact, stagger_t, stagger_lmin);
     });
     int rc = upload_built_sched(c, c->sa, sched_a.get(), static_cast<int>(m), static_cast<int>(n), c->a_ptr,
                                 c->a_idx, c->a_val, 0);
@@ -4668,6 +4718,10 @@ int hx_precondition(hx_ctx* c, int32_t ruiz_iters, double pc_alpha, double* row_
     // (v * d_row) * d_col, so all copies stay bit-identical to a_val
     for (int k = 0; k < c->colblock; ++k)  // column blocks of phase B (loop_kernel_stream_cb)
       scale_csr_kernel<<<nb, 256, 0, s>>>(m, c->cb_ptr[k], c->cb_idx[k], c->cb_val[k], dr, dc, 0);
+    // the bank-staggered copies the schedules index (their pads stay 0)
+    if (c->sa.pval) scale_csr_kernel<<<nb, 256, 0, s>>>(m, c->sa.pptr, c->sa.pidx, c->sa.pval, dr, dc, 0);
+    if (c->st.pval) scale_csr_kernel<<<nb, 256, 0, s>>>(n, c->st.pptr, c->st.pidx, c->st.pval, dr, dc, 1);
+    c->launches += (c->sa.pval ? 1 : 0) + (c->st.pval ? 1 : 0);
     scale_vec_kernel<<<nb, 256, 0, s>>>(m, c->b, dr);
     scale_vec_kernel<<<nb, 256, 0, s>>>(n, c->c, dc);
     if (c->ub) div_vec_kernel<<<nb, 256, 0, s>>>(n, c->ub, dc);  // x = C x': x' <= u / C

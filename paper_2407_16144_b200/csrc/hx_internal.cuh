@@ -40,6 +40,12 @@ constexpr int kEpochCap = 1 << 16;         // device epoch ring (host drains per
 // is flat from 32 to 200.
 constexpr double kRowCost = 5.0;           // epilogue cost of one row
 constexpr double kTaskCost = 64.0;         // fixed latency cost of one warp task
+// bank-staggered stream tasks (build_schedule stagger): pad slots allowed in
+// front of a row of A (phase B) / of A^T (phase A), and the shortest row
+// that gets any
+constexpr int kStaggerA = 15;
+constexpr int kStaggerT = 1;
+constexpr int kStaggerLmin = 4;
 // Warp 0 of every CTA runs the controller while warps 1..15 start the
 // speculative phase A: its schedule share starts with this lead (cost
 // units).  tools/lead_sweep.sh with CTA-first dealing, configs[1]: 600 / 1200
@@ -191,13 +197,24 @@ struct SchedHost {
   int n_long = 0;
   int n_slots = 0;
   double max_warp_cost = 0.0, mean_warp_cost = 0.0;
+  // bank-staggered layout (stagger > 0): padded row pointers [rows + 1]
+  // into a copy of idx / val with zero-valued pad slots; every task's
+  // positions refer to it (empty: the tasks index the CSR itself)
+  std::vector<int> pptr;
+  int64_t padded_nnz = 0;
 };
 
 // lead: initial load (cost units) of warp 0 of every CTA, which runs the
 // controller before its own tasks in the speculative phase A.
 // exact: reference summation order -- every long row becomes ONE run of
 // pieces (one warp carries the sequential sum through all of them).
+// stagger > 0: bank-staggered stream tasks -- before a row of >= stagger_lmin
+// nonzeros that is not a task's first, up to `stagger` zero-valued pad slots
+// move its first product to a shared-memory bank pair (slot mod 16) no other
+// row of its half-warp (16 lanes) starts on, so the lane-per-row sums read
+// the product buffer without bank conflicts.  Pads trail the previous row
+// (they add +0.0 to its sum: the same bits, since no row sum is -0.0).
 SchedHost build_schedule(const int* ptr_host, int rows, int warps, double lead = 0.0, double row_cost = kRowCost,
-                         double task_cost = kTaskCost, bool exact = false);
+                         double task_cost = kTaskCost, bool exact = false, int stagger = 0, int stagger_lmin = 4);
 
 }  // namespace hx

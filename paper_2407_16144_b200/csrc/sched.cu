@@ -19,10 +19,22 @@
 
 namespace hx {
 
-SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, double row_cost, double task_cost,
-                         bool exact) {
+SchedHost build_schedule(const int* ptr_in, int rows, int warps, double lead, double row_cost, double task_cost,
+                         bool exact, int stagger, int stagger_lmin) {
   SchedHost s;
-  const int64_t nnz = ptr[rows] - ptr[0];  // ptr may point into a larger matrix (a rank's block)
+  // Bank-staggered layout: positions in a padded copy of the matrix.  The
+  // padded row pointers are filled as rows are packed (pads only ever go in
+  // front of a non-first row of a stream task), and every task below refers
+  // to them.  ptr_in[0] must be 0 (a rank's block is never staggered).
+  stagger = ptr_in[0] == 0 ? std::max(0, std::min(stagger, 15)) : 0;
+  std::vector<int> padded;
+  if (stagger) padded.assign(static_cast<std::size_t>(rows) + 1, 0);
+  int64_t off = 0;  // pad slots inserted so far
+  const int* ptr = stagger ? padded.data() : ptr_in;
+  auto place = [&](int row) {  // the padded start of `row` with off pads before it
+    if (stagger) padded[row] = static_cast<int>(ptr_in[row] + off);
+  };
+  const int64_t nnz = ptr_in[rows] - ptr_in[0];  // ptr may point into a larger matrix (a rank's block)
   const double total = static_cast<double>(nnz) + row_cost * rows;
 
   std::vector<double> cost;
@@ -39,7 +51,8 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, doubl
   if (const char* e = std::getenv("HX_TASK_NNZ")) task_nnz = std::max(8, std::min<int>(kTaskNnz, std::atoi(e)));
   int r = 0;
   while (r < rows) {
-    const int64_t len = ptr[r + 1] - ptr[r];
+    const int64_t len = ptr_in[r + 1] - ptr_in[r];
+    place(r);
     if (len > kStreamRowMax) {
       const int np = static_cast<int>((len + kTaskNnz - 1) / kTaskNnz);
       // exact order: lane 0 adds every product in sequence, about as long
@@ -67,19 +80,45 @@ SchedHost build_schedule(const int* ptr, int rows, int warps, double lead, doubl
       continue;
     }
     const int r0 = r;
-    int64_t used = 0;
+    int64_t used = 0;  // slots (nonzeros + pads)
+    int64_t nz = 0;
+    int starts[4][16];  // per half-warp group: how many rows start on each bank pair
+    if (stagger) std::fill(&starts[0][0], &starts[0][0] + 64, 0);
     while (r < rows && r - r0 < kStreamRowsMax) {
-      const int64_t l = ptr[r + 1] - ptr[r];
-      if (l > kStreamRowMax || used + l > task_nnz) break;
+      const int64_t l = ptr_in[r + 1] - ptr_in[r];
+      if (l > kStreamRowMax) break;
+      int pad = 0;
+      const int g = (r - r0) >> 4;  // lanes 0-15, 16-31 (first rows), 32-47, 48-63 (second rows)
+      if (stagger && r > r0 && l >= stagger_lmin) {
+        // the fewest pads reaching the least-used bank pair within reach
+        int best = 1 << 30;
+        for (int p = 0; p <= stagger; ++p) {
+          const int c = starts[g][(used + p) & 15];
+          if (c < best) best = c, pad = p;
+          if (c == 0) break;
+        }
+      }
+      if (used + pad + l > task_nnz) break;
+      off += pad;
+      used += pad;
+      place(r);
+      if (stagger) ++starts[g][used & 15];
       used += l;
+      nz += l;
       ++r;
     }
+    place(r < rows ? r : rows);
     unit.push_back(s.tasks.size());
-    push(r0, r, kTaskStream, static_cast<int>(ptr[r0]), static_cast<int>(ptr[r]), int4{0, 0, 0, 0},
-         static_cast<double>(used) + row_cost * (r - r0));
+    push(r0, r, kTaskStream, static_cast<int>(ptr[r0]), static_cast<int>(stagger ? ptr_in[r] + off : ptr[r]),
+         int4{0, 0, 0, 0}, static_cast<double>(stagger ? used : nz) + row_cost * (r - r0));
   }
   const std::size_t nt = s.tasks.size();
   unit.push_back(nt);
+  if (stagger) {
+    padded[rows] = static_cast<int>(ptr_in[rows] + off);
+    s.padded_nnz = ptr_in[rows] + off;
+    s.pptr.swap(padded);
+  }
 
   // Longest-processing-time dealing: units heaviest first, each to the
   // currently least-loaded CTA, then its least-loaded warp (ties to the lower

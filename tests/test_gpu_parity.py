@@ -454,3 +454,41 @@ def test_trace_ring_minimum_capacity_and_disabled(gpu_required, monkeypatch):
         assert sum(len(np.setxor1d(u, v)) for u, v in zip(a["partition"], c["partition"])) <= 1
         assert a["kkt"] == b["kkt"] == c["kkt"]
     assert np.array_equal(base["x"], small["x"]) and np.array_equal(base["x"], off["x"])
+
+
+@pytest.mark.parametrize("name", ["cfg1_small", "zipf_small", "transport_small", "ragged"])
+def test_bank_staggered_layout_bit_identical(gpu_required, name, monkeypatch):
+    """Bank-staggered stream tasks (build_schedule stagger, HX_STAGGER): the
+    pad slots only append +0.0 to a row's sum and no row sum is -0.0, so both
+    SpMVs are bit-identical to the unpadded layout -- with the most padding
+    allowed (15 slots before every row) and with the default.  The solve's
+    norms and KKT sums follow the schedule's row -> lane map, which the pads
+    move, so iterates agree to rounding (1e-12), with identical statuses,
+    iteration counts and restarts -- on a preconditioned instance too (the
+    padded copies are rescaled with the CSR)."""
+    args = _ragged_lp() if name == "ragged" else csr_args(std(name)[1])
+    rng = np.random.default_rng(5)
+    x, y = rng.normal(size=args[1]), rng.normal(size=args[0])
+    runs = {}
+    for layout in ("0,0,4", "15,1,4", "15,15,1"):
+        monkeypatch.setenv("HX_STAGGER", layout)
+        hx = hplp.HX(device=0)
+        hx.upload(*args)
+        prods = (hx.spmv(x), hx.spmv_transpose(y))
+        hx.close()
+        out = []
+        for pc in (False, True):
+            sol = hplp.Solver(*args)
+            if pc:
+                sol.hx.precondition(2, 0.5)
+            r = sol.solve(iteration_limit=400, tolerance=1e-12)
+            out.append((r["x"], r["y"], r["status"], r["iterations"], [e[:2] for e in r["epochs"]]))
+            sol.close()
+        runs[layout] = (prods, out)
+    base_p, base = runs["0,0,4"]
+    for layout in ("15,1,4", "15,15,1"):
+        p, o = runs[layout]
+        assert np.array_equal(p[0], base_p[0]) and np.array_equal(p[1], base_p[1]), layout
+        for a, b in zip(o, base):
+            assert rel_inf(a[0], b[0]) <= 1e-12 and rel_inf(a[1], b[1]) <= 1e-12, layout
+            assert a[2:] == b[2:], layout
