@@ -18,7 +18,7 @@ its = int(sys.argv[2]) if len(sys.argv) > 2 else 5000
 s = hplp.to_standard_form(gen.generate(cid))
 rp, ci, v, b, c = (torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
                    for a in (s.row_ptr, s.col_idx, s.val, s.b, s.c))
-for rep in range(2):
+for rep in range(int(os.environ.get("E2E_REPS", "2"))):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     r = hplp.solve(s.m, s.n, rp, ci, v, b, c, iteration_limit=its, tolerance=1e-4)
