@@ -70,8 +70,11 @@ void fill_result(const hplp_gpu::SolveResult& r, hplp_io_t* io, hplp_result_t* r
   put_cert(r.primal_certificate, &res->primal_cert, io ? io->primal_cert : nullptr);
   put_cert(r.dual_certificate, &res->dual_cert, io ? io->dual_cert : nullptr);
   if (!io) return;
-  if (io->x) std::memcpy(io->x, r.final_iterate.x.data(), r.final_iterate.x.size() * sizeof(double));
-  if (io->y) std::memcpy(io->y, r.final_iterate.y.data(), r.final_iterate.y.size() * sizeof(double));
+  // (an empty final_iterate was read straight into io->x / io->y: SolverConfig::out_x)
+  if (io->x && !r.final_iterate.x.empty())
+    std::memcpy(io->x, r.final_iterate.x.data(), r.final_iterate.x.size() * sizeof(double));
+  if (io->y && !r.final_iterate.y.empty())
+    std::memcpy(io->y, r.final_iterate.y.data(), r.final_iterate.y.size() * sizeof(double));
   if (io->epochs)
     for (std::size_t e = 0; e < r.epochs.size() && static_cast<int64_t>(e) < io->epochs_capacity; ++e) {
       io->epochs[e].epoch = r.epochs[e].epoch;
@@ -235,6 +238,7 @@ int hplp_solver_solve(void* solver, const hplp_config_t* cfg, hplp_io_t* io, hpl
   return guarded([&] {
     auto* s = static_cast<hplp_gpu::Solver*>(solver);
     hplp_gpu::SolverConfig c = config_with_io(cfg, io, s->rows(), s->cols());
+    if (io && io->x && io->y) c.out_x = io->x, c.out_y = io->y;  // no host staging copy of the result
     fill_result(s->solve(c), io, result);
   });
 }

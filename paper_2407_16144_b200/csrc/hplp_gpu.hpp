@@ -238,6 +238,11 @@ struct SolverConfig {
   // Iteration scheme (HPLP_SCHEME_*): 0 = solve(); 1-3 = solve_baseline's
   // modes (set by solve_baseline, or directly through the C ABI).
   int scheme = 0;
+  // Extension (C ABI): when both are set, the final iterate is read from the
+  // device straight into these caller buffers (n and m doubles) and
+  // SolveResult::final_iterate stays empty -- no host staging copy.
+  double* out_x = nullptr;
+  double* out_y = nullptr;
 };
 
 // inc/solver.hpp:82-116

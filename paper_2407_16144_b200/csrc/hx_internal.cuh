@@ -46,6 +46,10 @@ constexpr double kTaskCost = 64.0;         // fixed latency cost of one warp tas
 constexpr int kStaggerA = 15;
 constexpr int kStaggerT = 1;
 constexpr int kStaggerLmin = 4;
+// build_schedule packs the rows of a matrix with >= kPackMinRows rows in
+// kPackSegments fixed segments on host threads
+constexpr int kPackSegments = 8;
+constexpr int kPackMinRows = 1 << 16;
 // Warp 0 of every CTA runs the controller while warps 1..15 start the
 // speculative phase A: its schedule share starts with this lead (cost
 // units).  tools/lead_sweep.sh with CTA-first dealing, configs[1]: 600 / 1200

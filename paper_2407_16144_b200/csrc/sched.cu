@@ -14,82 +14,89 @@
 #include <cstdlib>
 #include <functional>
 #include <queue>
+#include <thread>
 
 #include "hx_internal.cuh"
 
 namespace hx {
 
-SchedHost build_schedule(const int* ptr_in, int rows, int warps, double lead, double row_cost, double task_cost,
-                         bool exact, int stagger, int stagger_lmin) {
-  SchedHost s;
-  // Bank-staggered layout: positions in a padded copy of the matrix.  The
-  // padded row pointers are filled as rows are packed (pads only ever go in
-  // front of a non-first row of a stream task), and every task below refers
-  // to them.  ptr_in[0] must be 0 (a rank's block is never staggered).
-  stagger = ptr_in[0] == 0 ? std::max(0, std::min(stagger, 15)) : 0;
-  std::vector<int> padded;
-  if (stagger) padded.assign(static_cast<std::size_t>(rows) + 1, 0);
-  int64_t off = 0;  // pad slots inserted so far
-  const int* ptr = stagger ? padded.data() : ptr_in;
-  auto place = [&](int row) {  // the padded start of `row` with off pads before it
-    if (stagger) padded[row] = static_cast<int>(ptr_in[row] + off);
-  };
-  const int64_t nnz = ptr_in[rows] - ptr_in[0];  // ptr may point into a larger matrix (a rank's block)
-  const double total = static_cast<double>(nnz) + row_cost * rows;
+namespace {
 
+// One segment of rows packed into tasks (build_schedule): positions, slots and
+// long-row counters are local to the segment; build_schedule shifts them.
+struct Packed {
+  std::vector<int4> tasks, meta;
   std::vector<double> cost;
   std::vector<std::size_t> unit;  // first task of each dealing unit (a stream task or a run of pieces)
-  auto push = [&](int r0, int r1, int kind, int p0, int p1, int4 meta, double c) {
-    s.tasks.push_back(int4{r0, task_y(r1, kind), p0, p1});
-    s.meta.push_back(meta);
-    cost.push_back(c + task_cost);
+  int n_slots = 0, n_long = 0;
+  int64_t off = 0;  // pad slots inserted in the segment
+};
+
+struct PackArgs {
+  const int* ptr_in;
+  int stagger, stagger_lmin;
+  int64_t task_nnz;
+  bool exact;
+  double row_cost, task_cost, run_budget;
+  int* padded;  // padded row starts (segment-local pad offsets), or null
+};
+
+void pack_rows(const PackArgs& a, int ra, int rb, Packed& o) {
+  const int* ptr_in = a.ptr_in;
+  const int stagger = a.stagger;
+  int64_t& off = o.off;
+  auto pstart = [&](int row) -> int64_t { return ptr_in[row] + off; };  // row's start in the padded copy
+  auto place = [&](int row) {
+    if (stagger && row < rb) a.padded[row] = static_cast<int>(pstart(row));
   };
-  // a run of pieces is dealt to one warp as a unit: at most 1/kRunFrac of the
-  // mean warp cost, so the dealing stays balanced
-  const double run_budget = std::max(1.0, total / warps / kRunFrac);
-  int64_t task_nnz = kTaskNnz;
-  if (const char* e = std::getenv("HX_TASK_NNZ")) task_nnz = std::max(8, std::min<int>(kTaskNnz, std::atoi(e)));
-  int r = 0;
-  while (r < rows) {
+  auto push = [&](int r0, int r1, int kind, int64_t p0, int64_t p1, int4 meta, double c) {
+    o.tasks.push_back(int4{r0, task_y(r1, kind), static_cast<int>(p0), static_cast<int>(p1)});
+    o.meta.push_back(meta);
+    o.cost.push_back(c + a.task_cost);
+  };
+  int r = ra;
+  while (r < rb) {
     const int64_t len = ptr_in[r + 1] - ptr_in[r];
     place(r);
     if (len > kStreamRowMax) {
       const int np = static_cast<int>((len + kTaskNnz - 1) / kTaskNnz);
       // exact order: lane 0 adds every product in sequence, about as long
       // again as the gathers -- the piece costs twice as much
-      const double pc = static_cast<double>(len) / np * (exact ? 2.0 : 1.0) + task_cost;
-      const int per = std::max(1, std::min(kRunMax, static_cast<int>(run_budget / pc)));
-      const int nr = exact ? 1 : (np + per - 1) / per;
+      const double pc = static_cast<double>(len) / np * (a.exact ? 2.0 : 1.0) + a.task_cost;
+      const int per = std::max(1, std::min(kRunMax, static_cast<int>(a.run_budget / pc)));
+      const int nr = a.exact ? 1 : (np + per - 1) / per;
+      const int64_t base = stagger ? pstart(r) : ptr_in[r];
       for (int k = 0; k < nr; ++k) {
-        unit.push_back(s.tasks.size());
+        o.unit.push_back(o.tasks.size());
         const int q0 = static_cast<int>(static_cast<int64_t>(np) * k / nr);
         const int q1 = static_cast<int>(static_cast<int64_t>(np) * (k + 1) / nr);
         for (int q = q0; q < q1; ++q) {
-          const int p0 = static_cast<int>(ptr[r] + len * q / np);
-          const int p1 = static_cast<int>(ptr[r] + len * (q + 1) / np);
+          const int64_t p0 = base + len * q / np;
+          const int64_t p1 = base + len * (q + 1) / np;
           push(r, r + 1, q + 1 == q1 ? kTaskPiece : kTaskPieceRun, p0, p1,
-               int4{s.n_slots + k, nr, nr > 1 ? s.n_long : -1, k},
-               static_cast<double>(p1 - p0) * (exact ? 2.0 : 1.0) + (q + 1 == np ? row_cost : 0.0));
+               int4{o.n_slots + k, nr, nr > 1 ? o.n_long : -1, k},
+               static_cast<double>(p1 - p0) * (a.exact ? 2.0 : 1.0) + (q + 1 == np ? a.row_cost : 0.0));
         }
       }
       if (nr > 1) {
-        s.n_slots += nr;
-        s.n_long += 1;
+        o.n_slots += nr;
+        o.n_long += 1;
       }
       ++r;
       continue;
     }
     const int r0 = r;
+    const int64_t p0 = stagger ? pstart(r0) : ptr_in[r0];
     int64_t used = 0;  // slots (nonzeros + pads)
     int64_t nz = 0;
     int starts[4][16];  // per half-warp group: how many rows start on each bank pair
     if (stagger) std::fill(&starts[0][0], &starts[0][0] + 64, 0);
-    while (r < rows && r - r0 < kStreamRowsMax) {
+    while (r < rb && r - r0 < kStreamRowsMax) {
       const int64_t l = ptr_in[r + 1] - ptr_in[r];
       if (l > kStreamRowMax) break;
       int pad = 0;
       const int g = (r - r0) >> 4;  // lanes 0-15, 16-31 (first rows), 32-47, 48-63 (second rows)
-      if (stagger && r > r0 && l >= stagger_lmin) {
+      if (stagger && r > r0 && l >= a.stagger_lmin) {
         // the fewest pads reaching the least-used bank pair within reach
         int best = 1 << 30;
         for (int p = 0; p <= stagger; ++p) {
@@ -98,7 +105,7 @@ SchedHost build_schedule(const int* ptr_in, int rows, int warps, double lead, do
           if (c == 0) break;
         }
       }
-      if (used + pad + l > task_nnz) break;
+      if (used + pad + l > a.task_nnz) break;
       off += pad;
       used += pad;
       place(r);
@@ -107,10 +114,79 @@ SchedHost build_schedule(const int* ptr_in, int rows, int warps, double lead, do
       nz += l;
       ++r;
     }
-    place(r < rows ? r : rows);
-    unit.push_back(s.tasks.size());
-    push(r0, r, kTaskStream, static_cast<int>(ptr[r0]), static_cast<int>(stagger ? ptr_in[r] + off : ptr[r]),
-         int4{0, 0, 0, 0}, static_cast<double>(stagger ? used : nz) + row_cost * (r - r0));
+    place(r);
+    o.unit.push_back(o.tasks.size());
+    push(r0, r, kTaskStream, p0, stagger ? pstart(r) : ptr_in[r], int4{0, 0, 0, 0},
+         static_cast<double>(stagger ? used : nz) + a.row_cost * (r - r0));
+  }
+}
+
+}  // namespace
+
+SchedHost build_schedule(const int* ptr_in, int rows, int warps, double lead, double row_cost, double task_cost,
+                         bool exact, int stagger, int stagger_lmin) {
+  SchedHost s;
+  // Bank-staggered layout: positions in a padded copy of the matrix; pads only
+  // ever go in front of a non-first row of a stream task, and every task
+  // refers to the padded positions.  ptr_in[0] must be 0 (a rank's block is
+  // never staggered).
+  stagger = ptr_in[0] == 0 ? std::max(0, std::min(stagger, 15)) : 0;
+  std::vector<int> padded;
+  if (stagger) padded.assign(static_cast<std::size_t>(rows) + 1, 0);
+  const int64_t nnz = ptr_in[rows] - ptr_in[0];  // ptr may point into a larger matrix (a rank's block)
+  const double total = static_cast<double>(nnz) + row_cost * rows;
+  int64_t task_nnz = kTaskNnz;
+  if (const char* e = std::getenv("HX_TASK_NNZ")) task_nnz = std::max(8, std::min<int>(kTaskNnz, std::atoi(e)));
+  // a run of pieces is dealt to one warp as a unit: at most 1/kRunFrac of the
+  // mean warp cost, so the dealing stays balanced
+  const PackArgs pa{ptr_in, stagger, stagger_lmin, task_nnz, exact, row_cost, task_cost,
+                    std::max(1.0, total / warps / kRunFrac), stagger ? padded.data() : nullptr};
+  // Packing runs on kPackSegments host threads for large matrices: segment k
+  // starts at the first row at or past nonzero k * nnz / K (a fixed split, so
+  // the schedule does not depend on the host); a segment boundary also ends a
+  // stream task.
+  const int K = rows >= kPackMinRows ? kPackSegments : 1;
+  std::vector<int> seg(static_cast<std::size_t>(K) + 1, rows);
+  seg[0] = 0;
+  for (int k = 1; k < K; ++k) {
+    const int64_t target = ptr_in[0] + nnz * k / K;
+    seg[k] = std::max(seg[k - 1], static_cast<int>(std::lower_bound(ptr_in, ptr_in + rows + 1, target) - ptr_in));
+    seg[k] = std::min(seg[k], rows);
+  }
+  std::vector<Packed> part(static_cast<std::size_t>(K));
+  {
+    std::vector<std::thread> pool;
+    for (int k = 1; k < K; ++k) pool.emplace_back([&, k] { pack_rows(pa, seg[k], seg[k + 1], part[k]); });
+    pack_rows(pa, seg[0], seg[1], part[0]);
+    for (auto& t : pool) t.join();
+  }
+  // concatenate: shift positions by the pads of earlier segments, long-row
+  // slots / counters by theirs, unit starts by their task counts
+  std::vector<double> cost;
+  std::vector<std::size_t> unit;
+  int64_t off = 0;
+  for (int k = 0; k < K; ++k) {
+    Packed& p = part[k];
+    const std::size_t tb = s.tasks.size();
+    for (std::size_t t = 0; t < p.tasks.size(); ++t) {
+      int4 tk = p.tasks[t];
+      int4 mt = p.meta[t];
+      tk.z = static_cast<int>(tk.z + off);
+      tk.w = static_cast<int>(tk.w + off);
+      if (task_kind(tk.y) != kTaskStream) {
+        mt.x += s.n_slots;
+        if (mt.z >= 0) mt.z += s.n_long;
+      }
+      s.tasks.push_back(tk);
+      s.meta.push_back(mt);
+    }
+    cost.insert(cost.end(), p.cost.begin(), p.cost.end());
+    for (std::size_t u : p.unit) unit.push_back(u + tb);
+    if (stagger && off)
+      for (int r = seg[k]; r < seg[k + 1]; ++r) padded[r] = static_cast<int>(padded[r] + off);
+    s.n_slots += p.n_slots;
+    s.n_long += p.n_long;
+    off += p.off;
   }
   const std::size_t nt = s.tasks.size();
   unit.push_back(nt);

@@ -546,6 +546,7 @@ SolveResult Solver::solve(const SolverConfig& config) {
   if (config.scheme != HPLP_SCHEME_RHPDHG) throw std::invalid_argument("box form: rHPDHG only");
   SolverConfig cfg = config;
   cfg.infeasibility_check_period = 0;  // no certificates in the box form
+  cfg.out_x = cfg.out_y = nullptr;     // the result is mapped back to the standard form below
   if (cfg.initial_iterate) {  // standard-form dimensions: the leading parts
     Iterate z = *cfg.initial_iterate;
     if (static_cast<int64_t>(z.x.size()) == B.n_std && static_cast<int64_t>(z.y.size()) == B.m_std) {
@@ -619,7 +620,9 @@ SolveResult Solver::solve_core(const SolverConfig& config) {
   };
   // make_setup (:67-78)
   if (!start_.valid() || start_seed_ != config.seed) use_power_start(config.seed, draw_power_start_async(n_, config.seed));
-  const PowerResult pi = power_iteration(ctx, m_, n_, nnz_, kPowerTol, kPowerMaxIters, *start_.get());
+  const PowerStart& pstart = *start_.get();
+  stage("power start");
+  const PowerResult pi = power_iteration(ctx, m_, n_, nnz_, kPowerTol, kPowerMaxIters, pstart);
   stage("power iteration");
   const double sigma_used = pi.sigma * (1.0 + kPowerTol);
   long n_spmv = 2 * static_cast<long>(pi.iterations);
@@ -745,26 +748,35 @@ SolveResult Solver::solve_core(const SolverConfig& config) {
   SolveStatus status = p.status >= 0 ? static_cast<SolveStatus>(p.status) : SolveStatus::kTimeLimit;
   out.status = status;
   stage("loop");
-  out.final_iterate.x.resize(static_cast<std::size_t>(n_));
-  out.final_iterate.y.resize(static_cast<std::size_t>(m_));
+  // the final iterate: straight into the caller's buffers when given
+  const bool direct = config.out_x && config.out_y;
+  if (!direct) {
+    out.final_iterate.x.resize(static_cast<std::size_t>(n_));
+    out.final_iterate.y.resize(static_cast<std::size_t>(m_));
+  }
+  double* fx = direct ? config.out_x : out.final_iterate.x.data();
+  double* fy = direct ? config.out_y : out.final_iterate.y.data();
   long extra_spmv = 0;
   if (status == SolveStatus::kIterationLimit || status == SolveStatus::kTimeLimit) {
     // (:242-254) best iterate if any KKT value was finite, else z with fresh products
     if (p.best_valid) {
-      check(ctx, hx_get_iterate(ctx, HX_ITERATE_BEST, out.final_iterate.x.data(), out.final_iterate.y.data()));
+      check(ctx, hx_get_iterate(ctx, HX_ITERATE_BEST, fx, fy));
       out.final_kkt = kkt_of(p.best_err);
     } else {
-      check(ctx, hx_get_iterate(ctx, HX_ITERATE_CURRENT, out.final_iterate.x.data(), out.final_iterate.y.data()));
+      check(ctx, hx_get_iterate(ctx, HX_ITERATE_CURRENT, fx, fy));
       hplp_kkt_t k;
       check(ctx, hx_kkt_current(ctx, &k));
       out.final_kkt = kkt_of(k);
       extra_spmv = 2;
     }
   } else {
-    check(ctx, hx_get_iterate(ctx, HX_ITERATE_LAST, out.final_iterate.x.data(), out.final_iterate.y.data()));
+    check(ctx, hx_get_iterate(ctx, HX_ITERATE_LAST, fx, fy));
     out.final_kkt = kkt_of(p.final_kkt);
   }
-  unscale(out.final_iterate.x, out.final_iterate.y);
+  if (scaled_) {  // x = C x', y = R y'
+    for (int64_t j = 0; j < n_; ++j) fx[j] *= col_scale_[static_cast<std::size_t>(j)];
+    for (int64_t i = 0; i < m_; ++i) fy[i] *= row_scale_[static_cast<std::size_t>(i)];
+  }
   auto take_cert = [&](int kind, const hplp_cert_meta_t& meta, std::optional<Certificate>& dst, int64_t len) {
     if (!meta.present) return;
     Certificate c;
