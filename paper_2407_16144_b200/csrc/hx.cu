@@ -786,6 +786,42 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
         if (q < qe) s0 += st->prod[q];
         return s0 + s1;
       };
+#elif HX_RSUM == 4
+      // HX_RSUM 1's order (two interleaved partial sums), software-pipelined:
+      // the next four products are loaded before the current four are added,
+      // so the adds never hold back the next loads
+      auto row_sum = [&](int qa, int qe) {
+        if (exact) {
+          double s = 0.0;
+          for (int q = qa; q < qe; ++q) s += st->prod[q];
+          return s;
+        }
+        double s0 = 0.0, s1 = 0.0;
+        int q = qa;
+        if (q + 4 <= qe) {
+          double a0 = st->prod[q], a1 = st->prod[q + 1], a2 = st->prod[q + 2], a3 = st->prod[q + 3];
+          for (q += 4; q + 4 <= qe; q += 4) {
+            const double b0 = st->prod[q], b1 = st->prod[q + 1], b2 = st->prod[q + 2], b3 = st->prod[q + 3];
+            s0 += a0;
+            s1 += a1;
+            s0 += a2;
+            s1 += a3;
+            a0 = b0, a1 = b1, a2 = b2, a3 = b3;
+          }
+          s0 += a0;
+          s1 += a1;
+          s0 += a2;
+          s1 += a3;
+        }
+        if (q + 2 <= qe) {
+          const double a0 = st->prod[q], a1 = st->prod[q + 1];
+          s0 += a0;
+          s1 += a1;
+          q += 2;
+        }
+        if (q < qe) s0 += st->prod[q];
+        return s0 + s1;
+      };
 #else
       // ascending-order sums (the reference's), loads issued 4 ahead
       auto row_sum = [&](int qa, int qe) {
@@ -815,15 +851,41 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
         }
       } else
 #endif
-      if (has_row) {
-        double tm[Q];
-        epi.apply(r0 + lane, row_sum(ra - p0, rb - p0), in, tm);
-        acc_add<Q, MaxMask>(acc, tm);
-      }
-      if (has_row2) {
-        double tm[Q];
-        epi.apply(r0 + lane + 32, row_sum(ra2 - p0, rb2 - p0), in2, tm);
-        acc_add<Q, MaxMask>(acc, tm);
+#if HX_RSHORT
+      // both of a lane's rows of <= 4 nonzeros (slack columns, bound rows):
+      // all eight products loaded in one round, summed in HX_RSUM 1's order
+      // (s0 = 0 + a0 + a2, s1 = 0 + a1 + a3; a missing product adds +0.0,
+      // which leaves the bits alone: s0, s1 start at +0.0)
+      if (!exact && rb - ra <= 4 && rb2 - ra2 <= 4) {
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          v[k] = k < rb - ra ? st->prod[ra - p0 + k] : 0.0;
+          v[4 + k] = k < rb2 - ra2 ? st->prod[ra2 - p0 + k] : 0.0;
+        }
+        if (has_row) {
+          double tm[Q];
+          epi.apply(r0 + lane, ((0.0 + v[0]) + v[2]) + ((0.0 + v[1]) + v[3]), in, tm);
+          acc_add<Q, MaxMask>(acc, tm);
+        }
+        if (has_row2) {
+          double tm[Q];
+          epi.apply(r0 + lane + 32, ((0.0 + v[4]) + v[6]) + ((0.0 + v[5]) + v[7]), in2, tm);
+          acc_add<Q, MaxMask>(acc, tm);
+        }
+      } else
+#endif
+      {
+        if (has_row) {
+          double tm[Q];
+          epi.apply(r0 + lane, row_sum(ra - p0, rb - p0), in, tm);
+          acc_add<Q, MaxMask>(acc, tm);
+        }
+        if (has_row2) {
+          double tm[Q];
+          epi.apply(r0 + lane + 32, row_sum(ra2 - p0, rb2 - p0), in2, tm);
+          acc_add<Q, MaxMask>(acc, tm);
+        }
       }
       __syncwarp();
     } else if (exact) {

@@ -64,9 +64,13 @@ constexpr double kLead = 3000.0;
 // positions) added at the end, 2 four, 3 two with loads 8 ahead.  Measured on
 // configs[1] (tools/quick_rate.py): 26.81k / 27.86k / 27.47k / 26.97k it/s.
 // Reading 1's products as 16-byte pairs (LDS.128, same sums): 27.23k vs
-// 27.76k (8 B of spills), not kept.
+// 27.76k (8 B of spills), not kept.  4: 1's order, software-pipelined (the
+// next four products loaded before the current four are added; bit-identical
+// sums): 29.77k vs 29.65k on configs[1], configs[2] flat -- kept.
+// HX_RSHORT=1 (a lane's two rows of <= 4 nonzeros loaded in one round):
+// configs[1] 29.68k vs 29.77k, configs[2] 49.9k vs 50.7k, not kept.
 #ifndef HX_RSUM
-#define HX_RSUM 1
+#define HX_RSUM 4
 #endif
 // Pieces of long rows: 1 pairwise tree over each lane's products, 0 one
 // sequential chain (then a warp tree either way).
@@ -85,6 +89,9 @@ constexpr double kLead = 3000.0;
 // 27.89k vs 27.79k it/s, configs[2] 44.4k vs 44.2k), 0 an acquire load per poll.
 #ifndef HX_BAR_RELAXED
 #define HX_BAR_RELAXED 1
+#endif
+#ifndef HX_RSHORT
+#define HX_RSHORT 0
 #endif
 #ifndef HX_RSPLIT
 #define HX_RSPLIT 0
