@@ -131,6 +131,9 @@ SchedHost build_schedule(const int* ptr_in, int rows, int warps, double lead, do
   // refers to the padded positions.  ptr_in[0] must be 0 (a rank's block is
   // never staggered).
   stagger = ptr_in[0] == 0 ? std::max(0, std::min(stagger, 15)) : 0;
+  // padded positions stay int32: at most `stagger` pads per row
+  if (static_cast<int64_t>(ptr_in[rows]) + static_cast<int64_t>(stagger) * rows + kMatrixPad >= (int64_t{1} << 31) - 1)
+    stagger = 0;
   std::vector<int> padded;
   if (stagger) padded.assign(static_cast<std::size_t>(rows) + 1, 0);
   const int64_t nnz = ptr_in[rows] - ptr_in[0];  // ptr may point into a larger matrix (a rank's block)
