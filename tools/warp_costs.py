@@ -12,6 +12,8 @@ import sys
 from pathlib import Path
 
 os.environ["HX_PROFILE"] = "1"
+# task positions must index the CSR arrays below (no bank-staggered copy)
+os.environ.setdefault("HX_STAGGER", "0,0,4")
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import numpy as np  # noqa: E402
 
