@@ -4474,6 +4474,10 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   // overrides (0,0 turns it off)
   int stagger_a = kStaggerA, stagger_t = kStaggerT, stagger_lmin = kStaggerLmin;
   if (const char* e = std::getenv("HX_STAGGER")) std::sscanf(e, "%d,%d,%d", &stagger_a, &stagger_t, &stagger_lmin);
+  // the staggered copies cost another 12 bytes per nonzero per matrix: above
+  // kStaggerMaxNnz the plain layout keeps the footprint of the largest
+  // one-GPU problems
+  if (nnz > kStaggerMaxNnz) stagger_a = stagger_t = 0;
   std::future<SchedHost> sched_a;
   if (monotone)  // else the device check below reports it
     sched_a = std::async(std::launch::async, [&ph, m, sched_warps, exact, stagger_a, stagger_lmin] {

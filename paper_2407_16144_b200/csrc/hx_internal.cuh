@@ -46,6 +46,7 @@ constexpr double kTaskCost = 64.0;         // fixed latency cost of one warp tas
 constexpr int kStaggerA = 15;
 constexpr int kStaggerT = 1;
 constexpr int kStaggerLmin = 4;
+constexpr int64_t kStaggerMaxNnz = int64_t{1} << 29;  // larger matrices keep the plain layout
 // build_schedule packs the rows of a matrix with >= kPackMinRows rows in
 // kPackSegments fixed segments on host threads
 constexpr int kPackSegments = 8;
