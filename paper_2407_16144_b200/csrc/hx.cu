@@ -676,7 +676,7 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
     typename Epi::In in{}, in2{};
     if (has_row) {
       ra = __ldg(S.ptr + r0 + lane);
-      rb = __ldg(S.ptr + r0 + lane + 1);
+      rb = min(__ldg(S.ptr + r0 + lane + 1), tk.w);  // a staggered copy's alignment gap ends a task
       HX_CHECK(ra >= p0 && rb >= ra && rb - p0 <= kChunk, "stream row in task", ra - p0, rb - p0);
       in = epi.load(r0 + lane);
     }
@@ -691,7 +691,7 @@ __device__ __forceinline__ void spmv_rows(const Sched& S, int set, const Src& sr
 #endif
     if (has_row2) {
       ra2 = __ldg(S.ptr + r0 + lane + 32);
-      rb2 = __ldg(S.ptr + r0 + lane + 33);
+      rb2 = min(__ldg(S.ptr + r0 + lane + 33), tk.w);
       HX_CHECK(ra2 >= p0 && rb2 >= ra2 && rb2 - p0 <= kChunk, "stream row 2 in task", ra2 - p0, rb2 - p0);
       in2 = epi.load(r0 + lane + 32);
     }
@@ -4478,12 +4478,15 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
   // kStaggerMaxNnz the plain layout keeps the footprint of the largest
   // one-GPU problems
   if (nnz > kStaggerMaxNnz) stagger_a = stagger_t = 0;
+  int align = kTaskAlign;
+  if (const char* e = std::getenv("HX_ALIGN")) align = std::atoi(e);
   std::future<SchedHost> sched_a;
   if (monotone)  // else the device check below reports it
-    sched_a = std::async(std::launch::async, [&ph, m, sched_warps, exact, stagger_a, stagger_lmin] {
+    sched_a = std::async(std::launch::async, [&ph, m, sched_warps, exact, stagger_a, stagger_lmin, align] {
       double rc, tc;
       sched_costs(false, rc, tc);
-      return build_schedule(ph.data(), static_cast<int>(m), sched_warps, 0.0, rc, tc, exact, stagger_a, stagger_lmin);
+      return build_schedule(ph.data(), static_cast<int>(m), sched_warps, 0.0, rc, tc, exact, stagger_a, stagger_lmin,
+                            align);
     });
   cudaStream_t s = c->stream;
   const int nblk = 4 * c->sm_count;
@@ -4576,10 +4579,11 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
     double lead = kLead;
     if (const char* e = std::getenv("HX_LEAD")) lead = std::atof(e);
     // A^T's schedule is built on a host thread while A's uploads
-    auto sched_t = std::async(std::launch::async, [&pt, n, sched_warps, lead, exact, stagger_t, stagger_lmin] {
+    auto sched_t = std::async(std::launch::async, [&pt, n, sched_warps, lead, exact, stagger_t, stagger_lmin, align] {
       double rc, tc;
       sched_costs(true, rc, tc);
-      return build_schedule(pt.data(), static_cast<int>(n), sched_warps, lead, rc, tc, exact, stagger_t, stagger_lmin);
+      return build_schedule(pt.data(), static_cast<int>(n), sched_warps, lead, rc, tc, exact, stagger_t, stagger_lmin,
+                            align);
     });
     int rc = upload_built_sched(c, c->sa, sched_a.get(), static_cast<int>(m), static_cast<int>(n), c->a_ptr,
                                 c->a_idx, c->a_val, 0);

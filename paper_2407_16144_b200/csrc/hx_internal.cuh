@@ -46,6 +46,7 @@ constexpr double kTaskCost = 64.0;         // fixed latency cost of one warp tas
 constexpr int kStaggerA = 15;
 constexpr int kStaggerT = 1;
 constexpr int kStaggerLmin = 4;
+constexpr int kTaskAlign = 32;  // staggered copy: task starts on multiples of 32 slots (HX_ALIGN)
 constexpr int64_t kStaggerMaxNnz = int64_t{1} << 29;  // larger matrices keep the plain layout
 // build_schedule packs the rows of a matrix with >= kPackMinRows rows in
 // kPackSegments fixed segments on host threads
@@ -227,6 +228,7 @@ struct SchedHost {
 // the product buffer without bank conflicts.  Pads trail the previous row
 // (they add +0.0 to its sum: the same bits, since no row sum is -0.0).
 SchedHost build_schedule(const int* ptr_host, int rows, int warps, double lead = 0.0, double row_cost = kRowCost,
-                         double task_cost = kTaskCost, bool exact = false, int stagger = 0, int stagger_lmin = 4);
+                         double task_cost = kTaskCost, bool exact = false, int stagger = 0, int stagger_lmin = 4,
+                         int align = 0);
 
 }  // namespace hx

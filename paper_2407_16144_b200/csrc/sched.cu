@@ -35,6 +35,7 @@ struct Packed {
 struct PackArgs {
   const int* ptr_in;
   int stagger, stagger_lmin;
+  int align;  // staggered copy: every task starts at a multiple of `align` slots (0: anywhere)
   int64_t task_nnz;
   bool exact;
   double row_cost, task_cost, run_budget;
@@ -54,9 +55,19 @@ void pack_rows(const PackArgs& a, int ra, int rb, Packed& o) {
     o.meta.push_back(meta);
     o.cost.push_back(c + a.task_cost);
   };
+  // a task's first slot on a multiple of a.align (its idx / val streams then
+  // touch the fewest 128-byte lines); the gap trails the previous task's last
+  // row, whose sum the kernels clamp to its task's end
+  auto align_at = [&](int row) {
+    if (stagger && a.align) {
+      const int64_t rem = (ptr_in[row] + off) % a.align;
+      if (rem) off += a.align - rem;
+    }
+  };
   int r = ra;
   while (r < rb) {
     const int64_t len = ptr_in[r + 1] - ptr_in[r];
+    align_at(r);
     place(r);
     if (len > kStreamRowMax) {
       const int np = static_cast<int>((len + kTaskNnz - 1) / kTaskNnz);
@@ -119,12 +130,14 @@ void pack_rows(const PackArgs& a, int ra, int rb, Packed& o) {
     push(r0, r, kTaskStream, p0, stagger ? pstart(r) : ptr_in[r], int4{0, 0, 0, 0},
          static_cast<double>(stagger ? used : nz) + a.row_cost * (r - r0));
   }
+  // the segment's pads a multiple of a.align, so later segments keep theirs
+  if (stagger && a.align && off % a.align) off += a.align - off % a.align;
 }
 
 }  // namespace
 
 SchedHost build_schedule(const int* ptr_in, int rows, int warps, double lead, double row_cost, double task_cost,
-                         bool exact, int stagger, int stagger_lmin) {
+                         bool exact, int stagger, int stagger_lmin, int align) {
   SchedHost s;
   // Bank-staggered layout: positions in a padded copy of the matrix; pads only
   // ever go in front of a non-first row of a stream task, and every task
@@ -132,8 +145,10 @@ SchedHost build_schedule(const int* ptr_in, int rows, int warps, double lead, do
   // never staggered).
   stagger = ptr_in[0] == 0 ? std::max(0, std::min(stagger, 15)) : 0;
   // padded positions stay int32: at most `stagger` pads per row
-  if (static_cast<int64_t>(ptr_in[rows]) + static_cast<int64_t>(stagger) * rows + kMatrixPad >= (int64_t{1} << 31) - 1)
-    stagger = 0;
+  align = stagger ? std::max(0, std::min(align, 64)) : 0;
+  if (static_cast<int64_t>(ptr_in[rows]) + static_cast<int64_t>(stagger + align) * rows + kMatrixPad >=
+      (int64_t{1} << 31) - 1)
+    stagger = align = 0;
   std::vector<int> padded;
   if (stagger) padded.assign(static_cast<std::size_t>(rows) + 1, 0);
   const int64_t nnz = ptr_in[rows] - ptr_in[0];  // ptr may point into a larger matrix (a rank's block)
@@ -142,7 +157,7 @@ SchedHost build_schedule(const int* ptr_in, int rows, int warps, double lead, do
   if (const char* e = std::getenv("HX_TASK_NNZ")) task_nnz = std::max(8, std::min<int>(kTaskNnz, std::atoi(e)));
   // a run of pieces is dealt to one warp as a unit: at most 1/kRunFrac of the
   // mean warp cost, so the dealing stays balanced
-  const PackArgs pa{ptr_in, stagger, stagger_lmin, task_nnz, exact, row_cost, task_cost,
+  const PackArgs pa{ptr_in, stagger, stagger_lmin, align, task_nnz, exact, row_cost, task_cost,
                     std::max(1.0, total / warps / kRunFrac), stagger ? padded.data() : nullptr};
   // Packing runs on kPackSegments host threads for large matrices: segment k
   // starts at the first row at or past nonzero k * nnz / K (a fixed split, so
