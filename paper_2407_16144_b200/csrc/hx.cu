@@ -4675,10 +4675,11 @@ int hx_upload_csr(hx_ctx* c, int64_t m, int64_t n, const int64_t* row_ptr, const
       // the blocks' schedules are built concurrently on host threads
       std::vector<std::future<SchedHost>> sb(static_cast<size_t>(K));
       for (int k = 0; k < K; ++k)
-        sb[k] = std::async(std::launch::async, [pk = &ph_k[k], m, sched_warps] {
+        sb[k] = std::async(std::launch::async, [pk = &ph_k[k], m, sched_warps, stagger_a, stagger_lmin, align] {
           double rc, tc;
           sched_costs(false, rc, tc);
-          return build_schedule(pk->data(), static_cast<int>(m), sched_warps, 0.0, rc, tc);
+          return build_schedule(pk->data(), static_cast<int>(m), sched_warps, 0.0, rc, tc, false, stagger_a,
+                                stagger_lmin, align);
         });
       for (int k = 0; k < K; ++k) {
         const int rc = upload_built_sched(c, c->sb[k], sb[k].get(), static_cast<int>(m), static_cast<int>(n),
@@ -4792,6 +4793,11 @@ int hx_precondition(hx_ctx* c, int32_t ruiz_iters, double pc_alpha, double* row_
     if (c->sa.pval) scale_csr_kernel<<<nb, 256, 0, s>>>(m, c->sa.pptr, c->sa.pidx, c->sa.pval, dr, dc, 0);
     if (c->st.pval) scale_csr_kernel<<<nb, 256, 0, s>>>(n, c->st.pptr, c->st.pidx, c->st.pval, dr, dc, 1);
     c->launches += (c->sa.pval ? 1 : 0) + (c->st.pval ? 1 : 0);
+    for (int k = 0; k < c->colblock; ++k)  // the column blocks' staggered copies
+      if (c->sb[k].pval) {
+        scale_csr_kernel<<<nb, 256, 0, s>>>(m, c->sb[k].pptr, c->sb[k].pidx, c->sb[k].pval, dr, dc, 0);
+        c->launches += 1;
+      }
     scale_vec_kernel<<<nb, 256, 0, s>>>(m, c->b, dr);
     scale_vec_kernel<<<nb, 256, 0, s>>>(n, c->c, dc);
     if (c->ub) div_vec_kernel<<<nb, 256, 0, s>>>(n, c->ub, dc);  // x = C x': x' <= u / C

@@ -82,8 +82,12 @@ void pack_rows(const PackArgs& a, int ra, int rb, Packed& o) {
         const int q0 = static_cast<int>(static_cast<int64_t>(np) * k / nr);
         const int q1 = static_cast<int>(static_cast<int64_t>(np) * (k + 1) / nr);
         for (int q = q0; q < q1; ++q) {
-          const int64_t p0 = base + len * q / np;
-          const int64_t p1 = base + len * (q + 1) / np;
+          // equal pieces; in an aligned staggered copy, pieces of kTaskNnz
+          // slots from the aligned row start (the last one shorter), so every
+          // piece's streams start on a line
+          const bool al = stagger && a.align;
+          const int64_t p0 = base + (al ? std::min<int64_t>(len, int64_t{kTaskNnz} * q) : len * q / np);
+          const int64_t p1 = base + (al ? std::min<int64_t>(len, int64_t{kTaskNnz} * (q + 1)) : len * (q + 1) / np);
           push(r, r + 1, q + 1 == q1 ? kTaskPiece : kTaskPieceRun, p0, p1,
                int4{o.n_slots + k, nr, nr > 1 ? o.n_long : -1, k},
                static_cast<double>(p1 - p0) * (a.exact ? 2.0 : 1.0) + (q + 1 == np ? a.row_cost : 0.0));
