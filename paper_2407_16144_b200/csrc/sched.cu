@@ -106,7 +106,13 @@ void pack_rows(const PackArgs& a, int ra, int rb, Packed& o) {
     int64_t nz = 0;
     int starts[4][16];  // per half-warp group: how many rows start on each bank pair
     if (stagger) std::fill(&starts[0][0], &starts[0][0] + 64, 0);
-    while (r < rb && r - r0 < kStreamRowsMax) {
+    // aligned copy: a task that fills up by rows ends on a multiple of 32
+    // rows, so a run of short rows (slack columns, bound rows) is cut into
+    // tasks whose epilogue vectors start on a 256-byte boundary
+    const int row_end = stagger && a.align && (r0 + kStreamRowsMax) / 32 * 32 > r0
+                            ? (r0 + kStreamRowsMax) / 32 * 32
+                            : r0 + kStreamRowsMax;
+    while (r < rb && r < row_end) {
       const int64_t l = ptr_in[r + 1] - ptr_in[r];
       if (l > kStreamRowMax) break;
       int pad = 0;

@@ -459,14 +459,19 @@ def test_trace_ring_minimum_capacity_and_disabled(gpu_required, monkeypatch):
 @pytest.mark.parametrize("name", ["cfg1_small", "zipf_small", "transport_small", "ragged"])
 def test_bank_staggered_layout_bit_identical(gpu_required, name, monkeypatch):
     """Bank-staggered stream tasks (build_schedule stagger, HX_STAGGER): the
-    pad slots only append +0.0 to a row's sum and no row sum is -0.0, so both
-    SpMVs are bit-identical to the unpadded layout -- with the most padding
-    allowed (15 slots before every row) and with the default.  The solve's
-    norms and KKT sums follow the schedule's row -> lane map, which the pads
-    move, so iterates agree to rounding (1e-12), with identical statuses,
-    iteration counts and restarts -- on a preconditioned instance too (the
-    padded copies are rescaled with the CSR)."""
+    pad slots only append +0.0 to a row's sum and no row sum is -0.0, so on a
+    matrix of stream rows only (<= 64 nonzeros) both SpMVs are bit-identical
+    to the unpadded layout -- with the most padding allowed (15 slots before
+    every row) and with the default.  Rows beyond 64 nonzeros are cut into
+    pieces of 256 slots from their aligned start in the staggered copy
+    (equal pieces in the plain one), which moves the fast order's partial sums:
+    those SpMVs agree to 1e-13.  The solve's norms and KKT sums follow the
+    schedule's row -> lane map, which the pads move, so iterates agree to
+    rounding, with identical statuses, iteration counts and restarts -- on a
+    preconditioned instance too (the padded copies are rescaled with the
+    CSR)."""
     args = _ragged_lp() if name == "ragged" else csr_args(std(name)[1])
+    long_rows = max(np.diff(np.asarray(args[2])).max(), np.bincount(np.asarray(args[3]), minlength=args[1]).max()) > 64
     rng = np.random.default_rng(5)
     x, y = rng.normal(size=args[1]), rng.normal(size=args[0])
     runs = {}
@@ -488,7 +493,11 @@ def test_bank_staggered_layout_bit_identical(gpu_required, name, monkeypatch):
     base_p, base = runs["0,0,4"]
     for layout in ("15,1,4", "15,15,1"):
         p, o = runs[layout]
-        assert np.array_equal(p[0], base_p[0]) and np.array_equal(p[1], base_p[1]), layout
+        if long_rows:
+            assert rel_inf(p[0], base_p[0]) <= 1e-13 and rel_inf(p[1], base_p[1]) <= 1e-13, layout
+        else:
+            assert np.array_equal(p[0], base_p[0]) and np.array_equal(p[1], base_p[1]), layout
         for a, b in zip(o, base):
-            assert rel_inf(a[0], b[0]) <= 1e-12 and rel_inf(a[1], b[1]) <= 1e-12, layout
+            tol = 1e-11 if long_rows else 1e-12
+            assert rel_inf(a[0], b[0]) <= tol and rel_inf(a[1], b[1]) <= tol, layout
             assert a[2:] == b[2:], layout
